@@ -1,0 +1,175 @@
+/* q8p -- B200-native (sm_100a) QuIP# quantized-linear inference.
+ *
+ * C ABI: the drop-in boundary for the reference `latq` library's inference
+ * path.  Plain pointers and sizes only; no exceptions cross this boundary
+ * (every entry point returns a q8p_status; q8p_last_error() holds the
+ * message of the calling thread's last failure).
+ *
+ * Reference interfaces each entry point replaces (paths under
+ * /root/reference/proj):
+ *   q8p_layer_from_qshp   latq::deserialize  core/include/latq/pipeline.hpp:84
+ *                         (core/src/pipeline.cpp:323-383) + device upload
+ *   q8p_layer_create      latq::QuantizedLinear  pipeline.hpp:38-49 (fields
+ *                         given directly instead of as a parsed artifact)
+ *   q8p_forward           latq::infer  pipeline.hpp:73-74
+ *                         (pipeline.cpp:151-197), batched, device buffers, fp32
+ *   q8p_infer_host        latq::infer with host f64 vectors (the exact
+ *                         reference calling convention; CLI `latq infer`,
+ *                         tools/latq_cli.cpp:192-215, loops it per row)
+ *   q8p_decode_stage      Codebook::decode / e8p_decode  core/include/latq/
+ *                         codebook.hpp:31, e8p.hpp:35 over a whole stage
+ *   q8p_rht               SideTransform::apply / apply_transpose
+ *                         core/include/latq/transforms.hpp:30-33 (rht kind)
+ *   q8p_plan_hadamard     latq::plan_hadamard  core/include/latq/hadamard.hpp:42
+ *                         (registry extended with order 172)
+ *   q8p_forward_sharded   (new) row-sharded forward with an NCCL all-gather
+ * Error mapping: SizeError -> Q8P_ERR_SIZE, ValidationError ->
+ * Q8P_ERR_VALIDATION, FormatError -> Q8P_ERR_FORMAT, BadMagicError ->
+ * Q8P_ERR_BAD_MAGIC, UnsupportedVersionError -> Q8P_ERR_UNSUPPORTED_VERSION,
+ * TruncatedArtifactError -> Q8P_ERR_TRUNCATED (core/include/latq/errors.hpp).
+ */
+#ifndef Q8P_H_
+#define Q8P_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  Q8P_OK = 0,
+  Q8P_ERR_SIZE = 1,                /* latq::SizeError (length mismatch, unplannable dim) */
+  Q8P_ERR_VALIDATION = 2,          /* latq::ValidationError (unknown codebook id, bad args) */
+  Q8P_ERR_FORMAT = 3,              /* latq::FormatError */
+  Q8P_ERR_BAD_MAGIC = 4,           /* latq::BadMagicError */
+  Q8P_ERR_UNSUPPORTED_VERSION = 5, /* latq::UnsupportedVersionError */
+  Q8P_ERR_TRUNCATED = 6,           /* latq::TruncatedArtifactError */
+  Q8P_ERR_UNSUPPORTED = 7,         /* valid artifact, not on this path (e.g. rfft transform) */
+  Q8P_ERR_CUDA = 8,                /* CUDA runtime failure / no sm_100 device */
+  Q8P_ERR_NCCL = 9,
+  Q8P_ERR_INTERNAL = 10
+} q8p_status;
+
+typedef enum {
+  Q8P_CB_E8P_2BIT = 0, /* "e8p-2bit": 16-bit E8P codewords (core/src/e8p.cpp) */
+  Q8P_CB_E8_1BIT = 1   /* "e8-1bit": 256-entry E8 ball table (core/src/codebook.cpp:188-243) */
+} q8p_codebook;
+
+typedef struct {
+  q8p_codebook codebook;
+  float scale;        /* StageInfo::scale, f32-frozen (pipeline.hpp:27-32) */
+  const void* codes;  /* host, m * (n / 8) codewords, row-major [r * (n/8) + k] */
+  int code_bytes;     /* bytes per codeword in `codes`: 2 (uint16) or 1 (uint8, e8-1bit only) */
+} q8p_stage_desc;
+
+typedef struct {
+  uint32_t m, n;                 /* W is m x n; x has n entries, y has m */
+  int transform;                 /* 0 = rht (TransformKind::rht); rfft is not supported */
+  int num_stages;                /* 1 (2-bit) or 2 (3-/4-bit RVQ) */
+  const q8p_stage_desc* stages;
+  const uint8_t* signs_u;        /* left_signs, ceil(m/8) bytes, LSB-first, bit set = -1 */
+  const uint8_t* signs_v;        /* right_signs, ceil(n/8) bytes */
+} q8p_layer_desc;
+
+typedef struct {
+  uint32_t m, n;          /* full layer shape */
+  uint32_t row_begin;     /* this handle's rows [row_begin, row_end) (sharded layers) */
+  uint32_t row_end;
+  int num_stages;
+  int device;
+  size_t device_bytes;    /* HBM held by the layer */
+  size_t code_bytes;      /* algorithmic code bytes (m_local * n / 8 * sum code bytes) */
+} q8p_layer_info;
+
+typedef struct q8p_layer q8p_layer;
+
+/* Library / device queries. */
+const char* q8p_version(void);
+const char* q8p_status_string(q8p_status s);
+const char* q8p_last_error(void);
+/* Number of this library's kernels launched since load (process-wide counter). */
+uint64_t q8p_kernel_launches(void);
+
+/* Hadamard planning (registry {1, 4, 12, 20, 28, 172}). */
+q8p_status q8p_plan_hadamard(size_t n, size_t* p, size_t* q);
+
+/* Layer lifetime.  create/from_qshp copy host buffers to `device` memory;
+ * the caller keeps ownership of its buffers.  The layer is immutable after
+ * creation and may be used concurrently from different streams provided
+ * each call gets its own workspace. */
+q8p_status q8p_layer_create(const q8p_layer_desc* desc, int device, q8p_layer** out);
+q8p_status q8p_layer_from_qshp(const uint8_t* bytes, size_t len, int device, q8p_layer** out);
+/* Row shard [row_begin, row_end) of a full artifact for row-sharded
+ * tensor parallelism; S_U / S_V stay full. */
+q8p_status q8p_layer_from_qshp_rows(const uint8_t* bytes, size_t len, uint32_t row_begin,
+                                    uint32_t row_end, int device, q8p_layer** out);
+void q8p_layer_destroy(q8p_layer* layer);
+q8p_status q8p_layer_get_info(const q8p_layer* layer, q8p_layer_info* info);
+
+/* Device workspace needed by q8p_forward for `batch` vectors (bytes). */
+size_t q8p_workspace_bytes(const q8p_layer* layer, int batch);
+
+/* y = W_tilde x for `batch` vectors: x device fp32 [batch][n], y device fp32
+ * [batch][m] (m = full m).  Stream-ordered on `stream` (a cudaStream_t, or
+ * NULL for the legacy default stream); never allocates. */
+q8p_status q8p_forward(const q8p_layer* layer, const float* x, float* y, int batch,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
+/* Row-sharded forward: `layer` holds rows [row_begin, row_end) of the full
+ * layer on this rank.  Each rank computes its z slice, the slices are
+ * all-gathered over `nccl_comm` (an ncclComm_t), then every rank applies
+ * the output transform to the full z.  Shards must be equal-sized and
+ * ordered by rank. */
+q8p_status q8p_forward_sharded(const q8p_layer* layer, const float* x, float* y, int batch,
+                               void* workspace, size_t workspace_bytes, void* nccl_comm,
+                               void* stream);
+
+/* latq::infer drop-in: host f64 x [batch][n] -> host f64 y [batch][m].
+ * Synchronous; stages through an internal pinned buffer and workspace. */
+q8p_status q8p_infer_host(q8p_layer* layer, const double* x, double* y, int batch);
+
+/* Unscaled incoherent-domain decode of one stage into device fp32
+ * w_hat[m_local][n] (decoded values are exact quarter-integers). */
+q8p_status q8p_decode_stage(const q8p_layer* layer, int stage, float* w_hat, void* stream);
+
+/* Randomized Hadamard transform on device fp32 vectors:
+ *   transpose == 0:  y = H (S o x)          (SideTransform::apply)
+ *   transpose != 0:  y = S o (H^T x)        (SideTransform::apply_transpose)
+ * signs: device pointer to ceil(n/8) sign bytes. x and y may alias. */
+q8p_status q8p_rht(size_t n, const uint8_t* signs, const float* x, float* y, int batch,
+                   int transpose, void* stream);
+
+/* Host-side helpers (no GPU needed): artifact inspection and round trip
+ * (latq::deserialize / serialize, pipeline.cpp:269-383), codebook tables
+ * (e8p.hpp:22-35, codebook.cpp:188-243) and Hadamard bases (hadamard.hpp:35). */
+typedef struct {
+  uint32_t m, n;
+  int transform;          /* 0 = rht, 1 = rfft */
+  int num_stages;
+  q8p_codebook codebook[8];
+  float scale[8];
+  size_t serialized_size; /* == len for a valid artifact */
+} q8p_artifact_info;
+q8p_status q8p_qshp_inspect(const uint8_t* bytes, size_t len, q8p_artifact_info* info);
+/* deserialize(bytes) then serialize into out[cap]; *out_len = bytes written. */
+q8p_status q8p_qshp_reserialize(const uint8_t* bytes, size_t len, uint8_t* out, size_t cap,
+                                size_t* out_len);
+q8p_status q8p_e8p_decode_host(uint16_t word, float out[8]);
+/* doubled coordinates [256][8] of a codebook table (E8P: magnitudes 1/3/5
+ * with odd_parity[256] in parity_out; e8-1bit: signed, parity_out unused). */
+q8p_status q8p_codebook_table(q8p_codebook cb, int8_t* doubled, uint8_t* parity_out);
+q8p_status q8p_hadamard_base(size_t q, int8_t* out);
+
+/* NCCL plumbing for q8p_forward_sharded (wraps ncclGetUniqueId /
+ * ncclCommInitRank so callers need no NCCL headers). */
+q8p_status q8p_nccl_unique_id(uint8_t out[128]);
+q8p_status q8p_nccl_comm_init(const uint8_t id[128], int world, int rank, int device, void** comm);
+q8p_status q8p_nccl_comm_destroy(void* comm);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* Q8P_H_ */

@@ -1,0 +1,340 @@
+"""q8p: B200-native (sm_100a) QuIP# quantized-linear inference.
+
+Python mirror of the reference `latq` inference-path interface
+(/root/reference/proj/core/include/latq/pipeline.hpp: QuantizedLinear,
+infer, serialize/deserialize; hadamard.hpp: plan_hadamard), bound over the
+C ABI in include/q8p.h (libq8p.so, built in-tree by __graft_entry__.build()).
+
+There is no CPU fallback: every compute call runs the sm_100a kernels and
+fails loudly when the extension or a B200 is missing.  torch is used only
+for device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "Error", "SizeError", "ValidationError", "FormatError", "BadMagicError",
+    "UnsupportedVersionError", "TruncatedArtifactError", "UnsupportedError", "DeviceError",
+    "lib", "plan_hadamard", "hadamard_base", "codebook_table", "e8p_decode_host",
+    "inspect_artifact", "reserialize", "Layer", "rht", "kernel_launches",
+    "CB_E8P_2BIT", "CB_E8_1BIT",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libq8p.so")
+
+CB_E8P_2BIT = 0
+CB_E8_1BIT = 1
+
+
+# --- error taxonomy (core/include/latq/errors.hpp:9-53) ---------------------
+class Error(RuntimeError):
+    pass
+
+
+class SizeError(Error):
+    pass
+
+
+class ValidationError(Error):
+    pass
+
+
+class FormatError(Error):
+    pass
+
+
+class BadMagicError(FormatError):
+    pass
+
+
+class UnsupportedVersionError(FormatError):
+    pass
+
+
+class TruncatedArtifactError(FormatError):
+    pass
+
+
+class UnsupportedError(Error):
+    pass
+
+
+class DeviceError(Error):
+    pass
+
+
+_STATUS = {
+    1: SizeError, 2: ValidationError, 3: FormatError, 4: BadMagicError,
+    5: UnsupportedVersionError, 6: TruncatedArtifactError, 7: UnsupportedError,
+    8: DeviceError, 9: DeviceError, 10: Error,
+}
+
+
+class LayerDesc(ctypes.Structure):
+    pass
+
+
+class StageDesc(ctypes.Structure):
+    _fields_ = [("codebook", ctypes.c_int), ("scale", ctypes.c_float),
+                ("codes", ctypes.c_void_p), ("code_bytes", ctypes.c_int)]
+
+
+LayerDesc._fields_ = [("m", ctypes.c_uint32), ("n", ctypes.c_uint32), ("transform", ctypes.c_int),
+                      ("num_stages", ctypes.c_int), ("stages", ctypes.POINTER(StageDesc)),
+                      ("signs_u", ctypes.c_void_p), ("signs_v", ctypes.c_void_p)]
+
+
+class LayerInfo(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_uint32), ("n", ctypes.c_uint32), ("row_begin", ctypes.c_uint32),
+                ("row_end", ctypes.c_uint32), ("num_stages", ctypes.c_int), ("device", ctypes.c_int),
+                ("device_bytes", ctypes.c_size_t), ("code_bytes", ctypes.c_size_t)]
+
+
+class ArtifactInfo(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_uint32), ("n", ctypes.c_uint32), ("transform", ctypes.c_int),
+                ("num_stages", ctypes.c_int), ("codebook", ctypes.c_int * 8),
+                ("scale", ctypes.c_float * 8), ("serialized_size", ctypes.c_size_t)]
+
+
+# Every symbol include/q8p.h declares, with its ctypes signature.
+_SIGNATURES = {
+    "q8p_version": (ctypes.c_char_p, []),
+    "q8p_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "q8p_last_error": (ctypes.c_char_p, []),
+    "q8p_kernel_launches": (ctypes.c_uint64, []),
+    "q8p_plan_hadamard": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]),
+    "q8p_layer_create": (ctypes.c_int, [ctypes.POINTER(LayerDesc), ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "q8p_layer_from_qshp": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "q8p_layer_from_qshp_rows": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "q8p_layer_destroy": (None, [ctypes.c_void_p]),
+    "q8p_layer_get_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(LayerInfo)]),
+    "q8p_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int]),
+    "q8p_forward": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "q8p_forward_sharded": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]),
+    "q8p_infer_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
+    "q8p_decode_stage": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
+    "q8p_rht": (ctypes.c_int, [ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
+    "q8p_qshp_inspect": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ArtifactInfo)]),
+    "q8p_qshp_reserialize": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
+    "q8p_e8p_decode_host": (ctypes.c_int, [ctypes.c_uint16, ctypes.c_void_p]),
+    "q8p_codebook_table": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
+    "q8p_hadamard_base": (ctypes.c_int, [ctypes.c_size_t, ctypes.c_void_p]),
+    "q8p_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
+    "q8p_nccl_comm_init": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "q8p_nccl_comm_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+}
+
+_lib: Optional[ctypes.CDLL] = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libq8p.so (built in-tree).  Raises if it is missing: no fallback."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"q8p extension not built: {LIB_PATH} missing "
+                              "(run __graft_entry__.build())")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        msg = lib().q8p_last_error().decode(errors="replace")
+        raise _STATUS.get(status, Error)(msg)
+
+
+def kernel_launches() -> int:
+    return int(lib().q8p_kernel_launches())
+
+
+# --- host-side helpers (no GPU) ----------------------------------------------
+def plan_hadamard(n: int) -> tuple[int, int]:
+    """latq::plan_hadamard (hadamard.cpp:156-168), registry + 172 -> (p, q)."""
+    p, q = ctypes.c_size_t(), ctypes.c_size_t()
+    _check(lib().q8p_plan_hadamard(n, ctypes.byref(p), ctypes.byref(q)))
+    return p.value, q.value
+
+
+def hadamard_base(q: int) -> np.ndarray:
+    out = np.zeros(q * q, dtype=np.int8)
+    _check(lib().q8p_hadamard_base(q, out.ctypes.data))
+    return out.reshape(q, q)
+
+
+def codebook_table(cb: int) -> tuple[np.ndarray, np.ndarray]:
+    d = np.zeros((256, 8), dtype=np.int8)
+    p = np.zeros(256, dtype=np.uint8)
+    _check(lib().q8p_codebook_table(cb, d.ctypes.data, p.ctypes.data))
+    return d, p
+
+
+def e8p_decode_host(word: int) -> np.ndarray:
+    out = np.zeros(8, dtype=np.float32)
+    _check(lib().q8p_e8p_decode_host(word, out.ctypes.data))
+    return out
+
+
+def inspect_artifact(data: bytes) -> dict:
+    info = ArtifactInfo()
+    _check(lib().q8p_qshp_inspect(data, len(data), ctypes.byref(info)))
+    return {"m": info.m, "n": info.n, "transform": info.transform, "num_stages": info.num_stages,
+            "codebook": list(info.codebook[: info.num_stages]), "scale": list(info.scale[: info.num_stages]),
+            "serialized_size": info.serialized_size}
+
+
+def reserialize(data: bytes) -> bytes:
+    """serialize(deserialize(data)) through the product's QSHP reader/writer."""
+    n = ctypes.c_size_t()
+    buf = ctypes.create_string_buffer(len(data) + 64)
+    _check(lib().q8p_qshp_reserialize(data, len(data), buf, len(buf), ctypes.byref(n)))
+    return buf.raw[: n.value]
+
+
+# --- device API ---------------------------------------------------------------
+def _torch():
+    import torch  # plumbing only: device memory and streams
+    return torch
+
+
+def _stream_ptr(stream) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+class Layer:
+    """A QuantizedLinear resident on one B200 (or a row shard of one)."""
+
+    def __init__(self, handle: int):
+        self._h = ctypes.c_void_p(handle)
+        self._ws = None
+
+    @classmethod
+    def from_qshp(cls, data: bytes, device: int = 0, rows: Optional[tuple[int, int]] = None) -> "Layer":
+        h = ctypes.c_void_p()
+        if rows is None:
+            _check(lib().q8p_layer_from_qshp(data, len(data), device, ctypes.byref(h)))
+        else:
+            _check(lib().q8p_layer_from_qshp_rows(data, len(data), rows[0], rows[1], device, ctypes.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def create(cls, m: int, n: int, stages: Sequence[tuple[int, float, np.ndarray]],
+               signs_u: np.ndarray, signs_v: np.ndarray, device: int = 0) -> "Layer":
+        """q8p_layer_create from raw fields: stages = [(codebook, scale, codes)]."""
+        st = (StageDesc * len(stages))()
+        keep = []
+        for i, (cb, scale, codes) in enumerate(stages):
+            codes = np.ascontiguousarray(codes)
+            keep.append(codes)
+            st[i].codebook = cb
+            st[i].scale = scale
+            st[i].codes = codes.ctypes.data
+            st[i].code_bytes = codes.dtype.itemsize
+        su = np.ascontiguousarray(signs_u, dtype=np.uint8)
+        sv = np.ascontiguousarray(signs_v, dtype=np.uint8)
+        d = LayerDesc(m, n, 0, len(stages), st, su.ctypes.data, sv.ctypes.data)
+        h = ctypes.c_void_p()
+        _check(lib().q8p_layer_create(ctypes.byref(d), device, ctypes.byref(h)))
+        return cls(h.value)
+
+    def close(self) -> None:
+        if self._h and self._h.value:
+            lib().q8p_layer_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def info(self) -> dict:
+        i = LayerInfo()
+        _check(lib().q8p_layer_get_info(self._h, ctypes.byref(i)))
+        return {f: getattr(i, f) for f, _ in LayerInfo._fields_}
+
+    def workspace_bytes(self, batch: int) -> int:
+        return int(lib().q8p_workspace_bytes(self._h, batch))
+
+    def workspace(self, batch: int):
+        torch = _torch()
+        need = self.workspace_bytes(batch)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=f"cuda:{self.info['device']}")
+        return self._ws
+
+    def forward(self, x, out=None, stream=None, workspace=None):
+        """y = W_tilde x for a [batch, n] fp32 CUDA tensor -> [batch, m]."""
+        torch = _torch()
+        info = self.info
+        if x.dim() == 1:
+            return self.forward(x.view(1, -1), None if out is None else out.view(1, -1), stream, workspace).view(-1)
+        if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous():
+            raise ValidationError("x must be a contiguous float32 CUDA tensor")
+        if x.shape[1] != info["n"]:
+            raise SizeError("infer: input length != n")
+        batch = x.shape[0]
+        if out is None:
+            out = torch.empty(batch, info["m"], dtype=torch.float32, device=x.device)
+        ws = workspace if workspace is not None else self.workspace(batch)
+        _check(lib().q8p_forward(self._h, x.data_ptr(), out.data_ptr(), batch, ws.data_ptr(),
+                                 ws.numel(), _stream_ptr(stream)))
+        return out
+
+    def forward_sharded(self, x, comm, out=None, stream=None, workspace=None):
+        torch = _torch()
+        info = self.info
+        batch = x.shape[0]
+        if out is None:
+            out = torch.empty(batch, info["m"], dtype=torch.float32, device=x.device)
+        ws = workspace if workspace is not None else self.workspace(batch)
+        _check(lib().q8p_forward_sharded(self._h, x.data_ptr(), out.data_ptr(), batch, ws.data_ptr(),
+                                         ws.numel(), comm, _stream_ptr(stream)))
+        return out
+
+    def infer_host(self, x: np.ndarray) -> np.ndarray:
+        """latq::infer calling convention: host f64 [batch, n] -> host f64 [batch, m]."""
+        info = self.info
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        squeeze = x.ndim == 1
+        x2 = x.reshape(-1, info["n"]) if x.size % max(info["n"], 1) == 0 else None
+        if x2 is None or (squeeze and x.shape[0] != info["n"]):
+            raise SizeError("infer: input length != n")
+        y = np.zeros((x2.shape[0], info["m"]), dtype=np.float64)
+        _check(lib().q8p_infer_host(self._h, x2.ctypes.data, y.ctypes.data, x2.shape[0]))
+        return y[0] if squeeze else y
+
+    def decode_stage(self, stage: int, stream=None):
+        torch = _torch()
+        info = self.info
+        w = torch.empty(info["row_end"] - info["row_begin"], info["n"], dtype=torch.float32,
+                        device=f"cuda:{info['device']}")
+        _check(lib().q8p_decode_stage(self._h, stage, w.data_ptr(), _stream_ptr(stream)))
+        return w
+
+
+def rht(x, signs, transpose: bool = False, out=None, stream=None):
+    """SideTransform apply / apply_transpose on [batch, n] fp32 CUDA tensors;
+    signs: uint8 CUDA tensor of ceil(n/8) bytes."""
+    torch = _torch()
+    if x.dim() == 1:
+        x = x.view(1, -1)
+    if out is None:
+        out = torch.empty_like(x)
+    _check(lib().q8p_rht(x.shape[1], signs.data_ptr(), x.data_ptr(), out.data_ptr(), x.shape[0],
+                         1 if transpose else 0, _stream_ptr(stream)))
+    return out

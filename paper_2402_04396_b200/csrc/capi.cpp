@@ -1,0 +1,519 @@
+// The C ABI (include/q8p.h): layer upload, forward orchestration
+// (K1 -> K2 -> [all-gather] -> K3), host-buffer infer, and status mapping.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "device.hpp"
+
+namespace q8p::detail {
+
+std::atomic<std::uint64_t> g_launches{0};
+namespace {
+thread_local std::string t_last_error;
+}
+
+void set_last_error(const std::string& msg) { t_last_error = msg; }
+
+void throw_cuda(cudaError_t e, const char* what) {
+  throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+q8p_status status_of_current_exception() {
+  try {
+    throw;
+  } catch (const SizeError& e) {
+    set_last_error(e.what());
+    return Q8P_ERR_SIZE;
+  } catch (const ValidationError& e) {
+    set_last_error(e.what());
+    return Q8P_ERR_VALIDATION;
+  } catch (const BadMagicError& e) {
+    set_last_error(e.what());
+    return Q8P_ERR_BAD_MAGIC;
+  } catch (const UnsupportedVersionError& e) {
+    set_last_error(e.what());
+    return Q8P_ERR_UNSUPPORTED_VERSION;
+  } catch (const TruncatedArtifactError& e) {
+    set_last_error(e.what());
+    return Q8P_ERR_TRUNCATED;
+  } catch (const FormatError& e) {
+    set_last_error(e.what());
+    return Q8P_ERR_FORMAT;
+  } catch (const UnsupportedError& e) {
+    set_last_error(e.what());
+    return Q8P_ERR_UNSUPPORTED;
+  } catch (const DeviceError& e) {
+    set_last_error(e.what());
+    return Q8P_ERR_CUDA;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return Q8P_ERR_INTERNAL;
+  } catch (...) {
+    set_last_error("unknown exception");
+    return Q8P_ERR_INTERNAL;
+  }
+}
+
+namespace {
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cuda_check(cudaGetDevice(&prev), "cudaGetDevice");
+    if (prev != dev) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+void require_sm100(int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    throw DeviceError("no CUDA device available (q8p requires an sm_100 B200)");
+  if (device < 0 || device >= count) throw ValidationError("device index out of range");
+  cudaDeviceProp prop{};
+  cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (prop.major != 10 || prop.minor != 0)
+    throw DeviceError("q8p kernels are built for sm_100a only; device is sm_" +
+                      std::to_string(prop.major) + std::to_string(prop.minor));
+}
+
+void* dev_alloc(q8p_layer* L, std::size_t bytes) {
+  void* p = nullptr;
+  cuda_check(cudaMalloc(&p, bytes ? bytes : 1), "cudaMalloc");
+  L->allocations.push_back(p);
+  L->device_bytes += bytes;
+  return p;
+}
+
+void* upload(q8p_layer* L, const void* host, std::size_t bytes) {
+  void* d = dev_alloc(L, bytes);
+  cuda_check(cudaMemcpy(d, host, bytes, cudaMemcpyHostToDevice), "upload");
+  return d;
+}
+
+void setup_side(q8p_layer* L, DevSide& side, std::uint32_t n, const std::uint8_t* signs) {
+  const HadamardSpec spec = plan_hadamard(n);
+  side.n = n;
+  side.p = static_cast<std::uint32_t>(spec.p);
+  side.q = static_cast<std::uint32_t>(spec.q);
+  std::vector<std::uint8_t> sb(signs, signs + (n + 7) / 8);
+  if (n % 8) sb.back() &= static_cast<std::uint8_t>((1u << (n % 8)) - 1);  // from_bytes masks pad bits
+  side.signs = static_cast<const std::uint8_t*>(upload(L, sb.data(), sb.size()));
+  if (spec.q > 1) {
+    const std::vector<std::int8_t>& b = hadamard_base(spec.q);
+    side.base = static_cast<const std::int8_t*>(upload(L, b.data(), b.size()));
+  }
+}
+
+// Builds a device layer from host fields for rows [r0, r1).
+q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t r1, int device) {
+  if (!d.stages || d.num_stages < 1) throw ValidationError("artifact has no quantization stages");
+  if (d.num_stages > 2) throw UnsupportedError("more than two RVQ stages are not on this path");
+  if (d.transform != 0) throw UnsupportedError("rfft transform is not on this path");
+  if (d.m == 0 || d.n == 0) throw SizeError("empty layer");
+  if (d.n % 8 != 0) throw FormatError("artifact: n not divisible by codeword dimension");
+  if (!(r0 < r1 && r1 <= d.m)) throw ValidationError("row range out of bounds");
+  if (!d.signs_u || !d.signs_v) throw ValidationError("sign vectors required");
+  plan_hadamard(d.n);  // SizeError before any allocation
+  plan_hadamard(d.m);
+  require_sm100(device);
+  DeviceGuard g(device);
+  auto L = std::make_unique<q8p_layer>();
+  L->device = device;
+  L->m = d.m;
+  L->n = d.n;
+  L->row_begin = r0;
+  L->row_end = r1;
+  L->num_stages = d.num_stages;
+  try {
+    setup_side(L.get(), L->side_u, d.m, d.signs_u);
+    setup_side(L.get(), L->side_v, d.n, d.signs_v);
+    const std::size_t nb = d.n / 8, words = std::size_t(r1 - r0) * nb;
+    for (int s = 0; s < d.num_stages; ++s) {
+      const q8p_stage_desc& st = d.stages[s];
+      if (st.codebook != Q8P_CB_E8P_2BIT && st.codebook != Q8P_CB_E8_1BIT)
+        throw ValidationError("unknown codebook");
+      if (!st.codes) throw ValidationError("stage codes missing");
+      if (!(st.scale > 0.f) || !std::isfinite(st.scale)) throw ValidationError("stage scale must be positive");
+      if (st.code_bytes != 1 && st.code_bytes != 2) throw ValidationError("code_bytes must be 1 or 2");
+      if (st.codebook == Q8P_CB_E8P_2BIT && st.code_bytes != 2)
+        throw ValidationError("e8p-2bit codes are 16-bit");
+      L->cb[s] = st.codebook;
+      L->scale[s] = st.scale;
+      const auto* src = static_cast<const std::uint8_t*>(st.codes) + std::size_t(r0) * nb * st.code_bytes;
+      if (st.codebook == Q8P_CB_E8P_2BIT) {
+        L->codes[s] = upload(L.get(), src, words * 2);
+        L->code_bytes += words * 2;
+      } else {
+        // e8-1bit codewords are < 256 (codebook.cpp:66): narrow to u8 losslessly.
+        std::vector<std::uint8_t> narrow(words);
+        for (std::size_t i = 0; i < words; ++i) {
+          const std::uint32_t v = st.code_bytes == 2 ? reinterpret_cast<const std::uint16_t*>(src)[i] : src[i];
+          if (v >= 256) throw ValidationError("decode: codeword out of range");
+          narrow[i] = static_cast<std::uint8_t>(v);
+        }
+        L->codes[s] = upload(L.get(), narrow.data(), words);
+        L->code_bytes += words;
+      }
+    }
+  } catch (...) {
+    for (void* p : L->allocations) cudaFree(p);
+    throw;
+  }
+  return L.release();
+}
+
+q8p_layer* layer_from_bytes(const std::uint8_t* bytes, std::size_t len, std::uint32_t r0,
+                            std::uint32_t r1, bool full, int device) {
+  const QuantizedLinear a = deserialize(std::span(bytes, len));
+  if (a.transform != TransformKind::rht) throw UnsupportedError("rfft transform is not on this path");
+  std::vector<q8p_stage_desc> st(a.stages.size());
+  for (std::size_t s = 0; s < st.size(); ++s) {
+    codebook_code_bytes(a.stages[s].codebook);
+    st[s].codebook = a.stages[s].codebook == "e8p-2bit" ? Q8P_CB_E8P_2BIT : Q8P_CB_E8_1BIT;
+    st[s].scale = a.stages[s].scale;
+    st[s].codes = a.codes[s].data();
+    st[s].code_bytes = 2;
+  }
+  q8p_layer_desc d{};
+  d.m = a.m;
+  d.n = a.n;
+  d.transform = 0;
+  d.num_stages = static_cast<int>(st.size());
+  d.stages = st.data();
+  d.signs_u = a.left_signs.bytes().data();
+  d.signs_v = a.right_signs.bytes().data();
+  if (full) {
+    r0 = 0;
+    r1 = a.m;
+  }
+  return build_layer(d, r0, r1, device);
+}
+
+std::size_t round_up(std::size_t v, std::size_t a) { return (v + a - 1) / a * a; }
+
+struct Workspace {
+  float* t;
+  float* z;
+};
+std::size_t workspace_size(const q8p_layer* L, int batch) {
+  return round_up(std::size_t(batch) * L->n * 4, 256) + round_up(std::size_t(batch) * L->m * 4, 256);
+}
+Workspace carve(const q8p_layer* L, int batch, void* ws) {
+  auto* base = static_cast<std::uint8_t*>(ws);
+  Workspace w;
+  w.t = reinterpret_cast<float*>(base);
+  w.z = reinterpret_cast<float*>(base + round_up(std::size_t(batch) * L->n * 4, 256));
+  return w;
+}
+
+void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void* ws, std::size_t ws_bytes,
+                  cudaStream_t s) {
+  if (!L) throw ValidationError("null layer");
+  if (batch < 0) throw ValidationError("negative batch");
+  if (batch == 0) return;
+  if (!x || !y) throw ValidationError("null x / y");
+  if (L->row_begin != 0 || L->row_end != L->m)
+    throw ValidationError("row-sharded layer: use q8p_forward_sharded");
+  if (!ws || ws_bytes < workspace_size(L, batch)) throw SizeError("workspace too small");
+  DeviceGuard g(L->device);
+  const Workspace w = carve(L, batch, ws);
+  launch_rht(L->side_v, x, w.t, batch, /*transpose=*/false, s);  // t = T_v x
+  launch_gemv_simple(*L, w.t, w.z, batch, static_cast<int>(L->m), s);
+  launch_rht(L->side_u, w.z, y, batch, /*transpose=*/true, s);  // y = T_u^T z
+}
+
+}  // namespace
+}  // namespace q8p::detail
+
+using namespace q8p::detail;
+
+extern "C" {
+
+const char* q8p_version(void) { return "q8p 0.1.0 (sm_100a)"; }
+
+const char* q8p_status_string(q8p_status s) {
+  switch (s) {
+    case Q8P_OK: return "ok";
+    case Q8P_ERR_SIZE: return "size error";
+    case Q8P_ERR_VALIDATION: return "validation error";
+    case Q8P_ERR_FORMAT: return "format error";
+    case Q8P_ERR_BAD_MAGIC: return "bad magic";
+    case Q8P_ERR_UNSUPPORTED_VERSION: return "unsupported version";
+    case Q8P_ERR_TRUNCATED: return "truncated artifact";
+    case Q8P_ERR_UNSUPPORTED: return "unsupported on this path";
+    case Q8P_ERR_CUDA: return "CUDA error";
+    case Q8P_ERR_NCCL: return "NCCL error";
+    default: return "internal error";
+  }
+}
+
+const char* q8p_last_error(void) { return q8p::detail::t_last_error.c_str(); }
+
+uint64_t q8p_kernel_launches(void) { return g_launches.load(); }
+
+q8p_status q8p_plan_hadamard(size_t n, size_t* p, size_t* q) {
+  try {
+    const q8p::HadamardSpec s = q8p::plan_hadamard(n);
+    if (p) *p = s.p;
+    if (q) *q = s.q;
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_layer_create(const q8p_layer_desc* desc, int device, q8p_layer** out) {
+  try {
+    if (!desc || !out) throw q8p::ValidationError("null argument");
+    *out = build_layer(*desc, 0, desc->m, device);
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_layer_from_qshp(const uint8_t* bytes, size_t len, int device, q8p_layer** out) {
+  try {
+    if (!bytes || !out) throw q8p::ValidationError("null argument");
+    *out = layer_from_bytes(bytes, len, 0, 0, true, device);
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_layer_from_qshp_rows(const uint8_t* bytes, size_t len, uint32_t row_begin,
+                                    uint32_t row_end, int device, q8p_layer** out) {
+  try {
+    if (!bytes || !out) throw q8p::ValidationError("null argument");
+    *out = layer_from_bytes(bytes, len, row_begin, row_end, false, device);
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+void q8p_layer_destroy(q8p_layer* L) {
+  if (!L) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(L->device);
+  for (void* p : L->allocations) cudaFree(p);
+  if (L->dev_stage) cudaFree(L->dev_stage);
+  if (L->host_stage) cudaFreeHost(L->host_stage);
+  if (L->stream) cudaStreamDestroy(L->stream);
+  cudaSetDevice(prev);
+  delete L;
+}
+
+q8p_status q8p_layer_get_info(const q8p_layer* L, q8p_layer_info* info) {
+  if (!L || !info) {
+    set_last_error("null argument");
+    return Q8P_ERR_VALIDATION;
+  }
+  info->m = L->m;
+  info->n = L->n;
+  info->row_begin = L->row_begin;
+  info->row_end = L->row_end;
+  info->num_stages = L->num_stages;
+  info->device = L->device;
+  info->device_bytes = L->device_bytes;
+  info->code_bytes = L->code_bytes;
+  return Q8P_OK;
+}
+
+size_t q8p_workspace_bytes(const q8p_layer* L, int batch) {
+  if (!L || batch <= 0) return 0;
+  return workspace_size(L, batch);
+}
+
+q8p_status q8p_forward(const q8p_layer* L, const float* x, float* y, int batch, void* ws,
+                       size_t ws_bytes, void* stream) {
+  try {
+    forward_impl(L, x, y, batch, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_infer_host(q8p_layer* L, const double* x, double* y, int batch) {
+  try {
+    if (!L || !x || !y) throw q8p::ValidationError("null argument");
+    if (batch <= 0) return Q8P_OK;
+    std::scoped_lock lock(L->mu);
+    DeviceGuard g(L->device);
+    if (!L->stream) cuda_check(cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking), "stream");
+    const std::size_t xin = std::size_t(batch) * L->n, yout = std::size_t(batch) * L->m;
+    const std::size_t host_need = (xin + yout) * sizeof(float);
+    if (L->host_stage_bytes < host_need) {
+      if (L->host_stage) cudaFreeHost(L->host_stage);
+      cuda_check(cudaMallocHost(&L->host_stage, host_need), "cudaMallocHost");
+      L->host_stage_bytes = host_need;
+    }
+    const std::size_t ws = workspace_size(L, batch);
+    const std::size_t dev_need = round_up(xin * 4, 256) + round_up(yout * 4, 256) + ws;
+    if (L->dev_stage_bytes < dev_need) {
+      if (L->dev_stage) cudaFree(L->dev_stage);
+      cuda_check(cudaMalloc(&L->dev_stage, dev_need), "cudaMalloc stage");
+      L->dev_stage_bytes = dev_need;
+    }
+    float* hx = static_cast<float*>(L->host_stage);
+    float* hy = hx + xin;
+    for (std::size_t i = 0; i < xin; ++i) hx[i] = static_cast<float>(x[i]);
+    auto* dbase = static_cast<std::uint8_t*>(L->dev_stage);
+    float* dx = reinterpret_cast<float*>(dbase);
+    float* dy = reinterpret_cast<float*>(dbase + round_up(xin * 4, 256));
+    void* dws = dbase + round_up(xin * 4, 256) + round_up(yout * 4, 256);
+    cuda_check(cudaMemcpyAsync(dx, hx, xin * 4, cudaMemcpyHostToDevice, L->stream), "H2D");
+    forward_impl(L, dx, dy, batch, dws, ws, L->stream);
+    cuda_check(cudaMemcpyAsync(hy, dy, yout * 4, cudaMemcpyDeviceToHost, L->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(L->stream), "sync");
+    for (std::size_t i = 0; i < yout; ++i) y[i] = static_cast<double>(hy[i]);
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_decode_stage(const q8p_layer* L, int stage, float* w_hat, void* stream) {
+  try {
+    if (!L || !w_hat) throw q8p::ValidationError("null argument");
+    if (stage < 0 || stage >= L->num_stages) throw q8p::ValidationError("stage out of range");
+    DeviceGuard g(L->device);
+    launch_decode(*L, stage, w_hat, static_cast<cudaStream_t>(stream));
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_rht(size_t n, const uint8_t* signs, const float* x, float* y, int batch, int transpose,
+                   void* stream) {
+  try {
+    if (!signs || !x || !y) throw q8p::ValidationError("null argument");
+    const q8p::HadamardSpec spec = q8p::plan_hadamard(n);
+    DevSide side;
+    side.n = static_cast<std::uint32_t>(n);
+    side.p = static_cast<std::uint32_t>(spec.p);
+    side.q = static_cast<std::uint32_t>(spec.q);
+    side.signs = signs;
+    // Per-order device copies of the base, cached per process (single device per process).
+    static std::mutex mu;
+    static std::vector<std::pair<std::size_t, void*>> bases;
+    if (spec.q > 1) {
+      std::scoped_lock lock(mu);
+      for (auto& [q, ptr] : bases)
+        if (q == spec.q) side.base = static_cast<const std::int8_t*>(ptr);
+      if (!side.base) {
+        const auto& b = q8p::detail::hadamard_base(spec.q);
+        void* d = nullptr;
+        cuda_check(cudaMalloc(&d, b.size()), "cudaMalloc base");
+        cuda_check(cudaMemcpy(d, b.data(), b.size(), cudaMemcpyHostToDevice), "base upload");
+        bases.emplace_back(spec.q, d);
+        side.base = static_cast<const std::int8_t*>(d);
+      }
+    }
+    launch_rht(side, x, y, batch, transpose != 0, static_cast<cudaStream_t>(stream));
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_qshp_inspect(const uint8_t* bytes, size_t len, q8p_artifact_info* info) {
+  try {
+    if (!bytes || !info) throw q8p::ValidationError("null argument");
+    const q8p::QuantizedLinear a = q8p::deserialize(std::span(bytes, len));
+    *info = q8p_artifact_info{};
+    info->m = a.m;
+    info->n = a.n;
+    info->transform = static_cast<int>(a.transform);
+    info->num_stages = static_cast<int>(a.stages.size());
+    for (std::size_t s = 0; s < a.stages.size() && s < 8; ++s) {
+      info->codebook[s] = a.stages[s].codebook == "e8p-2bit" ? Q8P_CB_E8P_2BIT : Q8P_CB_E8_1BIT;
+      info->scale[s] = a.stages[s].scale;
+    }
+    info->serialized_size = q8p::serialized_size(a);
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_qshp_reserialize(const uint8_t* bytes, size_t len, uint8_t* out, size_t cap,
+                                size_t* out_len) {
+  try {
+    if (!bytes || !out_len) throw q8p::ValidationError("null argument");
+    const std::vector<std::uint8_t> b = q8p::serialize(q8p::deserialize(std::span(bytes, len)));
+    *out_len = b.size();
+    if (!out || cap < b.size()) throw q8p::SizeError("output buffer too small");
+    std::memcpy(out, b.data(), b.size());
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_e8p_decode_host(uint16_t word, float out[8]) {
+  try {
+    if (!out) throw q8p::ValidationError("null argument");
+    q8p::detail::e8p_decode_host(word, out);
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_codebook_table(q8p_codebook cb, int8_t* doubled, uint8_t* parity_out) {
+  try {
+    if (!doubled) throw q8p::ValidationError("null argument");
+    if (cb == Q8P_CB_E8P_2BIT) {
+      const auto& t = q8p::detail::e8p_table();
+      for (int i = 0; i < 256; ++i) {
+        for (int c = 0; c < 8; ++c) doubled[i * 8 + c] = t.doubled[i][c];
+        if (parity_out) parity_out[i] = t.odd_parity[i];
+      }
+    } else if (cb == Q8P_CB_E8_1BIT) {
+      const auto& t = q8p::detail::e8_1bit_doubled();
+      for (int i = 0; i < 256; ++i)
+        for (int c = 0; c < 8; ++c) doubled[i * 8 + c] = t[i][c];
+    } else {
+      throw q8p::ValidationError("unknown codebook");
+    }
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_hadamard_base(size_t q, int8_t* out) {
+  try {
+    if (!out) throw q8p::ValidationError("null argument");
+    const auto& b = q8p::detail::hadamard_base(q);
+    std::memcpy(out, b.data(), b.size());
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_forward_sharded(const q8p_layer*, const float*, float*, int, void*, size_t, void*, void*) {
+  set_last_error("q8p_forward_sharded: not built yet");
+  return Q8P_ERR_UNSUPPORTED;
+}
+q8p_status q8p_nccl_unique_id(uint8_t*) {
+  set_last_error("NCCL support not built yet");
+  return Q8P_ERR_UNSUPPORTED;
+}
+q8p_status q8p_nccl_comm_init(const uint8_t*, int, int, int, void**) {
+  set_last_error("NCCL support not built yet");
+  return Q8P_ERR_UNSUPPORTED;
+}
+q8p_status q8p_nccl_comm_destroy(void*) { return Q8P_OK; }
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+// Device-side layer representation and kernel launchers (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstddef>
+#include <cstdint>
+#include <mutex>
+
+#include "internal.hpp"
+
+namespace q8p::detail {
+
+extern std::atomic<std::uint64_t> g_launches;  // kernels launched by this library
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what);
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw_cuda(e, what);
+}
+
+// One side of the randomized Hadamard transform on device.
+struct DevSide {
+  std::uint32_t n = 0, p = 1, q = 1;
+  const std::uint8_t* signs = nullptr;  // ceil(n/8) bytes
+  const std::int8_t* base = nullptr;    // q x q (+-1), nullptr when q == 1
+};
+
+// Fast-path (IMMA GEMV) transcoded code tiles, see gemv_imma.cu.
+struct TileCodes {
+  void* tiles = nullptr;      // [row_tile][k_step][2 halves][32 lanes][16 B]
+  std::uint32_t row_tiles = 0, k_steps = 0;
+};
+
+}  // namespace q8p::detail
+
+struct q8p_layer {
+  int device = 0;
+  std::uint32_t m = 0, n = 0, row_begin = 0, row_end = 0;
+  int num_stages = 0;
+  int cb[2] = {0, 0};
+  float scale[2] = {1.f, 1.f};
+  q8p::detail::DevSide side_u, side_v;  // left (m) / right (n)
+  void* codes[2] = {nullptr, nullptr};  // plain [m_local][n/8]: u16 (E8P) / u8 (e8-1bit)
+  q8p::detail::TileCodes tiles[2];
+  std::size_t device_bytes = 0;
+  std::size_t code_bytes = 0;
+  std::vector<void*> allocations;
+  // q8p_infer_host staging (serialized by `mu`).
+  std::mutex mu;
+  void* host_stage = nullptr;
+  std::size_t host_stage_bytes = 0;
+  void* dev_stage = nullptr;
+  std::size_t dev_stage_bytes = 0;
+  cudaStream_t stream = nullptr;
+
+  std::uint32_t m_local() const { return row_end - row_begin; }
+};
+
+namespace q8p::detail {
+
+// Kernel launchers (kernels_*.cu).  All stream-ordered, no allocation.
+void launch_rht(const DevSide& side, const float* x, float* y, int batch, bool transpose,
+                cudaStream_t s);
+void launch_gemv_simple(const q8p_layer& L, const float* t, float* z, int batch, int z_stride,
+                        cudaStream_t s);
+void launch_decode(const q8p_layer& L, int stage, float* w, cudaStream_t s);
+
+}  // namespace q8p::detail

@@ -1,0 +1,144 @@
+"""Parity of the sm_100a path against the CPU oracle, through the C ABI.
+
+Bars: decode bit-exact (unscaled quarter-integers); layer outputs within
+||dy||/||y|| <= 1e-3 (the north-star fp32-accumulation tolerance; the
+reference's own infer-vs-dense check is 1e-4, acceptance.cpp:405-435, and we
+also assert that tighter bound); RHT within 1e-5 relative."""
+import numpy as np
+import pytest
+
+import paper_2402_04396_b200 as q8p
+from conftest import golden_names, load_case, rel_err
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3        # north star: max rel err <= 1e-3
+TIGHT = 1e-4      # acceptance.cpp:426 criterion-10 bound
+
+
+@pytest.fixture(scope="module")
+def dev():
+    assert torch.cuda.is_available(), "gpu tests need a B200"
+    return torch.device("cuda:0")
+
+
+def random_artifact(m, n, stages, seed, codes=None):
+    """A structurally valid QSHP artifact with random codes (acceptance.cpp:438-450 style)."""
+    import struct
+    rng = np.random.default_rng(seed)
+    body = b"QSHP" + struct.pack("<HIIBB", 1, m, n, 0, len(stages))
+    for cid, scale in stages:
+        body += bytes([len(cid)]) + cid.encode() + struct.pack("<f", scale)
+    body += rng.integers(0, 256, (m + 7) // 8, dtype=np.uint8).tobytes()
+    body += rng.integers(0, 256, (n + 7) // 8, dtype=np.uint8).tobytes()
+    words = m * n // 8
+    for s, (cid, _) in enumerate(stages):
+        if codes is not None and codes[s] is not None:
+            c = codes[s]
+        elif cid == "e8p-2bit":
+            c = rng.integers(0, 65536, words, dtype=np.uint16)
+        else:
+            c = rng.integers(0, 256, words, dtype=np.uint8)
+        body += np.ascontiguousarray(c).tobytes()
+    return body
+
+
+def test_decode_all_65536_words_bit_exact(dev, oracle):
+    # One layer whose codes enumerate every 16-bit word: m = 256, n = 2048.
+    words = np.arange(65536, dtype=np.uint16)
+    art = random_artifact(256, 2048, [("e8p-2bit", 1.0)], 0, codes=[words])
+    L = q8p.Layer.from_qshp(art)
+    w = L.decode_stage(0).cpu().numpy().astype(np.float64)
+    want = oracle.decode_stage(art, 0)
+    assert np.array_equal(w, want)
+
+
+def test_decode_e8_1bit_table_bit_exact(dev, oracle):
+    c2 = np.tile(np.arange(256, dtype=np.uint8), 64 * 64 // 256 // 8 * 8)[: 64 * 64 // 8]
+    art = random_artifact(64, 64, [("e8p-2bit", 1.0), ("e8-1bit", 0.5)], 1, codes=[None, c2])
+    L = q8p.Layer.from_qshp(art)
+    for s in (0, 1):
+        assert np.array_equal(L.decode_stage(s).cpu().numpy().astype(np.float64), oracle.decode_stage(art, s))
+
+
+@pytest.mark.parametrize("n", [4, 12, 24, 56, 112, 160, 4096, 8192, 11008, 28672])
+def test_rht_matches_oracle(dev, oracle, n):
+    rng = np.random.default_rng(n)
+    signs = rng.integers(0, 256, (n + 7) // 8, dtype=np.uint8)
+    x = rng.standard_normal((3, n)).astype(np.float32)
+    xd = torch.from_numpy(x).to(dev)
+    sd = torch.from_numpy(signs).to(dev)
+    for tr in (False, True):
+        got = q8p.rht(xd, sd, transpose=tr).cpu().numpy()
+        for b in range(3):
+            want = oracle.side_apply(signs, x[b].astype(np.float64), tr)
+            assert rel_err(got[b], want) < 1e-5, (n, tr, rel_err(got[b], want))
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_forward_matches_reference_golden(dev, name):
+    art, x, y = load_case(name)
+    L = q8p.Layer.from_qshp(art)
+    got = L.forward(torch.from_numpy(x.astype(np.float32)).to(dev)).cpu().numpy()
+    for b in range(x.shape[0]):
+        assert rel_err(got[b], y[b]) < TIGHT, (name, b, rel_err(got[b], y[b]))
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_infer_host_drop_in(dev, name):
+    art, x, y = load_case(name)
+    L = q8p.Layer.from_qshp(art)
+    got = L.infer_host(x)
+    assert got.dtype == np.float64 and got.shape == y.shape
+    assert rel_err(got, y) < TIGHT
+    assert rel_err(L.infer_host(x[0]), y[0]) < TIGHT
+
+
+def test_size_error_on_wrong_length(dev):
+    art, x, _ = load_case("e8p2_64x64")
+    L = q8p.Layer.from_qshp(art)
+    with pytest.raises(q8p.SizeError):
+        L.infer_host(np.zeros(63))
+    with pytest.raises(q8p.SizeError):
+        L.forward(torch.zeros(1, 65, device=dev))
+
+
+def test_empty_batch_is_noop(dev):
+    art, _, _ = load_case("e8p2_64x64")
+    L = q8p.Layer.from_qshp(art)
+    out = L.forward(torch.zeros(0, 64, device=dev))
+    assert out.shape == (0, 64)
+
+
+def test_unsupported_shapes_rejected(dev):
+    with pytest.raises(q8p.SizeError):  # 36 = 4 * 9: no base 9
+        q8p.Layer.from_qshp(random_artifact(36, 64, [("e8p-2bit", 1.0)], 2))
+
+
+@pytest.mark.parametrize("m,n,bits", [(4096, 4096, 2), (11008, 4096, 2), (4096, 11008, 2),
+                                      (4096, 4096, 3), (4096, 4096, 4)])
+def test_7b_shapes_vs_oracle(dev, oracle, m, n, bits):
+    stages = {2: [("e8p-2bit", 1.11)], 3: [("e8p-2bit", 1.02), ("e8-1bit", 0.49)],
+              4: [("e8p-2bit", 0.97), ("e8p-2bit", 0.29)]}[bits]
+    art = random_artifact(m, n, stages, m + n + bits)
+    L = q8p.Layer.from_qshp(art)
+    x = np.random.default_rng(3).standard_normal((2, n)).astype(np.float32).astype(np.float64)
+    want = oracle.infer(art, x, threads=8)
+    got = L.forward(torch.from_numpy(x.astype(np.float32)).to(dev)).cpu().numpy()
+    for b in range(2):
+        assert rel_err(got[b], want[b]) < TIGHT, rel_err(got[b], want[b])
+
+
+def test_linearity_and_batch_consistency(dev):
+    # Size-independent properties at a 70B shape: f(a x1 + b x2) = a f(x1) + b f(x2),
+    # and batched rows equal single-vector calls.
+    art = random_artifact(8192, 8192, [("e8p-2bit", 1.0)], 9)
+    L = q8p.Layer.from_qshp(art)
+    g = torch.Generator(device="cpu").manual_seed(0)
+    x = torch.randn(3, 8192, generator=g).to(dev)
+    y = L.forward(x)
+    y2 = L.forward((2.0 * x[0] - 0.5 * x[1]).contiguous())
+    assert rel_err((2.0 * y[0] - 0.5 * y[1]).cpu().numpy(), y2.cpu().numpy()) < 1e-5
+    for b in range(3):
+        assert rel_err(L.forward(x[b].contiguous()).cpu().numpy(), y[b].cpu().numpy()) < 1e-6
