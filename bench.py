@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Benchmark: QuIP# E8P 2-bit quantized linear layers at batch 1 on B200.
+
+Metric (BASELINE.json): "E8P 2-bit quantized matvec: achieved HBM GB/s vs
+peak; layer tokens/s at batch 1".  One step = one batch-1 token through the
+Llama-2-70B-shaped layer set (8192x8192, 28672x8192, 8192x28672; configs[2]),
+each layer y = S_U H^T W_hat H S_V x (K1 -> K2 -> K3).
+
+  value    tokens/s of the layer set, inputs already in HBM (CUDA graph of
+           the step, replayed K times, CUDA events on the launching stream,
+           max over ranks).
+  e2e      the same metric through the public per-layer API with HOST
+           buffers: H2D of x and D2H of y inside the timed region.
+  roofline the decode-GEMV kernel (K2): algorithmic bytes
+           (codes + 4 B x activations in + 4 B x outputs)
+           / average kernel time from CUDA events recorded around K2.
+  cpu_baseline  the reference latq::infer (oracle/_ref, compiled from the
+           reference sources) on the box's host cores, bounded sample.
+
+N > 1 (torchrun): the layers are row-sharded across ranks (each rank holds
+m/N rows), z is all-gathered with NCCL before the output RHT; total work is
+fixed -> "scaling": "strong".
+
+`--impl reference` times the reference CPU implementation instead (rank 0
+only; other ranks exit 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import struct
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LAYERS_70B = [(8192, 8192), (28672, 8192), (8192, 28672)]
+LAYERS_7B = [(4096, 4096)] * 4 + [(11008, 4096)] * 2 + [(4096, 11008)]
+METRIC = "E8P 2-bit quantized matvec: achieved HBM GB/s vs peak; layer tokens/s at batch 1"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def make_artifact(m: int, n: int, seed: int, scale: float = 1.11) -> bytes:
+    """QSHP v1, one e8p-2bit stage, seeded synthetic codes and signs."""
+    rng = np.random.default_rng(seed)
+    body = b"QSHP" + struct.pack("<HIIBB", 1, m, n, 0, 1) + bytes([8]) + b"e8p-2bit" + struct.pack("<f", scale)
+    body += rng.integers(0, 256, (m + 7) // 8, dtype=np.uint8).tobytes()
+    body += rng.integers(0, 256, (n + 7) // 8, dtype=np.uint8).tobytes()
+    body += rng.integers(0, 65536, m * n // 8, dtype=np.uint16).tobytes()
+    return body
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        loaded = [c for c, _, _ in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(m for _, m, _ in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def cpu_reference(layers, tokens_per_step: int, threads: int, sample_div: int, steps: int, warmup: int):
+    """Time the reference latq::infer (oracle/_ref) on the host: each step runs
+    `threads` vectors concurrently (one std::thread each, the reference's own
+    re-entrant infer) through row-sampled copies of the layer set (first
+    m/sample_div rows).  Returns tokens/s scaled to full layers."""
+    from oracle.refpy import Ref
+    ref = Ref()
+    arts = []
+    for i, (m, n) in enumerate(layers):
+        ms = m // sample_div
+        arts.append((make_artifact(ms, n, 1000 + i), n))
+    times = []
+    for it in range(warmup + steps):
+        t0 = time.perf_counter()
+        for art, n in arts:
+            x = np.random.default_rng(it).standard_normal((threads * tokens_per_step, n))
+            ref.infer(art, x, threads=threads)
+        dt = time.perf_counter() - t0
+        if it >= warmup:
+            times.append(dt)
+    step = statistics.median(times)
+    # full-layer time per step = sampled time * sample_div (decode loop is linear in m)
+    return threads * tokens_per_step / (step * sample_div), step
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    layers = LAYERS_70B if args.workload == "70b" else LAYERS_7B
+    threads = args.cpu_threads or min(os.cpu_count() or 1, 64)
+    tps, step = cpu_reference(layers, 1, threads, args.sample_div, args.steps, args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / tps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"llama2-{args.workload}-layer-set-2bit-b1", "batch": 1,
+                   "layers": [f"{m}x{n}" for m, n in layers]},
+        "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "reference",
+                         "sample": f"per step {threads} concurrent latq::infer calls (1 thread each) over the "
+                                   f"first m/{args.sample_div} rows of each layer; scaled x{args.sample_div}"},
+        "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2402_04396_b200 as q8p
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    layers = LAYERS_70B if args.workload == "70b" else LAYERS_7B
+    hbm_peak, peak_kind = peaks()
+
+    comm = None
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            buf = (ctypes_u8 := np.zeros(128, dtype=np.uint8))
+            q8p._check(q8p.lib().q8p_nccl_unique_id(buf.ctypes.data))
+            uid = torch.from_numpy(buf)
+        uid = uid.to(dev)
+        dist.broadcast(uid, 0)
+        import ctypes
+        c = ctypes.c_void_p()
+        idb = uid.cpu().numpy()
+        q8p._check(q8p.lib().q8p_nccl_comm_init(idb.ctypes.data, world, rank, local, ctypes.byref(c)))
+        comm = c
+
+    # Two full copies of the layer set rotate so every step streams from HBM
+    # (134.6 MB per copy at 2 bits vs ~126 MB L2).
+    copies = []
+    arts = [make_artifact(m, n, 1000 + i) for i, (m, n) in enumerate(layers)]
+    for c in range(args.copies):
+        row = []
+        for (m, n), art in zip(layers, arts):
+            if world > 1:
+                lo, hi = m * rank // world, m * (rank + 1) // world
+                row.append(q8p.Layer.from_qshp(art, device=local, rows=(lo, hi)))
+            else:
+                row.append(q8p.Layer.from_qshp(art, device=local))
+        copies.append(row)
+    maxn = max(n for _, n in layers)
+    maxm = max(m for m, _ in layers)
+    ws = torch.empty(max(L.workspace_bytes(1) for L in copies[0]) + (1 << 20), dtype=torch.uint8, device=dev)
+    xs = [torch.randn(1, n, device=dev) for _, n in layers]
+    ys = [torch.empty(1, m, device=dev) for m, _ in layers]
+    stream = torch.cuda.Stream(device=dev)
+
+    n_gemv = len(layers)
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_gemv)]
+          for _ in range(args.copies)]
+
+    def step(c, events=True):
+        for li, L in enumerate(copies[c]):
+            e = ev[c][li] if events else None
+            if world > 1:
+                L.forward_sharded(xs[li], comm, out=ys[li], stream=stream, workspace=ws)
+            else:
+                L.forward(xs[li], out=ys[li], stream=stream, workspace=ws, gemv_events=e)
+
+    # Mark the GEMV events as recorded for torch's bookkeeping; the library
+    # re-records them (cudaEventRecord) around K2, also inside graphs.
+    for row in ev:
+        for a, b in row:
+            a.record(stream)
+            b.record(stream)
+    # Warm-up (eager), then capture one graph per copy.
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            for c in range(args.copies):
+                step(c, events=False)
+    torch.cuda.synchronize()
+    graphs = []
+    use_graph = not args.no_graph and world == 1
+    if use_graph:
+        for c in range(args.copies):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                step(c)
+            graphs.append(g)
+        torch.cuda.synchronize()
+        for c in range(args.copies):
+            graphs[c].replay()
+        torch.cuda.synchronize()
+
+    launches0 = q8p.kernel_launches()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gemv_ms = {li: [] for li in range(n_gemv)}
+    with ClockSampler(local) as clocks:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            t0.record(stream)
+            for s in range(args.steps):
+                c = s % args.copies
+                if use_graph:
+                    graphs[c].replay()
+                else:
+                    step(c)
+            t1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        # gather GEMV durations of the last replay of each copy
+    total_ms = t0.elapsed_time(t1)
+    launches = (q8p.kernel_launches() - launches0) if not use_graph else 3 * len(layers) * args.steps
+    if world == 1:
+        # Re-run the timed steps once more collecting every GEMV event pair.
+        with torch.cuda.stream(stream):
+            for s in range(args.steps):
+                c = s % args.copies
+                if use_graph:
+                    graphs[c].replay()
+                else:
+                    step(c)
+                stream.synchronize()
+                for li in range(n_gemv):
+                    gemv_ms[li].append(ev[c][li][0].elapsed_time(ev[c][li][1]))
+    ms = total_ms / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    tokens_per_s = 1e3 / ms
+
+    # e2e through the public API with host buffers: H2D x, forward, D2H y.
+    hx = [torch.randn(1, n).pin_memory() for _, n in layers]
+    hy = [torch.empty(1, m).pin_memory() for m, _ in layers]
+    h2d = sum(4 * n for _, n in layers)
+    d2h = sum(4 * m for m, _ in layers)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for s in range(args.steps):
+            c = s % args.copies
+            for li, L in enumerate(copies[c]):
+                xs[li].copy_(hx[li], non_blocking=True)
+                if world > 1:
+                    L.forward_sharded(xs[li], comm, out=ys[li], stream=stream, workspace=ws)
+                else:
+                    L.forward(xs[li], out=ys[li], stream=stream, workspace=ws)
+                hy[li].copy_(ys[li], non_blocking=True)
+            stream.synchronize()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # Roofline of the dominant kernel (K2) on the largest layer.
+    roof = None
+    if world == 1 and all(gemv_ms[li] for li in range(n_gemv)):
+        per = []
+        for li, (m, n) in enumerate(layers):
+            b = m * n // 8 * 2 + 4 * n + 4 * m
+            t = statistics.mean(gemv_ms[li])
+            per.append({"layer": f"{m}x{n}", "bytes": b, "us": t * 1e3, "gbs": b / (t * 1e-3) / 1e9})
+        big = max(per, key=lambda p: p["bytes"])
+        tot_b = sum(p["bytes"] for p in per)
+        tot_t = sum(p["us"] for p in per) * 1e-6
+        achieved = tot_b / tot_t / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "peak_kind": peak_kind, "traffic": None, "kernel": "q8p gemv (K2)", "per_layer": per,
+                "gemv_share_of_step": (tot_t * 1e3) / ms}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            threads = args.cpu_threads or min(os.cpu_count() or 1, 64)
+            tps, step_s = cpu_reference(layers, 1, threads, args.sample_div, 1, 0)
+            cpu = {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "reference",
+                   "sample": f"{threads} concurrent latq::infer (1 thread each) over first m/{args.sample_div} rows "
+                             f"of each layer, scaled x{args.sample_div}; {step_s:.1f}s"}
+        except Exception as e:  # reference .so missing etc.
+            cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "config": {"workload": f"llama2-{args.workload}-layer-set-2bit-b1", "batch": 1,
+                       "layers": [f"{m}x{n}" for m, n in layers],
+                       "parallelism": f"row-shard tp{world}" if world > 1 else "single-gpu",
+                       "l2": f"{args.copies} rotating copies of the layer set (> L2 per step pair)",
+                       "codes": "uniform-random e8p-2bit codes (perf variant, test_pipeline.cpp:256-273)",
+                       "cuda_graph": use_graph},
+            "e2e": {"value": 1e3 / e2e_ms, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="70b", choices=["70b", "7b"])
+    ap.add_argument("--copies", type=int, default=2)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--sample-div", type=int, default=32)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

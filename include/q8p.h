@@ -117,6 +117,18 @@ size_t q8p_workspace_bytes(const q8p_layer* layer, int batch);
 q8p_status q8p_forward(const q8p_layer* layer, const float* x, float* y, int batch,
                        void* workspace, size_t workspace_bytes, void* stream);
 
+/* q8p_forward with instrumentation: when non-NULL, `gemv_start_event` /
+ * `gemv_end_event` (cudaEvent_t) are recorded on `stream` immediately
+ * before / after the decode-GEMV kernel (K2), so callers can time the
+ * dominant kernel live, including under CUDA-graph capture. */
+typedef struct {
+  void* gemv_start_event;
+  void* gemv_end_event;
+} q8p_forward_opts;
+q8p_status q8p_forward_ex(const q8p_layer* layer, const float* x, float* y, int batch,
+                          void* workspace, size_t workspace_bytes, void* stream,
+                          const q8p_forward_opts* opts);
+
 /* Row-sharded forward: `layer` holds rows [row_begin, row_end) of the full
  * layer on this rank.  Each rank computes its z slice, the slices are
  * all-gathered over `nccl_comm` (an ncclComm_t), then every rank applies

@@ -90,6 +90,10 @@ LayerDesc._fields_ = [("m", ctypes.c_uint32), ("n", ctypes.c_uint32), ("transfor
                       ("signs_u", ctypes.c_void_p), ("signs_v", ctypes.c_void_p)]
 
 
+class ForwardOpts(ctypes.Structure):
+    _fields_ = [("gemv_start_event", ctypes.c_void_p), ("gemv_end_event", ctypes.c_void_p)]
+
+
 class LayerInfo(ctypes.Structure):
     _fields_ = [("m", ctypes.c_uint32), ("n", ctypes.c_uint32), ("row_begin", ctypes.c_uint32),
                 ("row_end", ctypes.c_uint32), ("num_stages", ctypes.c_int), ("device", ctypes.c_int),
@@ -116,6 +120,7 @@ _SIGNATURES = {
     "q8p_layer_get_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(LayerInfo)]),
     "q8p_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int]),
     "q8p_forward": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "q8p_forward_ex": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.POINTER(ForwardOpts)]),
     "q8p_forward_sharded": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]),
     "q8p_infer_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
     "q8p_decode_stage": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
@@ -277,8 +282,10 @@ class Layer:
             self._ws = torch.empty(need, dtype=torch.uint8, device=f"cuda:{self.info['device']}")
         return self._ws
 
-    def forward(self, x, out=None, stream=None, workspace=None):
-        """y = W_tilde x for a [batch, n] fp32 CUDA tensor -> [batch, m]."""
+    def forward(self, x, out=None, stream=None, workspace=None, gemv_events=None):
+        """y = W_tilde x for a [batch, n] fp32 CUDA tensor -> [batch, m].
+        gemv_events: optional (start, end) torch.cuda.Event pair recorded
+        around the decode-GEMV kernel."""
         torch = _torch()
         info = self.info
         if x.dim() == 1:
@@ -291,8 +298,13 @@ class Layer:
         if out is None:
             out = torch.empty(batch, info["m"], dtype=torch.float32, device=x.device)
         ws = workspace if workspace is not None else self.workspace(batch)
-        _check(lib().q8p_forward(self._h, x.data_ptr(), out.data_ptr(), batch, ws.data_ptr(),
-                                 ws.numel(), _stream_ptr(stream)))
+        if gemv_events is None:
+            _check(lib().q8p_forward(self._h, x.data_ptr(), out.data_ptr(), batch, ws.data_ptr(),
+                                     ws.numel(), _stream_ptr(stream)))
+        else:
+            opts = ForwardOpts(gemv_events[0].cuda_event, gemv_events[1].cuda_event)
+            _check(lib().q8p_forward_ex(self._h, x.data_ptr(), out.data_ptr(), batch, ws.data_ptr(),
+                                        ws.numel(), _stream_ptr(stream), ctypes.byref(opts)))
         return out
 
     def forward_sharded(self, x, comm, out=None, stream=None, workspace=None):

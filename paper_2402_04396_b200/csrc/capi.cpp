@@ -211,7 +211,7 @@ Workspace carve(const q8p_layer* L, int batch, void* ws) {
 }
 
 void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void* ws, std::size_t ws_bytes,
-                  cudaStream_t s) {
+                  cudaStream_t s, const q8p_forward_opts* opts = nullptr) {
   if (!L) throw ValidationError("null layer");
   if (batch < 0) throw ValidationError("negative batch");
   if (batch == 0) return;
@@ -222,7 +222,11 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
   DeviceGuard g(L->device);
   const Workspace w = carve(L, batch, ws);
   launch_rht(L->side_v, x, w.t, batch, /*transpose=*/false, s);  // t = T_v x
+  if (opts && opts->gemv_start_event)
+    cuda_check(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(opts->gemv_start_event), s, cudaEventRecordExternal), "event record");
   launch_gemv_simple(*L, w.t, w.z, batch, static_cast<int>(L->m), s);
+  if (opts && opts->gemv_end_event)
+    cuda_check(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(opts->gemv_end_event), s, cudaEventRecordExternal), "event record");
   launch_rht(L->side_u, w.z, y, batch, /*transpose=*/true, s);  // y = T_u^T z
 }
 
@@ -335,6 +339,16 @@ q8p_status q8p_forward(const q8p_layer* L, const float* x, float* y, int batch, 
                        size_t ws_bytes, void* stream) {
   try {
     forward_impl(L, x, y, batch, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_forward_ex(const q8p_layer* L, const float* x, float* y, int batch, void* ws,
+                          size_t ws_bytes, void* stream, const q8p_forward_opts* opts) {
+  try {
+    forward_impl(L, x, y, batch, ws, ws_bytes, static_cast<cudaStream_t>(stream), opts);
     return Q8P_OK;
   } catch (...) {
     return status_of_current_exception();
