@@ -2,6 +2,7 @@
 // (K1 -> K2 -> [all-gather] -> K3), host-buffer infer, and status mapping.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -131,6 +132,12 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
   try {
     setup_side(L.get(), L->side_u, d.m, d.signs_u);
     setup_side(L.get(), L->side_v, d.n, d.signs_v);
+    {
+      std::vector<std::uint32_t> e8p, e81;
+      imma_tables(e8p, e81);
+      L->lut_e8p = static_cast<const std::uint32_t*>(upload(L.get(), e8p.data(), e8p.size() * 4));
+      L->lut_e81 = static_cast<const std::uint32_t*>(upload(L.get(), e81.data(), e81.size() * 4));
+    }
     const std::size_t nb = d.n / 8, words = std::size_t(r1 - r0) * nb;
     for (int s = 0; s < d.num_stages; ++s) {
       const q8p_stage_desc& st = d.stages[s];
@@ -144,6 +151,21 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
       L->cb[s] = st.codebook;
       L->scale[s] = st.scale;
       const auto* src = static_cast<const std::uint8_t*>(st.codes) + std::size_t(r0) * nb * st.code_bytes;
+      // Tensor-core tile format (lossless re-layout, gemv_imma.cu).
+      {
+        std::vector<std::uint16_t> wide(words);
+        for (std::size_t i = 0; i < words; ++i)
+          wide[i] = st.code_bytes == 2 ? reinterpret_cast<const std::uint16_t*>(src)[i] : src[i];
+        if (st.codebook == Q8P_CB_E8_1BIT)
+          for (std::size_t i = 0; i < words; ++i)
+            if (wide[i] >= 256) throw ValidationError("decode: codeword out of range");
+        const int kind = st.codebook == Q8P_CB_E8P_2BIT ? 0 : 1;
+        std::vector<std::uint8_t> tiles(imma_tile_bytes(r1 - r0, d.n, kind));
+        imma_transcode(wide.data(), r1 - r0, d.n, kind, tiles.data());
+        L->tiles[s].tiles = upload(L.get(), tiles.data(), tiles.size());
+        L->tiles[s].row_tiles = (r1 - r0 + 15) / 16;
+        L->tiles[s].k_steps = (d.n / 8 + 31) / 32;
+      }
       if (st.codebook == Q8P_CB_E8P_2BIT) {
         L->codes[s] = upload(L.get(), src, words * 2);
         L->code_bytes += words * 2;
@@ -196,17 +218,30 @@ q8p_layer* layer_from_bytes(const std::uint8_t* bytes, std::size_t len, std::uin
 std::size_t round_up(std::size_t v, std::size_t a) { return (v + a - 1) / a * a; }
 
 struct Workspace {
-  float* t;
-  float* z;
+  float* t;              // [batch][n]
+  float* z;              // [batch][m] fp32 (portable path) / scratch for the RHT passes
+  float* amax;           // [batch]
+  std::int32_t* zacc;    // [stages][8][rows_pad] int32 limb accumulators
+  std::uint32_t rows_pad;
 };
+std::uint32_t rows_pad_of(const q8p_layer* L) { return (L->m + 15) / 16 * 16; }
 std::size_t workspace_size(const q8p_layer* L, int batch) {
-  return round_up(std::size_t(batch) * L->n * 4, 256) + round_up(std::size_t(batch) * L->m * 4, 256);
+  const std::size_t mx = std::max(L->n, L->m);
+  return round_up(std::size_t(batch) * L->n * 4, 256) + round_up(std::size_t(batch) * mx * 4, 256) +
+         round_up(std::size_t(batch) * 4, 256) + round_up(std::size_t(2) * 8 * rows_pad_of(L) * 4, 256);
 }
 Workspace carve(const q8p_layer* L, int batch, void* ws) {
-  auto* base = static_cast<std::uint8_t*>(ws);
+  auto* p = static_cast<std::uint8_t*>(ws);
+  const std::size_t mx = std::max(L->n, L->m);
   Workspace w;
-  w.t = reinterpret_cast<float*>(base);
-  w.z = reinterpret_cast<float*>(base + round_up(std::size_t(batch) * L->n * 4, 256));
+  w.t = reinterpret_cast<float*>(p);
+  p += round_up(std::size_t(batch) * L->n * 4, 256);
+  w.z = reinterpret_cast<float*>(p);
+  p += round_up(std::size_t(batch) * mx * 4, 256);
+  w.amax = reinterpret_cast<float*>(p);
+  p += round_up(std::size_t(batch) * 4, 256);
+  w.zacc = reinterpret_cast<std::int32_t*>(p);
+  w.rows_pad = rows_pad_of(L);
   return w;
 }
 
@@ -221,6 +256,21 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
   if (!ws || ws_bytes < workspace_size(L, batch)) throw SizeError("workspace too small");
   DeviceGuard g(L->device);
   const Workspace w = carve(L, batch, ws);
+  if (imma_supported(*L, batch)) {
+    // K1: t = T_v x (+ per-vector amax, zeroed accumulators); K2: tensor-core
+    // decode-GEMV into int32 limb accumulators; K3: y = T_u^T z.
+    const std::size_t zwords = std::size_t(L->num_stages) * 8 * w.rows_pad;
+    launch_rht_in(L->side_v, x, w.t, w.z, w.amax, w.zacc, zwords, batch, s);
+    if (opts && opts->gemv_start_event)
+      cuda_check(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(opts->gemv_start_event), s, cudaEventRecordExternal), "event record");
+    launch_gemv_imma(*L, w.t, w.amax, w.zacc, w.rows_pad, batch, s);
+    if (opts && opts->gemv_end_event)
+      cuda_check(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(opts->gemv_end_event), s, cudaEventRecordExternal), "event record");
+    float zscale[2];
+    for (int st = 0; st < 2; ++st) zscale[st] = 0.5f * L->scale[st] / 16256.f;
+    launch_rht_out(L->side_u, w.zacc, L->num_stages, w.rows_pad, zscale, w.amax, w.z, y, batch, s);
+    return;
+  }
   launch_rht(L->side_v, x, w.t, batch, /*transpose=*/false, s);  // t = T_v x
   if (opts && opts->gemv_start_event)
     cuda_check(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(opts->gemv_start_event), s, cudaEventRecordExternal), "event record");

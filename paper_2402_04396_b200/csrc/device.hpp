@@ -7,6 +7,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <mutex>
+#include <vector>
 
 #include "internal.hpp"
 
@@ -43,6 +44,8 @@ struct q8p_layer {
   q8p::detail::DevSide side_u, side_v;  // left (m) / right (n)
   void* codes[2] = {nullptr, nullptr};  // plain [m_local][n/8]: u16 (E8P) / u8 (e8-1bit)
   q8p::detail::TileCodes tiles[2];
+  const std::uint32_t* lut_e8p = nullptr;  // device [256]   (tensor-core GEMV tables)
+  const std::uint32_t* lut_e81 = nullptr;  // device [256][2]
   std::size_t device_bytes = 0;
   std::size_t code_bytes = 0;
   std::vector<void*> allocations;
@@ -65,5 +68,19 @@ void launch_rht(const DevSide& side, const float* x, float* y, int batch, bool t
 void launch_gemv_simple(const q8p_layer& L, const float* t, float* z, int batch, int z_stride,
                         cudaStream_t s);
 void launch_decode(const q8p_layer& L, int stage, float* w, cudaStream_t s);
+
+// Tensor-core path (gemv_imma.cu, kernels_rht.cu).
+void imma_tables(std::vector<std::uint32_t>& e8p, std::vector<std::uint32_t>& e81);
+std::size_t imma_tile_bytes(std::uint32_t m_local, std::uint32_t n, int kind);
+void imma_transcode(const std::uint16_t* codes, std::uint32_t m_local, std::uint32_t n, int kind,
+                    std::uint8_t* out);
+bool imma_supported(const q8p_layer& L, int batch);
+void launch_gemv_imma(const q8p_layer& L, const float* t, const float* amax, std::int32_t* zacc,
+                      std::uint32_t rows_pad, int batch, cudaStream_t s);
+void launch_rht_in(const DevSide& side, const float* x, float* t, float* u_scratch, float* amax,
+                   std::int32_t* zero_ptr, std::size_t zero_words, int batch, cudaStream_t s);
+void launch_rht_out(const DevSide& side, const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows,
+                    const float zscale[2], const float* amax, float* u_scratch, float* y, int batch,
+                    cudaStream_t s);
 
 }  // namespace q8p::detail
