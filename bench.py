@@ -236,17 +236,24 @@ def run_ours(args):
             for c in range(args.copies):
                 step(c, events=False)
     torch.cuda.synchronize()
-    graphs = []
+    graphs, ev_graphs = [], []
     use_graph = not args.no_graph and world == 1
     if use_graph:
+        # headline graphs: no event nodes (they would break the programmatic
+        # dependent launch edges between kernels); instrumented twins time K2.
         for c in range(args.copies):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=stream):
-                step(c)
+                step(c, events=False)
             graphs.append(g)
+            g2 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g2, stream=stream):
+                step(c, events=True)
+            ev_graphs.append(g2)
         torch.cuda.synchronize()
         for c in range(args.copies):
             graphs[c].replay()
+            ev_graphs[c].replay()
         torch.cuda.synchronize()
 
     launches0 = q8p.kernel_launches()
@@ -277,7 +284,7 @@ def run_ours(args):
             for s in range(args.steps):
                 c = s % args.copies
                 if use_graph:
-                    graphs[c].replay()
+                    ev_graphs[c].replay()
                 else:
                     step(c)
                 stream.synchronize()

@@ -103,10 +103,17 @@ void setup_side(q8p_layer* L, DevSide& side, std::uint32_t n, const std::uint8_t
   std::vector<std::uint8_t> sb(signs, signs + (n + 7) / 8);
   if (n % 8) sb.back() &= static_cast<std::uint8_t>((1u << (n % 8)) - 1);  // from_bytes masks pad bits
   side.signs = static_cast<const std::uint8_t*>(upload(L, sb.data(), sb.size()));
+  std::vector<float> colsum(spec.q, 1.f);
   if (spec.q > 1) {
     const std::vector<std::int8_t>& b = hadamard_base(spec.q);
     side.base = static_cast<const std::int8_t*>(upload(L, b.data(), b.size()));
+    for (std::size_t j = 0; j < spec.q; ++j) {
+      long c = 0;
+      for (std::size_t i = 0; i < spec.q; ++i) c += b[i * spec.q + j];
+      colsum[j] = float(c);
+    }
   }
+  side.colsum = static_cast<const float*>(upload(L, colsum.data(), colsum.size() * 4));
 }
 
 // Builds a device layer from host fields for rows [r0, r1).
@@ -161,8 +168,10 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
             if (wide[i] >= 256) throw ValidationError("decode: codeword out of range");
         const int kind = st.codebook == Q8P_CB_E8P_2BIT ? 0 : 1;
         std::vector<std::uint8_t> tiles(imma_tile_bytes(r1 - r0, d.n, kind));
-        imma_transcode(wide.data(), r1 - r0, d.n, kind, tiles.data());
+        std::vector<std::uint8_t> shifts(imma_shift_bytes(r1 - r0, d.n, kind));
+        imma_transcode(wide.data(), r1 - r0, d.n, kind, tiles.data(), shifts.data());
         L->tiles[s].tiles = upload(L.get(), tiles.data(), tiles.size());
+        if (!shifts.empty()) L->tiles[s].shifts = upload(L.get(), shifts.data(), shifts.size());
         L->tiles[s].row_tiles = (r1 - r0 + 15) / 16;
         L->tiles[s].k_steps = (d.n / 8 + 31) / 32;
       }
@@ -217,10 +226,23 @@ q8p_layer* layer_from_bytes(const std::uint8_t* bytes, std::size_t len, std::uin
 
 std::size_t round_up(std::size_t v, std::size_t a) { return (v + a - 1) / a * a; }
 
+// Records a caller event on `s`; under stream capture it must become an
+// external event node to be timeable after graph replay.
+void record_event(void* ev, cudaStream_t s) {
+  if (!ev) return;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cuda_check(cudaStreamIsCapturing(s, &st), "capture status");
+  if (st == cudaStreamCaptureStatusActive)
+    cuda_check(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(ev), s, cudaEventRecordExternal), "event record");
+  else
+    cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(ev), s), "event record");
+}
+
 struct Workspace {
   float* t;              // [batch][n]
   float* z;              // [batch][m] fp32 (portable path) / scratch for the RHT passes
   float* amax;           // [batch]
+  float* tsum;           // [batch]
   std::int32_t* zacc;    // [stages][8][rows_pad] int32 limb accumulators
   std::uint32_t rows_pad;
 };
@@ -228,7 +250,7 @@ std::uint32_t rows_pad_of(const q8p_layer* L) { return (L->m + 15) / 16 * 16; }
 std::size_t workspace_size(const q8p_layer* L, int batch) {
   const std::size_t mx = std::max(L->n, L->m);
   return round_up(std::size_t(batch) * L->n * 4, 256) + round_up(std::size_t(batch) * mx * 4, 256) +
-         round_up(std::size_t(batch) * 4, 256) + round_up(std::size_t(2) * 8 * rows_pad_of(L) * 4, 256);
+         2 * round_up(std::size_t(batch) * 4, 256) + round_up(std::size_t(2) * 8 * rows_pad_of(L) * 4, 256);
 }
 Workspace carve(const q8p_layer* L, int batch, void* ws) {
   auto* p = static_cast<std::uint8_t*>(ws);
@@ -239,6 +261,8 @@ Workspace carve(const q8p_layer* L, int batch, void* ws) {
   w.z = reinterpret_cast<float*>(p);
   p += round_up(std::size_t(batch) * mx * 4, 256);
   w.amax = reinterpret_cast<float*>(p);
+  p += round_up(std::size_t(batch) * 4, 256);
+  w.tsum = reinterpret_cast<float*>(p);
   p += round_up(std::size_t(batch) * 4, 256);
   w.zacc = reinterpret_cast<std::int32_t*>(p);
   w.rows_pad = rows_pad_of(L);
@@ -260,23 +284,22 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
     // K1: t = T_v x (+ per-vector amax, zeroed accumulators); K2: tensor-core
     // decode-GEMV into int32 limb accumulators; K3: y = T_u^T z.
     const std::size_t zwords = std::size_t(L->num_stages) * 8 * w.rows_pad;
-    launch_rht_in(L->side_v, x, w.t, w.z, w.amax, w.zacc, zwords, batch, s);
-    if (opts && opts->gemv_start_event)
-      cuda_check(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(opts->gemv_start_event), s, cudaEventRecordExternal), "event record");
+    launch_rht_in(L->side_v, x, w.t, w.z, w.amax, w.tsum, w.zacc, zwords, batch, s);
+    if (opts) record_event(opts->gemv_start_event, s);
     launch_gemv_imma(*L, w.t, w.amax, w.zacc, w.rows_pad, batch, s);
-    if (opts && opts->gemv_end_event)
-      cuda_check(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(opts->gemv_end_event), s, cudaEventRecordExternal), "event record");
-    float zscale[2];
-    for (int st = 0; st < 2; ++st) zscale[st] = 0.5f * L->scale[st] / 16256.f;
-    launch_rht_out(L->side_u, w.zacc, L->num_stages, w.rows_pad, zscale, w.amax, w.z, y, batch, s);
+    if (opts) record_event(opts->gemv_end_event, s);
+    float zscale[2], zbias = 0.f;
+    for (int st = 0; st < 2; ++st) zscale[st] = 0.5f * L->scale[st] / imma_limb_max(batch);
+    for (int st = 0; st < L->num_stages; ++st)
+      if (L->cb[st] == Q8P_CB_E8P_2BIT) zbias -= 0.25f * L->scale[st];  // the -T/4 of each E8P stage
+    launch_rht_out(L->side_u, w.zacc, L->num_stages, w.rows_pad, imma_limbs(batch), zscale, zbias, w.amax, w.tsum,
+                   w.z, y, batch, s);
     return;
   }
   launch_rht(L->side_v, x, w.t, batch, /*transpose=*/false, s);  // t = T_v x
-  if (opts && opts->gemv_start_event)
-    cuda_check(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(opts->gemv_start_event), s, cudaEventRecordExternal), "event record");
+  if (opts) record_event(opts->gemv_start_event, s);
   launch_gemv_simple(*L, w.t, w.z, batch, static_cast<int>(L->m), s);
-  if (opts && opts->gemv_end_event)
-    cuda_check(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(opts->gemv_end_event), s, cudaEventRecordExternal), "event record");
+  if (opts) record_event(opts->gemv_end_event, s);
   launch_rht(L->side_u, w.z, y, batch, /*transpose=*/true, s);  // y = T_u^T z
 }
 
@@ -460,12 +483,15 @@ q8p_status q8p_rht(size_t n, const uint8_t* signs, const float* x, float* y, int
                    void* stream) {
   try {
     if (!signs || !x || !y) throw q8p::ValidationError("null argument");
+    if (batch < 0) throw q8p::ValidationError("negative batch");
+    if (batch == 0) return Q8P_OK;
     const q8p::HadamardSpec spec = q8p::plan_hadamard(n);
     DevSide side;
     side.n = static_cast<std::uint32_t>(n);
     side.p = static_cast<std::uint32_t>(spec.p);
     side.q = static_cast<std::uint32_t>(spec.q);
     side.signs = signs;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
     // Per-order device copies of the base, cached per process (single device per process).
     static std::mutex mu;
     static std::vector<std::pair<std::size_t, void*>> bases;
@@ -482,7 +508,29 @@ q8p_status q8p_rht(size_t n, const uint8_t* signs, const float* x, float* y, int
         side.base = static_cast<const std::int8_t*>(d);
       }
     }
-    launch_rht(side, x, y, batch, transpose != 0, static_cast<cudaStream_t>(stream));
+    if (n % 4 != 0) {  // tiny dims (n = 1, 2): single-CTA transform
+      launch_rht(side, x, y, batch, transpose != 0, s);
+      return Q8P_OK;
+    }
+    // Scratch for the two-pass transforms (and the amax the forward pass reports).
+    struct Scratch {
+      void* p = nullptr;
+      std::size_t bytes = 0;
+    };
+    static thread_local Scratch scratch;
+    const std::size_t need = std::size_t(batch) * n * 4 + 256;
+    if (scratch.bytes < need) {
+      if (scratch.p) cudaFree(scratch.p);
+      cuda_check(cudaMalloc(&scratch.p, need), "cudaMalloc rht scratch");
+      scratch.bytes = need;
+    }
+    float* u = static_cast<float*>(scratch.p);
+    float* amax = reinterpret_cast<float*>(static_cast<std::uint8_t*>(scratch.p) + std::size_t(batch) * n * 4);
+    if (!transpose) {
+      launch_rht_in(side, x, y, u, amax, nullptr, nullptr, 0, batch, s);
+    } else {
+      launch_rht_out(side, nullptr, 1, 0, 0, nullptr, 0.f, nullptr, nullptr, u, y, batch, s, x);
+    }
     return Q8P_OK;
   } catch (...) {
     return status_of_current_exception();

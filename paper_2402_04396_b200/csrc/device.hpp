@@ -7,6 +7,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "internal.hpp"
@@ -20,16 +21,45 @@ inline void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw_cuda(e, what);
 }
 
+// Programmatic dependent launch (PDL): every q8p kernel is launched with
+// programmatic stream serialization, waits (griddepcontrol.wait) before it
+// touches its predecessor's output and then lets its own dependents start
+// (griddepcontrol.launch_dependents), so launch latency and prologues (LUT
+// build, weight prefetch) overlap the previous kernel's tail -- also inside
+// CUDA graphs.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cuda_check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "kernel launch");
+}
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" :::); }
+#endif
+
 // One side of the randomized Hadamard transform on device.
 struct DevSide {
   std::uint32_t n = 0, p = 1, q = 1;
   const std::uint8_t* signs = nullptr;  // ceil(n/8) bytes
   const std::int8_t* base = nullptr;    // q x q (+-1), nullptr when q == 1
+  const float* colsum = nullptr;        // q column sums of the base (sum_i t_i in closed form)
 };
 
 // Fast-path (IMMA GEMV) transcoded code tiles, see gemv_imma.cu.
 struct TileCodes {
   void* tiles = nullptr;      // [row_tile][k_step][2 halves][32 lanes][16 B]
+  void* shifts = nullptr;     // [row_tile][k_step][32 lanes] u16 shift bits (E8P)
   std::uint32_t row_tiles = 0, k_steps = 0;
 };
 
@@ -72,15 +102,21 @@ void launch_decode(const q8p_layer& L, int stage, float* w, cudaStream_t s);
 // Tensor-core path (gemv_imma.cu, kernels_rht.cu).
 void imma_tables(std::vector<std::uint32_t>& e8p, std::vector<std::uint32_t>& e81);
 std::size_t imma_tile_bytes(std::uint32_t m_local, std::uint32_t n, int kind);
+std::size_t imma_shift_bytes(std::uint32_t m_local, std::uint32_t n, int kind);
 void imma_transcode(const std::uint16_t* codes, std::uint32_t m_local, std::uint32_t n, int kind,
-                    std::uint8_t* out);
+                    std::uint8_t* out, std::uint8_t* shifts);
 bool imma_supported(const q8p_layer& L, int batch);
+int imma_limbs(int batch);         // int8 activation limbs per vector (MMA columns)
+float imma_limb_max(int batch);    // 127 * 128^(limbs - 1)
 void launch_gemv_imma(const q8p_layer& L, const float* t, const float* amax, std::int32_t* zacc,
                       std::uint32_t rows_pad, int batch, cudaStream_t s);
-void launch_rht_in(const DevSide& side, const float* x, float* t, float* u_scratch, float* amax,
+// K1: t = T_v x (+ amax of t, tsum = sum_i t_i, zeroed accumulators when zero_ptr).
+void launch_rht_in(const DevSide& side, const float* x, float* t, float* u_scratch, float* amax, float* tsum,
                    std::int32_t* zero_ptr, std::size_t zero_words, int batch, cudaStream_t s);
+// K3: y = T_u^T z, z = sum_s zscale_s amax (128 hi + lo) + zbias * tsum from the
+// int32 accumulators, or z = zin (fp32) when zacc is null.
 void launch_rht_out(const DevSide& side, const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows,
-                    const float zscale[2], const float* amax, float* u_scratch, float* y, int batch,
-                    cudaStream_t s);
+                    int limbs, const float zscale[2], float zbias, const float* amax, const float* tsum, float* u_scratch,
+                    float* y, int batch, cudaStream_t s, const float* zin = nullptr);
 
 }  // namespace q8p::detail

@@ -2,307 +2,348 @@
 //
 // SideTransform (core/src/transforms.cpp:28-47) with had_apply
 // (core/src/hadamard.cpp:170-210):  H = (H_p (x) B_q) / sqrt(n), flat index
-// i = a * q + b.  The two Kronecker factors act on different index digits
-// and commute, so each side is split into two embarrassingly parallel
-// passes over HBM/L2-resident fp32 vectors:
-//   base pass  (I (x) B_q):   rows a split across CTAs, q x q +-1 products
-//   fwht pass  (H_p (x) I):   columns b split across CTAs, in-smem FWHT
-// K1 (input side):   x --signs--> [base] --> fwht --> t, amax(|t|) per vector
-// K3 (output side):  z_acc(int32 limbs) --> fwht --> [base^T] --signs--> y
-// For q == 1 there is no base pass.  K1 also zeroes the GEMV's int32
-// accumulators (extra CTAs), K3 consumes them.
+// i = a * q + b.  Split a = a_hi * P2 + a_lo.  The Kronecker factors act on
+// different index digits and commute, so each side is two passes, each one
+// kernel over many small CTAs (a 1-CTA transform of a 32-112 KB vector is
+// latency-bound at several microseconds on B200):
+//   pass 1  CTA = one contiguous chunk [a_hi][0..P2)[0..q):
+//           signs (fwd) | int32-limb -> fp32 (K3), base B_q (or B_q^T) on each
+//           q-row, FWHT over a_lo (stride q)
+//   pass 2  CTA = 4 adjacent columns (a_lo, b) x all P1 = p / P2 values of a_hi:
+//           FWHT over a_hi, 1/sqrt(n), signs (K3) / amax of t (K1)
+// K1 also zeroes the GEMV's int32 accumulators; K3 consumes them.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "device.hpp"
 
 namespace q8p::detail {
 namespace {
 
-constexpr int kThreads = 1024;
-
-__device__ __forceinline__ bool sign_bit(const std::uint8_t* s, std::uint32_t i) {
-  return (s[i >> 3] >> (i & 7)) & 1;
-}
-
 __device__ __forceinline__ void atomic_max_pos(float* addr, float v) {
   // |t| >= 0: IEEE ordering of non-negative floats equals their int ordering.
   atomicMax(reinterpret_cast<int*>(addr), __float_as_int(v));
 }
 
-__device__ __forceinline__ float block_reduce_max(float v, float* red) {
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) red[w] = v;
+__device__ __forceinline__ float4 sign4(float4 v, std::uint32_t nib) {
+  if (nib & 1) v.x = -v.x;
+  if (nib & 2) v.y = -v.y;
+  if (nib & 4) v.z = -v.z;
+  if (nib & 8) v.w = -v.w;
+  return v;
+}
+
+// Radix-2^R FWHT pass over index bits [sbit, sbit + R) of the row index of an
+// smem matrix with `rows` rows of Q floats (row stride Q): each task loads 2^R
+// elements, does R butterfly stages in registers, stores them back.
+template <int R, int Q>
+__device__ __forceinline__ void fwht_pass(float* s, std::uint32_t rows, std::uint32_t sbit) {
+  constexpr int K = 1 << R;
+  const std::uint32_t tasks = (rows >> R) * Q;
+  const std::uint32_t lowmask = (1u << sbit) - 1;
+  for (std::uint32_t t = threadIdx.x; t < tasks; t += blockDim.x) {
+    const std::uint32_t b = t % Q, tr = t / Q;
+    const std::uint32_t base = ((((tr >> sbit) << (sbit + R)) | (tr & lowmask)) * Q) + b;
+    float v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = s[base + ((std::uint32_t(k) << sbit) * Q)];
+#pragma unroll
+    for (int len = 1; len < K; len <<= 1)
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (!(k & len)) {
+          const float x = v[k], y = v[k + len];
+          v[k] = x + y;
+          v[k + len] = x - y;
+        }
+#pragma unroll
+    for (int k = 0; k < K; ++k) s[base + ((std::uint32_t(k) << sbit) * Q)] = v[k];
+  }
   __syncthreads();
-  if (w == 0) {
-    v = l < int(blockDim.x >> 5) ? red[l] : 0.f;
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  }
-  return v;  // valid in thread 0
 }
 
-// In-smem unnormalized FWHT over `p` rows of `cw` contiguous floats each
-// (row stride cw): butterflies between rows k and k + len.
-__device__ void smem_fwht(float* s, std::uint32_t p, std::uint32_t cw) {
-  const std::uint32_t half = (p >> 1) * cw;
-  for (std::uint32_t len = 1; len < p; len <<= 1) {
-    for (std::uint32_t t = threadIdx.x; t < half; t += blockDim.x) {
-      const std::uint32_t pair = t / cw, j = t - pair * cw;
-      const std::uint32_t blk = pair / len, off = pair - blk * len;
-      const std::uint32_t k = blk * 2 * len + off;
-      const float u = s[k * cw + j], v = s[(k + len) * cw + j];
-      s[k * cw + j] = u + v;
-      s[(k + len) * cw + j] = u - v;
-    }
-    __syncthreads();
+template <int Q>
+__device__ void fwht_rows(float* s, std::uint32_t rows) {
+  const std::uint32_t lb = 31 - __clz(rows);
+  std::uint32_t b = 0;
+  for (; b + 3 <= lb; b += 3) fwht_pass<3, Q>(s, rows, b);
+  if (b + 2 <= lb) {
+    fwht_pass<2, Q>(s, rows, b);
+    b += 2;
   }
+  if (b + 1 <= lb) fwht_pass<1, Q>(s, rows, b);
 }
 
-struct FwhtArgs {
-  std::uint32_t n, p, q;
-  std::uint32_t cols_per_cta;        // columns b handled by one CTA
-  const std::uint8_t* signs;         // applied on input (fwd, q == 1) or output (trans, q == 1)
-  const float* in;                   // fp32 input [batch][n] (fwd) / u (trans, q > 1 second pass input unused)
-  const std::int32_t* zacc;          // trans: int32 limb accumulators [stages][batch*2][rows_pad]
-  int zacc_stages;
-  std::uint32_t zacc_rows;           // rows_pad
-  const float* amax;                 // trans: per-vector amax of t (limb scale source)
-  float zscale[2];                   // trans: per-stage 0.5 * stage_scale / 16256
-  float* out;                        // [batch][n]
-  float* amax_out;                   // fwd: per-vector amax (atomicMax; zeroed by caller pass)
-  std::int32_t* zero_ptr;            // fwd: buffer to zero with spare CTAs
+struct RhtArgs {
+  std::uint32_t n, p, q, P2, P1;
+  const std::uint8_t* signs;   // ceil(n/8) bytes, LSB-first, bit set = -1
+  const std::int8_t* base;     // q x q (+-1) when q > 1
+  const float* in;             // pass 1 fp32 input [batch][n] (or nullptr with zacc)
+  const std::int32_t* zacc;    // K3 pass 1: int32 limb accumulators [stage][8][zrows]
+  std::uint32_t zrows;
+  int zstages;
+  int limbs;                   // K3: activation limbs per vector (zacc columns L*b .. L*b+L-1)
+  float zscale0, zscale1;      // 0.5 * stage_scale / limb_max
+  const float* amax_in;        // K3: per-vector amax of t
+  const float* tsum_in;        // K3: per-vector sum of t
+  float zbias;                 // K3: z += zbias * tsum
+  const float* colsum;         // K1: base column sums (q floats)
+  float* tsum_out;             // K1: per-vector sum of t (closed form, pass-1 CTA 0)
+  float* mid;                  // [batch][n] intermediate
+  float* out;                  // [batch][n]
+  float* amax_out;             // K1: per-vector amax (zeroed in pass 1, atomicMax in pass 2)
+  std::int32_t* zero_ptr;      // K1: accumulators to zero (pass-1 spare CTAs)
   std::size_t zero_words;
-  float out_scale;                   // 1/sqrt(n) applied on output
-  int fwd;                           // 1 = K1 (input side), 0 = K3
+  int batch;
+  int fwd;
 };
 
-// FWHT pass.  grid = (ceil(q / cols_per_cta) [+ zero CTAs], batch).
-__global__ void __launch_bounds__(kThreads) fwht_kernel(FwhtArgs a) {
-  extern __shared__ float s[];
-  __shared__ float red[32];
-  const std::uint32_t ncta_cols = (a.q + a.cols_per_cta - 1) / a.cols_per_cta;
+constexpr int kP1Threads = 256;
+
+// Pass 1.  grid = (P1 chunks [+ zeroing CTAs], batch).
+template <int Q>
+__global__ void __launch_bounds__(kP1Threads) rht_pass1(RhtArgs a) {
+  extern __shared__ __align__(16) float sm1[];
   const int b = blockIdx.y;
-  if (blockIdx.x >= ncta_cols) {
-    // Spare CTAs: zero the GEMV accumulators (only with the first vector's grid row).
+  pdl_wait();
+  pdl_trigger();
+  if (blockIdx.x >= a.P1) {
     if (b == 0 && a.zero_ptr) {
-      const std::size_t nz = gridDim.x - ncta_cols;
-      for (std::size_t i = (blockIdx.x - ncta_cols) * std::size_t(blockDim.x) + threadIdx.x; i < a.zero_words;
+      const std::size_t nz = gridDim.x - a.P1;
+      int4* zp = reinterpret_cast<int4*>(a.zero_ptr);
+      for (std::size_t i = (blockIdx.x - a.P1) * std::size_t(blockDim.x) + threadIdx.x; i < a.zero_words / 4;
            i += nz * blockDim.x)
-        a.zero_ptr[i] = 0;
+        zp[i] = make_int4(0, 0, 0, 0);
     }
     return;
   }
-  const std::uint32_t c0 = blockIdx.x * a.cols_per_cta;
-  const std::uint32_t cw = min(a.cols_per_cta, a.q - c0);
-  const std::uint32_t n = a.n, q = a.q;
-  // Load [p][cw] sub-block.
-  for (std::uint32_t e = threadIdx.x; e < a.p * cw; e += blockDim.x) {
-    const std::uint32_t r = e / cw, j = e - r * cw;
-    const std::uint32_t i = r * q + c0 + j;
-    float v;
-    if (a.fwd) {
-      v = a.in[std::size_t(b) * n + i];
-      if (q == 1 && sign_bit(a.signs, i)) v = -v;
-    } else if (a.zacc) {
-      // z = sum_s zscale_s * amax * (128 * hi + lo)   (limb recombination)
-      const float am = a.amax[b];
-      double acc = 0.0;
-      for (int st = 0; st < a.zacc_stages; ++st) {
-        const std::int32_t* z = a.zacc + (std::size_t(st) * 8 + 2 * b) * a.zacc_rows;
-        acc += double(a.zscale[st]) * (128.0 * double(z[i]) + double(z[a.zacc_rows + i]));
+  if (a.fwd && blockIdx.x == 0) {
+    if (a.amax_out && threadIdx.x == 0) a.amax_out[b] = 0.f;
+    // sum_i t_i = (p / sqrt(n)) sum_{b' < q} colsum[b'] s_b' x_b'  (Sylvester columns sum to p * delta)
+    if (a.tsum_out && threadIdx.x == 32) {
+      float acc = 0.f;
+      for (std::uint32_t j = 0; j < Q; ++j) {
+        float v = a.in[std::size_t(b) * a.n + j];
+        if ((a.signs[j >> 3] >> (j & 7)) & 1) v = -v;
+        acc += a.colsum[j] * v;
       }
-      v = float(acc * double(am));
-    } else {
-      v = a.in[std::size_t(b) * n + i];
+      a.tsum_out[b] = acc * float(a.p) * rsqrtf(float(a.n));
     }
-    s[r * cw + j] = v;
+  }
+  const std::uint32_t chunk = a.P2 * Q;  // floats, multiple of 4
+  const std::uint32_t e0 = blockIdx.x * chunk;
+  float* x = sm1;                         // [P2][Q]
+  float* y = sm1 + chunk;                 // base output (Q > 1)
+  float* Bs = sm1 + 2 * chunk;            // Q x Q base as float (Q <= 28) / int8 (Q = 172)
+  if constexpr (Q > 1) {
+    if constexpr (Q <= 28) {
+      for (std::uint32_t i = threadIdx.x; i < Q * Q; i += blockDim.x) Bs[i] = float(a.base[i]);
+    } else {
+      std::int8_t* B8 = reinterpret_cast<std::int8_t*>(Bs);
+      for (std::uint32_t i = threadIdx.x; i < Q * Q / 4; i += blockDim.x)
+        reinterpret_cast<std::uint32_t*>(B8)[i] = reinterpret_cast<const std::uint32_t*>(a.base)[i];
+    }
+  }
+  // load (float4, contiguous chunk)
+  for (std::uint32_t v = threadIdx.x; v < chunk / 4; v += blockDim.x) {
+    const std::uint32_t i = e0 + 4 * v;
+    float4 val;
+    if (a.zacc) {
+      const float am = a.amax_in[b];
+      const int L = a.limbs;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int st = 0; st < a.zstages; ++st) {
+        const std::int32_t* z = a.zacc + (std::size_t(st) * 8 + L * b) * a.zrows;
+        float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int l = 0; l < L; ++l) {  // limb weights 128^(L-1-l), Horner
+          const int4 v = *reinterpret_cast<const int4*>(z + std::size_t(l) * a.zrows + i);
+          c = make_float4(128.f * c.x + float(v.x), 128.f * c.y + float(v.y), 128.f * c.z + float(v.z),
+                          128.f * c.w + float(v.w));
+        }
+        const float zs = st == 0 ? a.zscale0 : a.zscale1;
+        acc = make_float4(acc.x + zs * c.x, acc.y + zs * c.y, acc.z + zs * c.z, acc.w + zs * c.w);
+      }
+      const float bias = a.zbias * a.tsum_in[b];
+      val = make_float4(acc.x * am + bias, acc.y * am + bias, acc.z * am + bias, acc.w * am + bias);
+    } else {
+      val = *reinterpret_cast<const float4*>(a.in + std::size_t(b) * a.n + i);
+      if (a.fwd) val = sign4(val, (a.signs[i >> 3] >> (i & 4)) & 0xFu);
+    }
+    reinterpret_cast<float4*>(x)[v] = val;
   }
   __syncthreads();
-  smem_fwht(s, a.p, cw);
+  float* cur = x;
+  if constexpr (Q > 1) {
+    // base along each contiguous q-row: y[r][c] = sum_k B[c][k] x[r][k] (fwd) or B[k][c] (K3)
+    for (std::uint32_t e = threadIdx.x; e < chunk; e += blockDim.x) {
+      const std::uint32_t r = e / Q, c = e - r * Q;
+      const float* xr = x + r * Q;
+      float acc = 0.f;
+      if constexpr (Q <= 28) {
+        if (a.fwd) {
+#pragma unroll 4
+          for (int k = 0; k < Q; ++k) acc += Bs[c * Q + k] * xr[k];
+        } else {
+#pragma unroll 4
+          for (int k = 0; k < Q; ++k) acc += Bs[k * Q + c] * xr[k];
+        }
+      } else {
+        const std::int8_t* B8 = reinterpret_cast<const std::int8_t*>(Bs);
+        if (a.fwd) {
+#pragma unroll 4
+          for (int k = 0; k < Q; ++k) acc += float(B8[c * Q + k]) * xr[k];
+        } else {
+#pragma unroll 4
+          for (int k = 0; k < Q; ++k) acc += float(B8[k * Q + c]) * xr[k];
+        }
+      }
+      y[e] = acc;
+    }
+    __syncthreads();
+    cur = y;
+  }
+  fwht_rows<Q>(cur, a.P2);
+  for (std::uint32_t v = threadIdx.x; v < chunk / 4; v += blockDim.x)
+    *reinterpret_cast<float4*>(a.mid + std::size_t(b) * a.n + e0 + 4 * v) = reinterpret_cast<float4*>(cur)[v];
+}
+
+// Pass 2.  grid = (P2 * q / 4 column groups, batch); block = 128 threads.
+__global__ void __launch_bounds__(128) rht_pass2(RhtArgs a) {
+  extern __shared__ __align__(16) float sm2[];
+  __shared__ float red[4];
+  const int b = blockIdx.y;
+  pdl_wait();
+  pdl_trigger();
+  const std::uint32_t stride = a.P2 * a.q;          // elements between consecutive a_hi
+  const std::uint32_t col = blockIdx.x * 4;         // 4 adjacent columns
+  for (std::uint32_t r = threadIdx.x; r < a.P1; r += blockDim.x)
+    reinterpret_cast<float4*>(sm2)[r] =
+        *reinterpret_cast<const float4*>(a.mid + std::size_t(b) * a.n + std::size_t(r) * stride + col);
+  __syncthreads();
+  fwht_rows<4>(sm2, a.P1);
+  const float sc = rsqrtf(float(a.n));
   float mx = 0.f;
-  for (std::uint32_t e = threadIdx.x; e < a.p * cw; e += blockDim.x) {
-    const std::uint32_t r = e / cw, j = e - r * cw;
-    const std::uint32_t i = r * q + c0 + j;
-    float v = s[r * cw + j] * a.out_scale;
-    if (!a.fwd && q == 1 && sign_bit(a.signs, i)) v = -v;
-    a.out[std::size_t(b) * n + i] = v;
-    mx = fmaxf(mx, fabsf(v));
+  for (std::uint32_t r = threadIdx.x; r < a.P1; r += blockDim.x) {
+    const std::uint32_t i = r * stride + col;
+    float4 v = reinterpret_cast<float4*>(sm2)[r];
+    v = make_float4(v.x * sc, v.y * sc, v.z * sc, v.w * sc);
+    if (!a.fwd) v = sign4(v, (a.signs[i >> 3] >> (i & 4)) & 0xFu);
+    *reinterpret_cast<float4*>(a.out + std::size_t(b) * a.n + i) = v;
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
   }
   if (a.fwd && a.amax_out) {
-    mx = block_reduce_max(mx, red);
-    if (threadIdx.x == 0) atomic_max_pos(a.amax_out + b, mx);
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const float m = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+      atomic_max_pos(a.amax_out + b, m);
+    }
   }
 }
 
-struct BaseArgs {
-  std::uint32_t n, p, q;
-  std::uint32_t rows_per_cta;
-  const std::int8_t* base;   // q x q
-  const std::uint8_t* signs;
-  const float* in;
-  float* out;
-  float out_scale;           // 1/sqrt(n) (trans) or 1 (fwd)
-  float* amax_zero;          // fwd: zero the per-vector amax (CTA 0)
-  int batch;
-  int fwd;                   // 1: y = B (S o x) per row ; 0: y = S o (B^T x) * scale
-};
-
-// Base pass: rows a in [a0, a0 + rows_per_cta) of one vector per grid row.
-// The +-1 base is staged in smem as float (q <= 28) or int8 (q = 172).
-template <typename BT>
-__global__ void __launch_bounds__(256) base_kernel(BaseArgs a) {
-  extern __shared__ float sm[];
-  const std::uint32_t q = a.q, n = a.n;
-  BT* B = reinterpret_cast<BT*>(sm);
-  float* seg = sm + (q * q * sizeof(BT) + 15) / 16 * 4;
-  const int b = blockIdx.y;
-  if (a.fwd && a.amax_zero && blockIdx.x == 0 && threadIdx.x < a.batch && b == 0) a.amax_zero[threadIdx.x] = 0.f;
-  for (std::uint32_t i = threadIdx.x; i < q * q; i += blockDim.x) B[i] = BT(a.base[i]);
-  const std::uint32_t r0 = blockIdx.x * a.rows_per_cta;
-  const std::uint32_t nr = min(a.rows_per_cta, a.p - r0);
-  for (std::uint32_t e = threadIdx.x; e < nr * q; e += blockDim.x) {
-    const std::uint32_t i = r0 * q + e;
-    float v = a.in[std::size_t(b) * n + i];
-    if (a.fwd && sign_bit(a.signs, i)) v = -v;
-    seg[e] = v;
-  }
-  __syncthreads();
-  for (std::uint32_t e = threadIdx.x; e < nr * q; e += blockDim.x) {
-    const std::uint32_t r = e / q, c = e - r * q;
-    const float* x = seg + r * q;
-    float acc = 0.f;
-    if (a.fwd)
-      for (std::uint32_t k = 0; k < q; ++k) acc += float(B[c * q + k]) * x[k];
-    else
-      for (std::uint32_t k = 0; k < q; ++k) acc += float(B[k * q + c]) * x[k];
-    acc *= a.out_scale;
-    const std::uint32_t i = (r0 + r) * q + c;
-    if (!a.fwd && sign_bit(a.signs, i)) acc = -acc;
-    a.out[std::size_t(b) * n + i] = acc;
-  }
+void plan_split(const DevSide& side, RhtArgs& a) {
+  a.n = side.n;
+  a.p = side.p;
+  a.q = side.q;
+  // pass-1 chunk P2 * q: ~1K floats (<= 512 for the order-172 base, whose
+  // dense product dominates pass 1)
+  const std::uint32_t target = side.q > 28 ? 512 : 1024;
+  std::uint32_t P2 = 1;
+  while (P2 * 2 <= side.p && P2 * 2 * side.q <= target) P2 *= 2;
+  if ((P2 * side.q) % 4 != 0) throw SizeError("rht: dimension too small for the float4 passes");
+  a.P2 = P2;
+  a.P1 = side.p / P2;
+  if (std::size_t(a.P1) * 16 > 96 * 1024) throw SizeError("rht: dimension too large");
 }
 
-void set_smem(const void* fn, std::size_t bytes) {
-  cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)), "smem attr");
-}
-
-std::uint32_t fwht_cols_per_cta(const DevSide& side) {
-  if (side.q == 1) {
-    if (side.p * 4 > 200 * 1024) throw SizeError("rht: power-of-two factor too large for one CTA");
-    return 1;
-  }
-  return side.q % 4 == 0 ? 4 : 1;  // 16-byte row segments per CTA
-}
-
-void launch_base(const DevSide& side, BaseArgs a, int batch, cudaStream_t s) {
-  a.rows_per_cta = std::max<std::uint32_t>(1, 256 / side.q);
-  const bool fl = side.q <= 28;
-  const std::size_t bsz = fl ? side.q * side.q * 4 : side.q * side.q;
-  const std::size_t smem = (bsz + 15) / 16 * 16 + std::size_t(a.rows_per_cta) * side.q * 4;
+template <int Q>
+void launch_pass1_q(const RhtArgs& a, std::uint32_t extra_ctas, cudaStream_t s) {
+  const std::size_t chunk = std::size_t(a.P2) * Q;
+  const std::size_t bsz = Q == 1 ? 0 : (Q <= 28 ? Q * Q * 4 : (Q * Q + 15) / 16 * 16);
+  const std::size_t smem = chunk * 4 * (Q > 1 ? 2 : 1) + bsz;
   static std::once_flag once;
   std::call_once(once, [] {
-    set_smem(reinterpret_cast<const void*>(base_kernel<float>), 200 * 1024);
-    set_smem(reinterpret_cast<const void*>(base_kernel<std::int8_t>), 200 * 1024);
+    cuda_check(cudaFuncSetAttribute(rht_pass1<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
+               "rht smem attr");
   });
-  dim3 grid((side.p + a.rows_per_cta - 1) / a.rows_per_cta, batch);
-  if (fl)
-    base_kernel<float><<<grid, 256, smem, s>>>(a);
-  else
-    base_kernel<std::int8_t><<<grid, 256, smem, s>>>(a);
-  cuda_check(cudaGetLastError(), "base launch");
+  launch_pdl(rht_pass1<Q>, dim3(a.P1 + extra_ctas, a.batch), dim3(kP1Threads), smem, s, a);
+}
+
+void launch_pass1(const RhtArgs& a, std::uint32_t extra, cudaStream_t s) {
+  switch (a.q) {
+    case 1: launch_pass1_q<1>(a, extra, s); break;
+    case 4: launch_pass1_q<4>(a, extra, s); break;
+    case 12: launch_pass1_q<12>(a, extra, s); break;
+    case 20: launch_pass1_q<20>(a, extra, s); break;
+    case 28: launch_pass1_q<28>(a, extra, s); break;
+    case 172: launch_pass1_q<172>(a, extra, s); break;
+    default: throw SizeError("rht: unsupported base order");
+  }
+  cuda_check(cudaGetLastError(), "rht pass1 launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
+void launch_pass2(const RhtArgs& a, cudaStream_t s) {
+  const std::uint32_t groups = a.P2 * a.q / 4;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cuda_check(cudaFuncSetAttribute(rht_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
+               "rht smem attr");
+  });
+  launch_pdl(rht_pass2, dim3(groups, a.batch), dim3(128), std::size_t(a.P1) * 16, s, a);
+  cuda_check(cudaGetLastError(), "rht pass2 launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
 
 }  // namespace
 
-void launch_rht_in(const DevSide& side, const float* x, float* t, float* u_scratch, float* amax,
+void launch_rht_in(const DevSide& side, const float* x, float* t, float* u_scratch, float* amax, float* tsum,
                    std::int32_t* zero_ptr, std::size_t zero_words, int batch, cudaStream_t s) {
   if (batch <= 0) return;
-  const float scale = rsqrtf(float(side.n));
-  const float* fw_in = x;
-  if (side.q > 1) {
-    BaseArgs a{};
-    a.n = side.n;
-    a.p = side.p;
-    a.q = side.q;
-    a.base = side.base;
-    a.signs = side.signs;
-    a.in = x;
-    a.out = u_scratch;
-    a.out_scale = 1.f;
-    a.amax_zero = amax;
-    a.batch = batch;
-    a.fwd = 1;
-    launch_base(side, a, batch, s);
-    fw_in = u_scratch;
-  } else {
-    cuda_check(cudaMemsetAsync(amax, 0, sizeof(float) * batch, s), "amax zero");
-  }
-  FwhtArgs a{};
-  a.n = side.n;
-  a.p = side.p;
-  a.q = side.q;
-  a.cols_per_cta = fwht_cols_per_cta(side);
+  RhtArgs a{};
+  plan_split(side, a);
   a.signs = side.signs;
-  a.in = fw_in;
+  a.base = side.base;
+  a.in = x;
+  a.mid = u_scratch;
   a.out = t;
   a.amax_out = amax;
+  a.tsum_out = tsum;
+  a.colsum = side.colsum;
   a.zero_ptr = zero_ptr;
   a.zero_words = zero_words;
-  a.out_scale = scale;
+  a.batch = batch;
   a.fwd = 1;
-  const std::uint32_t ncols = (side.q + a.cols_per_cta - 1) / a.cols_per_cta;
-  const std::uint32_t zero_ctas = zero_ptr && zero_words ? 16 : 0;
-  const std::size_t smem = std::size_t(side.p) * std::min(a.cols_per_cta, side.q) * 4;
-  static std::once_flag once;
-  std::call_once(once, [] { set_smem(reinterpret_cast<const void*>(fwht_kernel), 200 * 1024); });
-  fwht_kernel<<<dim3(ncols + zero_ctas, batch), kThreads, smem, s>>>(a);
-  cuda_check(cudaGetLastError(), "fwht launch");
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  launch_pass1(a, zero_ptr && zero_words ? 32 : 0, s);
+  launch_pass2(a, s);
 }
 
 void launch_rht_out(const DevSide& side, const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows,
-                    const float zscale[2], const float* amax, float* u_scratch, float* y, int batch,
-                    cudaStream_t s) {
+                    int limbs, const float zscale[2], float zbias, const float* amax, const float* tsum, float* u_scratch,
+                    float* y, int batch, cudaStream_t s, const float* zin) {
   if (batch <= 0) return;
-  const float scale = rsqrtf(float(side.n));
-  FwhtArgs a{};
-  a.n = side.n;
-  a.p = side.p;
-  a.q = side.q;
-  a.cols_per_cta = fwht_cols_per_cta(side);
+  RhtArgs a{};
+  plan_split(side, a);
   a.signs = side.signs;
+  a.base = side.base;
+  a.in = zin;
   a.zacc = zacc;
-  a.zacc_stages = zacc_stages;
-  a.zacc_rows = zacc_rows;
-  a.amax = amax;
-  a.zscale[0] = zscale[0];
-  a.zscale[1] = zscale[1];
-  a.out = side.q > 1 ? u_scratch : y;
-  a.out_scale = side.q > 1 ? 1.f : scale;
+  a.zrows = zacc_rows;
+  a.zstages = zacc_stages;
+  a.limbs = limbs;
+  a.zscale0 = zscale ? zscale[0] : 0.f;
+  a.zscale1 = zscale ? zscale[1] : 0.f;
+  a.amax_in = amax;
+  a.tsum_in = tsum;
+  a.zbias = zbias;
+  a.mid = u_scratch;
+  a.out = y;
+  a.batch = batch;
   a.fwd = 0;
-  const std::uint32_t ncols = (side.q + a.cols_per_cta - 1) / a.cols_per_cta;
-  const std::size_t smem = std::size_t(side.p) * std::min(a.cols_per_cta, side.q) * 4;
-  static std::once_flag once;
-  std::call_once(once, [] { set_smem(reinterpret_cast<const void*>(fwht_kernel), 200 * 1024); });
-  fwht_kernel<<<dim3(ncols, batch), kThreads, smem, s>>>(a);
-  cuda_check(cudaGetLastError(), "fwht launch");
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (side.q > 1) {
-    BaseArgs bb{};
-    bb.n = side.n;
-    bb.p = side.p;
-    bb.q = side.q;
-    bb.base = side.base;
-    bb.signs = side.signs;
-    bb.in = u_scratch;
-    bb.out = y;
-    bb.out_scale = scale;
-    bb.batch = batch;
-    bb.fwd = 0;
-    launch_base(side, bb, batch, s);
-  }
+  launch_pass1(a, 0, s);
+  launch_pass2(a, s);
 }
 
 }  // namespace q8p::detail
