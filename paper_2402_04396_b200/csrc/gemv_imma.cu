@@ -57,7 +57,10 @@ constexpr int kChunk = 8;        // k-steps per B chunk
 constexpr int kMaxChunks = 2;    // B chunks resident per CTA
 constexpr int kBWords = 20;      // u32 per (k-step, lane) in the B smem image (18 used)
 constexpr std::size_t kBBytes = std::size_t(kMaxChunks) * kChunk * 32 * kBWords * 4;  // 40 KiB
-constexpr std::size_t kSmemBytes = 128 * 1024 + 1024;  // 64-KiB-aligned LUT window + B images
+constexpr int kMaxUnits = 40;    // per-warp unit list capacity (host sizes the grid to fit)
+constexpr std::size_t kListBytes = 32 * kMaxUnits * 16;  // 20 KiB (32 warps)
+constexpr std::size_t kSmemBytes = 128 * 1024 + 1024;  // 64-KiB-aligned LUT window + B images + lists
+static_assert(kBBytes + kListBytes <= 63 * 1024, "B images + unit lists must fit below the LUT window");
 __host__ __device__ constexpr float limb_max(int L) { return L == 3 ? 2080768.f : 16256.f; }  // 127*128^(L-1)
 
 template <int STAGES>
@@ -240,7 +243,8 @@ __global__ void __launch_bounds__(Cfg<STAGES>::kThreads, 1) gemv_imma_kernel(Imm
   const std::uint32_t sbase = static_cast<std::uint32_t>(__cvta_generic_to_shared(smem));
   const std::uint32_t lutw = (sbase + 0xFFFFu) & ~0xFFFFu;
   char* lut = smem + (lutw - sbase);
-  std::uint32_t* bsm = reinterpret_cast<std::uint32_t*>(lutw - sbase >= kBBytes ? smem : lut + 65536);
+  std::uint32_t* bsm =
+      reinterpret_cast<std::uint32_t*>(lutw - sbase >= kBBytes + kListBytes ? smem : lut + 65536);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const std::uint32_t W = gridDim.x * kWarps;
   const std::uint32_t gw = blockIdx.x * kWarps + warp;
@@ -248,6 +252,26 @@ __global__ void __launch_bounds__(Cfg<STAGES>::kThreads, 1) gemv_imma_kernel(Imm
   const std::uint32_t u1 = std::uint32_t((std::uint64_t(a.units) * (gw + 1)) / W);
   const std::uint32_t cu0 = std::uint32_t((std::uint64_t(a.units) * (blockIdx.x * kWarps)) / W);
   const std::uint32_t cu1 = std::uint32_t((std::uint64_t(a.units) * ((blockIdx.x + 1) * kWarps)) / W);
+
+  // ---- per-warp unit lists (tile index, B-image offset, row tile) ---------
+  // Built once by lane 0 of each warp; the main loop then reads one broadcast
+  // 16-B entry per unit instead of walking a cursor (keeps the loop branch-light).
+  std::uint32_t rt_, ks_, kc_lo, kc_hi;
+  unit_coords(a, cu0, rt_, ks_, kc_lo);
+  unit_coords(a, cu1 > cu0 ? cu1 - 1 : cu0, rt_, ks_, kc_hi);
+  const std::uint32_t nchunk = kc_hi - kc_lo + 1;  // <= kMaxChunks (host guarantees)
+  uint4* lists = reinterpret_cast<uint4*>(bsm + kBBytes / 4);
+  uint4* list = lists + warp * kMaxUnits;
+  const int nu = int(u1 - u0);  // <= kMaxUnits (host guarantees)
+  if (lane == 0 && nu > 0) {
+    Cursor c;
+    c.init(a, u0);
+    for (int i = 0; i < nu; ++i) {
+      list[i] = make_uint4(c.tile(a), ((c.kc - kc_lo) * kChunk + c.ksl) * 32 * kBWords, c.rt, 0);
+      c.next(a);
+    }
+  }
+  __syncwarp();
 
   // ---- prefetch the first code units (overlaps the prologue) -------------
   uint4 pc0[kPrefetch][2];
@@ -271,16 +295,9 @@ __global__ void __launch_bounds__(Cfg<STAGES>::kThreads, 1) gemv_imma_kernel(Imm
       }
     }
   };
-  Cursor pc;  // prefetch cursor
-  pc.init(a, u0 < u1 ? u0 : 0);
-  std::uint32_t last_tile = pc.tile(a);
+  if (nu > 0) {
 #pragma unroll
-  for (int i = 0; i < kPrefetch; ++i) {
-    if (u0 + i < u1) {
-      last_tile = pc.tile(a);
-      pc.next(a);
-    }
-    load_unit(i, last_tile);
+    for (int i = 0; i < kPrefetch; ++i) load_unit(i, list[i < nu ? i : nu - 1].x);
   }
 
   // ---- LUTs: E8P nibbles replicated per lane (bytes [0,128) of each 256-B row),
@@ -302,10 +319,6 @@ __global__ void __launch_bounds__(Cfg<STAGES>::kThreads, 1) gemv_imma_kernel(Imm
   }
 
   // ---- B images for the CTA's k-chunks ------------------------------------
-  std::uint32_t rt_, ks_, kc_lo, kc_hi;
-  unit_coords(a, cu0, rt_, ks_, kc_lo);
-  unit_coords(a, cu1 > cu0 ? cu1 - 1 : cu0, rt_, ks_, kc_hi);
-  const std::uint32_t nchunk = kc_hi - kc_lo + 1;  // <= kMaxChunks (host guarantees)
   for (std::uint32_t i = threadIdx.x; i < nchunk * kChunk * 32 * kBWords / 4; i += kThreads)
     reinterpret_cast<uint4*>(bsm)[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
@@ -387,25 +400,25 @@ __global__ void __launch_bounds__(Cfg<STAGES>::kThreads, 1) gemv_imma_kernel(Imm
   const std::uint32_t lb8 = (lutw & 0xFFFF0000u) | (128u + std::uint32_t(lane & 15) * 8u);
   int acc0[4] = {0, 0, 0, 0};
   int acc1[4] = {0, 0, 0, 0};
-  std::uint32_t cur_rt = 0xFFFFFFFFu;
   const int g = lane >> 2, tq = lane & 3;
   const int ncols = a.limbs * a.batch;  // used B/C columns
+  const bool w0 = 2 * tq < ncols, w1 = 2 * tq + 1 < ncols;
+  std::int32_t* zrow = a.zacc + std::size_t(2 * tq) * a.rows_pad + g;
 
-  auto flush = [&]() {
+  auto flush = [&](std::uint32_t rt) {
     if (Q8P_EXP_MODE == 4 && acc0[0] != 12345) return;
-    if (cur_rt != 0xFFFFFFFFu && 2 * tq < ncols) {
-      const std::uint32_t r0 = cur_rt * 16 + g;
-      const bool second = 2 * tq + 1 < ncols;
+    std::int32_t* z = zrow + rt * 16;  // column 2 tq, row 16 rt + g
 #pragma unroll
-      for (int s = 0; s < STAGES; ++s) {
-        const int* acc = s == 0 ? acc0 : acc1;
-        std::int32_t* z = a.zacc + (std::size_t(s) * 8 + 2 * tq) * a.rows_pad + r0;  // column 2 tq
-        atomicAdd(z, acc[0]);
-        atomicAdd(z + 8, acc[2]);
-        if (second) {
-          atomicAdd(z + a.rows_pad, acc[1]);
-          atomicAdd(z + a.rows_pad + 8, acc[3]);
-        }
+    for (int s = 0; s < STAGES; ++s) {
+      const int* acc = s == 0 ? acc0 : acc1;
+      std::int32_t* zs = z + std::size_t(s) * 8 * a.rows_pad;
+      if (w0) {
+        atomicAdd(zs, acc[0]);
+        atomicAdd(zs + 8, acc[2]);
+      }
+      if (w1) {
+        atomicAdd(zs + a.rows_pad, acc[1]);
+        atomicAdd(zs + a.rows_pad + 8, acc[3]);
       }
     }
   };
@@ -423,9 +436,8 @@ __global__ void __launch_bounds__(Cfg<STAGES>::kThreads, 1) gemv_imma_kernel(Imm
     mma_u8s8(acc, s0, s1, s2, s3, bw[16], bw[17]);
   };
 
-  auto compute = [&](int i, std::uint32_t kc, std::uint32_t ksl) {
-    const uint4* bp = reinterpret_cast<const uint4*>(
-        bsm + ((kc - kc_lo) * kChunk + ksl) * 32 * kBWords + lane * kBWords);
+  auto compute = [&](int i, std::uint32_t boff) {
+    const uint4* bp = reinterpret_cast<const uint4*>(bsm + boff + lane * kBWords);
     const uint4 b0 = bp[0], b1 = bp[1], b2 = bp[2], b3 = bp[3];
     const uint2 b4 = *reinterpret_cast<const uint2*>(bp + 4);
     const std::uint32_t bw[18] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x,
@@ -446,38 +458,30 @@ __global__ void __launch_bounds__(Cfg<STAGES>::kThreads, 1) gemv_imma_kernel(Imm
     }
   };
 
-  Cursor cc;  // consume cursor
-  cc.init(a, u0 < u1 ? u0 : 0);
-  auto step = [&](int i, bool refill, bool refill_valid) {
-    if (cc.rt != cur_rt) {
-      flush();
+  if (nu > 0) {
+    std::uint32_t cur_rt = list[0].z;
+    auto step = [&](int u, int i, bool refill) {
+      const uint4 e = list[u];  // uniform smem broadcast
+      if (e.z != cur_rt) {
+        flush(cur_rt);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc0[q] = acc1[q] = 0;
-      cur_rt = cc.rt;
-    }
-    const std::uint32_t kc = cc.kc, ksl = cc.ksl;
-    cc.next(a);
-    compute(i, kc, ksl);
-    if (refill) {
-      if (refill_valid) {
-        last_tile = pc.tile(a);
-        pc.next(a);
+        for (int q = 0; q < 4; ++q) acc0[q] = acc1[q] = 0;
+        cur_rt = e.z;
       }
-      load_unit(i, last_tile);
+      compute(i, e.y);
+      if (refill) load_unit(i, list[min(u + kPrefetch, nu - 1)].x);
+    };
+    int u = 0;
+    // steady state; refills past the end re-load the last tile (harmless)
+    for (; u + kPrefetch <= nu; u += kPrefetch) {
+#pragma unroll
+      for (int i = 0; i < kPrefetch; ++i) step(u + i, i, true);
     }
-  };
-  std::uint32_t u = u0;
-  // Steady state: every slot holds a valid unit; refills past the end reload
-  // the last valid tile (harmless, keeps the loop branch-light).
-  for (; u + kPrefetch <= u1; u += kPrefetch) {
 #pragma unroll
-    for (int i = 0; i < kPrefetch; ++i) step(i, true, u + i + kPrefetch < u1);
+    for (int i = 0; i < kPrefetch; ++i)
+      if (u + i < nu) step(u + i, i, false);
+    flush(cur_rt);
   }
-  // Tail: fewer than kPrefetch units left, all already in flight.
-#pragma unroll
-  for (int i = 0; i < kPrefetch; ++i)
-    if (u + i < u1) step(i, false, false);
-  flush();
 }
 
 template <int S, int K>
@@ -607,7 +611,10 @@ void launch_gemv_imma(const q8p_layer& L, const float* t, const float* amax, std
   // exceeds one full chunk of units, so it touches at most kMaxChunks B chunks.
   std::uint32_t grid = std::uint32_t(sm_count());
   const std::uint32_t chunk_units = kChunk * a.RT;
-  while ((a.units + grid - 1) / grid + 1 > chunk_units) ++grid;
+  const std::uint32_t warps = L.num_stages == 1 ? Cfg<1>::kWarps : Cfg<2>::kWarps;
+  while ((a.units + grid - 1) / grid + 1 > chunk_units ||
+         (a.units + grid * warps - 1) / (grid * warps) + 1 > std::uint32_t(kMaxUnits))
+    ++grid;
   if (L.num_stages == 1) {
     set_attr<1, 0>();
     launch_pdl(gemv_imma_kernel<1, 0>, dim3(grid), dim3(Cfg<1>::kThreads), kSmemBytes, s, a);
