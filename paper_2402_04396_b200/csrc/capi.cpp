@@ -141,7 +141,7 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
     setup_side(L.get(), L->side_v, d.n, d.signs_v);
     {
       std::vector<std::uint32_t> e8p, e81;
-      imma_tables(e8p, e81);
+      tc_tables(e8p, e81);
       L->lut_e8p = static_cast<const std::uint32_t*>(upload(L.get(), e8p.data(), e8p.size() * 4));
       L->lut_e81 = static_cast<const std::uint32_t*>(upload(L.get(), e81.data(), e81.size() * 4));
     }
@@ -158,7 +158,7 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
       L->cb[s] = st.codebook;
       L->scale[s] = st.scale;
       const auto* src = static_cast<const std::uint8_t*>(st.codes) + std::size_t(r0) * nb * st.code_bytes;
-      // Tensor-core tile format (lossless re-layout, gemv_imma.cu).
+      // Tensor-core slab format (lossless re-layout, gemv_tc.cu).
       {
         std::vector<std::uint16_t> wide(words);
         for (std::size_t i = 0; i < words; ++i)
@@ -167,13 +167,9 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
           for (std::size_t i = 0; i < words; ++i)
             if (wide[i] >= 256) throw ValidationError("decode: codeword out of range");
         const int kind = st.codebook == Q8P_CB_E8P_2BIT ? 0 : 1;
-        std::vector<std::uint8_t> tiles(imma_tile_bytes(r1 - r0, d.n, kind));
-        std::vector<std::uint8_t> shifts(imma_shift_bytes(r1 - r0, d.n, kind));
-        imma_transcode(wide.data(), r1 - r0, d.n, kind, tiles.data(), shifts.data());
-        L->tiles[s].tiles = upload(L.get(), tiles.data(), tiles.size());
-        if (!shifts.empty()) L->tiles[s].shifts = upload(L.get(), shifts.data(), shifts.size());
-        L->tiles[s].row_tiles = (r1 - r0 + 15) / 16;
-        L->tiles[s].k_steps = (d.n / 8 + 31) / 32;
+        std::vector<std::uint8_t> slabs(tc_code_bytes(r1 - r0, d.n, kind));
+        tc_transcode(wide.data(), r1 - r0, d.n, kind, slabs.data());
+        L->tc[s].codes = upload(L.get(), slabs.data(), slabs.size());
       }
       if (st.codebook == Q8P_CB_E8P_2BIT) {
         L->codes[s] = upload(L.get(), src, words * 2);
@@ -238,35 +234,69 @@ void record_event(void* ev, cudaStream_t s) {
     cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(ev), s), "event record");
 }
 
+// Per-forward scratch, caller-provided (q8p_workspace_bytes).  Tensor-core path:
+// RHT scratch, per-chunk sums of squares, alpha / TL per vector, the B images of
+// the integer activations and the int32 accumulators.  Portable path: t, z.
 struct Workspace {
-  float* t;              // [batch][n]
-  float* z;              // [batch][m] fp32 (portable path) / scratch for the RHT passes
-  float* amax;           // [batch]
-  float* tsum;           // [batch]
-  std::int32_t* zacc;    // [stages][8][rows_pad] int32 limb accumulators
-  std::uint32_t rows_pad;
+  float* u;              // [batch][max(m, n)] RHT intermediate
+  float* t;              // [batch][n] (portable path)
+  float* z;              // [batch][m] (portable path)
+  float* ssq;            // [batch][n / 4]
+  float* alpha;          // [batch]
+  long long* tl;         // [batch]
+  std::uint8_t* bimg;    // tc_bimg_bytes(n, batch)
+  std::int32_t* zacc;    // [stages][N][rows_pad]
+  std::uint32_t rows_pad, zcols;
 };
-std::uint32_t rows_pad_of(const q8p_layer* L) { return (L->m + 15) / 16 * 16; }
-std::size_t workspace_size(const q8p_layer* L, int batch) {
-  const std::size_t mx = std::max(L->n, L->m);
-  return round_up(std::size_t(batch) * L->n * 4, 256) + round_up(std::size_t(batch) * mx * 4, 256) +
-         2 * round_up(std::size_t(batch) * 4, 256) + round_up(std::size_t(2) * 8 * rows_pad_of(L) * 4, 256);
+std::uint32_t rows_pad_of(const q8p_layer* L) { return tc_row_blocks(L->m_local()) * 128; }
+std::size_t workspace_parts(const q8p_layer* L, int batch, Workspace* w, void* base) {
+  auto* p0 = static_cast<std::uint8_t*>(base);
+  std::size_t off = 0;
+  auto take = [&](std::size_t bytes) {
+    std::uint8_t* r = p0 ? p0 + off : nullptr;
+    off += round_up(bytes ? bytes : 1, 256);
+    return r;
+  };
+  const std::size_t B = std::size_t(batch), mx = std::max(L->n, L->m);
+  const bool tc = tc_supported(*L, batch);
+  Workspace v{};
+  v.rows_pad = rows_pad_of(L);
+  v.zcols = std::uint32_t(tc_ncols_pad(4 * batch));
+  v.u = reinterpret_cast<float*>(take(B * mx * 4));
+  if (tc) {
+    v.ssq = reinterpret_cast<float*>(take(B * std::max<std::size_t>(64, L->n / 4) * 4));
+    v.alpha = reinterpret_cast<float*>(take(B * 4));
+    v.tl = reinterpret_cast<long long*>(take(B * 8));
+    v.bimg = take(tc_bimg_bytes(L->n, batch));
+    v.zacc = reinterpret_cast<std::int32_t*>(take(std::size_t(L->num_stages) * v.zcols * v.rows_pad * 4));
+  } else {
+    v.t = reinterpret_cast<float*>(take(B * L->n * 4));
+    v.z = reinterpret_cast<float*>(take(B * L->m * 4));
+  }
+  if (w) *w = v;
+  return off;
 }
-Workspace carve(const q8p_layer* L, int batch, void* ws) {
-  auto* p = static_cast<std::uint8_t*>(ws);
-  const std::size_t mx = std::max(L->n, L->m);
-  Workspace w;
-  w.t = reinterpret_cast<float*>(p);
-  p += round_up(std::size_t(batch) * L->n * 4, 256);
-  w.z = reinterpret_cast<float*>(p);
-  p += round_up(std::size_t(batch) * mx * 4, 256);
-  w.amax = reinterpret_cast<float*>(p);
-  p += round_up(std::size_t(batch) * 4, 256);
-  w.tsum = reinterpret_cast<float*>(p);
-  p += round_up(std::size_t(batch) * 4, 256);
-  w.zacc = reinterpret_cast<std::int32_t*>(p);
-  w.rows_pad = rows_pad_of(L);
-  return w;
+std::size_t workspace_size(const q8p_layer* L, int batch) { return workspace_parts(L, batch, nullptr, nullptr); }
+
+// K1 -> K2 on the layer's local rows: leaves int32 accumulators in w.zacc (tensor-core
+// path) or fp32 z rows in w.z (portable path).
+void forward_local(const q8p_layer* L, const float* x, int batch, const Workspace& w, cudaStream_t s,
+                   const q8p_forward_opts* opts) {
+  if (tc_supported(*L, batch)) {
+    const std::uint32_t N = w.zcols, KSL = tc_k_slabs(L->n), bb = 9u * N * 32u;
+    const bool ragged = (L->n / 8) % 32 != 0;
+    launch_rht_in_limbs(L->side_v, x, w.u, w.ssq, w.alpha, w.tl, w.bimg, bb, N,
+                        ragged ? w.bimg + std::size_t(KSL - 1) * bb : nullptr, ragged ? bb : 0, w.zacc,
+                        std::size_t(L->num_stages) * N * w.rows_pad, batch, s);
+    if (opts) record_event(opts->gemv_start_event, s);
+    launch_gemv_tc(*L, w.bimg, w.zacc, w.rows_pad, batch, s);
+    if (opts) record_event(opts->gemv_end_event, s);
+  } else {
+    launch_rht(L->side_v, x, w.t, batch, /*transpose=*/false, s);  // t = T_v x
+    if (opts) record_event(opts->gemv_start_event, s);
+    launch_gemv_simple(*L, w.t, w.z, batch, static_cast<int>(L->m), s);
+    if (opts) record_event(opts->gemv_end_event, s);
+  }
 }
 
 void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void* ws, std::size_t ws_bytes,
@@ -279,28 +309,17 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
     throw ValidationError("row-sharded layer: use q8p_forward_sharded");
   if (!ws || ws_bytes < workspace_size(L, batch)) throw SizeError("workspace too small");
   DeviceGuard g(L->device);
-  const Workspace w = carve(L, batch, ws);
-  if (imma_supported(*L, batch)) {
-    // K1: t = T_v x (+ per-vector amax, zeroed accumulators); K2: tensor-core
-    // decode-GEMV into int32 limb accumulators; K3: y = T_u^T z.
-    const std::size_t zwords = std::size_t(L->num_stages) * 8 * w.rows_pad;
-    launch_rht_in(L->side_v, x, w.t, w.z, w.amax, w.tsum, w.zacc, zwords, batch, s);
-    if (opts) record_event(opts->gemv_start_event, s);
-    launch_gemv_imma(*L, w.t, w.amax, w.zacc, w.rows_pad, batch, s);
-    if (opts) record_event(opts->gemv_end_event, s);
-    float zscale[2], zbias = 0.f;
-    for (int st = 0; st < 2; ++st) zscale[st] = 0.5f * L->scale[st] / imma_limb_max(batch);
-    for (int st = 0; st < L->num_stages; ++st)
-      if (L->cb[st] == Q8P_CB_E8P_2BIT) zbias -= 0.25f * L->scale[st];  // the -T/4 of each E8P stage
-    launch_rht_out(L->side_u, w.zacc, L->num_stages, w.rows_pad, imma_limbs(batch), zscale, zbias, w.amax, w.tsum,
-                   w.z, y, batch, s);
-    return;
+  Workspace w;
+  workspace_parts(L, batch, &w, ws);
+  forward_local(L, x, batch, w, s, opts);
+  if (tc_supported(*L, batch)) {
+    float zscale[2] = {L->scale[0], L->scale[1]};
+    int ze8p[2] = {L->cb[0] == Q8P_CB_E8P_2BIT, L->cb[1] == Q8P_CB_E8P_2BIT};
+    launch_rht_out_acc(L->side_u, w.zacc, L->num_stages, w.rows_pad, w.zcols, zscale, ze8p, w.alpha, w.tl, w.u, y,
+                       batch, s);
+  } else {
+    launch_rht(L->side_u, w.z, y, batch, /*transpose=*/true, s);  // y = T_u^T z
   }
-  launch_rht(L->side_v, x, w.t, batch, /*transpose=*/false, s);  // t = T_v x
-  if (opts) record_event(opts->gemv_start_event, s);
-  launch_gemv_simple(*L, w.t, w.z, batch, static_cast<int>(L->m), s);
-  if (opts) record_event(opts->gemv_end_event, s);
-  launch_rht(L->side_u, w.z, y, batch, /*transpose=*/true, s);  // y = T_u^T z
 }
 
 }  // namespace
@@ -529,7 +548,7 @@ q8p_status q8p_rht(size_t n, const uint8_t* signs, const float* x, float* y, int
     if (!transpose) {
       launch_rht_in(side, x, y, u, amax, nullptr, nullptr, 0, batch, s);
     } else {
-      launch_rht_out(side, nullptr, 1, 0, 0, nullptr, 0.f, nullptr, nullptr, u, y, batch, s, x);
+      launch_rht_out(side, x, u, y, batch, s);
     }
     return Q8P_OK;
   } catch (...) {

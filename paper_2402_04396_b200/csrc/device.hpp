@@ -56,11 +56,9 @@ struct DevSide {
   const float* colsum = nullptr;        // q column sums of the base (sum_i t_i in closed form)
 };
 
-// Fast-path (IMMA GEMV) transcoded code tiles, see gemv_imma.cu.
-struct TileCodes {
-  void* tiles = nullptr;      // [row_tile][k_step][2 halves][32 lanes][16 B]
-  void* shifts = nullptr;     // [row_tile][k_step][32 lanes] u16 shift bits (E8P)
-  std::uint32_t row_tiles = 0, k_steps = 0;
+// Tensor-core GEMV slab records (gemv_tc.cu): [row block][k slab][slab bytes].
+struct SlabCodes {
+  void* codes = nullptr;
 };
 
 }  // namespace q8p::detail
@@ -73,7 +71,7 @@ struct q8p_layer {
   float scale[2] = {1.f, 1.f};
   q8p::detail::DevSide side_u, side_v;  // left (m) / right (n)
   void* codes[2] = {nullptr, nullptr};  // plain [m_local][n/8]: u16 (E8P) / u8 (e8-1bit)
-  q8p::detail::TileCodes tiles[2];
+  q8p::detail::SlabCodes tc[2];
   const std::uint32_t* lut_e8p = nullptr;  // device [256]   (tensor-core GEMV tables)
   const std::uint32_t* lut_e81 = nullptr;  // device [256][2]
   std::size_t device_bytes = 0;
@@ -99,24 +97,33 @@ void launch_gemv_simple(const q8p_layer& L, const float* t, float* z, int batch,
                         cudaStream_t s);
 void launch_decode(const q8p_layer& L, int stage, float* w, cudaStream_t s);
 
-// Tensor-core path (gemv_imma.cu, kernels_rht.cu).
-void imma_tables(std::vector<std::uint32_t>& e8p, std::vector<std::uint32_t>& e81);
-std::size_t imma_tile_bytes(std::uint32_t m_local, std::uint32_t n, int kind);
-std::size_t imma_shift_bytes(std::uint32_t m_local, std::uint32_t n, int kind);
-void imma_transcode(const std::uint16_t* codes, std::uint32_t m_local, std::uint32_t n, int kind,
-                    std::uint8_t* out, std::uint8_t* shifts);
-bool imma_supported(const q8p_layer& L, int batch);
-int imma_limbs(int batch);         // int8 activation limbs per vector (MMA columns)
-float imma_limb_max(int batch);    // 127 * 128^(limbs - 1)
-void launch_gemv_imma(const q8p_layer& L, const float* t, const float* amax, std::int32_t* zacc,
-                      std::uint32_t rows_pad, int batch, cudaStream_t s);
-// K1: t = T_v x (+ amax of t, tsum = sum_i t_i, zeroed accumulators when zero_ptr).
+// Tensor-core path (gemv_tc.cu, kernels_rht.cu).
+void tc_tables(std::vector<std::uint32_t>& e8p, std::vector<std::uint32_t>& e81);
+std::uint32_t tc_slab_bytes(int kind);
+std::uint32_t tc_row_blocks(std::uint32_t m_local);
+std::uint32_t tc_k_slabs(std::uint32_t n);
+std::size_t tc_code_bytes(std::uint32_t m_local, std::uint32_t n, int kind);
+void tc_transcode(const std::uint16_t* codes, std::uint32_t m_local, std::uint32_t n, int kind, std::uint8_t* out);
+bool tc_supported(const q8p_layer& L, int batch);
+int tc_ncols_pad(int ncols);                              // MMA N for `ncols` B rows
+std::uint32_t tc_bimg_bytes(std::uint32_t n, int batch);  // B images for all k slabs
+void launch_gemv_tc(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* zacc, std::uint32_t rows_pad,
+                    int batch, cudaStream_t s);
+// K1 (fp32 flavour, q8p_rht): t = T_v x (+ amax, tsum when non-null).
 void launch_rht_in(const DevSide& side, const float* x, float* t, float* u_scratch, float* amax, float* tsum,
                    std::int32_t* zero_ptr, std::size_t zero_words, int batch, cudaStream_t s);
-// K3: y = T_u^T z, z = sum_s zscale_s amax (128 hi + lo) + zbias * tsum from the
-// int32 accumulators, or z = zin (fp32) when zacc is null.
-void launch_rht_out(const DevSide& side, const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows,
-                    int limbs, const float zscale[2], float zbias, const float* amax, const float* tsum, float* u_scratch,
-                    float* y, int batch, cudaStream_t s, const float* zin = nullptr);
+// K1 (limb flavour): x -> B images of the integer activations (gemv_tc.cu), alpha, TL;
+// zeroes the GEMV accumulators and the B-image tail.
+void launch_rht_in_limbs(const DevSide& side, const float* x, float* u_scratch, float* ssq, float* alpha,
+                         long long* tl, std::uint8_t* bimg, std::uint32_t b_bytes, std::uint32_t bcols,
+                         std::uint8_t* bimg_tail, std::size_t tail_bytes, std::int32_t* zero_ptr,
+                         std::size_t zero_words, int batch, cudaStream_t s);
+// K3 (fp32 input): y = T_u^T z.
+void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, float* y, int batch, cudaStream_t s);
+// K3 (accumulator input): z = sum_s zscale_s alpha (2 Z_s - [E8P] TL) / 4 from the int32
+// limb accumulators [stage][zacc_cols][zacc_rows], then y = T_u^T z.
+void launch_rht_out_acc(const DevSide& side, const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows,
+                        std::uint32_t zacc_cols, const float zscale[2], const int ze8p[2], const float* alpha,
+                        const long long* tl, float* u_scratch, float* y, int batch, cudaStream_t s);
 
 }  // namespace q8p::detail

@@ -1,0 +1,537 @@
+// K2: E8P / RVQ decode fused into a small-batch GEMV on the 5th-gen tensor
+// cores (tcgen05.mma kind::i8, A operand in tensor memory).
+//
+// Semantics: z[r] = sum_s scale_s * sum_k <decode_s(codes[s][r][k]), t[8k:8k+8]>
+// (core/src/pipeline.cpp:172-191) with decode = e8p_decode
+// (core/src/e8p.cpp:81-100) or the e8-1bit table (core/src/codebook.cpp:65-72).
+//
+// Algebra.  e8p_decode gives v_c = sigma_c d_c / 2 + (2 b - 1) / 4 with
+// d in {1,3,5} (256-row pattern table), sigma the coordinate signs (coordinate
+// 0 parity-inferred, e8p.cpp:97-98) and b the shift bit.  With the
+// activations as integers, t = alpha * Lt (K1; Lt = sum_l 128^(3-l) limb_l,
+// 4 int8 limbs), and q_k = floor(sum_c Lt_{8k+c} / 8):
+//     z = alpha * ( Z / 2 - TL / 4 ),   Z = sum (sigma d) Lt + sum_k 8 b_k q_k
+// TL = sum_i Lt_i (exact, K1).  Z is what the tensor cores accumulate:
+//   main MMAs  A = sigma_c d_c  (s8, from TMEM)   B = limb rows of Lt  (smem)
+//   side MMA   A = 8 b_k        (s8, from TMEM)   B = limb rows of q_k (smem)
+// e8-1bit stages: A = doubled table row, no side term, z = alpha Z / 2.
+// Every product is exact int32; segments combine with integer atomics, so the
+// result is deterministic and independent of the CTA count.
+//
+// Data layout ("slab" = 128 rows x 32 codewords of one stage, built once at
+// upload; a lossless re-layout of the QSHP codes):
+//   E8P slab, 8704 B:  [plane 0..1: idx bytes of codewords 16p..16p+15][128 rows][16 B]
+//                      [plane 2..3: negate flags, 4 x u32 per row: word g covers
+//                       codewords 4g..4g+3, bit 4c + (w & 3) = flag of coordinate c
+//                       (coordinate 0 resolved from the parity at upload)][128][16 B]
+//                      [plane 4: shift word per row, bit (w >> 2) + 8 (w & 3) = b_w][128][4 B]
+//   e8-1bit slab, 4096 B: [plane 0..1: code bytes][128 rows][16 B]
+//   slabs ordered [row block][k slab] per stage: a CTA's contiguous work range is
+//   one contiguous byte range, streamed by 1-D bulk copies.
+//   B image per k slab (K1): 9 K-blocks x [N rows][32 B] in the K-major
+//   no-swizzle core-matrix layout ([N/8][2][8][16 B]); K-block 8 = side.
+//
+// CTA (one per SM, persistent over a contiguous range of (row block, k slab,
+// stage) items; warp-specialised):
+//   warp 0      producer: cp.async.bulk of code slabs (before griddepcontrol.wait,
+//               so they overlap K1) and B slabs into an smem ring (mbarriers)
+//   warp 1      MMA issuer: 8 + 1 tcgen05.mma (M=128, N, K=32) per slab into a
+//               TMEM accumulator per row block; tcgen05.commit frees the ring
+//               stage and the A buffer
+//   warps 2..5  epilogue: tcgen05.ld of finished accumulators -> int32 atomics
+//   warps 6..   G decode groups of 4 warps (thread = TMEM lane = row): smem codes
+//               -> A bytes -> tcgen05.st into a double-buffered A tile
+// Decode per codeword: PRMT (LUT address) + LDS (lane-replicated nibble LUT,
+// 64-KiB-aligned window) + shift + LOP3 (sign flags) + 2 PRMT from the constant
+// byte table {1,3,5,_,-1,-3,-5,_}.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "device.hpp"
+#include "tc05.hpp"
+
+namespace q8p::detail {
+namespace {
+using namespace tc05;
+
+constexpr int kSlabCw = 32;                 // codewords per slab row
+constexpr std::uint32_t kE8pSlab = 4 * 2048 + 512;
+constexpr std::uint32_t kE81Slab = 2 * 2048;
+constexpr std::uint32_t kAcols = 72;        // TMEM columns per A buffer (64 main + 8 side)
+constexpr int kWarpProd = 0, kWarpMma = 1, kWarpDec = 6;  // warps 2..5: epilogue
+constexpr int kMaxStages = 24;
+constexpr std::uint32_t kCtl = 1024;        // control block (barriers) at the smem base
+constexpr std::size_t kSmemBytes = 200 * 1024;
+
+template <int G>
+struct Roles {
+  static constexpr int kThreads = (kWarpDec + 4 * G) * 32;
+};
+
+struct TcArgs {
+  const std::uint8_t* codes[2];   // per stage slab records
+  std::uint32_t slab_bytes[2];
+  int kind[2];                    // 0 = e8p, 1 = e8-1bit
+  int nst;                        // stages (1 or 2)
+  std::uint32_t KSL;              // k slabs per row block
+  std::uint32_t items;            // RB * KSL * nst
+  const std::uint8_t* bimg;       // [KSL][b_bytes]
+  std::uint32_t b_bytes;          // 9 * N * 32
+  std::int32_t* zacc;             // [nst][N][rows_pad]
+  std::uint32_t rows_pad, m_local;
+  int ncols;                      // used B rows (limbs x batch)
+  std::uint32_t smem_bytes;
+  const std::uint32_t* lut_e8p;   // [256]
+  const std::uint32_t* lut_e81;   // [512]
+};
+
+__device__ __forceinline__ std::uint32_t lds32(std::uint32_t addr) {
+  std::uint32_t r;
+  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(r) : "r"(addr));
+  return r;
+}
+__device__ __forceinline__ uint2 lds64(std::uint32_t addr) {
+  uint2 r;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];\n" : "=r"(r.x), "=r"(r.y) : "r"(addr));
+  return r;
+}
+__device__ __forceinline__ uint4 lds128(std::uint32_t addr) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr));
+  return r;
+}
+__device__ __forceinline__ void sts128(std::uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+// Raw PTX prmt (default mode); our selectors never set bit 3 of a nibble.
+__device__ __forceinline__ std::uint32_t prmt(std::uint32_t a, std::uint32_t b, std::uint32_t sel) {
+  std::uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+constexpr std::uint32_t kCtLo = 0x00050301u;  // {+1,+3,+5,0}
+constexpr std::uint32_t kCtHi = 0x00FBFDFFu;  // {-1,-3,-5,0}
+
+// A bytes of one E8P codeword: slot jj (0..3) of an idx / flag register pair.
+// `lb` = LUT window bytes 2..3 | lane * 4: PRMT drops idx into byte 1.
+template <int JJ>
+__device__ __forceinline__ void e8p_a(std::uint32_t idxreg, std::uint32_t fl, std::uint32_t lb, std::uint32_t& lo,
+                                      std::uint32_t& hi) {
+  const std::uint32_t nib = lds32(prmt(idxreg, lb, 0x7604u | (std::uint32_t(JJ) << 4)));
+  std::uint32_t rs;
+  if constexpr (JJ == 0)
+    rs = fl << 2;
+  else if constexpr (JJ == 1)
+    rs = fl << 1;
+  else if constexpr (JJ == 2)
+    rs = fl;
+  else
+    rs = __umulhi(fl, 0x80000000u);  // fl >> 1 on the FMA pipe
+  const std::uint32_t sel = nib ^ (rs & 0x44444444u);
+  lo = prmt(kCtLo, kCtHi, sel);
+  hi = prmt(kCtLo, kCtHi, __umulhi(sel, 65536u));  // sel >> 16
+}
+
+template <int N, int G>
+__global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a) {
+  extern __shared__ __align__(1024) std::uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::uint32_t sbase = smem_u32(smem);
+  const std::uint32_t send = sbase + a.smem_bytes;
+  const std::uint32_t lutw = (sbase + kCtl + 0xFFFFu) & ~0xFFFFu;
+  // control block: barriers + TMEM base
+  const std::uint32_t bar_full_code = sbase;                  // [kMaxStages]
+  const std::uint32_t bar_full_b = sbase + 8 * kMaxStages;    // [kMaxStages]
+  const std::uint32_t bar_empty = sbase + 16 * kMaxStages;    // [kMaxStages]
+  const std::uint32_t bar_a_full = sbase + 24 * kMaxStages;   // [G][2]
+  const std::uint32_t bar_a_empty = bar_a_full + 8 * 2 * G;   // [G][2]
+  const std::uint32_t bar_d_full = bar_a_empty + 8 * 2 * G;   // [2]
+  const std::uint32_t bar_d_empty = bar_d_full + 16;          // [2]
+  const std::uint32_t tmem_slot = bar_d_empty + 16;
+  // ring: stages below the LUT window, then above it
+  const std::uint32_t stage_bytes = ((a.nst > 0 ? kE8pSlab : 0) + a.b_bytes + 127) & ~127u;
+  const std::uint32_t lo_base = sbase + kCtl;
+  const std::uint32_t n_lo = lutw > lo_base ? (lutw - lo_base) / stage_bytes : 0;
+  const std::uint32_t hi_base = lutw + 65536;
+  std::uint32_t S = n_lo + (send > hi_base ? (send - hi_base) / stage_bytes : 0);
+  if (S > kMaxStages) S = kMaxStages;
+  auto stage_addr = [&](std::uint32_t st) { return st < n_lo ? lo_base + st * stage_bytes : hi_base + (st - n_lo) * stage_bytes; };
+
+  const std::uint32_t it0 = std::uint32_t((std::uint64_t(a.items) * blockIdx.x) / gridDim.x);
+  const std::uint32_t it1 = std::uint32_t((std::uint64_t(a.items) * (blockIdx.x + 1)) / gridDim.x);
+  const std::uint32_t count = it1 - it0;
+  const std::uint32_t nst = std::uint32_t(a.nst);
+
+  if (threadIdx.x == 0) {
+    for (std::uint32_t i = 0; i < S; ++i) {
+      mbar_init(bar_full_code + 8 * i, 1);
+      mbar_init(bar_full_b + 8 * i, 1);
+      mbar_init(bar_empty + 8 * i, 1);
+    }
+    for (int i = 0; i < 2 * G; ++i) {
+      mbar_init(bar_a_full + 8 * i, 128);
+      mbar_init(bar_a_empty + 8 * i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar_d_full + 8 * i, 1);
+      mbar_init(bar_d_empty + 8 * i, 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == kWarpMma) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tbase = *reinterpret_cast<volatile std::uint32_t*>(smem + (tmem_slot - sbase));
+  const std::uint32_t dcol0 = std::uint32_t(G) * 2 * kAcols;
+
+  if (warp == kWarpProd) {
+    // ===== producer =====
+    if (lane == 0 && count > 0) {
+      const std::uint64_t pol = policy_evict_first();
+      auto issue_code = [&](std::uint32_t i, std::uint32_t st) {
+        const std::uint32_t it = it0 + i, u = it / nst, s = it - u * nst;
+        mbar_arrive_expect_tx(bar_full_code + 8 * st, (s ? a.slab_bytes[1] : a.slab_bytes[0]));
+        bulk_g2s_hint(stage_addr(st), (s ? a.codes[1] : a.codes[0]) + std::size_t(u) * (s ? a.slab_bytes[1] : a.slab_bytes[0]), (s ? a.slab_bytes[1] : a.slab_bytes[0]),
+                      bar_full_code + 8 * st, pol);
+      };
+      auto issue_b = [&](std::uint32_t i, std::uint32_t st) {
+        const std::uint32_t u = (it0 + i) / nst, ks = u % a.KSL;
+        mbar_arrive_expect_tx(bar_full_b + 8 * st, a.b_bytes);
+        bulk_g2s(stage_addr(st) + kE8pSlab, a.bimg + std::size_t(ks) * a.b_bytes, a.b_bytes, bar_full_b + 8 * st);
+      };
+      const std::uint32_t pre = count < S ? count : S;
+      for (std::uint32_t i = 0; i < pre; ++i) issue_code(i, i);
+      pdl_wait();  // K1's B images (and zeroed accumulators) are visible from here on
+      for (std::uint32_t i = 0; i < pre; ++i) issue_b(i, i);
+      std::uint32_t st = pre == S ? 0 : pre, r = 1;
+      for (std::uint32_t i = pre; i < count; ++i) {
+        mbar_wait(bar_empty + 8 * st, (r & 1) ^ 1);
+        issue_code(i, st);
+        issue_b(i, st);
+        if (++st == S) {
+          st = 0;
+          ++r;
+        }
+      }
+    }
+    pdl_trigger();
+  } else if (warp == kWarpMma) {
+    // ===== MMA issuer =====
+    pdl_trigger();
+    if (lane == 0 && count > 0) {
+      constexpr std::uint32_t idesc = idesc_i8(128, N);
+      std::uint32_t prev_rb = 0xFFFFFFFFu, seg = 0, dreg = 0, started = 0;
+      std::uint32_t st = 0, r = 0, g = 0, use = 0;
+      for (std::uint32_t i = 0; i < count; ++i) {
+        const std::uint32_t it = it0 + i, u = it / nst, s = it - u * nst, rb = u / a.KSL;
+        if (rb != prev_rb) {
+          if (prev_rb != 0xFFFFFFFFu) {
+            mma_commit(bar_d_full + 8 * dreg);
+            ++seg;
+          }
+          dreg = seg & 1;
+          mbar_wait(bar_d_empty + 8 * dreg, ((seg >> 1) & 1) ^ 1);
+          tc_fence_after();
+          started = 0;
+          prev_rb = rb;
+        }
+        const std::uint32_t buf = use & 1, bph = (use >> 1) & 1;
+        mbar_wait(bar_a_full + 8 * (2 * g + buf), bph);
+        mbar_wait(bar_full_b + 8 * st, r & 1);
+        tc_fence_after();
+        const std::uint32_t d = tbase + dcol0 + (dreg * nst + s) * N;
+        const std::uint32_t abuf = tbase + (2 * g + buf) * kAcols;
+        const std::uint32_t bsm = stage_addr(st) + kE8pSlab;
+        const std::uint32_t acc0 = (started >> s) & 1;
+#pragma unroll
+        for (int kb = 0; kb < 8; ++kb)
+          mma_i8_ts(d, abuf + 8 * kb, sdesc(bsm + kb * N * 32, 128, 256), idesc, (kb > 0) | acc0);
+        if ((s ? a.kind[1] : a.kind[0]) == 0) mma_i8_ts(d, abuf + 64, sdesc(bsm + 8 * N * 32, 128, 256), idesc, 1);
+        started |= 1u << s;
+        mma_commit(bar_a_empty + 8 * (2 * g + buf));
+        mma_commit(bar_empty + 8 * st);
+        if (++st == S) {
+          st = 0;
+          ++r;
+        }
+        if (++g == G) {
+          g = 0;
+          ++use;
+        }
+      }
+      mma_commit(bar_d_full + 8 * dreg);
+    }
+  } else if (warp < kWarpDec) {
+    // ===== epilogue (lanes 32 (warp % 4) ..) =====
+    pdl_trigger();
+    if (count > 0) {
+      const std::uint32_t q = warp & 3, row_in = q * 32 + lane;
+      const std::uint32_t tl = tbase + ((q * 32) << 16);
+      const std::uint32_t rb0 = (it0 / nst) / a.KSL, rb1 = ((it1 - 1) / nst) / a.KSL;
+      for (std::uint32_t sg = 0; sg <= rb1 - rb0; ++sg) {
+        const std::uint32_t rb = rb0 + sg, dreg = sg & 1;
+        // item range of this segment within [it0, it1)
+        const std::uint32_t ia = std::max(it0, rb * a.KSL * nst), ib = std::min(it1, (rb + 1) * a.KSL * nst);
+        mbar_wait(bar_d_full + 8 * dreg, (sg >> 1) & 1);
+        tc_fence_after();
+        const std::uint32_t row = rb * 128 + row_in;
+        const bool row_ok = row < a.m_local;
+        for (std::uint32_t s = 0; s < nst; ++s) {
+          const bool present = (ib - ia >= nst) || ((ia % nst) == s);
+          std::int32_t* z = a.zacc + std::size_t(s) * N * a.rows_pad + row;
+#pragma unroll
+          for (int c0 = 0; c0 < N; c0 += 8) {
+            std::uint32_t t8[8];
+            tmem_ld8(tl + dcol0 + (dreg * nst + s) * N + c0, t8);
+            tmem_wait_ld();
+            if (present && row_ok) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (c0 + j < a.ncols) atomicAdd(z + std::size_t(c0 + j) * a.rows_pad, std::int32_t(t8[j]));
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(bar_d_empty + 8 * dreg);
+      }
+    }
+  } else {
+    // ===== decoders =====
+    // LUT: E8P nibbles replicated per lane (bytes [0,128) of each 256-B row),
+    // e8-1bit rows replicated per half-warp lane (bytes [128,256)).
+    const int dt = threadIdx.x - kWarpDec * 32;
+    constexpr int kDecThreads = 4 * G * 32;
+    for (int i = dt; i < 256 * 16; i += kDecThreads) {
+      const int row = i >> 4, part = i & 15;
+      uint4 v;
+      if (part < 8) {
+        const std::uint32_t e = a.lut_e8p[row];
+        v = make_uint4(e, e, e, e);
+      } else {
+        const std::uint32_t e0 = a.lut_e81[2 * row], e1 = a.lut_e81[2 * row + 1];
+        v = make_uint4(e0, e1, e0, e1);
+      }
+      sts128(lutw + row * 256 + part * 16, v);
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"n"(kDecThreads) : "memory");
+    pdl_trigger();
+    const int grp = (warp - kWarpDec) >> 2;
+    const std::uint32_t q = warp & 3, row_in = q * 32 + lane;
+    const std::uint32_t tl = (q * 32) << 16;
+    const std::uint32_t lb = (lutw & 0xFFFF0000u) | (std::uint32_t(lane) * 4u);
+    const std::uint32_t lb8 = (lutw & 0xFFFF0000u) | (128u + std::uint32_t(lane & 15) * 8u);
+    std::uint32_t st = std::uint32_t(grp) % S, r = std::uint32_t(grp) / S, use = 0;
+    for (std::uint32_t i = grp; i < count; i += G) {
+      const std::uint32_t it = it0 + i, s = it % nst;
+      const std::uint32_t buf = use & 1, bph = (use >> 1) & 1;
+      const std::uint32_t sa = stage_addr(st);
+      mbar_wait(bar_full_code + 8 * st, r & 1);
+      const std::uint32_t abuf = tbase + tl + (2 * grp + buf) * kAcols;
+      if ((s ? a.kind[1] : a.kind[0]) == 0) {
+        const uint4 i0 = lds128(sa + row_in * 16), i1 = lds128(sa + 2048 + row_in * 16);
+        const uint4 f0 = lds128(sa + 4096 + row_in * 16), f1 = lds128(sa + 6144 + row_in * 16);
+        const std::uint32_t sw = lds32(sa + 8192 + row_in * 4);
+        const std::uint32_t idx[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
+        const std::uint32_t fl[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+        mbar_wait(bar_a_empty + 8 * (2 * grp + buf), bph ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          std::uint32_t o[16];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int g4 = 2 * qq + h;  // codewords 4 g4 .. 4 g4 + 3
+            e8p_a<0>(idx[g4], fl[g4], lb, o[8 * h + 0], o[8 * h + 1]);
+            e8p_a<1>(idx[g4], fl[g4], lb, o[8 * h + 2], o[8 * h + 3]);
+            e8p_a<2>(idx[g4], fl[g4], lb, o[8 * h + 4], o[8 * h + 5]);
+            e8p_a<3>(idx[g4], fl[g4], lb, o[8 * h + 6], o[8 * h + 7]);
+          }
+          tmem_st16(abuf + 16 * qq, o);
+        }
+        std::uint32_t sd[8];
+        sd[0] = (sw << 3) & 0x08080808u;
+        sd[1] = (sw << 2) & 0x08080808u;
+        sd[2] = (sw << 1) & 0x08080808u;
+        sd[3] = sw & 0x08080808u;
+        sd[4] = (sw >> 1) & 0x08080808u;
+        sd[5] = (sw >> 2) & 0x08080808u;
+        sd[6] = (sw >> 3) & 0x08080808u;
+        sd[7] = (sw >> 4) & 0x08080808u;
+        tmem_st8(abuf + 64, sd);
+      } else {
+        const uint4 c0 = lds128(sa + row_in * 16), c1 = lds128(sa + 2048 + row_in * 16);
+        const std::uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        mbar_wait(bar_a_empty + 8 * (2 * grp + buf), bph ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          std::uint32_t o[16];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              const uint2 v = lds64(prmt(cw[2 * qq + h], lb8, 0x7604u | (std::uint32_t(jj) << 4)));
+              o[8 * h + 2 * jj] = v.x;
+              o[8 * h + 2 * jj + 1] = v.y;
+            }
+          }
+          tmem_st16(abuf + 16 * qq, o);
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(bar_a_full + 8 * (2 * grp + buf));
+      ++use;
+      st += G;
+      while (st >= S) {
+        st -= S;
+        ++r;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kWarpMma) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
+template <int N, int G>
+void set_attr() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(kSmemBytes)),
+               "tc smem attr");
+  });
+}
+
+int sm_count() {
+  static int v = [] {
+    int d = 0, c = 148;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, d);
+    return c;
+  }();
+  return v;
+}
+
+template <int N, int G>
+void launch_ng(const TcArgs& a, cudaStream_t s) {
+  set_attr<N, G>();
+  launch_pdl(gemv_tc_kernel<N, G>, dim3(sm_count()), dim3(Roles<G>::kThreads), kSmemBytes, s, a);
+}
+
+}  // namespace
+
+// ---- host: tables and slab transcoding ---------------------------------------
+void tc_tables(std::vector<std::uint32_t>& e8p, std::vector<std::uint32_t>& e81) {
+  const E8PTable& t = e8p_table();
+  e8p.assign(256, 0);
+  for (int i = 0; i < 256; ++i) {
+    std::uint32_t w = 0;
+    for (int c = 0; c < 8; ++c) w |= std::uint32_t((t.doubled[i][c] - 1) / 2) << (4 * c);  // 1,3,5 -> 0,1,2
+    e8p[i] = w;
+  }
+  e81.assign(512, 0);
+  const auto& d = e8_1bit_doubled();
+  for (int i = 0; i < 256; ++i)
+    for (int c = 0; c < 8; ++c) e81[2 * i + c / 4] |= (std::uint32_t(std::uint8_t(d[i][c])) << (8 * (c % 4)));
+}
+
+std::uint32_t tc_slab_bytes(int kind) { return kind == 0 ? kE8pSlab : kE81Slab; }
+std::uint32_t tc_row_blocks(std::uint32_t m_local) { return (m_local + 127) / 128; }
+std::uint32_t tc_k_slabs(std::uint32_t n) { return (n / 8 + kSlabCw - 1) / kSlabCw; }
+
+std::size_t tc_code_bytes(std::uint32_t m_local, std::uint32_t n, int kind) {
+  return std::size_t(tc_row_blocks(m_local)) * tc_k_slabs(n) * tc_slab_bytes(kind);
+}
+
+void tc_transcode(const std::uint16_t* codes, std::uint32_t m_local, std::uint32_t n, int kind, std::uint8_t* out) {
+  const E8PTable& T = e8p_table();
+  const std::uint32_t nb = n / 8, RB = tc_row_blocks(m_local), KSL = tc_k_slabs(n);
+  const std::size_t SB = tc_slab_bytes(kind);
+  std::memset(out, 0, tc_code_bytes(m_local, n, kind));
+  for (std::uint32_t rb = 0; rb < RB; ++rb)
+    for (std::uint32_t ks = 0; ks < KSL; ++ks) {
+      std::uint8_t* slab = out + (std::size_t(rb) * KSL + ks) * SB;
+      for (std::uint32_t r = 0; r < 128; ++r) {
+        const std::uint32_t row = rb * 128 + r;
+        std::uint32_t fl[8] = {0, 0, 0, 0, 0, 0, 0, 0}, sw = 0;
+        for (std::uint32_t w = 0; w < 32; ++w) {
+          const std::uint32_t k = ks * 32 + w;
+          const std::uint16_t word = (row < m_local && k < nb) ? codes[std::size_t(row) * nb + k] : 0;
+          if (kind == 0) {
+            const unsigned idx = word >> 8, sb = (word >> 1) & 0x7Fu;
+            slab[(w / 16) * 2048 + r * 16 + (w % 16)] = std::uint8_t(idx);
+            // effective negate flags (e8p.cpp:88-98): word bit k (1..7) -> coordinate 8 - k,
+            // coordinate 0 restores the row's parity
+            unsigned neg[8];
+            neg[0] = unsigned(__builtin_popcount(sb) & 1) ^ T.odd_parity[idx];
+            for (int c = 1; c < 8; ++c) neg[c] = (word >> (8 - c)) & 1u;
+            for (int c = 0; c < 8; ++c) fl[w / 4] |= std::uint32_t(neg[c]) << (4 * c + (w & 3));
+            sw |= std::uint32_t(word & 1u) << ((w >> 2) + 8 * (w & 3));
+          } else {
+            slab[(w / 16) * 2048 + r * 16 + (w % 16)] = std::uint8_t(word);
+          }
+        }
+        if (kind == 0) {
+          std::memcpy(slab + 4096 + r * 16, fl, 16);
+          std::memcpy(slab + 6144 + r * 16, fl + 4, 16);
+          std::memcpy(slab + 8192 + r * 4, &sw, 4);
+        }
+      }
+    }
+}
+
+int tc_ncols_pad(int ncols) { return ncols <= 8 ? 8 : ncols <= 16 ? 16 : (ncols + 15) / 16 * 16; }
+bool tc_supported(const q8p_layer& L, int batch) {
+  return batch >= 1 && batch <= 16 && L.tc[0].codes != nullptr && L.cb[0] == Q8P_CB_E8P_2BIT &&
+         (L.num_stages == 1 || L.tc[1].codes != nullptr);
+}
+std::uint32_t tc_bimg_bytes(std::uint32_t n, int batch) {
+  return tc_k_slabs(n) * 9u * std::uint32_t(tc_ncols_pad(4 * batch)) * 32u;
+}
+
+void launch_gemv_tc(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* zacc, std::uint32_t rows_pad,
+                    int batch, cudaStream_t s) {
+  TcArgs a{};
+  a.nst = L.num_stages;
+  for (int st = 0; st < L.num_stages; ++st) {
+    a.codes[st] = static_cast<const std::uint8_t*>(L.tc[st].codes);
+    a.kind[st] = L.cb[st] == Q8P_CB_E8P_2BIT ? 0 : 1;
+    a.slab_bytes[st] = tc_slab_bytes(a.kind[st]);
+  }
+  const int N = tc_ncols_pad(4 * batch);
+  a.KSL = tc_k_slabs(L.n);
+  a.items = tc_row_blocks(L.m_local()) * a.KSL * std::uint32_t(a.nst);
+  a.bimg = bimg;
+  a.b_bytes = 9u * std::uint32_t(N) * 32u;
+  a.zacc = zacc;
+  a.rows_pad = rows_pad;
+  a.m_local = L.m_local();
+  a.ncols = 4 * batch;
+  a.smem_bytes = std::uint32_t(kSmemBytes);
+  a.lut_e8p = L.lut_e8p;
+  a.lut_e81 = L.lut_e81;
+  // TMEM: G decode groups x 2 A buffers x 72 columns + 2 accumulators x stages x N <= 512
+  auto fits = [&](int G) { return G * 2 * int(kAcols) + 2 * a.nst * N <= 512; };
+  switch (N) {
+    case 8: launch_ng<8, 3>(a, s); break;
+    case 16: launch_ng<16, 3>(a, s); break;
+    case 32: fits(3) ? launch_ng<32, 3>(a, s) : launch_ng<32, 2>(a, s); break;
+    case 48: launch_ng<48, 2>(a, s); break;
+    default: fits(2) ? launch_ng<64, 2>(a, s) : launch_ng<64, 1>(a, s); break;
+  }
+  cuda_check(cudaGetLastError(), "gemv_tc launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+}  // namespace q8p::detail
