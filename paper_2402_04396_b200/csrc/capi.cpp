@@ -140,10 +140,8 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
     setup_side(L.get(), L->side_u, d.m, d.signs_u);
     setup_side(L.get(), L->side_v, d.n, d.signs_v);
     {
-      std::vector<std::uint32_t> e8p, e81;
-      tc_tables(e8p, e81);
-      L->lut_e8p = static_cast<const std::uint32_t*>(upload(L.get(), e8p.data(), e8p.size() * 4));
-      L->lut_e81 = static_cast<const std::uint32_t*>(upload(L.get(), e81.data(), e81.size() * 4));
+      const std::vector<std::uint8_t> img = tc_lut_image();
+      L->lut_img = static_cast<const std::uint8_t*>(upload(L.get(), img.data(), img.size()));
     }
     const std::size_t nb = d.n / 8, words = std::size_t(r1 - r0) * nb;
     for (int s = 0; s < d.num_stages; ++s) {

@@ -72,8 +72,7 @@ struct q8p_layer {
   q8p::detail::DevSide side_u, side_v;  // left (m) / right (n)
   void* codes[2] = {nullptr, nullptr};  // plain [m_local][n/8]: u16 (E8P) / u8 (e8-1bit)
   q8p::detail::SlabCodes tc[2];
-  const std::uint32_t* lut_e8p = nullptr;  // device [256]   (tensor-core GEMV tables)
-  const std::uint32_t* lut_e81 = nullptr;  // device [256][2]
+  const std::uint8_t* lut_img = nullptr;   // device 64 KiB lane-replicated decode LUT (gemv_tc.cu)
   std::size_t device_bytes = 0;
   std::size_t code_bytes = 0;
   std::vector<void*> allocations;
@@ -98,7 +97,7 @@ void launch_gemv_simple(const q8p_layer& L, const float* t, float* z, int batch,
 void launch_decode(const q8p_layer& L, int stage, float* w, cudaStream_t s);
 
 // Tensor-core path (gemv_tc.cu, kernels_rht.cu).
-void tc_tables(std::vector<std::uint32_t>& e8p, std::vector<std::uint32_t>& e81);
+std::vector<std::uint8_t> tc_lut_image();  // the 64 KiB smem LUT window, bulk-copied per CTA
 std::uint32_t tc_slab_bytes(int kind);
 std::uint32_t tc_row_blocks(std::uint32_t m_local);
 std::uint32_t tc_k_slabs(std::uint32_t n);

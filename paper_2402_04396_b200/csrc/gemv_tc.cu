@@ -47,7 +47,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <string>
+#include <vector>
 #include <mutex>
 
 #include "device.hpp"
@@ -61,14 +65,14 @@ constexpr int kSlabCw = 32;                 // codewords per slab row
 constexpr std::uint32_t kE8pSlab = 4 * 2048 + 512;
 constexpr std::uint32_t kE81Slab = 2 * 2048;
 constexpr std::uint32_t kAcols = 72;        // TMEM columns per A buffer (64 main + 8 side)
-constexpr int kWarpProd = 0, kWarpMma = 1, kWarpDec = 6;  // warps 2..5: epilogue
+constexpr int kWarpProd = 0;                // warps 1..4G: G decode groups
 constexpr int kMaxStages = 24;
 constexpr std::uint32_t kCtl = 1024;        // control block (barriers) at the smem base
 constexpr std::size_t kSmemBytes = 200 * 1024;
 
 template <int G>
 struct Roles {
-  static constexpr int kThreads = (kWarpDec + 4 * G) * 32;
+  static constexpr int kThreads = (1 + 4 * G) * 32;
 };
 
 struct TcArgs {
@@ -84,9 +88,20 @@ struct TcArgs {
   std::uint32_t rows_pad, m_local;
   int ncols;                      // used B rows (limbs x batch)
   std::uint32_t smem_bytes;
-  const std::uint32_t* lut_e8p;   // [256]
-  const std::uint32_t* lut_e81;   // [512]
+  const std::uint8_t* lut_img;    // 64 KiB LUT window image (tc_lut_image)
+  unsigned long long* trace;      // debug timeline (Q8P_TRACE), CTA 0 only; nullptr = off
 };
+
+// Debug timeline: trace[role][item][4] clock64 stamps (roles 0..7 decoder
+// groups, 8 MMA issuer, 9 producer); written by CTA 0 when a.trace != nullptr.
+constexpr int kTraceItems = 128;
+__device__ __forceinline__ void tstamp(const TcArgs& a, int role, std::uint32_t item, int ev) {
+#ifndef Q8P_K2_TRACE
+  return;
+#endif
+  if (a.trace != nullptr && blockIdx.x == 0 && item < kTraceItems && (threadIdx.x & 31) == 0)
+    a.trace[(role * kTraceItems + item) * 4 + ev] = clock64();
+}
 
 __device__ __forceinline__ std::uint32_t lds32(std::uint32_t addr) {
   std::uint32_t r;
@@ -120,8 +135,8 @@ constexpr std::uint32_t kCtHi = 0x00FBFDFFu;  // {-1,-3,-5,0}
 // A bytes of one E8P codeword: slot jj (0..3) of an idx / flag register pair.
 // `lb` = LUT window bytes 2..3 | lane * 4: PRMT drops idx into byte 1.
 template <int JJ>
-__device__ __forceinline__ void e8p_a(std::uint32_t idxreg, std::uint32_t fl, std::uint32_t lb, std::uint32_t& lo,
-                                      std::uint32_t& hi) {
+__device__ __forceinline__ void e8p_a(std::uint32_t idxreg, std::uint32_t fl, std::uint32_t lb, std::uint32_t ct_lo,
+                                      std::uint32_t ct_hi, std::uint32_t& lo, std::uint32_t& hi) {
   const std::uint32_t nib = lds32(prmt(idxreg, lb, 0x7604u | (std::uint32_t(JJ) << 4)));
   std::uint32_t rs;
   if constexpr (JJ == 0)
@@ -133,28 +148,28 @@ __device__ __forceinline__ void e8p_a(std::uint32_t idxreg, std::uint32_t fl, st
   else
     rs = __umulhi(fl, 0x80000000u);  // fl >> 1 on the FMA pipe
   const std::uint32_t sel = nib ^ (rs & 0x44444444u);
-  lo = prmt(kCtLo, kCtHi, sel);
-  hi = prmt(kCtLo, kCtHi, __umulhi(sel, 65536u));  // sel >> 16
+  lo = prmt(ct_lo, ct_hi, sel);
+  hi = prmt(ct_lo, ct_hi, __umulhi(sel, 65536u));  // sel >> 16
 }
 
 template <int N, int G>
 __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a) {
   extern __shared__ __align__(1024) std::uint8_t smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index via shfl: the compiler then knows every role branch is warp-uniform
+  const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const std::uint32_t sbase = smem_u32(smem);
   const std::uint32_t send = sbase + a.smem_bytes;
   const std::uint32_t lutw = (sbase + kCtl + 0xFFFFu) & ~0xFFFFu;
   // control block: barriers + TMEM base
-  const std::uint32_t bar_full_code = sbase;                  // [kMaxStages]
-  const std::uint32_t bar_full_b = sbase + 8 * kMaxStages;    // [kMaxStages]
-  const std::uint32_t bar_empty = sbase + 16 * kMaxStages;    // [kMaxStages]
-  const std::uint32_t bar_a_full = sbase + 24 * kMaxStages;   // [G][2]
-  const std::uint32_t bar_a_empty = bar_a_full + 8 * 2 * G;   // [G][2]
-  const std::uint32_t bar_d_full = bar_a_empty + 8 * 2 * G;   // [2]
-  const std::uint32_t bar_d_empty = bar_d_full + 16;          // [2]
-  const std::uint32_t tmem_slot = bar_d_empty + 16;
+  const std::uint32_t bar_full = sbase;                       // [kMaxStages] codes + B image landed
+  const std::uint32_t bar_empty = sbase + 8 * kMaxStages;     // [kMaxStages] stage consumed (MMA commit)
+  const std::uint32_t bar_a_empty = sbase + 16 * kMaxStages;  // [G][2] A buffer read by its MMAs
+  const std::uint32_t bar_d_full = bar_a_empty + 8 * 2 * G;   // [G] accumulator final for a row block
+  const std::uint32_t bar_lut = bar_d_full + 8 * G;           // LUT window landed
+  const std::uint32_t tmem_slot = bar_lut + 8;
+  const std::uint32_t ct_slot = tmem_slot + 8;  // the constant byte table, read back by the decoders
   // ring: stages below the LUT window, then above it
-  const std::uint32_t stage_bytes = ((a.nst > 0 ? kE8pSlab : 0) + a.b_bytes + 127) & ~127u;
+  const std::uint32_t stage_bytes = (kE8pSlab + a.b_bytes + 127) & ~127u;
   const std::uint32_t lo_base = sbase + kCtl;
   const std::uint32_t n_lo = lutw > lo_base ? (lutw - lo_base) / stage_bytes : 0;
   const std::uint32_t hi_base = lutw + 65536;
@@ -169,51 +184,67 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
 
   if (threadIdx.x == 0) {
     for (std::uint32_t i = 0; i < S; ++i) {
-      mbar_init(bar_full_code + 8 * i, 1);
-      mbar_init(bar_full_b + 8 * i, 1);
+      mbar_init(bar_full + 8 * i, 1);
       mbar_init(bar_empty + 8 * i, 1);
     }
-    for (int i = 0; i < 2 * G; ++i) {
-      mbar_init(bar_a_full + 8 * i, 128);
-      mbar_init(bar_a_empty + 8 * i, 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(bar_d_full + 8 * i, 1);
-      mbar_init(bar_d_empty + 8 * i, 128);
-    }
+    for (int i = 0; i < 2 * G; ++i) mbar_init(bar_a_empty + 8 * i, 1);
+    for (int i = 0; i < G; ++i) mbar_init(bar_d_full + 8 * i, 1);
+    mbar_init(bar_lut, 1);
     fence_mbar_init();
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n" ::"r"(ct_slot), "r"(kCtLo), "r"(kCtHi) : "memory");
   }
-  if (warp == kWarpMma) tmem_alloc<512>(tmem_slot);
+  if (warp == kWarpProd) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const std::uint32_t tbase = *reinterpret_cast<volatile std::uint32_t*>(smem + (tmem_slot - sbase));
-  const std::uint32_t dcol0 = std::uint32_t(G) * 2 * kAcols;
 
   if (warp == kWarpProd) {
-    // ===== producer =====
-    if (lane == 0 && count > 0) {
+    // ===== producer (whole warp, lane-elected issue) =====
+    if (count > 0) {
       const std::uint64_t pol = policy_evict_first();
-      auto issue_code = [&](std::uint32_t i, std::uint32_t st) {
-        const std::uint32_t it = it0 + i, u = it / nst, s = it - u * nst;
-        mbar_arrive_expect_tx(bar_full_code + 8 * st, (s ? a.slab_bytes[1] : a.slab_bytes[0]));
-        bulk_g2s_hint(stage_addr(st), (s ? a.codes[1] : a.codes[0]) + std::size_t(u) * (s ? a.slab_bytes[1] : a.slab_bytes[0]), (s ? a.slab_bytes[1] : a.slab_bytes[0]),
-                      bar_full_code + 8 * st, pol);
+      // item -> (u = row block * KSL + k slab, stage s); ks = u % KSL
+      std::uint32_t s = it0 % nst, u = it0 / nst, ks = u % a.KSL;
+      auto issue_code = [&](std::uint32_t st) {
+        const std::uint32_t sb = s ? a.slab_bytes[1] : a.slab_bytes[0];
+        mbar_arrive_expect_tx_e(bar_full + 8 * st, sb + a.b_bytes);
+        bulk_g2s_hint_e(stage_addr(st), (s ? a.codes[1] : a.codes[0]) + std::size_t(u) * sb, sb, bar_full + 8 * st, pol);
       };
-      auto issue_b = [&](std::uint32_t i, std::uint32_t st) {
-        const std::uint32_t u = (it0 + i) / nst, ks = u % a.KSL;
-        mbar_arrive_expect_tx(bar_full_b + 8 * st, a.b_bytes);
-        bulk_g2s(stage_addr(st) + kE8pSlab, a.bimg + std::size_t(ks) * a.b_bytes, a.b_bytes, bar_full_b + 8 * st);
+      auto issue_b = [&](std::uint32_t st, std::uint32_t k) {
+        bulk_g2s_e(stage_addr(st) + kE8pSlab, a.bimg + std::size_t(k) * a.b_bytes, a.b_bytes, bar_full + 8 * st);
+      };
+      auto advance = [&]() {
+        if (++s == nst) {
+          s = 0;
+          ++u;
+          if (++ks == a.KSL) ks = 0;
+        }
       };
       const std::uint32_t pre = count < S ? count : S;
-      for (std::uint32_t i = 0; i < pre; ++i) issue_code(i, i);
+      const std::uint32_t s0 = s, u0 = u, ks0 = ks;
+      if (pre > 0) issue_code(0), advance();  // first code slab, then the (L2-resident) LUT window
+      mbar_arrive_expect_tx_e(bar_lut, 65536);
+      bulk_g2s_e(lutw, a.lut_img, 65536, bar_lut);
+      for (std::uint32_t i = 1; i < pre; ++i) {
+        issue_code(i);
+        advance();
+      }
+      const std::uint32_t s1 = s, u1 = u, ks1 = ks;
+      s = s0, u = u0, ks = ks0;
       pdl_wait();  // K1's B images (and zeroed accumulators) are visible from here on
-      for (std::uint32_t i = 0; i < pre; ++i) issue_b(i, i);
+      for (std::uint32_t i = 0; i < pre; ++i) {
+        issue_b(i, ks);
+        advance();
+      }
+      s = s1, u = u1, ks = ks1;
       std::uint32_t st = pre == S ? 0 : pre, r = 1;
       for (std::uint32_t i = pre; i < count; ++i) {
+        tstamp(a, 9, i, 0);
         mbar_wait(bar_empty + 8 * st, (r & 1) ^ 1);
-        issue_code(i, st);
-        issue_b(i, st);
+        tstamp(a, 9, i, 1);
+        issue_code(st);
+        issue_b(st, ks);
+        advance();
         if (++st == S) {
           st = 0;
           ++r;
@@ -221,125 +252,49 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
       }
     }
     pdl_trigger();
-  } else if (warp == kWarpMma) {
-    // ===== MMA issuer =====
-    pdl_trigger();
-    if (lane == 0 && count > 0) {
-      constexpr std::uint32_t idesc = idesc_i8(128, N);
-      std::uint32_t prev_rb = 0xFFFFFFFFu, seg = 0, dreg = 0, started = 0;
-      std::uint32_t st = 0, r = 0, g = 0, use = 0;
-      for (std::uint32_t i = 0; i < count; ++i) {
-        const std::uint32_t it = it0 + i, u = it / nst, s = it - u * nst, rb = u / a.KSL;
-        if (rb != prev_rb) {
-          if (prev_rb != 0xFFFFFFFFu) {
-            mma_commit(bar_d_full + 8 * dreg);
-            ++seg;
-          }
-          dreg = seg & 1;
-          mbar_wait(bar_d_empty + 8 * dreg, ((seg >> 1) & 1) ^ 1);
-          tc_fence_after();
-          started = 0;
-          prev_rb = rb;
-        }
-        const std::uint32_t buf = use & 1, bph = (use >> 1) & 1;
-        mbar_wait(bar_a_full + 8 * (2 * g + buf), bph);
-        mbar_wait(bar_full_b + 8 * st, r & 1);
-        tc_fence_after();
-        const std::uint32_t d = tbase + dcol0 + (dreg * nst + s) * N;
-        const std::uint32_t abuf = tbase + (2 * g + buf) * kAcols;
-        const std::uint32_t bsm = stage_addr(st) + kE8pSlab;
-        const std::uint32_t acc0 = (started >> s) & 1;
-#pragma unroll
-        for (int kb = 0; kb < 8; ++kb)
-          mma_i8_ts(d, abuf + 8 * kb, sdesc(bsm + kb * N * 32, 128, 256), idesc, (kb > 0) | acc0);
-        if ((s ? a.kind[1] : a.kind[0]) == 0) mma_i8_ts(d, abuf + 64, sdesc(bsm + 8 * N * 32, 128, 256), idesc, 1);
-        started |= 1u << s;
-        mma_commit(bar_a_empty + 8 * (2 * g + buf));
-        mma_commit(bar_empty + 8 * st);
-        if (++st == S) {
-          st = 0;
-          ++r;
-        }
-        if (++g == G) {
-          g = 0;
-          ++use;
-        }
-      }
-      mma_commit(bar_d_full + 8 * dreg);
-    }
-  } else if (warp < kWarpDec) {
-    // ===== epilogue (lanes 32 (warp % 4) ..) =====
-    pdl_trigger();
-    if (count > 0) {
-      const std::uint32_t q = warp & 3, row_in = q * 32 + lane;
-      const std::uint32_t tl = tbase + ((q * 32) << 16);
-      const std::uint32_t rb0 = (it0 / nst) / a.KSL, rb1 = ((it1 - 1) / nst) / a.KSL;
-      for (std::uint32_t sg = 0; sg <= rb1 - rb0; ++sg) {
-        const std::uint32_t rb = rb0 + sg, dreg = sg & 1;
-        // item range of this segment within [it0, it1)
-        const std::uint32_t ia = std::max(it0, rb * a.KSL * nst), ib = std::min(it1, (rb + 1) * a.KSL * nst);
-        mbar_wait(bar_d_full + 8 * dreg, (sg >> 1) & 1);
-        tc_fence_after();
-        const std::uint32_t row = rb * 128 + row_in;
-        const bool row_ok = row < a.m_local;
-        for (std::uint32_t s = 0; s < nst; ++s) {
-          const bool present = (ib - ia >= nst) || ((ia % nst) == s);
-          std::int32_t* z = a.zacc + std::size_t(s) * N * a.rows_pad + row;
-#pragma unroll
-          for (int c0 = 0; c0 < N; c0 += 8) {
-            std::uint32_t t8[8];
-            tmem_ld8(tl + dcol0 + (dreg * nst + s) * N + c0, t8);
-            tmem_wait_ld();
-            if (present && row_ok) {
-#pragma unroll
-              for (int j = 0; j < 8; ++j)
-                if (c0 + j < a.ncols) atomicAdd(z + std::size_t(c0 + j) * a.rows_pad, std::int32_t(t8[j]));
-            }
-          }
-        }
-        tc_fence_before();
-        mbar_arrive(bar_d_empty + 8 * dreg);
-      }
-    }
   } else {
-    // ===== decoders =====
-    // LUT: E8P nibbles replicated per lane (bytes [0,128) of each 256-B row),
-    // e8-1bit rows replicated per half-warp lane (bytes [128,256)).
-    const int dt = threadIdx.x - kWarpDec * 32;
+    // ===== decode groups: decode -> TMEM A, one warp per group issues the MMAs =====
     constexpr int kDecThreads = 4 * G * 32;
-    for (int i = dt; i < 256 * 16; i += kDecThreads) {
-      const int row = i >> 4, part = i & 15;
-      uint4 v;
-      if (part < 8) {
-        const std::uint32_t e = a.lut_e8p[row];
-        v = make_uint4(e, e, e, e);
-      } else {
-        const std::uint32_t e0 = a.lut_e81[2 * row], e1 = a.lut_e81[2 * row + 1];
-        v = make_uint4(e0, e1, e0, e1);
-      }
-      sts128(lutw + row * 256 + part * 16, v);
-    }
-    asm volatile("bar.sync 1, %0;\n" ::"n"(kDecThreads) : "memory");
+    (void)kDecThreads;
     pdl_trigger();
-    const int grp = (warp - kWarpDec) >> 2;
+    const int grp = (warp - 1) >> 2;
+    const bool issuer = ((warp - 1) & 3) == 0;
     const std::uint32_t q = warp & 3, row_in = q * 32 + lane;
     const std::uint32_t tl = (q * 32) << 16;
     const std::uint32_t lb = (lutw & 0xFFFF0000u) | (std::uint32_t(lane) * 4u);
     const std::uint32_t lb8 = (lutw & 0xFFFF0000u) | (128u + std::uint32_t(lane & 15) * 8u);
-    std::uint32_t st = std::uint32_t(grp) % S, r = std::uint32_t(grp) / S, use = 0;
+    const std::uint32_t dcol = tbase + std::uint32_t(G) * 2 * kAcols + std::uint32_t(grp) * nst * N;
+    const std::uint32_t per_rb = a.KSL * nst;
+    const std::uint64_t dhi = sdesc(0, 128, 256);
+    constexpr std::uint32_t idesc = idesc_i8(128, N);
+    // this group's items: i = grp, grp + G, ...; position j within the row block
+    std::uint32_t st = std::uint32_t(grp) % S, r = std::uint32_t(grp) / S, use = 0, seg = 0, started = 0;
+    std::uint32_t j = (it0 + grp) % per_rb, rb = (it0 + grp) / per_rb;
+    const std::uint32_t barg = 1 + grp;  // named barrier of this group
+    // constant byte table {+1,+3,+5,_ | -1,-3,-5,_} loaded from smem so it lives
+    // in ONE register (as an immediate/uniform value ptxas re-materialises it
+    // with a UR->R move in front of every PRMT: +1 instruction per codeword)
+    const uint2 ct = lds64(ct_slot);
+    const std::uint32_t ct_lo = ct.x, ct_hi = ct.y;
+    if (count > 0) mbar_wait(bar_lut, 0);  // the producer copies the LUT only when it has work
     for (std::uint32_t i = grp; i < count; i += G) {
-      const std::uint32_t it = it0 + i, s = it % nst;
+      const std::uint32_t s = j & (nst - 1);  // nst in {1, 2}
       const std::uint32_t buf = use & 1, bph = (use >> 1) & 1;
       const std::uint32_t sa = stage_addr(st);
-      mbar_wait(bar_full_code + 8 * st, r & 1);
+      const bool e8p = (s ? a.kind[1] : a.kind[0]) == 0;
+      const bool tw = q == 1;
+      if (tw) tstamp(a, grp, i, 0);
+      mbar_wait(bar_full + 8 * st, r & 1);
+      if (tw) tstamp(a, grp, i, 1);
       const std::uint32_t abuf = tbase + tl + (2 * grp + buf) * kAcols;
-      if ((s ? a.kind[1] : a.kind[0]) == 0) {
+      if (e8p) {
         const uint4 i0 = lds128(sa + row_in * 16), i1 = lds128(sa + 2048 + row_in * 16);
         const uint4 f0 = lds128(sa + 4096 + row_in * 16), f1 = lds128(sa + 6144 + row_in * 16);
         const std::uint32_t sw = lds32(sa + 8192 + row_in * 4);
         const std::uint32_t idx[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
         const std::uint32_t fl[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
         mbar_wait(bar_a_empty + 8 * (2 * grp + buf), bph ^ 1);
+        if (tw) tstamp(a, grp, i, 2);
         tc_fence_after();
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) {
@@ -347,10 +302,10 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int g4 = 2 * qq + h;  // codewords 4 g4 .. 4 g4 + 3
-            e8p_a<0>(idx[g4], fl[g4], lb, o[8 * h + 0], o[8 * h + 1]);
-            e8p_a<1>(idx[g4], fl[g4], lb, o[8 * h + 2], o[8 * h + 3]);
-            e8p_a<2>(idx[g4], fl[g4], lb, o[8 * h + 4], o[8 * h + 5]);
-            e8p_a<3>(idx[g4], fl[g4], lb, o[8 * h + 6], o[8 * h + 7]);
+            e8p_a<0>(idx[g4], fl[g4], lb, ct_lo, ct_hi, o[8 * h + 0], o[8 * h + 1]);
+            e8p_a<1>(idx[g4], fl[g4], lb, ct_lo, ct_hi, o[8 * h + 2], o[8 * h + 3]);
+            e8p_a<2>(idx[g4], fl[g4], lb, ct_lo, ct_hi, o[8 * h + 4], o[8 * h + 5]);
+            e8p_a<3>(idx[g4], fl[g4], lb, ct_lo, ct_hi, o[8 * h + 6], o[8 * h + 7]);
           }
           tmem_st16(abuf + 16 * qq, o);
         }
@@ -386,18 +341,63 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(bar_a_full + 8 * (2 * grp + buf));
+      // row block ends with this group's item?  (next item of the group is past it)
+      const bool last_in_rb = (j + G >= per_rb) || (i + G >= count);
+      asm volatile("bar.sync %0, 128;\n" ::"r"(barg) : "memory");
+      if (issuer) {
+        tc_fence_after();
+        const std::uint64_t bd = dhi | (((sa + kE8pSlab) >> 4) & 0x3FFFu);
+        mma_i8_slab_e<2 * N>(dcol + s * N, abuf - tl, bd, idesc, (started >> s) & 1, e8p,
+                             bar_a_empty + 8 * (2 * grp + buf), bar_empty + 8 * st);
+        if (last_in_rb) mma_commit_e(bar_d_full + 8 * grp);
+        if (tw) tstamp(a, grp, i, 3);
+      }
+      started |= 1u << s;
+      if (last_in_rb) {
+        // epilogue of this row block: D (int32, exact) -> global accumulators
+        mbar_wait(bar_d_full + 8 * grp, seg & 1);
+        tc_fence_after();
+        const std::uint32_t row = rb * 128 + row_in;
+        const bool row_ok = row < a.m_local;
+        const std::uint32_t ia = std::max(it0, rb * per_rb), ib = std::min(it1, (rb + 1) * per_rb);
+        for (std::uint32_t s2 = 0; s2 < nst; ++s2) {
+          // stage s2 got at least one item from this group in this row block?
+          if (!((started >> s2) & 1)) continue;
+          (void)ia;
+          (void)ib;
+          std::int32_t* z = a.zacc + std::size_t(s2) * N * a.rows_pad + row;
+#pragma unroll
+          for (int c0 = 0; c0 < N; c0 += 8) {
+            std::uint32_t t8[8];
+            tmem_ld8(dcol + tl + s2 * N + c0, t8);
+            tmem_wait_ld();
+            if (row_ok) {
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj)
+                if (c0 + jj < a.ncols) atomicAdd(z + std::size_t(c0 + jj) * a.rows_pad, std::int32_t(t8[jj]));
+            }
+          }
+        }
+        tc_fence_before();
+        started = 0;
+        ++seg;
+      }
       ++use;
       st += G;
       while (st >= S) {
         st -= S;
         ++r;
       }
+      j += G;
+      while (j >= per_rb) {
+        j -= per_rb;
+        ++rb;
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == kWarpMma) {
+  if (warp == kWarpProd) {
     tc_fence_after();
     tmem_dealloc<512>(tbase);
   }
@@ -432,18 +432,25 @@ void launch_ng(const TcArgs& a, cudaStream_t s) {
 }  // namespace
 
 // ---- host: tables and slab transcoding ---------------------------------------
-void tc_tables(std::vector<std::uint32_t>& e8p, std::vector<std::uint32_t>& e81) {
+// 64 KiB shared-memory LUT window, 256 rows of 256 B (row = idx, 64-KiB aligned
+// in smem so a PRMT of (window, idx byte, lane) forms the LDS address):
+//   bytes [0, 128):   E8P magnitude nibbles of row idx (d = 1,3,5 -> 0,1,2 at
+//                     bits 4c), replicated once per lane (lane * 4)
+//   bytes [128, 256): e8-1bit doubled row (8 x s8), replicated per half-warp lane
+std::vector<std::uint8_t> tc_lut_image() {
   const E8PTable& t = e8p_table();
-  e8p.assign(256, 0);
+  const auto& d = e8_1bit_doubled();
+  std::vector<std::uint8_t> img(65536, 0);
   for (int i = 0; i < 256; ++i) {
     std::uint32_t w = 0;
-    for (int c = 0; c < 8; ++c) w |= std::uint32_t((t.doubled[i][c] - 1) / 2) << (4 * c);  // 1,3,5 -> 0,1,2
-    e8p[i] = w;
+    for (int c = 0; c < 8; ++c) w |= std::uint32_t((t.doubled[i][c] - 1) / 2) << (4 * c);
+    std::uint8_t e81[8];
+    for (int c = 0; c < 8; ++c) e81[c] = std::uint8_t(d[i][c]);
+    std::uint8_t* row = img.data() + i * 256;
+    for (int l = 0; l < 32; ++l) std::memcpy(row + 4 * l, &w, 4);
+    for (int l = 0; l < 16; ++l) std::memcpy(row + 128 + 8 * l, e81, 8);
   }
-  e81.assign(512, 0);
-  const auto& d = e8_1bit_doubled();
-  for (int i = 0; i < 256; ++i)
-    for (int c = 0; c < 8; ++c) e81[2 * i + c / 4] |= (std::uint32_t(std::uint8_t(d[i][c])) << (8 * (c % 4)));
+  return img;
 }
 
 std::uint32_t tc_slab_bytes(int kind) { return kind == 0 ? kE8pSlab : kE81Slab; }
@@ -519,18 +526,37 @@ void launch_gemv_tc(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* 
   a.m_local = L.m_local();
   a.ncols = 4 * batch;
   a.smem_bytes = std::uint32_t(kSmemBytes);
-  a.lut_e8p = L.lut_e8p;
-  a.lut_e81 = L.lut_e81;
-  // TMEM: G decode groups x 2 A buffers x 72 columns + 2 accumulators x stages x N <= 512
-  auto fits = [&](int G) { return G * 2 * int(kAcols) + 2 * a.nst * N <= 512; };
+  a.lut_img = L.lut_img;
+  static const char* trace_env = std::getenv("Q8P_TRACE");  // debug: dump CTA 0's timeline
+  unsigned long long* tr = nullptr;
+  if (trace_env != nullptr) {
+    cuda_check(cudaMalloc(&tr, 16 * kTraceItems * 4 * 8), "trace alloc");
+    cuda_check(cudaMemset(tr, 0, 16 * kTraceItems * 4 * 8), "trace memset");
+  }
+  a.trace = tr;
+  // TMEM: G decode groups x (2 A buffers x 72 columns + an accumulator of stages x N) <= 512
+  auto fits = [&](int G) { return G * (2 * int(kAcols) + a.nst * N) <= 512; };
   switch (N) {
     case 8: launch_ng<8, 3>(a, s); break;
-    case 16: launch_ng<16, 3>(a, s); break;
-    case 32: fits(3) ? launch_ng<32, 3>(a, s) : launch_ng<32, 2>(a, s); break;
+    case 16: fits(3) ? launch_ng<16, 3>(a, s) : launch_ng<16, 2>(a, s); break;
+    case 32: launch_ng<32, 2>(a, s); break;
     case 48: launch_ng<48, 2>(a, s); break;
     default: fits(2) ? launch_ng<64, 2>(a, s) : launch_ng<64, 1>(a, s); break;
   }
   cuda_check(cudaGetLastError(), "gemv_tc launch");
+  if (tr != nullptr) {
+    std::vector<unsigned long long> h(16 * kTraceItems * 4);
+    cuda_check(cudaStreamSynchronize(s), "trace sync");
+    cuda_check(cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost), "trace copy");
+    cudaFree(tr);
+    static int seq = 0;
+    const std::string path = std::string(trace_env) + "." + std::to_string(seq++) + "." + std::to_string(L.m_local()) +
+                             "x" + std::to_string(L.n) + ".bin";
+    if (FILE* f = std::fopen(path.c_str(), "wb")) {
+      std::fwrite(h.data(), 8, h.size(), f);
+      std::fclose(f);
+    }
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 

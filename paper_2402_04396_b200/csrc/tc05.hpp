@@ -43,9 +43,18 @@ __device__ __forceinline__ bool mbar_try_wait(std::uint32_t bar, std::uint32_t p
       : "memory");
   return ok != 0;
 }
+// Spin inside the asm: a C++ retry loop makes the compiler treat everything
+// after the wait as potentially divergent (per-lane predicate), which demotes
+// uniform values to per-lane registers (R2UR + VOTEU in front of every
+// tcgen05 / bulk-copy issue).
 __device__ __forceinline__ void mbar_wait(std::uint32_t bar, std::uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
-  }
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
 }
 
 // ---- bulk async copy global -> shared (completes on an mbarrier) --------------
@@ -158,6 +167,88 @@ __device__ __forceinline__ void mma_f16_ss(std::uint32_t d_tmem, std::uint64_t a
 __device__ __forceinline__ void mma_commit(std::uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
                : "memory");
+}
+// ---- warp-converged, lane-elected issue -------------------------------------
+// Executed by ALL 32 lanes of a converged warp; `elect.sync` picks one lane
+// inside the asm.  Issuing tcgen05/bulk-copy instructions from a divergent
+// `if (lane == 0)` region makes the compiler wrap each one in a BRA.U.ANY
+// waterfall loop (R2UR per operand): measured 44-80 cycles per tcgen05.mma
+// vs 14 cycles converged (tools/ubench_tc.cu, B200).
+__device__ __forceinline__ void mma_i8_ts_e(std::uint32_t d_tmem, std::uint32_t a_tmem, std::uint64_t b_desc,
+                                            std::uint32_t idesc, std::uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// One slab of a K-major kind::i8 product, lane-elected once: 8 MMAs walking K
+// (A: +8 TMEM columns = 32 B of K, B: +b_step descriptor units of 16 B),
+// accumulate predicate on the first, then (when `side`) a 9th MMA with A at
+// column 64 and B at 8 * b_step, then two commits.  All in one asm block so
+// the issue costs one elect and no per-MMA predicate plumbing.
+template <int BStep>
+__device__ __forceinline__ void mma_i8_slab_e(std::uint32_t d, std::uint32_t a, std::uint64_t bdesc,
+                                              std::uint32_t idesc, std::uint32_t acc, std::uint32_t side,
+                                              std::uint32_t bar0, std::uint32_t bar1) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, q;\n\t.reg .b64 b;\n\t.reg .b32 x;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t"
+      "add.s32 x, %1, 8;\n\tadd.s64 b, %2, %8;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [x], b, %3, 1;\n\t"
+      "add.s32 x, %1, 16;\n\tadd.s64 b, %2, %9;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [x], b, %3, 1;\n\t"
+      "add.s32 x, %1, 24;\n\tadd.s64 b, %2, %10;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [x], b, %3, 1;\n\t"
+      "add.s32 x, %1, 32;\n\tadd.s64 b, %2, %11;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [x], b, %3, 1;\n\t"
+      "add.s32 x, %1, 40;\n\tadd.s64 b, %2, %12;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [x], b, %3, 1;\n\t"
+      "add.s32 x, %1, 48;\n\tadd.s64 b, %2, %13;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [x], b, %3, 1;\n\t"
+      "add.s32 x, %1, 56;\n\tadd.s64 b, %2, %14;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [x], b, %3, 1;\n\t"
+      "add.s32 x, %1, 64;\n\tadd.s64 b, %2, %15;\n\t"
+      "and.pred q, q, e;\n\t"
+      "@q tcgen05.mma.cta_group::1.kind::i8 [%0], [x], b, %3, 1;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t"
+      "}\n" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc), "r"(side), "r"(bar0), "r"(bar1), "n"(1 * BStep), "n"(2 * BStep),
+      "n"(3 * BStep), "n"(4 * BStep), "n"(5 * BStep), "n"(6 * BStep), "n"(7 * BStep), "n"(8 * BStep)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_e(std::uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_e(std::uint32_t bar, std::uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b64 st;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}\n" ::"r"(bar),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_e(std::uint32_t dst, const void* src, std::uint32_t bytes, std::uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t}\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_hint_e(std::uint32_t dst, const void* src, std::uint32_t bytes,
+                                                std::uint32_t bar, std::uint64_t policy) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+      "%4;\n\t}\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+      : "memory");
 }
 #endif  // __CUDACC__
 

@@ -1,0 +1,148 @@
+// Microbenchmark: tcgen05.mma kind::i8 issue/drain rate at small N, A in TMEM
+// vs A in smem, and tcgen05.st throughput.  Not part of the product; run with
+//   nvcc -std=c++20 -O3 -gencode arch=compute_100a,code=sm_100a -I paper_2402_04396_b200/csrc tools/ubench_tc.cu -o /tmp/ub && /tmp/ub
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "tc05.hpp"
+using namespace q8p::detail::tc05;
+
+__device__ __forceinline__ std::uint64_t sdesc_ss(std::uint32_t saddr, std::uint32_t lbo, std::uint32_t sbo) {
+  return sdesc(saddr, lbo, sbo);
+}
+__device__ __forceinline__ void mma_i8_ts_elect(std::uint32_t d, std::uint32_t a, std::uint64_t b, std::uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, 1;\n\t}\n" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_ss(std::uint32_t d, std::uint64_t a, std::uint64_t b, std::uint32_t idesc,
+                                          std::uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+template <int N, bool TS, int R = 1, bool WARP = false>
+__global__ void __launch_bounds__(128, 1) k_mma(int groups, int per_group, unsigned long long* out) {
+  extern __shared__ __align__(1024) std::uint8_t smem[];
+  const std::uint32_t sb = smem_u32(smem);
+  const std::uint32_t bar = sb, slot = sb + 8;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<std::uint32_t*>(smem + 1024)[i] = 0x01010101u;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  fence_proxy_async_smem();
+  const std::uint32_t tb = *reinterpret_cast<volatile std::uint32_t*>(smem + 8);
+  if (WARP ? warp == 0 : threadIdx.x == 0) {
+    constexpr std::uint32_t idesc = idesc_i8(128, N);
+    const std::uint32_t bsm = sb + 1024, asm_ = sb + 1024 + 16384;
+    std::uint64_t bd[8], ad[8];
+    std::uint32_t dd[8], at[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      bd[k] = sdesc(bsm + k * N * 32, 128, 256);
+      ad[k] = sdesc(asm_ + k * 4096, 128, 256);
+      dd[k] = tb + 256 + (k % R) * N;
+      at[k] = tb + 8 * k;
+    }
+    std::uint64_t t0 = clock64();
+    for (int g = 0; g < groups; ++g) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if constexpr (WARP)
+          mma_i8_ts_elect(dd[k], at[k], bd[k], idesc);
+        else if constexpr (TS)
+          mma_i8_ts(dd[k], at[k], bd[k], idesc, 1);
+        else
+          mma_i8_ss(dd[k], ad[k], bd[k], idesc, 1);
+      }
+    }
+    if (!WARP || (threadIdx.x & 31) == 0) mma_commit(bar);
+    mbar_wait(bar, 0);
+    std::uint64_t t1 = clock64();
+    if (blockIdx.x == 0) out[0] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tb);
+  }
+}
+
+// 4 warps store x16 columns repeatedly into TMEM.
+__global__ void __launch_bounds__(128, 1) k_sttm(int iters, unsigned long long* out) {
+  __shared__ std::uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc<512>(smem_u32(&slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tb = slot + (std::uint32_t(warp * 32) << 16);
+  std::uint32_t v[16];
+  for (int i = 0; i < 16; ++i) v[i] = threadIdx.x * i;
+  std::uint64_t t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_st16(tb + (it & 3) * 64 + 16 * c, v);
+    v[0] += it;
+  }
+  tmem_wait_st();
+  std::uint64_t t1 = clock64();
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = t1 - t0;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(slot);
+  }
+}
+
+template <int N, bool TS, int R = 1, bool WARP = false>
+void run(unsigned long long* d) {
+  const int groups = 2000, per = 8;
+  auto k = k_mma<N, TS, R, WARP>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  k<<<148, 128, 100 * 1024>>>(groups, per, d);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  k<<<148, 128, 100 * 1024>>>(groups, per, d);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  unsigned long long c;
+  cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+  printf("mma i8 M=128 N=%d K=32 R=%d warp=%d %s: %.1f cyc/mma  (%.1f us total, err=%s)\n", N, R, int(WARP), TS ? "A=TMEM" : "A=SMEM",
+         double(c) / (groups * per), ms * 1e3, cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  unsigned long long* d;
+  cudaMalloc(&d, 64);
+  run<8, true, 1>(d);
+  run<8, true, 1, true>(d);
+  run<16, true, 1, true>(d);
+  run<64, true, 1, true>(d);
+  run<128, true, 1, true>(d);
+  run<256, true, 1, true>(d);
+  k_sttm<<<148, 128>>>(4000, d);
+  cudaDeviceSynchronize();
+  unsigned long long c;
+  cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+  printf("sttm x16 (4 warps): %.1f cyc per 4x x16 round => %.1f B/cyc\n", double(c) / 4000,
+         4.0 * 4 * 32 * 16 * 4 / (double(c) / 4000));
+  return 0;
+}
