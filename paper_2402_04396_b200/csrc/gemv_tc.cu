@@ -63,16 +63,21 @@ using namespace tc05;
 
 constexpr int kSlabCw = 32;                 // codewords per slab row
 constexpr std::uint32_t kE8pSlab = 4 * 2048 + 512;
+constexpr std::uint32_t kCodeSlot = kE8pSlab;  // code ring slot (e8-1bit slabs are smaller)
+constexpr std::uint32_t kMaxB = 12;            // B-image ring slots (max, all groups)
 constexpr std::uint32_t kE81Slab = 2 * 2048;
 constexpr std::uint32_t kAcols = 72;        // TMEM columns per A buffer (64 main + 8 side)
-constexpr int kWarpProd = 0;                // warps 1..4G: G decode groups
-constexpr int kMaxStages = 24;
+constexpr int kWarpProd = 0, kWarpMma = 1;  // warps 1..G: one MMA issuer per decode group; then 4G decoder warps
+constexpr int kMaxStages = 32;
 constexpr std::uint32_t kCtl = 1024;        // control block (barriers) at the smem base
-constexpr std::size_t kSmemBytes = 200 * 1024;
+constexpr std::size_t kSmemBytes = 227 * 1024;
 
 template <int G>
 struct Roles {
-  static constexpr int kThreads = (1 + 4 * G) * 32;
+  static constexpr int kWarpDec = 1 + G;
+  static constexpr int kThreads = (kWarpDec + 4 * G) * 32;
+  template <int N>
+  static constexpr std::uint32_t kBg = N <= 8 ? 3 : (N <= 16 ? 2 : 1);  // B-image ring slots per group
 };
 
 struct TcArgs {
@@ -161,33 +166,57 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
   const std::uint32_t send = sbase + a.smem_bytes;
   const std::uint32_t lutw = (sbase + kCtl + 0xFFFFu) & ~0xFFFFu;
   // control block: barriers + TMEM base
-  const std::uint32_t bar_full = sbase;                       // [kMaxStages] codes + B image landed
-  const std::uint32_t bar_empty = sbase + 8 * kMaxStages;     // [kMaxStages] stage consumed (MMA commit)
-  const std::uint32_t bar_a_empty = sbase + 16 * kMaxStages;  // [G][2] A buffer read by its MMAs
-  const std::uint32_t bar_d_full = bar_a_empty + 8 * 2 * G;   // [G] accumulator final for a row block
-  const std::uint32_t bar_lut = bar_d_full + 8 * G;           // LUT window landed
+  const std::uint32_t bar_full_c = sbase;                       // [kMaxStages] code slab landed
+  const std::uint32_t bar_empty_c = sbase + 8 * kMaxStages;     // [kMaxStages] code slab read (4 warps)
+  const std::uint32_t bar_full_b = sbase + 16 * kMaxStages;     // [kMaxB] B image landed
+  const std::uint32_t bar_empty_b = bar_full_b + 8 * kMaxB;     // [kMaxB] B image read by its MMAs
+  const std::uint32_t bar_a_empty = bar_empty_b + 8 * kMaxB;    // [G][2] A buffer read by its MMAs
+  const std::uint32_t bar_a_full = bar_a_empty + 8 * 2 * G;     // [G][2] A buffer written (4 warp arrivals)
+  const std::uint32_t bar_d_full = bar_a_full + 8 * 2 * G;      // [G] accumulator final for a row block
+  const std::uint32_t bar_lut = bar_d_full + 8 * G;             // LUT window landed
   const std::uint32_t tmem_slot = bar_lut + 8;
   const std::uint32_t ct_slot = tmem_slot + 8;  // the constant byte table, read back by the decoders
-  // ring: stages below the LUT window, then above it
-  const std::uint32_t stage_bytes = (kE8pSlab + a.b_bytes + 127) & ~127u;
+  // B ring right above the LUT window; code ring below the window, then above the B ring
+  const std::uint32_t b_slot = (a.b_bytes + 127) & ~127u;
+  constexpr std::uint32_t SBg = Roles<G>::template kBg<N>, SB = SBg * G;  // B ring: [group][slot]
+  constexpr int kWarpDec = Roles<G>::kWarpDec;
+  const std::uint32_t b_base = lutw + 65536;
   const std::uint32_t lo_base = sbase + kCtl;
-  const std::uint32_t n_lo = lutw > lo_base ? (lutw - lo_base) / stage_bytes : 0;
-  const std::uint32_t hi_base = lutw + 65536;
-  std::uint32_t S = n_lo + (send > hi_base ? (send - hi_base) / stage_bytes : 0);
+  const std::uint32_t n_lo = lutw > lo_base ? (lutw - lo_base) / kCodeSlot : 0;
+  const std::uint32_t hi_base = b_base + SB * b_slot;
+  std::uint32_t S = n_lo + (send > hi_base ? (send - hi_base) / kCodeSlot : 0);
   if (S > kMaxStages) S = kMaxStages;
-  auto stage_addr = [&](std::uint32_t st) { return st < n_lo ? lo_base + st * stage_bytes : hi_base + (st - n_lo) * stage_bytes; };
+  auto code_addr = [&](std::uint32_t st) { return st < n_lo ? lo_base + st * kCodeSlot : hi_base + (st - n_lo) * kCodeSlot; };
 
   const std::uint32_t it0 = std::uint32_t((std::uint64_t(a.items) * blockIdx.x) / gridDim.x);
   const std::uint32_t it1 = std::uint32_t((std::uint64_t(a.items) * (blockIdx.x + 1)) / gridDim.x);
   const std::uint32_t count = it1 - it0;
   const std::uint32_t nst = std::uint32_t(a.nst);
 
+  if (threadIdx.x == 0) tstamp(a, 10, 0, 0);
+#ifdef Q8P_K2_TRACE
+  auto gstamp = [&](int ev) {  // per-CTA globaltimer (ns): 0 entry, 1 setup done, 2 work done
+    if (a.trace != nullptr && blockIdx.x < 256) {
+      std::uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[11 * kTraceItems * 4 + blockIdx.x * 4 + ev] = t;
+    }
+  };
+  if (threadIdx.x == 0) gstamp(0);
+#endif
   if (threadIdx.x == 0) {
     for (std::uint32_t i = 0; i < S; ++i) {
-      mbar_init(bar_full + 8 * i, 1);
-      mbar_init(bar_empty + 8 * i, 1);
+      mbar_init(bar_full_c + 8 * i, 1);
+      mbar_init(bar_empty_c + 8 * i, 4);
     }
-    for (int i = 0; i < 2 * G; ++i) mbar_init(bar_a_empty + 8 * i, 1);
+    for (std::uint32_t i = 0; i < SB; ++i) {
+      mbar_init(bar_full_b + 8 * i, 1);
+      mbar_init(bar_empty_b + 8 * i, 1);
+    }
+    for (int i = 0; i < 2 * G; ++i) {
+      mbar_init(bar_a_empty + 8 * i, 1);
+      mbar_init(bar_a_full + 8 * i, 4);
+    }
     for (int i = 0; i < G; ++i) mbar_init(bar_d_full + 8 * i, 1);
     mbar_init(bar_lut, 1);
     fence_mbar_init();
@@ -198,53 +227,36 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
   __syncthreads();
   tc_fence_after();
   const std::uint32_t tbase = *reinterpret_cast<volatile std::uint32_t*>(smem + (tmem_slot - sbase));
+  if (threadIdx.x == 0) tstamp(a, 10, 0, 1);
+#ifdef Q8P_K2_TRACE
+  if (threadIdx.x == 0) gstamp(1);
+#endif
 
   if (warp == kWarpProd) {
-    // ===== producer (whole warp, lane-elected issue) =====
+    // ===== code producer (whole warp, lane-elected issue); codes do not depend on K1 =====
     if (count > 0) {
       const std::uint64_t pol = policy_evict_first();
-      // item -> (u = row block * KSL + k slab, stage s); ks = u % KSL
-      std::uint32_t s = it0 % nst, u = it0 / nst, ks = u % a.KSL;
+      std::uint32_t s = it0 % nst, u = it0 / nst;  // item -> (u = row block * KSL + k slab, stage s)
       auto issue_code = [&](std::uint32_t st) {
         const std::uint32_t sb = s ? a.slab_bytes[1] : a.slab_bytes[0];
-        mbar_arrive_expect_tx_e(bar_full + 8 * st, sb + a.b_bytes);
-        bulk_g2s_hint_e(stage_addr(st), (s ? a.codes[1] : a.codes[0]) + std::size_t(u) * sb, sb, bar_full + 8 * st, pol);
-      };
-      auto issue_b = [&](std::uint32_t st, std::uint32_t k) {
-        bulk_g2s_e(stage_addr(st) + kE8pSlab, a.bimg + std::size_t(k) * a.b_bytes, a.b_bytes, bar_full + 8 * st);
-      };
-      auto advance = [&]() {
+        mbar_arrive_expect_tx_e(bar_full_c + 8 * st, sb);
+        bulk_g2s_hint_e(code_addr(st), (s ? a.codes[1] : a.codes[0]) + std::size_t(u) * sb, sb, bar_full_c + 8 * st, pol);
         if (++s == nst) {
           s = 0;
           ++u;
-          if (++ks == a.KSL) ks = 0;
         }
       };
       const std::uint32_t pre = count < S ? count : S;
-      const std::uint32_t s0 = s, u0 = u, ks0 = ks;
-      if (pre > 0) issue_code(0), advance();  // first code slab, then the (L2-resident) LUT window
+      issue_code(0);  // first code slab, then the (L2-resident) LUT window
       mbar_arrive_expect_tx_e(bar_lut, 65536);
       bulk_g2s_e(lutw, a.lut_img, 65536, bar_lut);
-      for (std::uint32_t i = 1; i < pre; ++i) {
-        issue_code(i);
-        advance();
-      }
-      const std::uint32_t s1 = s, u1 = u, ks1 = ks;
-      s = s0, u = u0, ks = ks0;
-      pdl_wait();  // K1's B images (and zeroed accumulators) are visible from here on
-      for (std::uint32_t i = 0; i < pre; ++i) {
-        issue_b(i, ks);
-        advance();
-      }
-      s = s1, u = u1, ks = ks1;
+      for (std::uint32_t i = 1; i < pre; ++i) issue_code(i);
       std::uint32_t st = pre == S ? 0 : pre, r = 1;
       for (std::uint32_t i = pre; i < count; ++i) {
         tstamp(a, 9, i, 0);
-        mbar_wait(bar_empty + 8 * st, (r & 1) ^ 1);
+        mbar_wait(bar_empty_c + 8 * st, (r & 1) ^ 1);
         tstamp(a, 9, i, 1);
         issue_code(st);
-        issue_b(st, ks);
-        advance();
         if (++st == S) {
           st = 0;
           ++r;
@@ -252,39 +264,107 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
       }
     }
     pdl_trigger();
-  } else {
-    // ===== decode groups: decode -> TMEM A, one warp per group issues the MMAs =====
-    constexpr int kDecThreads = 4 * G * 32;
-    (void)kDecThreads;
+  } else if (warp < kWarpDec) {
+    // ===== MMA issuer of group g (+ its B-image prefetch): items i = g, g + G, ... =====
+    // One issuer per group keeps each accumulator's MMAs on one thread (in-order
+    // accumulate, per-thread commit tracking) and runs the groups' handshakes in
+    // parallel; every per-item quantity is an incremental counter.
     pdl_trigger();
-    const int grp = (warp - 1) >> 2;
-    const bool issuer = ((warp - 1) & 3) == 0;
+    const std::uint32_t g = std::uint32_t(warp - kWarpMma);
+    if (count > g) {
+      constexpr std::uint32_t idesc = idesc_i8(128, N);
+      const std::uint32_t per_rb = a.KSL * nst;
+      const std::uint32_t bb = b_base + g * SBg * b_slot;  // this group's B slots
+      const std::uint32_t fb = bar_full_b + 8 * g * SBg, eb = bar_empty_b + 8 * g * SBg;
+      const std::uint64_t bd0 = sdesc(bb, 128, 256);
+      const std::uint32_t bstep = b_slot >> 4;  // descriptor units per B slot
+      const std::uint32_t n_g = (count - g + G - 1) / G;  // this group's items
+      // B prefetch cursor: (stage, k slab) of the next group item to fetch
+      std::uint32_t bs = (it0 + g) % nst, bks = ((it0 + g) / nst) % a.KSL, bnext = 0, bslot_n = 0;
+      auto issue_b = [&]() {
+        mbar_arrive_expect_tx_e(fb + 8 * bslot_n, a.b_bytes);
+        bulk_g2s_e(bb + bslot_n * b_slot, a.bimg + std::size_t(bks) * a.b_bytes, a.b_bytes, fb + 8 * bslot_n);
+#pragma unroll
+        for (int t = 0; t < G; ++t)
+          if (++bs == nst) {
+            bs = 0;
+            if (++bks == a.KSL) bks = 0;
+          }
+        ++bnext;
+        if (++bslot_n == SBg) bslot_n = 0;
+      };
+      pdl_wait();  // K1's B images (and zeroed accumulators) are visible from here on
+      while (bnext < n_g && bnext < SBg) issue_b();
+      std::uint32_t j = (it0 + g) % per_rb;
+      std::uint32_t buf = 0, bph = 0, started = 0;
+      std::uint32_t bslot = 0, bphase = 0, rslot = 0, rphase = 0;
+      const std::uint32_t dcol_g = tbase + std::uint32_t(G) * 2 * kAcols + g * nst * N;
+      const std::uint32_t acol0 = tbase + 2 * g * kAcols;
+      const std::uint32_t af0 = bar_a_full + 16 * g, ae0 = bar_a_empty + 16 * g;
+      for (std::uint32_t k = 0, i = g; k < n_g; ++k, i += G) {
+        const std::uint32_t s = j & (nst - 1);
+        tstamp(a, 8 + (g == 0 ? 0 : 4 + g), k, 0);
+        mbar_wait(af0 + 8 * buf, bph);
+        mbar_wait(fb + 8 * bslot, bphase);
+        tc_fence_after();
+#ifdef Q8P_EXP_NO_MMA
+        mma_commit_e(ae0 + 8 * buf);
+        mma_commit_e(eb + 8 * bslot);
+#else
+        mma_i8_slab_e<2 * N>(dcol_g + s * N, acol0 + buf * kAcols, bd0 + bslot * bstep, idesc, (started >> s) & 1,
+                             (s ? a.kind[1] : a.kind[0]) == 0, ae0 + 8 * buf, eb + 8 * bslot);
+#endif
+#ifdef Q8P_K2_TRACE_SYNC
+        mbar_wait(ae0 + 8 * buf, bph);  // debug: serialise to time one item's MMAs
+        tstamp(a, 8 + (g == 0 ? 0 : 4 + g), k, 2);
+#endif
+        started |= 1u << s;
+        if ((j + G >= per_rb) || (i + G >= count)) {  // this group's last item of the row block
+          mma_commit_e(bar_d_full + 8 * g);
+          started = 0;
+        }
+        tstamp(a, 8 + (g == 0 ? 0 : 4 + g), k, 3);
+        // refill the slot of the previous group item (its MMAs were issued one item ago)
+        if (k >= 1 && bnext < n_g) {
+          mbar_wait(eb + 8 * rslot, rphase);
+          issue_b();
+          if (++rslot == SBg) rslot = 0, rphase ^= 1;
+        }
+        if (++bslot == SBg) bslot = 0, bphase ^= 1;
+        buf ^= 1;
+        if (buf == 0) bph ^= 1;
+        j += G;
+        while (j >= per_rb) j -= per_rb;
+      }
+    }
+  } else {
+    // ===== decode groups: codes -> A bytes -> TMEM (4 warps = 4 lane quadrants) =====
+    pdl_trigger();
+    const int grp = (warp - kWarpDec) >> 2;
     const std::uint32_t q = warp & 3, row_in = q * 32 + lane;
     const std::uint32_t tl = (q * 32) << 16;
     const std::uint32_t lb = (lutw & 0xFFFF0000u) | (std::uint32_t(lane) * 4u);
     const std::uint32_t lb8 = (lutw & 0xFFFF0000u) | (128u + std::uint32_t(lane & 15) * 8u);
     const std::uint32_t dcol = tbase + std::uint32_t(G) * 2 * kAcols + std::uint32_t(grp) * nst * N;
     const std::uint32_t per_rb = a.KSL * nst;
-    const std::uint64_t dhi = sdesc(0, 128, 256);
-    constexpr std::uint32_t idesc = idesc_i8(128, N);
-    // this group's items: i = grp, grp + G, ...; position j within the row block
     std::uint32_t st = std::uint32_t(grp) % S, r = std::uint32_t(grp) / S, use = 0, seg = 0, started = 0;
     std::uint32_t j = (it0 + grp) % per_rb, rb = (it0 + grp) / per_rb;
-    const std::uint32_t barg = 1 + grp;  // named barrier of this group
     // constant byte table {+1,+3,+5,_ | -1,-3,-5,_} loaded from smem so it lives
     // in ONE register (as an immediate/uniform value ptxas re-materialises it
     // with a UR->R move in front of every PRMT: +1 instruction per codeword)
     const uint2 ct = lds64(ct_slot);
     const std::uint32_t ct_lo = ct.x, ct_hi = ct.y;
-    if (count > 0) mbar_wait(bar_lut, 0);  // the producer copies the LUT only when it has work
+    std::uint32_t sink = 0;
+    if (count > std::uint32_t(grp)) mbar_wait(bar_lut, 0);  // the producer copies the LUT only when it has work
+    if (warp == kWarpDec) tstamp(a, 10, 1, 0);
     for (std::uint32_t i = grp; i < count; i += G) {
       const std::uint32_t s = j & (nst - 1);  // nst in {1, 2}
       const std::uint32_t buf = use & 1, bph = (use >> 1) & 1;
-      const std::uint32_t sa = stage_addr(st);
+      const std::uint32_t sa = code_addr(st);
       const bool e8p = (s ? a.kind[1] : a.kind[0]) == 0;
       const bool tw = q == 1;
       if (tw) tstamp(a, grp, i, 0);
-      mbar_wait(bar_full + 8 * st, r & 1);
+      mbar_wait(bar_full_c + 8 * st, r & 1);
       if (tw) tstamp(a, grp, i, 1);
       const std::uint32_t abuf = tbase + tl + (2 * grp + buf) * kAcols;
       if (e8p) {
@@ -293,6 +373,8 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
         const std::uint32_t sw = lds32(sa + 8192 + row_in * 4);
         const std::uint32_t idx[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
         const std::uint32_t fl[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_empty_c + 8 * st);  // slab is in registers: hand the slot back
         mbar_wait(bar_a_empty + 8 * (2 * grp + buf), bph ^ 1);
         if (tw) tstamp(a, grp, i, 2);
         tc_fence_after();
@@ -302,12 +384,20 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int g4 = 2 * qq + h;  // codewords 4 g4 .. 4 g4 + 3
+#ifdef Q8P_EXP_NO_DECODE
+            for (int z = 0; z < 8; ++z) o[8 * h + z] = idx[g4] ^ fl[g4];
+#else
             e8p_a<0>(idx[g4], fl[g4], lb, ct_lo, ct_hi, o[8 * h + 0], o[8 * h + 1]);
             e8p_a<1>(idx[g4], fl[g4], lb, ct_lo, ct_hi, o[8 * h + 2], o[8 * h + 3]);
             e8p_a<2>(idx[g4], fl[g4], lb, ct_lo, ct_hi, o[8 * h + 4], o[8 * h + 5]);
             e8p_a<3>(idx[g4], fl[g4], lb, ct_lo, ct_hi, o[8 * h + 6], o[8 * h + 7]);
+#endif
           }
+#ifdef Q8P_EXP_NO_STTM
+          for (int z = 0; z < 16; ++z) sink ^= o[z];
+#else
           tmem_st16(abuf + 16 * qq, o);
+#endif
         }
         std::uint32_t sd[8];
         sd[0] = (sw << 3) & 0x08080808u;
@@ -322,6 +412,8 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
       } else {
         const uint4 c0 = lds128(sa + row_in * 16), c1 = lds128(sa + 2048 + row_in * 16);
         const std::uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_empty_c + 8 * st);
         mbar_wait(bar_a_empty + 8 * (2 * grp + buf), bph ^ 1);
         tc_fence_after();
 #pragma unroll
@@ -339,32 +431,24 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
           tmem_st16(abuf + 16 * qq, o);
         }
       }
+#ifdef Q8P_EXP_NO_STTM
+      if (sink == 0x12345679u) a.zacc[0] = 1;
+#endif
       tmem_wait_st();
       tc_fence_before();
-      // row block ends with this group's item?  (next item of the group is past it)
-      const bool last_in_rb = (j + G >= per_rb) || (i + G >= count);
-      asm volatile("bar.sync %0, 128;\n" ::"r"(barg) : "memory");
-      if (issuer) {
-        tc_fence_after();
-        const std::uint64_t bd = dhi | (((sa + kE8pSlab) >> 4) & 0x3FFFu);
-        mma_i8_slab_e<2 * N>(dcol + s * N, abuf - tl, bd, idesc, (started >> s) & 1, e8p,
-                             bar_a_empty + 8 * (2 * grp + buf), bar_empty + 8 * st);
-        if (last_in_rb) mma_commit_e(bar_d_full + 8 * grp);
-        if (tw) tstamp(a, grp, i, 3);
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_a_full + 8 * (2 * grp + buf));
+      if (tw) tstamp(a, grp, i, 3);
       started |= 1u << s;
-      if (last_in_rb) {
+      if ((j + G >= per_rb) || (i + G >= count)) {
         // epilogue of this row block: D (int32, exact) -> global accumulators
+        if (seg == 0) pdl_wait();  // K1 zeroed the accumulators
         mbar_wait(bar_d_full + 8 * grp, seg & 1);
         tc_fence_after();
         const std::uint32_t row = rb * 128 + row_in;
         const bool row_ok = row < a.m_local;
-        const std::uint32_t ia = std::max(it0, rb * per_rb), ib = std::min(it1, (rb + 1) * per_rb);
         for (std::uint32_t s2 = 0; s2 < nst; ++s2) {
-          // stage s2 got at least one item from this group in this row block?
-          if (!((started >> s2) & 1)) continue;
-          (void)ia;
-          (void)ib;
+          if (!((started >> s2) & 1)) continue;  // no item of stage s2 from this group here
           std::int32_t* z = a.zacc + std::size_t(s2) * N * a.rows_pad + row;
 #pragma unroll
           for (int c0 = 0; c0 < N; c0 += 8) {
@@ -395,11 +479,17 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
       }
     }
   }
+  if (threadIdx.x == 0) tstamp(a, 10, 0, 2);
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) tstamp(a, 10, 0, 3);
+
   if (warp == kWarpProd) {
     tc_fence_after();
     tmem_dealloc<512>(tbase);
+#ifdef Q8P_K2_TRACE
+    if (lane == 0) gstamp(2);
+#endif
   }
 }
 
@@ -410,6 +500,7 @@ void set_attr() {
     cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(kSmemBytes)),
                "tc smem attr");
+    cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
   });
 }
 

@@ -389,6 +389,7 @@ void launch_pass1_q(const RhtArgs& a, std::uint32_t extra_ctas, cudaStream_t s) 
   std::call_once(once, [] {
     cuda_check(cudaFuncSetAttribute(rht_pass1<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
                "rht smem attr");
+    cuda_check(cudaFuncSetAttribute(rht_pass1<Q>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
   });
   launch_pdl(rht_pass1<Q>, dim3(a.P1 + extra_ctas, a.batch), dim3(kP1Threads), smem, s, a);
 }
@@ -413,6 +414,7 @@ void launch_pass2(const RhtArgs& a, cudaStream_t s) {
   std::call_once(once, [] {
     cuda_check(cudaFuncSetAttribute(rht_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
                "rht smem attr");
+    cuda_check(cudaFuncSetAttribute(rht_pass2, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
   });
   launch_pdl(rht_pass2, dim3(groups, a.batch), dim3(128), std::size_t(a.P1) * 16, s, a);
   cuda_check(cudaGetLastError(), "rht pass2 launch");
@@ -426,6 +428,7 @@ void launch_pass2_limbs(const RhtArgs& a, cudaStream_t s) {
   std::call_once(once, [] {
     cuda_check(cudaFuncSetAttribute(rht_pass2_limbs, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
                "rht smem attr");
+    cuda_check(cudaFuncSetAttribute(rht_pass2_limbs, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
   });
   launch_pdl(rht_pass2_limbs, dim3(chunk / 8, a.batch), dim3(128), std::size_t(a.P1) * 32, s, a);
   cuda_check(cudaGetLastError(), "rht pass2 limbs launch");

@@ -8,7 +8,7 @@ os.environ["Q8P_TRACE"] = out
 import torch
 import bench
 import paper_2402_04396_b200 as q8p
-m, n = (int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else "28672x8192").split("x"))
+m, n = (int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else os.environ.get("SHAPE", "28672x8192")).split("x"))
 L = q8p.Layer.from_qshp(bench.make_artifact(m, n, 7), device=0)
 x = torch.randn(1, n, device="cuda")
 for _ in range(3):

@@ -26,15 +26,16 @@ __device__ __forceinline__ void mma_i8_ss(std::uint32_t d, std::uint64_t a, std:
       : "memory");
 }
 
-template <int N, bool TS, int R = 1, bool WARP = false>
-__global__ void __launch_bounds__(128, 1) k_mma(int groups, int per_group, unsigned long long* out) {
+template <int N, bool TS, int R = 1, bool WARP = false, int STW = 0, int CPG = 0>
+__global__ void __launch_bounds__(128 + 32 * STW, 1) k_mma(int groups, int per_group, unsigned long long* out) {
   extern __shared__ __align__(1024) std::uint8_t smem[];
   const std::uint32_t sb = smem_u32(smem);
-  const std::uint32_t bar = sb, slot = sb + 8;
+  const std::uint32_t bar = sb, slot = sb + 8;  // extra barriers at sb + 16 ..
   const int warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<std::uint32_t*>(smem + 1024)[i] = 0x01010101u;
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
+    for (int c = 0; c < 4; ++c) mbar_init(bar + 16 + 8 * c, 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<512>(slot);
@@ -43,6 +44,22 @@ __global__ void __launch_bounds__(128, 1) k_mma(int groups, int per_group, unsig
   tc_fence_after();
   fence_proxy_async_smem();
   const std::uint32_t tb = *reinterpret_cast<volatile std::uint32_t*>(smem + 8);
+  __shared__ int stop;
+  if (threadIdx.x == 0) stop = 0;
+  __syncthreads();
+  if (warp >= 4) {
+    // concurrent TMEM writers: x16 stores into columns 128..255 of their lane quadrant
+    std::uint32_t v[16];
+    for (int i = 0; i < 16; ++i) v[i] = threadIdx.x * i;
+    const std::uint32_t ta = tb + (std::uint32_t((warp & 3) * 32) << 16) + 128;
+    int it = 0;
+    while (*reinterpret_cast<volatile int*>(&stop) == 0) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) tmem_st16(ta + 16 * c, v);
+      v[0] += ++it;
+    }
+    tmem_wait_st();
+  }
   if (WARP ? warp == 0 : threadIdx.x == 0) {
     constexpr std::uint32_t idesc = idesc_i8(128, N);
     const std::uint32_t bsm = sb + 1024, asm_ = sb + 1024 + 16384;
@@ -66,11 +83,13 @@ __global__ void __launch_bounds__(128, 1) k_mma(int groups, int per_group, unsig
         else
           mma_i8_ss(dd[k], ad[k], bd[k], idesc, 1);
       }
+      for (int c = 0; c < CPG; ++c) mma_commit_e(bar + 16 + 8 * c);
     }
     if (!WARP || (threadIdx.x & 31) == 0) mma_commit(bar);
     mbar_wait(bar, 0);
     std::uint64_t t1 = clock64();
-    if (blockIdx.x == 0) out[0] = t1 - t0;
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) out[0] = t1 - t0;
+    if ((threadIdx.x & 31) == 0) atomicExch(&stop, 1);
   }
   tc_fence_before();
   __syncthreads();
@@ -108,36 +127,34 @@ __global__ void __launch_bounds__(128, 1) k_sttm(int iters, unsigned long long* 
   }
 }
 
-template <int N, bool TS, int R = 1, bool WARP = false>
+template <int N, bool TS, int R = 1, bool WARP = false, int STW = 0, int CPG = 0>
 void run(unsigned long long* d) {
   const int groups = 2000, per = 8;
-  auto k = k_mma<N, TS, R, WARP>;
+  auto k = k_mma<N, TS, R, WARP, STW, CPG>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  k<<<148, 128, 100 * 1024>>>(groups, per, d);
+  k<<<148, 128 + 32 * STW, 100 * 1024>>>(groups, per, d);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   cudaEventRecord(a);
-  k<<<148, 128, 100 * 1024>>>(groups, per, d);
+  k<<<148, 128 + 32 * STW, 100 * 1024>>>(groups, per, d);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
   cudaEventElapsedTime(&ms, a, b);
   unsigned long long c;
   cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
-  printf("mma i8 M=128 N=%d K=32 R=%d warp=%d %s: %.1f cyc/mma  (%.1f us total, err=%s)\n", N, R, int(WARP), TS ? "A=TMEM" : "A=SMEM",
+  printf("mma i8 M=128 N=%d K=32 R=%d warp=%d stw=%d commits/8=%d %s: %.1f cyc/mma  (%.1f us total, err=%s)\n", N, R, int(WARP), STW, CPG, TS ? "A=TMEM" : "A=SMEM",
          double(c) / (groups * per), ms * 1e3, cudaGetErrorString(cudaGetLastError()));
 }
 
 int main() {
   unsigned long long* d;
   cudaMalloc(&d, 64);
-  run<8, true, 1>(d);
   run<8, true, 1, true>(d);
-  run<16, true, 1, true>(d);
-  run<64, true, 1, true>(d);
-  run<128, true, 1, true>(d);
-  run<256, true, 1, true>(d);
+  run<8, true, 1, true, 0, 1>(d);
+  run<8, true, 1, true, 0, 3>(d);
+  run<8, true, 4, true, 0, 3>(d);
   k_sttm<<<148, 128>>>(4000, d);
   cudaDeviceSynchronize();
   unsigned long long c;
