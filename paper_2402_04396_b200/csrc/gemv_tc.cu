@@ -108,6 +108,19 @@ __device__ __forceinline__ void tstamp(const TcArgs& a, int role, std::uint32_t 
     a.trace[(role * kTraceItems + item) * 4 + ev] = clock64();
 }
 
+// LUT reads: the LUT window is constant once bar_lut completed, so these are
+// plain (non-volatile, no memory clobber) asm the scheduler may move freely,
+// e.g. across the A-buffer wait.
+__device__ __forceinline__ std::uint32_t lut32(std::uint32_t addr) {
+  std::uint32_t r;
+  asm("ld.shared.u32 %0, [%1];\n" : "=r"(r) : "r"(addr));
+  return r;
+}
+__device__ __forceinline__ uint2 lut64(std::uint32_t addr) {
+  uint2 r;
+  asm("ld.shared.v2.u32 {%0,%1}, [%2];\n" : "=r"(r.x), "=r"(r.y) : "r"(addr));
+  return r;
+}
 __device__ __forceinline__ std::uint32_t lds32(std::uint32_t addr) {
   std::uint32_t r;
   asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(r) : "r"(addr));
@@ -140,9 +153,15 @@ constexpr std::uint32_t kCtHi = 0x00FBFDFFu;  // {-1,-3,-5,0}
 // A bytes of one E8P codeword: slot jj (0..3) of an idx / flag register pair.
 // `lb` = LUT window bytes 2..3 | lane * 4: PRMT drops idx into byte 1.
 template <int JJ>
-__device__ __forceinline__ void e8p_a(std::uint32_t idxreg, std::uint32_t fl, std::uint32_t lb, std::uint32_t ct_lo,
-                                      std::uint32_t ct_hi, std::uint32_t& lo, std::uint32_t& hi) {
-  const std::uint32_t nib = lds32(prmt(idxreg, lb, 0x7604u | (std::uint32_t(JJ) << 4)));
+__device__ __forceinline__ std::uint32_t e8p_nib(std::uint32_t idxreg, std::uint32_t lb) {
+  // volatile: issued before the A-buffer wait so the LDS latency overlaps it
+  std::uint32_t r;
+  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(r) : "r"(prmt(idxreg, lb, 0x7604u | (std::uint32_t(JJ) << 4))));
+  return r;
+}
+template <int JJ>
+__device__ __forceinline__ void e8p_fin(std::uint32_t nib, std::uint32_t fl, std::uint32_t ct_lo, std::uint32_t ct_hi,
+                                        std::uint32_t& lo, std::uint32_t& hi) {
   std::uint32_t rs;
   if constexpr (JJ == 0)
     rs = fl << 2;
@@ -357,6 +376,11 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
     std::uint32_t sink = 0;
     if (count > std::uint32_t(grp)) mbar_wait(bar_lut, 0);  // the producer copies the LUT only when it has work
     if (warp == kWarpDec) tstamp(a, 10, 1, 0);
+#ifdef Q8P_STAGGER_NS
+    // desynchronise the groups: identical loops started together stay in phase,
+    // decoding (ALU-bound) at the same time and waiting at the same time
+    if (grp > 0) __nanosleep(std::uint32_t(grp) * Q8P_STAGGER_NS);
+#endif
     for (std::uint32_t i = grp; i < count; i += G) {
       const std::uint32_t s = j & (nst - 1);  // nst in {1, 2}
       const std::uint32_t buf = use & 1, bph = (use >> 1) & 1;
@@ -375,6 +399,15 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
         const std::uint32_t fl[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_empty_c + 8 * st);  // slab is in registers: hand the slot back
+        // magnitude nibbles of all 32 codewords first (LDS latency overlaps the wait)
+        std::uint32_t nib[32];
+#pragma unroll
+        for (int g4 = 0; g4 < 8; ++g4) {
+          nib[4 * g4 + 0] = e8p_nib<0>(idx[g4], lb);
+          nib[4 * g4 + 1] = e8p_nib<1>(idx[g4], lb);
+          nib[4 * g4 + 2] = e8p_nib<2>(idx[g4], lb);
+          nib[4 * g4 + 3] = e8p_nib<3>(idx[g4], lb);
+        }
         mbar_wait(bar_a_empty + 8 * (2 * grp + buf), bph ^ 1);
         if (tw) tstamp(a, grp, i, 2);
         tc_fence_after();
@@ -387,10 +420,10 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
 #ifdef Q8P_EXP_NO_DECODE
             for (int z = 0; z < 8; ++z) o[8 * h + z] = idx[g4] ^ fl[g4];
 #else
-            e8p_a<0>(idx[g4], fl[g4], lb, ct_lo, ct_hi, o[8 * h + 0], o[8 * h + 1]);
-            e8p_a<1>(idx[g4], fl[g4], lb, ct_lo, ct_hi, o[8 * h + 2], o[8 * h + 3]);
-            e8p_a<2>(idx[g4], fl[g4], lb, ct_lo, ct_hi, o[8 * h + 4], o[8 * h + 5]);
-            e8p_a<3>(idx[g4], fl[g4], lb, ct_lo, ct_hi, o[8 * h + 6], o[8 * h + 7]);
+            e8p_fin<0>(nib[4 * g4 + 0], fl[g4], ct_lo, ct_hi, o[8 * h + 0], o[8 * h + 1]);
+            e8p_fin<1>(nib[4 * g4 + 1], fl[g4], ct_lo, ct_hi, o[8 * h + 2], o[8 * h + 3]);
+            e8p_fin<2>(nib[4 * g4 + 2], fl[g4], ct_lo, ct_hi, o[8 * h + 4], o[8 * h + 5]);
+            e8p_fin<3>(nib[4 * g4 + 3], fl[g4], ct_lo, ct_hi, o[8 * h + 6], o[8 * h + 7]);
 #endif
           }
 #ifdef Q8P_EXP_NO_STTM
@@ -423,7 +456,7 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
           for (int h = 0; h < 2; ++h) {
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
-              const uint2 v = lds64(prmt(cw[2 * qq + h], lb8, 0x7604u | (std::uint32_t(jj) << 4)));
+              const uint2 v = lut64(prmt(cw[2 * qq + h], lb8, 0x7604u | (std::uint32_t(jj) << 4)));
               o[8 * h + 2 * jj] = v.x;
               o[8 * h + 2 * jj + 1] = v.y;
             }
