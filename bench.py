@@ -179,18 +179,11 @@ def run_ours(args):
 
     comm = None
     if world > 1:
-        uid = torch.zeros(128, dtype=torch.uint8)
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
-            buf = (ctypes_u8 := np.zeros(128, dtype=np.uint8))
-            q8p._check(q8p.lib().q8p_nccl_unique_id(buf.ctypes.data))
-            uid = torch.from_numpy(buf)
-        uid = uid.to(dev)
+            uid.copy_(torch.frombuffer(bytearray(q8p.NcclComm.unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
-        import ctypes
-        c = ctypes.c_void_p()
-        idb = uid.cpu().numpy()
-        q8p._check(q8p.lib().q8p_nccl_comm_init(idb.ctypes.data, world, rank, local, ctypes.byref(c)))
-        comm = c
+        comm = q8p.NcclComm(bytes(uid.cpu().numpy()), world, rank, local)
 
     # Two full copies of the layer set rotate so every step streams from HBM
     # (134.6 MB per copy at 2 bits vs ~126 MB L2).
@@ -200,8 +193,7 @@ def run_ours(args):
         row = []
         for (m, n), art in zip(layers, arts):
             if world > 1:
-                lo, hi = m * rank // world, m * (rank + 1) // world
-                row.append(q8p.Layer.from_qshp(art, device=local, rows=(lo, hi)))
+                row.append(q8p.Layer.from_qshp(art, device=local, rows=q8p.shard_rows(m, world, rank)))
             else:
                 row.append(q8p.Layer.from_qshp(art, device=local))
         copies.append(row)
@@ -344,10 +336,11 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             threads = args.cpu_threads or min(os.cpu_count() or 1, 64)
-            tps, step_s = cpu_reference(layers, 1, threads, args.sample_div, 1, 0)
+            tps, step_s = cpu_reference(layers, 1, threads, args.cpu_sample_div, 2, 0)
             cpu = {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "reference",
-                   "sample": f"{threads} concurrent latq::infer (1 thread each) over first m/{args.sample_div} rows "
-                             f"of each layer, scaled x{args.sample_div}; {step_s:.1f}s"}
+                   "sample": f"{threads} concurrent latq::infer calls (1 thread each, one token each) through "
+                             f"the first m/{args.cpu_sample_div} rows of each layer, scaled x{args.cpu_sample_div}; "
+                             f"median of 2 steps, {step_s:.1f} s per step"}
         except Exception as e:  # reference .so missing etc.
             cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
@@ -369,6 +362,8 @@ def run_ours(args):
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -384,7 +379,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
-    ap.add_argument("--sample-div", type=int, default=32)
+    ap.add_argument("--sample-div", type=int, default=8, help="row sampling of --impl reference steps")
+    ap.add_argument("--cpu-sample-div", type=int, default=1, help="row sampling of our line's cpu_baseline")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -53,6 +53,10 @@ class DeviceError : public Error {  // CUDA / NCCL failures
  public:
   using Error::Error;
 };
+class NcclError : public DeviceError {  // NCCL failures (Q8P_ERR_NCCL)
+ public:
+  using DeviceError::DeviceError;
+};
 
 // Throws the typed exception for a non-OK status (message: q8p_last_error()).
 void throw_status(q8p_status s);

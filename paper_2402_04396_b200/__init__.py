@@ -22,7 +22,7 @@ __all__ = [
     "UnsupportedVersionError", "TruncatedArtifactError", "UnsupportedError", "DeviceError",
     "lib", "plan_hadamard", "hadamard_base", "codebook_table", "e8p_decode_host",
     "inspect_artifact", "reserialize", "Layer", "rht", "kernel_launches",
-    "CB_E8P_2BIT", "CB_E8_1BIT",
+    "CB_E8P_2BIT", "CB_E8_1BIT", "NcclError", "shard_rows", "NcclComm",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -69,10 +69,14 @@ class DeviceError(Error):
     pass
 
 
+class NcclError(DeviceError):
+    pass
+
+
 _STATUS = {
     1: SizeError, 2: ValidationError, 3: FormatError, 4: BadMagicError,
     5: UnsupportedVersionError, 6: TruncatedArtifactError, 7: UnsupportedError,
-    8: DeviceError, 9: DeviceError, 10: Error,
+    8: DeviceError, 9: NcclError, 10: Error,
 }
 
 
@@ -207,6 +211,47 @@ def reserialize(data: bytes) -> bytes:
     return buf.raw[: n.value]
 
 
+def shard_rows(m: int, world: int, rank: int) -> tuple[int, int]:
+    """Row shard [lo, hi) of rank `rank` for q8p_forward_sharded: equal shards,
+    ordered by rank (the all-gather's rank-major layout is then z itself)."""
+    if world <= 0 or not 0 <= rank < world:
+        raise ValidationError(f"bad world/rank {world}/{rank}")
+    if m % world:
+        raise ValidationError(f"m={m} is not divisible by world={world}")
+    per = m // world
+    return rank * per, (rank + 1) * per
+
+
+class NcclComm:
+    """NCCL communicator for Layer.forward_sharded (q8p_nccl_* plumbing: the
+    unique id is broadcast by the caller, e.g. over torch.distributed)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * 128)()
+        _check(lib().q8p_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, uid: bytes, world: int, rank: int, device: int):
+        if len(uid) != 128:
+            raise ValidationError("NCCL unique id must be 128 bytes")
+        c = ctypes.c_void_p()
+        _check(lib().q8p_nccl_comm_init(uid, world, rank, device, ctypes.byref(c)))
+        self.handle = c
+        self.world, self.rank = world, rank
+
+    def close(self) -> None:
+        if self.handle:
+            _check(lib().q8p_nccl_comm_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 # --- device API ---------------------------------------------------------------
 def _torch():
     import torch  # plumbing only: device memory and streams
@@ -308,6 +353,11 @@ class Layer:
         return out
 
     def forward_sharded(self, x, comm, out=None, stream=None, workspace=None):
+        """Row-sharded forward (q8p_forward_sharded): this layer holds rows
+        shard_rows(m, world, rank); z slices are all-gathered over `comm`
+        (NcclComm or a raw ncclComm_t pointer) and every rank gets the full y."""
+        if isinstance(comm, NcclComm):
+            comm = comm.handle
         torch = _torch()
         info = self.info
         batch = x.shape[0]

@@ -1,6 +1,7 @@
 // The C ABI (include/q8p.h): layer upload, forward orchestration
 // (K1 -> K2 -> [all-gather] -> K3), host-buffer infer, and status mapping.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -46,6 +47,9 @@ q8p_status status_of_current_exception() {
   } catch (const UnsupportedError& e) {
     set_last_error(e.what());
     return Q8P_ERR_UNSUPPORTED;
+  } catch (const NcclError& e) {
+    set_last_error(e.what());
+    return Q8P_ERR_NCCL;
   } catch (const DeviceError& e) {
     set_last_error(e.what());
     return Q8P_ERR_CUDA;
@@ -244,6 +248,8 @@ struct Workspace {
   long long* tl;         // [batch]
   std::uint8_t* bimg;    // tc_bimg_bytes(n, batch)
   std::int32_t* zacc;    // [stages][N][rows_pad]
+  float* z_loc;          // row-sharded: [batch][m_local] this rank's z rows
+  float* z_full;         // row-sharded: [batch][m] all-gathered z
   std::uint32_t rows_pad, zcols;
 };
 std::uint32_t rows_pad_of(const q8p_layer* L) { return tc_row_blocks(L->m_local()) * 128; }
@@ -267,6 +273,8 @@ std::size_t workspace_parts(const q8p_layer* L, int batch, Workspace* w, void* b
     v.tl = reinterpret_cast<long long*>(take(B * 8));
     v.bimg = take(tc_bimg_bytes(L->n, batch));
     v.zacc = reinterpret_cast<std::int32_t*>(take(std::size_t(L->num_stages) * v.zcols * v.rows_pad * 4));
+    v.z_full = reinterpret_cast<float*>(take(B * L->m * 4));  // q8p_forward_sharded
+    if (L->row_begin != 0 || L->row_end != L->m) v.z_loc = reinterpret_cast<float*>(take(B * L->m_local() * 4));
   } else {
     v.t = reinterpret_cast<float*>(take(B * L->n * 4));
     v.z = reinterpret_cast<float*>(take(B * L->m * 4));
@@ -295,6 +303,48 @@ void forward_local(const q8p_layer* L, const float* x, int batch, const Workspac
     launch_gemv_simple(*L, w.t, w.z, batch, static_cast<int>(L->m), s);
     if (opts) record_event(opts->gemv_end_event, s);
   }
+}
+
+[[noreturn]] void throw_nccl(ncclResult_t r, const char* what) {
+  throw q8p::NcclError(std::string(what) + ": " + ncclGetErrorString(r));
+}
+inline void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw_nccl(r, what);
+}
+
+// Row-sharded forward: K1 (replicated) -> K2 on this rank's rows ->
+// combine -> ncclAllGather of the z slices over NVLink -> K3 on the full z.  Each
+// row's integer accumulation is unchanged by sharding, and the combine / K3
+// arithmetic is the unsharded one, so sharded y equals unsharded y bit for bit.
+void forward_sharded_impl(const q8p_layer* L, const float* x, float* y, int batch, void* ws, std::size_t ws_bytes,
+                          ncclComm_t comm, cudaStream_t s) {
+  if (!L) throw ValidationError("null layer");
+  if (batch < 0) throw ValidationError("negative batch");
+  if (batch == 0) return;
+  if (!x || !y) throw ValidationError("null x / y");
+  if (!comm) throw ValidationError("null communicator");
+  if (!tc_supported(*L, batch)) throw UnsupportedError("row-sharded forward needs the tensor-core path (batch <= 16)");
+  int world = 0, rank = 0;
+  nccl_check(ncclCommCount(comm, &world), "ncclCommCount");
+  nccl_check(ncclCommUserRank(comm, &rank), "ncclCommUserRank");
+  const std::uint32_t ml = L->m_local();
+  if (std::size_t(ml) * std::size_t(world) != L->m || L->row_begin != std::uint32_t(rank) * ml)
+    throw ValidationError("row shards must be equal-sized and ordered by rank");
+  if (!ws || ws_bytes < workspace_size(L, batch)) throw SizeError("workspace too small");
+  DeviceGuard g(L->device);
+  Workspace w;
+  workspace_parts(L, batch, &w, ws);
+  forward_local(L, x, batch, w, s, nullptr);
+  float zscale[2] = {L->scale[0], L->scale[1]};
+  int ze8p[2] = {L->cb[0] == Q8P_CB_E8P_2BIT, L->cb[1] == Q8P_CB_E8P_2BIT};
+  float* zl = L->row_begin == 0 && L->row_end == L->m ? w.z_full : w.z_loc;
+  launch_combine_acc(w.zacc, L->num_stages, w.rows_pad, w.zcols, zscale, ze8p, w.alpha, w.tl, zl, ml, batch, s);
+  nccl_check(ncclGroupStart(), "ncclGroupStart");
+  for (int b = 0; b < batch; ++b)
+    nccl_check(ncclAllGather(zl + std::size_t(b) * ml, w.z_full + std::size_t(b) * L->m, ml, ncclFloat32, comm, s),
+               "ncclAllGather");
+  nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  launch_rht_out(L->side_u, w.z_full, w.u, y, batch, s);
 }
 
 void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void* ws, std::size_t ws_bytes,
@@ -631,18 +681,50 @@ q8p_status q8p_hadamard_base(size_t q, int8_t* out) {
   }
 }
 
-q8p_status q8p_forward_sharded(const q8p_layer*, const float*, float*, int, void*, size_t, void*, void*) {
-  set_last_error("q8p_forward_sharded: not built yet");
-  return Q8P_ERR_UNSUPPORTED;
+q8p_status q8p_forward_sharded(const q8p_layer* L, const float* x, float* y, int batch, void* ws, size_t ws_bytes,
+                               void* nccl_comm, void* stream) {
+  try {
+    forward_sharded_impl(L, x, y, batch, ws, ws_bytes, static_cast<ncclComm_t>(nccl_comm),
+                         static_cast<cudaStream_t>(stream));
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
 }
-q8p_status q8p_nccl_unique_id(uint8_t*) {
-  set_last_error("NCCL support not built yet");
-  return Q8P_ERR_UNSUPPORTED;
+q8p_status q8p_nccl_unique_id(uint8_t out[128]) {
+  try {
+    if (!out) throw q8p::ValidationError("null argument");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out, &id, sizeof(id));
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
 }
-q8p_status q8p_nccl_comm_init(const uint8_t*, int, int, int, void**) {
-  set_last_error("NCCL support not built yet");
-  return Q8P_ERR_UNSUPPORTED;
+q8p_status q8p_nccl_comm_init(const uint8_t id[128], int world, int rank, int device, void** comm) {
+  try {
+    if (!id || !comm) throw q8p::ValidationError("null argument");
+    if (world <= 0 || rank < 0 || rank >= world) throw q8p::ValidationError("bad world / rank");
+    DeviceGuard g(device);
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    ncclComm_t c = nullptr;
+    nccl_check(ncclCommInitRank(&c, world, uid, rank), "ncclCommInitRank");
+    *comm = c;
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
 }
-q8p_status q8p_nccl_comm_destroy(void*) { return Q8P_OK; }
+q8p_status q8p_nccl_comm_destroy(void* comm) {
+  try {
+    if (comm) nccl_check(ncclCommDestroy(static_cast<ncclComm_t>(comm)), "ncclCommDestroy");
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
 
 }  // extern "C"

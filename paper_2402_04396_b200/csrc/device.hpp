@@ -117,6 +117,10 @@ void launch_rht_in_limbs(const DevSide& side, const float* x, float* u_scratch, 
                          long long* tl, std::uint8_t* bimg, std::uint32_t b_bytes, std::uint32_t bcols,
                          std::uint8_t* bimg_tail, std::size_t tail_bytes, std::int32_t* zero_ptr,
                          std::size_t zero_words, int batch, cudaStream_t s);
+// Row-sharded forward: this rank's fp32 z rows [batch][m_local] from the limb accumulators.
+void launch_combine_acc(const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows, std::uint32_t zacc_cols,
+                        const float zscale[2], const int ze8p[2], const float* alpha, const long long* tl, float* z,
+                        std::uint32_t m_local, int batch, cudaStream_t s);
 // K3 (fp32 input): y = T_u^T z.
 void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, float* y, int batch, cudaStream_t s);
 // K3 (accumulator input): z = sum_s zscale_s alpha (2 Z_s - [E8P] TL) / 4 from the int32

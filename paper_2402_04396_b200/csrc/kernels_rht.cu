@@ -105,6 +105,52 @@ struct RhtArgs {
   int fwd;
 };
 
+// z rows i..i+3 of vector b from the int32 limb accumulators:
+// z = sum_s scale_s alpha (2 Z_s - [E8P] TL) / 4, Z_s = sum_l 128^(3-l) zacc[s][4b + l]
+// (exact int64 combine, one double rounding per stage sum, then fp32).  Shared by
+// K3 pass 1 and the row-sharded combine kernel so both round identically.
+__device__ __forceinline__ float4 combine4(const RhtArgs& a, int b, std::uint32_t i) {
+  const double al = double(a.alpha_in[b]) * 0.25;
+  const long long tl = a.tl_in[b];
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int st = 0; st < a.zstages; ++st) {
+    const std::int32_t* z = a.zacc + (std::size_t(st) * a.zcols + 4 * b) * a.zrows + i;
+    const int4 v0 = *reinterpret_cast<const int4*>(z);
+    const int4 v1 = *reinterpret_cast<const int4*>(z + a.zrows);
+    const int4 v2 = *reinterpret_cast<const int4*>(z + 2 * std::size_t(a.zrows));
+    const int4 v3 = *reinterpret_cast<const int4*>(z + 3 * std::size_t(a.zrows));
+    const long long sub = (st == 0 ? a.ze8p0 : a.ze8p1) ? tl : 0;
+    const double c = al * double(st == 0 ? a.zscale0 : a.zscale1);
+    auto zt = [&](int x0, int x1, int x2, int x3) {
+      const long long Z = ((static_cast<long long>(x0) * 128 + x1) * 128 + x2) * 128 + x3;
+      return double(2 * Z - sub) * c;
+    };
+    acc[0] += zt(v0.x, v1.x, v2.x, v3.x);
+    acc[1] += zt(v0.y, v1.y, v2.y, v3.y);
+    acc[2] += zt(v0.z, v1.z, v2.z, v3.z);
+    acc[3] += zt(v0.w, v1.w, v2.w, v3.w);
+  }
+  return make_float4(float(acc[0]), float(acc[1]), float(acc[2]), float(acc[3]));
+}
+
+// Row-sharded forward: this rank's z rows [0, m_local) as fp32 [batch][m_local]
+// (all-gathered by the caller), same arithmetic as K3 pass 1.
+__global__ void __launch_bounds__(256) combine_kernel(RhtArgs a, float* z, std::uint32_t m_local) {
+  pdl_wait();
+  pdl_trigger();
+  const int b = blockIdx.y;
+  for (std::uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; 4 * v < m_local; v += gridDim.x * blockDim.x) {
+    const float4 r = combine4(a, b, 4 * v);
+    float* o = z + std::size_t(b) * m_local + 4 * v;
+    if (4 * v + 4 <= m_local && (m_local & 3) == 0) {
+      *reinterpret_cast<float4*>(o) = r;
+    } else {
+      const float rv[4] = {r.x, r.y, r.z, r.w};
+      for (int k = 0; k < 4 && 4 * v + k < m_local; ++k) o[k] = rv[k];
+    }
+  }
+}
+
 constexpr int kP1Threads = 256;
 
 // Pass 1.  grid = (P1 chunks [+ zeroing CTAs], batch).
@@ -163,28 +209,7 @@ __global__ void __launch_bounds__(kP1Threads) rht_pass1(RhtArgs a) {
     const std::uint32_t i = e0 + 4 * v;
     float4 val;
     if (a.zacc) {
-      // z = sum_s scale_s alpha (2 Z_s - [E8P] TL) / 4, Z_s = sum_l 128^(3-l) zacc[s][4b + l]
-      const double al = double(a.alpha_in[b]) * 0.25;
-      const long long tl = a.tl_in[b];
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int st = 0; st < a.zstages; ++st) {
-        const std::int32_t* z = a.zacc + (std::size_t(st) * a.zcols + 4 * b) * a.zrows + i;
-        const int4 v0 = *reinterpret_cast<const int4*>(z);
-        const int4 v1 = *reinterpret_cast<const int4*>(z + a.zrows);
-        const int4 v2 = *reinterpret_cast<const int4*>(z + 2 * std::size_t(a.zrows));
-        const int4 v3 = *reinterpret_cast<const int4*>(z + 3 * std::size_t(a.zrows));
-        const long long sub = (st == 0 ? a.ze8p0 : a.ze8p1) ? tl : 0;
-        const double c = al * double(st == 0 ? a.zscale0 : a.zscale1);
-        auto zt = [&](int x0, int x1, int x2, int x3) {
-          const long long Z = ((static_cast<long long>(x0) * 128 + x1) * 128 + x2) * 128 + x3;
-          return double(2 * Z - sub) * c;
-        };
-        acc[0] += zt(v0.x, v1.x, v2.x, v3.x);
-        acc[1] += zt(v0.y, v1.y, v2.y, v3.y);
-        acc[2] += zt(v0.z, v1.z, v2.z, v3.z);
-        acc[3] += zt(v0.w, v1.w, v2.w, v3.w);
-      }
-      val = make_float4(float(acc[0]), float(acc[1]), float(acc[2]), float(acc[3]));
+      val = combine4(a, b, i);
     } else {
       val = *reinterpret_cast<const float4*>(a.in + std::size_t(b) * a.n + i);
       ss += val.x * val.x + val.y * val.y + val.z * val.z + val.w * val.w;
@@ -524,6 +549,28 @@ void launch_rht_out_acc(const DevSide& side, const std::int32_t* zacc, int zacc_
   a.fwd = 0;
   launch_pass1(a, 0, s);
   launch_pass2(a, s);
+}
+
+void launch_combine_acc(const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows, std::uint32_t zacc_cols,
+                        const float zscale[2], const int ze8p[2], const float* alpha, const long long* tl, float* z,
+                        std::uint32_t m_local, int batch, cudaStream_t s) {
+  if (batch <= 0 || m_local == 0) return;
+  RhtArgs a{};
+  a.zacc = zacc;
+  a.zrows = zacc_rows;
+  a.zcols = zacc_cols;
+  a.zstages = zacc_stages;
+  a.zscale0 = zscale[0];
+  a.zscale1 = zscale[1];
+  a.ze8p0 = ze8p[0];
+  a.ze8p1 = ze8p[1];
+  a.alpha_in = alpha;
+  a.tl_in = tl;
+  const std::uint32_t quads = (m_local + 3) / 4;
+  launch_pdl(combine_kernel, dim3(std::min<std::uint32_t>((quads + 255) / 256, 148), batch), dim3(256), 0, s, a, z,
+             m_local);
+  cuda_check(cudaGetLastError(), "combine launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 }  // namespace q8p::detail

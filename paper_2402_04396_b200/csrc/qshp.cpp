@@ -216,8 +216,9 @@ void throw_status(q8p_status s) {
       throw TruncatedArtifactError(msg);
     case Q8P_ERR_UNSUPPORTED:
       throw UnsupportedError(msg);
-    case Q8P_ERR_CUDA:
     case Q8P_ERR_NCCL:
+      throw NcclError(msg);
+    case Q8P_ERR_CUDA:
       throw DeviceError(msg);
     default:
       throw Error(msg);
