@@ -291,9 +291,11 @@ void forward_local(const q8p_layer* L, const float* x, int batch, const Workspac
   if (tc_supported(*L, batch)) {
     const std::uint32_t N = w.zcols, KSL = tc_k_slabs(L->n), bb = 9u * N * 32u;
     const bool ragged = (L->n / 8) % 32 != 0;
+#ifndef Q8P_EXP_SKIP_K1
     launch_rht_in_limbs(L->side_v, x, w.u, w.ssq, w.alpha, w.tl, w.bimg, bb, N,
                         ragged ? w.bimg + std::size_t(KSL - 1) * bb : nullptr, ragged ? bb : 0, w.zacc,
                         std::size_t(L->num_stages) * N * w.rows_pad, batch, s);
+#endif
     if (opts) record_event(opts->gemv_start_event, s);
     launch_gemv_tc(*L, w.bimg, w.zacc, w.rows_pad, batch, s);
     if (opts) record_event(opts->gemv_end_event, s);
@@ -363,8 +365,10 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
   if (tc_supported(*L, batch)) {
     float zscale[2] = {L->scale[0], L->scale[1]};
     int ze8p[2] = {L->cb[0] == Q8P_CB_E8P_2BIT, L->cb[1] == Q8P_CB_E8P_2BIT};
+#ifndef Q8P_EXP_SKIP_K3
     launch_rht_out_acc(L->side_u, w.zacc, L->num_stages, w.rows_pad, w.zcols, zscale, ze8p, w.alpha, w.tl, w.u, y,
                        batch, s);
+#endif
   } else {
     launch_rht(L->side_u, w.z, y, batch, /*transpose=*/true, s);  // y = T_u^T z
   }

@@ -39,7 +39,11 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t sme
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
+#ifdef Q8P_EXP_NO_PDL
+  cfg.numAttrs = 0;
+#else
   cfg.numAttrs = 1;
+#endif
   cuda_check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "kernel launch");
 }
 

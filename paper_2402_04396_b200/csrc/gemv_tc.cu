@@ -69,13 +69,23 @@ constexpr std::uint32_t kE81Slab = 2 * 2048;
 constexpr std::uint32_t kAcols = 72;        // TMEM columns per A buffer (64 main + 8 side)
 constexpr int kWarpProd = 0, kWarpMma = 1;  // warps 1..G: one MMA issuer per decode group; then 4G decoder warps
 constexpr int kMaxStages = 32;
+#ifndef Q8P_K2_TEAMS
+#define Q8P_K2_TEAMS 1  // decoder teams per group at batch <= 2 (2: +3% K2, but the register
+                         // file then leaves no room to co-reside with K1 under PDL)
+#endif
 constexpr std::uint32_t kCtl = 1024;        // control block (barriers) at the smem base
-constexpr std::size_t kSmemBytes = 227 * 1024;
+#ifndef Q8P_K2_SMEM_KB
+#define Q8P_K2_SMEM_KB 200  // < 227: lets K2's prologue co-reside with K1 under PDL
+#endif
+constexpr std::size_t kSmemBytes = Q8P_K2_SMEM_KB * 1024;
 
-template <int G>
+// G decode groups (one TMEM accumulator + one MMA issuer each), T teams of 4
+// decoder warps per group: team t decodes the group's items that use A buffer
+// t (T = 2) or both buffers alternately (T = 1).
+template <int G, int T = 1>
 struct Roles {
   static constexpr int kWarpDec = 1 + G;
-  static constexpr int kThreads = (kWarpDec + 4 * G) * 32;
+  static constexpr int kThreads = (kWarpDec + 4 * G * T) * 32;
   template <int N>
   static constexpr std::uint32_t kBg = N <= 8 ? 3 : (N <= 16 ? 2 : 1);  // B-image ring slots per group
 };
@@ -176,8 +186,8 @@ __device__ __forceinline__ void e8p_fin(std::uint32_t nib, std::uint32_t fl, std
   hi = prmt(ct_lo, ct_hi, __umulhi(sel, 65536u));  // sel >> 16
 }
 
-template <int N, int G>
-__global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a) {
+template <int N, int G, int T>
+__global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArgs a) {
   extern __shared__ __align__(1024) std::uint8_t smem[];
   // warp index via shfl: the compiler then knows every role branch is warp-uniform
   const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -191,8 +201,9 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
   const std::uint32_t bar_empty_b = bar_full_b + 8 * kMaxB;     // [kMaxB] B image read by its MMAs
   const std::uint32_t bar_a_empty = bar_empty_b + 8 * kMaxB;    // [G][2] A buffer read by its MMAs
   const std::uint32_t bar_a_full = bar_a_empty + 8 * 2 * G;     // [G][2] A buffer written (4 warp arrivals)
-  const std::uint32_t bar_d_full = bar_a_full + 8 * 2 * G;      // [G] accumulator final for a row block
-  const std::uint32_t bar_lut = bar_d_full + 8 * G;             // LUT window landed
+  const std::uint32_t bar_d_full = bar_a_full + 8 * 2 * G;      // [G][T] accumulator final (team t's epilogue)
+  const std::uint32_t bar_d_empty = bar_d_full + 8 * G * T;     // [G] accumulator read out (4 warp arrivals)
+  const std::uint32_t bar_lut = bar_d_empty + 8 * G;            // LUT window landed
   const std::uint32_t tmem_slot = bar_lut + 8;
   const std::uint32_t ct_slot = tmem_slot + 8;  // the constant byte table, read back by the decoders
   // B ring right above the LUT window; code ring below the window, then above the B ring
@@ -236,12 +247,37 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
       mbar_init(bar_a_empty + 8 * i, 1);
       mbar_init(bar_a_full + 8 * i, 4);
     }
-    for (int i = 0; i < G; ++i) mbar_init(bar_d_full + 8 * i, 1);
+    for (int i = 0; i < G * T; ++i) mbar_init(bar_d_full + 8 * i, 1);
+    for (int i = 0; i < G; ++i) mbar_init(bar_d_empty + 8 * i, 4);
     mbar_init(bar_lut, 1);
     fence_mbar_init();
     asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n" ::"r"(ct_slot), "r"(kCtLo), "r"(kCtHi) : "memory");
   }
-  if (warp == kWarpProd) tmem_alloc<512>(tmem_slot);
+  // Code producer state; the first S code slabs (and the LUT window) are issued
+  // before the TMEM allocation and the CTA barrier, so HBM latency overlaps setup.
+  const std::uint64_t pol = policy_evict_first();
+  std::uint32_t ps = it0 % nst, pu = it0 / nst;  // next item -> (u = row block * KSL + k slab, stage)
+  auto issue_code = [&](std::uint32_t st) {
+    const std::uint32_t sb = ps ? a.slab_bytes[1] : a.slab_bytes[0];
+    mbar_arrive_expect_tx_e(bar_full_c + 8 * st, sb);
+    bulk_g2s_hint_e(code_addr(st), (ps ? a.codes[1] : a.codes[0]) + std::size_t(pu) * sb, sb, bar_full_c + 8 * st,
+                    pol);
+    if (++ps == nst) {
+      ps = 0;
+      ++pu;
+    }
+  };
+  const std::uint32_t pre = count < S ? count : S;
+  if (warp == kWarpProd) {
+    __syncwarp();  // lane 0 initialised the barriers
+    if (count > 0) {
+      issue_code(0);  // first code slab, then the (L2-resident) LUT window
+      mbar_arrive_expect_tx_e(bar_lut, 65536);
+      bulk_g2s_e(lutw, a.lut_img, 65536, bar_lut);
+      for (std::uint32_t i = 1; i < pre; ++i) issue_code(i);
+    }
+    tmem_alloc<512>(tmem_slot);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -254,22 +290,6 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
   if (warp == kWarpProd) {
     // ===== code producer (whole warp, lane-elected issue); codes do not depend on K1 =====
     if (count > 0) {
-      const std::uint64_t pol = policy_evict_first();
-      std::uint32_t s = it0 % nst, u = it0 / nst;  // item -> (u = row block * KSL + k slab, stage s)
-      auto issue_code = [&](std::uint32_t st) {
-        const std::uint32_t sb = s ? a.slab_bytes[1] : a.slab_bytes[0];
-        mbar_arrive_expect_tx_e(bar_full_c + 8 * st, sb);
-        bulk_g2s_hint_e(code_addr(st), (s ? a.codes[1] : a.codes[0]) + std::size_t(u) * sb, sb, bar_full_c + 8 * st, pol);
-        if (++s == nst) {
-          s = 0;
-          ++u;
-        }
-      };
-      const std::uint32_t pre = count < S ? count : S;
-      issue_code(0);  // first code slab, then the (L2-resident) LUT window
-      mbar_arrive_expect_tx_e(bar_lut, 65536);
-      bulk_g2s_e(lutw, a.lut_img, 65536, bar_lut);
-      for (std::uint32_t i = 1; i < pre; ++i) issue_code(i);
       std::uint32_t st = pre == S ? 0 : pre, r = 1;
       for (std::uint32_t i = pre; i < count; ++i) {
         tstamp(a, 9, i, 0);
@@ -315,7 +335,7 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
       pdl_wait();  // K1's B images (and zeroed accumulators) are visible from here on
       while (bnext < n_g && bnext < SBg) issue_b();
       std::uint32_t j = (it0 + g) % per_rb;
-      std::uint32_t buf = 0, bph = 0, started = 0;
+      std::uint32_t buf = 0, bph = 0, started = 0, seg = 0, team = 0;
       std::uint32_t bslot = 0, bphase = 0, rslot = 0, rphase = 0;
       const std::uint32_t dcol_g = tbase + std::uint32_t(G) * 2 * kAcols + g * nst * N;
       const std::uint32_t acol0 = tbase + 2 * g * kAcols;
@@ -323,6 +343,8 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
       for (std::uint32_t k = 0, i = g; k < n_g; ++k, i += G) {
         const std::uint32_t s = j & (nst - 1);
         tstamp(a, 8 + (g == 0 ? 0 : 4 + g), k, 0);
+        // first MMA of a new row block overwrites D: the previous epilogue must have read it
+        if (started == 0 && seg > 0) mbar_wait(bar_d_empty + 8 * g, (seg - 1) & 1);
         mbar_wait(af0 + 8 * buf, bph);
         mbar_wait(fb + 8 * bslot, bphase);
         tc_fence_after();
@@ -339,8 +361,9 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
 #endif
         started |= 1u << s;
         if ((j + G >= per_rb) || (i + G >= count)) {  // this group's last item of the row block
-          mma_commit_e(bar_d_full + 8 * g);
+          mma_commit_e(bar_d_full + 8 * (g * T + team));
           started = 0;
+          ++seg;
         }
         tstamp(a, 8 + (g == 0 ? 0 : 4 + g), k, 3);
         // refill the slot of the previous group item (its MMAs were issued one item ago)
@@ -352,6 +375,7 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
         if (++bslot == SBg) bslot = 0, bphase ^= 1;
         buf ^= 1;
         if (buf == 0) bph ^= 1;
+        if (++team == T) team = 0;
         j += G;
         while (j >= per_rb) j -= per_rb;
       }
@@ -359,29 +383,31 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
   } else {
     // ===== decode groups: codes -> A bytes -> TMEM (4 warps = 4 lane quadrants) =====
     pdl_trigger();
-    const int grp = (warp - kWarpDec) >> 2;
+    const int tq = (warp - kWarpDec) >> 2;  // team index over all groups
+    const int grp = tq / T, tm = tq % T;
     const std::uint32_t q = warp & 3, row_in = q * 32 + lane;
     const std::uint32_t tl = (q * 32) << 16;
     const std::uint32_t lb = (lutw & 0xFFFF0000u) | (std::uint32_t(lane) * 4u);
     const std::uint32_t lb8 = (lutw & 0xFFFF0000u) | (128u + std::uint32_t(lane & 15) * 8u);
     const std::uint32_t dcol = tbase + std::uint32_t(G) * 2 * kAcols + std::uint32_t(grp) * nst * N;
     const std::uint32_t per_rb = a.KSL * nst;
-    std::uint32_t st = std::uint32_t(grp) % S, r = std::uint32_t(grp) / S, use = 0, seg = 0, started = 0;
-    std::uint32_t j = (it0 + grp) % per_rb, rb = (it0 + grp) / per_rb;
+    const std::uint32_t i_first = std::uint32_t(grp + G * tm);
+    std::uint32_t st = i_first % S, r = i_first / S, use = std::uint32_t(tm), seg = 0, started = 0;
+    std::uint32_t j = (it0 + i_first) % per_rb, rb = (it0 + i_first) / per_rb;
     // constant byte table {+1,+3,+5,_ | -1,-3,-5,_} loaded from smem so it lives
     // in ONE register (as an immediate/uniform value ptxas re-materialises it
     // with a UR->R move in front of every PRMT: +1 instruction per codeword)
     const uint2 ct = lds64(ct_slot);
     const std::uint32_t ct_lo = ct.x, ct_hi = ct.y;
     std::uint32_t sink = 0;
-    if (count > std::uint32_t(grp)) mbar_wait(bar_lut, 0);  // the producer copies the LUT only when it has work
+    if (count > i_first) mbar_wait(bar_lut, 0);  // the producer copies the LUT only when it has work
     if (warp == kWarpDec) tstamp(a, 10, 1, 0);
 #ifdef Q8P_STAGGER_NS
     // desynchronise the groups: identical loops started together stay in phase,
     // decoding (ALU-bound) at the same time and waiting at the same time
     if (grp > 0) __nanosleep(std::uint32_t(grp) * Q8P_STAGGER_NS);
 #endif
-    for (std::uint32_t i = grp; i < count; i += G) {
+    for (std::uint32_t i = i_first; i < count; i += G * T) {
       const std::uint32_t s = j & (nst - 1);  // nst in {1, 2}
       const std::uint32_t buf = use & 1, bph = (use >> 1) & 1;
       const std::uint32_t sa = code_addr(st);
@@ -472,11 +498,18 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_a_full + 8 * (2 * grp + buf));
       if (tw) tstamp(a, grp, i, 3);
-      started |= 1u << s;
       if ((j + G >= per_rb) || (i + G >= count)) {
-        // epilogue of this row block: D (int32, exact) -> global accumulators
+        // epilogue of this row block: D (int32, exact) -> global accumulators.
+        // Stages present in D: the group's items of this row block sit at
+        // positions j, j - G, ... >= lo0 (the CTA's first position in it); with
+        // nst = 2 and G odd, two or more items cover both stages.
+        {
+          const std::uint32_t lo0 = j >= i ? j - i : 0;
+          started = 1u << s;
+          if (nst == 2 && (G & 1) && j >= lo0 + G) started = 3;
+        }
         if (seg == 0) pdl_wait();  // K1 zeroed the accumulators
-        mbar_wait(bar_d_full + 8 * grp, seg & 1);
+        mbar_wait(bar_d_full + 8 * (grp * T + tm), seg & 1);
         tc_fence_after();
         const std::uint32_t row = rb * 128 + row_in;
         const bool row_ok = row < a.m_local;
@@ -496,16 +529,18 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
           }
         }
         tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_d_empty + 8 * grp);  // D may be overwritten now
         started = 0;
         ++seg;
       }
-      ++use;
-      st += G;
+      use += T;
+      st += G * T;
       while (st >= S) {
         st -= S;
         ++r;
       }
-      j += G;
+      j += G * T;
       while (j >= per_rb) {
         j -= per_rb;
         ++rb;
@@ -526,14 +561,14 @@ __global__ void __launch_bounds__(Roles<G>::kThreads, 1) gemv_tc_kernel(TcArgs a
   }
 }
 
-template <int N, int G>
+template <int N, int G, int T>
 void set_attr() {
   static std::once_flag once;
   std::call_once(once, [] {
-    cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(kSmemBytes)),
                "tc smem attr");
-    cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
+    cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
   });
 }
 
@@ -547,10 +582,10 @@ int sm_count() {
   return v;
 }
 
-template <int N, int G>
+template <int N, int G, int T = 1>
 void launch_ng(const TcArgs& a, cudaStream_t s) {
-  set_attr<N, G>();
-  launch_pdl(gemv_tc_kernel<N, G>, dim3(sm_count()), dim3(Roles<G>::kThreads), kSmemBytes, s, a);
+  set_attr<N, G, T>();
+  launch_pdl(gemv_tc_kernel<N, G, T>, dim3(sm_count()), dim3(Roles<G, T>::kThreads), kSmemBytes, s, a);
 }
 
 }  // namespace
@@ -661,7 +696,7 @@ void launch_gemv_tc(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* 
   // TMEM: G decode groups x (2 A buffers x 72 columns + an accumulator of stages x N) <= 512
   auto fits = [&](int G) { return G * (2 * int(kAcols) + a.nst * N) <= 512; };
   switch (N) {
-    case 8: launch_ng<8, 3>(a, s); break;
+    case 8: launch_ng<8, 3, Q8P_K2_TEAMS>(a, s); break;
     case 16: fits(3) ? launch_ng<16, 3>(a, s) : launch_ng<16, 2>(a, s); break;
     case 32: launch_ng<32, 2>(a, s); break;
     case 48: launch_ng<48, 2>(a, s); break;

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "device.hpp"
 
@@ -390,6 +391,335 @@ __global__ void __launch_bounds__(128) rht_pass2_limbs(RhtArgs a) {
               static_cast<unsigned long long>(red[0] + red[1] + red[2] + red[3]));
 }
 
+
+// ---------------------------------------------------------------------------
+// Single-kernel cluster RHT (replaces pass1 + pass2 on the tensor-core path).
+// One thread-block cluster of C CTAs per vector (grid = (C, batch [+ zeroing])):
+//   CTA c loads the contiguous chunk of rows a in [c p/C, (c+1) p/C)
+//   (n/C floats: signs | limb-accumulator combine), applies the base B_q
+//   (B_q^T for K3) along each q-row, FWHT over the local a bits, then the
+//   chunks are transposed through distributed shared memory: CTA c takes
+//   columns [c W, (c+1) W) (W = n/C^2) of every source CTA, FWHT over the
+//   log2(C) cluster bits, and writes its part of the result.
+// Same H = (H_p (x) B_q) / sqrt(n) as had_apply (hadamard.cpp:170-210); the
+// butterflies are split differently from pass1/pass2, so fp32 rounding (not
+// the math) differs.  Smem per CTA is 2 n/C floats, small enough to co-reside
+// with the GEMV's CTAs under programmatic dependent launch.
+enum RhtMode { kK1Limbs = 0, kK3Acc = 1, kK3F32 = 2 };
+constexpr int kClThreads = 256;
+constexpr int kClMaxJ = 16;  // base-product outputs per thread (n/C <= 4096)
+
+__device__ __forceinline__ std::uint32_t cluster_ctarank() {
+  std::uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ float ld_dsmem_f32(const float* local_ptr, std::uint32_t cta) {
+  std::uint32_t a = static_cast<std::uint32_t>(__cvta_generic_to_shared(local_ptr)), r;
+  float v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(cta));
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(r));
+  return v;
+}
+__device__ __forceinline__ float4 ld_dsmem_f32x4(const float* local_ptr, std::uint32_t cta) {
+  std::uint32_t a = static_cast<std::uint32_t>(__cvta_generic_to_shared(local_ptr)), r;
+  float4 v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(cta));
+  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(r));
+  return v;
+}
+
+template <int Q, int MODE>
+__global__ void __launch_bounds__(kClThreads) rht_cluster(RhtArgs a, std::uint32_t C) {
+  extern __shared__ __align__(16) float smc[];
+  __shared__ float s_ss;
+  __shared__ long long s_tl;
+  __shared__ float red_f[kClThreads / 32];
+  __shared__ long long red_l[kClThreads / 32];
+  const int b = blockIdx.y;
+  const std::uint32_t c = cluster_ctarank();
+  pdl_wait();
+  pdl_trigger();
+  if (b >= a.batch) {  // K1: zero the GEMV accumulators / B-image tail (one cluster row)
+    if constexpr (MODE == kK1Limbs) {
+      const std::size_t nz = std::size_t(gridDim.x) * (gridDim.y - a.batch) * blockDim.x;
+      const std::size_t t0 = (std::size_t(b - a.batch) * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+      if (a.zero_ptr)
+        for (std::size_t i = t0; i < a.zero_words / 4; i += nz)
+          reinterpret_cast<int4*>(a.zero_ptr)[i] = make_int4(0, 0, 0, 0);
+      if (a.zero2_ptr)
+        for (std::size_t i = t0; i < a.zero2_bytes / 16; i += nz)
+          reinterpret_cast<int4*>(a.zero2_ptr)[i] = make_int4(0, 0, 0, 0);
+    }
+    return;
+  }
+  const std::uint32_t n = a.n, chunk = n / C, P = a.p / C, W = chunk / C;
+  const std::uint32_t e0 = c * chunk;
+  float* x = smc;              // [P][Q] local chunk
+  float* T = smc + chunk;      // [C][W] gathered columns
+  float* Bs = smc + 2 * chunk; // base (float for Q <= 28, int8 for 172)
+  if constexpr (Q > 1) {
+    if constexpr (Q <= 28) {
+      for (std::uint32_t i = threadIdx.x; i < Q * Q; i += blockDim.x) Bs[i] = float(a.base[i]);
+    } else {
+      for (std::uint32_t i = threadIdx.x; i < Q * Q / 4; i += blockDim.x)
+        reinterpret_cast<std::uint32_t*>(Bs)[i] = reinterpret_cast<const std::uint32_t*>(a.base)[i];
+    }
+  }
+  float ss = 0.f;
+  for (std::uint32_t v = threadIdx.x; v < chunk / 4; v += blockDim.x) {
+    const std::uint32_t i = e0 + 4 * v;
+    float4 val;
+    if constexpr (MODE == kK3Acc) {
+      val = combine4(a, b, i);
+    } else {
+      val = *reinterpret_cast<const float4*>(a.in + std::size_t(b) * n + i);
+      if constexpr (MODE == kK1Limbs) {
+        ss += val.x * val.x + val.y * val.y + val.z * val.z + val.w * val.w;
+        val = sign4(val, (a.signs[i >> 3] >> (i & 4)) & 0xFu);
+      }
+    }
+    reinterpret_cast<float4*>(x)[v] = val;
+  }
+  if constexpr (MODE == kK1Limbs) {  // deterministic CTA partial of |x|^2 (fixed tree)
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red_f[threadIdx.x >> 5] = ss;
+  }
+  __syncthreads();
+  if constexpr (MODE == kK1Limbs) {
+    if (threadIdx.x == 0) {
+      float t = 0.f;
+      for (int w = 0; w < kClThreads / 32; ++w) t += red_f[w];
+      s_ss = t;
+    }
+  }
+  if constexpr (Q > 1) {
+    // base along each q-row, two-phase through registers (in place)
+    float outv[kClMaxJ];
+#pragma unroll
+    for (int j = 0; j < kClMaxJ; ++j) {
+      const std::uint32_t e = threadIdx.x + j * kClThreads;
+      if (e < chunk) {
+        const std::uint32_t r = e / Q, cc = e - r * Q;
+        const float* xr = x + r * Q;
+        float acc = 0.f;
+        if constexpr (Q <= 28) {
+          if constexpr (MODE == kK1Limbs) {
+#pragma unroll 4
+            for (int k = 0; k < Q; ++k) acc += Bs[cc * Q + k] * xr[k];
+          } else {
+#pragma unroll 4
+            for (int k = 0; k < Q; ++k) acc += Bs[k * Q + cc] * xr[k];
+          }
+        } else {
+          const std::int8_t* B8 = reinterpret_cast<const std::int8_t*>(Bs);
+          if constexpr (MODE == kK1Limbs) {
+#pragma unroll 4
+            for (int k = 0; k < Q; ++k) acc += float(B8[cc * Q + k]) * xr[k];
+          } else {
+#pragma unroll 4
+            for (int k = 0; k < Q; ++k) acc += float(B8[k * Q + cc]) * xr[k];
+          }
+        }
+        outv[j] = acc;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kClMaxJ; ++j) {
+      const std::uint32_t e = threadIdx.x + j * kClThreads;
+      if (e < chunk) x[e] = outv[j];
+    }
+    __syncthreads();
+  }
+  fwht_rows<Q>(x, P);  // local a bits (ends with __syncthreads)
+  // -------- cluster transpose + FWHT over the C cluster bits --------
+  const float* res;    // this CTA's results: [C][W] with flat index s * chunk + c * W + w
+  std::uint32_t rstride;
+  if (C > 1) {
+    cluster_sync_all();  // every chunk is final and visible cluster-wide
+    for (std::uint32_t v = threadIdx.x; v < C * W / 4; v += blockDim.x) {
+      const std::uint32_t src = (4 * v) / W, w = (4 * v) - src * W;
+      reinterpret_cast<float4*>(T)[v] = ld_dsmem_f32x4(x + c * W + w, src);
+    }
+    __syncthreads();
+    for (std::uint32_t len = 1; len < C; len <<= 1) {  // radix-2 over the source-CTA index
+      for (std::uint32_t t = threadIdx.x; t < (C / 2) * W; t += blockDim.x) {
+        const std::uint32_t w = t % W, pr = t / W;
+        const std::uint32_t lo = ((pr / len) * 2 * len) + (pr % len), hi = lo + len;
+        const float u = T[lo * W + w], v2 = T[hi * W + w];
+        T[lo * W + w] = u + v2;
+        T[hi * W + w] = u - v2;
+      }
+      __syncthreads();
+    }
+    res = T;
+    rstride = W;
+  } else {
+    res = x;
+    rstride = chunk;
+  }
+  const float sc = rsqrtf(float(n));
+  if constexpr (MODE == kK1Limbs) {
+    // alpha: power of two >= |x|_2 / kLtMax from the cluster's |x|^2 partials (fixed order)
+    float ssum = 0.f;
+    if (C > 1) {
+      for (std::uint32_t r = 0; r < C; ++r) ssum += ld_dsmem_f32(&s_ss, r);
+    } else {
+      ssum = s_ss;
+    }
+    const float vv = sqrtf(ssum) * (1.0f + 1.0f / 1024.f) / float(kLtMax);
+    int ex = 0;
+    if (vv > 0.f) frexpf(vv, &ex);
+    const float alpha = vv > 0.f ? ldexpf(1.f, ex) : 1.f, inv = vv > 0.f ? ldexpf(1.f, -ex) : 1.f;
+    if (c == 0 && threadIdx.x == 0) a.alpha_out[b] = alpha;
+    long long tl = 0;
+    const std::uint32_t N = a.bcols, cw_per_row = rstride / 8, ncw = (C > 1 ? C : 1) * cw_per_row;
+    for (std::uint32_t t = threadIdx.x; t < ncw; t += blockDim.x) {
+      const std::uint32_t srow = t / cw_per_row, wc = (t - srow * cw_per_row) * 8;
+      const float* v = res + srow * rstride + wc;
+      const std::uint32_t flat = C > 1 ? srow * chunk + c * W + wc : e0 + wc;
+      const std::uint32_t k = flat >> 3;  // codeword index
+      int lt[8];
+      long long S = 0;
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        float tt = rintf(v[cc] * sc * inv);
+        tt = fminf(fmaxf(tt, -float(kLtMax)), float(kLtMax));
+        lt[cc] = int(tt);
+        S += lt[cc];
+      }
+      tl += S;
+      const int qk = int(S >> 3);  // floor(S / 8)
+      std::uint32_t wv[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        int l[4];
+        limbs4(lt[cc], l);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) wv[i][cc >> 2] |= (std::uint32_t(l[i]) & 0xFFu) << (8 * (cc & 3));
+      }
+      int ql[4];
+      limbs4(qk, ql);
+      const std::uint32_t ks = k >> 5, j = k & 31, kb = j >> 2;
+      std::uint8_t* slab = a.bimg + std::size_t(ks) * a.b_bytes;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        const std::uint32_t row = 4 * b + l;
+        const std::uint32_t rowoff = (row >> 3) * 256 + (row & 7) * 16;
+        *reinterpret_cast<uint2*>(slab + kb * N * 32 + rowoff + ((j & 3) >> 1) * 128 + (j & 1) * 8) =
+            make_uint2(wv[l][0], wv[l][1]);
+        slab[8 * N * 32 + rowoff + (j >> 4) * 128 + (j & 15)] = std::uint8_t(ql[l]);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) tl += __shfl_xor_sync(0xffffffffu, tl, o);
+    if ((threadIdx.x & 31) == 0) red_l[threadIdx.x >> 5] = tl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long t = 0;
+      for (int w = 0; w < kClThreads / 32; ++w) t += red_l[w];
+      s_tl = t;
+    }
+    if (C > 1) {
+      cluster_sync_all();  // partial TLs visible; no CTA leaves while its smem is read
+      if (c == 0 && threadIdx.x == 0) {
+        long long t = 0;
+        for (std::uint32_t r = 0; r < C; ++r) {
+          std::uint32_t aa = static_cast<std::uint32_t>(__cvta_generic_to_shared(&s_tl)), rr;
+          long long v;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rr) : "r"(aa), "r"(r));
+          asm volatile("ld.shared::cluster.s64 %0, [%1];" : "=l"(v) : "r"(rr));
+          t += v;
+        }
+        a.tl_out[b] = t;
+      }
+      cluster_sync_all();
+    } else {
+      __syncthreads();
+      if (threadIdx.x == 0) a.tl_out[b] = s_tl;
+    }
+  } else {
+    // K3: y_i = s_i (H^T z)_i / sqrt(n)
+    for (std::uint32_t t = threadIdx.x; t < (C > 1 ? C : 1) * rstride; t += blockDim.x) {
+      const std::uint32_t srow = t / rstride, w = t - srow * rstride;
+      const std::uint32_t flat = C > 1 ? srow * chunk + c * W + w : e0 + w;
+      float v = res[srow * rstride + w] * sc;
+      if ((a.signs[flat >> 3] >> (flat & 7)) & 1) v = -v;
+      a.out[std::size_t(b) * n + flat] = v;
+    }
+    if (C > 1) cluster_sync_all();  // no CTA leaves while its smem may still be read
+  }
+}
+
+// Cluster size for the single-kernel RHT: the largest C in {8, 4, 2, 1} with
+// C | p, (n / C^2) % 8 == 0 (codewords stay within one CTA's column block) and
+// n / C <= 4096 (register budget of the base product); 0 = unsupported.
+std::uint32_t cluster_size_for(const DevSide& side) {
+  // experiment knob: Q8P_RHT_MAXC=0 -> two-pass RHT, else the largest cluster size tried
+  static const int maxc = [] {
+    const char* e = std::getenv("Q8P_RHT_MAXC");
+    return e ? std::atoi(e) : 0;  // default: two-pass (measured faster in the pipeline)
+  }();
+  if (maxc <= 0) return 0;
+  for (std::uint32_t C = std::uint32_t(maxc); C >= 1; C >>= 1) {
+    if (side.p % C) continue;
+    const std::uint32_t chunk = side.n / C;
+    if (chunk > 4096 || chunk % 4) continue;
+    if (C > 1 && (chunk % C || (chunk / C) % 8)) continue;
+    if (C == 1 && chunk % 8) continue;
+    if ((side.q > 1) && chunk > kClThreads * kClMaxJ) continue;
+    return C;
+  }
+  return 0;
+}
+
+template <int Q, int MODE>
+void launch_cluster_q(const RhtArgs& a, std::uint32_t C, std::uint32_t zero_rows, cudaStream_t s) {
+  const std::size_t chunk = a.n / C;
+  const std::size_t bsz = Q == 1 ? 0 : (Q <= 28 ? Q * Q * 4 : (Q * Q + 15) / 16 * 16);
+  const std::size_t smem = 2 * chunk * 4 + bsz;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cuda_check(cudaFuncSetAttribute(rht_cluster<Q, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
+               "rht cluster smem attr");
+    cuda_check(cudaFuncSetAttribute(rht_cluster<Q, MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+               "rht cluster attr");
+  });
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(C, a.batch + zero_rows);
+  cfg.blockDim = dim3(kClThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  static const bool no_pdl = std::getenv("Q8P_RHT_CLUSTER_NOPDL") != nullptr;  // experiment knob
+  cfg.numAttrs = no_pdl ? 1 : 2;
+  cuda_check(cudaLaunchKernelEx(&cfg, rht_cluster<Q, MODE>, a, C), "rht cluster launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+template <int MODE>
+void launch_cluster(const RhtArgs& a, std::uint32_t C, std::uint32_t zero_rows, cudaStream_t s) {
+  switch (a.q) {
+    case 1: launch_cluster_q<1, MODE>(a, C, zero_rows, s); break;
+    case 4: launch_cluster_q<4, MODE>(a, C, zero_rows, s); break;
+    case 12: launch_cluster_q<12, MODE>(a, C, zero_rows, s); break;
+    case 20: launch_cluster_q<20, MODE>(a, C, zero_rows, s); break;
+    case 28: launch_cluster_q<28, MODE>(a, C, zero_rows, s); break;
+    case 172: launch_cluster_q<172, MODE>(a, C, zero_rows, s); break;
+    default: throw SizeError("rht: unsupported base order");
+  }
+}
+
 void plan_split(const DevSide& side, RhtArgs& a) {
   a.n = side.n;
   a.p = side.p;
@@ -414,7 +744,6 @@ void launch_pass1_q(const RhtArgs& a, std::uint32_t extra_ctas, cudaStream_t s) 
   std::call_once(once, [] {
     cuda_check(cudaFuncSetAttribute(rht_pass1<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
                "rht smem attr");
-    cuda_check(cudaFuncSetAttribute(rht_pass1<Q>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
   });
   launch_pdl(rht_pass1<Q>, dim3(a.P1 + extra_ctas, a.batch), dim3(kP1Threads), smem, s, a);
 }
@@ -439,7 +768,6 @@ void launch_pass2(const RhtArgs& a, cudaStream_t s) {
   std::call_once(once, [] {
     cuda_check(cudaFuncSetAttribute(rht_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
                "rht smem attr");
-    cuda_check(cudaFuncSetAttribute(rht_pass2, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
   });
   launch_pdl(rht_pass2, dim3(groups, a.batch), dim3(128), std::size_t(a.P1) * 16, s, a);
   cuda_check(cudaGetLastError(), "rht pass2 launch");
@@ -453,7 +781,6 @@ void launch_pass2_limbs(const RhtArgs& a, cudaStream_t s) {
   std::call_once(once, [] {
     cuda_check(cudaFuncSetAttribute(rht_pass2_limbs, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
                "rht smem attr");
-    cuda_check(cudaFuncSetAttribute(rht_pass2_limbs, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
   });
   launch_pdl(rht_pass2_limbs, dim3(chunk / 8, a.batch), dim3(128), std::size_t(a.P1) * 32, s, a);
   cuda_check(cudaGetLastError(), "rht pass2 limbs launch");
@@ -494,6 +821,10 @@ void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, flo
   a.out = y;
   a.batch = batch;
   a.fwd = 0;
+  if (const std::uint32_t C = cluster_size_for(side)) {
+    launch_cluster<kK3F32>(a, C, 0, s);
+    return;
+  }
   launch_pass1(a, 0, s);
   launch_pass2(a, s);
 }
@@ -521,6 +852,10 @@ void launch_rht_in_limbs(const DevSide& side, const float* x, float* u_scratch, 
   a.zero2_bytes = tail_bytes;
   a.batch = batch;
   a.fwd = 1;
+  if (const std::uint32_t C = cluster_size_for(side)) {
+    launch_cluster<kK1Limbs>(a, C, (zero_ptr && zero_words) || (bimg_tail && tail_bytes) ? 4 : 0, s);
+    return;
+  }
   launch_pass1(a, 32, s);
   launch_pass2_limbs(a, s);
 }
@@ -547,6 +882,10 @@ void launch_rht_out_acc(const DevSide& side, const std::int32_t* zacc, int zacc_
   a.out = y;
   a.batch = batch;
   a.fwd = 0;
+  if (const std::uint32_t C = cluster_size_for(side)) {
+    launch_cluster<kK3Acc>(a, C, 0, s);
+    return;
+  }
   launch_pass1(a, 0, s);
   launch_pass2(a, s);
 }
