@@ -99,6 +99,84 @@ __global__ void __launch_bounds__(128 + 32 * STW, 1) k_mma(int groups, int per_g
   }
 }
 
+// NI issuer warps, each issuing groups of 9 MMAs (N=8) into its own D with its own A columns.
+template <int NI, int FENCE, int STW = 0, int SLEEP = 0>
+__global__ void __launch_bounds__(512, 1) k_multi(int groups, unsigned long long* out) {
+  extern __shared__ __align__(1024) std::uint8_t smem[];
+  const std::uint32_t sb = smem_u32(smem);
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 16 * 1024 / 4; i += blockDim.x) reinterpret_cast<std::uint32_t*>(smem + 1024)[i] = 0x01010101u;
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < 8; ++c) mbar_init(sb + 16 + 8 * c, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(sb + 8);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  fence_proxy_async_smem();
+  const std::uint32_t tb = *reinterpret_cast<volatile std::uint32_t*>(smem + 8);
+  __shared__ int stop2;
+  if (threadIdx.x == 0) stop2 = 0;
+  __syncthreads();
+  if (warp >= 4 && warp < 4 + STW) {
+    std::uint32_t v[16];
+    for (int i = 0; i < 16; ++i) v[i] = threadIdx.x * i;
+    const std::uint32_t ta = tb + (std::uint32_t((warp & 3) * 32) << 16) + 296 + 8 * ((warp >> 2) & 1);
+    unsigned long long bytes = 0;
+    const std::uint64_t t0 = clock64();
+    while (*reinterpret_cast<volatile int*>(&stop2) == 0) {
+      for (int c = 0; c < 4; ++c) tmem_st16(ta, v);
+      tmem_st8(ta, *reinterpret_cast<std::uint32_t(*)[8]>(v));
+      tmem_wait_st();
+      bytes += 32 * 72 * 4;
+      v[0] += 1;
+      if (SLEEP) __nanosleep(SLEEP);
+    }
+    const std::uint64_t t1 = clock64();
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && warp == 4) out[8] = bytes * 1000 / (t1 - t0);  // per warp B/kcyc
+  }
+  if (warp < NI) {
+    constexpr std::uint32_t idesc = idesc_i8(128, 8);
+    const std::uint64_t bd = sdesc(sb + 1024 + warp * 2304, 128, 256);
+    const std::uint32_t a = tb + warp * 144, d = tb + 448 + warp * 16;
+    std::uint64_t t0 = clock64();
+    for (int g = 0; g < groups; ++g) {
+      if (FENCE & 1) tc_fence_after();
+      if (FENCE & 2) mbar_wait(sb + 48 + 8 * warp, 1);  // fresh barrier: completes at once
+      mma_i8_slab_e<16>(d, a + (g & 1) * 72, bd, idesc, 1, 1, sb + 16 + 8 * warp, sb + 16 + 8 * warp);
+    }
+    mma_commit_e(sb + 16 + 8 * warp);
+    // drain: wait for the final phase parity of this warp's barrier (2 commits/group + 1)
+    const std::uint32_t total = 2u * groups + 1u;
+    mbar_wait(sb + 16 + 8 * warp, (total - 1) & 1);
+    std::uint64_t t1 = clock64();
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) out[warp] = t1 - t0;
+    if ((threadIdx.x & 31) == 0) atomicAdd(&stop2, 1);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tb);
+  }
+}
+
+template <int NI, int FENCE = 0, int STW = 0, int SLEEP = 0>
+void run_multi(unsigned long long* d) {
+  const int groups = 2000;
+  cudaFuncSetAttribute(k_multi<NI, FENCE, STW, SLEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 1024);
+  k_multi<NI, FENCE, STW, SLEEP><<<148, 128 + 32 * STW, 32 * 1024>>>(groups, d);
+  cudaDeviceSynchronize();
+  unsigned long long c[4] = {0, 0, 0, 0};
+  cudaMemcpy(c, d, 8 * NI, cudaMemcpyDeviceToHost);
+  unsigned long long mx = 0;
+  for (int i = 0; i < NI; ++i) mx = c[i] > mx ? c[i] : mx;
+  unsigned long long sb8 = 0; cudaMemcpy(&sb8, d + 8, 8, cudaMemcpyDeviceToHost);
+  printf("multi-issuer fence=%d NI=%d stw=%d sleep=%d (sttm %.0f B/kcyc/warp): %.1f cyc per 9-MMA group per issuer, %.1f cyc per MMA aggregate (err=%s)\n", FENCE, NI, STW, SLEEP, double(sb8),
+         double(mx) / groups, double(mx) / (groups * 9.0 * NI), cudaGetErrorString(cudaGetLastError()));
+}
+
 // 4 warps store x16 columns repeatedly into TMEM.
 __global__ void __launch_bounds__(128, 1) k_sttm(int iters, unsigned long long* out) {
   __shared__ std::uint32_t slot;
@@ -150,11 +228,14 @@ void run(unsigned long long* d) {
 
 int main() {
   unsigned long long* d;
-  cudaMalloc(&d, 64);
+  cudaMalloc(&d, 64 * 8);
   run<8, true, 1, true>(d);
-  run<8, true, 1, true, 0, 1>(d);
-  run<8, true, 1, true, 0, 3>(d);
-  run<8, true, 4, true, 0, 3>(d);
+  cudaMemset(d, 0, 64 * 8);
+  run_multi<3>(d);
+  run_multi<3, 0, 12, 0>(d);
+  run_multi<3, 0, 12, 500>(d);
+  run_multi<3, 0, 12, 1000>(d);
+  run_multi<3, 0, 4, 0>(d);
   k_sttm<<<148, 128>>>(4000, d);
   cudaDeviceSynchronize();
   unsigned long long c;
