@@ -176,13 +176,15 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     layers = LAYERS_70B if args.workload == "70b" else LAYERS_7B
     hbm_peak, peak_kind = peaks()
+    sharded = world > 1 or args.sharded  # --sharded at N=1: the row-sharded path over a 1-rank NCCL comm
 
     comm = None
-    if world > 1:
+    if sharded:
         uid = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
             uid.copy_(torch.frombuffer(bytearray(q8p.NcclComm.unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid, 0)
+        if world > 1:
+            dist.broadcast(uid, 0)
         comm = q8p.NcclComm(bytes(uid.cpu().numpy()), world, rank, local)
 
     # Two full copies of the layer set rotate so every step streams from HBM
@@ -192,7 +194,7 @@ def run_ours(args):
     for c in range(args.copies):
         row = []
         for (m, n), art in zip(layers, arts):
-            if world > 1:
+            if sharded:
                 row.append(q8p.Layer.from_qshp(art, device=local, rows=q8p.shard_rows(m, world, rank)))
             else:
                 row.append(q8p.Layer.from_qshp(art, device=local))
@@ -211,7 +213,7 @@ def run_ours(args):
     def step(c, events=True):
         for li, L in enumerate(copies[c]):
             e = ev[c][li] if events else None
-            if world > 1:
+            if sharded:
                 L.forward_sharded(xs[li], comm, out=ys[li], stream=stream, workspace=ws)
             else:
                 L.forward(xs[li], out=ys[li], stream=stream, workspace=ws, gemv_events=e)
@@ -229,7 +231,7 @@ def run_ours(args):
                 step(c, events=False)
     torch.cuda.synchronize()
     graphs, ev_graphs = [], []
-    use_graph = not args.no_graph and world == 1
+    use_graph = not args.no_graph and not sharded
     if use_graph:
         # headline graphs: no event nodes (they would break the programmatic
         # dependent launch edges between kernels); instrumented twins time K2.
@@ -270,7 +272,7 @@ def run_ours(args):
         # gather GEMV durations of the last replay of each copy
     total_ms = t0.elapsed_time(t1)
     launches = (q8p.kernel_launches() - launches0) if not use_graph else 3 * len(layers) * args.steps
-    if world == 1:
+    if not sharded:
         # Re-run the timed steps once more collecting every GEMV event pair.
         with torch.cuda.stream(stream):
             for s in range(args.steps):
@@ -302,7 +304,7 @@ def run_ours(args):
             c = s % args.copies
             for li, L in enumerate(copies[c]):
                 xs[li].copy_(hx[li], non_blocking=True)
-                if world > 1:
+                if sharded:
                     L.forward_sharded(xs[li], comm, out=ys[li], stream=stream, workspace=ws)
                 else:
                     L.forward(xs[li], out=ys[li], stream=stream, workspace=ws)
@@ -318,7 +320,7 @@ def run_ours(args):
 
     # Roofline of the dominant kernel (K2) on the largest layer.
     roof = None
-    if world == 1 and all(gemv_ms[li] for li in range(n_gemv)):
+    if not sharded and all(gemv_ms[li] for li in range(n_gemv)):
         per = []
         for li, (m, n) in enumerate(layers):
             b = m * n // 8 * 2 + 4 * n + 4 * m
@@ -389,6 +391,7 @@ def main():
     ap.add_argument("--workload", default="70b", choices=["70b", "7b"])
     ap.add_argument("--copies", type=int, default=2)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="use q8p_forward_sharded even at N=1 (1-rank NCCL)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--sample-div", type=int, default=8, help="row sampling of --impl reference steps")
