@@ -237,8 +237,10 @@ def run_ours(args):
         # dependent launch edges between kernels); instrumented twins time K2.
         for c in range(args.copies):
             g = torch.cuda.CUDAGraph()
+            k0 = q8p.kernel_launches()
             with torch.cuda.graph(g, stream=stream):
                 step(c, events=False)
+            launches_per_step = q8p.kernel_launches() - k0  # q8p kernels captured per step
             graphs.append(g)
             g2 = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g2, stream=stream):
@@ -271,7 +273,7 @@ def run_ours(args):
             dist.barrier()
         # gather GEMV durations of the last replay of each copy
     total_ms = t0.elapsed_time(t1)
-    launches = (q8p.kernel_launches() - launches0) if not use_graph else 3 * len(layers) * args.steps
+    launches = (q8p.kernel_launches() - launches0) if not use_graph else launches_per_step * args.steps
     if not sharded:
         # Re-run the timed steps once more collecting every GEMV event pair.
         with torch.cuda.stream(stream):
