@@ -146,6 +146,8 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
     {
       const std::vector<std::uint8_t> img = tc_lut_image();
       L->lut_img = static_cast<const std::uint8_t*>(upload(L.get(), img.data(), img.size()));
+      const unsigned zero2[2] = {0u, 0u};
+      L->gbar = static_cast<unsigned*>(upload(L.get(), zero2, sizeof(zero2)));
     }
     const std::size_t nb = d.n / 8, words = std::size_t(r1 - r0) * nb;
     for (int s = 0; s < d.num_stages; ++s) {
@@ -361,6 +363,12 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
   DeviceGuard g(L->device);
   Workspace w;
   workspace_parts(L, batch, &w, ws);
+  if (tc_fused_supported(*L, batch)) {  // one persistent launch: K1 + K2 + K3
+    if (opts) record_event(opts->gemv_start_event, s);
+    launch_layer_fused(*L, x, y, w.u, w.ssq, w.alpha, w.tl, w.bimg, w.zacc, w.rows_pad, batch, s);
+    if (opts) record_event(opts->gemv_end_event, s);
+    return;
+  }
   forward_local(L, x, batch, w, s, opts);
   if (tc_supported(*L, batch)) {
     float zscale[2] = {L->scale[0], L->scale[1]};

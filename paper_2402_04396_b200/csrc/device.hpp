@@ -77,6 +77,7 @@ struct q8p_layer {
   void* codes[2] = {nullptr, nullptr};  // plain [m_local][n/8]: u16 (E8P) / u8 (e8-1bit)
   q8p::detail::SlabCodes tc[2];
   const std::uint8_t* lut_img = nullptr;   // device 64 KiB lane-replicated decode LUT (gemv_tc.cu)
+  unsigned* gbar = nullptr;                // device [2] grid-barrier counters of the fused layer kernel
   std::size_t device_bytes = 0;
   std::size_t code_bytes = 0;
   std::vector<void*> allocations;
@@ -121,6 +122,11 @@ void launch_rht_in_limbs(const DevSide& side, const float* x, float* u_scratch, 
                          long long* tl, std::uint8_t* bimg, std::uint32_t b_bytes, std::uint32_t bcols,
                          std::uint8_t* bimg_tail, std::size_t tail_bytes, std::int32_t* zero_ptr,
                          std::size_t zero_words, int batch, cudaStream_t s);
+// Fused layer kernel (gemv_tc.cu): K1 + K2 (+ K3 when y != nullptr) in one persistent launch.
+bool tc_fused_supported(const q8p_layer& L, int batch);
+void launch_layer_fused(const q8p_layer& L, const float* x, float* y, float* u_scratch, float* ssq, float* alpha,
+                        long long* tl, std::uint8_t* bimg, std::int32_t* zacc, std::uint32_t rows_pad, int batch,
+                        cudaStream_t s);
 // Row-sharded forward: this rank's fp32 z rows [batch][m_local] from the limb accumulators.
 void launch_combine_acc(const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows, std::uint32_t zacc_cols,
                         const float zscale[2], const int ze8p[2], const float* alpha, const long long* tl, float* z,

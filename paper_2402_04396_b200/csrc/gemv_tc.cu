@@ -55,6 +55,7 @@
 #include <mutex>
 
 #include "device.hpp"
+#include "rht_device.cuh"
 #include "tc05.hpp"
 
 namespace q8p::detail {
@@ -105,6 +106,17 @@ struct TcArgs {
   std::uint32_t smem_bytes;
   const std::uint8_t* lut_img;    // 64 KiB LUT window image (tc_lut_image)
   unsigned long long* trace;      // debug timeline (Q8P_TRACE), CTA 0 only; nullptr = off
+  // ---- fused layer kernel (K1 + K2 [+ K3] in one launch) ----
+  int fuse;                       // 0: K2 only, 1: K1 + K2, 2: K1 + K2 + K3
+  int batch;
+  RhtArgs k1, k3;                 // pass arguments of the input / output transforms
+  std::uint32_t k1_p1, k1_p2, k3_p1, k3_p2;  // virtual blocks (x batch) of each pass
+  unsigned* gbar;                 // [2] grid-barrier counters of this layer (zero at rest)
+  std::uint32_t scratch_bytes;    // RHT scratch at the top of the dynamic smem
+  std::int32_t* zero_ptr;         // accumulators to zero (K1 duty)
+  std::size_t zero_words;
+  std::uint8_t* zero2_ptr;        // B-image tail to zero (ragged n)
+  std::size_t zero2_bytes;
 };
 
 // Debug timeline: trace[role][item][4] clock64 stamps (roles 0..7 decoder
@@ -186,13 +198,13 @@ __device__ __forceinline__ void e8p_fin(std::uint32_t nib, std::uint32_t fl, std
   hi = prmt(ct_lo, ct_hi, __umulhi(sel, 65536u));  // sel >> 16
 }
 
-template <int N, int G, int T>
+template <int N, int G, int T, bool FUSED>
 __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArgs a) {
   extern __shared__ __align__(1024) std::uint8_t smem[];
   // warp index via shfl: the compiler then knows every role branch is warp-uniform
   const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const std::uint32_t sbase = smem_u32(smem);
-  const std::uint32_t send = sbase + a.smem_bytes;
+  const std::uint32_t send = sbase + a.smem_bytes - a.scratch_bytes;  // RHT scratch above the ring
   const std::uint32_t lutw = (sbase + kCtl + 0xFFFFu) & ~0xFFFFu;
   // control block: barriers + TMEM base
   const std::uint32_t bar_full_c = sbase;                       // [kMaxStages] code slab landed
@@ -286,6 +298,54 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
 #ifdef Q8P_K2_TRACE
   if (threadIdx.x == 0) gstamp(1);
 #endif
+
+  // ---- fused layer: K1 on the issue + decode warps while warp 0 streams codes ----
+  __shared__ float s_red[32];
+  __shared__ long long s_redl[32];
+  __shared__ float s_alpha[2];
+  const Team tm{threadIdx.x - 32u, std::uint32_t(Roles<G, T>::kThreads - 32), 1u};
+  auto tm_tid0 = [&]() { return threadIdx.x == 32; };
+  (void)tm_tid0;
+#ifdef Q8P_K2_TRACE
+  auto pstamp = [&](int k) {  // fused-phase timeline, per CTA (globaltimer ns), team thread 0
+    if (a.trace != nullptr && blockIdx.x < 148 && tm_tid0()) {
+      std::uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[12 * kTraceItems * 4 + blockIdx.x * 12 + k] = t;
+    }
+  };
+#else
+  auto pstamp = [](int) {};
+#endif
+  float* const scr = reinterpret_cast<float*>(smem + (a.smem_bytes - a.scratch_bytes));
+  if constexpr (FUSED) {
+    if (warp != kWarpProd) {
+      pstamp(0);
+      pdl_wait();  // x (and our workspace) are the previous kernel's
+      pstamp(1);
+      {  // K1 duties: zero the accumulators, the ragged B-image tail and TL
+        const std::size_t t0 = std::size_t(blockIdx.x) * tm.n + tm.tid, ts = std::size_t(gridDim.x) * tm.n;
+        if (a.zero_ptr)
+          for (std::size_t i = t0; i < a.zero_words / 4; i += ts)
+            reinterpret_cast<int4*>(a.zero_ptr)[i] = make_int4(0, 0, 0, 0);
+        if (a.zero2_ptr)
+          for (std::size_t i = t0; i < a.zero2_bytes / 16; i += ts)
+            reinterpret_cast<int4*>(a.zero2_ptr)[i] = make_int4(0, 0, 0, 0);
+        if (blockIdx.x == 0 && tm.tid < std::uint32_t(a.batch)) a.k1.tl_out[tm.tid] = 0;
+      }
+      for (std::uint32_t vb = blockIdx.x; vb < a.k1_p1; vb += gridDim.x)
+        rht_p1_dispatch(a.k1, vb % a.k1.P1, int(vb / a.k1.P1), scr, s_red, tm);
+      pstamp(2);
+      grid_barrier(a.gbar, gridDim.x, tm);
+      pstamp(3);
+      const std::uint32_t g8 = a.k1.P2 * a.k1.q / 8;
+      for (std::uint32_t vb = blockIdx.x; vb < a.k1_p2; vb += gridDim.x)
+        rht_p2_limbs_body(a.k1, vb % g8, int(vb / g8), scr, s_redl, s_alpha, tm);
+      pstamp(4);
+      grid_barrier(a.gbar, 2 * gridDim.x, tm);  // B images, alpha, TL complete
+      pstamp(5);
+    }
+  }
 
   if (warp == kWarpProd) {
     // ===== code producer (whole warp, lane-elected issue); codes do not depend on K1 =====
@@ -547,6 +607,34 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
       }
     }
   }
+  if constexpr (FUSED) {
+    if (warp != kWarpProd) {
+      if (a.fuse == 2) {  // K3 on the full z once every CTA's accumulators are in
+        team_sync(tm);
+        pstamp(6);
+        grid_barrier(a.gbar, 3 * gridDim.x, tm);
+        pstamp(7);
+        for (std::uint32_t vb = blockIdx.x; vb < a.k3_p1; vb += gridDim.x)
+          rht_p1_dispatch(a.k3, vb % a.k3.P1, int(vb / a.k3.P1), scr, s_red, tm);
+        pstamp(8);
+        grid_barrier(a.gbar, 4 * gridDim.x, tm);
+        pstamp(9);
+        const std::uint32_t g4 = a.k3.P2 * a.k3.q / 4;
+        for (std::uint32_t vb = blockIdx.x; vb < a.k3_p2; vb += gridDim.x)
+          rht_p2_body(a.k3, vb % g4, int(vb / g4), scr, s_red, tm);
+        pstamp(10);
+      }
+      team_sync(tm);
+      if (tm.tid == 0) {  // last CTA out resets the barrier for the next launch
+        const unsigned old = atomicAdd(a.gbar + 1, 1u);
+        if (old == gridDim.x - 1) {
+          a.gbar[0] = 0;
+          a.gbar[1] = 0;
+          __threadfence();
+        }
+      }
+    }
+  }
   if (threadIdx.x == 0) tstamp(a, 10, 0, 2);
   tc_fence_before();
   __syncthreads();
@@ -561,14 +649,18 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
   }
 }
 
-template <int N, int G, int T>
+constexpr std::size_t kSmemFused = 225 * 1024;  // fused layer kernel: nothing else to co-reside with
+
+template <int N, int G, int T, bool FUSED>
 void set_attr() {
   static std::once_flag once;
   std::call_once(once, [] {
-    cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(kSmemBytes)),
+    cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G, T, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(FUSED ? kSmemFused : kSmemBytes)),
                "tc smem attr");
-    cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
+    cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G, T, FUSED>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    100),
+               "carveout");
   });
 }
 
@@ -582,10 +674,11 @@ int sm_count() {
   return v;
 }
 
-template <int N, int G, int T = 1>
+template <int N, int G, int T = 1, bool FUSED = false>
 void launch_ng(const TcArgs& a, cudaStream_t s) {
-  set_attr<N, G, T>();
-  launch_pdl(gemv_tc_kernel<N, G, T>, dim3(sm_count()), dim3(Roles<G, T>::kThreads), kSmemBytes, s, a);
+  set_attr<N, G, T, FUSED>();
+  launch_pdl(gemv_tc_kernel<N, G, T, FUSED>, dim3(sm_count()), dim3(Roles<G, T>::kThreads),
+             FUSED ? kSmemFused : kSmemBytes, s, a);
 }
 
 }  // namespace
@@ -666,9 +759,10 @@ std::uint32_t tc_bimg_bytes(std::uint32_t n, int batch) {
   return tc_k_slabs(n) * 9u * std::uint32_t(tc_ncols_pad(4 * batch)) * 32u;
 }
 
-void launch_gemv_tc(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* zacc, std::uint32_t rows_pad,
-                    int batch, cudaStream_t s) {
-  TcArgs a{};
+namespace {
+void fill_tc_args(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* zacc, std::uint32_t rows_pad, int batch,
+                  TcArgs& a) {
+  a = TcArgs{};
   a.nst = L.num_stages;
   for (int st = 0; st < L.num_stages; ++st) {
     a.codes[st] = static_cast<const std::uint8_t*>(L.tc[st].codes);
@@ -686,6 +780,15 @@ void launch_gemv_tc(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* 
   a.ncols = 4 * batch;
   a.smem_bytes = std::uint32_t(kSmemBytes);
   a.lut_img = L.lut_img;
+  a.batch = batch;
+}
+}  // namespace
+
+void launch_gemv_tc(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* zacc, std::uint32_t rows_pad,
+                    int batch, cudaStream_t s) {
+  TcArgs a;
+  fill_tc_args(L, bimg, zacc, rows_pad, batch, a);
+  const int N = tc_ncols_pad(4 * batch);
   static const char* trace_env = std::getenv("Q8P_TRACE");  // debug: dump CTA 0's timeline
   unsigned long long* tr = nullptr;
   if (trace_env != nullptr) {
@@ -696,7 +799,7 @@ void launch_gemv_tc(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* 
   // TMEM: G decode groups x (2 A buffers x 72 columns + an accumulator of stages x N) <= 512
   auto fits = [&](int G) { return G * (2 * int(kAcols) + a.nst * N) <= 512; };
   switch (N) {
-    case 8: launch_ng<8, 3, Q8P_K2_TEAMS>(a, s); break;
+    case 8: launch_ng<8, 3, Q8P_K2_TEAMS, false>(a, s); break;
     case 16: fits(3) ? launch_ng<16, 3>(a, s) : launch_ng<16, 2>(a, s); break;
     case 32: launch_ng<32, 2>(a, s); break;
     case 48: launch_ng<48, 2>(a, s); break;
@@ -710,6 +813,99 @@ void launch_gemv_tc(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* 
     cudaFree(tr);
     static int seq = 0;
     const std::string path = std::string(trace_env) + "." + std::to_string(seq++) + "." + std::to_string(L.m_local()) +
+                             "x" + std::to_string(L.n) + ".bin";
+    if (FILE* f = std::fopen(path.c_str(), "wb")) {
+      std::fwrite(h.data(), 8, h.size(), f);
+      std::fclose(f);
+    }
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+bool tc_fused_supported(const q8p_layer& L, int batch) {
+  // experiment knob: the fused layer kernel is correct (GPU tests) but slower in the
+  // pipeline (grid barriers under a saturated memory system) -> opt-in
+  static const bool on = std::getenv("Q8P_FUSE") != nullptr;
+  if (!on || !tc_supported(L, batch) || tc_ncols_pad(4 * batch) != 8 || L.gbar == nullptr) return false;
+  // RHT scratch must leave a useful code ring
+  const std::size_t scr = std::max({rht_p1_smem_bytes(L.side_v), rht_p2_smem_bytes(L.side_v),
+                                    rht_p1_smem_bytes(L.side_u), rht_p2_smem_bytes(L.side_u)});
+  return scr <= 40 * 1024;
+}
+
+void launch_layer_fused(const q8p_layer& L, const float* x, float* y, float* u_scratch, float* ssq, float* alpha,
+                        long long* tl, std::uint8_t* bimg, std::int32_t* zacc, std::uint32_t rows_pad, int batch,
+                        cudaStream_t s) {
+  TcArgs a;
+  fill_tc_args(L, bimg, zacc, rows_pad, batch, a);
+  const std::uint32_t N = std::uint32_t(tc_ncols_pad(4 * batch)), KSL = tc_k_slabs(L.n), bb = 9u * N * 32u;
+  a.fuse = y != nullptr ? 2 : 1;
+  a.gbar = L.gbar;
+  a.smem_bytes = std::uint32_t(kSmemFused);
+  const std::size_t scr = std::max({rht_p1_smem_bytes(L.side_v), rht_p2_smem_bytes(L.side_v),
+                                    rht_p1_smem_bytes(L.side_u), rht_p2_smem_bytes(L.side_u)});
+  a.scratch_bytes = std::uint32_t((scr + 1023) & ~std::size_t(1023));
+  // K1: t = T_v x -> B images, alpha, TL (same arguments as launch_rht_in_limbs)
+  RhtArgs& k1 = a.k1;
+  rht_plan_split(L.side_v, k1);
+  k1.signs = L.side_v.signs;
+  k1.base = L.side_v.base;
+  k1.in = x;
+  k1.mid = u_scratch;
+  k1.ssq = ssq;
+  k1.alpha_out = alpha;
+  k1.tl_out = tl;
+  k1.bimg = bimg;
+  k1.b_bytes = bb;
+  k1.bcols = N;
+  k1.batch = batch;
+  k1.fwd = 1;
+  a.k1_p1 = k1.P1 * std::uint32_t(batch);
+  a.k1_p2 = (k1.P2 * k1.q / 8) * std::uint32_t(batch);
+  a.zero_ptr = zacc;
+  a.zero_words = std::size_t(L.num_stages) * N * rows_pad;
+  if ((L.n / 8) % 32 != 0) {
+    a.zero2_ptr = bimg + std::size_t(KSL - 1) * bb;
+    a.zero2_bytes = bb;
+  }
+  if (y != nullptr) {  // K3: y = T_u^T z from the limb accumulators (launch_rht_out_acc)
+    RhtArgs& k3 = a.k3;
+    rht_plan_split(L.side_u, k3);
+    k3.signs = L.side_u.signs;
+    k3.base = L.side_u.base;
+    k3.zacc = zacc;
+    k3.zrows = rows_pad;
+    k3.zcols = N;
+    k3.zstages = L.num_stages;
+    k3.zscale0 = L.scale[0];
+    k3.zscale1 = L.scale[1];
+    k3.ze8p0 = L.cb[0] == Q8P_CB_E8P_2BIT;
+    k3.ze8p1 = L.cb[1] == Q8P_CB_E8P_2BIT;
+    k3.alpha_in = alpha;
+    k3.tl_in = tl;
+    k3.mid = u_scratch;
+    k3.out = y;
+    k3.batch = batch;
+    k3.fwd = 0;
+    a.k3_p1 = k3.P1 * std::uint32_t(batch);
+    a.k3_p2 = (k3.P2 * k3.q / 4) * std::uint32_t(batch);
+  }
+  static const char* trace_env = std::getenv("Q8P_TRACE");  // debug: per-CTA phase timeline
+  unsigned long long* tr = nullptr;
+  if (trace_env != nullptr) {
+    cuda_check(cudaMalloc(&tr, 16 * kTraceItems * 4 * 8), "trace alloc");
+    cuda_check(cudaMemset(tr, 0, 16 * kTraceItems * 4 * 8), "trace memset");
+  }
+  a.trace = tr;
+  launch_ng<8, 3, 1, true>(a, s);
+  cuda_check(cudaGetLastError(), "fused layer launch");
+  if (tr != nullptr) {
+    std::vector<unsigned long long> h(16 * kTraceItems * 4);
+    cuda_check(cudaStreamSynchronize(s), "trace sync");
+    cuda_check(cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost), "trace copy");
+    cudaFree(tr);
+    static int seq = 0;
+    const std::string path = std::string(trace_env) + ".fused." + std::to_string(seq++) + "." + std::to_string(L.m) +
                              "x" + std::to_string(L.n) + ".bin";
     if (FILE* f = std::fopen(path.c_str(), "wb")) {
       std::fwrite(h.data(), 8, h.size(), f);

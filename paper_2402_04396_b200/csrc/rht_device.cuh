@@ -1,0 +1,394 @@
+// Device-side pieces of the randomized Hadamard transforms (K1 / K3), shared
+// by the standalone RHT kernels (kernels_rht.cu) and the fused layer kernel
+// (gemv_tc.cu).  The pass bodies run on a "team" of threads (a whole CTA with
+// __syncthreads, or a subset of a CTA's warps with a named barrier), so the
+// fused kernel can run them on its decode/issue warps while its producer warp
+// streams codes.
+//
+// SideTransform (core/src/transforms.cpp:28-47) with had_apply
+// (core/src/hadamard.cpp:170-210):  H = (H_p (x) B_q) / sqrt(n), flat index
+// i = a * q + b, a = a_hi * P2 + a_lo.  Pass 1 = a contiguous chunk
+// [a_hi][0..P2)[0..q) (signs | limb combine, base B_q or B_q^T on each q-row,
+// FWHT over a_lo); pass 2 = a group of adjacent columns (a_lo, b) over all P1
+// values of a_hi (FWHT over a_hi, 1/sqrt(n), signs / integer limbs).
+#pragma once
+
+#include <cstdint>
+
+namespace q8p::detail {
+
+struct RhtArgs {
+  std::uint32_t n, p, q, P2, P1;
+  const std::uint8_t* signs;   // ceil(n/8) bytes, LSB-first, bit set = -1
+  const std::int8_t* base;     // q x q (+-1) when q > 1
+  const float* in;             // pass 1 fp32 input [batch][n] (or nullptr with zacc)
+  const std::int32_t* zacc;    // K3 pass 1: int32 limb accumulators [stage][zcols][zrows]
+  std::uint32_t zrows, zcols;
+  int zstages;
+  int ze8p0, ze8p1;            // K3: stage s is E8P (subtract TL / 4)
+  float zscale0, zscale1;      // K3: stage scales
+  const float* alpha_in;       // K3: per-vector activation scale
+  const long long* tl_in;      // K3: per-vector sum of integer activations
+  const float* colsum;         // K1 (fp32 path): base column sums (q floats)
+  float* tsum_out;             // K1 (fp32 path): per-vector sum of t
+  float* mid;                  // [batch][n] intermediate
+  float* out;                  // [batch][n] (fp32 path)
+  float* amax_out;             // K1 (fp32 path): per-vector amax
+  float* ssq;                  // K1 (limb path): [batch][P1] per-chunk sums of squares of x
+  float* alpha_out;            // K1 (limb path): [batch]
+  long long* tl_out;           // K1 (limb path): [batch]
+  std::uint8_t* bimg;          // K1 (limb path): B images [KSL][9][bcols/8][2][8][16]
+  std::uint32_t b_bytes, bcols;
+  std::int32_t* zero_ptr;      // K1: accumulators to zero (pass-1 spare CTAs)
+  std::size_t zero_words;
+  std::uint8_t* zero2_ptr;     // K1: B-image tail to zero
+  std::size_t zero2_bytes;
+  int batch;
+  int fwd;
+};
+
+struct Team {
+  std::uint32_t tid, n, bar;  // thread index in the team, team size, named barrier (0 = __syncthreads)
+};
+
+// Host helpers (kernels_rht.cu): pass geometry / arguments for the fused layer kernel.
+void rht_plan_split(const DevSide& side, RhtArgs& a);  // n, p, q, P2, P1
+std::size_t rht_p1_smem_bytes(const DevSide& side);     // pass-1 scratch of this side
+std::size_t rht_p2_smem_bytes(const DevSide& side);     // pass-2 scratch (limb flavour, the larger)
+
+namespace {
+
+
+__device__ __forceinline__ Team block_team() { return Team{threadIdx.x, blockDim.x, 0u}; }
+__device__ __forceinline__ void team_sync(const Team& t) {
+  if (t.bar == 0)
+    __syncthreads();
+  else
+    asm volatile("bar.sync %0, %1;\n" ::"r"(t.bar), "r"(t.n) : "memory");
+}
+
+__device__ __forceinline__ void atomic_max_pos(float* addr, float v) {
+  // |t| >= 0: IEEE ordering of non-negative floats equals their int ordering.
+  atomicMax(reinterpret_cast<int*>(addr), __float_as_int(v));
+}
+
+__device__ __forceinline__ float4 sign4(float4 v, std::uint32_t nib) {
+  if (nib & 1) v.x = -v.x;
+  if (nib & 2) v.y = -v.y;
+  if (nib & 4) v.z = -v.z;
+  if (nib & 8) v.w = -v.w;
+  return v;
+}
+
+// Radix-2^R FWHT pass over index bits [sbit, sbit + R) of the row index of an
+// smem matrix with `rows` rows of Q floats (row stride Q): each task loads 2^R
+// elements, does R butterfly stages in registers, stores them back.
+template <int R, int Q>
+__device__ __forceinline__ void fwht_pass(float* s, std::uint32_t rows, std::uint32_t sbit, const Team& tm) {
+  constexpr int K = 1 << R;
+  const std::uint32_t tasks = (rows >> R) * Q;
+  const std::uint32_t lowmask = (1u << sbit) - 1;
+  for (std::uint32_t t = tm.tid; t < tasks; t += tm.n) {
+    const std::uint32_t b = t % Q, tr = t / Q;
+    const std::uint32_t base = ((((tr >> sbit) << (sbit + R)) | (tr & lowmask)) * Q) + b;
+    float v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = s[base + ((std::uint32_t(k) << sbit) * Q)];
+#pragma unroll
+    for (int len = 1; len < K; len <<= 1)
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (!(k & len)) {
+          const float x = v[k], y = v[k + len];
+          v[k] = x + y;
+          v[k + len] = x - y;
+        }
+#pragma unroll
+    for (int k = 0; k < K; ++k) s[base + ((std::uint32_t(k) << sbit) * Q)] = v[k];
+  }
+  team_sync(tm);
+}
+
+template <int Q>
+__device__ void fwht_rows(float* s, std::uint32_t rows, const Team& tm) {
+  const std::uint32_t lb = 31 - __clz(rows);
+  std::uint32_t b = 0;
+  for (; b + 3 <= lb; b += 3) fwht_pass<3, Q>(s, rows, b, tm);
+  if (b + 2 <= lb) {
+    fwht_pass<2, Q>(s, rows, b, tm);
+    b += 2;
+  }
+  if (b + 1 <= lb) fwht_pass<1, Q>(s, rows, b, tm);
+}
+
+// z rows i..i+3 of vector b from the int32 limb accumulators:
+// z = sum_s scale_s alpha (2 Z_s - [E8P] TL) / 4, Z_s = sum_l 128^(3-l) zacc[s][4b + l]
+// (exact int64 combine, one double rounding per stage sum, then fp32).  Shared by
+// K3 pass 1 and the row-sharded combine kernel so both round identically.
+__device__ __forceinline__ float4 combine4(const RhtArgs& a, int b, std::uint32_t i) {
+  // __ldcg: written earlier in the same fused kernel by other CTAs (L1 is not coherent)
+  const double al = double(__ldcg(a.alpha_in + b)) * 0.25;
+  const long long tl = __ldcg(a.tl_in + b);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int st = 0; st < a.zstages; ++st) {
+    const std::int32_t* z = a.zacc + (std::size_t(st) * a.zcols + 4 * b) * a.zrows + i;
+    const int4 v0 = __ldcg(reinterpret_cast<const int4*>(z));
+    const int4 v1 = __ldcg(reinterpret_cast<const int4*>(z + a.zrows));
+    const int4 v2 = __ldcg(reinterpret_cast<const int4*>(z + 2 * std::size_t(a.zrows)));
+    const int4 v3 = __ldcg(reinterpret_cast<const int4*>(z + 3 * std::size_t(a.zrows)));
+    const long long sub = (st == 0 ? a.ze8p0 : a.ze8p1) ? tl : 0;
+    const double c = al * double(st == 0 ? a.zscale0 : a.zscale1);
+    auto zt = [&](int x0, int x1, int x2, int x3) {
+      const long long Z = ((static_cast<long long>(x0) * 128 + x1) * 128 + x2) * 128 + x3;
+      return double(2 * Z - sub) * c;
+    };
+    acc[0] += zt(v0.x, v1.x, v2.x, v3.x);
+    acc[1] += zt(v0.y, v1.y, v2.y, v3.y);
+    acc[2] += zt(v0.z, v1.z, v2.z, v3.z);
+    acc[3] += zt(v0.w, v1.w, v2.w, v3.w);
+  }
+  return make_float4(float(acc[0]), float(acc[1]), float(acc[2]), float(acc[3]));
+}
+
+
+// Pass-1 smem bytes for chunk P2 * Q (x, base output, base).
+template <int Q>
+__host__ __device__ constexpr std::size_t p1_smem_bytes(std::uint32_t P2) {
+  return std::size_t(P2) * Q * 4 * (Q > 1 ? 2 : 1) + (Q == 1 ? 0 : (Q <= 28 ? Q * Q * 4 : (Q * Q + 15) / 16 * 16));
+}
+
+// Pass 1 on chunk `ch` of vector b.  red: >= 32 floats of team-shared smem.
+template <int Q>
+__device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* sm1, float* red, const Team& tm) {
+  const std::uint32_t chunk = a.P2 * Q;  // floats, multiple of 4
+  const std::uint32_t e0 = ch * chunk;
+  float* x = sm1;                         // [P2][Q]
+  float* y = sm1 + chunk;                 // base output (Q > 1)
+  float* Bs = sm1 + 2 * chunk;            // Q x Q base as float (Q <= 28) / int8 (Q = 172)
+  if constexpr (Q > 1) {
+    if constexpr (Q <= 28) {
+      for (std::uint32_t i = tm.tid; i < Q * Q; i += tm.n) Bs[i] = float(a.base[i]);
+    } else {
+      std::int8_t* B8 = reinterpret_cast<std::int8_t*>(Bs);
+      for (std::uint32_t i = tm.tid; i < Q * Q / 4; i += tm.n)
+        reinterpret_cast<std::uint32_t*>(B8)[i] = reinterpret_cast<const std::uint32_t*>(a.base)[i];
+    }
+  }
+  float ss = 0.f;
+  for (std::uint32_t v = tm.tid; v < chunk / 4; v += tm.n) {
+    const std::uint32_t i = e0 + 4 * v;
+    float4 val;
+    if (a.zacc) {
+      val = combine4(a, b, i);
+    } else {
+      val = __ldcg(reinterpret_cast<const float4*>(a.in + std::size_t(b) * a.n + i));
+      ss += val.x * val.x + val.y * val.y + val.z * val.z + val.w * val.w;
+      if (a.fwd) val = sign4(val, (a.signs[i >> 3] >> (i & 4)) & 0xFu);
+    }
+    reinterpret_cast<float4*>(x)[v] = val;
+  }
+  if (a.ssq) {  // deterministic per-chunk sum of squares (fixed reduction tree)
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((tm.tid & 31) == 0) red[tm.tid >> 5] = ss;
+    team_sync(tm);
+    if (tm.tid == 0) {
+      float t = 0.f;
+      for (std::uint32_t w = 0; w < (tm.n + 31) / 32; ++w) t += red[w];
+      a.ssq[std::size_t(b) * a.P1 + ch] = t;
+    }
+  }
+  team_sync(tm);
+  float* cur = x;
+  if constexpr (Q > 1) {
+    // base along each contiguous q-row: y[r][c] = sum_k B[c][k] x[r][k] (fwd) or B[k][c] (K3)
+    for (std::uint32_t e = tm.tid; e < chunk; e += tm.n) {
+      const std::uint32_t r = e / Q, c = e - r * Q;
+      const float* xr = x + r * Q;
+      float acc = 0.f;
+      if constexpr (Q <= 28) {
+        if (a.fwd) {
+#pragma unroll 4
+          for (int k = 0; k < Q; ++k) acc += Bs[c * Q + k] * xr[k];
+        } else {
+#pragma unroll 4
+          for (int k = 0; k < Q; ++k) acc += Bs[k * Q + c] * xr[k];
+        }
+      } else {
+        const std::int8_t* B8 = reinterpret_cast<const std::int8_t*>(Bs);
+        if (a.fwd) {
+#pragma unroll 4
+          for (int k = 0; k < Q; ++k) acc += float(B8[c * Q + k]) * xr[k];
+        } else {
+#pragma unroll 4
+          for (int k = 0; k < Q; ++k) acc += float(B8[k * Q + c]) * xr[k];
+        }
+      }
+      y[e] = acc;
+    }
+    team_sync(tm);
+    cur = y;
+  }
+  fwht_rows<Q>(cur, a.P2, tm);
+  for (std::uint32_t v = tm.tid; v < chunk / 4; v += tm.n)
+    *reinterpret_cast<float4*>(a.mid + std::size_t(b) * a.n + e0 + 4 * v) = reinterpret_cast<float4*>(cur)[v];
+  team_sync(tm);  // smem reusable by the caller
+}
+
+// Pass 2 (fp32 output) on the 4-column group `cg` of vector b.  red: >= 32 floats.
+__device__ void rht_p2_body(const RhtArgs& a, std::uint32_t cg, int b, float* sm2, float* red, const Team& tm) {
+  const std::uint32_t stride = a.P2 * a.q;  // elements between consecutive a_hi
+  const std::uint32_t col = cg * 4;         // 4 adjacent columns
+  for (std::uint32_t r = tm.tid; r < a.P1; r += tm.n)
+    reinterpret_cast<float4*>(sm2)[r] =
+        __ldcg(reinterpret_cast<const float4*>(a.mid + std::size_t(b) * a.n + std::size_t(r) * stride + col));
+  team_sync(tm);
+  fwht_rows<4>(sm2, a.P1, tm);
+  const float sc = rsqrtf(float(a.n));
+  float mx = 0.f;
+  for (std::uint32_t r = tm.tid; r < a.P1; r += tm.n) {
+    const std::uint32_t i = r * stride + col;
+    float4 v = reinterpret_cast<float4*>(sm2)[r];
+    v = make_float4(v.x * sc, v.y * sc, v.z * sc, v.w * sc);
+    if (!a.fwd) v = sign4(v, (a.signs[i >> 3] >> (i & 4)) & 0xFu);
+    *reinterpret_cast<float4*>(a.out + std::size_t(b) * a.n + i) = v;
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+  if (a.fwd && a.amax_out) {
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((tm.tid & 31) == 0) red[tm.tid >> 5] = mx;
+    team_sync(tm);
+    if (tm.tid == 0) {
+      float m = 0.f;
+      for (std::uint32_t w = 0; w < (tm.n + 31) / 32; ++w) m = fmaxf(m, red[w]);
+      atomic_max_pos(a.amax_out + b, m);
+    }
+  }
+  team_sync(tm);
+}
+
+// Integer activations of the tensor-core GEMV (gemv_tc.cu): Lt = rint(t / alpha)
+// with alpha = the power of two >= |x|_2 / kLtMax (|t_i| <= |t|_2 = |x|_2, so no
+// clamping is ever active), four balanced base-128 int8 limbs per value
+// (28-bit activations), the block term q_k = floor(sum_c Lt / 8) for the side
+// MMA, and TL = sum_i Lt_i.
+constexpr int kLtMax = 266338304;  // 127 * 128^3
+
+// Balanced base-128 digits: v in [-kLtMax, kLtMax] -> l0 in [-127, 127], l1..l3 in [-64, 64].
+__device__ __forceinline__ void limbs4(int v, int (&l)[4]) {
+  l[0] = (v + (1 << 20)) >> 21;
+  int rem = v - (l[0] << 21);
+  l[1] = (rem + (1 << 13)) >> 14;
+  rem -= l[1] << 14;
+  l[2] = (rem + 64) >> 7;
+  l[3] = rem - (l[2] << 7);
+}
+
+// Pass 2 of K1, limb flavour, on the 8-column group `cg` (one codeword per a_hi
+// row) of vector b.  redl: >= 32 long longs; s_alpha: 2 floats (team-shared).
+__device__ void rht_p2_limbs_body(const RhtArgs& a, std::uint32_t cg, int b, float* sm2, long long* redl,
+                                  float* s_alpha, const Team& tm) {
+  const std::uint32_t stride = a.P2 * a.q;  // elements between consecutive a_hi
+  const std::uint32_t col = cg * 8;
+  for (std::uint32_t r = tm.tid; r < 2 * a.P1; r += tm.n)
+    reinterpret_cast<float4*>(sm2)[r] = __ldcg(reinterpret_cast<const float4*>(
+        a.mid + std::size_t(b) * a.n + std::size_t(r >> 1) * stride + col + 4 * (r & 1)));
+  if (tm.tid == 0) {
+    float ss = 0.f;
+    for (std::uint32_t j = 0; j < a.P1; ++j) ss += __ldcg(a.ssq + std::size_t(b) * a.P1 + j);
+    const float v = sqrtf(ss) * (1.0f + 1.0f / 1024.f) / float(kLtMax);
+    int e = 0;
+    if (v > 0.f) frexpf(v, &e);
+    s_alpha[0] = v > 0.f ? ldexpf(1.f, e) : 1.f;
+    s_alpha[1] = v > 0.f ? ldexpf(1.f, -e) : 1.f;
+    if (cg == 0) a.alpha_out[b] = s_alpha[0];
+  }
+  team_sync(tm);
+  fwht_rows<8>(sm2, a.P1, tm);
+  const float sc = rsqrtf(float(a.n)), inv = s_alpha[1];
+  long long tl = 0;
+  const std::uint32_t N = a.bcols;
+  for (std::uint32_t r = tm.tid; r < a.P1; r += tm.n) {
+    const std::uint32_t k = (r * stride + col) >> 3;  // codeword index
+    const float* v = sm2 + r * 8;
+    int lt[8];
+    long long S = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      float t = rintf(v[c] * sc * inv);
+      t = fminf(fmaxf(t, -float(kLtMax)), float(kLtMax));
+      lt[c] = int(t);
+      S += lt[c];
+    }
+    tl += S;
+    const int qk = int(S >> 3);  // floor(S / 8)
+    std::uint32_t w[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      int l[4];
+      limbs4(lt[c], l);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) w[i][c >> 2] |= (std::uint32_t(l[i]) & 0xFFu) << (8 * (c & 3));
+    }
+    int ql[4];
+    limbs4(qk, ql);
+    const std::uint32_t ks = k >> 5, j = k & 31, kb = j >> 2;
+    std::uint8_t* slab = a.bimg + std::size_t(ks) * a.b_bytes;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const std::uint32_t row = 4 * b + l;
+      const std::uint32_t rowoff = (row >> 3) * 256 + (row & 7) * 16;
+      // main: K-block kb, K bytes 8 (j % 4) .. +7 -> chunk (j % 4) / 2, offset 8 (j % 2)
+      *reinterpret_cast<uint2*>(slab + kb * N * 32 + rowoff + ((j & 3) >> 1) * 128 + (j & 1) * 8) =
+          make_uint2(w[l][0], w[l][1]);
+      // side: K-block 8, K byte j
+      slab[8 * N * 32 + rowoff + (j >> 4) * 128 + (j & 15)] = std::uint8_t(ql[l]);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) tl += __shfl_xor_sync(0xffffffffu, tl, o);
+  if ((tm.tid & 31) == 0) redl[tm.tid >> 5] = tl;
+  team_sync(tm);
+  if (tm.tid == 0) {
+    long long t = 0;
+    for (std::uint32_t w = 0; w < (tm.n + 31) / 32; ++w) t += redl[w];
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.tl_out + b), static_cast<unsigned long long>(t));
+  }
+  team_sync(tm);
+}
+
+// Pass 1 with the base order dispatched at run time (fused layer kernel).
+__device__ __forceinline__ void rht_p1_dispatch(const RhtArgs& a, std::uint32_t ch, int b, float* sm, float* red,
+                                                const Team& tm) {
+  switch (a.q) {
+    case 1: rht_p1_body<1>(a, ch, b, sm, red, tm); break;
+    case 4: rht_p1_body<4>(a, ch, b, sm, red, tm); break;
+    case 12: rht_p1_body<12>(a, ch, b, sm, red, tm); break;
+    case 20: rht_p1_body<20>(a, ch, b, sm, red, tm); break;
+    case 28: rht_p1_body<28>(a, ch, b, sm, red, tm); break;
+    default: rht_p1_body<172>(a, ch, b, sm, red, tm); break;
+  }
+}
+
+// Grid-wide barrier over co-resident persistent CTAs (one team per CTA takes
+// part): monotone arrival counter, barrier k waits for k * gridDim.x arrivals.
+// Generic writes before it are made visible to both proxies (the async proxy
+// reads the B images through TMA afterwards).
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target, const Team& tm) {
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+  team_sync(tm);
+  if (tm.tid == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    unsigned v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ctr) : "memory");
+      if (v >= target) break;
+      __nanosleep(64);
+    }
+    __threadfence();
+  }
+  team_sync(tm);
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+
+}  // namespace
+}  // namespace q8p::detail
