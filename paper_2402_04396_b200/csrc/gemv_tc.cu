@@ -107,6 +107,7 @@ struct TcArgs {
   const std::uint8_t* lut_img;    // 64 KiB LUT window image (tc_lut_image)
   unsigned long long* trace;      // debug timeline (Q8P_TRACE), CTA 0 only; nullptr = off
   // ---- fused layer kernel (K1 + K2 [+ K3] in one launch) ----
+  int late_prefetch;              // producer waits for the previous kernel before streaming codes
   int fuse;                       // 0: K2 only, 1: K1 + K2, 2: K1 + K2 + K3
   int batch;
   RhtArgs k1, k3;                 // pass arguments of the input / output transforms
@@ -282,6 +283,10 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
   const std::uint32_t pre = count < S ? count : S;
   if (warp == kWarpProd) {
     __syncwarp();  // lane 0 initialised the barriers
+    // Q8P_K2_LATE_PREFETCH: hold the code stream until the previous kernel (K1)
+    // is done, so K1's few dependent accesses do not queue behind ~20 MB of
+    // prefetch (the prologue still overlaps K1)
+    if (a.late_prefetch) pdl_wait();
     if (count > 0) {
       issue_code(0);  // first code slab, then the (L2-resident) LUT window
       mbar_arrive_expect_tx_e(bar_lut, 65536);
@@ -781,6 +786,11 @@ void fill_tc_args(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* za
   a.smem_bytes = std::uint32_t(kSmemBytes);
   a.lut_img = L.lut_img;
   a.batch = batch;
+  static const int late = [] {
+    const char* e = std::getenv("Q8P_K2_LATE_PREFETCH");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.late_prefetch = late;
 }
 }  // namespace
 

@@ -437,6 +437,113 @@ void launch_cluster(const RhtArgs& a, std::uint32_t C, std::uint32_t zero_rows, 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Single-CTA RHT for power-of-two n <= kSingleMaxN (q = 1): one 1024-thread CTA
+// per vector holds the whole vector in smem: load (signs | limb combine), all
+// log2(n) FWHT stages, then the limb B images (K1) or y (K3) straight from
+// smem -- one launch and one global round trip instead of two passes.
+constexpr std::uint32_t kSingleMaxN = 8192;
+enum SingleMode { kSingleK1 = 0, kSingleK3Acc = 1, kSingleK3F32 = 2 };
+
+template <int MODE>
+__global__ void __launch_bounds__(1024) rht_single(RhtArgs a) {
+  extern __shared__ __align__(16) float sx[];
+  __shared__ float red[32];
+  __shared__ long long redl[32];
+  __shared__ float s_ss;
+  const int b = blockIdx.x;
+  pdl_wait();
+  pdl_trigger();
+  if (b >= a.batch) {  // K1: zero the GEMV accumulators / ragged B-image tail
+    if constexpr (MODE == kSingleK1) {
+      const std::size_t nz = std::size_t(gridDim.x - a.batch) * blockDim.x;
+      const std::size_t t0 = std::size_t(b - a.batch) * blockDim.x + threadIdx.x;
+      if (a.zero_ptr)
+        for (std::size_t i = t0; i < a.zero_words / 4; i += nz)
+          reinterpret_cast<int4*>(a.zero_ptr)[i] = make_int4(0, 0, 0, 0);
+      if (a.zero2_ptr)
+        for (std::size_t i = t0; i < a.zero2_bytes / 16; i += nz)
+          reinterpret_cast<int4*>(a.zero2_ptr)[i] = make_int4(0, 0, 0, 0);
+    }
+    return;
+  }
+  const Team tm = block_team();
+  const std::uint32_t n = a.n;
+  float ss = 0.f;
+  for (std::uint32_t v = threadIdx.x; v < n / 4; v += blockDim.x) {
+    const std::uint32_t i = 4 * v;
+    float4 val;
+    if constexpr (MODE == kSingleK3Acc) {
+      val = combine4(a, b, i);
+    } else {
+      val = *reinterpret_cast<const float4*>(a.in + std::size_t(b) * n + i);
+      if constexpr (MODE == kSingleK1) {
+        ss += val.x * val.x + val.y * val.y + val.z * val.z + val.w * val.w;
+        val = sign4(val, (a.signs[i >> 3] >> (i & 4)) & 0xFu);
+      }
+    }
+    reinterpret_cast<float4*>(sx)[v] = val;
+  }
+  if constexpr (MODE == kSingleK1) {
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  }
+  __syncthreads();
+  if constexpr (MODE == kSingleK1) {
+    if (threadIdx.x == 0) {
+      float t = 0.f;
+      for (std::uint32_t w = 0; w < blockDim.x / 32; ++w) t += red[w];
+      s_ss = t;
+    }
+  }
+  fwht_rows<1>(sx, n, tm);  // all log2(n) stages (ends with __syncthreads)
+  const float sc = rsqrtf(float(n));
+  if constexpr (MODE == kSingleK1) {
+    const float2 al = alpha_of(s_ss);
+    if (threadIdx.x == 0) a.alpha_out[b] = al.x;
+    long long tl = 0;
+    for (std::uint32_t k = threadIdx.x; k < n / 8; k += blockDim.x) tl += emit_limbs(a, b, k, sx + 8 * k, sc, al.y);
+    for (int o = 16; o > 0; o >>= 1) tl += __shfl_xor_sync(0xffffffffu, tl, o);
+    if ((threadIdx.x & 31) == 0) redl[threadIdx.x >> 5] = tl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long t = 0;
+      for (std::uint32_t w = 0; w < blockDim.x / 32; ++w) t += redl[w];
+      a.tl_out[b] = t;
+    }
+  } else {
+    for (std::uint32_t v = threadIdx.x; v < n / 4; v += blockDim.x) {
+      const std::uint32_t i = 4 * v;
+      float4 val = reinterpret_cast<const float4*>(sx)[v];
+      val = make_float4(val.x * sc, val.y * sc, val.z * sc, val.w * sc);
+      val = sign4(val, (a.signs[i >> 3] >> (i & 4)) & 0xFu);
+      *reinterpret_cast<float4*>(a.out + std::size_t(b) * n + i) = val;
+    }
+  }
+}
+
+bool single_ok(const DevSide& side) {
+  // experiment knob (Q8P_RHT_SINGLE=1): correct, but one SM doing all log2(n)
+  // stages is issue-bound (~750 instructions per warp, ~3 us even at full issue)
+  // and slower in the pipeline than the two passes
+  static const bool on = std::getenv("Q8P_RHT_SINGLE") != nullptr;
+  return on && side.q == 1 && side.n <= kSingleMaxN && side.n % 8 == 0;
+}
+
+template <int MODE>
+void launch_single(const RhtArgs& a, std::uint32_t zero_ctas, cudaStream_t s) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cuda_check(cudaFuncSetAttribute(rht_single<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(kSingleMaxN * 4)),
+               "rht single smem attr");
+  });
+  launch_pdl(rht_single<MODE>, dim3(a.batch + zero_ctas), dim3(1024), std::size_t(a.n) * 4, s, a);
+  cuda_check(cudaGetLastError(), "rht single launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
 void plan_split_impl(const DevSide& side, RhtArgs& a) {
   a.n = side.n;
   a.p = side.p;
@@ -558,6 +665,10 @@ void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, flo
   a.out = y;
   a.batch = batch;
   a.fwd = 0;
+  if (single_ok(side)) {
+    launch_single<kSingleK3F32>(a, 0, s);
+    return;
+  }
   if (const std::uint32_t C = cluster_size_for(side)) {
     launch_cluster<kK3F32>(a, C, 0, s);
     return;
@@ -589,6 +700,10 @@ void launch_rht_in_limbs(const DevSide& side, const float* x, float* u_scratch, 
   a.zero2_bytes = tail_bytes;
   a.batch = batch;
   a.fwd = 1;
+  if (single_ok(side)) {
+    launch_single<kSingleK1>(a, (zero_ptr && zero_words) || (bimg_tail && tail_bytes) ? 16 : 0, s);
+    return;
+  }
   if (const std::uint32_t C = cluster_size_for(side)) {
     launch_cluster<kK1Limbs>(a, C, (zero_ptr && zero_words) || (bimg_tail && tail_bytes) ? 4 : 0, s);
     return;
@@ -619,6 +734,10 @@ void launch_rht_out_acc(const DevSide& side, const std::int32_t* zacc, int zacc_
   a.out = y;
   a.batch = batch;
   a.fwd = 0;
+  if (single_ok(side)) {
+    launch_single<kSingleK3Acc>(a, 0, s);
+    return;
+  }
   if (const std::uint32_t C = cluster_size_for(side)) {
     launch_cluster<kK3Acc>(a, C, 0, s);
     return;

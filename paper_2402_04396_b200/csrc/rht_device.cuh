@@ -283,6 +283,54 @@ __device__ __forceinline__ void limbs4(int v, int (&l)[4]) {
   l[3] = rem - (l[2] << 7);
 }
 
+// One codeword k of vector b (8 transformed values v): integer activations,
+// limbs into the B image, returns sum_c Lt_c (for TL).
+__device__ __forceinline__ long long emit_limbs(const RhtArgs& a, int b, std::uint32_t k, const float* v, float sc,
+                                                float inv) {
+  const std::uint32_t N = a.bcols;
+  int lt[8];
+  long long S = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    float t = rintf(v[c] * sc * inv);
+    t = fminf(fmaxf(t, -float(kLtMax)), float(kLtMax));
+    lt[c] = int(t);
+    S += lt[c];
+  }
+  const int qk = int(S >> 3);  // floor(S / 8)
+  std::uint32_t w[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    int l[4];
+    limbs4(lt[c], l);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i][c >> 2] |= (std::uint32_t(l[i]) & 0xFFu) << (8 * (c & 3));
+  }
+  int ql[4];
+  limbs4(qk, ql);
+  const std::uint32_t ks = k >> 5, j = k & 31, kb = j >> 2;
+  std::uint8_t* slab = a.bimg + std::size_t(ks) * a.b_bytes;
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const std::uint32_t row = 4 * b + l;
+    const std::uint32_t rowoff = (row >> 3) * 256 + (row & 7) * 16;
+    // main: K-block kb, K bytes 8 (j % 4) .. +7 -> chunk (j % 4) / 2, offset 8 (j % 2)
+    *reinterpret_cast<uint2*>(slab + kb * N * 32 + rowoff + ((j & 3) >> 1) * 128 + (j & 1) * 8) =
+        make_uint2(w[l][0], w[l][1]);
+    // side: K-block 8, K byte j
+    slab[8 * N * 32 + rowoff + (j >> 4) * 128 + (j & 15)] = std::uint8_t(ql[l]);
+  }
+  return S;
+}
+
+// alpha = the power of two >= |x|_2 (1 + 2^-10) / kLtMax; returns {alpha, 1/alpha}.
+__device__ __forceinline__ float2 alpha_of(float ss) {
+  const float v = sqrtf(ss) * (1.0f + 1.0f / 1024.f) / float(kLtMax);
+  int e = 0;
+  if (v > 0.f) frexpf(v, &e);
+  return v > 0.f ? make_float2(ldexpf(1.f, e), ldexpf(1.f, -e)) : make_float2(1.f, 1.f);
+}
+
 // Pass 2 of K1, limb flavour, on the 8-column group `cg` (one codeword per a_hi
 // row) of vector b.  redl: >= 32 long longs; s_alpha: 2 floats (team-shared).
 __device__ void rht_p2_limbs_body(const RhtArgs& a, std::uint32_t cg, int b, float* sm2, long long* redl,
@@ -295,55 +343,16 @@ __device__ void rht_p2_limbs_body(const RhtArgs& a, std::uint32_t cg, int b, flo
   if (tm.tid == 0) {
     float ss = 0.f;
     for (std::uint32_t j = 0; j < a.P1; ++j) ss += __ldcg(a.ssq + std::size_t(b) * a.P1 + j);
-    const float v = sqrtf(ss) * (1.0f + 1.0f / 1024.f) / float(kLtMax);
-    int e = 0;
-    if (v > 0.f) frexpf(v, &e);
-    s_alpha[0] = v > 0.f ? ldexpf(1.f, e) : 1.f;
-    s_alpha[1] = v > 0.f ? ldexpf(1.f, -e) : 1.f;
+    const float2 al = alpha_of(ss);
+    s_alpha[0] = al.x;
+    s_alpha[1] = al.y;
     if (cg == 0) a.alpha_out[b] = s_alpha[0];
   }
   team_sync(tm);
   fwht_rows<8>(sm2, a.P1, tm);
   const float sc = rsqrtf(float(a.n)), inv = s_alpha[1];
   long long tl = 0;
-  const std::uint32_t N = a.bcols;
-  for (std::uint32_t r = tm.tid; r < a.P1; r += tm.n) {
-    const std::uint32_t k = (r * stride + col) >> 3;  // codeword index
-    const float* v = sm2 + r * 8;
-    int lt[8];
-    long long S = 0;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      float t = rintf(v[c] * sc * inv);
-      t = fminf(fmaxf(t, -float(kLtMax)), float(kLtMax));
-      lt[c] = int(t);
-      S += lt[c];
-    }
-    tl += S;
-    const int qk = int(S >> 3);  // floor(S / 8)
-    std::uint32_t w[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      int l[4];
-      limbs4(lt[c], l);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) w[i][c >> 2] |= (std::uint32_t(l[i]) & 0xFFu) << (8 * (c & 3));
-    }
-    int ql[4];
-    limbs4(qk, ql);
-    const std::uint32_t ks = k >> 5, j = k & 31, kb = j >> 2;
-    std::uint8_t* slab = a.bimg + std::size_t(ks) * a.b_bytes;
-#pragma unroll
-    for (int l = 0; l < 4; ++l) {
-      const std::uint32_t row = 4 * b + l;
-      const std::uint32_t rowoff = (row >> 3) * 256 + (row & 7) * 16;
-      // main: K-block kb, K bytes 8 (j % 4) .. +7 -> chunk (j % 4) / 2, offset 8 (j % 2)
-      *reinterpret_cast<uint2*>(slab + kb * N * 32 + rowoff + ((j & 3) >> 1) * 128 + (j & 1) * 8) =
-          make_uint2(w[l][0], w[l][1]);
-      // side: K-block 8, K byte j
-      slab[8 * N * 32 + rowoff + (j >> 4) * 128 + (j & 15)] = std::uint8_t(ql[l]);
-    }
-  }
+  for (std::uint32_t r = tm.tid; r < a.P1; r += tm.n) tl += emit_limbs(a, b, (r * stride + col) >> 3, sm2 + r * 8, sc, inv);
   for (int o = 16; o > 0; o >>= 1) tl += __shfl_xor_sync(0xffffffffu, tl, o);
   if ((tm.tid & 31) == 0) redl[tm.tid >> 5] = tl;
   team_sync(tm);
