@@ -70,6 +70,12 @@ constexpr std::uint32_t kE81Slab = 2 * 2048;
 constexpr std::uint32_t kAcols = 72;        // TMEM columns per A buffer (64 main + 8 side)
 constexpr int kWarpProd = 0, kWarpMma = 1;  // warps 1..G: one MMA issuer per decode group; then 4G decoder warps
 constexpr int kMaxStages = 32;
+#ifndef Q8P_K2_CPASYNC
+#define Q8P_K2_CPASYNC 0  // 1: code ring filled by 2 producer warps with 16-B cp.async (LDGSTS)
+                          // instead of 1-D bulk copies from one warp.  Faster in the streaming
+                          // ubench (5.9 vs 5.2 TB/s) but slower in K2 (25.3 vs 21.3 us, the
+                          // LDGSTS compete with the decoders' shared-memory pipe).
+#endif
 #ifndef Q8P_K2_TEAMS
 #define Q8P_K2_TEAMS 1  // decoder teams per group at batch <= 2 (2: +3% K2, but the register
                          // file then leaves no room to co-reside with K1 under PDL)
@@ -86,7 +92,8 @@ constexpr std::size_t kSmemBytes = Q8P_K2_SMEM_KB * 1024;
 template <int G, int T = 1>
 struct Roles {
   static constexpr int kWarpDec = 1 + G;
-  static constexpr int kThreads = (kWarpDec + 4 * G * T) * 32;
+  static constexpr int kWarpProd2 = kWarpDec + 4 * G * T;  // second code producer (cp.async mode)
+  static constexpr int kThreads = (kWarpDec + 4 * G * T + (Q8P_K2_CPASYNC ? 1 : 0)) * 32;
   template <int N>
   static constexpr std::uint32_t kBg = N <= 8 ? 3 : (N <= 16 ? 2 : 1);  // B-image ring slots per group
 };
@@ -249,7 +256,7 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
 #endif
   if (threadIdx.x == 0) {
     for (std::uint32_t i = 0; i < S; ++i) {
-      mbar_init(bar_full_c + 8 * i, 1);
+      mbar_init(bar_full_c + 8 * i, Q8P_K2_CPASYNC ? 32 : 1);  // cp.async: one warp's noinc arrivals
       mbar_init(bar_empty_c + 8 * i, 4);
     }
     for (std::uint32_t i = 0; i < SB; ++i) {
@@ -266,20 +273,28 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
     fence_mbar_init();
     asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n" ::"r"(ct_slot), "r"(kCtLo), "r"(kCtHi) : "memory");
   }
-  // Code producer state; the first S code slabs (and the LUT window) are issued
-  // before the TMEM allocation and the CTA barrier, so HBM latency overlaps setup.
+  // Code producers.  Item i goes to ring slot i % S (phase i / S).  Bulk mode: warp 0
+  // issues every slab as one 1-D cp.async.bulk; cp.async mode: warps 0 and
+  // kWarpProd2 take alternate items, each lane moving 16 B per LDGSTS, completion
+  // via cp.async.mbarrier.arrive.noinc.  The first S slabs (and the LUT window)
+  // of warp 0 are issued before the TMEM allocation and the CTA barrier.
   const std::uint64_t pol = policy_evict_first();
-  std::uint32_t ps = it0 % nst, pu = it0 / nst;  // next item -> (u = row block * KSL + k slab, stage)
-  auto issue_code = [&](std::uint32_t st) {
-    const std::uint32_t sb = ps ? a.slab_bytes[1] : a.slab_bytes[0];
+  auto issue_item = [&](std::uint32_t i) {
+    const std::uint32_t it = it0 + i, u = it / nst, sidx = it - u * nst, st = i % S;
+    const std::uint32_t sb = sidx ? a.slab_bytes[1] : a.slab_bytes[0];
+    const std::uint8_t* src = (sidx ? a.codes[1] : a.codes[0]) + std::size_t(u) * sb;
+#if Q8P_K2_CPASYNC
+    const std::uint32_t dst = code_addr(st);
+    for (std::uint32_t o = std::uint32_t(lane) * 16u; o < sb; o += 512u)
+      // (the .L2::cache_hint form with the evict-first policy faults at run time on sm_100a)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + o), "l"(src + o) : "memory");
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar_full_c + 8 * st) : "memory");
+#else
     mbar_arrive_expect_tx_e(bar_full_c + 8 * st, sb);
-    bulk_g2s_hint_e(code_addr(st), (ps ? a.codes[1] : a.codes[0]) + std::size_t(pu) * sb, sb, bar_full_c + 8 * st,
-                    pol);
-    if (++ps == nst) {
-      ps = 0;
-      ++pu;
-    }
+    bulk_g2s_hint_e(code_addr(st), src, sb, bar_full_c + 8 * st, pol);
+#endif
   };
+  constexpr std::uint32_t NP = Q8P_K2_CPASYNC ? 2u : 1u;
   const std::uint32_t pre = count < S ? count : S;
   if (warp == kWarpProd) {
     __syncwarp();  // lane 0 initialised the barriers
@@ -288,10 +303,10 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
     // prefetch (the prologue still overlaps K1)
     if (a.late_prefetch) pdl_wait();
     if (count > 0) {
-      issue_code(0);  // first code slab, then the (L2-resident) LUT window
+      issue_item(0);  // first code slab, then the (L2-resident) LUT window
       mbar_arrive_expect_tx_e(bar_lut, 65536);
       bulk_g2s_e(lutw, a.lut_img, 65536, bar_lut);
-      for (std::uint32_t i = 1; i < pre; ++i) issue_code(i);
+      for (std::uint32_t i = NP; i < pre; i += NP) issue_item(i);
     }
     tmem_alloc<512>(tmem_slot);
   }
@@ -308,7 +323,9 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
   __shared__ float s_red[32];
   __shared__ long long s_redl[32];
   __shared__ float s_alpha[2];
-  const Team tm{threadIdx.x - 32u, std::uint32_t(Roles<G, T>::kThreads - 32), 1u};
+  // team: MMA issuers + decoders (not the code producers)
+  const Team tm{threadIdx.x - 32u, std::uint32_t(Roles<G, T>::kWarpProd2 - 1) * 32u, 1u};
+  const bool in_team = warp != kWarpProd && warp < Roles<G, T>::kWarpProd2;
   auto tm_tid0 = [&]() { return threadIdx.x == 32; };
   (void)tm_tid0;
 #ifdef Q8P_K2_TRACE
@@ -324,7 +341,7 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
 #endif
   float* const scr = reinterpret_cast<float*>(smem + (a.smem_bytes - a.scratch_bytes));
   if constexpr (FUSED) {
-    if (warp != kWarpProd) {
+    if (in_team) {
       pstamp(0);
       pdl_wait();  // x (and our workspace) are the previous kernel's
       pstamp(1);
@@ -353,21 +370,23 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
   }
 
   if (warp == kWarpProd) {
-    // ===== code producer (whole warp, lane-elected issue); codes do not depend on K1 =====
-    if (count > 0) {
-      std::uint32_t st = pre == S ? 0 : pre, r = 1;
-      for (std::uint32_t i = pre; i < count; ++i) {
-        tstamp(a, 9, i, 0);
-        mbar_wait(bar_empty_c + 8 * st, (r & 1) ^ 1);
-        tstamp(a, 9, i, 1);
-        issue_code(st);
-        if (++st == S) {
-          st = 0;
-          ++r;
-        }
-      }
+    // ===== code producer 0 (codes do not depend on K1) =====
+    for (std::uint32_t i = pre + ((NP - pre % NP) % NP); i < count; i += NP) {
+      tstamp(a, 9, i, 0);
+      mbar_wait(bar_empty_c + 8 * (i % S), ((i / S) & 1) ^ 1);
+      tstamp(a, 9, i, 1);
+      issue_item(i);
     }
     pdl_trigger();
+#if Q8P_K2_CPASYNC
+  } else if (warp == Roles<G, T>::kWarpProd2) {
+    // ===== code producer 1: odd items =====
+    for (std::uint32_t i = 1; i < count; i += 2) {
+      if (i >= S) mbar_wait(bar_empty_c + 8 * (i % S), ((i / S) & 1) ^ 1);
+      issue_item(i);
+    }
+    pdl_trigger();
+#endif
   } else if (warp < kWarpDec) {
     // ===== MMA issuer of group g (+ its B-image prefetch): items i = g, g + G, ... =====
     // One issuer per group keeps each accumulator's MMAs on one thread (in-order
@@ -613,7 +632,7 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
     }
   }
   if constexpr (FUSED) {
-    if (warp != kWarpProd) {
+    if (in_team) {
       if (a.fuse == 2) {  // K3 on the full z once every CTA's accumulators are in
         team_sync(tm);
         pstamp(6);
