@@ -76,6 +76,9 @@ constexpr int kMaxStages = 32;
                           // ubench (5.9 vs 5.2 TB/s) but slower in K2 (25.3 vs 21.3 us, the
                           // LDGSTS compete with the decoders' shared-memory pipe).
 #endif
+#ifndef Q8P_K2_N8_G2NB3
+#define Q8P_K2_N8_G2NB3 0  // batch <= 2: 2 groups x 3 A buffers instead of 3 groups x 2
+#endif
 #ifndef Q8P_K2_TEAMS
 #define Q8P_K2_TEAMS 1  // decoder teams per group at batch <= 2 (2: +3% K2, but the register
                          // file then leaves no room to co-reside with K1 under PDL)
@@ -206,7 +209,7 @@ __device__ __forceinline__ void e8p_fin(std::uint32_t nib, std::uint32_t fl, std
   hi = prmt(ct_lo, ct_hi, __umulhi(sel, 65536u));  // sel >> 16
 }
 
-template <int N, int G, int T, bool FUSED>
+template <int N, int G, int T, bool FUSED, int NB>
 __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArgs a) {
   extern __shared__ __align__(1024) std::uint8_t smem[];
   // warp index via shfl: the compiler then knows every role branch is warp-uniform
@@ -220,8 +223,8 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
   const std::uint32_t bar_full_b = sbase + 16 * kMaxStages;     // [kMaxB] B image landed
   const std::uint32_t bar_empty_b = bar_full_b + 8 * kMaxB;     // [kMaxB] B image read by its MMAs
   const std::uint32_t bar_a_empty = bar_empty_b + 8 * kMaxB;    // [G][2] A buffer read by its MMAs
-  const std::uint32_t bar_a_full = bar_a_empty + 8 * 2 * G;     // [G][2] A buffer written (4 warp arrivals)
-  const std::uint32_t bar_d_full = bar_a_full + 8 * 2 * G;      // [G][T] accumulator final (team t's epilogue)
+  const std::uint32_t bar_a_full = bar_a_empty + 8 * NB * G;    // [G][NB] A buffer written (4 warp arrivals)
+  const std::uint32_t bar_d_full = bar_a_full + 8 * NB * G;     // [G][T] accumulator final (team t's epilogue)
   const std::uint32_t bar_d_empty = bar_d_full + 8 * G * T;     // [G] accumulator read out (4 warp arrivals)
   const std::uint32_t bar_lut = bar_d_empty + 8 * G;            // LUT window landed
   const std::uint32_t tmem_slot = bar_lut + 8;
@@ -263,7 +266,7 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
       mbar_init(bar_full_b + 8 * i, 1);
       mbar_init(bar_empty_b + 8 * i, 1);
     }
-    for (int i = 0; i < 2 * G; ++i) {
+    for (int i = 0; i < NB * G; ++i) {
       mbar_init(bar_a_empty + 8 * i, 1);
       mbar_init(bar_a_full + 8 * i, 4);
     }
@@ -421,16 +424,20 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
       std::uint32_t j = (it0 + g) % per_rb;
       std::uint32_t buf = 0, bph = 0, started = 0, seg = 0, team = 0;
       std::uint32_t bslot = 0, bphase = 0, rslot = 0, rphase = 0;
-      const std::uint32_t dcol_g = tbase + std::uint32_t(G) * 2 * kAcols + g * nst * N;
-      const std::uint32_t acol0 = tbase + 2 * g * kAcols;
-      const std::uint32_t af0 = bar_a_full + 16 * g, ae0 = bar_a_empty + 16 * g;
+      const std::uint32_t dcol_g = tbase + std::uint32_t(G) * NB * kAcols + g * nst * N;
+      const std::uint32_t acol0 = tbase + NB * g * kAcols;
+      const std::uint32_t af0 = bar_a_full + 8 * NB * g, ae0 = bar_a_empty + 8 * NB * g;
       for (std::uint32_t k = 0, i = g; k < n_g; ++k, i += G) {
         const std::uint32_t s = j & (nst - 1);
         tstamp(a, 8 + (g == 0 ? 0 : 4 + g), k, 0);
         // first MMA of a new row block overwrites D: the previous epilogue must have read it
         if (started == 0 && seg > 0) mbar_wait(bar_d_empty + 8 * g, (seg - 1) & 1);
         mbar_wait(af0 + 8 * buf, bph);
+        tstamp(a, 8 + (g == 0 ? 0 : 4 + g), k, 1);
         mbar_wait(fb + 8 * bslot, bphase);
+#ifndef Q8P_K2_TRACE_SYNC
+        tstamp(a, 8 + (g == 0 ? 0 : 4 + g), k, 2);
+#endif
         tc_fence_after();
 #ifdef Q8P_EXP_NO_MMA
         mma_commit_e(ae0 + 8 * buf);
@@ -457,8 +464,7 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
           if (++rslot == SBg) rslot = 0, rphase ^= 1;
         }
         if (++bslot == SBg) bslot = 0, bphase ^= 1;
-        buf ^= 1;
-        if (buf == 0) bph ^= 1;
+        if (++buf == NB) buf = 0, bph ^= 1;
         if (++team == T) team = 0;
         j += G;
         while (j >= per_rb) j -= per_rb;
@@ -473,7 +479,7 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
     const std::uint32_t tl = (q * 32) << 16;
     const std::uint32_t lb = (lutw & 0xFFFF0000u) | (std::uint32_t(lane) * 4u);
     const std::uint32_t lb8 = (lutw & 0xFFFF0000u) | (128u + std::uint32_t(lane & 15) * 8u);
-    const std::uint32_t dcol = tbase + std::uint32_t(G) * 2 * kAcols + std::uint32_t(grp) * nst * N;
+    const std::uint32_t dcol = tbase + std::uint32_t(G) * NB * kAcols + std::uint32_t(grp) * nst * N;
     const std::uint32_t per_rb = a.KSL * nst;
     const std::uint32_t i_first = std::uint32_t(grp + G * tm);
     std::uint32_t st = i_first % S, r = i_first / S, use = std::uint32_t(tm), seg = 0, started = 0;
@@ -493,14 +499,14 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
 #endif
     for (std::uint32_t i = i_first; i < count; i += G * T) {
       const std::uint32_t s = j & (nst - 1);  // nst in {1, 2}
-      const std::uint32_t buf = use & 1, bph = (use >> 1) & 1;
+      const std::uint32_t buf = use % NB, bph = (use / NB) & 1;
       const std::uint32_t sa = code_addr(st);
       const bool e8p = (s ? a.kind[1] : a.kind[0]) == 0;
       const bool tw = q == 1;
       if (tw) tstamp(a, grp, i, 0);
       mbar_wait(bar_full_c + 8 * st, r & 1);
       if (tw) tstamp(a, grp, i, 1);
-      const std::uint32_t abuf = tbase + tl + (2 * grp + buf) * kAcols;
+      const std::uint32_t abuf = tbase + tl + (NB * grp + buf) * kAcols;
       if (e8p) {
         const uint4 i0 = lds128(sa + row_in * 16), i1 = lds128(sa + 2048 + row_in * 16);
         const uint4 f0 = lds128(sa + 4096 + row_in * 16), f1 = lds128(sa + 6144 + row_in * 16);
@@ -518,7 +524,7 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
           nib[4 * g4 + 2] = e8p_nib<2>(idx[g4], lb);
           nib[4 * g4 + 3] = e8p_nib<3>(idx[g4], lb);
         }
-        mbar_wait(bar_a_empty + 8 * (2 * grp + buf), bph ^ 1);
+        mbar_wait(bar_a_empty + 8 * (NB * grp + buf), bph ^ 1);
         if (tw) tstamp(a, grp, i, 2);
         tc_fence_after();
 #pragma unroll
@@ -557,7 +563,7 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
         const std::uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_empty_c + 8 * st);
-        mbar_wait(bar_a_empty + 8 * (2 * grp + buf), bph ^ 1);
+        mbar_wait(bar_a_empty + 8 * (NB * grp + buf), bph ^ 1);
         tc_fence_after();
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) {
@@ -580,7 +586,7 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar_a_full + 8 * (2 * grp + buf));
+      if (lane == 0) mbar_arrive(bar_a_full + 8 * (NB * grp + buf));
       if (tw) tstamp(a, grp, i, 3);
       if ((j + G >= per_rb) || (i + G >= count)) {
         // epilogue of this row block: D (int32, exact) -> global accumulators.
@@ -675,14 +681,14 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
 
 constexpr std::size_t kSmemFused = 225 * 1024;  // fused layer kernel: nothing else to co-reside with
 
-template <int N, int G, int T, bool FUSED>
+template <int N, int G, int T, bool FUSED, int NB>
 void set_attr() {
   static std::once_flag once;
   std::call_once(once, [] {
-    cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G, T, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G, T, FUSED, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(FUSED ? kSmemFused : kSmemBytes)),
                "tc smem attr");
-    cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G, T, FUSED>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G, T, FUSED, NB>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                     100),
                "carveout");
   });
@@ -698,10 +704,10 @@ int sm_count() {
   return v;
 }
 
-template <int N, int G, int T = 1, bool FUSED = false>
+template <int N, int G, int T = 1, bool FUSED = false, int NB = 2>
 void launch_ng(const TcArgs& a, cudaStream_t s) {
-  set_attr<N, G, T, FUSED>();
-  launch_pdl(gemv_tc_kernel<N, G, T, FUSED>, dim3(sm_count()), dim3(Roles<G, T>::kThreads),
+  set_attr<N, G, T, FUSED, NB>();
+  launch_pdl(gemv_tc_kernel<N, G, T, FUSED, NB>, dim3(sm_count()), dim3(Roles<G, T>::kThreads),
              FUSED ? kSmemFused : kSmemBytes, s, a);
 }
 
@@ -828,7 +834,12 @@ void launch_gemv_tc(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* 
   // TMEM: G decode groups x (2 A buffers x 72 columns + an accumulator of stages x N) <= 512
   auto fits = [&](int G) { return G * (2 * int(kAcols) + a.nst * N) <= 512; };
   switch (N) {
-    case 8: launch_ng<8, 3, Q8P_K2_TEAMS, false>(a, s); break;
+    case 8:
+      if (Q8P_K2_N8_G2NB3)
+        launch_ng<8, 2, 1, false, 3>(a, s);
+      else
+        launch_ng<8, 3, Q8P_K2_TEAMS, false, 2>(a, s);
+      break;
     case 16: fits(3) ? launch_ng<16, 3>(a, s) : launch_ng<16, 2>(a, s); break;
     case 32: launch_ng<32, 2>(a, s); break;
     case 48: launch_ng<48, 2>(a, s); break;

@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(128 + 32 * STW, 1) k_mma(int groups, int per_g
 }
 
 // NI issuer warps, each issuing groups of 9 MMAs (N=8) into its own D with its own A columns.
-template <int NI, int FENCE, int STW = 0, int SLEEP = 0>
+template <int NI, int FENCE, int STW = 0, int SLEEP = 0, int LDSW = 0>
 __global__ void __launch_bounds__(512, 1) k_multi(int groups, unsigned long long* out) {
   extern __shared__ __align__(1024) std::uint8_t smem[];
   const std::uint32_t sb = smem_u32(smem);
@@ -119,6 +119,20 @@ __global__ void __launch_bounds__(512, 1) k_multi(int groups, unsigned long long
   __shared__ int stop2;
   if (threadIdx.x == 0) stop2 = 0;
   __syncthreads();
+  if (LDSW && warp >= 4 && warp < 4 + LDSW) {  // LUT-style LDS traffic (lane-replicated rows)
+    std::uint32_t acc = threadIdx.x, x = threadIdx.x * 2654435761u;
+    const std::uint32_t lut = sb + 1024 + 8192;
+    while (*reinterpret_cast<volatile int*>(&stop2) == 0) {
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        x = x * 1664525u + 1013904223u;
+        std::uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(lut + ((x >> 24) & 63) * 256 + (threadIdx.x & 31) * 4));
+        acc += v;
+      }
+    }
+    if (acc == 0x12345679u) out[9] = acc;
+  }
   if (warp >= 4 && warp < 4 + STW) {
     std::uint32_t v[16];
     for (int i = 0; i < 16; ++i) v[i] = threadIdx.x * i;
@@ -162,18 +176,18 @@ __global__ void __launch_bounds__(512, 1) k_multi(int groups, unsigned long long
   }
 }
 
-template <int NI, int FENCE = 0, int STW = 0, int SLEEP = 0>
+template <int NI, int FENCE = 0, int STW = 0, int SLEEP = 0, int LDSW = 0>
 void run_multi(unsigned long long* d) {
   const int groups = 2000;
-  cudaFuncSetAttribute(k_multi<NI, FENCE, STW, SLEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 1024);
-  k_multi<NI, FENCE, STW, SLEEP><<<148, 128 + 32 * STW, 32 * 1024>>>(groups, d);
+  cudaFuncSetAttribute(k_multi<NI, FENCE, STW, SLEEP, LDSW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 1024);
+  k_multi<NI, FENCE, STW, SLEEP, LDSW><<<148, 128 + 32 * (STW > LDSW ? STW : LDSW), 32 * 1024>>>(groups, d);
   cudaDeviceSynchronize();
   unsigned long long c[4] = {0, 0, 0, 0};
   cudaMemcpy(c, d, 8 * NI, cudaMemcpyDeviceToHost);
   unsigned long long mx = 0;
   for (int i = 0; i < NI; ++i) mx = c[i] > mx ? c[i] : mx;
   unsigned long long sb8 = 0; cudaMemcpy(&sb8, d + 8, 8, cudaMemcpyDeviceToHost);
-  printf("multi-issuer fence=%d NI=%d stw=%d sleep=%d (sttm %.0f B/kcyc/warp): %.1f cyc per 9-MMA group per issuer, %.1f cyc per MMA aggregate (err=%s)\n", FENCE, NI, STW, SLEEP, double(sb8),
+  printf("multi-issuer ldsw=%d fence=%d NI=%d stw=%d sleep=%d (sttm %.0f B/kcyc/warp): %.1f cyc per 9-MMA group per issuer, %.1f cyc per MMA aggregate (err=%s)\n", LDSW, FENCE, NI, STW, SLEEP, double(sb8),
          double(mx) / groups, double(mx) / (groups * 9.0 * NI), cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -232,10 +246,8 @@ int main() {
   run<8, true, 1, true>(d);
   cudaMemset(d, 0, 64 * 8);
   run_multi<3>(d);
-  run_multi<3, 0, 12, 0>(d);
-  run_multi<3, 0, 12, 500>(d);
-  run_multi<3, 0, 12, 1000>(d);
-  run_multi<3, 0, 4, 0>(d);
+  run_multi<3, 0, 0, 0, 4>(d);
+  run_multi<3, 0, 0, 0, 12>(d);
   k_sttm<<<148, 128>>>(4000, d);
   cudaDeviceSynchronize();
   unsigned long long c;
