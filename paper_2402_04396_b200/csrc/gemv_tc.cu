@@ -9,11 +9,12 @@
 // d in {1,3,5} (256-row pattern table), sigma the coordinate signs (coordinate
 // 0 parity-inferred, e8p.cpp:97-98) and b the shift bit.  With the
 // activations as integers, t = alpha * Lt (K1; Lt = sum_l 128^(3-l) limb_l,
-// 4 int8 limbs), and q_k = floor(sum_c Lt_{8k+c} / 8):
-//     z = alpha * ( Z / 2 - TL / 4 ),   Z = sum (sigma d) Lt + sum_k 8 b_k q_k
+// 25-bit values in 4 int8 limbs) and the block sums S_k = sum_c Lt_{8k+c} (exact in
+// 4 limbs):
+//     z = alpha * ( Z / 2 - TL / 4 ),   Z = sum (sigma d) Lt + sum_k b_k S_k
 // TL = sum_i Lt_i (exact, K1).  Z is what the tensor cores accumulate:
 //   main MMAs  A = sigma_c d_c  (s8, from TMEM)   B = limb rows of Lt  (smem)
-//   side MMA   A = 8 b_k        (s8, from TMEM)   B = limb rows of q_k (smem)
+//   side MMA   A = b_k          (s8, from TMEM)   B = limb rows of S_k (smem)
 // e8-1bit stages: A = doubled table row, no side term, z = alpha Z / 2.
 // Every product is exact int32; segments combine with integer atomics, so the
 // result is deterministic and independent of the CTA count.
@@ -549,14 +550,14 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
 #endif
         }
         std::uint32_t sd[8];
-        sd[0] = (sw << 3) & 0x08080808u;
-        sd[1] = (sw << 2) & 0x08080808u;
-        sd[2] = (sw << 1) & 0x08080808u;
-        sd[3] = sw & 0x08080808u;
-        sd[4] = (sw >> 1) & 0x08080808u;
-        sd[5] = (sw >> 2) & 0x08080808u;
-        sd[6] = (sw >> 3) & 0x08080808u;
-        sd[7] = (sw >> 4) & 0x08080808u;
+        sd[0] = sw & 0x01010101u;  // side A = b_k (0/1): the side B rows are the exact S_k
+        sd[1] = (sw >> 1) & 0x01010101u;
+        sd[2] = (sw >> 2) & 0x01010101u;
+        sd[3] = (sw >> 3) & 0x01010101u;
+        sd[4] = (sw >> 4) & 0x01010101u;
+        sd[5] = (sw >> 5) & 0x01010101u;
+        sd[6] = (sw >> 6) & 0x01010101u;
+        sd[7] = (sw >> 7) & 0x01010101u;
         tmem_st8(abuf + 64, sd);
       } else {
         const uint4 c0 = lds128(sa + row_in * 16), c1 = lds128(sa + 2048 + row_in * 16);

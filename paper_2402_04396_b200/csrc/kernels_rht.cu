@@ -96,9 +96,9 @@ __global__ void __launch_bounds__(128) rht_pass2(RhtArgs a) {
 // Each CTA owns 8 adjacent flat columns = one codeword per a_hi row: FWHT over
 // a_hi, 1/sqrt(n), then the integer activations of the tensor-core GEMV
 // (gemv_tc.cu): Lt = rint(t / alpha) with alpha = the power of two >=
-// |x|_2 / kLtMax (|t_i| <= |t|_2 = |x|_2, so no clamping is ever active),
-// four balanced base-128 int8 limbs per value (28-bit activations), the block term
-// q_k = floor(sum_c Lt / 8) for the side MMA, and TL = sum_i Lt_i.
+// |x|_2 / kActMax (|t_i| <= |t|_2 = |x|_2, so no clamping is ever active),
+// four balanced base-128 int8 limbs per value (25-bit activations), the exact
+// block sums S_k = sum_c Lt for the side MMA, and TL = sum_i Lt_i.
 __global__ void __launch_bounds__(128) rht_pass2_limbs(RhtArgs a) {
   extern __shared__ __align__(16) float sm2[];
   __shared__ long long redl[32];
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kClThreads) rht_cluster(RhtArgs a, std::uint32
     } else {
       ssum = s_ss;
     }
-    const float vv = sqrtf(ssum) * (1.0f + 1.0f / 1024.f) / float(kLtMax);
+    const float vv = sqrtf(ssum) * (1.0f + 1.0f / 1024.f) / float(kActMax);
     int ex = 0;
     if (vv > 0.f) frexpf(vv, &ex);
     const float alpha = vv > 0.f ? ldexpf(1.f, ex) : 1.f, inv = vv > 0.f ? ldexpf(1.f, -ex) : 1.f;
@@ -305,12 +305,12 @@ __global__ void __launch_bounds__(kClThreads) rht_cluster(RhtArgs a, std::uint32
 #pragma unroll
       for (int cc = 0; cc < 8; ++cc) {
         float tt = rintf(v[cc] * sc * inv);
-        tt = fminf(fmaxf(tt, -float(kLtMax)), float(kLtMax));
+        tt = fminf(fmaxf(tt, -float(kActMax)), float(kActMax));
         lt[cc] = int(tt);
         S += lt[cc];
       }
       tl += S;
-      const int qk = int(S >> 3);  // floor(S / 8)
+      const int qk = int(S);  // exact block sum
       std::uint32_t wv[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
 #pragma unroll
       for (int cc = 0; cc < 8; ++cc) {

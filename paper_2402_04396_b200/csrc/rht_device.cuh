@@ -267,11 +267,15 @@ __device__ void rht_p2_body(const RhtArgs& a, std::uint32_t cg, int b, float* sm
 }
 
 // Integer activations of the tensor-core GEMV (gemv_tc.cu): Lt = rint(t / alpha)
-// with alpha = the power of two >= |x|_2 / kLtMax (|t_i| <= |t|_2 = |x|_2, so no
-// clamping is ever active), four balanced base-128 int8 limbs per value
-// (28-bit activations), the block term q_k = floor(sum_c Lt / 8) for the side
-// MMA, and TL = sum_i Lt_i.
-constexpr int kLtMax = 266338304;  // 127 * 128^3
+// with alpha = the power of two >= |x|_2 / kActMax (|t_i| <= |t|_2 = |x|_2, so no
+// clamping is ever active), four balanced base-128 int8 limbs per value, the
+// block sums S_k = sum_c Lt_{8k+c} for the side MMA, and TL = sum_i Lt_i.
+constexpr int kLtMax = 266338304;  // 127 * 128^3: range of 4 balanced base-128 int8 limbs
+// Activations are 25-bit (|Lt| <= kActMax) so the block sums S_k = sum_c Lt_{8k+c}
+// of the side MMA also fit 4 limbs exactly (|S_k| <= 8 kActMax <= kLtMax): the
+// shift term sum_k b_k S_k is then exact.  (A q_k = floor(S_k / 8) side operand
+// drops sum_k b_k (S_k mod 8) -- a per-row bias that accumulates in y_0 = sum z / sqrt(m).)
+constexpr int kActMax = kLtMax / 8;
 
 // Balanced base-128 digits: v in [-kLtMax, kLtMax] -> l0 in [-127, 127], l1..l3 in [-64, 64].
 __device__ __forceinline__ void limbs4(int v, int (&l)[4]) {
@@ -293,11 +297,11 @@ __device__ __forceinline__ long long emit_limbs(const RhtArgs& a, int b, std::ui
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     float t = rintf(v[c] * sc * inv);
-    t = fminf(fmaxf(t, -float(kLtMax)), float(kLtMax));
+    t = fminf(fmaxf(t, -float(kActMax)), float(kActMax));
     lt[c] = int(t);
     S += lt[c];
   }
-  const int qk = int(S >> 3);  // floor(S / 8)
+  const int qk = int(S);  // exact block sum (|S| <= kLtMax)
   std::uint32_t w[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
@@ -323,9 +327,9 @@ __device__ __forceinline__ long long emit_limbs(const RhtArgs& a, int b, std::ui
   return S;
 }
 
-// alpha = the power of two >= |x|_2 (1 + 2^-10) / kLtMax; returns {alpha, 1/alpha}.
+// alpha = the power of two >= |x|_2 (1 + 2^-10) / kActMax; returns {alpha, 1/alpha}.
 __device__ __forceinline__ float2 alpha_of(float ss) {
-  const float v = sqrtf(ss) * (1.0f + 1.0f / 1024.f) / float(kLtMax);
+  const float v = sqrtf(ss) * (1.0f + 1.0f / 1024.f) / float(kActMax);
   int e = 0;
   if (v > 0.f) frexpf(v, &e);
   return v > 0.f ? make_float2(ldexpf(1.f, e), ldexpf(1.f, -e)) : make_float2(1.f, 1.f);

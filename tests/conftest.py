@@ -63,3 +63,24 @@ def rel_err(a, b) -> float:
     a = np.asarray(a, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def random_artifact(m, n, stages, seed, codes=None):
+    """A structurally valid QSHP artifact with random codes (acceptance.cpp:438-450 style)."""
+    import struct
+    rng = np.random.default_rng(seed)
+    body = b"QSHP" + struct.pack("<HIIBB", 1, m, n, 0, len(stages))
+    for cid, scale in stages:
+        body += bytes([len(cid)]) + cid.encode() + struct.pack("<f", scale)
+    body += rng.integers(0, 256, (m + 7) // 8, dtype=np.uint8).tobytes()
+    body += rng.integers(0, 256, (n + 7) // 8, dtype=np.uint8).tobytes()
+    words = m * n // 8
+    for s, (cid, _) in enumerate(stages):
+        if codes is not None and codes[s] is not None:
+            c = codes[s]
+        elif cid == "e8p-2bit":
+            c = rng.integers(0, 65536, words, dtype=np.uint16)
+        else:
+            c = rng.integers(0, 256, words, dtype=np.uint8)
+        body += np.ascontiguousarray(c).tobytes()
+    return body

@@ -1,0 +1,61 @@
+"""GPU parity across the batch sizes and shapes of BASELINE.json's configs:
+every tensor-core variant (N = 8/16/32/48/64 columns of activation limbs,
+1- and 2-stage codebooks, 2/3 decode groups) and the portable path beyond
+batch 16, against the CPU oracle (oracle/latq_oracle.c restating
+core/src/pipeline.cpp:151-197), plus the 70B-shaped layers at batch 1."""
+import numpy as np
+import pytest
+
+import paper_2402_04396_b200 as q8p
+from conftest import random_artifact, rel_err
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TC = 1e-5    # tensor-core path: 25-bit integer activations (see test_gpu_parity.py)
+TOL = 1e-3   # portable fp32 path / north-star bar
+
+STAGES = {2: [("e8p-2bit", 1.11)], 3: [("e8p-2bit", 1.02), ("e8-1bit", 0.49)],
+          4: [("e8p-2bit", 0.97), ("e8p-2bit", 0.29)]}
+
+
+@pytest.fixture(scope="module")
+def dev():
+    assert torch.cuda.is_available(), "gpu tests need a B200"
+    return torch.device("cuda:0")
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4])
+@pytest.mark.parametrize("batch", [1, 2, 3, 4, 8, 13, 16, 17])
+def test_batches_vs_oracle(dev, oracle, bits, batch):
+    m, n = 1024, 2048
+    art = random_artifact(m, n, STAGES[bits], 100 * bits + batch)
+    L = q8p.Layer.from_qshp(art)
+    x = np.random.default_rng(batch).standard_normal((batch, n)).astype(np.float32).astype(np.float64)
+    want = oracle.infer(art, x, threads=8)
+    got = L.forward(torch.from_numpy(x.astype(np.float32)).to(dev)).cpu().numpy()
+    bar = TC if batch <= 16 else TOL
+    for b in range(batch):
+        assert rel_err(got[b], want[b]) < bar, (b, rel_err(got[b], want[b]))
+
+
+@pytest.mark.parametrize("m,n", [(8192, 8192), (28672, 8192), (8192, 28672)])
+def test_70b_shapes_vs_oracle(dev, oracle, m, n):
+    art = random_artifact(m, n, STAGES[2], m ^ n)
+    L = q8p.Layer.from_qshp(art)
+    x = np.random.default_rng(7).standard_normal((1, n)).astype(np.float32).astype(np.float64)
+    want = oracle.infer(art, x, threads=16)
+    got = L.forward(torch.from_numpy(x.astype(np.float32)).to(dev)).cpu().numpy()
+    assert rel_err(got[0], want[0]) < TC, rel_err(got[0], want[0])
+
+
+def test_batched_equals_single_all_variants(dev):
+    # per-vector activation scales: every row of a batched call equals the
+    # single-vector call bit for bit, whatever N / group variant the batch picks
+    art = random_artifact(512, 1024, STAGES[3], 5)
+    L = q8p.Layer.from_qshp(art)
+    x = torch.randn(16, 1024, generator=torch.Generator().manual_seed(1)).to(dev)
+    for batch in (2, 4, 8, 16):
+        y = L.forward(x[:batch].contiguous())
+        for b in (0, batch - 1):
+            assert torch.equal(y[b], L.forward(x[b:b + 1].contiguous())[0])
