@@ -80,6 +80,9 @@ constexpr int kMaxStages = 32;
 #ifndef Q8P_K2_N8_G2NB3
 #define Q8P_K2_N8_G2NB3 0  // batch <= 2: 2 groups x 3 A buffers instead of 3 groups x 2
 #endif
+#ifndef Q8P_K2_DECODE_AHEAD
+#define Q8P_K2_DECODE_AHEAD 1  // decode a whole slab into registers before waiting for the A buffer
+#endif
 #ifndef Q8P_K2_TEAMS
 #define Q8P_K2_TEAMS 1  // decoder teams per group at batch <= 2 (2: +3% K2, but the register
                          // file then leaves no room to co-reside with K1 under PDL)
@@ -516,6 +519,37 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
         const std::uint32_t fl[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_empty_c + 8 * st);  // slab is in registers: hand the slot back
+#if Q8P_K2_DECODE_AHEAD
+        // Decode the whole slab into registers first, then wait for the A buffer:
+        // the decode overlaps the MMA turnaround of the buffer's previous item.
+        std::uint32_t o[64];
+#pragma unroll
+        for (int g4 = 0; g4 < 8; ++g4) {
+          const int ob = 16 * (g4 >> 1) + 8 * (g4 & 1);
+          e8p_fin<0>(e8p_nib<0>(idx[g4], lb), fl[g4], ct_lo, ct_hi, o[ob + 0], o[ob + 1]);
+          e8p_fin<1>(e8p_nib<1>(idx[g4], lb), fl[g4], ct_lo, ct_hi, o[ob + 2], o[ob + 3]);
+          e8p_fin<2>(e8p_nib<2>(idx[g4], lb), fl[g4], ct_lo, ct_hi, o[ob + 4], o[ob + 5]);
+          e8p_fin<3>(e8p_nib<3>(idx[g4], lb), fl[g4], ct_lo, ct_hi, o[ob + 6], o[ob + 7]);
+        }
+        std::uint32_t sd[8];
+#pragma unroll
+        for (int k8 = 0; k8 < 8; ++k8) sd[k8] = (sw >> k8) & 0x01010101u;  // side A = b_k
+        // pin every result before the wait (an empty asm consuming them; no code)
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4)
+          asm volatile("" ::"r"(o[16 * q4 + 0]), "r"(o[16 * q4 + 1]), "r"(o[16 * q4 + 2]), "r"(o[16 * q4 + 3]),
+                       "r"(o[16 * q4 + 4]), "r"(o[16 * q4 + 5]), "r"(o[16 * q4 + 6]), "r"(o[16 * q4 + 7]),
+                       "r"(o[16 * q4 + 8]), "r"(o[16 * q4 + 9]), "r"(o[16 * q4 + 10]), "r"(o[16 * q4 + 11]),
+                       "r"(o[16 * q4 + 12]), "r"(o[16 * q4 + 13]), "r"(o[16 * q4 + 14]), "r"(o[16 * q4 + 15]));
+        asm volatile("" ::"r"(sd[0]), "r"(sd[1]), "r"(sd[2]), "r"(sd[3]), "r"(sd[4]), "r"(sd[5]), "r"(sd[6]),
+                     "r"(sd[7]));
+        mbar_wait(bar_a_empty + 8 * (NB * grp + buf), bph ^ 1);
+        if (tw) tstamp(a, grp, i, 2);
+        tc_fence_after();
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) tmem_st16(abuf + 16 * qq, *reinterpret_cast<std::uint32_t(*)[16]>(o + 16 * qq));
+        tmem_st8(abuf + 64, sd);
+#else
         // magnitude nibbles of all 32 codewords first (LDS latency overlaps the wait)
         std::uint32_t nib[32];
 #pragma unroll
@@ -559,6 +593,7 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
         sd[6] = (sw >> 6) & 0x01010101u;
         sd[7] = (sw >> 7) & 0x01010101u;
         tmem_st8(abuf + 64, sd);
+#endif
       } else {
         const uint4 c0 = lds128(sa + row_in * 16), c1 = lds128(sa + 2048 + row_in * 16);
         const std::uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
