@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -255,6 +256,16 @@ struct Workspace {
   std::uint32_t rows_pad, zcols;
 };
 std::uint32_t rows_pad_of(const q8p_layer* L) { return tc_row_blocks(L->m_local()) * 128; }
+// Batches above the tensor-core path's 16 vectors run as 16-vector chunks through
+// it (weights streamed once per chunk) instead of the portable fp32 GEMV;
+// Q8P_PORTABLE_BIG_BATCH=1 restores the portable path (experiment knob).
+int tc_chunk(const q8p_layer* L, int batch) {
+  static const bool portable = std::getenv("Q8P_PORTABLE_BIG_BATCH") != nullptr;
+  if (tc_supported(*L, batch)) return batch;
+  if (!portable && batch > 16 && tc_supported(*L, 16)) return 16;
+  return 0;  // portable path
+}
+
 std::size_t workspace_parts(const q8p_layer* L, int batch, Workspace* w, void* base) {
   auto* p0 = static_cast<std::uint8_t*>(base);
   std::size_t off = 0;
@@ -263,8 +274,10 @@ std::size_t workspace_parts(const q8p_layer* L, int batch, Workspace* w, void* b
     off += round_up(bytes ? bytes : 1, 256);
     return r;
   };
+  const int chunk = tc_chunk(L, batch);
+  const bool tc = chunk > 0;
+  if (tc) batch = chunk;  // the workspace holds one chunk
   const std::size_t B = std::size_t(batch), mx = std::max(L->n, L->m);
-  const bool tc = tc_supported(*L, batch);
   Workspace v{};
   v.rows_pad = rows_pad_of(L);
   v.zcols = std::uint32_t(tc_ncols_pad(4 * batch));
@@ -290,8 +303,9 @@ std::size_t workspace_size(const q8p_layer* L, int batch) { return workspace_par
 // path) or fp32 z rows in w.z (portable path).
 void forward_local(const q8p_layer* L, const float* x, int batch, const Workspace& w, cudaStream_t s,
                    const q8p_forward_opts* opts) {
-  if (tc_supported(*L, batch)) {
-    const std::uint32_t N = w.zcols, KSL = tc_k_slabs(L->n), bb = 9u * N * 32u;
+  if (tc_supported(*L, batch)) {  // (callers chunk batches above 16)
+    // N from this call's batch (a chunk may be smaller than the workspace's 16)
+    const std::uint32_t N = std::uint32_t(tc_ncols_pad(4 * batch)), KSL = tc_k_slabs(L->n), bb = 9u * N * 32u;
     const bool ragged = (L->n / 8) % 32 != 0;
 #ifndef Q8P_EXP_SKIP_K1
     launch_rht_in_limbs(L->side_v, x, w.u, w.ssq, w.alpha, w.tl, w.bimg, bb, N,
@@ -369,15 +383,19 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
     if (opts) record_event(opts->gemv_end_event, s);
     return;
   }
-  forward_local(L, x, batch, w, s, opts);
-  if (tc_supported(*L, batch)) {
+  if (const int chunk = tc_chunk(L, batch)) {
     float zscale[2] = {L->scale[0], L->scale[1]};
     int ze8p[2] = {L->cb[0] == Q8P_CB_E8P_2BIT, L->cb[1] == Q8P_CB_E8P_2BIT};
+    for (int b0 = 0; b0 < batch; b0 += chunk) {  // one pass for batch <= 16
+      const int nb = std::min(chunk, batch - b0);
+      forward_local(L, x + std::size_t(b0) * L->n, nb, w, s, b0 == 0 ? opts : nullptr);
 #ifndef Q8P_EXP_SKIP_K3
-    launch_rht_out_acc(L->side_u, w.zacc, L->num_stages, w.rows_pad, w.zcols, zscale, ze8p, w.alpha, w.tl, w.u, y,
-                       batch, s);
+      launch_rht_out_acc(L->side_u, w.zacc, L->num_stages, w.rows_pad, std::uint32_t(tc_ncols_pad(4 * nb)), zscale,
+                         ze8p, w.alpha, w.tl, w.u, y + std::size_t(b0) * L->m, nb, s);
 #endif
+    }
   } else {
+    forward_local(L, x, batch, w, s, opts);
     launch_rht(L->side_u, w.z, y, batch, /*transpose=*/true, s);  // y = T_u^T z
   }
 }

@@ -102,7 +102,9 @@ struct Roles {
   static constexpr int kWarpProd2 = kWarpDec + 4 * G * T;  // second code producer (cp.async mode)
   static constexpr int kThreads = (kWarpDec + 4 * G * T + (Q8P_K2_CPASYNC ? 1 : 0)) * 32;
   template <int N>
-  static constexpr std::uint32_t kBg = N <= 8 ? 3 : (N <= 16 ? 2 : 1);  // B-image ring slots per group
+  // B-image ring slots per group.  >= 2: the issuer refills the slot of item
+  // k - 1 with item k - 1 + kBg after issuing item k, so one slot would deadlock.
+  static constexpr std::uint32_t kBg = N <= 8 ? 3 : 2;
 };
 
 struct TcArgs {
