@@ -201,9 +201,10 @@ def run_ours(args):
         copies.append(row)
     maxn = max(n for _, n in layers)
     maxm = max(m for m, _ in layers)
-    ws = torch.empty(max(L.workspace_bytes(1) for L in copies[0]) + (1 << 20), dtype=torch.uint8, device=dev)
-    xs = [torch.randn(1, n, device=dev) for _, n in layers]
-    ys = [torch.empty(1, m, device=dev) for m, _ in layers]
+    B = args.batch
+    ws = torch.empty(max(L.workspace_bytes(B) for L in copies[0]) + (1 << 20), dtype=torch.uint8, device=dev)
+    xs = [torch.randn(B, n, device=dev) for _, n in layers]
+    ys = [torch.empty(B, m, device=dev) for m, _ in layers]
     stream = torch.cuda.Stream(device=dev)
 
     n_gemv = len(layers)
@@ -291,13 +292,13 @@ def run_ours(args):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    tokens_per_s = 1e3 / ms
+    tokens_per_s = B * 1e3 / ms
 
     # e2e through the public API with host buffers: H2D x, forward, D2H y.
-    hx = [torch.randn(1, n).pin_memory() for _, n in layers]
-    hy = [torch.empty(1, m).pin_memory() for m, _ in layers]
-    h2d = sum(4 * n for _, n in layers)
-    d2h = sum(4 * m for m, _ in layers)
+    hx = [torch.randn(B, n).pin_memory() for _, n in layers]
+    hy = [torch.empty(B, m).pin_memory() for m, _ in layers]
+    h2d = sum(4 * B * n for _, n in layers)
+    d2h = sum(4 * B * m for m, _ in layers)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
@@ -325,7 +326,7 @@ def run_ours(args):
     if not sharded and all(gemv_ms[li] for li in range(n_gemv)):
         per = []
         for li, (m, n) in enumerate(layers):
-            b = m * n // 8 * 2 + 4 * n + 4 * m
+            b = m * n // 8 * 2 + 4 * B * n + 4 * B * m
             t = statistics.mean(gemv_ms[li])
             per.append({"layer": f"{m}x{n}", "bytes": b, "us": t * 1e3, "gbs": b / (t * 1e-3) / 1e9})
         # dominant kernel: K2 on the largest layer(s) (both 70B MLP shapes move the same bytes)
@@ -365,13 +366,13 @@ def run_ours(args):
             "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-            "config": {"workload": f"llama2-{args.workload}-layer-set-2bit-b1", "batch": 1,
+            "config": {"workload": f"llama2-{args.workload}-layer-set-2bit-b{B}", "batch": B,
                        "layers": [f"{m}x{n}" for m, n in layers],
                        "parallelism": f"row-shard tp{world}" if world > 1 else "single-gpu",
                        "l2": f"{args.copies} rotating copies of the layer set (> L2 per step pair)",
                        "codes": "uniform-random e8p-2bit codes (perf variant, test_pipeline.cpp:256-273)",
                        "cuda_graph": use_graph},
-            "e2e": {"value": 1e3 / e2e_ms, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": B * 1e3 / e2e_ms, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": int(launches),
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -392,6 +393,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="70b", choices=["70b", "7b"])
     ap.add_argument("--copies", type=int, default=2)
+    ap.add_argument("--batch", type=int, default=1, help="vectors per layer call (BASELINE configs[1]: 1..16)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="use q8p_forward_sharded even at N=1 (1-rank NCCL)")
     ap.add_argument("--no-cpu", action="store_true")
