@@ -528,6 +528,13 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
 #pragma unroll
         for (int g4 = 0; g4 < 8; ++g4) {
           const int ob = 16 * (g4 >> 1) + 8 * (g4 & 1);
+#ifdef Q8P_EXP_LDS_ONLY  // experiment: keep the LUT loads, drop the ALU decode
+          o[ob + 0] = e8p_nib<0>(idx[g4], lb); o[ob + 1] = fl[g4];
+          o[ob + 2] = e8p_nib<1>(idx[g4], lb); o[ob + 3] = fl[g4];
+          o[ob + 4] = e8p_nib<2>(idx[g4], lb); o[ob + 5] = fl[g4];
+          o[ob + 6] = e8p_nib<3>(idx[g4], lb); o[ob + 7] = fl[g4];
+          continue;
+#endif
           e8p_fin<0>(e8p_nib<0>(idx[g4], lb), fl[g4], ct_lo, ct_hi, o[ob + 0], o[ob + 1]);
           e8p_fin<1>(e8p_nib<1>(idx[g4], lb), fl[g4], ct_lo, ct_hi, o[ob + 2], o[ob + 3]);
           e8p_fin<2>(e8p_nib<2>(idx[g4], lb), fl[g4], ct_lo, ct_hi, o[ob + 4], o[ob + 5]);
