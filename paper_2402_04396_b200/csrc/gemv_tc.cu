@@ -194,8 +194,17 @@ constexpr std::uint32_t kCtHi = 0x00FBFDFFu;  // {-1,-3,-5,0}
 template <int JJ>
 __device__ __forceinline__ std::uint32_t e8p_nib(std::uint32_t idxreg, std::uint32_t lb) {
   // volatile: issued before the A-buffer wait so the LDS latency overlaps it
-  std::uint32_t r;
-  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(r) : "r"(prmt(idxreg, lb, 0x7604u | (std::uint32_t(JJ) << 4))));
+  std::uint32_t r, addr;
+  if constexpr (JJ == 3) {
+    // top byte: two FMA-pipe ops (mul.hi by 256, mad) instead of one ALU PRMT --
+    // the decode is ALU-bound, the FMA pipe has room
+    asm("{\n\t.reg .u32 t;\n\tmul.hi.u32 t, %1, 256;\n\tmad.lo.u32 %0, t, 256, %2;\n\t}\n"
+        : "=r"(addr)
+        : "r"(idxreg), "r"(lb));
+  } else {
+    addr = prmt(idxreg, lb, 0x7604u | (std::uint32_t(JJ) << 4));
+  }
+  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(r) : "r"(addr));
   return r;
 }
 template <int JJ>
@@ -542,7 +551,8 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
         }
         std::uint32_t sd[8];
 #pragma unroll
-        for (int k8 = 0; k8 < 8; ++k8) sd[k8] = (sw >> k8) & 0x01010101u;  // side A = b_k
+        for (int k8 = 0; k8 < 8; ++k8)  // side A = b_k; the shift on the FMA pipe (mul.hi)
+          sd[k8] = (k8 == 0 ? sw : __umulhi(sw, 1u << (32 - k8))) & 0x01010101u;
         // pin every result before the wait (an empty asm consuming them; no code)
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4)

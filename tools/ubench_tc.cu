@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(128 + 32 * STW, 1) k_mma(int groups, int per_g
 }
 
 // NI issuer warps, each issuing groups of 9 MMAs (N=8) into its own D with its own A columns.
-template <int NI, int FENCE, int STW = 0, int SLEEP = 0, int LDSW = 0>
+template <int NI, int FENCE, int STW = 0, int SLEEP = 0, int LDSW = 0, int ALUW = 0>
 __global__ void __launch_bounds__(512, 1) k_multi(int groups, unsigned long long* out) {
   extern __shared__ __align__(1024) std::uint8_t smem[];
   const std::uint32_t sb = smem_u32(smem);
@@ -119,6 +119,21 @@ __global__ void __launch_bounds__(512, 1) k_multi(int groups, unsigned long long
   __shared__ int stop2;
   if (threadIdx.x == 0) stop2 = 0;
   __syncthreads();
+  if (ALUW && warp >= 4 && warp < 4 + ALUW) {  // ALU-heavy decode-like work (PRMT / LOP3 chains)
+    std::uint32_t a0 = threadIdx.x, a1 = threadIdx.x * 7u, a2 = 0x00050301u, a3 = 0x00FBFDFFu, acc = 0;
+    while (*reinterpret_cast<volatile int*>(&stop2) == 0) {
+#pragma unroll 16
+      for (int k = 0; k < 64; ++k) {
+        std::uint32_t r;
+        asm volatile("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a2), "r"(a3), "r"(a0));
+        a0 = (a0 ^ (a1 & 0x44444444u)) + r;
+        asm volatile("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a2), "r"(a3), "r"(a1));
+        a1 ^= r;
+        acc += r;
+      }
+    }
+    if (acc == 0x12345679u) out[10] = acc;
+  }
   if (LDSW && warp >= 4 && warp < 4 + LDSW) {  // LUT-style LDS traffic (lane-replicated rows)
     std::uint32_t acc = threadIdx.x, x = threadIdx.x * 2654435761u;
     const std::uint32_t lut = sb + 1024 + 8192;
@@ -176,18 +191,18 @@ __global__ void __launch_bounds__(512, 1) k_multi(int groups, unsigned long long
   }
 }
 
-template <int NI, int FENCE = 0, int STW = 0, int SLEEP = 0, int LDSW = 0>
+template <int NI, int FENCE = 0, int STW = 0, int SLEEP = 0, int LDSW = 0, int ALUW = 0>
 void run_multi(unsigned long long* d) {
   const int groups = 2000;
-  cudaFuncSetAttribute(k_multi<NI, FENCE, STW, SLEEP, LDSW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 1024);
-  k_multi<NI, FENCE, STW, SLEEP, LDSW><<<148, 128 + 32 * (STW > LDSW ? STW : LDSW), 32 * 1024>>>(groups, d);
+  cudaFuncSetAttribute(k_multi<NI, FENCE, STW, SLEEP, LDSW, ALUW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 1024);
+  k_multi<NI, FENCE, STW, SLEEP, LDSW, ALUW><<<148, 128 + 32 * (STW > LDSW ? (STW > ALUW ? STW : ALUW) : (LDSW > ALUW ? LDSW : ALUW)), 32 * 1024>>>(groups, d);
   cudaDeviceSynchronize();
   unsigned long long c[4] = {0, 0, 0, 0};
   cudaMemcpy(c, d, 8 * NI, cudaMemcpyDeviceToHost);
   unsigned long long mx = 0;
   for (int i = 0; i < NI; ++i) mx = c[i] > mx ? c[i] : mx;
   unsigned long long sb8 = 0; cudaMemcpy(&sb8, d + 8, 8, cudaMemcpyDeviceToHost);
-  printf("multi-issuer ldsw=%d fence=%d NI=%d stw=%d sleep=%d (sttm %.0f B/kcyc/warp): %.1f cyc per 9-MMA group per issuer, %.1f cyc per MMA aggregate (err=%s)\n", LDSW, FENCE, NI, STW, SLEEP, double(sb8),
+  printf("multi-issuer aluw=%d ldsw=%d fence=%d NI=%d stw=%d sleep=%d (sttm %.0f B/kcyc/warp): %.1f cyc per 9-MMA group per issuer, %.1f cyc per MMA aggregate (err=%s)\n", ALUW, LDSW, FENCE, NI, STW, SLEEP, double(sb8),
          double(mx) / groups, double(mx) / (groups * 9.0 * NI), cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -246,8 +261,8 @@ int main() {
   run<8, true, 1, true>(d);
   cudaMemset(d, 0, 64 * 8);
   run_multi<3>(d);
-  run_multi<3, 0, 0, 0, 4>(d);
-  run_multi<3, 0, 0, 0, 12>(d);
+  run_multi<3, 0, 0, 0, 0, 4>(d);
+  run_multi<3, 0, 0, 0, 0, 12>(d);
   k_sttm<<<148, 128>>>(4000, d);
   cudaDeviceSynchronize();
   unsigned long long c;
