@@ -550,7 +550,11 @@ void plan_split_impl(const DevSide& side, RhtArgs& a) {
   a.q = side.q;
   // pass-1 chunk P2 * q: ~1K floats (<= 512 for the order-172 base, whose
   // dense product dominates pass 1)
-  const std::uint32_t target = side.q > 28 ? 512 : 1024;
+  static const std::uint32_t tune = [] {  // experiment knob: pass-1 chunk target (floats)
+    const char* e = std::getenv("Q8P_RHT_CHUNK");
+    return e ? std::uint32_t(std::atoi(e)) : 0u;
+  }();
+  const std::uint32_t target = tune ? tune : 512;  // 512 measured best for the step (1024: +3 %)
   std::uint32_t P2 = 1;
   while (P2 * 2 <= side.p && P2 * 2 * side.q <= target) P2 *= 2;
   if ((P2 * side.q) % 4 != 0) throw SizeError("rht: dimension too small for the float4 passes");
