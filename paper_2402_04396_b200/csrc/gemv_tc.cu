@@ -83,6 +83,11 @@ constexpr int kMaxStages = 32;
 #ifndef Q8P_K2_DECODE_AHEAD
 #define Q8P_K2_DECODE_AHEAD 1  // decode a whole slab into registers before waiting for the A buffer
 #endif
+#ifdef Q8P_EXP_POLL_AEMPTY
+#define A_EMPTY_WAIT mbar_wait_poll
+#else
+#define A_EMPTY_WAIT mbar_wait
+#endif
 #ifndef Q8P_K2_TEAMS
 #define Q8P_K2_TEAMS 1  // decoder teams per group at batch <= 2 (2: +3% K2, but the register
                          // file then leaves no room to co-reside with K1 under PDL)
@@ -458,8 +463,14 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
         mma_commit_e(ae0 + 8 * buf);
         mma_commit_e(eb + 8 * bslot);
 #else
+#ifdef Q8P_EXP_ONE_MMA  // experiment: one MMA per item (wrong results) to split per-MMA vs per-item cost
+        mma_i8_ts_e(dcol_g + s * N, acol0 + buf * kAcols, bd0 + bslot * bstep, idesc, (started >> s) & 1);
+        mma_commit_e(ae0 + 8 * buf);
+        mma_commit_e(eb + 8 * bslot);
+#else
         mma_i8_slab_e<2 * N>(dcol_g + s * N, acol0 + buf * kAcols, bd0 + bslot * bstep, idesc, (started >> s) & 1,
                              (s ? a.kind[1] : a.kind[0]) == 0, ae0 + 8 * buf, eb + 8 * bslot);
+#endif
 #endif
 #ifdef Q8P_K2_TRACE_SYNC
         mbar_wait(ae0 + 8 * buf, bph);  // debug: serialise to time one item's MMAs
@@ -562,7 +573,7 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
                        "r"(o[16 * q4 + 12]), "r"(o[16 * q4 + 13]), "r"(o[16 * q4 + 14]), "r"(o[16 * q4 + 15]));
         asm volatile("" ::"r"(sd[0]), "r"(sd[1]), "r"(sd[2]), "r"(sd[3]), "r"(sd[4]), "r"(sd[5]), "r"(sd[6]),
                      "r"(sd[7]));
-        mbar_wait(bar_a_empty + 8 * (NB * grp + buf), bph ^ 1);
+        A_EMPTY_WAIT(bar_a_empty + 8 * (NB * grp + buf), bph ^ 1);
         if (tw) tstamp(a, grp, i, 2);
         tc_fence_after();
 #pragma unroll
@@ -578,7 +589,7 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
           nib[4 * g4 + 2] = e8p_nib<2>(idx[g4], lb);
           nib[4 * g4 + 3] = e8p_nib<3>(idx[g4], lb);
         }
-        mbar_wait(bar_a_empty + 8 * (NB * grp + buf), bph ^ 1);
+        A_EMPTY_WAIT(bar_a_empty + 8 * (NB * grp + buf), bph ^ 1);
         if (tw) tstamp(a, grp, i, 2);
         tc_fence_after();
 #pragma unroll
@@ -618,7 +629,7 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
         const std::uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_empty_c + 8 * st);
-        mbar_wait(bar_a_empty + 8 * (NB * grp + buf), bph ^ 1);
+        A_EMPTY_WAIT(bar_a_empty + 8 * (NB * grp + buf), bph ^ 1);
         tc_fence_after();
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) {

@@ -57,6 +57,17 @@ __device__ __forceinline__ void mbar_wait(std::uint32_t bar, std::uint32_t parit
       : "memory");
 }
 
+// Busy-poll variant (mbarrier.test_wait never suspends the thread).
+__device__ __forceinline__ void mbar_wait_poll(std::uint32_t bar, std::uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "P_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra P_%=;\n\t}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
 // ---- bulk async copy global -> shared (completes on an mbarrier) --------------
 __device__ __forceinline__ void bulk_g2s(std::uint32_t dst, const void* src, std::uint32_t bytes, std::uint32_t bar) {
   asm volatile(
