@@ -365,7 +365,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "s8xs8->s32 (K2 tensor cores) + fp32 (RHT, I/O)", "data": "synthetic",
             "config": {"workload": f"llama2-{args.workload}-layer-set-2bit-b{B}", "batch": B,
                        "layers": [f"{m}x{n}" for m, n in layers],
                        "parallelism": f"row-shard tp{world}" if world > 1 else "single-gpu",
