@@ -341,7 +341,8 @@ void forward_sharded_impl(const q8p_layer* L, const float* x, float* y, int batc
   if (batch == 0) return;
   if (!x || !y) throw ValidationError("null x / y");
   if (!comm) throw ValidationError("null communicator");
-  if (!tc_supported(*L, batch)) throw UnsupportedError("row-sharded forward needs the tensor-core path (batch <= 16)");
+  const int chunk = tc_chunk(L, batch);  // batches above 16 go through in 16-vector chunks
+  if (chunk == 0) throw UnsupportedError("row-sharded forward needs the tensor-core path");
   int world = 0, rank = 0;
   nccl_check(ncclCommCount(comm, &world), "ncclCommCount");
   nccl_check(ncclCommUserRank(comm, &rank), "ncclCommUserRank");
@@ -352,17 +353,21 @@ void forward_sharded_impl(const q8p_layer* L, const float* x, float* y, int batc
   DeviceGuard g(L->device);
   Workspace w;
   workspace_parts(L, batch, &w, ws);
-  forward_local(L, x, batch, w, s, nullptr);
   float zscale[2] = {L->scale[0], L->scale[1]};
   int ze8p[2] = {L->cb[0] == Q8P_CB_E8P_2BIT, L->cb[1] == Q8P_CB_E8P_2BIT};
   float* zl = L->row_begin == 0 && L->row_end == L->m ? w.z_full : w.z_loc;
-  launch_combine_acc(w.zacc, L->num_stages, w.rows_pad, w.zcols, zscale, ze8p, w.alpha, w.tl, zl, ml, batch, s);
-  nccl_check(ncclGroupStart(), "ncclGroupStart");
-  for (int b = 0; b < batch; ++b)
-    nccl_check(ncclAllGather(zl + std::size_t(b) * ml, w.z_full + std::size_t(b) * L->m, ml, ncclFloat32, comm, s),
-               "ncclAllGather");
-  nccl_check(ncclGroupEnd(), "ncclGroupEnd");
-  launch_rht_out(L->side_u, w.z_full, w.u, y, batch, s);
+  for (int b0 = 0; b0 < batch; b0 += chunk) {
+    const int nb = std::min(chunk, batch - b0);
+    forward_local(L, x + std::size_t(b0) * L->n, nb, w, s, nullptr);
+    launch_combine_acc(w.zacc, L->num_stages, w.rows_pad, std::uint32_t(tc_ncols_pad(4 * nb)), zscale, ze8p, w.alpha,
+                       w.tl, zl, ml, nb, s);
+    nccl_check(ncclGroupStart(), "ncclGroupStart");
+    for (int b = 0; b < nb; ++b)
+      nccl_check(ncclAllGather(zl + std::size_t(b) * ml, w.z_full + std::size_t(b) * L->m, ml, ncclFloat32, comm, s),
+                 "ncclAllGather");
+    nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+    launch_rht_out(L->side_u, w.z_full, w.u, y + std::size_t(b0) * L->m, nb, s);
+  }
 }
 
 void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void* ws, std::size_t ws_bytes,

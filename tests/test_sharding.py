@@ -118,3 +118,20 @@ def test_forward_sharded_world1_bit_exact(name):
         assert torch.equal(y0, y1)
     finally:
         comm.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("batch", [3, 16, 20])
+def test_forward_sharded_world1_batches(batch):
+    import torch
+
+    import paper_2402_04396_b200 as q8p
+
+    art = open(os.path.join(GOLDEN, "rvq4_128x128.qshp"), "rb").read()
+    x = torch.randn(batch, 128, generator=torch.Generator().manual_seed(batch)).cuda()
+    comm = q8p.NcclComm(q8p.NcclComm.unique_id(), 1, 0, 0)
+    try:
+        L = q8p.Layer.from_qshp(art, device=0)
+        assert torch.equal(L.forward(x), L.forward_sharded(x, comm))
+    finally:
+        comm.close()
