@@ -327,21 +327,28 @@ class Layer:
             self._ws = torch.empty(need, dtype=torch.uint8, device=f"cuda:{self.info['device']}")
         return self._ws
 
+    def _dims(self):
+        d = self.__dict__.get("_dims_cache")
+        if d is None:  # immutable after creation: query the C ABI once
+            i = self.info
+            d = self.__dict__["_dims_cache"] = (i["m"], i["n"])
+        return d
+
     def forward(self, x, out=None, stream=None, workspace=None, gemv_events=None):
         """y = W_tilde x for a [batch, n] fp32 CUDA tensor -> [batch, m].
         gemv_events: optional (start, end) torch.cuda.Event pair recorded
         around the decode-GEMV kernel."""
         torch = _torch()
-        info = self.info
+        m, n = self._dims()
         if x.dim() == 1:
             return self.forward(x.view(1, -1), None if out is None else out.view(1, -1), stream, workspace).view(-1)
         if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous():
             raise ValidationError("x must be a contiguous float32 CUDA tensor")
-        if x.shape[1] != info["n"]:
+        if x.shape[1] != n:
             raise SizeError("infer: input length != n")
         batch = x.shape[0]
         if out is None:
-            out = torch.empty(batch, info["m"], dtype=torch.float32, device=x.device)
+            out = torch.empty(batch, m, dtype=torch.float32, device=x.device)
         ws = workspace if workspace is not None else self.workspace(batch)
         if gemv_events is None:
             _check(lib().q8p_forward(self._h, x.data_ptr(), out.data_ptr(), batch, ws.data_ptr(),

@@ -405,6 +405,56 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
   }
 }
 
+// q8p_forward fast path: the forward's 5-kernel chain is captured once per
+// (x, y, batch, workspace) into a CUDA graph and replayed with a single
+// cudaGraphLaunch -- one host launch instead of five, same kernels, same
+// stream order.  Skipped while the caller's stream is itself capturing (the
+// kernels then go into the caller's graph) and with Q8P_NO_GRAPH_CACHE.
+void forward_cached(q8p_layer* L, const float* x, float* y, int batch, void* ws, std::size_t ws_bytes,
+                    cudaStream_t s) {
+  static const bool off = std::getenv("Q8P_NO_GRAPH_CACHE") != nullptr;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (off || !L || batch <= 0 || cudaStreamIsCapturing(s, &cap) != cudaSuccess ||
+      cap != cudaStreamCaptureStatusNone) {
+    forward_impl(L, x, y, batch, ws, ws_bytes, s);
+    return;
+  }
+  cudaGraphExec_t exec = nullptr;
+  {
+    std::scoped_lock lock(L->graph_mu);
+    for (const auto& e : L->graphs)
+      if (e.x == x && e.y == y && e.batch == batch && e.ws == ws && e.ws_bytes == ws_bytes) exec = e.exec;
+    if (!exec) {
+      DeviceGuard g(L->device);
+      if (!L->capture_stream)
+        cuda_check(cudaStreamCreateWithFlags(&L->capture_stream, cudaStreamNonBlocking), "capture stream");
+      cudaGraph_t graph = nullptr;
+      const std::uint64_t k0 = g_launches.load();
+      cuda_check(cudaStreamBeginCapture(L->capture_stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+      try {
+        forward_impl(L, x, y, batch, ws, ws_bytes, L->capture_stream);  // validates arguments
+      } catch (...) {
+        cudaStreamEndCapture(L->capture_stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      cuda_check(cudaStreamEndCapture(L->capture_stream, &graph), "end capture");
+      const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      cuda_check(ie, "graph instantiate");
+      if (L->graphs.size() >= 8) {  // bounded: evict the oldest
+        cudaGraphExecDestroy(L->graphs.front().exec);
+        L->graphs.erase(L->graphs.begin());
+      }
+      L->graphs.push_back({x, y, batch, ws, ws_bytes, exec, std::uint32_t(g_launches.load() - k0)});
+      g_launches.fetch_sub(L->graphs.back().kernels);  // counted per replay below
+    }
+    for (const auto& e : L->graphs)
+      if (e.exec == exec) g_launches.fetch_add(e.kernels, std::memory_order_relaxed);
+  }
+  cuda_check(cudaGraphLaunch(exec, s), "graph launch");
+}
+
 }  // namespace
 }  // namespace q8p::detail
 
@@ -481,6 +531,9 @@ void q8p_layer_destroy(q8p_layer* L) {
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(L->device);
+  for (auto& e : L->graphs) cudaGraphExecDestroy(e.exec);
+  L->graphs.clear();
+  if (L->capture_stream) cudaStreamDestroy(L->capture_stream);
   for (void* p : L->allocations) cudaFree(p);
   if (L->dev_stage) cudaFree(L->dev_stage);
   if (L->host_stage) cudaFreeHost(L->host_stage);
@@ -513,7 +566,7 @@ size_t q8p_workspace_bytes(const q8p_layer* L, int batch) {
 q8p_status q8p_forward(const q8p_layer* L, const float* x, float* y, int batch, void* ws,
                        size_t ws_bytes, void* stream) {
   try {
-    forward_impl(L, x, y, batch, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+    forward_cached(const_cast<q8p_layer*>(L), x, y, batch, ws, ws_bytes, static_cast<cudaStream_t>(stream));
     return Q8P_OK;
   } catch (...) {
     return status_of_current_exception();

@@ -88,6 +88,20 @@ struct q8p_layer {
   void* dev_stage = nullptr;
   std::size_t dev_stage_bytes = 0;
   cudaStream_t stream = nullptr;
+  // q8p_forward graph cache (capi.cpp): the forward's kernel chain captured once per
+  // (x, y, batch, workspace) and replayed with one cudaGraphLaunch.
+  struct GraphEntry {
+    const float* x;
+    float* y;
+    int batch;
+    void* ws;
+    std::size_t ws_bytes;
+    cudaGraphExec_t exec;
+    std::uint32_t kernels;  // q8p kernels per replay (kernel_launches accounting)
+  };
+  std::mutex graph_mu;
+  std::vector<GraphEntry> graphs;  // small, most recent last
+  cudaStream_t capture_stream = nullptr;
 
   std::uint32_t m_local() const { return row_end - row_begin; }
 };
