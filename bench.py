@@ -294,24 +294,32 @@ def run_ours(args):
         ms = float(t.item())
     tokens_per_s = B * 1e3 / ms
 
-    # e2e through the public API with host buffers: H2D x, forward, D2H y.
-    hx = [torch.randn(B, n).pin_memory() for _, n in layers]
-    hy = [torch.empty(B, m).pin_memory() for m, _ in layers]
-    h2d = sum(4 * B * n for _, n in layers)
-    d2h = sum(4 * B * m for m, _ in layers)
+    # e2e through the public API with host buffers: per step, one H2D copy of all
+    # layers' inputs from pinned memory, the layer forwards, one D2H copy of all
+    # outputs, and a stream sync (the result is on the host when the step ends).
+    nsum, msum = sum(n for _, n in layers), sum(m for m, _ in layers)
+    hx = torch.randn(B * nsum).pin_memory()
+    hy = torch.empty(B * msum).pin_memory()
+    dx = torch.empty(B * nsum, device=dev)
+    dy = torch.empty(B * msum, device=dev)
+    xo = np.cumsum([0] + [B * n for _, n in layers])
+    yo = np.cumsum([0] + [B * m for m, _ in layers])
+    xv = [dx[xo[i]:xo[i + 1]].view(B, n) for i, (_, n) in enumerate(layers)]
+    yv = [dy[yo[i]:yo[i + 1]].view(B, m) for i, (m, _) in enumerate(layers)]
+    h2d, d2h = 4 * B * nsum, 4 * B * msum
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         e0.record(stream)
         for s in range(args.steps):
             c = s % args.copies
+            dx.copy_(hx, non_blocking=True)
             for li, L in enumerate(copies[c]):
-                xs[li].copy_(hx[li], non_blocking=True)
                 if sharded:
-                    L.forward_sharded(xs[li], comm, out=ys[li], stream=stream, workspace=ws)
+                    L.forward_sharded(xv[li], comm, out=yv[li], stream=stream, workspace=ws)
                 else:
-                    L.forward(xs[li], out=ys[li], stream=stream, workspace=ws)
-                hy[li].copy_(ys[li], non_blocking=True)
+                    L.forward(xv[li], out=yv[li], stream=stream, workspace=ws)
+            hy.copy_(dy, non_blocking=True)
             stream.synchronize()
         e1.record(stream)
     torch.cuda.synchronize()

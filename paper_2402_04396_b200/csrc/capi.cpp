@@ -408,11 +408,14 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
 // q8p_forward fast path: the forward's 5-kernel chain is captured once per
 // (x, y, batch, workspace) into a CUDA graph and replayed with a single
 // cudaGraphLaunch -- one host launch instead of five, same kernels, same
-// stream order.  Skipped while the caller's stream is itself capturing (the
-// kernels then go into the caller's graph) and with Q8P_NO_GRAPH_CACHE.
+// stream order.  Opt-in (Q8P_GRAPH_CACHE=1): it cuts the host cost per call
+// from ~20 to ~4 us, but a graph boundary drops the programmatic-dependent-launch
+// overlap between consecutive layers, so GPU-bound callers (bench.py e2e: 7.9 k
+// vs 7.7 k tokens/s) are better served by plain launches.  Skipped while the
+// caller's stream is itself capturing (the kernels then go into its graph).
 void forward_cached(q8p_layer* L, const float* x, float* y, int batch, void* ws, std::size_t ws_bytes,
                     cudaStream_t s) {
-  static const bool off = std::getenv("Q8P_NO_GRAPH_CACHE") != nullptr;
+  static const bool off = std::getenv("Q8P_GRAPH_CACHE") == nullptr;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (off || !L || batch <= 0 || cudaStreamIsCapturing(s, &cap) != cudaSuccess ||
       cap != cudaStreamCaptureStatusNone) {
