@@ -45,6 +45,15 @@
 // Decode per codeword: PRMT (LUT address) + LDS (lane-replicated nibble LUT,
 // 64-KiB-aligned window) + shift + LOP3 (sign flags) + 2 PRMT from the constant
 // byte table {1,3,5,_,-1,-3,-5,_}.
+//
+// Build-time switches (NVEXTRA=-D... to paper_2402_04396_b200/csrc/Makefile), all
+// measured and documented in DESIGN.md sections 6-7; defaults are the fastest:
+//   Q8P_K2_SMEM_KB (200)  Q8P_K2_TEAMS (1)  Q8P_K2_CPASYNC (0)  Q8P_K2_DECODE_AHEAD (1)
+//   Q8P_K2_N8_G2NB3 (0)   Q8P_K2_TRACE (off: per-item clock64 timeline of CTA 0)
+//   experiments that compile parts of the loop out (wrong results, timing only):
+//   Q8P_EXP_NO_DECODE / _NO_STTM / _NO_MMA / _LDS_ONLY / _ONE_MMA / _POLL_AEMPTY,
+//   Q8P_STAGGER_NS.  Run-time knobs: Q8P_FUSE (fused layer kernel),
+//   Q8P_K2_LATE_PREFETCH, Q8P_TRACE (timeline file prefix).
 #include <cuda_runtime.h>
 
 #include <algorithm>
