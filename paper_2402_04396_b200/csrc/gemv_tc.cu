@@ -33,15 +33,20 @@
 //   no-swizzle core-matrix layout ([N/8][2][8][16 B]); K-block 8 = side.
 //
 // CTA (one per SM, persistent over a contiguous range of (row block, k slab,
-// stage) items; warp-specialised):
-//   warp 0      producer: cp.async.bulk of code slabs (before griddepcontrol.wait,
-//               so they overlap K1) and B slabs into an smem ring (mbarriers)
-//   warp 1      MMA issuer: 8 + 1 tcgen05.mma (M=128, N, K=32) per slab into a
-//               TMEM accumulator per row block; tcgen05.commit frees the ring
-//               stage and the A buffer
-//   warps 2..5  epilogue: tcgen05.ld of finished accumulators -> int32 atomics
-//   warps 6..   G decode groups of 4 warps (thread = TMEM lane = row): smem codes
-//               -> A bytes -> tcgen05.st into a double-buffered A tile
+// stage) items; warp-specialised; item i belongs to decode group i % G):
+//   warp 0        code producer: 1-D cp.async.bulk of code slabs into a ring
+//                 (the first S before TMEM allocation, all before
+//                 griddepcontrol.wait, so they overlap K1), the LUT window;
+//                 a decoder releases its slot right after loading the slab
+//   warps 1..G    one MMA issuer per group: waits for the group's A buffer,
+//                 8 + 1 tcgen05.mma (M=128, N, K=32) into the group's TMEM
+//                 accumulator with B from its own B-image ring (prefetched from
+//                 L2 after griddepcontrol.wait); commits free the A buffer and
+//                 the B slot, and at a row-block end hand D to the epilogue
+//   warps 1+G..   G groups x 4 decode warps (warp = TMEM lane quadrant, thread =
+//                 row): slab -> A bytes in registers -> tcgen05.st into the
+//                 group's double-buffered A tile; the group's row-block epilogue
+//                 (tcgen05.ld -> int32 atomics) once its D is final
 // Decode per codeword: PRMT (LUT address) + LDS (lane-replicated nibble LUT,
 // 64-KiB-aligned window) + shift + LOP3 (sign flags) + 2 PRMT from the constant
 // byte table {1,3,5,_,-1,-3,-5,_}.
