@@ -134,6 +134,13 @@ q8p_status q8p_forward_ex(const q8p_layer* layer, const float* x, float* y, int 
  * all-gathered over `nccl_comm` (an ncclComm_t), then every rank applies
  * the output transform to the full z.  Shards must be equal-sized and
  * ordered by rank. */
+/* This handle's rows of the incoherent-domain product, z = W_hat (T_v x) for
+ * rows [row_begin, row_end): z [batch][row_end - row_begin] fp32 (the slice
+ * q8p_forward_sharded all-gathers; y = T_u^T z over the concatenated slices).
+ * Stream-ordered, uses the same workspace as the forward. */
+q8p_status q8p_forward_rows_z(const q8p_layer* layer, const float* x, float* z, int batch,
+                              void* workspace, size_t workspace_bytes, void* stream);
+
 q8p_status q8p_forward_sharded(const q8p_layer* layer, const float* x, float* y, int batch,
                                void* workspace, size_t workspace_bytes, void* nccl_comm,
                                void* stream);

@@ -125,6 +125,7 @@ _SIGNATURES = {
     "q8p_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int]),
     "q8p_forward": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "q8p_forward_ex": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.POINTER(ForwardOpts)]),
+    "q8p_forward_rows_z": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "q8p_forward_sharded": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]),
     "q8p_infer_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
     "q8p_decode_stage": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
@@ -358,6 +359,18 @@ class Layer:
             _check(lib().q8p_forward_ex(self._h, x.data_ptr(), out.data_ptr(), batch, ws.data_ptr(),
                                         ws.numel(), _stream_ptr(stream), ctypes.byref(opts)))
         return out
+
+    def rows_z(self, x, stream=None, workspace=None):
+        """This handle's rows of z = W_hat T_v x ([batch, rows]); the slice a
+        row-sharded forward all-gathers before y = T_u^T z."""
+        torch = _torch()
+        info = self.info
+        batch = x.shape[0]
+        z = torch.empty(batch, info["row_end"] - info["row_begin"], dtype=torch.float32, device=x.device)
+        ws = workspace if workspace is not None else self.workspace(batch)
+        _check(lib().q8p_forward_rows_z(self._h, x.data_ptr(), z.data_ptr(), batch, ws.data_ptr(), ws.numel(),
+                                        _stream_ptr(stream)))
+        return z
 
     def forward_sharded(self, x, comm, out=None, stream=None, workspace=None):
         """Row-sharded forward (q8p_forward_sharded): this layer holds rows

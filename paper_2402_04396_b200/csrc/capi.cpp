@@ -772,6 +772,28 @@ q8p_status q8p_hadamard_base(size_t q, int8_t* out) {
   }
 }
 
+q8p_status q8p_forward_rows_z(const q8p_layer* L, const float* x, float* z, int batch, void* ws, size_t ws_bytes,
+                              void* stream) {
+  try {
+    if (!L || !x || !z) throw q8p::ValidationError("null argument");
+    if (batch <= 0) return Q8P_OK;
+    if (!tc_supported(*L, batch)) throw q8p::UnsupportedError("rows_z needs the tensor-core path (batch <= 16)");
+    if (!ws || ws_bytes < workspace_size(L, batch)) throw q8p::SizeError("workspace too small");
+    DeviceGuard g(L->device);
+    Workspace w;
+    workspace_parts(L, batch, &w, ws);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    forward_local(L, x, batch, w, s, nullptr);
+    float zscale[2] = {L->scale[0], L->scale[1]};
+    int ze8p[2] = {L->cb[0] == Q8P_CB_E8P_2BIT, L->cb[1] == Q8P_CB_E8P_2BIT};
+    launch_combine_acc(w.zacc, L->num_stages, w.rows_pad, w.zcols, zscale, ze8p, w.alpha, w.tl, z, L->m_local(), batch,
+                       s);
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
 q8p_status q8p_forward_sharded(const q8p_layer* L, const float* x, float* y, int batch, void* ws, size_t ws_bytes,
                                void* nccl_comm, void* stream) {
   try {

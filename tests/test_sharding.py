@@ -135,3 +135,31 @@ def test_forward_sharded_world1_batches(batch):
         assert torch.equal(L.forward(x), L.forward_sharded(x, comm))
     finally:
         comm.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("bits", [2, 3])
+def test_row_shards_on_one_gpu(world, bits):
+    # What q8p_forward_sharded computes at G ranks, run on one GPU without NCCL:
+    # every shard handle's z rows (K1 -> K2 on its rows -> combine) concatenate to
+    # the full layer's z bit for bit (row sharding leaves each row's integer
+    # accumulation unchanged), and T_u^T of that z is the layer's forward.
+    import torch
+
+    import paper_2402_04396_b200 as q8p
+    from conftest import random_artifact
+
+    m, n = 2048, 1024
+    stages = {2: [("e8p-2bit", 1.11)], 3: [("e8p-2bit", 1.02), ("e8-1bit", 0.49)]}[bits]
+    art = random_artifact(m, n, stages, 17 * world + bits)
+    x = torch.randn(2, n, generator=torch.Generator().manual_seed(world)).cuda()
+    full = q8p.Layer.from_qshp(art, device=0)
+    z_full = full.rows_z(x)
+    parts = [q8p.Layer.from_qshp(art, device=0, rows=q8p.shard_rows(m, world, r)).rows_z(x) for r in range(world)]
+    assert torch.equal(torch.cat(parts, dim=1), z_full)
+    _m, _n, _scales, su, _sv = _qshp_signs_scales(art)
+    y = full.forward(x)
+    y_from_z = q8p.rht(z_full, torch.from_numpy(su.copy()).cuda(), transpose=True)
+    rel = float((y_from_z - y).norm() / y.norm())
+    assert rel < 1e-5, rel
