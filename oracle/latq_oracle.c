@@ -11,6 +11,11 @@
  * by tests/test_oracle.py against oracle/_ref, the reference compiled in
  * place, and against the golden fixtures in tests/golden/).
  *
+ * The rfft transform (rfft.cpp) is restated with a direct DFT in place of
+ * FFTW3 (absent): equal to the reference to rounding (~1e-15), pinned
+ * against the reference compiled with oracle/shim/fftw3.h and against the
+ * properties test_rfft.cpp checks (tests/test_oracle.py).
+ *
  * One deliberate extension: the Hadamard registry gains order 172
  * (oracle/had172.h) so n = 11008 = 64 * 172 can be planned; the reference
  * throws SizeError there (core/src/hadamard.cpp:156-168).
@@ -342,8 +347,86 @@ int oracle_side_apply(size_t n, const uint8_t* sign_bytes, double* x, int transp
   return OK;
 }
 
+/* rfft_apply (core/src/rfft.cpp:39-71): pairs (x[2k], x[2k+1]) as complex
+ * c_k; forward: c_k *= e^{i theta_k}, unnormalized forward DFT of length
+ * M = n/2 (FFTW_FORWARD, exponent -2 pi i jk/M), then * 1/sqrt(M); transpose:
+ * unnormalized backward DFT, then * (1/sqrt(M)) e^{-i theta_k}.  FFTW3 (the
+ * reference's dependency, version unpinned, absent here) is restated by the
+ * DFT definition, computed directly in double (O(M^2)); the reference
+ * compiled against oracle/shim/fftw3.h runs the same formula. */
+static void dft_direct(size_t M, double* re, double* im, int sign) {
+  const double two_pi = 6.283185307179586476925286766559;
+  double* c = (double*)malloc(M * sizeof(double));
+  double* s = (double*)malloc(M * sizeof(double));
+  double* r0 = (double*)malloc(M * sizeof(double));
+  double* i0 = (double*)malloc(M * sizeof(double));
+  for (size_t e = 0; e < M; ++e) {
+    const double a = two_pi * (double)e / (double)M;
+    c[e] = cos(a);
+    s[e] = (double)sign * sin(a);
+  }
+  memcpy(r0, re, M * sizeof(double));
+  memcpy(i0, im, M * sizeof(double));
+  for (size_t k = 0; k < M; ++k) {
+    double ar = 0.0, ai = 0.0;
+    size_t e = 0; /* j k mod M */
+    for (size_t j = 0; j < M; ++j) {
+      ar += r0[j] * c[e] - i0[j] * s[e];
+      ai += r0[j] * s[e] + i0[j] * c[e];
+      e += k;
+      if (e >= M) e -= M;
+    }
+    re[k] = ar;
+    im[k] = ai;
+  }
+  free(c);
+  free(s);
+  free(r0);
+  free(i0);
+}
+
+int oracle_rfft_apply(size_t n, const double* phases, double* x, int transpose) {
+  if (n == 0 || n % 2 != 0) return E_SIZE;
+  const size_t M = n / 2;
+  double* re = (double*)malloc(M * sizeof(double));
+  double* im = (double*)malloc(M * sizeof(double));
+  for (size_t k = 0; k < M; ++k) {
+    re[k] = x[2 * k];
+    im[k] = x[2 * k + 1];
+  }
+  const double scale = 1.0 / sqrt((double)M);
+  if (!transpose) {
+    for (size_t k = 0; k < M; ++k) { /* buf[k] *= polar(1, theta) */
+      const double pc = cos(phases[k]), ps = sin(phases[k]);
+      const double r = re[k] * pc - im[k] * ps, i = re[k] * ps + im[k] * pc;
+      re[k] = r;
+      im[k] = i;
+    }
+    dft_direct(M, re, im, -1);
+    for (size_t k = 0; k < M; ++k) {
+      re[k] *= scale;
+      im[k] *= scale;
+    }
+  } else {
+    dft_direct(M, re, im, +1);
+    for (size_t k = 0; k < M; ++k) { /* buf[k] *= scale * polar(1, -theta) */
+      const double pc = scale * cos(-phases[k]), ps = scale * sin(-phases[k]);
+      const double r = re[k] * pc - im[k] * ps, i = re[k] * ps + im[k] * pc;
+      re[k] = r;
+      im[k] = i;
+    }
+  }
+  for (size_t k = 0; k < M; ++k) {
+    x[2 * k] = re[k];
+    x[2 * k + 1] = im[k];
+  }
+  free(re);
+  free(im);
+  return OK;
+}
+
 /* ------------------------------------------------------------------------ */
-/* QSHP v1 parse: core/src/pipeline.cpp:323-383 (rht only; rfft out of scope) */
+/* QSHP v1 parse: core/src/pipeline.cpp:323-383                              */
 /* ------------------------------------------------------------------------ */
 
 typedef struct {
@@ -351,8 +434,11 @@ typedef struct {
   int stages;
   int kind[8]; /* 0 = e8p-2bit, 1 = e8-1bit */
   double scale[8];
+  int transform; /* 0 = rht, 1 = rfft */
   const uint8_t* sign_u;
   const uint8_t* sign_v;
+  const uint8_t* phase_u; /* rfft: m/2 f32 angles (LE) */
+  const uint8_t* phase_v; /* rfft: n/2 f32 angles */
   const uint8_t* codes[8];
 } art_t;
 
@@ -394,13 +480,23 @@ static int parse(const uint8_t* b, size_t len, art_t* a) {
     a->scale[s] = (double)f;
     pos += 4;
   }
-  if (kind != 0) return E_VALIDATION; /* rfft: out of scope */
-  TAKE((a->m + 7) / 8);
-  a->sign_u = b + pos;
-  pos += (a->m + 7) / 8;
-  TAKE((a->n + 7) / 8);
-  a->sign_v = b + pos;
-  pos += (a->n + 7) / 8;
+  a->transform = kind;
+  if (kind == 0) {
+    TAKE((a->m + 7) / 8);
+    a->sign_u = b + pos;
+    pos += (a->m + 7) / 8;
+    TAKE((a->n + 7) / 8);
+    a->sign_v = b + pos;
+    pos += (a->n + 7) / 8;
+  } else { /* read_phases (pipeline.cpp:259-265, 353-357) */
+    if (a->m % 2 != 0 || a->n % 2 != 0) return E_FORMAT;
+    TAKE((size_t)a->m / 2 * 4);
+    a->phase_u = b + pos;
+    pos += (size_t)a->m / 2 * 4;
+    TAKE((size_t)a->n / 2 * 4);
+    a->phase_v = b + pos;
+    pos += (size_t)a->n / 2 * 4;
+  }
   if (a->n % 8 != 0) return E_FORMAT;
   const size_t words = (size_t)a->m * (a->n / 8);
   for (int s = 0; s < a->stages; ++s) {
@@ -412,6 +508,17 @@ static int parse(const uint8_t* b, size_t len, art_t* a) {
   if (pos != len) return E_FORMAT;
   return OK;
 #undef TAKE
+}
+
+/* f32 phases widened to double (PhaseVector keeps f32-exact angles). */
+static double* phases_of(const uint8_t* p, size_t count) {
+  double* out = (double*)malloc((count ? count : 1) * sizeof(double));
+  for (size_t k = 0; k < count; ++k) {
+    float f;
+    memcpy(&f, p + 4 * k, 4);
+    out[k] = (double)f;
+  }
+  return out;
 }
 
 int oracle_artifact_info(const uint8_t* b, size_t len, uint32_t* m, uint32_t* n, int* stages) {
@@ -479,13 +586,22 @@ int oracle_infer(const uint8_t* qshp, size_t len, const double* x, int count, do
   int st = parse(qshp, len, &a);
   if (st) return st;
   size_t p, q;
-  if (oracle_plan_hadamard(a.n, &p, &q) || oracle_plan_hadamard(a.m, &p, &q)) return E_SIZE;
+  double *ph_u = NULL, *ph_v = NULL;
+  if (a.transform == 0) {
+    if (oracle_plan_hadamard(a.n, &p, &q) || oracle_plan_hadamard(a.m, &p, &q)) return E_SIZE;
+  } else {
+    ph_u = phases_of(a.phase_u, a.m / 2);
+    ph_v = phases_of(a.phase_v, a.n / 2);
+  }
   double* t = (double*)malloc(sizeof(double) * a.n);
   if (threads < 1) threads = 1;
   if (threads > 256) threads = 256;
   for (int i = 0; i < count; ++i) {
     memcpy(t, x + (size_t)i * a.n, sizeof(double) * a.n);
-    oracle_side_apply(a.n, a.sign_v, t, 0); /* t = T_v x */
+    if (a.transform == 0)
+      oracle_side_apply(a.n, a.sign_v, t, 0); /* t = T_v x */
+    else
+      oracle_rfft_apply(a.n, ph_v, t, 0);
     double* z = y + (size_t)i * a.m;
     if (threads == 1) {
       rows_dot(&a, t, z, 0, a.m);
@@ -498,9 +614,14 @@ int oracle_infer(const uint8_t* qshp, size_t len, const double* x, int count, do
       }
       for (int k = 0; k < threads; ++k) pthread_join(th[k], NULL);
     }
-    oracle_side_apply(a.m, a.sign_u, z, 1); /* y = T_u^T z */
+    if (a.transform == 0)
+      oracle_side_apply(a.m, a.sign_u, z, 1); /* y = T_u^T z */
+    else
+      oracle_rfft_apply(a.m, ph_u, z, 1);
   }
   free(t);
+  free(ph_u);
+  free(ph_v);
   return OK;
 }
 

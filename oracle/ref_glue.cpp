@@ -8,7 +8,8 @@
 // Everything here forwards to reference functions; the only restated piece
 // is `gen_weights` ("gaussian" branch, proj/core/src/harness.cpp:136-146),
 // because harness.cpp needs nlohmann/json + Eigen::rankUpdate which are not
-// in this image, and the rfft stub (FFTW3 is absent; rfft is out of scope).
+// in this image.  rfft.cpp is compiled unmodified against oracle/shim/fftw3.h
+// (FFTW3 is absent: the shim computes the same unnormalized DFT directly).
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -28,16 +29,6 @@
 #include "latq/rng.hpp"
 #include "latq/rvq.hpp"
 #include "latq/transforms.hpp"
-
-namespace latq {
-// FFTW3 is not available; the RFFT transform is out of scope for this path.
-void rfft_apply(const PhaseVector&, std::span<double>, bool) {
-  throw Error("rfft_apply: FFTW3 not available in the oracle build");
-}
-Eigen::MatrixXd dense_rfft(const PhaseVector&) {
-  throw Error("dense_rfft: FFTW3 not available in the oracle build");
-}
-}  // namespace latq
 
 namespace {
 
@@ -144,7 +135,7 @@ int ref_quantize_layer(const double* w, const double* h, std::uint32_t m, std::u
 // ldlq.cpp nearest_round == block_ldlq under an exactly-identity H,
 // harness.cpp:416-429).  W = gen_weights(m, n, gaussian, substream(10) of
 // `seed`) exactly as `latq quantize` does (latq_cli.cpp:145-148).
-int ref_quantize_hi(std::uint32_t m, std::uint32_t n, int bits, std::uint64_t seed,
+int ref_quantize_hi(std::uint32_t m, std::uint32_t n, int bits, int transform, std::uint64_t seed,
                     int threads, std::uint8_t** out, std::size_t* len) {
   try {
     latq::Rng root(seed);
@@ -153,8 +144,11 @@ int ref_quantize_hi(std::uint32_t m, std::uint32_t n, int bits, std::uint64_t se
     const int g = latq::make_codebook(scheme.front().codebook)->dim();
     if (n % static_cast<std::uint32_t>(g) != 0) throw latq::SizeError("n % 8 != 0");
     latq::Rng sides(seed);
-    const latq::SideTransform left = latq::make_rht_side(m, sides.substream(0));
-    const latq::SideTransform right = latq::make_rht_side(n, sides.substream(1));
+    const bool rht = transform == 0;  // conjugate_layer's make_side (transforms.cpp:137-144)
+    const latq::SideTransform left =
+        rht ? latq::make_rht_side(m, sides.substream(0)) : latq::make_rfft_side(m, sides.substream(0));
+    const latq::SideTransform right =
+        rht ? latq::make_rht_side(n, sides.substream(1)) : latq::make_rfft_side(n, sides.substream(1));
     latq::transform_cols(left, w);
     latq::transform_rows(right, w);
     const double r1 = w.norm() / std::sqrt(static_cast<double>(m) * n);
@@ -170,10 +164,15 @@ int ref_quantize_hi(std::uint32_t m, std::uint32_t n, int bits, std::uint64_t se
     latq::QuantizedLinear a;
     a.m = m;
     a.n = n;
-    a.transform = latq::TransformKind::rht;
+    a.transform = rht ? latq::TransformKind::rht : latq::TransformKind::rfft;
     a.stages = std::move(stages);
-    a.left_signs = left.signs;
-    a.right_signs = right.signs;
+    if (rht) {
+      a.left_signs = left.signs;
+      a.right_signs = right.signs;
+    } else {
+      a.left_phases = left.phases;
+      a.right_phases = right.phases;
+    }
     a.codes = std::move(rounded.codes);
     return emit(latq::serialize(a), out, len);
   } catch (...) {
@@ -355,6 +354,31 @@ int ref_side_apply(std::size_t n, const std::uint8_t* sign_bytes, double* x, int
       side.apply_transpose(std::span<double>(x, n));
     else
       side.apply(std::span<double>(x, n));
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// rfft_apply (rfft.cpp:39-71) on one vector with the given n/2 phases.
+int ref_rfft_apply(std::size_t n, const double* phases, double* x, int transpose) {
+  try {
+    latq::PhaseVector p;
+    p.length = n;
+    p.phases.assign(phases, phases + n / 2);
+    latq::rfft_apply(p, std::span<double>(x, n), transpose != 0);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// Random PhaseVector(length) drawn from Rng(seed) (bitpack.cpp:42-53).
+int ref_random_phases(std::size_t n, std::uint64_t seed, double* out) {
+  try {
+    latq::Rng rng(seed);
+    const latq::PhaseVector p = latq::PhaseVector::random(n, rng);
+    std::memcpy(out, p.phases.data(), sizeof(double) * p.phases.size());
     return 0;
   } catch (...) {
     return map_exception();

@@ -42,7 +42,8 @@ class Ref:
         L.ref_last_error.restype = ctypes.c_char_p
         L.ref_substream_seed.restype = ctypes.c_uint64
         L.ref_substream_seed.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
-        L.ref_quantize_hi.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int, ctypes.c_uint64, ctypes.c_int,
+        L.ref_quantize_hi.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
+                                      ctypes.c_int,
                                       ctypes.POINTER(ctypes.POINTER(ctypes.c_uint8)), ctypes.POINTER(ctypes.c_size_t)]
         L.ref_quantize_layer.argtypes = [_P, _P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_uint64, ctypes.c_int,
@@ -62,6 +63,8 @@ class Ref:
         L.ref_side_apply.argtypes = [ctypes.c_size_t, _P, _P, ctypes.c_int]
         L.ref_gen_weights.argtypes = [ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint64, _P]
         L.ref_random_signs.argtypes = [ctypes.c_size_t, ctypes.c_uint64, _P]
+        L.ref_rfft_apply.argtypes = [ctypes.c_size_t, _P, _P, ctypes.c_int]
+        L.ref_random_phases.argtypes = [ctypes.c_size_t, ctypes.c_uint64, _P]
         L.ref_artifact_info.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_uint32),
                                         ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int)]
         self.L = L
@@ -81,14 +84,16 @@ class Ref:
     def substream_seed(self, seed: int, stream: int) -> int:
         return int(self.L.ref_substream_seed(seed, stream))
 
-    def quantize_hi(self, m: int, n: int, bits: int, seed: int, threads: int = 8) -> bytes:
-        return self._bytes_out(self.L.ref_quantize_hi, m, n, bits, seed, threads)
+    def quantize_hi(self, m: int, n: int, bits: int, seed: int, threads: int = 8, transform: int = 0) -> bytes:
+        """transform 0 = rht, 1 = rfft (TransformKind)."""
+        return self._bytes_out(self.L.ref_quantize_hi, m, n, bits, transform, seed, threads)
 
-    def quantize_layer(self, w: np.ndarray, h: np.ndarray | None, bits: int, seed: int, threads: int = 8) -> bytes:
+    def quantize_layer(self, w: np.ndarray, h: np.ndarray | None, bits: int, seed: int, threads: int = 8,
+                       transform: int = 0) -> bytes:
         w = np.ascontiguousarray(w, dtype=np.float64)
         hp = None if h is None else _ptr(np.ascontiguousarray(h, dtype=np.float64))
         m, n = w.shape
-        return self._bytes_out(self.L.ref_quantize_layer, _ptr(w), hp, m, n, bits, 0, seed, threads)
+        return self._bytes_out(self.L.ref_quantize_layer, _ptr(w), hp, m, n, bits, transform, seed, threads)
 
     def roundtrip(self, data: bytes) -> bytes:
         return self._bytes_out(self.L.ref_roundtrip, data, len(data))
@@ -166,6 +171,18 @@ class Ref:
         self._ck(self.L.ref_gen_weights(m, n, seed, _ptr(w)))
         return w
 
+    def rfft_apply(self, phases: np.ndarray, x: np.ndarray, transpose: bool = False) -> np.ndarray:
+        y = np.ascontiguousarray(x, dtype=np.float64).copy()
+        ph = np.ascontiguousarray(phases, dtype=np.float64)
+        assert ph.size == y.size // 2
+        self._ck(self.L.ref_rfft_apply(y.size, _ptr(ph), _ptr(y), int(transpose)))
+        return y
+
+    def random_phases(self, n: int, seed: int) -> np.ndarray:
+        out = np.zeros(n // 2)
+        self._ck(self.L.ref_random_phases(n, seed, _ptr(out)))
+        return out
+
     def random_signs(self, n: int, seed: int) -> np.ndarray:
         out = np.zeros((n + 7) // 8, dtype=np.uint8)
         self.L.ref_random_signs(n, seed, _ptr(out))
@@ -191,6 +208,7 @@ class Oracle:
                                            ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int)]
         L.oracle_infer.argtypes = [ctypes.c_char_p, ctypes.c_size_t, _P, ctypes.c_int, _P, ctypes.c_int]
         L.oracle_decode_stage.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_int, _P]
+        L.oracle_rfft_apply.argtypes = [ctypes.c_size_t, _P, _P, ctypes.c_int]
         self.L = L
 
     @staticmethod
@@ -239,6 +257,13 @@ class Oracle:
         y = np.ascontiguousarray(x, dtype=np.float64).copy()
         s = np.ascontiguousarray(signs, dtype=np.uint8)
         self._ck(self.L.oracle_side_apply(y.size, _ptr(s), _ptr(y), int(transpose)))
+        return y
+
+    def rfft_apply(self, phases: np.ndarray, x: np.ndarray, transpose: bool = False) -> np.ndarray:
+        y = np.ascontiguousarray(x, dtype=np.float64).copy()
+        ph = np.ascontiguousarray(phases, dtype=np.float64)
+        assert ph.size == y.size // 2
+        self._ck(self.L.oracle_rfft_apply(y.size, _ptr(ph), _ptr(y), int(transpose)))
         return y
 
     def artifact_info(self, data: bytes) -> tuple[int, int, int]:
