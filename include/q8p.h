@@ -46,7 +46,7 @@ typedef enum {
   Q8P_ERR_BAD_MAGIC = 4,           /* latq::BadMagicError */
   Q8P_ERR_UNSUPPORTED_VERSION = 5, /* latq::UnsupportedVersionError */
   Q8P_ERR_TRUNCATED = 6,           /* latq::TruncatedArtifactError */
-  Q8P_ERR_UNSUPPORTED = 7,         /* valid artifact, not on this path (e.g. rfft transform) */
+  Q8P_ERR_UNSUPPORTED = 7,         /* valid artifact, not on this path (e.g. > 2 RVQ stages) */
   Q8P_ERR_CUDA = 8,                /* CUDA runtime failure / no sm_100 device */
   Q8P_ERR_NCCL = 9,
   Q8P_ERR_INTERNAL = 10
@@ -66,11 +66,13 @@ typedef struct {
 
 typedef struct {
   uint32_t m, n;                 /* W is m x n; x has n entries, y has m */
-  int transform;                 /* 0 = rht (TransformKind::rht); rfft is not supported */
+  int transform;                 /* TransformKind: 0 = rht, 1 = rfft (transforms.hpp) */
   int num_stages;                /* 1 (2-bit) or 2 (3-/4-bit RVQ) */
   const q8p_stage_desc* stages;
-  const uint8_t* signs_u;        /* left_signs, ceil(m/8) bytes, LSB-first, bit set = -1 */
-  const uint8_t* signs_v;        /* right_signs, ceil(n/8) bytes */
+  const uint8_t* signs_u;        /* rht: left_signs, ceil(m/8) bytes, LSB-first, bit set = -1 */
+  const uint8_t* signs_v;        /* rht: right_signs, ceil(n/8) bytes */
+  const float* phases_u;         /* rfft: left_phases, m/2 angles (PhaseVector, f32 as serialized) */
+  const float* phases_v;         /* rfft: right_phases, n/2 angles */
 } q8p_layer_desc;
 
 typedef struct {

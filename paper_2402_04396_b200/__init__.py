@@ -91,7 +91,8 @@ class StageDesc(ctypes.Structure):
 
 LayerDesc._fields_ = [("m", ctypes.c_uint32), ("n", ctypes.c_uint32), ("transform", ctypes.c_int),
                       ("num_stages", ctypes.c_int), ("stages", ctypes.POINTER(StageDesc)),
-                      ("signs_u", ctypes.c_void_p), ("signs_v", ctypes.c_void_p)]
+                      ("signs_u", ctypes.c_void_p), ("signs_v", ctypes.c_void_p),
+                      ("phases_u", ctypes.c_void_p), ("phases_v", ctypes.c_void_p)]
 
 
 class ForwardOpts(ctypes.Structure):
@@ -283,8 +284,10 @@ class Layer:
 
     @classmethod
     def create(cls, m: int, n: int, stages: Sequence[tuple[int, float, np.ndarray]],
-               signs_u: np.ndarray, signs_v: np.ndarray, device: int = 0) -> "Layer":
-        """q8p_layer_create from raw fields: stages = [(codebook, scale, codes)]."""
+               signs_u: np.ndarray | None = None, signs_v: np.ndarray | None = None, device: int = 0,
+               phases_u: np.ndarray | None = None, phases_v: np.ndarray | None = None) -> "Layer":
+        """q8p_layer_create from raw fields: stages = [(codebook, scale, codes)];
+        sign bytes (rht) or f32 phase angles (rfft, m/2 and n/2 of them)."""
         st = (StageDesc * len(stages))()
         keep = []
         for i, (cb, scale, codes) in enumerate(stages):
@@ -294,9 +297,17 @@ class Layer:
             st[i].scale = scale
             st[i].codes = codes.ctypes.data
             st[i].code_bytes = codes.dtype.itemsize
-        su = np.ascontiguousarray(signs_u, dtype=np.uint8)
-        sv = np.ascontiguousarray(signs_v, dtype=np.uint8)
-        d = LayerDesc(m, n, 0, len(stages), st, su.ctypes.data, sv.ctypes.data)
+        rfft = phases_u is not None or phases_v is not None
+        if rfft:
+            pu = np.ascontiguousarray(phases_u, dtype=np.float32)
+            pv = np.ascontiguousarray(phases_v, dtype=np.float32)
+            keep += [pu, pv]
+            d = LayerDesc(m, n, 1, len(stages), st, None, None, pu.ctypes.data, pv.ctypes.data)
+        else:
+            su = np.ascontiguousarray(signs_u, dtype=np.uint8)
+            sv = np.ascontiguousarray(signs_v, dtype=np.uint8)
+            keep += [su, sv]
+            d = LayerDesc(m, n, 0, len(stages), st, su.ctypes.data, sv.ctypes.data, None, None)
         h = ctypes.c_void_p()
         _check(lib().q8p_layer_create(ctypes.byref(d), device, ctypes.byref(h)))
         return cls(h.value)

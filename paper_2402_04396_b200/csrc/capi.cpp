@@ -121,17 +121,38 @@ void setup_side(q8p_layer* L, DevSide& side, std::uint32_t n, const std::uint8_t
   side.colsum = static_cast<const float*>(upload(L, colsum.data(), colsum.size() * 4));
 }
 
+// rfft side (rfft.cpp): DFT factorization + rotor / twiddle tables.
+void setup_side_rfft(q8p_layer* L, DevSide& side, std::uint32_t n, const float* phases, bool codewords) {
+  side.kind = 1;
+  side.n = n;
+  if (!rfft_factor(n, codewords, side.M1, side.M2))
+    throw UnsupportedError("rfft: DFT length " + std::to_string(n / 2) + " has no factorization the kernels fit");
+  std::vector<float> rot, tw;
+  rfft_tables(n, phases, rot, tw);
+  side.rot = static_cast<const float2*>(upload(L, rot.data(), rot.size() * 4));
+  side.tw = static_cast<const float2*>(upload(L, tw.data(), tw.size() * 4));
+}
+
 // Builds a device layer from host fields for rows [r0, r1).
 q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t r1, int device) {
   if (!d.stages || d.num_stages < 1) throw ValidationError("artifact has no quantization stages");
   if (d.num_stages > 2) throw UnsupportedError("more than two RVQ stages are not on this path");
-  if (d.transform != 0) throw UnsupportedError("rfft transform is not on this path");
+  if (d.transform != 0 && d.transform != 1) throw ValidationError("unknown transform kind");
+  const bool rfft = d.transform == 1;
   if (d.m == 0 || d.n == 0) throw SizeError("empty layer");
   if (d.n % 8 != 0) throw FormatError("artifact: n not divisible by codeword dimension");
   if (!(r0 < r1 && r1 <= d.m)) throw ValidationError("row range out of bounds");
-  if (!d.signs_u || !d.signs_v) throw ValidationError("sign vectors required");
-  plan_hadamard(d.n);  // SizeError before any allocation
-  plan_hadamard(d.m);
+  if (rfft) {
+    if (!d.phases_u || !d.phases_v) throw ValidationError("phase vectors required");
+    if (d.m % 2 != 0) throw SizeError("rfft_apply: length must be even and positive");  // rfft.cpp:41-42
+    std::uint32_t a, b;
+    if (!rfft_factor(d.n, true, a, b) || !rfft_factor(d.m, false, a, b))
+      throw UnsupportedError("rfft: DFT length has no factorization the kernels fit");
+  } else {
+    if (!d.signs_u || !d.signs_v) throw ValidationError("sign vectors required");
+    plan_hadamard(d.n);  // SizeError before any allocation
+    plan_hadamard(d.m);
+  }
   require_sm100(device);
   DeviceGuard g(device);
   auto L = std::make_unique<q8p_layer>();
@@ -142,8 +163,13 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
   L->row_end = r1;
   L->num_stages = d.num_stages;
   try {
-    setup_side(L.get(), L->side_u, d.m, d.signs_u);
-    setup_side(L.get(), L->side_v, d.n, d.signs_v);
+    if (rfft) {
+      setup_side_rfft(L.get(), L->side_u, d.m, d.phases_u, false);
+      setup_side_rfft(L.get(), L->side_v, d.n, d.phases_v, true);
+    } else {
+      setup_side(L.get(), L->side_u, d.m, d.signs_u);
+      setup_side(L.get(), L->side_v, d.n, d.signs_v);
+    }
     {
       const std::vector<std::uint8_t> img = tc_lut_image();
       L->lut_img = static_cast<const std::uint8_t*>(upload(L.get(), img.data(), img.size()));
@@ -201,7 +227,6 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
 q8p_layer* layer_from_bytes(const std::uint8_t* bytes, std::size_t len, std::uint32_t r0,
                             std::uint32_t r1, bool full, int device) {
   const QuantizedLinear a = deserialize(std::span(bytes, len));
-  if (a.transform != TransformKind::rht) throw UnsupportedError("rfft transform is not on this path");
   std::vector<q8p_stage_desc> st(a.stages.size());
   for (std::size_t s = 0; s < st.size(); ++s) {
     codebook_code_bytes(a.stages[s].codebook);
@@ -213,11 +238,13 @@ q8p_layer* layer_from_bytes(const std::uint8_t* bytes, std::size_t len, std::uin
   q8p_layer_desc d{};
   d.m = a.m;
   d.n = a.n;
-  d.transform = 0;
+  d.transform = a.transform == TransformKind::rht ? 0 : 1;
   d.num_stages = static_cast<int>(st.size());
   d.stages = st.data();
   d.signs_u = a.left_signs.bytes().data();
   d.signs_v = a.right_signs.bytes().data();
+  d.phases_u = a.left_phases.data();
+  d.phases_v = a.right_phases.data();
   if (full) {
     r0 = 0;
     r1 = a.m;
@@ -315,6 +342,11 @@ void forward_local(const q8p_layer* L, const float* x, int batch, const Workspac
     if (opts) record_event(opts->gemv_start_event, s);
     launch_gemv_tc(*L, w.bimg, w.zacc, w.rows_pad, batch, s);
     if (opts) record_event(opts->gemv_end_event, s);
+  } else if (L->side_v.kind == 1) {  // rfft (kernels_rfft.cu): t = T_v x through the scratch
+    launch_rht_in(L->side_v, x, w.t, w.u, nullptr, nullptr, nullptr, 0, batch, s);
+    if (opts) record_event(opts->gemv_start_event, s);
+    launch_gemv_simple(*L, w.t, w.z, batch, static_cast<int>(L->m), s);
+    if (opts) record_event(opts->gemv_end_event, s);
   } else {
     launch_rht(L->side_v, x, w.t, batch, /*transpose=*/false, s);  // t = T_v x
     if (opts) record_event(opts->gemv_start_event, s);
@@ -401,7 +433,10 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
     }
   } else {
     forward_local(L, x, batch, w, s, opts);
-    launch_rht(L->side_u, w.z, y, batch, /*transpose=*/true, s);  // y = T_u^T z
+    if (L->side_u.kind == 1)
+      launch_rht_out(L->side_u, w.z, w.u, y, batch, s);  // rfft
+    else
+      launch_rht(L->side_u, w.z, y, batch, /*transpose=*/true, s);  // y = T_u^T z
   }
 }
 

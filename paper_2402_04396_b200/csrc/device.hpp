@@ -52,12 +52,17 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" :::); }
 #endif
 
-// One side of the randomized Hadamard transform on device.
+// One side transform on device: randomized Hadamard (kind 0) or rfft (kind 1).
 struct DevSide {
+  int kind = 0;                         // TransformKind: 0 = rht, 1 = rfft
   std::uint32_t n = 0, p = 1, q = 1;
   const std::uint8_t* signs = nullptr;  // ceil(n/8) bytes
   const std::int8_t* base = nullptr;    // q x q (+-1), nullptr when q == 1
   const float* colsum = nullptr;        // q column sums of the base (sum_i t_i in closed form)
+  // rfft (kernels_rfft.cu): DFT length M = n / 2 = M1 * M2
+  std::uint32_t M1 = 1, M2 = 1;
+  const float2* rot = nullptr;          // [M] e^{i theta_k}
+  const float2* tw = nullptr;           // [M] e^{-2 pi i e / M}
 };
 
 // Tensor-core GEMV slab records (gemv_tc.cu): [row block][k slab][slab bytes].
@@ -145,6 +150,19 @@ void launch_layer_fused(const q8p_layer& L, const float* x, float* y, float* u_s
 void launch_combine_acc(const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows, std::uint32_t zacc_cols,
                         const float zscale[2], const int ze8p[2], const float* alpha, const long long* tl, float* z,
                         std::uint32_t m_local, int batch, cudaStream_t s);
+// rfft side transform (kernels_rfft.cu): factorization M = n / 2 = M1 * M2
+// (`codewords`: M2 % 4 == 0 so K1 can emit whole codewords; false if no
+// factorization fits the kernels), host tables (rot = e^{i theta}, tw =
+// e^{-2 pi i e / M}, interleaved float pairs), fp32 apply / apply_transpose
+// through `u_scratch` ([batch][n] floats), and K1's limb flavour.
+bool rfft_factor(std::uint32_t n, bool codewords, std::uint32_t& M1, std::uint32_t& M2);
+void rfft_tables(std::uint32_t n, const float* phases, std::vector<float>& rot, std::vector<float>& tw);
+void launch_rfft_f32(const DevSide& side, const float* x, float* u_scratch, float* y, int batch, bool transpose,
+                     cudaStream_t s);
+void launch_rfft_in_limbs(const DevSide& side, const float* x, float* u_scratch, float* ssq, float* alpha,
+                          long long* tl, std::uint8_t* bimg, std::uint32_t b_bytes, std::uint32_t bcols,
+                          std::uint8_t* bimg_tail, std::size_t tail_bytes, std::int32_t* zero_ptr,
+                          std::size_t zero_words, int batch, cudaStream_t s);
 // K3 (fp32 input): y = T_u^T z.
 void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, float* y, int batch, cudaStream_t s);
 // K3 (accumulator input): z = sum_s zscale_s alpha (2 Z_s - [E8P] TL) / 4 from the int32

@@ -947,6 +947,7 @@ bool tc_fused_supported(const q8p_layer& L, int batch) {
   // pipeline (grid barriers under a saturated memory system) -> opt-in
   static const bool on = std::getenv("Q8P_FUSE") != nullptr;
   if (!on || !tc_supported(L, batch) || tc_ncols_pad(4 * batch) != 8 || L.gbar == nullptr) return false;
+  if (L.side_u.kind != 0 || L.side_v.kind != 0) return false;  // rht only
   // RHT scratch must leave a useful code ring
   const std::size_t scr = std::max({rht_p1_smem_bytes(L.side_v), rht_p2_smem_bytes(L.side_v),
                                     rht_p1_smem_bytes(L.side_u), rht_p2_smem_bytes(L.side_u)});

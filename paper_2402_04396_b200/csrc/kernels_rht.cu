@@ -640,6 +640,11 @@ std::size_t rht_p2_smem_bytes(const DevSide& side) {
 void launch_rht_in(const DevSide& side, const float* x, float* t, float* u_scratch, float* amax, float* tsum,
                    std::int32_t* zero_ptr, std::size_t zero_words, int batch, cudaStream_t s) {
   if (batch <= 0) return;
+  if (side.kind == 1) {
+    if (amax || tsum) throw UnsupportedError("rfft: amax / tsum outputs are rht-only");
+    launch_rfft_f32(side, x, u_scratch, t, batch, false, s);
+    return;
+  }
   RhtArgs a{};
   plan_split_impl(side, a);
   a.signs = side.signs;
@@ -660,6 +665,10 @@ void launch_rht_in(const DevSide& side, const float* x, float* t, float* u_scrat
 
 void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, float* y, int batch, cudaStream_t s) {
   if (batch <= 0) return;
+  if (side.kind == 1) {
+    launch_rfft_f32(side, zin, u_scratch, y, batch, true, s);
+    return;
+  }
   RhtArgs a{};
   plan_split_impl(side, a);
   a.signs = side.signs;
@@ -686,6 +695,11 @@ void launch_rht_in_limbs(const DevSide& side, const float* x, float* u_scratch, 
                          std::uint8_t* bimg_tail, std::size_t tail_bytes, std::int32_t* zero_ptr,
                          std::size_t zero_words, int batch, cudaStream_t s) {
   if (batch <= 0) return;
+  if (side.kind == 1) {
+    launch_rfft_in_limbs(side, x, u_scratch, ssq, alpha, tl, bimg, b_bytes, bcols, bimg_tail, tail_bytes, zero_ptr,
+                         zero_words, batch, s);
+    return;
+  }
   RhtArgs a{};
   plan_split_impl(side, a);
   a.signs = side.signs;
@@ -720,6 +734,11 @@ void launch_rht_out_acc(const DevSide& side, const std::int32_t* zacc, int zacc_
                         std::uint32_t zacc_cols, const float zscale[2], const int ze8p[2], const float* alpha,
                         const long long* tl, float* u_scratch, float* y, int batch, cudaStream_t s) {
   if (batch <= 0) return;
+  if (side.kind == 1) {  // rfft: z (into y) from the accumulators, then the two DFT passes y -> u -> y
+    launch_combine_acc(zacc, zacc_stages, zacc_rows, zacc_cols, zscale, ze8p, alpha, tl, y, side.n, batch, s);
+    launch_rfft_f32(side, y, u_scratch, y, batch, true, s);
+    return;
+  }
   RhtArgs a{};
   plan_split_impl(side, a);
   a.signs = side.signs;

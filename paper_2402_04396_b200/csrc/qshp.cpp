@@ -228,7 +228,6 @@ void throw_status(q8p_status s) {
 // ---- DeviceLayer -----------------------------------------------------------
 namespace {
 q8p_layer* make_from(const QuantizedLinear& a, int device) {
-  if (a.transform != TransformKind::rht) throw UnsupportedError("rfft transform is not on this path");
   std::vector<q8p_stage_desc> st(a.stages.size());
   for (std::size_t s = 0; s < st.size(); ++s) {
     st[s].codebook = a.stages[s].codebook == "e8p-2bit" ? Q8P_CB_E8P_2BIT : Q8P_CB_E8_1BIT;
@@ -240,13 +239,20 @@ q8p_layer* make_from(const QuantizedLinear& a, int device) {
   q8p_layer_desc d{};
   d.m = a.m;
   d.n = a.n;
-  d.transform = 0;
+  d.transform = a.transform == TransformKind::rht ? 0 : 1;
   d.num_stages = static_cast<int>(st.size());
   d.stages = st.data();
-  d.signs_u = a.left_signs.bytes().data();
-  d.signs_v = a.right_signs.bytes().data();
-  if (a.left_signs.size() != a.m || a.right_signs.size() != a.n)
-    throw SizeError("sign vector lengths disagree with m, n");
+  if (a.transform == TransformKind::rht) {
+    d.signs_u = a.left_signs.bytes().data();
+    d.signs_v = a.right_signs.bytes().data();
+    if (a.left_signs.size() != a.m || a.right_signs.size() != a.n)
+      throw SizeError("sign vector lengths disagree with m, n");
+  } else {
+    d.phases_u = a.left_phases.data();
+    d.phases_v = a.right_phases.data();
+    if (a.left_phases.size() != a.m / 2 || a.right_phases.size() != a.n / 2)
+      throw SizeError("phase vector lengths disagree with m, n");
+  }
   q8p_layer* l = nullptr;
   check(q8p_layer_create(&d, device, &l));
   return l;

@@ -65,15 +65,20 @@ def rel_err(a, b) -> float:
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
-def random_artifact(m, n, stages, seed, codes=None):
-    """A structurally valid QSHP artifact with random codes (acceptance.cpp:438-450 style)."""
+def random_artifact(m, n, stages, seed, codes=None, transform=0):
+    """A structurally valid QSHP artifact with random codes (acceptance.cpp:438-450 style);
+    transform 0 = rht (random sign bytes), 1 = rfft (random f32 phases in [0, 2 pi))."""
     import struct
     rng = np.random.default_rng(seed)
-    body = b"QSHP" + struct.pack("<HIIBB", 1, m, n, 0, len(stages))
+    body = b"QSHP" + struct.pack("<HIIBB", 1, m, n, transform, len(stages))
     for cid, scale in stages:
         body += bytes([len(cid)]) + cid.encode() + struct.pack("<f", scale)
-    body += rng.integers(0, 256, (m + 7) // 8, dtype=np.uint8).tobytes()
-    body += rng.integers(0, 256, (n + 7) // 8, dtype=np.uint8).tobytes()
+    if transform == 0:
+        body += rng.integers(0, 256, (m + 7) // 8, dtype=np.uint8).tobytes()
+        body += rng.integers(0, 256, (n + 7) // 8, dtype=np.uint8).tobytes()
+    else:
+        body += rng.uniform(0, 2 * np.pi, m // 2).astype("<f4").tobytes()
+        body += rng.uniform(0, 2 * np.pi, n // 2).astype("<f4").tobytes()
     words = m * n // 8
     for s, (cid, _) in enumerate(stages):
         if codes is not None and codes[s] is not None:

@@ -18,7 +18,7 @@ TIGHT = 1e-4      # acceptance.cpp:426 criterion-10 bound
 # The tensor-core path (batch <= 16) carries activations as integers
 # t = alpha * Lt with 4 int8 limbs (25-bit values, alpha a power of two >= |x|_2 / 2^25):
 # per-element error <= |x|_2 / 2^25, ~1e-7..1e-6 relative on outputs.  Batch > 16 runs
-# the portable fp32 path.
+# as 16-vector chunks through the same path.
 TC = 1e-5
 
 

@@ -99,7 +99,7 @@ def test_row_sharded_decomposition_gloo(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["e8p2_1024x1024", "rvq3_256x128", "rvq4_128x128"])
+@pytest.mark.parametrize("name", ["e8p2_1024x1024", "rvq3_256x128", "rvq4_128x128", "rfft2_344x512"])
 def test_forward_sharded_world1_bit_exact(name):
     import torch
 
