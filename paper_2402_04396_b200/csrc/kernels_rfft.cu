@@ -35,7 +35,7 @@
 namespace q8p::detail {
 namespace {
 
-constexpr std::size_t kMaxSmem = 227 * 1024;
+constexpr std::size_t kMaxSmem = 216 * 1024;  // dynamic smem cap (227 KB less static smem)
 constexpr int kP1Threads = 256, kP2Threads = 128;
 
 struct RfftArgs {
