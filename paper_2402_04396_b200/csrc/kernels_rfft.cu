@@ -216,13 +216,16 @@ void plan(const DevSide& side, RfftArgs& a) {
   a.TJ = std::min<std::uint32_t>(8, a.M1);
   while (a.TJ > 1 && smem1_of(a.M2, a.TJ) > kMaxSmem) a.TJ /= 2;
   a.tiles1 = (a.M1 + a.TJ - 1) / a.TJ;
-  // split the outputs so no CTA does more than ~2^17 complex MACs
-  const std::uint64_t w1 = std::uint64_t(a.M2) * a.M2 * a.TJ;
-  a.ks1 = std::uint32_t(std::min<std::uint64_t>(a.M2, std::max<std::uint64_t>(1, (w1 + (1u << 17) - 1) >> 17)));
+  // split the outputs so each pass has >= ~128 CTAs per vector and no CTA does
+  // more than ~2^13 complex MACs (latency: the transform is a few us of the step)
+  auto split = [](std::uint64_t work, std::uint32_t units, std::uint32_t cap) {
+    const std::uint64_t k = std::max<std::uint64_t>((work + 8191) >> 13, (128 + units - 1) / units);
+    return std::uint32_t(std::min<std::uint64_t>(cap, std::max<std::uint64_t>(1, k)));
+  };
+  a.ks1 = split(std::uint64_t(a.M2) * a.M2 * a.TJ, a.tiles1, a.M2);
   a.R = a.M2 % 4 == 0 ? 4 : 1;
   a.groups2 = (a.M2 + a.R - 1) / a.R;
-  const std::uint64_t w2 = std::uint64_t(a.R) * a.M1 * a.M1;
-  a.ks2 = std::uint32_t(std::min<std::uint64_t>(a.M1, std::max<std::uint64_t>(1, (w2 + (1u << 16) - 1) >> 16)));
+  a.ks2 = split(std::uint64_t(a.R) * a.M1 * a.M1, a.groups2, a.M1);
 }
 
 void set_smem_attrs() {
