@@ -9,8 +9,11 @@ each layer y = S_U H^T W_hat H S_V x (K1 -> K2 -> K3).
   value    tokens/s of the layer set, inputs already in HBM (CUDA graph of
            the step, replayed K times, CUDA events on the launching stream,
            max over ranks).
-  e2e      the same metric through the public per-layer API with HOST
-           buffers: H2D of x and D2H of y inside the timed region.
+  e2e      the same metric through the public API with HOST buffers: per
+           step one q8p_forward_set_host call (H2D of every layer's x, the
+           layer forwards, D2H of every y, stream sync; pinned buffers, so the
+           library replays the step as one cached CUDA graph).  Sharded runs
+           loop q8p_forward_sharded per layer between the two copies.
   roofline the decode-GEMV kernel (K2): algorithmic bytes
            (codes + 4 B x activations in + 4 B x outputs)
            / average kernel time from CUDA events recorded around K2.
@@ -307,20 +310,28 @@ def run_ours(args):
     xv = [dx[xo[i]:xo[i + 1]].view(B, n) for i, (_, n) in enumerate(layers)]
     yv = [dy[yo[i]:yo[i + 1]].view(B, m) for i, (m, _) in enumerate(layers)]
     h2d, d2h = 4 * B * nsum, 4 * B * msum
+    sets = None if sharded else [q8p.LayerSet(row) for row in copies]
+    ws_set = None if sharded else torch.empty(max(S.workspace_bytes(B) for S in sets), dtype=torch.uint8, device=dev)
+
+    def e2e_step(c):
+        if sharded:
+            dx.copy_(hx, non_blocking=True)
+            for li, L in enumerate(copies[c]):
+                L.forward_sharded(xv[li], comm, out=yv[li], stream=stream, workspace=ws)
+            hy.copy_(dy, non_blocking=True)
+            stream.synchronize()
+        else:
+            sets[c].forward_host(hx, hy, B, stream=stream, workspace=ws_set)
+
+    with torch.cuda.stream(stream):
+        for c in range(args.copies):  # warm-up (the set path captures its graphs here)
+            e2e_step(c)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         e0.record(stream)
         for s in range(args.steps):
-            c = s % args.copies
-            dx.copy_(hx, non_blocking=True)
-            for li, L in enumerate(copies[c]):
-                if sharded:
-                    L.forward_sharded(xv[li], comm, out=yv[li], stream=stream, workspace=ws)
-                else:
-                    L.forward(xv[li], out=yv[li], stream=stream, workspace=ws)
-            hy.copy_(dy, non_blocking=True)
-            stream.synchronize()
+            e2e_step(s % args.copies)
         e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps

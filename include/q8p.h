@@ -147,6 +147,25 @@ q8p_status q8p_forward_sharded(const q8p_layer* layer, const float* x, float* y,
                                void* workspace, size_t workspace_bytes, void* nccl_comm,
                                void* stream);
 
+/* Layer sets: `count` independent forwards y_i = W_i x_i in one call (one
+ * decode step through a model's linear layers), stream-ordered, sharing one
+ * workspace of q8p_forward_set_workspace_bytes(...) bytes (the largest layer's
+ * q8p_workspace_bytes plus staging for the host variant).  No reference
+ * counterpart: the reference loops `infer` per layer (latq_cli.cpp:211-212). */
+size_t q8p_forward_set_workspace_bytes(const q8p_layer* const* layers, int count, int batch);
+/* Device buffers: x[i] fp32 [batch][n_i], y[i] fp32 [batch][m_i]. */
+q8p_status q8p_forward_set(const q8p_layer* const* layers, int count, const float* const* x,
+                           float* const* y, int batch, void* workspace, size_t workspace_bytes,
+                           void* stream);
+/* Host buffers: x_host = the inputs concatenated [i][batch][n_i], y_host = the
+ * outputs concatenated [i][batch][m_i].  Copies in, runs every layer, copies
+ * out and synchronizes `stream`.  With pinned host buffers the whole step is
+ * captured once per (layers, x_host, y_host, batch, workspace) into a CUDA
+ * graph and replayed (one host launch per step). */
+q8p_status q8p_forward_set_host(const q8p_layer* const* layers, int count, const float* x_host,
+                                float* y_host, int batch, void* workspace, size_t workspace_bytes,
+                                void* stream);
+
 /* latq::infer drop-in: host f64 x [batch][n] -> host f64 y [batch][m].
  * Synchronous; stages through an internal pinned buffer and workspace. */
 q8p_status q8p_infer_host(q8p_layer* layer, const double* x, double* y, int batch);

@@ -18,7 +18,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 __all__ = [
-    "Error", "SizeError", "ValidationError", "FormatError", "BadMagicError",
+    "LayerSet", "Error", "SizeError", "ValidationError", "FormatError", "BadMagicError",
     "UnsupportedVersionError", "TruncatedArtifactError", "UnsupportedError", "DeviceError",
     "lib", "plan_hadamard", "hadamard_base", "codebook_table", "e8p_decode_host",
     "inspect_artifact", "reserialize", "Layer", "rht", "kernel_launches",
@@ -129,6 +129,11 @@ _SIGNATURES = {
     "q8p_forward_rows_z": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "q8p_forward_sharded": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]),
     "q8p_infer_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
+    "q8p_forward_set_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
+    "q8p_forward_set": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                       ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "q8p_forward_set_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                            ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "q8p_decode_stage": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
     "q8p_rht": (ctypes.c_int, [ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
     "q8p_qshp_inspect": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ArtifactInfo)]),
@@ -418,6 +423,61 @@ class Layer:
                         device=f"cuda:{info['device']}")
         _check(lib().q8p_decode_stage(self._h, stage, w.data_ptr(), _stream_ptr(stream)))
         return w
+
+
+class LayerSet:
+    """Independent layer forwards per call (q8p_forward_set / _host): one decode
+    step through a model's linear layers."""
+
+    def __init__(self, layers: Sequence[Layer]):
+        self.layers = list(layers)  # keeps the handles alive
+        self._arr = (ctypes.c_void_p * len(self.layers))(*[L._h.value for L in self.layers])
+        self._ws = None
+        self._nsum = sum(L._dims()[1] for L in self.layers)
+        self._msum = sum(L._dims()[0] for L in self.layers)
+
+    def workspace_bytes(self, batch: int) -> int:
+        return int(lib().q8p_forward_set_workspace_bytes(self._arr, len(self.layers), batch))
+
+    def workspace(self, batch: int):
+        torch = _torch()
+        need = self.workspace_bytes(batch)
+        if self._ws is None or self._ws.numel() < need:
+            dev = self.layers[0].info["device"]
+            self._ws = torch.empty(need, dtype=torch.uint8, device=f"cuda:{dev}")
+        return self._ws
+
+    def forward(self, xs, outs=None, stream=None, workspace=None):
+        """xs: [batch, n_i] fp32 CUDA tensors -> [batch, m_i] tensors."""
+        torch = _torch()
+        batch = xs[0].shape[0]
+        if outs is None:
+            outs = [torch.empty(batch, L._dims()[0], dtype=torch.float32, device=x.device)
+                    for L, x in zip(self.layers, xs)]
+        for L, x, y in zip(self.layers, xs, outs):
+            if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous() or x.shape != (batch, L._dims()[1]):
+                raise ValidationError("xs[i] must be contiguous float32 CUDA [batch, n_i]")
+            if y.shape != (batch, L._dims()[0]) or not y.is_contiguous():
+                raise ValidationError("outs[i] must be contiguous [batch, m_i]")
+        xp = (ctypes.c_void_p * len(xs))(*[x.data_ptr() for x in xs])
+        yp = (ctypes.c_void_p * len(outs))(*[y.data_ptr() for y in outs])
+        ws = workspace if workspace is not None else self.workspace(batch)
+        _check(lib().q8p_forward_set(self._arr, len(self.layers), xp, yp, batch, ws.data_ptr(), ws.numel(),
+                                     _stream_ptr(stream)))
+        return outs
+
+    def forward_host(self, x_host, y_host, batch: int, stream=None, workspace=None):
+        """Host fp32 buffers (torch CPU tensors, pinned for the graph path):
+        x_host = inputs concatenated [i][batch][n_i], y_host = outputs [i][batch][m_i].
+        Returns when y_host holds the results."""
+        if x_host.numel() < batch * self._nsum or y_host.numel() < batch * self._msum:
+            raise SizeError("host buffers too small for the layer set")
+        ws = workspace if workspace is not None else self.workspace(batch)
+        st = lib().q8p_forward_set_host(self._arr, len(self._arr), x_host.data_ptr(), y_host.data_ptr(), batch,
+                                        ws.data_ptr(), ws.numel(), _stream_ptr(stream))
+        if st:
+            _check(st)
+        return y_host
 
 
 def rht(x, signs, transpose: bool = False, out=None, stream=None):

@@ -493,6 +493,211 @@ void forward_cached(q8p_layer* L, const float* x, float* y, int batch, void* ws,
   cuda_check(cudaGraphLaunch(exec, s), "graph launch");
 }
 
+// ---- layer sets (q8p_forward_set / q8p_forward_set_host) ------------------
+// Several independent layer forwards per call (one decode step through a
+// model's linear layers).  The host variant stages the concatenated inputs /
+// outputs through the tail of the workspace and, when the host buffers are
+// pinned, replays the whole step (H2D, every layer's kernel chain with its PDL
+// edges, D2H) as ONE cached CUDA graph: one host launch per step.
+struct SetGraph {
+  std::vector<const q8p_layer*> layers;
+  const float* xh;
+  float* yh;
+  int batch;
+  void* ws;
+  std::size_t ws_bytes;
+  int device;
+  cudaGraphExec_t exec;
+  std::uint64_t kernels;
+};
+std::mutex g_set_mu;
+std::vector<SetGraph> g_set_graphs;
+cudaStream_t g_set_capture[64] = {};
+
+std::size_t set_stage_offset(const q8p_layer* const* layers, int count, int batch) {
+  std::size_t ws = 0;
+  for (int i = 0; i < count; ++i) ws = std::max(ws, workspace_size(layers[i], batch));
+  return round_up(ws, 256);
+}
+std::size_t set_workspace_size(const q8p_layer* const* layers, int count, int batch) {
+  std::size_t io = 0;
+  for (int i = 0; i < count; ++i) io += std::size_t(batch) * (layers[i]->n + layers[i]->m) * 4;
+  return set_stage_offset(layers, count, batch) + round_up(io, 256);
+}
+
+void check_set(const q8p_layer* const* layers, int count, int batch) {
+  if (count < 0 || batch < 0) throw ValidationError("negative layer count / batch");
+  if (count > 0 && !layers) throw ValidationError("null layer list");
+  for (int i = 0; i < count; ++i) {
+    if (!layers[i]) throw ValidationError("null layer");
+    if (layers[i]->device != layers[0]->device) throw ValidationError("layers on different devices");
+  }
+}
+
+void forward_set_impl(const q8p_layer* const* layers, int count, const float* const* x, float* const* y, int batch,
+                      void* ws, std::size_t ws_bytes, cudaStream_t s) {
+  for (int i = 0; i < count; ++i) forward_impl(layers[i], x[i], y[i], batch, ws, ws_bytes, s);
+}
+
+// Per-device side stream + events for the copies of a layer set.
+struct SetAux {
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ev;
+};
+SetAux g_set_aux[64];
+std::mutex g_set_aux_mu;
+
+// H2D of every input, the forwards, D2H of every output (stream-ordered on `s`
+// when it returns, no sync).  The copies run on a side stream: layer i waits only
+// for its own input, and y_i goes back while later layers compute, so only the
+// first input and the last output are exposed.
+void forward_set_host_enqueue(const q8p_layer* const* layers, int count, const float* xh, float* yh, int batch,
+                              void* ws, std::size_t ws_bytes, cudaStream_t s) {
+  const int dev = layers[0]->device;
+  std::scoped_lock lock(g_set_aux_mu);
+  SetAux& aux = g_set_aux[dev];
+  if (!aux.side) cuda_check(cudaStreamCreateWithFlags(&aux.side, cudaStreamNonBlocking), "side stream");
+  while (aux.ev.size() < std::size_t(2 * count + 2)) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    aux.ev.push_back(e);
+  }
+  auto* stage = static_cast<std::uint8_t*>(ws) + set_stage_offset(layers, count, batch);
+  std::size_t nsum = 0;
+  for (int i = 0; i < count; ++i) nsum += layers[i]->n;
+  float* dx = reinterpret_cast<float*>(stage);
+  float* dy = dx + std::size_t(batch) * nsum;
+  cudaEvent_t fork = aux.ev[0], join = aux.ev[1];
+  cuda_check(cudaEventRecord(fork, s), "fork");
+  cuda_check(cudaStreamWaitEvent(aux.side, fork, 0), "fork wait");
+  std::size_t xo = 0;
+  for (int i = 0; i < count; ++i) {
+    const std::size_t nb = std::size_t(batch) * layers[i]->n;
+    cuda_check(cudaMemcpyAsync(dx + xo, xh + xo, nb * 4, cudaMemcpyHostToDevice, aux.side), "set H2D");
+    cuda_check(cudaEventRecord(aux.ev[2 + i], aux.side), "H2D event");
+    xo += nb;
+  }
+  xo = 0;
+  std::size_t yo = 0;
+  for (int i = 0; i < count; ++i) {
+    const std::size_t nb = std::size_t(batch) * layers[i]->n, mb = std::size_t(batch) * layers[i]->m;
+    cuda_check(cudaStreamWaitEvent(s, aux.ev[2 + i], 0), "H2D wait");
+    forward_impl(layers[i], dx + xo, dy + yo, batch, ws, ws_bytes, s);
+    cuda_check(cudaEventRecord(aux.ev[2 + count + i], s), "layer event");
+    cuda_check(cudaStreamWaitEvent(aux.side, aux.ev[2 + count + i], 0), "layer wait");
+    cuda_check(cudaMemcpyAsync(yh + yo, dy + yo, mb * 4, cudaMemcpyDeviceToHost, aux.side), "set D2H");
+    xo += nb;
+    yo += mb;
+  }
+  cuda_check(cudaEventRecord(join, aux.side), "join");
+  cuda_check(cudaStreamWaitEvent(s, join, 0), "join wait");
+}
+
+// Device-side address of pinned (page-locked, mapped) host memory, or nullptr.
+void* mapped_ptr(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
+// Zero-copy step (Q8P_SET_ZERO_COPY=1): K1 reads every x straight from pinned
+// host memory over PCIe and K3 writes every y straight into it (the same bytes
+// cross the link as with copies, without copy-engine round trips).
+void forward_set_mapped_enqueue(const q8p_layer* const* layers, int count, const float* dxh, float* dyh, int batch,
+                                void* ws, std::size_t ws_bytes, cudaStream_t s) {
+  std::size_t xo = 0, yo = 0;
+  for (int i = 0; i < count; ++i) {
+    forward_impl(layers[i], dxh + xo, dyh + yo, batch, ws, ws_bytes, s);
+    xo += std::size_t(batch) * layers[i]->n;
+    yo += std::size_t(batch) * layers[i]->m;
+  }
+}
+
+void forward_set_host_impl(const q8p_layer* const* layers, int count, const float* xh, float* yh, int batch, void* ws,
+                           std::size_t ws_bytes, cudaStream_t s) {
+  check_set(layers, count, batch);
+  if (count == 0 || batch == 0) return;
+  if (!xh || !yh) throw ValidationError("null host x / y");
+  if (!ws || ws_bytes < set_workspace_size(layers, count, batch)) throw SizeError("workspace too small");
+  const int dev = layers[0]->device;
+  DeviceGuard g(dev);
+  static const bool no_graph = std::getenv("Q8P_NO_SET_GRAPH") != nullptr;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cuda_check(cudaStreamIsCapturing(s, &cap), "capture status");
+  const auto* dxh = static_cast<const float*>(mapped_ptr(xh));
+  auto* dyh = static_cast<float*>(mapped_ptr(yh));
+  // experiment knob: zero-copy (kernels read x / write y in pinned host memory over
+  // PCIe) measured no faster than the overlapped copies (109-111 us per 70B step)
+  static const bool zero_copy = std::getenv("Q8P_SET_ZERO_COPY") != nullptr;
+  const bool mapped = dxh && dyh && zero_copy;
+  auto enqueue = [&](cudaStream_t st) {
+    if (mapped)
+      forward_set_mapped_enqueue(layers, count, dxh, dyh, batch, ws, ws_bytes, st);
+    else
+      forward_set_host_enqueue(layers, count, xh, yh, batch, ws, ws_bytes, st);
+  };
+  if (no_graph || cap != cudaStreamCaptureStatusNone || !dxh || !dyh || dev < 0 || dev >= 64) {
+    enqueue(s);
+    cuda_check(cudaStreamSynchronize(s), "set sync");
+    return;
+  }
+  cudaGraphExec_t exec = nullptr;
+  {
+    std::scoped_lock lock(g_set_mu);
+    for (const auto& e : g_set_graphs)
+      if (e.xh == xh && e.yh == yh && e.batch == batch && e.ws == ws && e.ws_bytes == ws_bytes && e.device == dev &&
+          e.layers.size() == std::size_t(count) && std::equal(e.layers.begin(), e.layers.end(), layers))
+        exec = e.exec;
+    if (!exec) {
+      if (!g_set_capture[dev])
+        cuda_check(cudaStreamCreateWithFlags(&g_set_capture[dev], cudaStreamNonBlocking), "capture stream");
+      cudaStream_t cs = g_set_capture[dev];
+      cudaGraph_t graph = nullptr;
+      const std::uint64_t k0 = g_launches.load();
+      cuda_check(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin capture");
+      try {
+        enqueue(cs);
+      } catch (...) {
+        cudaStreamEndCapture(cs, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      cuda_check(cudaStreamEndCapture(cs, &graph), "end capture");
+      const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      cuda_check(ie, "graph instantiate");
+      if (g_set_graphs.size() >= 16) {  // bounded: evict the oldest
+        cudaGraphExecDestroy(g_set_graphs.front().exec);
+        g_set_graphs.erase(g_set_graphs.begin());
+      }
+      const std::uint64_t k = g_launches.load() - k0;
+      g_launches.fetch_sub(k);  // counted per replay below
+      g_set_graphs.push_back({std::vector<const q8p_layer*>(layers, layers + count), xh, yh, batch, ws, ws_bytes, dev,
+                              exec, k});
+    }
+    for (const auto& e : g_set_graphs)
+      if (e.exec == exec) g_launches.fetch_add(e.kernels, std::memory_order_relaxed);
+  }
+  cuda_check(cudaGraphLaunch(exec, s), "graph launch");
+  cuda_check(cudaStreamSynchronize(s), "set sync");
+}
+
+// Drops cached layer-set graphs that reference `L` (q8p_layer_destroy).
+void forget_set_graphs(const q8p_layer* L) {
+  std::scoped_lock lock(g_set_mu);
+  for (auto it = g_set_graphs.begin(); it != g_set_graphs.end();) {
+    if (std::find(it->layers.begin(), it->layers.end(), L) != it->layers.end()) {
+      cudaGraphExecDestroy(it->exec);
+      it = g_set_graphs.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
 }  // namespace
 }  // namespace q8p::detail
 
@@ -571,6 +776,7 @@ void q8p_layer_destroy(q8p_layer* L) {
   cudaSetDevice(L->device);
   for (auto& e : L->graphs) cudaGraphExecDestroy(e.exec);
   L->graphs.clear();
+  forget_set_graphs(L);
   if (L->capture_stream) cudaStreamDestroy(L->capture_stream);
   for (void* p : L->allocations) cudaFree(p);
   if (L->dev_stage) cudaFree(L->dev_stage);
@@ -615,6 +821,38 @@ q8p_status q8p_forward_ex(const q8p_layer* L, const float* x, float* y, int batc
                           size_t ws_bytes, void* stream, const q8p_forward_opts* opts) {
   try {
     forward_impl(L, x, y, batch, ws, ws_bytes, static_cast<cudaStream_t>(stream), opts);
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+size_t q8p_forward_set_workspace_bytes(const q8p_layer* const* layers, int count, int batch) {
+  try {
+    check_set(layers, count, batch);
+    return count > 0 && batch > 0 ? set_workspace_size(layers, count, batch) : 0;
+  } catch (...) {
+    status_of_current_exception();
+    return 0;
+  }
+}
+
+q8p_status q8p_forward_set(const q8p_layer* const* layers, int count, const float* const* x, float* const* y,
+                           int batch, void* ws, size_t ws_bytes, void* stream) {
+  try {
+    check_set(layers, count, batch);
+    if (count > 0 && (!x || !y)) throw q8p::ValidationError("null x / y lists");
+    forward_set_impl(layers, count, x, y, batch, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_forward_set_host(const q8p_layer* const* layers, int count, const float* x_host, float* y_host,
+                                int batch, void* ws, size_t ws_bytes, void* stream) {
+  try {
+    forward_set_host_impl(layers, count, x_host, y_host, batch, ws, ws_bytes, static_cast<cudaStream_t>(stream));
     return Q8P_OK;
   } catch (...) {
     return status_of_current_exception();
