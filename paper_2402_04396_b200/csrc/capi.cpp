@@ -283,13 +283,13 @@ struct Workspace {
   std::uint32_t rows_pad, zcols;
 };
 std::uint32_t rows_pad_of(const q8p_layer* L) { return tc_row_blocks(L->m_local()) * 128; }
-// Batches above the tensor-core path's 16 vectors run as 16-vector chunks through
+// Batches above the tensor-core path's 32 vectors run as 32-vector chunks through
 // it (weights streamed once per chunk) instead of the portable fp32 GEMV;
 // Q8P_PORTABLE_BIG_BATCH=1 restores the portable path (experiment knob).
 int tc_chunk(const q8p_layer* L, int batch) {
   static const bool portable = std::getenv("Q8P_PORTABLE_BIG_BATCH") != nullptr;
   if (tc_supported(*L, batch)) return batch;
-  if (!portable && batch > 16 && tc_supported(*L, 16)) return 16;
+  if (!portable && batch > kTcMaxBatch && tc_supported(*L, kTcMaxBatch)) return kTcMaxBatch;
   return 0;  // portable path
 }
 
@@ -330,7 +330,7 @@ std::size_t workspace_size(const q8p_layer* L, int batch) { return workspace_par
 // path) or fp32 z rows in w.z (portable path).
 void forward_local(const q8p_layer* L, const float* x, int batch, const Workspace& w, cudaStream_t s,
                    const q8p_forward_opts* opts) {
-  if (tc_supported(*L, batch)) {  // (callers chunk batches above 16)
+  if (tc_supported(*L, batch)) {  // (callers chunk batches above kTcMaxBatch)
     // N from this call's batch (a chunk may be smaller than the workspace's 16)
     const std::uint32_t N = std::uint32_t(tc_ncols_pad(4 * batch)), KSL = tc_k_slabs(L->n), bb = 9u * N * 32u;
     const bool ragged = (L->n / 8) % 32 != 0;
@@ -373,7 +373,7 @@ void forward_sharded_impl(const q8p_layer* L, const float* x, float* y, int batc
   if (batch == 0) return;
   if (!x || !y) throw ValidationError("null x / y");
   if (!comm) throw ValidationError("null communicator");
-  const int chunk = tc_chunk(L, batch);  // batches above 16 go through in 16-vector chunks
+  const int chunk = tc_chunk(L, batch);  // batches above kTcMaxBatch go through in chunks
   if (chunk == 0) throw UnsupportedError("row-sharded forward needs the tensor-core path");
   int world = 0, rank = 0;
   nccl_check(ncclCommCount(comm, &world), "ncclCommCount");
@@ -423,7 +423,7 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
   if (const int chunk = tc_chunk(L, batch)) {
     float zscale[2] = {L->scale[0], L->scale[1]};
     int ze8p[2] = {L->cb[0] == Q8P_CB_E8P_2BIT, L->cb[1] == Q8P_CB_E8P_2BIT};
-    for (int b0 = 0; b0 < batch; b0 += chunk) {  // one pass for batch <= 16
+    for (int b0 = 0; b0 < batch; b0 += chunk) {  // one pass for batch <= kTcMaxBatch
       const int nb = std::min(chunk, batch - b0);
       forward_local(L, x + std::size_t(b0) * L->n, nb, w, s, b0 == 0 ? opts : nullptr);
 #ifndef Q8P_EXP_SKIP_K3
@@ -1050,7 +1050,7 @@ q8p_status q8p_forward_rows_z(const q8p_layer* L, const float* x, float* z, int 
   try {
     if (!L || !x || !z) throw q8p::ValidationError("null argument");
     if (batch <= 0) return Q8P_OK;
-    if (!tc_supported(*L, batch)) throw q8p::UnsupportedError("rows_z needs the tensor-core path (batch <= 16)");
+    if (!tc_supported(*L, batch)) throw q8p::UnsupportedError("rows_z needs the tensor-core path (batch <= 32)");
     if (!ws || ws_bytes < workspace_size(L, batch)) throw q8p::SizeError("workspace too small");
     DeviceGuard g(L->device);
     Workspace w;

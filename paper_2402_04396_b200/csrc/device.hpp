@@ -127,6 +127,7 @@ std::uint32_t tc_row_blocks(std::uint32_t m_local);
 std::uint32_t tc_k_slabs(std::uint32_t n);
 std::size_t tc_code_bytes(std::uint32_t m_local, std::uint32_t n, int kind);
 void tc_transcode(const std::uint16_t* codes, std::uint32_t m_local, std::uint32_t n, int kind, std::uint8_t* out);
+constexpr int kTcMaxBatch = 32;  // tensor-core path: batch <= 32 per launch (MMA N <= 128)
 bool tc_supported(const q8p_layer& L, int batch);
 int tc_ncols_pad(int ncols);                              // MMA N for `ncols` B rows
 std::uint32_t tc_bimg_bytes(std::uint32_t n, int batch);  // B images for all k slabs

@@ -271,6 +271,7 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
   const std::uint32_t lo_base = sbase + kCtl;
   const std::uint32_t n_lo = lutw > lo_base ? (lutw - lo_base) / kCodeSlot : 0;
   const std::uint32_t hi_base = b_base + SB * b_slot;
+  if (hi_base > send) __trap();  // B ring past the dynamic smem (host sizing bug): fail loudly
   std::uint32_t S = n_lo + (send > hi_base ? (send - hi_base) / kCodeSlot : 0);
   if (S > kMaxStages) S = kMaxStages;
   auto code_addr = [&](std::uint32_t st) { return st < n_lo ? lo_base + st * kCodeSlot : hi_base + (st - n_lo) * kCodeSlot; };
@@ -760,13 +761,18 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
 }
 
 constexpr std::size_t kSmemFused = 225 * 1024;  // fused layer kernel: nothing else to co-reside with
+constexpr std::size_t kSmemWide = 225 * 1024;   // N = 128 (prefill chunks of 32 vectors): 2 x 36 KB B slots
+template <int N, bool FUSED>
+constexpr std::size_t smem_for() {
+  return FUSED ? kSmemFused : (N >= 128 ? kSmemWide : kSmemBytes);
+}
 
 template <int N, int G, int T, bool FUSED, int NB>
 void set_attr() {
   static std::once_flag once;
   std::call_once(once, [] {
     cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G, T, FUSED, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(FUSED ? kSmemFused : kSmemBytes)),
+                                    int(smem_for<N, FUSED>())),
                "tc smem attr");
     cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G, T, FUSED, NB>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                     100),
@@ -785,10 +791,11 @@ int sm_count() {
 }
 
 template <int N, int G, int T = 1, bool FUSED = false, int NB = 2>
-void launch_ng(const TcArgs& a, cudaStream_t s) {
+void launch_ng(TcArgs a, cudaStream_t s) {
   set_attr<N, G, T, FUSED, NB>();
+  a.smem_bytes = std::uint32_t(smem_for<N, FUSED>());
   launch_pdl(gemv_tc_kernel<N, G, T, FUSED, NB>, dim3(sm_count()), dim3(Roles<G, T>::kThreads),
-             FUSED ? kSmemFused : kSmemBytes, s, a);
+             smem_for<N, FUSED>(), s, a);
 }
 
 }  // namespace
@@ -860,9 +867,12 @@ void tc_transcode(const std::uint16_t* codes, std::uint32_t m_local, std::uint32
     }
 }
 
-int tc_ncols_pad(int ncols) { return ncols <= 8 ? 8 : ncols <= 16 ? 16 : (ncols + 15) / 16 * 16; }
+// MMA N for `ncols` B rows (4 limbs x batch): 8, 16, 32, 48, 64, then 128 (batch 17..32).
+int tc_ncols_pad(int ncols) {
+  return ncols <= 8 ? 8 : ncols <= 16 ? 16 : ncols <= 64 ? (ncols + 15) / 16 * 16 : 128;
+}
 bool tc_supported(const q8p_layer& L, int batch) {
-  return batch >= 1 && batch <= 16 && L.tc[0].codes != nullptr && L.cb[0] == Q8P_CB_E8P_2BIT &&
+  return batch >= 1 && batch <= kTcMaxBatch && L.tc[0].codes != nullptr && L.cb[0] == Q8P_CB_E8P_2BIT &&
          (L.num_stages == 1 || L.tc[1].codes != nullptr);
 }
 std::uint32_t tc_bimg_bytes(std::uint32_t n, int batch) {
@@ -923,7 +933,8 @@ void launch_gemv_tc(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* 
     case 16: fits(3) ? launch_ng<16, 3>(a, s) : launch_ng<16, 2>(a, s); break;
     case 32: launch_ng<32, 2>(a, s); break;
     case 48: launch_ng<48, 2>(a, s); break;
-    default: fits(2) ? launch_ng<64, 2>(a, s) : launch_ng<64, 1>(a, s); break;
+    case 64: fits(2) ? launch_ng<64, 2>(a, s) : launch_ng<64, 1>(a, s); break;
+    default: launch_ng<128, 1>(a, s); break;  // prefill chunks: one decode group, 400 TMEM columns
   }
   cuda_check(cudaGetLastError(), "gemv_tc launch");
   if (tr != nullptr) {

@@ -19,5 +19,10 @@ for batch in [int(b) for b in (sys.argv[2] if len(sys.argv) > 2 else "16,128,512
         a.record(); L.forward(x, out=y, workspace=ws); b.record(); torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     t = statistics.median(ts)
+    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    ev[0].record(); ev[1].record()
+    L.forward(x, out=y, workspace=ws, gemv_events=ev)  # K2 of the first chunk
+    torch.cuda.synchronize()
+    k2 = ev[0].elapsed_time(ev[1])
     print(f"{m}x{n} batch {batch}: {t:.3f} ms  {2 * m * n * batch / (t * 1e-3) / 1e12:.2f} TFLOP/s-equiv  "
-          f"{batch / (t * 1e-3):.0f} tokens/s", flush=True)
+          f"{batch / (t * 1e-3):.0f} tokens/s  (K2 of the first chunk {k2 * 1e3:.1f} us)", flush=True)
