@@ -11,7 +11,7 @@ import paper_2402_04396_b200 as q8p
 m, n = (int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else os.environ.get("SHAPE", "28672x8192")).split("x"))
 # 3 distinct copies (> L2 for the big layers) so the traced launch streams from HBM
 Ls = [q8p.Layer.from_qshp(bench.make_artifact(m, n, 7 + c), device=0) for c in range(3)]
-x = torch.randn(1, n, device="cuda")
+x = torch.randn(int(os.environ.get("BATCH", "1")), n, device="cuda")
 for c in range(3):
     y = Ls[c].forward(x)
 torch.cuda.synchronize()
