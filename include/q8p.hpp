@@ -45,7 +45,7 @@ class TruncatedArtifactError : public FormatError {
  public:
   using FormatError::FormatError;
 };
-class UnsupportedError : public Error {  // valid artifact, not on this path (rfft)
+class UnsupportedError : public Error {  // valid artifact, not on this path (e.g. > 2 RVQ stages)
  public:
   using Error::Error;
 };
