@@ -165,6 +165,21 @@ q8p_status q8p_forward_set(const q8p_layer* const* layers, int count, const floa
 q8p_status q8p_forward_set_host(const q8p_layer* const* layers, int count, const float* x_host,
                                 float* y_host, int batch, void* workspace, size_t workspace_bytes,
                                 void* stream);
+/* Flags for the _ex variants.  Q8P_SET_CONCURRENT: the layers are independent
+ * (each reads only its own input, e.g. q/k/v or gate/up projections), so they
+ * run on parallel streams with one workspace slice each (size it with
+ * q8p_forward_set_workspace_bytes_ex): one layer's latency-bound transforms
+ * overlap another's bandwidth-bound GEMV.  Results are bit-identical to the
+ * sequential call. */
+#define Q8P_SET_CONCURRENT 1u
+size_t q8p_forward_set_workspace_bytes_ex(const q8p_layer* const* layers, int count, int batch,
+                                          unsigned flags);
+q8p_status q8p_forward_set_ex(const q8p_layer* const* layers, int count, const float* const* x,
+                              float* const* y, int batch, void* workspace, size_t workspace_bytes,
+                              void* stream, unsigned flags);
+q8p_status q8p_forward_set_host_ex(const q8p_layer* const* layers, int count, const float* x_host,
+                                   float* y_host, int batch, void* workspace, size_t workspace_bytes,
+                                   void* stream, unsigned flags);
 
 /* latq::infer drop-in: host f64 x [batch][n] -> host f64 y [batch][m].
  * Synchronous; stages through an internal pinned buffer and workspace. */

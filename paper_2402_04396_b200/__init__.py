@@ -130,6 +130,12 @@ _SIGNATURES = {
     "q8p_forward_sharded": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]),
     "q8p_infer_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
     "q8p_forward_set_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
+    "q8p_forward_set_workspace_bytes_ex": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_uint]),
+    "q8p_forward_set_ex": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                          ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_uint]),
+    "q8p_forward_set_host_ex": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                               ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                                               ctypes.c_uint]),
     "q8p_forward_set": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                        ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "q8p_forward_set_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
@@ -425,11 +431,16 @@ class Layer:
         return w
 
 
-class LayerSet:
-    """Independent layer forwards per call (q8p_forward_set / _host): one decode
-    step through a model's linear layers."""
+SET_CONCURRENT = 1  # Q8P_SET_CONCURRENT
 
-    def __init__(self, layers: Sequence[Layer]):
+
+class LayerSet:
+    """Independent layer forwards per call (q8p_forward_set_ex / _host_ex): one
+    decode step through a model's linear layers.  concurrent=True: the layers
+    read only their own inputs and run on parallel streams (Q8P_SET_CONCURRENT)."""
+
+    def __init__(self, layers: Sequence[Layer], concurrent: bool = False):
+        self.flags = SET_CONCURRENT if concurrent else 0
         self.layers = list(layers)  # keeps the handles alive
         self._arr = (ctypes.c_void_p * len(self.layers))(*[L._h.value for L in self.layers])
         self._ws = None
@@ -437,7 +448,7 @@ class LayerSet:
         self._msum = sum(L._dims()[0] for L in self.layers)
 
     def workspace_bytes(self, batch: int) -> int:
-        return int(lib().q8p_forward_set_workspace_bytes(self._arr, len(self.layers), batch))
+        return int(lib().q8p_forward_set_workspace_bytes_ex(self._arr, len(self.layers), batch, self.flags))
 
     def workspace(self, batch: int):
         torch = _torch()
@@ -462,8 +473,8 @@ class LayerSet:
         xp = (ctypes.c_void_p * len(xs))(*[x.data_ptr() for x in xs])
         yp = (ctypes.c_void_p * len(outs))(*[y.data_ptr() for y in outs])
         ws = workspace if workspace is not None else self.workspace(batch)
-        _check(lib().q8p_forward_set(self._arr, len(self.layers), xp, yp, batch, ws.data_ptr(), ws.numel(),
-                                     _stream_ptr(stream)))
+        _check(lib().q8p_forward_set_ex(self._arr, len(self.layers), xp, yp, batch, ws.data_ptr(), ws.numel(),
+                                        _stream_ptr(stream), self.flags))
         return outs
 
     def forward_host(self, x_host, y_host, batch: int, stream=None, workspace=None):
@@ -473,8 +484,8 @@ class LayerSet:
         if x_host.numel() < batch * self._nsum or y_host.numel() < batch * self._msum:
             raise SizeError("host buffers too small for the layer set")
         ws = workspace if workspace is not None else self.workspace(batch)
-        st = lib().q8p_forward_set_host(self._arr, len(self._arr), x_host.data_ptr(), y_host.data_ptr(), batch,
-                                        ws.data_ptr(), ws.numel(), _stream_ptr(stream))
+        st = lib().q8p_forward_set_host_ex(self._arr, len(self._arr), x_host.data_ptr(), y_host.data_ptr(), batch,
+                                           ws.data_ptr(), ws.numel(), _stream_ptr(stream), self.flags)
         if st:
             _check(st)
         return y_host

@@ -507,6 +507,7 @@ struct SetGraph {
   void* ws;
   std::size_t ws_bytes;
   int device;
+  unsigned flags;
   cudaGraphExec_t exec;
   std::uint64_t kernels;
 };
@@ -514,15 +515,25 @@ std::mutex g_set_mu;
 std::vector<SetGraph> g_set_graphs;
 cudaStream_t g_set_capture[64] = {};
 
-std::size_t set_stage_offset(const q8p_layer* const* layers, int count, int batch) {
+// Workspace of a layer set: sequential -> one shared layer workspace (the largest);
+// Q8P_SET_CONCURRENT -> one slice per layer (offset of layer i = layer_ws_offset);
+// then the host variant's staging.
+std::size_t layer_ws_offset(const q8p_layer* const* layers, int i, int batch, unsigned flags) {
+  if (!(flags & Q8P_SET_CONCURRENT)) return 0;
+  std::size_t off = 0;
+  for (int j = 0; j < i; ++j) off += round_up(workspace_size(layers[j], batch), 256);
+  return off;
+}
+std::size_t set_stage_offset(const q8p_layer* const* layers, int count, int batch, unsigned flags) {
+  if (flags & Q8P_SET_CONCURRENT) return layer_ws_offset(layers, count, batch, flags);
   std::size_t ws = 0;
   for (int i = 0; i < count; ++i) ws = std::max(ws, workspace_size(layers[i], batch));
   return round_up(ws, 256);
 }
-std::size_t set_workspace_size(const q8p_layer* const* layers, int count, int batch) {
+std::size_t set_workspace_size(const q8p_layer* const* layers, int count, int batch, unsigned flags) {
   std::size_t io = 0;
   for (int i = 0; i < count; ++i) io += std::size_t(batch) * (layers[i]->n + layers[i]->m) * 4;
-  return set_stage_offset(layers, count, batch) + round_up(io, 256);
+  return set_stage_offset(layers, count, batch, flags) + round_up(io, 256);
 }
 
 void check_set(const q8p_layer* const* layers, int count, int batch) {
@@ -534,39 +545,96 @@ void check_set(const q8p_layer* const* layers, int count, int batch) {
   }
 }
 
-void forward_set_impl(const q8p_layer* const* layers, int count, const float* const* x, float* const* y, int batch,
-                      void* ws, std::size_t ws_bytes, cudaStream_t s) {
-  for (int i = 0; i < count; ++i) forward_impl(layers[i], x[i], y[i], batch, ws, ws_bytes, s);
-}
-
-// Per-device side stream + events for the copies of a layer set.
+// Per-device side streams + events for a layer set's copies / concurrent layers.
 struct SetAux {
   cudaStream_t side = nullptr;
+  std::vector<cudaStream_t> lanes;
   std::vector<cudaEvent_t> ev;
 };
 SetAux g_set_aux[64];
 std::mutex g_set_aux_mu;
+constexpr int kSetLanes = 4;
+
+// `lanes` streams and `events` events of device `dev` (created on first use).
+SetAux& set_aux(int dev, int lanes, int events) {
+  SetAux& aux = g_set_aux[dev];
+  if (!aux.side) cuda_check(cudaStreamCreateWithFlags(&aux.side, cudaStreamNonBlocking), "side stream");
+  while (int(aux.lanes.size()) < lanes) {
+    cudaStream_t st;
+    cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "lane stream");
+    aux.lanes.push_back(st);
+  }
+  while (int(aux.ev.size()) < events) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    aux.ev.push_back(e);
+  }
+  return aux;
+}
+
+// Q8P_SET_CONCURRENT: layer i runs on lane i % kSetLanes with its own workspace
+// slice; `body(i, lane)` enqueues layer i's work.  Forked from / joined back
+// into `s` with events (also under stream capture: the graph gets parallel branches).
+template <typename F>
+void run_lanes(const q8p_layer* const* layers, int count, cudaStream_t s, F&& body) {
+  const int dev = layers[0]->device, nl = std::min(count, kSetLanes);
+  std::scoped_lock lock(g_set_aux_mu);
+  SetAux& aux = set_aux(dev, nl, 2 + nl);
+  cuda_check(cudaEventRecord(aux.ev[0], s), "fork");
+  for (int k = 0; k < nl; ++k) cuda_check(cudaStreamWaitEvent(aux.lanes[k], aux.ev[0], 0), "fork wait");
+  for (int i = 0; i < count; ++i) body(i, aux.lanes[i % nl]);
+  for (int k = 0; k < nl; ++k) {
+    cuda_check(cudaEventRecord(aux.ev[2 + k], aux.lanes[k]), "join");
+    cuda_check(cudaStreamWaitEvent(s, aux.ev[2 + k], 0), "join wait");
+  }
+}
+
+void forward_set_impl(const q8p_layer* const* layers, int count, const float* const* x, float* const* y, int batch,
+                      void* ws, std::size_t ws_bytes, cudaStream_t s, unsigned flags) {
+  if (count == 0 || batch == 0) return;
+  if (!(flags & Q8P_SET_CONCURRENT)) {
+    for (int i = 0; i < count; ++i) forward_impl(layers[i], x[i], y[i], batch, ws, ws_bytes, s);
+    return;
+  }
+  if (!ws || ws_bytes < set_stage_offset(layers, count, batch, flags)) throw SizeError("workspace too small");
+  DeviceGuard g(layers[0]->device);
+  run_lanes(layers, count, s, [&](int i, cudaStream_t lane) {
+    const std::size_t off = layer_ws_offset(layers, i, batch, flags);
+    forward_impl(layers[i], x[i], y[i], batch, static_cast<std::uint8_t*>(ws) + off, ws_bytes - off, lane);
+  });
+}
 
 // H2D of every input, the forwards, D2H of every output (stream-ordered on `s`
 // when it returns, no sync).  The copies run on a side stream: layer i waits only
 // for its own input, and y_i goes back while later layers compute, so only the
 // first input and the last output are exposed.
 void forward_set_host_enqueue(const q8p_layer* const* layers, int count, const float* xh, float* yh, int batch,
-                              void* ws, std::size_t ws_bytes, cudaStream_t s) {
-  const int dev = layers[0]->device;
-  std::scoped_lock lock(g_set_aux_mu);
-  SetAux& aux = g_set_aux[dev];
-  if (!aux.side) cuda_check(cudaStreamCreateWithFlags(&aux.side, cudaStreamNonBlocking), "side stream");
-  while (aux.ev.size() < std::size_t(2 * count + 2)) {
-    cudaEvent_t e;
-    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-    aux.ev.push_back(e);
-  }
-  auto* stage = static_cast<std::uint8_t*>(ws) + set_stage_offset(layers, count, batch);
+                              void* ws, std::size_t ws_bytes, cudaStream_t s, unsigned flags) {
+  auto* stage = static_cast<std::uint8_t*>(ws) + set_stage_offset(layers, count, batch, flags);
   std::size_t nsum = 0;
   for (int i = 0; i < count; ++i) nsum += layers[i]->n;
   float* dx = reinterpret_cast<float*>(stage);
   float* dy = dx + std::size_t(batch) * nsum;
+  if (flags & Q8P_SET_CONCURRENT) {  // each layer's H2D, forward and D2H on its own lane
+    std::vector<std::size_t> xo(count + 1, 0), yo(count + 1, 0);
+    for (int i = 0; i < count; ++i) {
+      xo[i + 1] = xo[i] + std::size_t(batch) * layers[i]->n;
+      yo[i + 1] = yo[i] + std::size_t(batch) * layers[i]->m;
+    }
+    run_lanes(layers, count, s, [&](int i, cudaStream_t lane) {
+      const std::size_t off = layer_ws_offset(layers, i, batch, flags);
+      cuda_check(cudaMemcpyAsync(dx + xo[i], xh + xo[i], (xo[i + 1] - xo[i]) * 4, cudaMemcpyHostToDevice, lane),
+                 "set H2D");
+      forward_impl(layers[i], dx + xo[i], dy + yo[i], batch, static_cast<std::uint8_t*>(ws) + off, ws_bytes - off,
+                   lane);
+      cuda_check(cudaMemcpyAsync(yh + yo[i], dy + yo[i], (yo[i + 1] - yo[i]) * 4, cudaMemcpyDeviceToHost, lane),
+                 "set D2H");
+    });
+    return;
+  }
+  const int dev = layers[0]->device;
+  std::scoped_lock lock(g_set_aux_mu);
+  SetAux& aux = set_aux(dev, 0, 2 * count + 2);
   cudaEvent_t fork = aux.ev[0], join = aux.ev[1];
   cuda_check(cudaEventRecord(fork, s), "fork");
   cuda_check(cudaStreamWaitEvent(aux.side, fork, 0), "fork wait");
@@ -617,11 +685,11 @@ void forward_set_mapped_enqueue(const q8p_layer* const* layers, int count, const
 }
 
 void forward_set_host_impl(const q8p_layer* const* layers, int count, const float* xh, float* yh, int batch, void* ws,
-                           std::size_t ws_bytes, cudaStream_t s) {
+                           std::size_t ws_bytes, cudaStream_t s, unsigned flags) {
   check_set(layers, count, batch);
   if (count == 0 || batch == 0) return;
   if (!xh || !yh) throw ValidationError("null host x / y");
-  if (!ws || ws_bytes < set_workspace_size(layers, count, batch)) throw SizeError("workspace too small");
+  if (!ws || ws_bytes < set_workspace_size(layers, count, batch, flags)) throw SizeError("workspace too small");
   const int dev = layers[0]->device;
   DeviceGuard g(dev);
   static const bool no_graph = std::getenv("Q8P_NO_SET_GRAPH") != nullptr;
@@ -637,7 +705,7 @@ void forward_set_host_impl(const q8p_layer* const* layers, int count, const floa
     if (mapped)
       forward_set_mapped_enqueue(layers, count, dxh, dyh, batch, ws, ws_bytes, st);
     else
-      forward_set_host_enqueue(layers, count, xh, yh, batch, ws, ws_bytes, st);
+      forward_set_host_enqueue(layers, count, xh, yh, batch, ws, ws_bytes, st, flags);
   };
   if (no_graph || cap != cudaStreamCaptureStatusNone || !dxh || !dyh || dev < 0 || dev >= 64) {
     enqueue(s);
@@ -649,6 +717,7 @@ void forward_set_host_impl(const q8p_layer* const* layers, int count, const floa
     std::scoped_lock lock(g_set_mu);
     for (const auto& e : g_set_graphs)
       if (e.xh == xh && e.yh == yh && e.batch == batch && e.ws == ws && e.ws_bytes == ws_bytes && e.device == dev &&
+          e.flags == flags &&
           e.layers.size() == std::size_t(count) && std::equal(e.layers.begin(), e.layers.end(), layers))
         exec = e.exec;
     if (!exec) {
@@ -676,7 +745,7 @@ void forward_set_host_impl(const q8p_layer* const* layers, int count, const floa
       const std::uint64_t k = g_launches.load() - k0;
       g_launches.fetch_sub(k);  // counted per replay below
       g_set_graphs.push_back({std::vector<const q8p_layer*>(layers, layers + count), xh, yh, batch, ws, ws_bytes, dev,
-                              exec, k});
+                              flags, exec, k});
     }
     for (const auto& e : g_set_graphs)
       if (e.exec == exec) g_launches.fetch_add(e.kernels, std::memory_order_relaxed);
@@ -827,36 +896,48 @@ q8p_status q8p_forward_ex(const q8p_layer* L, const float* x, float* y, int batc
   }
 }
 
-size_t q8p_forward_set_workspace_bytes(const q8p_layer* const* layers, int count, int batch) {
+size_t q8p_forward_set_workspace_bytes_ex(const q8p_layer* const* layers, int count, int batch, unsigned flags) {
   try {
     check_set(layers, count, batch);
-    return count > 0 && batch > 0 ? set_workspace_size(layers, count, batch) : 0;
+    return count > 0 && batch > 0 ? set_workspace_size(layers, count, batch, flags) : 0;
   } catch (...) {
     status_of_current_exception();
     return 0;
   }
 }
+size_t q8p_forward_set_workspace_bytes(const q8p_layer* const* layers, int count, int batch) {
+  return q8p_forward_set_workspace_bytes_ex(layers, count, batch, 0);
+}
 
-q8p_status q8p_forward_set(const q8p_layer* const* layers, int count, const float* const* x, float* const* y,
-                           int batch, void* ws, size_t ws_bytes, void* stream) {
+q8p_status q8p_forward_set_ex(const q8p_layer* const* layers, int count, const float* const* x, float* const* y,
+                              int batch, void* ws, size_t ws_bytes, void* stream, unsigned flags) {
   try {
     check_set(layers, count, batch);
     if (count > 0 && (!x || !y)) throw q8p::ValidationError("null x / y lists");
-    forward_set_impl(layers, count, x, y, batch, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+    forward_set_impl(layers, count, x, y, batch, ws, ws_bytes, static_cast<cudaStream_t>(stream), flags);
     return Q8P_OK;
   } catch (...) {
     return status_of_current_exception();
   }
 }
+q8p_status q8p_forward_set(const q8p_layer* const* layers, int count, const float* const* x, float* const* y,
+                           int batch, void* ws, size_t ws_bytes, void* stream) {
+  return q8p_forward_set_ex(layers, count, x, y, batch, ws, ws_bytes, stream, 0);
+}
 
-q8p_status q8p_forward_set_host(const q8p_layer* const* layers, int count, const float* x_host, float* y_host,
-                                int batch, void* ws, size_t ws_bytes, void* stream) {
+q8p_status q8p_forward_set_host_ex(const q8p_layer* const* layers, int count, const float* x_host, float* y_host,
+                                   int batch, void* ws, size_t ws_bytes, void* stream, unsigned flags) {
   try {
-    forward_set_host_impl(layers, count, x_host, y_host, batch, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+    forward_set_host_impl(layers, count, x_host, y_host, batch, ws, ws_bytes, static_cast<cudaStream_t>(stream),
+                          flags);
     return Q8P_OK;
   } catch (...) {
     return status_of_current_exception();
   }
+}
+q8p_status q8p_forward_set_host(const q8p_layer* const* layers, int count, const float* x_host, float* y_host,
+                                int batch, void* ws, size_t ws_bytes, void* stream) {
+  return q8p_forward_set_host_ex(layers, count, x_host, y_host, batch, ws, ws_bytes, stream, 0);
 }
 
 q8p_status q8p_infer_host(q8p_layer* L, const double* x, double* y, int batch) {

@@ -22,10 +22,11 @@ def _layers():
             for i, (m, n, st, tr) in enumerate(SHAPES)]
 
 
+@pytest.mark.parametrize("concurrent", [False, True])
 @pytest.mark.parametrize("batch", [1, 4, 17])
-def test_forward_set_equals_per_layer(batch):
+def test_forward_set_equals_per_layer(batch, concurrent):
     layers = _layers()
-    S = q8p.LayerSet(layers)
+    S = q8p.LayerSet(layers, concurrent=concurrent)
     g = torch.Generator().manual_seed(batch)
     xs = [torch.randn(batch, L.info["n"], generator=g).cuda() for L in layers]
     want = [L.forward(x) for L, x in zip(layers, xs)]
@@ -34,10 +35,11 @@ def test_forward_set_equals_per_layer(batch):
         assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("concurrent", [False, True])
 @pytest.mark.parametrize("pinned", [True, False])
-def test_forward_set_host_graph_replays(pinned):
+def test_forward_set_host_graph_replays(pinned, concurrent):
     layers = _layers()
-    S = q8p.LayerSet(layers)
+    S = q8p.LayerSet(layers, concurrent=concurrent)
     batch = 2
     nsum = sum(L.info["n"] for L in layers)
     msum = sum(L.info["m"] for L in layers)
@@ -73,6 +75,29 @@ def test_layer_destroy_drops_cached_graphs():
     S2 = q8p.LayerSet(layers2)
     S2.forward_host(hx, hy, 1)
     assert torch.equal(hy, y0)  # same artifacts, same inputs: same results through a fresh graph
+
+
+def test_concurrent_set_under_caller_graph_capture():
+    # the caller captures the concurrent set into its own graph: forked lanes become branches
+    layers = _layers()
+    S = q8p.LayerSet(layers, concurrent=True)
+    xs = [torch.randn(2, L.info["n"]).cuda() for L in layers]
+    ys = [torch.empty(2, L.info["m"]).cuda() for L in layers]
+    ws = S.workspace(2)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        S.forward(xs, ys, stream=s, workspace=ws)
+    torch.cuda.synchronize()
+    want = [y.clone() for y in ys]
+    for y in ys:
+        y.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        S.forward(xs, ys, stream=s, workspace=ws)
+    g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(ys, want):
+        assert torch.equal(a, b)
 
 
 def test_forward_set_validation():
