@@ -160,6 +160,9 @@ bool rfft_factor(std::uint32_t n, bool codewords, std::uint32_t& M1, std::uint32
 void rfft_tables(std::uint32_t n, const float* phases, std::vector<float>& rot, std::vector<float>& tw);
 void launch_rfft_f32(const DevSide& side, const float* x, float* u_scratch, float* y, int batch, bool transpose,
                      cudaStream_t s);
+void launch_rfft_out_acc(const DevSide& side, const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows,
+                         std::uint32_t zacc_cols, const float zscale[2], const int ze8p[2], const float* alpha,
+                         const long long* tl, float* u_scratch, float* y, int batch, cudaStream_t s);
 void launch_rfft_in_limbs(const DevSide& side, const float* x, float* u_scratch, float* ssq, float* alpha,
                           long long* tl, std::uint8_t* bimg, std::uint32_t b_bytes, std::uint32_t bcols,
                           std::uint8_t* bimg_tail, std::size_t tail_bytes, std::int32_t* zero_ptr,

@@ -66,6 +66,25 @@ __device__ __forceinline__ float2 tw_dir(const RfftArgs& a, std::uint32_t e) {
   return w;
 }
 
+// sum_j x[j * stride] W^{j k} (length L, twiddles w[e] = W^e): two interleaved
+// accumulators so the dependent complex-FMA chains overlap.
+__device__ __forceinline__ float2 dft_sum(const float2* x, std::uint32_t stride, const float2* w, std::uint32_t L,
+                                          std::uint32_t k) {
+  float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0;
+  const std::uint32_t k2 = (2 * k) % L;
+  std::uint32_t e0 = 0, e1 = k % L, j = 0;
+  for (; j + 1 < L; j += 2) {
+    acc0 = cfma(x[j * stride], w[e0], acc0);
+    acc1 = cfma(x[(j + 1) * stride], w[e1], acc1);
+    e0 += k2;
+    if (e0 >= L) e0 -= L;
+    e1 += k2;
+    if (e1 >= L) e1 -= L;
+  }
+  if (j < L) acc0 = cfma(x[j * stride], w[e0], acc0);
+  return make_float2(acc0.x + acc1.x, acc0.y + acc1.y);
+}
+
 // Pass 1.  grid = (tiles1 * ks1 [+ zeroing CTAs], batch).
 __global__ void __launch_bounds__(kP1Threads) rfft_pass1(RfftArgs a) {
   extern __shared__ __align__(16) float2 sm[];
@@ -91,11 +110,11 @@ __global__ void __launch_bounds__(kP1Threads) rfft_pass1(RfftArgs a) {
   const std::uint32_t j10 = tile * a.TJ, cols = min(a.TJ, a.M1 - j10);
   float2* v = sm;                   // [M2][TJ]
   float2* w2 = sm + a.M2 * a.TJ;    // [M2] W_M2^e = W_M^{e M1}
-  const float2* x = reinterpret_cast<const float2*>(a.in + std::size_t(b) * a.n);
+  const float2* x = reinterpret_cast<const float2*>(a.in + (a.in ? std::size_t(b) * a.n : 0));
   float ss = 0.f;
   for (std::uint32_t t = threadIdx.x; t < a.M2 * cols; t += blockDim.x) {
     const std::uint32_t j2 = t / cols, jj = t - j2 * cols, idx = j10 + jj + a.M1 * j2;
-    float2 c = __ldcg(x + idx);
+    float2 c = a.k.zacc ? combine2(a.k, b, 2 * idx) : __ldcg(x + idx);  // K3: z from the limb accumulators
     ss += c.x * c.x + c.y * c.y;
     if (a.fwd) c = cmul(c, __ldg(a.rot + idx));
     v[j2 * a.TJ + jj] = c;
@@ -117,13 +136,7 @@ __global__ void __launch_bounds__(kP1Threads) rfft_pass1(RfftArgs a) {
   float2* dst = a.mid + std::size_t(b) * a.M;
   for (std::uint32_t o = threadIdx.x; o < nout; o += blockDim.x) {
     const std::uint32_t k2 = k2a + o / cols, jj = o % cols;
-    float2 acc = make_float2(0.f, 0.f);
-    std::uint32_t e = 0;  // j2 k2 mod M2
-    for (std::uint32_t j2 = 0; j2 < a.M2; ++j2) {
-      acc = cfma(v[j2 * a.TJ + jj], w2[e], acc);
-      e += k2;
-      if (e >= a.M2) e -= a.M2;
-    }
+    const float2 acc = dft_sum(v + jj, a.TJ, w2, a.M2, k2);
     dst[std::size_t(k2) * a.M1 + j10 + jj] = cmul(acc, tw_dir(a, (j10 + jj) * k2));  // j1 k2 < M
   }
 }
@@ -185,13 +198,7 @@ __global__ void __launch_bounds__(kP2Threads) rfft_pass2(RfftArgs a) {
   const std::uint32_t nout = (k1b - k1a) * rows;
   for (std::uint32_t o = threadIdx.x; o < nout; o += blockDim.x) {
     const std::uint32_t r = o % rows, k1 = k1a + o / rows;
-    float2 acc = make_float2(0.f, 0.f);
-    std::uint32_t e = 0;
-    for (std::uint32_t j1 = 0; j1 < a.M1; ++j1) {
-      acc = cfma(u[r * a.M1 + j1], w1[e], acc);
-      e += k1;
-      if (e >= a.M1) e -= a.M1;
-    }
+    float2 acc = dft_sum(u + r * a.M1, 1, w1, a.M1, k1);
     const std::uint32_t k = k20 + r + a.M2 * k1;
     acc = make_float2(acc.x * sc, acc.y * sc);
     if (!a.fwd) {
@@ -293,6 +300,32 @@ void launch_rfft_f32(const DevSide& side, const float* x, float* u_scratch, floa
   a.mid = reinterpret_cast<float2*>(u_scratch);
   a.out = y;
   a.fwd = transpose ? 0 : 1;
+  launch_passes(a, batch, 0, s);
+}
+
+void launch_rfft_out_acc(const DevSide& side, const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows,
+                         std::uint32_t zacc_cols, const float zscale[2], const int ze8p[2], const float* alpha,
+                         const long long* tl, float* u_scratch, float* y, int batch, cudaStream_t s) {
+  if (batch <= 0) return;
+  RfftArgs a{};
+  plan(side, a);
+  a.in = nullptr;
+  a.mid = reinterpret_cast<float2*>(u_scratch);
+  a.out = y;
+  a.fwd = 0;
+  a.k.zacc = zacc;
+  a.k.zrows = zacc_rows;
+  a.k.zcols = zacc_cols;
+  a.k.zstages = zacc_stages;
+  a.k.zscale0 = zscale[0];
+  a.k.zscale1 = zscale[1];
+  a.k.ze8p0 = ze8p[0];
+  a.k.ze8p1 = ze8p[1];
+  a.k.alpha_in = alpha;
+  a.k.tl_in = tl;
+  // every k2 split of a tile re-combines the tile from the accumulators (int64 /
+  // double arithmetic): keep the splits few
+  a.ks1 = std::min<std::uint32_t>(a.ks1, 2);
   launch_passes(a, batch, 0, s);
 }
 

@@ -734,9 +734,9 @@ void launch_rht_out_acc(const DevSide& side, const std::int32_t* zacc, int zacc_
                         std::uint32_t zacc_cols, const float zscale[2], const int ze8p[2], const float* alpha,
                         const long long* tl, float* u_scratch, float* y, int batch, cudaStream_t s) {
   if (batch <= 0) return;
-  if (side.kind == 1) {  // rfft: z (into y) from the accumulators, then the two DFT passes y -> u -> y
-    launch_combine_acc(zacc, zacc_stages, zacc_rows, zacc_cols, zscale, ze8p, alpha, tl, y, side.n, batch, s);
-    launch_rfft_f32(side, y, u_scratch, y, batch, true, s);
+  if (side.kind == 1) {  // rfft: pass 1 combines z from the accumulators itself
+    launch_rfft_out_acc(side, zacc, zacc_stages, zacc_rows, zacc_cols, zscale, ze8p, alpha, tl, u_scratch, y, batch,
+                        s);
     return;
   }
   RhtArgs a{};

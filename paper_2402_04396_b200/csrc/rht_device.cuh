@@ -150,6 +150,30 @@ __device__ __forceinline__ float4 combine4(const RhtArgs& a, int b, std::uint32_
   return make_float4(float(acc[0]), float(acc[1]), float(acc[2]), float(acc[3]));
 }
 
+// z rows i, i + 1 (i even) of vector b: combine4's arithmetic on an aligned pair
+// (the rfft K3 reads complex pairs).
+__device__ __forceinline__ float2 combine2(const RhtArgs& a, int b, std::uint32_t i) {
+  const double al = double(__ldcg(a.alpha_in + b)) * 0.25;
+  const long long tl = __ldcg(a.tl_in + b);
+  double acc[2] = {0.0, 0.0};
+  for (int st = 0; st < a.zstages; ++st) {
+    const std::int32_t* z = a.zacc + (std::size_t(st) * a.zcols + 4 * b) * a.zrows + i;
+    const int2 v0 = __ldcg(reinterpret_cast<const int2*>(z));
+    const int2 v1 = __ldcg(reinterpret_cast<const int2*>(z + a.zrows));
+    const int2 v2 = __ldcg(reinterpret_cast<const int2*>(z + 2 * std::size_t(a.zrows)));
+    const int2 v3 = __ldcg(reinterpret_cast<const int2*>(z + 3 * std::size_t(a.zrows)));
+    const long long sub = (st == 0 ? a.ze8p0 : a.ze8p1) ? tl : 0;
+    const double c = al * double(st == 0 ? a.zscale0 : a.zscale1);
+    auto zt = [&](int x0, int x1, int x2, int x3) {
+      const long long Z = ((static_cast<long long>(x0) * 128 + x1) * 128 + x2) * 128 + x3;
+      return double(2 * Z - sub) * c;
+    };
+    acc[0] += zt(v0.x, v1.x, v2.x, v3.x);
+    acc[1] += zt(v0.y, v1.y, v2.y, v3.y);
+  }
+  return make_float2(float(acc[0]), float(acc[1]));
+}
+
 
 // Pass-1 smem bytes for chunk P2 * Q (x, base output, base).
 template <int Q>
