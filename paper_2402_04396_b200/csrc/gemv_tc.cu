@@ -123,7 +123,7 @@ struct Roles {
   template <int N>
   // B-image ring slots per group.  >= 2: the issuer refills the slot of item
   // k - 1 with item k - 1 + kBg after issuing item k, so one slot would deadlock.
-  static constexpr std::uint32_t kBg = N <= 8 ? 3 : 2;
+  static constexpr std::uint32_t kBg = N <= 8 || N >= 128 ? 3 : 2;
 };
 
 struct TcArgs {
@@ -250,7 +250,13 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
   const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const std::uint32_t sbase = smem_u32(smem);
   const std::uint32_t send = sbase + a.smem_bytes - a.scratch_bytes;  // RHT scratch above the ring
-  const std::uint32_t lutw = (sbase + kCtl + 0xFFFFu) & ~0xFFFFu;
+  // B ring: [group][slot], b_slot bytes per k-slab image
+  const std::uint32_t b_slot = (a.b_bytes + 127) & ~127u;
+  constexpr std::uint32_t SBg = Roles<G>::template kBg<N>, SB = SBg * G;
+  // smem layout.  N <= 64: [ctl][code slots][LUT window, 64 KiB aligned][B ring][code slots].
+  // N = 128 (36 KB B slots, 3 deep): [ctl][B ring][code slot(s)][LUT window][code slots].
+  constexpr bool kBLow = N >= 128;
+  const std::uint32_t lutw = (sbase + kCtl + (kBLow ? SB * b_slot : 0u) + 0xFFFFu) & ~0xFFFFu;
   // control block: barriers + TMEM base
   const std::uint32_t bar_full_c = sbase;                       // [kMaxStages] code slab landed
   const std::uint32_t bar_empty_c = sbase + 8 * kMaxStages;     // [kMaxStages] code slab read (4 warps)
@@ -263,14 +269,11 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
   const std::uint32_t bar_lut = bar_d_empty + 8 * G;            // LUT window landed
   const std::uint32_t tmem_slot = bar_lut + 8;
   const std::uint32_t ct_slot = tmem_slot + 8;  // the constant byte table, read back by the decoders
-  // B ring right above the LUT window; code ring below the window, then above the B ring
-  const std::uint32_t b_slot = (a.b_bytes + 127) & ~127u;
-  constexpr std::uint32_t SBg = Roles<G>::template kBg<N>, SB = SBg * G;  // B ring: [group][slot]
   constexpr int kWarpDec = Roles<G>::kWarpDec;
-  const std::uint32_t b_base = lutw + 65536;
-  const std::uint32_t lo_base = sbase + kCtl;
+  const std::uint32_t b_base = kBLow ? sbase + kCtl : lutw + 65536;
+  const std::uint32_t lo_base = sbase + kCtl + (kBLow ? SB * b_slot : 0u);
   const std::uint32_t n_lo = lutw > lo_base ? (lutw - lo_base) / kCodeSlot : 0;
-  const std::uint32_t hi_base = b_base + SB * b_slot;
+  const std::uint32_t hi_base = kBLow ? lutw + 65536 : b_base + SB * b_slot;
   if (hi_base > send) __trap();  // B ring past the dynamic smem (host sizing bug): fail loudly
   std::uint32_t S = n_lo + (send > hi_base ? (send - hi_base) / kCodeSlot : 0);
   if (S > kMaxStages) S = kMaxStages;
