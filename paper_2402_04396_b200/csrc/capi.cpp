@@ -293,6 +293,15 @@ int tc_chunk(const q8p_layer* L, int batch) {
   return 0;  // portable path
 }
 
+// Batches of several whole chunks run K1 once for all vectors (B images per chunk),
+// then K2 + K3 per chunk with K3 clearing the accumulators it read (multi-chunk K1).
+bool multi_chunk_k1(const q8p_layer* L, int batch) {
+  static const bool off = std::getenv("Q8P_NO_MULTI_K1") != nullptr;  // experiment knob
+  const int chunk = tc_chunk(L, batch);
+  return !off && chunk > 0 && batch > chunk && batch % chunk == 0 && L->side_v.kind == 0 && L->side_u.kind == 0 &&
+         (L->n / 8) % 32 == 0;
+}
+
 std::size_t workspace_parts(const q8p_layer* L, int batch, Workspace* w, void* base) {
   auto* p0 = static_cast<std::uint8_t*>(base);
   std::size_t off = 0;
@@ -303,17 +312,19 @@ std::size_t workspace_parts(const q8p_layer* L, int batch, Workspace* w, void* b
   };
   const int chunk = tc_chunk(L, batch);
   const bool tc = chunk > 0;
-  if (tc) batch = chunk;  // the workspace holds one chunk
+  const bool multi = multi_chunk_k1(L, batch);
+  const std::size_t BK = std::size_t(multi ? batch : chunk);  // vectors of one K1 launch
+  if (tc) batch = chunk;  // otherwise the workspace holds one chunk
   const std::size_t B = std::size_t(batch), mx = std::max(L->n, L->m);
   Workspace v{};
   v.rows_pad = rows_pad_of(L);
   v.zcols = std::uint32_t(tc_ncols_pad(4 * batch));
-  v.u = reinterpret_cast<float*>(take(B * mx * 4));
+  v.u = reinterpret_cast<float*>(take((tc ? BK : B) * mx * 4));  // transform scratch of one K1 launch
   if (tc) {
-    v.ssq = reinterpret_cast<float*>(take(B * std::max<std::size_t>(64, L->n / 4) * 4));
-    v.alpha = reinterpret_cast<float*>(take(B * 4));
-    v.tl = reinterpret_cast<long long*>(take(B * 8));
-    v.bimg = take(tc_bimg_bytes(L->n, batch));
+    v.ssq = reinterpret_cast<float*>(take(BK * std::max<std::size_t>(64, L->n / 4) * 4));
+    v.alpha = reinterpret_cast<float*>(take(BK * 4));
+    v.tl = reinterpret_cast<long long*>(take(BK * 8));
+    v.bimg = take(tc_bimg_bytes(L->n, batch) * (BK / B));
     v.zacc = reinterpret_cast<std::int32_t*>(take(std::size_t(L->num_stages) * v.zcols * v.rows_pad * 4));
     v.z_full = reinterpret_cast<float*>(take(B * L->m * 4));  // q8p_forward_sharded
     if (L->row_begin != 0 || L->row_end != L->m) v.z_loc = reinterpret_cast<float*>(take(B * L->m_local() * 4));
@@ -423,6 +434,20 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
   if (const int chunk = tc_chunk(L, batch)) {
     float zscale[2] = {L->scale[0], L->scale[1]};
     int ze8p[2] = {L->cb[0] == Q8P_CB_E8P_2BIT, L->cb[1] == Q8P_CB_E8P_2BIT};
+    if (multi_chunk_k1(L, batch)) {
+      const std::uint32_t N = std::uint32_t(tc_ncols_pad(4 * chunk)), bb = 9u * N * 32u;
+      const std::size_t cb = std::size_t(tc_k_slabs(L->n)) * bb;  // one chunk's B images
+      launch_rht_in_limbs(L->side_v, x, w.u, w.ssq, w.alpha, w.tl, w.bimg, bb, N, nullptr, 0, w.zacc,
+                          std::size_t(L->num_stages) * N * w.rows_pad, batch, s, std::uint32_t(chunk), cb);
+      for (int b0 = 0, c = 0; b0 < batch; b0 += chunk, ++c) {
+        if (opts && c == 0) record_event(opts->gemv_start_event, s);
+        launch_gemv_tc(*L, w.bimg + std::size_t(c) * cb, w.zacc, w.rows_pad, chunk, s);
+        if (opts && c == 0) record_event(opts->gemv_end_event, s);
+        launch_rht_out_acc(L->side_u, w.zacc, L->num_stages, w.rows_pad, N, zscale, ze8p, w.alpha + b0, w.tl + b0,
+                           w.u, y + std::size_t(b0) * L->m, chunk, s, /*zero_after=*/b0 + chunk < batch);
+      }
+      return;
+    }
     for (int b0 = 0; b0 < batch; b0 += chunk) {  // one pass for batch <= kTcMaxBatch
       const int nb = std::min(chunk, batch - b0);
       forward_local(L, x + std::size_t(b0) * L->n, nb, w, s, b0 == 0 ? opts : nullptr);

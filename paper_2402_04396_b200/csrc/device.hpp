@@ -141,7 +141,8 @@ void launch_rht_in(const DevSide& side, const float* x, float* t, float* u_scrat
 void launch_rht_in_limbs(const DevSide& side, const float* x, float* u_scratch, float* ssq, float* alpha,
                          long long* tl, std::uint8_t* bimg, std::uint32_t b_bytes, std::uint32_t bcols,
                          std::uint8_t* bimg_tail, std::size_t tail_bytes, std::int32_t* zero_ptr,
-                         std::size_t zero_words, int batch, cudaStream_t s);
+                         std::size_t zero_words, int batch, cudaStream_t s, std::uint32_t chunk_vec = 0,
+                         std::size_t chunk_bytes = 0);
 // Fused layer kernel (gemv_tc.cu): K1 + K2 (+ K3 when y != nullptr) in one persistent launch.
 bool tc_fused_supported(const q8p_layer& L, int batch);
 void launch_layer_fused(const q8p_layer& L, const float* x, float* y, float* u_scratch, float* ssq, float* alpha,
@@ -173,6 +174,7 @@ void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, flo
 // limb accumulators [stage][zacc_cols][zacc_rows], then y = T_u^T z.
 void launch_rht_out_acc(const DevSide& side, const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows,
                         std::uint32_t zacc_cols, const float zscale[2], const int ze8p[2], const float* alpha,
-                        const long long* tl, float* u_scratch, float* y, int batch, cudaStream_t s);
+                        const long long* tl, float* u_scratch, float* y, int batch, cudaStream_t s,
+                        bool zero_after = false);
 
 }  // namespace q8p::detail

@@ -693,9 +693,11 @@ void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, flo
 void launch_rht_in_limbs(const DevSide& side, const float* x, float* u_scratch, float* ssq, float* alpha,
                          long long* tl, std::uint8_t* bimg, std::uint32_t b_bytes, std::uint32_t bcols,
                          std::uint8_t* bimg_tail, std::size_t tail_bytes, std::int32_t* zero_ptr,
-                         std::size_t zero_words, int batch, cudaStream_t s) {
+                         std::size_t zero_words, int batch, cudaStream_t s, std::uint32_t chunk_vec,
+                         std::size_t chunk_bytes) {
   if (batch <= 0) return;
   if (side.kind == 1) {
+    if (chunk_vec) throw UnsupportedError("rfft: multi-chunk K1");
     launch_rfft_in_limbs(side, x, u_scratch, ssq, alpha, tl, bimg, b_bytes, bcols, bimg_tail, tail_bytes, zero_ptr,
                          zero_words, batch, s);
     return;
@@ -718,6 +720,8 @@ void launch_rht_in_limbs(const DevSide& side, const float* x, float* u_scratch, 
   a.zero2_bytes = tail_bytes;
   a.batch = batch;
   a.fwd = 1;
+  a.chunk_vec = chunk_vec;
+  a.chunk_bytes = chunk_bytes;
   if (single_ok(side)) {
     launch_single<kSingleK1>(a, (zero_ptr && zero_words) || (bimg_tail && tail_bytes) ? 16 : 0, s);
     return;
@@ -732,7 +736,8 @@ void launch_rht_in_limbs(const DevSide& side, const float* x, float* u_scratch, 
 
 void launch_rht_out_acc(const DevSide& side, const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows,
                         std::uint32_t zacc_cols, const float zscale[2], const int ze8p[2], const float* alpha,
-                        const long long* tl, float* u_scratch, float* y, int batch, cudaStream_t s) {
+                        const long long* tl, float* u_scratch, float* y, int batch, cudaStream_t s,
+                        bool zero_after) {
   if (batch <= 0) return;
   if (side.kind == 1) {  // rfft: pass 1 combines z from the accumulators itself
     launch_rfft_out_acc(side, zacc, zacc_stages, zacc_rows, zacc_cols, zscale, ze8p, alpha, tl, u_scratch, y, batch,
@@ -757,6 +762,13 @@ void launch_rht_out_acc(const DevSide& side, const std::int32_t* zacc, int zacc_
   a.out = y;
   a.batch = batch;
   a.fwd = 0;
+  a.zacc_zero = zero_after ? 1 : 0;
+  if (zero_after) {  // the two-pass kernels clear what they read
+    if (side.kind == 1) throw UnsupportedError("rfft: zero-after K3");
+    launch_pass1(a, 0, s);
+    launch_pass2(a, s);
+    return;
+  }
   if (single_ok(side)) {
     launch_single<kSingleK3Acc>(a, 0, s);
     return;

@@ -45,6 +45,11 @@ struct RhtArgs {
   std::size_t zero2_bytes;
   int batch;
   int fwd;
+  // multi-chunk K1 (batches above the GEMV's 32 vectors): vector b's B images go to
+  // chunk b / chunk_vec (chunk_bytes apart) as local column b % chunk_vec; 0 = off
+  std::uint32_t chunk_vec;
+  std::size_t chunk_bytes;
+  int zacc_zero;                // K3 pass 1: zero the accumulators after reading them (next chunk's K2)
 };
 
 struct Team {
@@ -204,6 +209,12 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* sm
     float4 val;
     if (a.zacc) {
       val = combine4(a, b, i);
+      if (a.zacc_zero) {  // each (vector, row quad) is read by exactly one thread: clear it for the next chunk
+        for (int st = 0; st < a.zstages; ++st)
+          for (int l = 0; l < 4; ++l)
+            *reinterpret_cast<int4*>(const_cast<std::int32_t*>(a.zacc) +
+                                     (std::size_t(st) * a.zcols + 4 * b + l) * a.zrows + i) = make_int4(0, 0, 0, 0);
+      }
     } else {
       val = __ldcg(reinterpret_cast<const float4*>(a.in + std::size_t(b) * a.n + i));
       ss += val.x * val.x + val.y * val.y + val.z * val.z + val.w * val.w;
@@ -338,9 +349,14 @@ __device__ __forceinline__ long long emit_limbs(const RhtArgs& a, int b, std::ui
   limbs4(qk, ql);
   const std::uint32_t ks = k >> 5, j = k & 31, kb = j >> 2;
   std::uint8_t* slab = a.bimg + std::size_t(ks) * a.b_bytes;
+  std::uint32_t bl = std::uint32_t(b);
+  if (a.chunk_vec) {
+    slab += std::size_t(bl / a.chunk_vec) * a.chunk_bytes;
+    bl %= a.chunk_vec;
+  }
 #pragma unroll
   for (int l = 0; l < 4; ++l) {
-    const std::uint32_t row = 4 * b + l;
+    const std::uint32_t row = 4 * bl + l;
     const std::uint32_t rowoff = (row >> 3) * 256 + (row & 7) * 16;
     // main: K-block kb, K bytes 8 (j % 4) .. +7 -> chunk (j % 4) / 2, offset 8 (j % 2)
     *reinterpret_cast<uint2*>(slab + kb * N * 32 + rowoff + ((j & 3) >> 1) * 128 + (j & 1) * 8) =

@@ -26,7 +26,7 @@ def dev():
 
 
 @pytest.mark.parametrize("bits", [2, 3, 4])
-@pytest.mark.parametrize("batch", [1, 2, 3, 4, 8, 13, 16, 17, 24, 32, 40, 70])
+@pytest.mark.parametrize("batch", [1, 2, 3, 4, 8, 13, 16, 17, 24, 32, 40, 64, 70, 96])
 def test_batches_vs_oracle(dev, oracle, bits, batch):
     m, n = 1024, 2048
     art = random_artifact(m, n, STAGES[bits], 100 * bits + batch)
@@ -34,7 +34,7 @@ def test_batches_vs_oracle(dev, oracle, bits, batch):
     x = np.random.default_rng(batch).standard_normal((batch, n)).astype(np.float32).astype(np.float64)
     want = oracle.infer(art, x, threads=8)
     got = L.forward(torch.from_numpy(x.astype(np.float32)).to(dev)).cpu().numpy()
-    bar = TC  # batches 17..32 run with MMA N = 128; above 32 as 32-vector chunks
+    bar = TC  # batches 17..32 run with MMA N = 128; above 32 as 32-vector chunks (one K1 when whole)
     for b in range(batch):
         assert rel_err(got[b], want[b]) < bar, (b, rel_err(got[b], want[b]))
 
@@ -54,14 +54,14 @@ def test_batched_equals_single_all_variants(dev):
     # single-vector call bit for bit, whatever N / group variant the batch picks
     art = random_artifact(512, 1024, STAGES[3], 5)
     L = q8p.Layer.from_qshp(art)
-    x = torch.randn(32, 1024, generator=torch.Generator().manual_seed(1)).to(dev)
-    for batch in (2, 4, 8, 16, 20, 32):
+    x = torch.randn(96, 1024, generator=torch.Generator().manual_seed(1)).to(dev)
+    for batch in (2, 4, 8, 16, 20, 32, 64, 96):  # 64 / 96: one K1 for all chunks
         y = L.forward(x[:batch].contiguous())
         for b in (0, batch - 1):
             assert torch.equal(y[b], L.forward(x[b:b + 1].contiguous())[0])
 
 
-@pytest.mark.parametrize("batch", [4, 8, 16, 32, 40])
+@pytest.mark.parametrize("batch", [4, 8, 16, 32, 40, 64])
 def test_large_layer_all_batch_variants(dev, oracle, batch):
     # many items per CTA at every N variant (the B-image ring wraps several times)
     m, n = 4096, 8192

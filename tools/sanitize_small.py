@@ -13,7 +13,7 @@ for tr in (0, 1):
     for bits in (2, 3, 4):
         art = random_artifact(384, 512, ST[bits], bits, transform=tr)
         L = q8p.Layer.from_qshp(art)
-        for b in (1, 5, 20, 40):
+        for b in (1, 5, 20, 40, 64):
             y = L.forward(torch.randn(b, 512).cuda())
         z = q8p.Layer.from_qshp(art, rows=(128, 256)).rows_z(torch.randn(3, 512).cuda())
 torch.cuda.synchronize()
