@@ -633,8 +633,13 @@ void forward_set_impl(const q8p_layer* const* layers, int count, const float* co
 // when it returns, no sync).  The copies run on a side stream: layer i waits only
 // for its own input, and y_i goes back while later layers compute, so only the
 // first input and the last output are exposed.
+// x0_mapped / ylast_mapped (device addresses of pinned host memory, or nullptr):
+// the first layer's K1 reads its x straight from the host buffer and the last
+// layer's K3 writes its y straight into it, so neither end of the step waits for
+// a copy-engine round trip; the other layers' copies overlap the kernels.
 void forward_set_host_enqueue(const q8p_layer* const* layers, int count, const float* xh, float* yh, int batch,
-                              void* ws, std::size_t ws_bytes, cudaStream_t s, unsigned flags) {
+                              void* ws, std::size_t ws_bytes, cudaStream_t s, unsigned flags,
+                              const float* x0_mapped = nullptr, float* ylast_mapped = nullptr) {
   auto* stage = static_cast<std::uint8_t*>(ws) + set_stage_offset(layers, count, batch, flags);
   std::size_t nsum = 0;
   for (int i = 0; i < count; ++i) nsum += layers[i]->n;
@@ -666,19 +671,24 @@ void forward_set_host_enqueue(const q8p_layer* const* layers, int count, const f
   std::size_t xo = 0;
   for (int i = 0; i < count; ++i) {
     const std::size_t nb = std::size_t(batch) * layers[i]->n;
-    cuda_check(cudaMemcpyAsync(dx + xo, xh + xo, nb * 4, cudaMemcpyHostToDevice, aux.side), "set H2D");
-    cuda_check(cudaEventRecord(aux.ev[2 + i], aux.side), "H2D event");
+    if (!(i == 0 && x0_mapped)) {
+      cuda_check(cudaMemcpyAsync(dx + xo, xh + xo, nb * 4, cudaMemcpyHostToDevice, aux.side), "set H2D");
+      cuda_check(cudaEventRecord(aux.ev[2 + i], aux.side), "H2D event");
+    }
     xo += nb;
   }
   xo = 0;
   std::size_t yo = 0;
   for (int i = 0; i < count; ++i) {
     const std::size_t nb = std::size_t(batch) * layers[i]->n, mb = std::size_t(batch) * layers[i]->m;
-    cuda_check(cudaStreamWaitEvent(s, aux.ev[2 + i], 0), "H2D wait");
-    forward_impl(layers[i], dx + xo, dy + yo, batch, ws, ws_bytes, s);
-    cuda_check(cudaEventRecord(aux.ev[2 + count + i], s), "layer event");
-    cuda_check(cudaStreamWaitEvent(aux.side, aux.ev[2 + count + i], 0), "layer wait");
-    cuda_check(cudaMemcpyAsync(yh + yo, dy + yo, mb * 4, cudaMemcpyDeviceToHost, aux.side), "set D2H");
+    const bool xin = i == 0 && x0_mapped, yout = i == count - 1 && ylast_mapped;
+    if (!xin) cuda_check(cudaStreamWaitEvent(s, aux.ev[2 + i], 0), "H2D wait");
+    forward_impl(layers[i], xin ? x0_mapped : dx + xo, yout ? ylast_mapped + yo : dy + yo, batch, ws, ws_bytes, s);
+    if (!yout) {
+      cuda_check(cudaEventRecord(aux.ev[2 + count + i], s), "layer event");
+      cuda_check(cudaStreamWaitEvent(aux.side, aux.ev[2 + count + i], 0), "layer wait");
+      cuda_check(cudaMemcpyAsync(yh + yo, dy + yo, mb * 4, cudaMemcpyDeviceToHost, aux.side), "set D2H");
+    }
     xo += nb;
     yo += mb;
   }
@@ -725,12 +735,15 @@ void forward_set_host_impl(const q8p_layer* const* layers, int count, const floa
   // experiment knob: zero-copy (kernels read x / write y in pinned host memory over
   // PCIe) measured no faster than the overlapped copies (109-111 us per 70B step)
   static const bool zero_copy = std::getenv("Q8P_SET_ZERO_COPY") != nullptr;
+  static const bool no_ends = std::getenv("Q8P_SET_COPY_ENDS") != nullptr;  // experiment knob
   const bool mapped = dxh && dyh && zero_copy;
+  const bool ends = dxh && dyh && !no_ends && !(flags & Q8P_SET_CONCURRENT);
   auto enqueue = [&](cudaStream_t st) {
     if (mapped)
       forward_set_mapped_enqueue(layers, count, dxh, dyh, batch, ws, ws_bytes, st);
     else
-      forward_set_host_enqueue(layers, count, xh, yh, batch, ws, ws_bytes, st, flags);
+      forward_set_host_enqueue(layers, count, xh, yh, batch, ws, ws_bytes, st, flags, ends ? dxh : nullptr,
+                               ends ? dyh : nullptr);
   };
   if (no_graph || cap != cudaStreamCaptureStatusNone || !dxh || !dyh || dev < 0 || dev >= 64) {
     enqueue(s);
