@@ -45,17 +45,17 @@ def test_rfft_forward_vs_oracle(dev, oracle, m, n, bits):
 
 @pytest.mark.gpu
 def test_rfft_batches_and_portable_path(dev, oracle):
-    # batch 1..17 (17: tensor-core chunks of 16 + 1) and an e8-1bit-first artifact
+    # batch 1..64 (17-32: MMA N = 128, 64: two chunks) and an e8-1bit-first artifact
     # (no tensor-core path: the portable GEMV between the rfft passes)
     import torch
 
     import paper_2402_04396_b200 as q8p
 
     art = random_artifact(256, 512, STAGES[3], 7, transform=1)
-    x = np.random.default_rng(6).standard_normal((17, 512)).astype(np.float32).astype(np.float64)
+    x = np.random.default_rng(6).standard_normal((64, 512)).astype(np.float32).astype(np.float64)
     want = oracle.infer(art, x)
     L = q8p.Layer.from_qshp(art)
-    for nb in (1, 3, 8, 16, 17):
+    for nb in (1, 3, 8, 16, 17, 32, 64):  # 32: MMA N = 128; 64: 32-vector chunks
         got = L.forward(torch.from_numpy(x[:nb].astype(np.float32)).to(dev)).cpu().numpy()
         assert rel_err(got, want[:nb]) < TC, (nb, rel_err(got, want[:nb]))
     art2 = random_artifact(128, 256, [("e8-1bit", 0.7)], 8, transform=1)
