@@ -181,6 +181,12 @@ q8p_status q8p_forward_set_host_ex(const q8p_layer* const* layers, int count, co
                                    float* y_host, int batch, void* workspace, size_t workspace_bytes,
                                    void* stream, unsigned flags);
 
+/* e8p_encode (core/src/e8p.cpp:114-156) on `device`, bit-identical to the
+ * reference: v = device f64 [nblocks][8] -> words = device uint16 [nblocks],
+ * the nearest E8P codeword of each 8-vector (ties to the smaller word).  The
+ * inner search of the offline producer (RvqQuantizer::quantize, rvq.cpp). */
+q8p_status q8p_e8p_encode(const double* v, uint16_t* words, size_t nblocks, int device, void* stream);
+
 /* latq::infer drop-in: host f64 x [batch][n] -> host f64 y [batch][m].
  * Synchronous; stages through an internal pinned buffer and workspace. */
 q8p_status q8p_infer_host(q8p_layer* layer, const double* x, double* y, int batch);

@@ -21,7 +21,7 @@ __all__ = [
     "LayerSet", "Error", "SizeError", "ValidationError", "FormatError", "BadMagicError",
     "UnsupportedVersionError", "TruncatedArtifactError", "UnsupportedError", "DeviceError",
     "lib", "plan_hadamard", "hadamard_base", "codebook_table", "e8p_decode_host",
-    "inspect_artifact", "reserialize", "Layer", "rht", "kernel_launches",
+    "inspect_artifact", "reserialize", "Layer", "rht", "kernel_launches", "e8p_encode",
     "CB_E8P_2BIT", "CB_E8_1BIT", "NcclError", "shard_rows", "NcclComm",
 ]
 
@@ -129,6 +129,7 @@ _SIGNATURES = {
     "q8p_forward_rows_z": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "q8p_forward_sharded": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]),
     "q8p_infer_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
+    "q8p_e8p_encode": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]),
     "q8p_forward_set_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
     "q8p_forward_set_workspace_bytes_ex": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_uint]),
     "q8p_forward_set_ex": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
@@ -489,6 +490,17 @@ class LayerSet:
         if st:
             _check(st)
         return y_host
+
+
+def e8p_encode(v, stream=None):
+    """Nearest E8P codewords of a float64 CUDA tensor [nblocks, 8] (reference
+    e8p_encode, bit-identical) -> int32 tensor [nblocks] of 16-bit words."""
+    torch = _torch()
+    if v.dtype != torch.float64 or not v.is_cuda or not v.is_contiguous() or v.dim() != 2 or v.shape[1] != 8:
+        raise ValidationError("v must be a contiguous float64 CUDA tensor [nblocks, 8]")
+    out = torch.empty(v.shape[0], dtype=torch.int16, device=v.device)
+    _check(lib().q8p_e8p_encode(v.data_ptr(), out.data_ptr(), v.shape[0], v.device.index or 0, _stream_ptr(stream)))
+    return out.to(torch.int32) & 0xFFFF
 
 
 def rht(x, signs, transpose: bool = False, out=None, stream=None):

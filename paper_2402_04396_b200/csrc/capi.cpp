@@ -978,6 +978,19 @@ q8p_status q8p_forward_set_host(const q8p_layer* const* layers, int count, const
   return q8p_forward_set_host_ex(layers, count, x_host, y_host, batch, ws, ws_bytes, stream, 0);
 }
 
+q8p_status q8p_e8p_encode(const double* v, uint16_t* words, size_t nblocks, int device, void* stream) {
+  try {
+    if (nblocks == 0) return Q8P_OK;
+    if (!v || !words) throw q8p::ValidationError("null v / words");
+    require_sm100(device);
+    DeviceGuard g(device);
+    launch_e8p_encode(v, words, nblocks, static_cast<cudaStream_t>(stream));
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
 q8p_status q8p_infer_host(q8p_layer* L, const double* x, double* y, int batch) {
   try {
     if (!L || !x || !y) throw q8p::ValidationError("null argument");

@@ -119,6 +119,8 @@ void launch_rht(const DevSide& side, const float* x, float* y, int batch, bool t
 void launch_gemv_simple(const q8p_layer& L, const float* t, float* z, int batch, int z_stride,
                         cudaStream_t s);
 void launch_decode(const q8p_layer& L, int stage, float* w, cudaStream_t s);
+// e8p_encode (core/src/e8p.cpp:114-156) on device, bit-identical: v [nblocks][8] f64 -> words.
+void launch_e8p_encode(const double* v, std::uint16_t* words, std::size_t nblocks, cudaStream_t s);
 
 // Tensor-core path (gemv_tc.cu, kernels_rht.cu).
 std::vector<std::uint8_t> tc_lut_image();  // the 64 KiB smem LUT window, bulk-copied per CTA

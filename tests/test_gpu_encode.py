@@ -1,0 +1,38 @@
+"""GPU E8P encoder (q8p_e8p_encode) vs the reference e8p_encode
+(core/src/e8p.cpp:114-156, compiled in place): bit-identical words, including
+inputs on the quarter-integer grid where distance ties decide by the smaller word."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2402_04396_b200 as q8p
+
+pytestmark = pytest.mark.gpu
+
+
+def _inputs():
+    rng = np.random.default_rng(0)
+    parts = [rng.standard_normal((4000, 8)) * s for s in (0.3, 1.0, 2.0, 4.0)]
+    parts.append(rng.integers(-12, 13, (4000, 8)) / 4.0)   # quarter-integer grid: exact ties
+    parts.append(rng.integers(-6, 7, (2000, 8)) / 2.0)
+    parts.append(np.zeros((4, 8)))
+    return np.concatenate(parts)
+
+
+def test_encode_bit_identical_to_reference(ref):
+    v = _inputs()
+    got = q8p.e8p_encode(torch.from_numpy(v).cuda()).cpu().numpy()
+    want = np.array([ref.e8p_encode(b) for b in v], dtype=np.int64)
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, (bad[:5], got[bad[:5]], want[bad[:5]])
+
+
+def test_encode_decode_round_trip():
+    # encoding an exactly representable codeword returns it (its distance is 0)
+    words = np.random.default_rng(1).integers(0, 65536, 5000)
+    pts = np.stack([q8p.e8p_decode_host(int(w)) for w in words]).astype(np.float64)
+    got = q8p.e8p_encode(torch.from_numpy(pts).cuda()).cpu().numpy()
+    back = np.stack([q8p.e8p_decode_host(int(w)) for w in got]).astype(np.float64)
+    assert np.array_equal(back, pts)
