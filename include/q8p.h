@@ -186,6 +186,13 @@ q8p_status q8p_forward_set_host_ex(const q8p_layer* const* layers, int count, co
  * the nearest E8P codeword of each 8-vector (ties to the smaller word).  The
  * inner search of the offline producer (RvqQuantizer::quantize, rvq.cpp). */
 q8p_status q8p_e8p_encode(const double* v, uint16_t* words, size_t nblocks, int device, void* stream);
+/* RvqQuantizer::quantize (rvq.cpp:59-79) for every 8-vector, bit-identical:
+ * per stage scaled = residual / scale_s, code = the codebook's nearest word,
+ * residual -= scale_s * decode(code).  v = device f64 [nblocks][8], codes =
+ * device uint16 [num_stages][nblocks].  With the H = I nearest rounding
+ * (ldlq.cpp:128-226, u = nullptr) this is the producer's whole code search. */
+q8p_status q8p_rvq_quantize(const double* v, uint16_t* codes, size_t nblocks, int num_stages,
+                            const q8p_codebook* codebooks, const double* scales, int device, void* stream);
 
 /* latq::infer drop-in: host f64 x [batch][n] -> host f64 y [batch][m].
  * Synchronous; stages through an internal pinned buffer and workspace. */

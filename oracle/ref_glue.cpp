@@ -360,6 +360,24 @@ int ref_side_apply(std::size_t n, const std::uint8_t* sign_bytes, double* x, int
   }
 }
 
+// RvqQuantizer(default_scheme(bits), scales).quantize on `count` 8-vectors
+// (rvq.cpp:59-79) -> codes [stage][count].
+int ref_rvq_quantize(int bits, const double* scales, const double* v, std::size_t count, std::uint16_t* codes) {
+  try {
+    const latq::RvqScheme scheme = latq::default_scheme(bits);
+    const latq::RvqQuantizer q(scheme, std::vector<double>(scales, scales + scheme.size()));
+    std::vector<double> out(8);
+    std::vector<std::uint16_t> w(scheme.size());
+    for (std::size_t i = 0; i < count; ++i) {
+      q.quantize(std::span<const double>(v + 8 * i, 8), out, w.data(), i);
+      for (std::size_t s = 0; s < scheme.size(); ++s) codes[s * count + i] = w[s];
+    }
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
 // rfft_apply (rfft.cpp:39-71) on one vector with the given n/2 phases.
 int ref_rfft_apply(std::size_t n, const double* phases, double* x, int transpose) {
   try {

@@ -64,6 +64,7 @@ class Ref:
         L.ref_gen_weights.argtypes = [ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint64, _P]
         L.ref_random_signs.argtypes = [ctypes.c_size_t, ctypes.c_uint64, _P]
         L.ref_rfft_apply.argtypes = [ctypes.c_size_t, _P, _P, ctypes.c_int]
+        L.ref_rvq_quantize.argtypes = [ctypes.c_int, _P, _P, ctypes.c_size_t, _P]
         L.ref_random_phases.argtypes = [ctypes.c_size_t, ctypes.c_uint64, _P]
         L.ref_artifact_info.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_uint32),
                                         ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int)]
@@ -177,6 +178,13 @@ class Ref:
         assert ph.size == y.size // 2
         self._ck(self.L.ref_rfft_apply(y.size, _ptr(ph), _ptr(y), int(transpose)))
         return y
+
+    def rvq_quantize(self, bits: int, scales, v: np.ndarray) -> np.ndarray:
+        v = np.ascontiguousarray(v, dtype=np.float64).reshape(-1, 8)
+        sc = np.ascontiguousarray(scales, dtype=np.float64)
+        out = np.zeros((sc.size, v.shape[0]), dtype=np.uint16)
+        self._ck(self.L.ref_rvq_quantize(bits, _ptr(sc), _ptr(v), v.shape[0], _ptr(out)))
+        return out
 
     def random_phases(self, n: int, seed: int) -> np.ndarray:
         out = np.zeros(n // 2)

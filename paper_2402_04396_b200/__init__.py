@@ -21,7 +21,7 @@ __all__ = [
     "LayerSet", "Error", "SizeError", "ValidationError", "FormatError", "BadMagicError",
     "UnsupportedVersionError", "TruncatedArtifactError", "UnsupportedError", "DeviceError",
     "lib", "plan_hadamard", "hadamard_base", "codebook_table", "e8p_decode_host",
-    "inspect_artifact", "reserialize", "Layer", "rht", "kernel_launches", "e8p_encode",
+    "inspect_artifact", "reserialize", "Layer", "rht", "kernel_launches", "e8p_encode", "rvq_quantize",
     "CB_E8P_2BIT", "CB_E8_1BIT", "NcclError", "shard_rows", "NcclComm",
 ]
 
@@ -130,6 +130,8 @@ _SIGNATURES = {
     "q8p_forward_sharded": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]),
     "q8p_infer_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
     "q8p_e8p_encode": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]),
+    "q8p_rvq_quantize": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
     "q8p_forward_set_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
     "q8p_forward_set_workspace_bytes_ex": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_uint]),
     "q8p_forward_set_ex": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
@@ -500,6 +502,21 @@ def e8p_encode(v, stream=None):
         raise ValidationError("v must be a contiguous float64 CUDA tensor [nblocks, 8]")
     out = torch.empty(v.shape[0], dtype=torch.int16, device=v.device)
     _check(lib().q8p_e8p_encode(v.data_ptr(), out.data_ptr(), v.shape[0], v.device.index or 0, _stream_ptr(stream)))
+    return out.to(torch.int32) & 0xFFFF
+
+
+def rvq_quantize(v, stages, stream=None):
+    """RvqQuantizer::quantize on a float64 CUDA tensor [nblocks, 8]; stages =
+    [(codebook, scale)] (CB_E8P_2BIT / CB_E8_1BIT, float scale) -> int32 codes
+    [num_stages, nblocks] (bit-identical to the reference)."""
+    torch = _torch()
+    if v.dtype != torch.float64 or not v.is_cuda or not v.is_contiguous() or v.dim() != 2 or v.shape[1] != 8:
+        raise ValidationError("v must be a contiguous float64 CUDA tensor [nblocks, 8]")
+    out = torch.empty(len(stages), v.shape[0], dtype=torch.int16, device=v.device)
+    cbs = (ctypes.c_int * len(stages))(*[int(cb) for cb, _ in stages])
+    scs = (ctypes.c_double * len(stages))(*[float(sc) for _, sc in stages])
+    _check(lib().q8p_rvq_quantize(v.data_ptr(), out.data_ptr(), v.shape[0], len(stages), cbs, scs,
+                                  v.device.index or 0, _stream_ptr(stream)))
     return out.to(torch.int32) & 0xFFFF
 
 

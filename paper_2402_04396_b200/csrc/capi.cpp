@@ -991,6 +991,23 @@ q8p_status q8p_e8p_encode(const double* v, uint16_t* words, size_t nblocks, int 
   }
 }
 
+q8p_status q8p_rvq_quantize(const double* v, uint16_t* codes, size_t nblocks, int num_stages,
+                            const q8p_codebook* codebooks, const double* scales, int device, void* stream) {
+  try {
+    if (nblocks == 0) return Q8P_OK;
+    if (!v || !codes || !codebooks || !scales) throw q8p::ValidationError("null argument");
+    if (num_stages < 1 || num_stages > 2) throw q8p::ValidationError("1 or 2 RVQ stages on this path");
+    int kinds[2] = {0, 0};
+    for (int i = 0; i < num_stages; ++i) kinds[i] = codebooks[i] == Q8P_CB_E8P_2BIT ? 0 : 1;
+    require_sm100(device);
+    DeviceGuard g(device);
+    launch_rvq_quantize(v, codes, nblocks, num_stages, kinds, scales, static_cast<cudaStream_t>(stream));
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
 q8p_status q8p_infer_host(q8p_layer* L, const double* x, double* y, int batch) {
   try {
     if (!L || !x || !y) throw q8p::ValidationError("null argument");

@@ -121,6 +121,9 @@ void launch_gemv_simple(const q8p_layer& L, const float* t, float* z, int batch,
 void launch_decode(const q8p_layer& L, int stage, float* w, cudaStream_t s);
 // e8p_encode (core/src/e8p.cpp:114-156) on device, bit-identical: v [nblocks][8] f64 -> words.
 void launch_e8p_encode(const double* v, std::uint16_t* words, std::size_t nblocks, cudaStream_t s);
+// RvqQuantizer::quantize (rvq.cpp:59-79) per 8-vector, bit-identical: codes [stage][nblocks].
+void launch_rvq_quantize(const double* v, std::uint16_t* codes, std::size_t nblocks, int stages, const int* kinds,
+                         const double* scales, cudaStream_t s);
 
 // Tensor-core path (gemv_tc.cu, kernels_rht.cu).
 std::vector<std::uint8_t> tc_lut_image();  // the 64 KiB smem LUT window, bulk-copied per CTA

@@ -15,24 +15,17 @@
 // is the optional accelerator of its inner search).
 #include <cuda_runtime.h>
 
+#include <cmath>
+#include <mutex>
+#include <vector>
+
 #include "device.hpp"
 
 namespace q8p::detail {
 namespace {
 
-__global__ void __launch_bounds__(256) e8p_encode_kernel(const double* __restrict__ v, std::uint16_t* __restrict__ out,
-                                                        std::size_t nblocks, const std::int8_t* __restrict__ doubled,
-                                                        const std::uint8_t* __restrict__ odd) {
-  __shared__ double half_d[256][8];  // doubled / 2 (exact)
-  __shared__ std::uint8_t par[256];
-  for (int i = threadIdx.x; i < 256 * 8; i += blockDim.x) half_d[i >> 3][i & 7] = 0.5 * double(doubled[i]);
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) par[i] = odd[i];
-  __syncthreads();
-  for (std::size_t blk = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x; blk < nblocks;
-       blk += std::size_t(gridDim.x) * blockDim.x) {
-    double x[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) x[c] = v[blk * 8 + c];
+// e8p_encode of one 8-vector against the shared-memory tables.
+__device__ std::uint32_t e8p_search(const double (&x)[8], const double (*half_d)[8], const std::uint8_t* par) {
     double best = __longlong_as_double(0x7FF0000000000000LL);  // +inf
     std::uint32_t best_word = 0;
     for (std::uint32_t idx = 0; idx < 256; ++idx) {
@@ -72,40 +65,171 @@ __global__ void __launch_bounds__(256) e8p_encode_kernel(const double* __restric
         }
       }
     }
-    out[blk] = std::uint16_t(best_word);
+    return best_word;
+}
+
+// E8P point of `word` (e8p.cpp:81-100): exact quarter-integers.
+__device__ void e8p_point(std::uint32_t word, const double (*half_d)[8], const std::uint8_t* par, double (&p)[8]) {
+  const std::uint32_t idx = word >> 8, sb = (word >> 1) & 0x7Fu;
+  const double sh = (word & 1u) ? 0.25 : -0.25;
+  const std::uint32_t neg0 = (__popc(sb) & 1u) ^ par[idx];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const std::uint32_t neg = c == 0 ? neg0 : ((sb >> (7 - c)) & 1u);
+    p[c] = __dadd_rn(neg ? -half_d[idx][c] : half_d[idx][c], sh);
+  }
+}
+
+// TableCodebook::encode (codebook.cpp:45-62) over the e8-1bit table: strict <, ties keep the smaller index.
+__device__ std::uint32_t table_search(const double (&x)[8], const double (*tab)[8]) {
+  double best = __longlong_as_double(0x7FF0000000000000LL);
+  std::uint32_t best_i = 0;
+  for (std::uint32_t i = 0; i < 256; ++i) {
+    double dist = 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double d = __dsub_rn(x[c], tab[i][c]);
+      dist = __dadd_rn(dist, __dmul_rn(d, d));
+    }
+    if (dist < best) {
+      best = dist;
+      best_i = i;
+    }
+  }
+  return best_i;
+}
+
+struct SharedTables {
+  double half_d[256][8];  // E8P doubled / 2 (exact)
+  double e81[256][8];     // e8-1bit entries (doubled / 2, exact)
+  std::uint8_t par[256];
+};
+
+__device__ void load_tables(SharedTables& T, const std::int8_t* doubled, const std::uint8_t* odd,
+                            const std::int8_t* e81_doubled) {
+  for (int i = threadIdx.x; i < 256 * 8; i += blockDim.x) {
+    T.half_d[i >> 3][i & 7] = 0.5 * double(doubled[i]);
+    T.e81[i >> 3][i & 7] = 0.5 * double(e81_doubled[i]);
+  }
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) T.par[i] = odd[i];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) e8p_encode_kernel(const double* __restrict__ v, std::uint16_t* __restrict__ out,
+                                                        std::size_t nblocks, const std::int8_t* __restrict__ doubled,
+                                                        const std::uint8_t* __restrict__ odd,
+                                                        const std::int8_t* __restrict__ e81) {
+  __shared__ SharedTables T;
+  load_tables(T, doubled, odd, e81);
+  for (std::size_t blk = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x; blk < nblocks;
+       blk += std::size_t(gridDim.x) * blockDim.x) {
+    double x[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x[c] = v[blk * 8 + c];
+    out[blk] = std::uint16_t(e8p_search(x, T.half_d, T.par));
+  }
+}
+
+// RvqQuantizer::quantize (rvq.cpp:59-79) per 8-vector: per stage scaled = residual / s,
+// word = encode(scaled), residual -= s * decode(word).  kinds[i]: 0 = e8p-2bit, 1 = e8-1bit.
+struct RvqStages {
+  int n;
+  int kind[2];
+  double scale[2];
+};
+__global__ void __launch_bounds__(256) rvq_quantize_kernel(const double* __restrict__ v, std::uint16_t* __restrict__ codes,
+                                                          std::size_t nblocks, RvqStages st,
+                                                          const std::int8_t* __restrict__ doubled,
+                                                          const std::uint8_t* __restrict__ odd,
+                                                          const std::int8_t* __restrict__ e81) {
+  __shared__ SharedTables T;
+  load_tables(T, doubled, odd, e81);
+  for (std::size_t blk = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x; blk < nblocks;
+       blk += std::size_t(gridDim.x) * blockDim.x) {
+    double res[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) res[c] = v[blk * 8 + c];
+    for (int i = 0; i < st.n; ++i) {
+      const double s = st.scale[i];
+      double sc[8], p[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) sc[c] = __ddiv_rn(res[c], s);
+      std::uint32_t word;
+      if (st.kind[i] == 0) {
+        word = e8p_search(sc, T.half_d, T.par);
+        e8p_point(word, T.half_d, T.par, p);
+      } else {
+        word = table_search(sc, T.e81);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) p[c] = T.e81[word][c];
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) res[c] = __dsub_rn(res[c], __dmul_rn(s, p[c]));
+      codes[std::size_t(i) * nblocks + blk] = std::uint16_t(word);
+    }
   }
 }
 
 struct EncodeTables {
   std::int8_t* doubled = nullptr;
   std::uint8_t* odd = nullptr;
+  std::int8_t* e81 = nullptr;
 };
+
+const EncodeTables& device_tables(int& dev) {
+  cuda_check(cudaGetDevice(&dev), "get device");
+  static std::mutex mu;
+  static EncodeTables tabs[64];
+  std::scoped_lock lock(mu);
+  if (dev < 0 || dev >= 64) throw DeviceError("device index out of range");
+  if (!tabs[dev].doubled) {
+    const E8PTable& t = e8p_table();
+    std::vector<std::int8_t> e81(256 * 8);
+    for (int i = 0; i < 256; ++i)
+      for (int c = 0; c < 8; ++c) e81[i * 8 + c] = e8_1bit_doubled()[i][c];
+    cuda_check(cudaMalloc(&tabs[dev].doubled, 256 * 8), "encode tables");
+    cuda_check(cudaMalloc(&tabs[dev].odd, 256), "encode tables");
+    cuda_check(cudaMalloc(&tabs[dev].e81, 256 * 8), "encode tables");
+    cuda_check(cudaMemcpy(tabs[dev].doubled, t.doubled.data(), 256 * 8, cudaMemcpyHostToDevice), "encode tables");
+    cuda_check(cudaMemcpy(tabs[dev].odd, t.odd_parity.data(), 256, cudaMemcpyHostToDevice), "encode tables");
+    cuda_check(cudaMemcpy(tabs[dev].e81, e81.data(), 256 * 8, cudaMemcpyHostToDevice), "encode tables");
+  }
+  return tabs[dev];
+}
+
+unsigned grid_for(std::size_t nblocks, int dev) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return unsigned(std::min<std::size_t>((nblocks + 255) / 256, std::size_t(sms) * 8));
+}
 
 }  // namespace
 
 void launch_e8p_encode(const double* v, std::uint16_t* words, std::size_t nblocks, cudaStream_t s) {
   if (nblocks == 0) return;
   int dev = 0;
-  cuda_check(cudaGetDevice(&dev), "get device");
-  static std::mutex mu;
-  static EncodeTables tabs[64];
-  {
-    std::scoped_lock lock(mu);
-    if (dev < 0 || dev >= 64) throw DeviceError("device index out of range");
-    if (!tabs[dev].doubled) {
-      const E8PTable& t = e8p_table();
-      cuda_check(cudaMalloc(&tabs[dev].doubled, 256 * 8), "encode tables");
-      cuda_check(cudaMalloc(&tabs[dev].odd, 256), "encode tables");
-      cuda_check(cudaMemcpy(tabs[dev].doubled, t.doubled.data(), 256 * 8, cudaMemcpyHostToDevice), "encode tables");
-      cuda_check(cudaMemcpy(tabs[dev].odd, t.odd_parity.data(), 256, cudaMemcpyHostToDevice), "encode tables");
-    }
-  }
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const std::size_t want = (nblocks + 255) / 256;
-  const unsigned grid = unsigned(std::min<std::size_t>(want, std::size_t(sms) * 8));
-  e8p_encode_kernel<<<grid, 256, 0, s>>>(v, words, nblocks, tabs[dev].doubled, tabs[dev].odd);
+  const EncodeTables& t = device_tables(dev);
+  e8p_encode_kernel<<<grid_for(nblocks, dev), 256, 0, s>>>(v, words, nblocks, t.doubled, t.odd, t.e81);
   cuda_check(cudaGetLastError(), "e8p encode launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void launch_rvq_quantize(const double* v, std::uint16_t* codes, std::size_t nblocks, int stages, const int* kinds,
+                         const double* scales, cudaStream_t s) {
+  if (nblocks == 0) return;
+  if (stages < 1 || stages > 2) throw ValidationError("rvq: 1 or 2 stages on this path");
+  RvqStages st{};
+  st.n = stages;
+  for (int i = 0; i < stages; ++i) {
+    if (kinds[i] != 0 && kinds[i] != 1) throw ValidationError("rvq: unknown codebook");
+    if (!(scales[i] > 0.0) || !std::isfinite(scales[i])) throw ValidationError("RvqQuantizer: scales must be positive");
+    st.kind[i] = kinds[i];
+    st.scale[i] = scales[i];
+  }
+  int dev = 0;
+  const EncodeTables& t = device_tables(dev);
+  rvq_quantize_kernel<<<grid_for(nblocks, dev), 256, 0, s>>>(v, codes, nblocks, st, t.doubled, t.odd, t.e81);
+  cuda_check(cudaGetLastError(), "rvq quantize launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 

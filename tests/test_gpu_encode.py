@@ -36,3 +36,15 @@ def test_encode_decode_round_trip():
     got = q8p.e8p_encode(torch.from_numpy(pts).cuda()).cpu().numpy()
     back = np.stack([q8p.e8p_decode_host(int(w)) for w in got]).astype(np.float64)
     assert np.array_equal(back, pts)
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4])
+def test_rvq_quantize_bit_identical_to_reference(ref, bits):
+    # default_scheme(bits) (rvq.cpp:9-21) with f32-frozen scales as the producer uses them
+    cbs = {2: [q8p.CB_E8P_2BIT], 3: [q8p.CB_E8P_2BIT, q8p.CB_E8_1BIT], 4: [q8p.CB_E8P_2BIT, q8p.CB_E8P_2BIT]}[bits]
+    rho = {2: [0.9], 3: [0.98, 2.04], 4: [1.03, 3.45]}[bits]
+    scales = [float(np.float32(1.0 / r)) for r in rho]
+    v = _inputs()[:12000]
+    got = q8p.rvq_quantize(torch.from_numpy(v).cuda(), list(zip(cbs, scales))).cpu().numpy()
+    want = ref.rvq_quantize(bits, scales, v).astype(np.int64)
+    assert np.array_equal(got, want), np.argwhere(got != want)[:5]
