@@ -193,6 +193,13 @@ q8p_status q8p_e8p_encode(const double* v, uint16_t* words, size_t nblocks, int 
  * (ldlq.cpp:128-226, u = nullptr) this is the producer's whole code search. */
 q8p_status q8p_rvq_quantize(const double* v, uint16_t* codes, size_t nblocks, int num_stages,
                             const q8p_codebook* codebooks, const double* scales, int device, void* stream);
+/* SideTransform::apply (rht: x <- H (S o x), transforms.cpp:28-36) on every
+ * column of a row-major rows x cols device f64 matrix, in place, bit-identical
+ * to the reference's transform_cols (transforms.cpp:66-79); signs: device,
+ * ceil(rows/8) bytes; scratch: rows * cols doubles.  With a transpose it is
+ * transform_rows; the producer's incoherence step W~ = T_u W T_v^T. */
+q8p_status q8p_rht_cols_f64(double* w, double* scratch, size_t rows, size_t cols, const uint8_t* signs,
+                            int device, void* stream);
 
 /* latq::infer drop-in: host f64 x [batch][n] -> host f64 y [batch][m].
  * Synchronous; stages through an internal pinned buffer and workspace. */

@@ -21,7 +21,7 @@ __all__ = [
     "LayerSet", "Error", "SizeError", "ValidationError", "FormatError", "BadMagicError",
     "UnsupportedVersionError", "TruncatedArtifactError", "UnsupportedError", "DeviceError",
     "lib", "plan_hadamard", "hadamard_base", "codebook_table", "e8p_decode_host",
-    "inspect_artifact", "reserialize", "Layer", "rht", "kernel_launches", "e8p_encode", "rvq_quantize",
+    "inspect_artifact", "reserialize", "Layer", "rht", "kernel_launches", "e8p_encode", "rvq_quantize", "rht_cols_f64",
     "CB_E8P_2BIT", "CB_E8_1BIT", "NcclError", "shard_rows", "NcclComm",
 ]
 
@@ -131,6 +131,8 @@ _SIGNATURES = {
     "q8p_infer_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
     "q8p_e8p_encode": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]),
     "q8p_rvq_quantize": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
+    "q8p_rht_cols_f64": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_size_t,
                                         ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
     "q8p_forward_set_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
     "q8p_forward_set_workspace_bytes_ex": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_uint]),
@@ -518,6 +520,19 @@ def rvq_quantize(v, stages, stream=None):
     _check(lib().q8p_rvq_quantize(v.data_ptr(), out.data_ptr(), v.shape[0], len(stages), cbs, scs,
                                   v.device.index or 0, _stream_ptr(stream)))
     return out.to(torch.int32) & 0xFFFF
+
+
+def rht_cols_f64(w, signs, stream=None):
+    """SideTransform::apply (rht) on every column of a contiguous float64 CUDA
+    matrix [rows, cols], in place; signs: uint8 CUDA tensor of ceil(rows/8)
+    bytes.  Bit-identical to the reference's transform_cols."""
+    torch = _torch()
+    if w.dtype != torch.float64 or not w.is_cuda or not w.is_contiguous() or w.dim() != 2:
+        raise ValidationError("w must be a contiguous float64 CUDA matrix")
+    scratch = torch.empty_like(w)
+    _check(lib().q8p_rht_cols_f64(w.data_ptr(), scratch.data_ptr(), w.shape[0], w.shape[1], signs.data_ptr(),
+                                  w.device.index or 0, _stream_ptr(stream)))
+    return w
 
 
 def rht(x, signs, transpose: bool = False, out=None, stream=None):

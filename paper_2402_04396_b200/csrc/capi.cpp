@@ -991,6 +991,21 @@ q8p_status q8p_e8p_encode(const double* v, uint16_t* words, size_t nblocks, int 
   }
 }
 
+q8p_status q8p_rht_cols_f64(double* w, double* scratch, size_t rows, size_t cols, const uint8_t* signs, int device,
+                            void* stream) {
+  try {
+    if (rows == 0 || cols == 0) return Q8P_OK;
+    if (!w || !scratch || !signs) throw q8p::ValidationError("null argument");
+    q8p::plan_hadamard(rows);
+    require_sm100(device);
+    DeviceGuard g(device);
+    launch_rht_cols_f64(w, scratch, std::uint32_t(rows), std::uint32_t(cols), signs, static_cast<cudaStream_t>(stream));
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
 q8p_status q8p_rvq_quantize(const double* v, uint16_t* codes, size_t nblocks, int num_stages,
                             const q8p_codebook* codebooks, const double* scales, int device, void* stream) {
   try {

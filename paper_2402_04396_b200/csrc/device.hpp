@@ -124,6 +124,10 @@ void launch_e8p_encode(const double* v, std::uint16_t* words, std::size_t nblock
 // RvqQuantizer::quantize (rvq.cpp:59-79) per 8-vector, bit-identical: codes [stage][nblocks].
 void launch_rvq_quantize(const double* v, std::uint16_t* codes, std::size_t nblocks, int stages, const int* kinds,
                          const double* scales, cudaStream_t s);
+// SideTransform::apply (rht) on every column of a row-major L x ncols f64 matrix, in place
+// (scratch: L * ncols doubles), bit-identical to transform_cols (transforms.cpp:66-79).
+void launch_rht_cols_f64(double* w, double* scratch, std::uint32_t L, std::uint32_t ncols, const std::uint8_t* signs,
+                         cudaStream_t s);
 
 // Tensor-core path (gemv_tc.cu, kernels_rht.cu).
 std::vector<std::uint8_t> tc_lut_image();  // the 64 KiB smem LUT window, bulk-copied per CTA

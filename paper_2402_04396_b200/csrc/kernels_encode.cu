@@ -170,6 +170,49 @@ __global__ void __launch_bounds__(256) rvq_quantize_kernel(const double* __restr
   }
 }
 
+// SideTransform::apply (transforms.cpp:28-36) = had_apply(S o x) (hadamard.cpp:170-210)
+// on every column of a row-major L x ncols f64 matrix, bit-identical to the
+// reference's transform_cols (transforms.cpp:66-79): the same butterfly
+// network (stride q, len ascending) and the same sequential base sums, in IEEE
+// double without contraction.  CTA = 32 adjacent columns (lane = column, rows
+// coalesced); butterflies in place in `w`, the base / 1/sqrt(n) step writes `out`.
+__global__ void __launch_bounds__(256) rht_cols_f64_kernel(double* __restrict__ w, double* __restrict__ out,
+                                                          std::uint32_t L, std::uint32_t ncols, std::uint32_t p,
+                                                          std::uint32_t q, const std::uint8_t* __restrict__ signs,
+                                                          const std::int8_t* __restrict__ base, double scale) {
+  const std::uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const std::uint32_t col = blockIdx.x * 32 + lane;
+  const bool on = col < ncols;
+  for (std::uint32_t i = wid; i < L; i += nw)
+    if (on && ((signs[i >> 3] >> (i & 7)) & 1u)) w[std::size_t(i) * ncols + col] = -w[std::size_t(i) * ncols + col];
+  __syncthreads();
+  for (std::uint32_t len = 1; len < p; len <<= 1) {
+    for (std::uint32_t t = wid; t < (p / 2) * q; t += nw) {
+      const std::uint32_t pi = t / q, j = t - pi * q;
+      const std::uint32_t k = (pi / len) * 2 * len + pi % len;
+      const std::size_t a = (std::size_t(k) * q + j) * ncols + col, b = (std::size_t(k + len) * q + j) * ncols + col;
+      if (on) {
+        const double u = w[a], v = w[b];
+        w[a] = __dadd_rn(u, v);
+        w[b] = __dsub_rn(u, v);
+      }
+    }
+    __syncthreads();
+  }
+  for (std::uint32_t e = wid; e < L; e += nw) {
+    if (!on) continue;
+    if (q == 1) {
+      out[std::size_t(e) * ncols + col] = __dmul_rn(w[std::size_t(e) * ncols + col], scale);
+    } else {
+      const std::uint32_t r = e / q, a = e - r * q;
+      double acc = 0.0;
+      for (std::uint32_t b = 0; b < q; ++b)
+        acc = __dadd_rn(acc, __dmul_rn(double(base[a * q + b]), w[(std::size_t(r) * q + b) * ncols + col]));
+      out[std::size_t(e) * ncols + col] = __dmul_rn(acc, scale);
+    }
+  }
+}
+
 struct EncodeTables {
   std::int8_t* doubled = nullptr;
   std::uint8_t* odd = nullptr;
@@ -212,6 +255,36 @@ void launch_e8p_encode(const double* v, std::uint16_t* words, std::size_t nblock
   e8p_encode_kernel<<<grid_for(nblocks, dev), 256, 0, s>>>(v, words, nblocks, t.doubled, t.odd, t.e81);
   cuda_check(cudaGetLastError(), "e8p encode launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void launch_rht_cols_f64(double* w, double* scratch, std::uint32_t L, std::uint32_t ncols, const std::uint8_t* signs,
+                         cudaStream_t s) {
+  if (L == 0 || ncols == 0) return;
+  const HadamardSpec spec = plan_hadamard(L);
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "get device");
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, std::size_t>, std::int8_t*>> bases;  // (device, q) -> base
+  const std::int8_t* base = nullptr;
+  if (spec.q > 1) {
+    std::scoped_lock lock(mu);
+    for (auto& e : bases)
+      if (e.first == std::make_pair(dev, spec.q)) base = e.second;
+    if (!base) {
+      const std::vector<std::int8_t>& hb = hadamard_base(spec.q);
+      std::int8_t* d = nullptr;
+      cuda_check(cudaMalloc(&d, hb.size()), "base alloc");
+      cuda_check(cudaMemcpy(d, hb.data(), hb.size(), cudaMemcpyHostToDevice), "base upload");
+      bases.push_back({{dev, spec.q}, d});
+      base = d;
+    }
+  }
+  const double scale = 1.0 / std::sqrt(double(L));  // had_apply's 1/sqrt(n) (hadamard.cpp:188)
+  rht_cols_f64_kernel<<<(ncols + 31) / 32, 256, 0, s>>>(w, scratch, L, ncols, std::uint32_t(spec.p),
+                                                        std::uint32_t(spec.q), signs, base, scale);
+  cuda_check(cudaGetLastError(), "rht f64 launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cuda_check(cudaMemcpyAsync(w, scratch, std::size_t(L) * ncols * 8, cudaMemcpyDeviceToDevice, s), "rht f64 copy");
 }
 
 void launch_rvq_quantize(const double* v, std::uint16_t* codes, std::size_t nblocks, int stages, const int* kinds,

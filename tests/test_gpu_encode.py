@@ -48,3 +48,36 @@ def test_rvq_quantize_bit_identical_to_reference(ref, bits):
     got = q8p.rvq_quantize(torch.from_numpy(v).cuda(), list(zip(cbs, scales))).cpu().numpy()
     want = ref.rvq_quantize(bits, scales, v).astype(np.int64)
     assert np.array_equal(got, want), np.argwhere(got != want)[:5]
+
+
+@pytest.mark.parametrize("m,n,bits,seed", [(64, 128, 2, 11), (96, 160, 3, 6), (56, 112, 4, 7), (256, 512, 2, 3)])
+def test_gpu_producer_equals_reference_quantize(ref, m, n, bits, seed):
+    # The H = I producer route (ref_quantize_hi == quantize_layer(W, I, cfg)) with
+    # every numeric step on the GPU: W~ = T_u W T_v^T in f64 (q8p_rht_cols_f64),
+    # RVQ codes (q8p_rvq_quantize); the artifact bytes must equal the reference's.
+    import struct
+
+    w = ref.gen_weights(m, n, ref.substream_seed(seed, 10))
+    su = ref.random_signs(m, ref.substream_seed(seed, 0))
+    sv = ref.random_signs(n, ref.substream_seed(seed, 1))
+    d = torch.from_numpy(w).cuda()
+    q8p.rht_cols_f64(d, torch.from_numpy(su).cuda())                 # transform_cols(left)
+    dt = d.t().contiguous()
+    q8p.rht_cols_f64(dt, torch.from_numpy(sv).cuda())                # transform_rows(right)
+    wt = dt.t().contiguous()
+    host = wt.cpu().numpy()
+    sq = host.T.ravel() ** 2                                         # column-major, left-to-right sum
+    r1 = np.sqrt(np.cumsum(sq)[-1]) / np.sqrt(float(m) * n)
+    ids = {2: ["e8p-2bit"], 3: ["e8p-2bit", "e8-1bit"], 4: ["e8p-2bit", "e8p-2bit"]}[bits]
+    rho = {2: [0.9], 3: [0.98, 2.04], 4: [1.03, 3.45]}[bits]
+    s32 = [np.float32(r1 / r) for r in rho]
+    cbs = [q8p.CB_E8P_2BIT if i == "e8p-2bit" else q8p.CB_E8_1BIT for i in ids]
+    codes = q8p.rvq_quantize(wt.view(-1, 8), list(zip(cbs, [float(x) for x in s32]))).cpu().numpy()
+    body = b"QSHP" + struct.pack("<HIIBB", 1, m, n, 0, len(ids))
+    for i, sc in zip(ids, s32):
+        body += bytes([len(i)]) + i.encode() + struct.pack("<f", sc)
+    body += su.tobytes() + sv.tobytes()
+    for cid, c in zip(ids, codes):
+        body += c.astype("<u2" if cid == "e8p-2bit" else "u1").tobytes()
+    want = ref.quantize_hi(m, n, bits, seed)
+    assert body == want
