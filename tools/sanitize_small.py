@@ -25,3 +25,10 @@ for conc in (False, True):
     S.forward_host(hx, hy, 2)
 torch.cuda.synchronize()
 print("sanitize run ok")
+v = torch.randn(5000, 8, dtype=torch.float64, device="cuda")
+q8p.e8p_encode(v)
+q8p.rvq_quantize(v, [(q8p.CB_E8P_2BIT, 1.0), (q8p.CB_E8_1BIT, 0.5)])
+w = torch.randn(96, 160, dtype=torch.float64, device="cuda")
+q8p.rht_cols_f64(w, torch.randint(0, 256, (12,), dtype=torch.uint8, device="cuda"))
+torch.cuda.synchronize()
+print("sanitize producer ok")
