@@ -102,6 +102,9 @@ constexpr int kMaxStages = 32;
 #else
 #define A_EMPTY_WAIT mbar_wait
 #endif
+#ifndef Q8P_K2_KBG8
+#define Q8P_K2_KBG8 3  // B-image ring slots per group at N = 8 (4: neutral; G x slots <= kMaxB)
+#endif
 #ifndef Q8P_K2_TEAMS
 #define Q8P_K2_TEAMS 1  // decoder teams per group at batch <= 2 (2: +3% K2, but the register
                          // file then leaves no room to co-reside with K1 under PDL)
@@ -123,7 +126,7 @@ struct Roles {
   template <int N>
   // B-image ring slots per group.  >= 2: the issuer refills the slot of item
   // k - 1 with item k - 1 + kBg after issuing item k, so one slot would deadlock.
-  static constexpr std::uint32_t kBg = N <= 8 || N >= 128 ? 3 : 2;
+  static constexpr std::uint32_t kBg = N <= 8 ? Q8P_K2_KBG8 : N >= 128 ? 3 : 2;
 };
 
 struct TcArgs {
@@ -253,6 +256,7 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
   // B ring: [group][slot], b_slot bytes per k-slab image
   const std::uint32_t b_slot = (a.b_bytes + 127) & ~127u;
   constexpr std::uint32_t SBg = Roles<G>::template kBg<N>, SB = SBg * G;
+  static_assert(SB <= kMaxB, "B-image ring slots exceed the barrier block (kMaxB)");
   // smem layout.  N <= 64: [ctl][code slots][LUT window, 64 KiB aligned][B ring][code slots].
   // N = 128 (36 KB B slots, 3 deep): [ctl][B ring][code slot(s)][LUT window][code slots].
   constexpr bool kBLow = N >= 128;
