@@ -58,13 +58,27 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def make_artifact(m: int, n: int, seed: int, scale: float = 1.11) -> bytes:
-    """QSHP v1, one e8p-2bit stage, seeded synthetic codes and signs."""
+# default_scheme(bits) (rvq.cpp:9-21) stage codebooks, with the scales a unit-RMS
+# layer gets (s = r1 / rho, r1 ~ 1)
+SCHEMES = {2: [("e8p-2bit", 1.11)], 3: [("e8p-2bit", 1.02), ("e8-1bit", 0.49)],
+           4: [("e8p-2bit", 0.97), ("e8p-2bit", 0.29)]}
+CODE_BYTES = {"e8p-2bit": 2, "e8-1bit": 1}
+
+
+def make_artifact(m: int, n: int, seed: int, scale: float = 1.11, bits: int = 2) -> bytes:
+    """QSHP v1 with default_scheme(bits) stages, seeded synthetic codes and signs."""
     rng = np.random.default_rng(seed)
-    body = b"QSHP" + struct.pack("<HIIBB", 1, m, n, 0, 1) + bytes([8]) + b"e8p-2bit" + struct.pack("<f", scale)
+    stages = SCHEMES[bits] if bits != 2 else [("e8p-2bit", scale)]
+    body = b"QSHP" + struct.pack("<HIIBB", 1, m, n, 0, len(stages))
+    for cid, sc in stages:
+        body += bytes([len(cid)]) + cid.encode() + struct.pack("<f", sc)
     body += rng.integers(0, 256, (m + 7) // 8, dtype=np.uint8).tobytes()
     body += rng.integers(0, 256, (n + 7) // 8, dtype=np.uint8).tobytes()
-    body += rng.integers(0, 65536, m * n // 8, dtype=np.uint16).tobytes()
+    for cid, _ in stages:
+        if cid == "e8p-2bit":
+            body += rng.integers(0, 65536, m * n // 8, dtype=np.uint16).tobytes()
+        else:
+            body += rng.integers(0, 256, m * n // 8, dtype=np.uint8).tobytes()
     return body
 
 
@@ -118,7 +132,7 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-def cpu_reference(layers, tokens_per_step: int, threads: int, sample_div: int, steps: int, warmup: int):
+def cpu_reference(layers, tokens_per_step: int, threads: int, sample_div: int, steps: int, warmup: int, bits: int = 2):
     """Time the reference latq::infer (oracle/_ref) on the host: each step runs
     `threads` vectors concurrently (one std::thread each, the reference's own
     re-entrant infer) through row-sampled copies of the layer set (first
@@ -128,7 +142,7 @@ def cpu_reference(layers, tokens_per_step: int, threads: int, sample_div: int, s
     arts = []
     for i, (m, n) in enumerate(layers):
         ms = m // sample_div
-        arts.append((make_artifact(ms, n, 1000 + i), n))
+        arts.append((make_artifact(ms, n, 1000 + i, bits=bits), n))
     times = []
     for it in range(warmup + steps):
         t0 = time.perf_counter()
@@ -149,12 +163,12 @@ def run_reference(args):
         return
     layers = LAYERS_70B if args.workload == "70b" else LAYERS_7B
     threads = args.cpu_threads or min(os.cpu_count() or 1, 64)
-    tps, step = cpu_reference(layers, 1, threads, args.sample_div, args.steps, args.warmup)
+    tps, step = cpu_reference(layers, 1, threads, args.sample_div, args.steps, args.warmup, args.bits)
     line = {
         "impl": "reference", "metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / tps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"llama2-{args.workload}-layer-set-2bit-b1", "batch": 1,
+        "config": {"workload": f"llama2-{args.workload}-layer-set-{args.bits}bit-b1", "batch": 1,
                    "layers": [f"{m}x{n}" for m, n in layers]},
         "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "reference",
                          "sample": f"per step {threads} concurrent latq::infer calls (1 thread each) over the "
@@ -193,7 +207,7 @@ def run_ours(args):
     # Two full copies of the layer set rotate so every step streams from HBM
     # (134.6 MB per copy at 2 bits vs ~126 MB L2).
     copies = []
-    arts = [make_artifact(m, n, 1000 + i) for i, (m, n) in enumerate(layers)]
+    arts = [make_artifact(m, n, 1000 + i, bits=args.bits) for i, (m, n) in enumerate(layers)]
     for c in range(args.copies):
         row = []
         for (m, n), art in zip(layers, arts):
@@ -391,7 +405,7 @@ def run_ours(args):
     if not sharded and all(gemv_ms[li] for li in range(n_gemv)):
         per = []
         for li, (m, n) in enumerate(layers):
-            b = m * n // 8 * 2 + 4 * B * n + 4 * B * m
+            b = m * n // 8 * sum(CODE_BYTES[c] for c, _ in SCHEMES[args.bits]) + 4 * B * n + 4 * B * m
             t = statistics.mean(gemv_ms[li])
             per.append({"layer": f"{m}x{n}", "bytes": b, "us": t * 1e3, "gbs": b / (t * 1e-3) / 1e9})
         # dominant kernel: K2 on the largest layer(s) (both 70B MLP shapes move the same bytes)
@@ -418,7 +432,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             threads = args.cpu_threads or min(os.cpu_count() or 1, 64)
-            tps, step_s = cpu_reference(layers, 1, threads, args.cpu_sample_div, 2, 0)
+            tps, step_s = cpu_reference(layers, 1, threads, args.cpu_sample_div, 2, 0, args.bits)
             cpu = {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "reference",
                    "sample": f"{threads} concurrent latq::infer calls (1 thread each, one token each) through "
                              f"the first m/{args.cpu_sample_div} rows of each layer, scaled x{args.cpu_sample_div}; "
@@ -431,11 +445,11 @@ def run_ours(args):
             "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "s8xs8->s32 (K2 tensor cores) + fp32 (RHT, I/O)", "data": "synthetic",
-            "config": {"workload": f"llama2-{args.workload}-layer-set-2bit-b{B}", "batch": B,
+            "config": {"workload": f"llama2-{args.workload}-layer-set-{args.bits}bit-b{B}", "batch": B,
                        "layers": [f"{m}x{n}" for m, n in layers],
                        "parallelism": f"row-shard tp{world}" if world > 1 else "single-gpu",
                        "l2": f"{args.copies} rotating copies of the layer set (> L2 per step pair)",
-                       "codes": "uniform-random e8p-2bit codes (perf variant, test_pipeline.cpp:256-273)",
+                       "codes": f"uniform-random codes, default_scheme({args.bits}) stages (perf variant, test_pipeline.cpp:256-273)",
                        "cuda_graph": use_graph},
             "e2e": {"value": B * 1e3 / e2e_ms, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": int(launches),
@@ -460,6 +474,8 @@ def main():
     ap.add_argument("--workload", default="70b", choices=["70b", "7b"])
     ap.add_argument("--copies", type=int, default=2)
     ap.add_argument("--batch", type=int, default=1, help="vectors per layer call (BASELINE configs[1]: 1..16)")
+    ap.add_argument("--bits", type=int, default=2, choices=[2, 3, 4],
+                    help="2: E8P (headline); 3 / 4: RVQ variants (BASELINE configs[3])")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="use q8p_forward_sharded even at N=1 (1-rank NCCL)")
     ap.add_argument("--no-cpu", action="store_true")
