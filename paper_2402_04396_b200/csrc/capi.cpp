@@ -177,6 +177,7 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
       L->gbar = static_cast<unsigned*>(upload(L.get(), zero2, sizeof(zero2)));
     }
     const std::size_t nb = d.n / 8, words = std::size_t(r1 - r0) * nb;
+    const std::uint8_t* odd_dev = nullptr;  // E8P odd-parity table for the device transcode
     for (int s = 0; s < d.num_stages; ++s) {
       const q8p_stage_desc& st = d.stages[s];
       if (st.codebook != Q8P_CB_E8P_2BIT && st.codebook != Q8P_CB_E8_1BIT)
@@ -189,19 +190,6 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
       L->cb[s] = st.codebook;
       L->scale[s] = st.scale;
       const auto* src = static_cast<const std::uint8_t*>(st.codes) + std::size_t(r0) * nb * st.code_bytes;
-      // Tensor-core slab format (lossless re-layout, gemv_tc.cu).
-      {
-        std::vector<std::uint16_t> wide(words);
-        for (std::size_t i = 0; i < words; ++i)
-          wide[i] = st.code_bytes == 2 ? reinterpret_cast<const std::uint16_t*>(src)[i] : src[i];
-        if (st.codebook == Q8P_CB_E8_1BIT)
-          for (std::size_t i = 0; i < words; ++i)
-            if (wide[i] >= 256) throw ValidationError("decode: codeword out of range");
-        const int kind = st.codebook == Q8P_CB_E8P_2BIT ? 0 : 1;
-        std::vector<std::uint8_t> slabs(tc_code_bytes(r1 - r0, d.n, kind));
-        tc_transcode(wide.data(), r1 - r0, d.n, kind, slabs.data());
-        L->tc[s].codes = upload(L.get(), slabs.data(), slabs.size());
-      }
       if (st.codebook == Q8P_CB_E8P_2BIT) {
         L->codes[s] = upload(L.get(), src, words * 2);
         L->code_bytes += words * 2;
@@ -215,6 +203,19 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
         }
         L->codes[s] = upload(L.get(), narrow.data(), words);
         L->code_bytes += words;
+      }
+      // Tensor-core slab format (lossless re-layout, gemv_tc.cu), built on the device
+      // from the plain codes just uploaded.
+      {
+        const int kind = st.codebook == Q8P_CB_E8P_2BIT ? 0 : 1;
+        if (!odd_dev) {
+          const E8PTable& t = e8p_table();
+          odd_dev = static_cast<const std::uint8_t*>(upload(L.get(), t.odd_parity.data(), 256));
+        }
+        void* slabs = dev_alloc(L.get(), tc_code_bytes(r1 - r0, d.n, kind));
+        tc_transcode_device(L->codes[s], r1 - r0, d.n, kind, static_cast<std::uint8_t*>(slabs), odd_dev, nullptr);
+        cuda_check(cudaDeviceSynchronize(), "transcode");
+        L->tc[s].codes = slabs;
       }
     }
   } catch (...) {

@@ -136,6 +136,9 @@ std::uint32_t tc_row_blocks(std::uint32_t m_local);
 std::uint32_t tc_k_slabs(std::uint32_t n);
 std::size_t tc_code_bytes(std::uint32_t m_local, std::uint32_t n, int kind);
 void tc_transcode(const std::uint16_t* codes, std::uint32_t m_local, std::uint32_t n, int kind, std::uint8_t* out);
+// tc_transcode on the device from the uploaded plain codes (u16 E8P / u8 e8-1bit).
+void tc_transcode_device(const void* codes, std::uint32_t m_local, std::uint32_t n, int kind, std::uint8_t* out,
+                         const std::uint8_t* odd_parity_dev, cudaStream_t s);
 constexpr int kTcMaxBatch = 32;  // tensor-core path: batch <= 32 per launch (MMA N <= 128)
 bool tc_supported(const q8p_layer& L, int batch);
 int tc_ncols_pad(int ncols);                              // MMA N for `ncols` B rows

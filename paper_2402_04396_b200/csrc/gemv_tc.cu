@@ -874,6 +874,62 @@ void tc_transcode(const std::uint16_t* codes, std::uint32_t m_local, std::uint32
     }
 }
 
+namespace {
+// tc_transcode on the device: one thread per (row, k slab) of the plain codes
+// ([m_local][nb], u16 for E8P, u8 for e8-1bit), same bytes as the host version.
+__global__ void __launch_bounds__(256) tc_transcode_kernel(const void* __restrict__ codes, std::uint32_t m_local,
+                                                          std::uint32_t nb, std::uint32_t KSL, int kind,
+                                                          std::uint8_t* __restrict__ out,
+                                                          const std::uint8_t* __restrict__ odd) {
+  const std::uint32_t RB = (m_local + 127) / 128;
+  const std::size_t total = std::size_t(RB) * 128 * KSL;
+  const std::size_t SB = kind == 0 ? kE8pSlab : kE81Slab;
+  for (std::size_t t = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += std::size_t(gridDim.x) * blockDim.x) {
+    const std::uint32_t r = std::uint32_t(t % 128), ks = std::uint32_t((t / 128) % KSL),
+                        rb = std::uint32_t(t / (128 * std::size_t(KSL)));
+    const std::uint32_t row = rb * 128 + r;
+    std::uint8_t* slab = out + (std::size_t(rb) * KSL + ks) * SB;
+    std::uint32_t idxw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, fl[8] = {0, 0, 0, 0, 0, 0, 0, 0}, sw = 0;
+    for (std::uint32_t w = 0; w < 32; ++w) {
+      const std::uint32_t k = ks * 32 + w;
+      std::uint32_t word = 0;
+      if (row < m_local && k < nb)
+        word = kind == 0 ? static_cast<const std::uint16_t*>(codes)[std::size_t(row) * nb + k]
+                         : static_cast<const std::uint8_t*>(codes)[std::size_t(row) * nb + k];
+      const std::uint32_t byte = kind == 0 ? (word >> 8) : word;
+      idxw[w / 4] |= byte << (8 * (w & 3));
+      if (kind == 0) {
+        const std::uint32_t idx = word >> 8, sb = (word >> 1) & 0x7Fu;
+        // effective negate flags (e8p.cpp:88-98): word bit k (1..7) -> coordinate 8 - k,
+        // coordinate 0 restores the row's parity
+        fl[w / 4] |= ((std::uint32_t(__popc(sb)) & 1u) ^ odd[idx]) << (w & 3);
+        for (std::uint32_t c = 1; c < 8; ++c) fl[w / 4] |= ((word >> (8 - c)) & 1u) << (4 * c + (w & 3));
+        sw |= (word & 1u) << ((w >> 2) + 8 * (w & 3));
+      }
+    }
+    // idx / code bytes: plane w / 16, row r, byte w % 16
+    *reinterpret_cast<uint4*>(slab + r * 16) = make_uint4(idxw[0], idxw[1], idxw[2], idxw[3]);
+    *reinterpret_cast<uint4*>(slab + 2048 + r * 16) = make_uint4(idxw[4], idxw[5], idxw[6], idxw[7]);
+    if (kind == 0) {
+      *reinterpret_cast<uint4*>(slab + 4096 + r * 16) = make_uint4(fl[0], fl[1], fl[2], fl[3]);
+      *reinterpret_cast<uint4*>(slab + 6144 + r * 16) = make_uint4(fl[4], fl[5], fl[6], fl[7]);
+      *reinterpret_cast<std::uint32_t*>(slab + 8192 + r * 4) = sw;
+    }
+  }
+}
+}  // namespace
+
+void tc_transcode_device(const void* codes, std::uint32_t m_local, std::uint32_t n, int kind, std::uint8_t* out,
+                         const std::uint8_t* odd_parity_dev, cudaStream_t s) {
+  const std::uint32_t nb = n / 8, KSL = tc_k_slabs(n);
+  const std::size_t total = std::size_t(tc_row_blocks(m_local)) * 128 * KSL;
+  const unsigned grid = unsigned(std::min<std::size_t>((total + 255) / 256, 148 * 16));
+  tc_transcode_kernel<<<grid, 256, 0, s>>>(codes, m_local, nb, KSL, kind, out, odd_parity_dev);
+  cuda_check(cudaGetLastError(), "transcode launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
 // MMA N for `ncols` B rows (4 limbs x batch): 8, 16, 32, 48, 64, then 128 (batch 17..32).
 int tc_ncols_pad(int ncols) {
   return ncols <= 8 ? 8 : ncols <= 16 ? 16 : ncols <= 64 ? (ncols + 15) / 16 * 16 : 128;
