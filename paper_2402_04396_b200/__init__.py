@@ -26,7 +26,8 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libq8p.so")
+# Q8P_LIB: an alternative in-tree build of the same library (experiment builds)
+LIB_PATH = os.environ.get("Q8P_LIB") or os.path.join(_HERE, "libq8p.so")
 
 CB_E8P_2BIT = 0
 CB_E8_1BIT = 1

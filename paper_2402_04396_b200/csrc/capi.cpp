@@ -173,6 +173,8 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
     {
       const std::vector<std::uint8_t> img = tc_lut_image();
       L->lut_img = static_cast<const std::uint8_t*>(upload(L.get(), img.data(), img.size()));
+      const std::vector<std::uint32_t> tw = mma_table_words();
+      L->mma_tables = static_cast<const std::uint32_t*>(upload(L.get(), tw.data(), tw.size() * 4));
       const unsigned zero2[2] = {0u, 0u};
       L->gbar = static_cast<unsigned*>(upload(L.get(), zero2, sizeof(zero2)));
     }
@@ -214,8 +216,11 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
         }
         void* slabs = dev_alloc(L.get(), tc_code_bytes(r1 - r0, d.n, kind));
         tc_transcode_device(L->codes[s], r1 - r0, d.n, kind, static_cast<std::uint8_t*>(slabs), odd_dev, nullptr);
-        cuda_check(cudaDeviceSynchronize(), "transcode");
         L->tc[s].codes = slabs;
+        void* recs = dev_alloc(L.get(), mma_code_bytes(r1 - r0, d.n, kind));
+        mma_transcode_device(L->codes[s], r1 - r0, d.n, kind, static_cast<std::uint8_t*>(recs), odd_dev, nullptr);
+        cuda_check(cudaDeviceSynchronize(), "transcode");
+        L->mma[s] = recs;
       }
     }
   } catch (...) {
@@ -338,6 +343,16 @@ std::size_t workspace_parts(const q8p_layer* L, int batch, Workspace* w, void* b
 }
 std::size_t workspace_size(const q8p_layer* L, int batch) { return workspace_parts(L, batch, nullptr, nullptr); }
 
+// K2 kernel for decode batches: Q8P_K2=mma selects the warp-level MMA kernel
+// (gemv_mma.cu), otherwise the tcgen05 kernel (A/B knob; same accumulators bit for bit).
+bool use_mma(const q8p_layer* L, int batch) {
+  static const bool mma = [] {
+    const char* e = std::getenv("Q8P_K2");
+    return e && std::string(e) == "mma";
+  }();
+  return mma && mma_supported(*L, batch);
+}
+
 // K1 -> K2 on the layer's local rows: leaves int32 accumulators in w.zacc (tensor-core
 // path) or fp32 z rows in w.z (portable path).
 void forward_local(const q8p_layer* L, const float* x, int batch, const Workspace& w, cudaStream_t s,
@@ -352,7 +367,10 @@ void forward_local(const q8p_layer* L, const float* x, int batch, const Workspac
                         std::size_t(L->num_stages) * N * w.rows_pad, batch, s);
 #endif
     if (opts) record_event(opts->gemv_start_event, s);
-    launch_gemv_tc(*L, w.bimg, w.zacc, w.rows_pad, batch, s);
+    if (use_mma(L, batch))
+      launch_gemv_mma(*L, w.bimg, w.zacc, w.rows_pad, batch, s);
+    else
+      launch_gemv_tc(*L, w.bimg, w.zacc, w.rows_pad, batch, s);
     if (opts) record_event(opts->gemv_end_event, s);
   } else if (L->side_v.kind == 1) {  // rfft (kernels_rfft.cu): t = T_v x through the scratch
     launch_rht_in(L->side_v, x, w.t, w.u, nullptr, nullptr, nullptr, 0, batch, s);
