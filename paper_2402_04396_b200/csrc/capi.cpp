@@ -20,6 +20,25 @@ thread_local std::string t_last_error;
 
 void set_last_error(const std::string& msg) { t_last_error = msg; }
 
+int current_device() {
+  int d = 0;
+  cuda_check(cudaGetDevice(&d), "cudaGetDevice");
+  return d;
+}
+
+void kernel_attrs(const void* fn, int max_dyn_smem, bool cluster) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  const int dev = current_device();
+  std::scoped_lock lock(mu);
+  for (const auto& e : done)
+    if (e.first == fn && e.second == dev) return;
+  cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn_smem), "smem attr");
+  cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout attr");
+  if (cluster) cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1), "cluster attr");
+  done.emplace_back(fn, dev);
+}
+
 void throw_cuda(cudaError_t e, const char* what) {
   throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -133,6 +152,14 @@ void setup_side_rfft(q8p_layer* L, DevSide& side, std::uint32_t n, const float* 
   side.tw = static_cast<const float2*>(upload(L, tw.data(), tw.size() * 4));
 }
 
+bool mma_k2_selected() {
+  static const bool on = [] {
+    const char* e = std::getenv("Q8P_K2");
+    return e && std::string(e) == "mma";
+  }();
+  return on;
+}
+
 // Builds a device layer from host fields for rows [r0, r1).
 q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t r1, int device) {
   if (!d.stages || d.num_stages < 1) throw ValidationError("artifact has no quantization stages");
@@ -217,10 +244,12 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
         void* slabs = dev_alloc(L.get(), tc_code_bytes(r1 - r0, d.n, kind));
         tc_transcode_device(L->codes[s], r1 - r0, d.n, kind, static_cast<std::uint8_t*>(slabs), odd_dev, nullptr);
         L->tc[s].codes = slabs;
-        void* recs = dev_alloc(L.get(), mma_code_bytes(r1 - r0, d.n, kind));
-        mma_transcode_device(L->codes[s], r1 - r0, d.n, kind, static_cast<std::uint8_t*>(recs), odd_dev, nullptr);
+        if (mma_k2_selected()) {  // warp-MMA records only when that kernel is selected (A/B)
+          void* recs = dev_alloc(L.get(), mma_code_bytes(r1 - r0, d.n, kind));
+          mma_transcode_device(L->codes[s], r1 - r0, d.n, kind, static_cast<std::uint8_t*>(recs), odd_dev, nullptr);
+          L->mma[s] = recs;
+        }
         cuda_check(cudaDeviceSynchronize(), "transcode");
-        L->mma[s] = recs;
       }
     }
   } catch (...) {
@@ -344,14 +373,9 @@ std::size_t workspace_parts(const q8p_layer* L, int batch, Workspace* w, void* b
 std::size_t workspace_size(const q8p_layer* L, int batch) { return workspace_parts(L, batch, nullptr, nullptr); }
 
 // K2 kernel for decode batches: Q8P_K2=mma selects the warp-level MMA kernel
-// (gemv_mma.cu), otherwise the tcgen05 kernel (A/B knob; same accumulators bit for bit).
-bool use_mma(const q8p_layer* L, int batch) {
-  static const bool mma = [] {
-    const char* e = std::getenv("Q8P_K2");
-    return e && std::string(e) == "mma";
-  }();
-  return mma && mma_supported(*L, batch);
-}
+// (gemv_mma.cu; measured slower in the pipeline), otherwise the
+// tcgen05 kernel -- an A/B knob, same accumulators bit for bit.
+bool use_mma(const q8p_layer* L, int batch) { return mma_k2_selected() && mma_supported(*L, batch); }
 
 // K1 -> K2 on the layer's local rows: leaves int32 accumulators in w.zacc (tensor-core
 // path) or fp32 z rows in w.z (portable path).

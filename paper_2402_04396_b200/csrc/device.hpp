@@ -47,6 +47,14 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t sme
   cuda_check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "kernel launch");
 }
 
+// One-time (per device) kernel attributes: dynamic shared-memory limit, the
+// maximum shared-memory carveout for every q8p kernel (so consecutive kernels of
+// a forward never force an L1 / shared-memory reconfiguration of the SMs), and
+// optionally non-portable cluster sizes.  Thread-safe; keyed by (kernel, device).
+void kernel_attrs(const void* fn, int max_dyn_smem, bool cluster = false);
+// Device of the calling thread (cudaGetDevice), for per-device one-time state.
+int current_device();
+
 #ifdef __CUDACC__
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" :::); }

@@ -13,12 +13,11 @@
 // Why warp-level MMAs at batch <= 8: the decode (PRMT LUT address, LDS of the
 // lane-replicated magnitude LUT, sign-flag LOP3, two PRMT from the byte table
 // {1,3,5,_,-1,-3,-5,_}) is ~7 instructions per 8-weight codeword; the tensor core
-// does every multiply-add from registers, so a warp needs no shared-memory
-// staging of its codes and no hand-off to another warp: each warp streams its own
-// records straight from HBM into registers (LDG.128, two cells ahead), decodes
-// and issues its MMAs.  Only the activation B images are shared: one producer
-// warp streams them through a shared-memory ring that all warps of the CTA walk
-// in the same k order.
+// does every multiply-add from registers and no warp hands anything to another:
+// a producer warp streams whole cells (8 row pairs' code records + the k step's
+// activation B image, one contiguous byte range per stage) into a ring of shared
+// memory slots with 1-D bulk copies; each consumer warp loads its half-record and
+// B fragments into registers, hands the slot back, decodes and issues its MMAs.
 //
 // Data layout ("mma records", built once at upload from the plain codes; a
 // lossless re-layout).  Cell = (row pair rp: 32 rows, k step ks:
@@ -33,16 +32,16 @@
 //     shift bit of codeword (row 32 rp + 16 h + 8 r8 + g, block 32 ks + 16 half + 4 t + i)
 //     -- the side MMA's A fragment order.
 //   e8-1bit, 1024 B: [code words 0..3][32][16 B] [code words 4..7][32][16 B].
-//   Records ordered [row block rb][ks][row pair in rb] (a CTA's cells are one
-//   contiguous byte range); rp padded to whole row blocks of 16 row pairs.
+//   Records ordered [row block rb][ks][row pair in rb] (a cell's records are one
+//   contiguous byte range); rp padded to whole row blocks of 8 row pairs.
 // MMA j of a cell covers blocks 4j..4j+3: thread (g, t) holds codeword 4j + t, so
 // a0/a2 = coordinates 0-3 / 4-7 of row g and a1/a3 of row g + 8; the B fragment of
 // the same logical K order is 8 consecutive bytes of K1's B image (no permutation
 // of the activations).
 //
-// CTA: 16 consumer warps (warp w = row pair 16 rb + w of the current cell's row
-// block rb) + 1 B-image producer warp; persistent over a contiguous range of cells
-// (rb-major); per-row-block int32 accumulators flushed with integer atomics.
+// CTA: TEAMS x 8 consumer warps (warp = row pair rp of the cell) + 1 producer warp;
+// persistent over a contiguous range of cells (row-block-major), team t taking
+// every TEAMS-th cell; per-row-block int32 accumulators flushed with integer atomics.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -59,15 +58,11 @@ namespace q8p::detail {
 namespace {
 using namespace tc05;
 
-constexpr int kWarps = 16;                       // consumer warps (row pairs per row block)
-constexpr int kThreads = (kWarps + 1) * 32;      // + B-image producer warp
+constexpr int kRowPairs = 8;                     // row pairs (32 rows) per cell
 constexpr std::uint32_t kRecE8p = 2176, kRecE81 = 1024;
-constexpr std::uint32_t kMaxRing = 8;
+constexpr std::uint32_t kMaxSlots = 16;
 constexpr std::uint32_t kCtl = 1024;             // barriers at the dynamic smem base
-constexpr std::size_t kSmem = 130 * 1024;        // ring + a 64 KiB-aligned LUT window
-#ifndef Q8P_MMA_DEPTH
-#define Q8P_MMA_DEPTH 3  // cells of code records in flight per warp (registers), 2-bit layers
-#endif
+constexpr std::size_t kSmem = 227 * 1024;        // cell ring around a 64 KiB-aligned LUT window
 
 struct MmaArgs {
   const std::uint8_t* codes[2];
@@ -79,6 +74,7 @@ struct MmaArgs {
   std::int32_t* zacc;         // [stage][N][rows_pad]
   std::uint32_t rows_pad, m_local;
   int ncols;                  // 4 * batch
+  std::uint32_t smem_bytes;
   const std::uint32_t* nib;   // [256] E8P magnitude nibble words
   const uint2* e81;           // [256] e8-1bit doubled rows
   unsigned long long* trace;  // debug (Q8P_TRACE): per CTA globaltimer stamps, nullptr = off
@@ -145,12 +141,9 @@ constexpr std::uint32_t kCtHi = 0x00FBFDFFu;  // {-1,-3,-5,0}
 template <int JJ>
 __device__ __forceinline__ void e8p_a(std::uint32_t iw, std::uint32_t fw, std::uint32_t lb, std::uint32_t ct_lo,
                                       std::uint32_t ct_hi, std::uint32_t& lo, std::uint32_t& hi) {
-  std::uint32_t addr;
-  if constexpr (JJ == 3) {  // top byte on the FMA pipe (mul.hi by 256, mad) instead of an ALU PRMT
-    asm("{\n\t.reg .u32 t;\n\tmul.hi.u32 t, %1, 256;\n\tmad.lo.u32 %0, t, 256, %2;\n\t}\n" : "=r"(addr) : "r"(iw), "r"(lb));
-  } else {
-    addr = prmt(iw, lb, 0x7604u | (std::uint32_t(JJ) << 4));
-  }
+  // Pipe balance (measured, tools/ubench_alu.cu): PRMT / LOP3 / SHF issue to the
+  // ALU pipe at 16 lanes/clk, IMAD at 16, IMAD.HI (mul.hi) at only 8 lanes/clk.
+  const std::uint32_t addr = prmt(iw, lb, 0x7604u | (std::uint32_t(JJ) << 4));
   const std::uint32_t nib = lut32(addr);
   std::uint32_t rs;
   if constexpr (JJ == 0)
@@ -163,209 +156,197 @@ __device__ __forceinline__ void e8p_a(std::uint32_t iw, std::uint32_t fw, std::u
     rs = __umulhi(fw, 0x80000000u);  // fw >> 1 on the FMA pipe
   const std::uint32_t sel = nib ^ (rs & 0x44444444u);
   lo = prmt(ct_lo, ct_hi, sel);
-  hi = prmt(ct_lo, ct_hi, __umulhi(sel, 65536u));  // sel >> 16
+  // sel >> 16: on the ALU (SHF) for even slots, on the FMA pipe (mul.hi) for odd ones
+  hi = prmt(ct_lo, ct_hi, (JJ & 1) ? __umulhi(sel, 65536u) : sel >> 16);
 }
 template <int JJ>
 __device__ __forceinline__ uint2 e81_a(std::uint32_t cw, std::uint32_t lb8) {
   return lut64(prmt(cw, lb8, 0x7604u | (std::uint32_t(JJ) << 4)));
 }
 
-struct RecE8p {
-  uint4 i0, i1, f0, f1;
-  std::uint32_t sw;
-};
-struct RecE81 {
-  uint4 i0, i1;
-};
 __device__ __forceinline__ std::uint32_t w4(const uint4& v, int k) {
   return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
 }
+__device__ __forceinline__ uint4 lds128(std::uint32_t addr) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr));
+  return r;
+}
 
-template <int NST, int K1>
-struct Bundle {
-  RecE8p e;
-  RecE8p e2;  // stage 1, K1 == 0
-  RecE81 b2;  // stage 1, K1 == 1
+// One warp's half (H = 0: MMAs 0..3, H = 1: MMAs 4..7) of an E8P record, from smem.
+struct HalfE8p {
+  uint4 iw, fw;
+  std::uint32_t sw;
+};
+// Main MMAs 4H..4H+3 of an E8P half-record into acc[h][nb] (B fragments bf[j][nb]).
+template <int NB8>
+__device__ __forceinline__ void e8p_half(const HalfE8p& r, const uint2 (&bf)[4][NB8], std::uint32_t lb,
+                                         std::uint32_t ct_lo, std::uint32_t ct_hi, int (&acc)[2][NB8][4]) {
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      // word 2 h + r8 of the half: codeword (row 16 h + 8 r8 + g, block 4 (4H + jj) + t)
+      const std::uint32_t iw0 = w4(r.iw, 2 * h), iw1 = w4(r.iw, 2 * h + 1);
+      const std::uint32_t fw0 = w4(r.fw, 2 * h), fw1 = w4(r.fw, 2 * h + 1);
+      std::uint32_t a0, a1, a2, a3;
+      switch (jj) {
+        case 0: e8p_a<0>(iw0, fw0, lb, ct_lo, ct_hi, a0, a2); e8p_a<0>(iw1, fw1, lb, ct_lo, ct_hi, a1, a3); break;
+        case 1: e8p_a<1>(iw0, fw0, lb, ct_lo, ct_hi, a0, a2); e8p_a<1>(iw1, fw1, lb, ct_lo, ct_hi, a1, a3); break;
+        case 2: e8p_a<2>(iw0, fw0, lb, ct_lo, ct_hi, a0, a2); e8p_a<2>(iw1, fw1, lb, ct_lo, ct_hi, a1, a3); break;
+        default: e8p_a<3>(iw0, fw0, lb, ct_lo, ct_hi, a0, a2); e8p_a<3>(iw1, fw1, lb, ct_lo, ct_hi, a1, a3); break;
+      }
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb) mma(acc[h][nb], a0, a1, a2, a3, bf[jj][nb].x, bf[jj][nb].y);
+    }
+  }
+}
+template <int NB8>
+__device__ __forceinline__ void e81_half(const uint4& cw, const uint2 (&bf)[4][NB8], std::uint32_t lb8,
+                                         int (&acc)[2][NB8][4]) {
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const std::uint32_t c0 = w4(cw, 2 * h), c1 = w4(cw, 2 * h + 1);
+      uint2 v0, v1;
+      switch (jj) {
+        case 0: v0 = e81_a<0>(c0, lb8); v1 = e81_a<0>(c1, lb8); break;
+        case 1: v0 = e81_a<1>(c0, lb8); v1 = e81_a<1>(c1, lb8); break;
+        case 2: v0 = e81_a<2>(c0, lb8); v1 = e81_a<2>(c1, lb8); break;
+        default: v0 = e81_a<3>(c0, lb8); v1 = e81_a<3>(c1, lb8); break;
+      }
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb) mma(acc[h][nb], v0.x, v1.x, v0.y, v1.y, bf[jj][nb].x, bf[jj][nb].y);
+    }
+  }
+}
+// Side MMA of row tile h (A = shift bits b_k as 0/1 bytes, B = block sums S_k).
+template <int h, int NB8>
+__device__ __forceinline__ void side_mma(std::uint32_t sw, const uint2 (&bs)[NB8], int (&acc)[2][NB8][4]) {
+  std::uint32_t s[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int sh = 4 * h + q;
+    s[q] = (sh == 0 ? sw : __umulhi(sw, 1u << (32 - sh))) & 0x01010101u;
+  }
+#pragma unroll
+  for (int nb = 0; nb < NB8; ++nb) mma(acc[h][nb], s[0], s[1], s[2], s[3], bs[nb].x, bs[nb].y);
+}
+
+// TEAMS teams of 8 consumer warps (warp = row pair rp of the cell) + one producer
+// warp.  Team t takes the CTA's local cells t, t + TEAMS, ...
+template <int TEAMS>
+struct Shape {
+  static constexpr int kConsumers = kRowPairs * TEAMS;
+  static constexpr int kThreads = (kConsumers + 1) * 32;
 };
 
-// Half `H` of a cell's records (the words MMAs 4H..4H+3 read; half 1 also the shift word).
-template <int H, int NST, int K1>
-__device__ __forceinline__ void load_half(Bundle<NST, K1>& b, const MmaArgs& a, std::uint32_t rec, int lane) {
-  {
-    const std::uint8_t* p = a.codes[0] + std::size_t(rec) * kRecE8p + lane * 16 + H * 512;
-    (H ? b.e.i1 : b.e.i0) = ldg_stream(p);
-    (H ? b.e.f1 : b.e.f0) = ldg_stream(p + 1024);
-    if constexpr (H == 1) b.e.sw = ldg_stream32(a.codes[0] + std::size_t(rec) * kRecE8p + 2048 + lane * 4);
-  }
-  if constexpr (NST == 2) {
-    if constexpr (K1 == 0) {
-      const std::uint8_t* p = a.codes[1] + std::size_t(rec) * kRecE8p + lane * 16 + H * 512;
-      (H ? b.e2.i1 : b.e2.i0) = ldg_stream(p);
-      (H ? b.e2.f1 : b.e2.f0) = ldg_stream(p + 1024);
-      if constexpr (H == 1) b.e2.sw = ldg_stream32(a.codes[1] + std::size_t(rec) * kRecE8p + 2048 + lane * 4);
-    } else {
-      const std::uint8_t* p = a.codes[1] + std::size_t(rec) * kRecE81 + lane * 16 + H * 512;
-      (H ? b.b2.i1 : b.b2.i0) = ldg_stream(p);
-    }
-  }
-}
-
-// Main MMAs of one E8P record at MMA index J into acc[h][nb8] (B fragments bf[nb8]).
-template <int J, int NB8>
-__device__ __forceinline__ void e8p_mmas(const RecE8p& r, const uint2 (&bf)[NB8], std::uint32_t lb, std::uint32_t ct_lo,
-                                         std::uint32_t ct_hi, int (&acc)[2][NB8][4]) {
-  constexpr int jj = J & 3, half = J >> 2;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    // word 4 half + 2 h + r8: chunk `half` (MMAs 4 half .. 4 half + 3), word 2 h + r8
-    const std::uint32_t iw0 = w4(half ? r.i1 : r.i0, 2 * h), iw1 = w4(half ? r.i1 : r.i0, 2 * h + 1);
-    const std::uint32_t fw0 = w4(half ? r.f1 : r.f0, 2 * h), fw1 = w4(half ? r.f1 : r.f0, 2 * h + 1);
-    std::uint32_t a0, a1, a2, a3;
-    e8p_a<jj>(iw0, fw0, lb, ct_lo, ct_hi, a0, a2);
-    e8p_a<jj>(iw1, fw1, lb, ct_lo, ct_hi, a1, a3);
-#pragma unroll
-    for (int nb = 0; nb < NB8; ++nb) mma(acc[h][nb], a0, a1, a2, a3, bf[nb].x, bf[nb].y);
-  }
-}
-template <int J, int NB8>
-__device__ __forceinline__ void e81_mmas(const RecE81& r, const uint2 (&bf)[NB8], std::uint32_t lb8,
-                                         int (&acc)[2][NB8][4]) {
-  constexpr int jj = J & 3, half = J >> 2;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const std::uint32_t cw0 = w4(half ? r.i1 : r.i0, 2 * h), cw1 = w4(half ? r.i1 : r.i0, 2 * h + 1);
-    const uint2 v0 = e81_a<jj>(cw0, lb8), v1 = e81_a<jj>(cw1, lb8);
-#pragma unroll
-    for (int nb = 0; nb < NB8; ++nb) mma(acc[h][nb], v0.x, v1.x, v0.y, v1.y, bf[nb].x, bf[nb].y);
-  }
-}
-// Side MMA (A = shift bits b_k as 0/1 bytes, B = block sums S_k) of one E8P record.
-template <int NB8>
-__device__ __forceinline__ void side_mmas(std::uint32_t sw, const uint2 (&bs)[NB8], int (&acc)[2][NB8][4]) {
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    std::uint32_t s[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int sh = 4 * h + q;
-      s[q] = (sh == 0 ? sw : __umulhi(sw, 1u << (32 - sh))) & 0x01010101u;
-    }
-#pragma unroll
-    for (int nb = 0; nb < NB8; ++nb) mma(acc[h][nb], s[0], s[1], s[2], s[3], bs[nb].x, bs[nb].y);
-  }
-}
-
-template <int NST, int K1, int NB8>
-__global__ void __launch_bounds__(kThreads, 1) gemv_mma_kernel(MmaArgs a) {
+template <int NST, int K1, int NB8, int TEAMS>
+__global__ void __launch_bounds__(Shape<TEAMS>::kThreads, 1) gemv_mma_kernel(MmaArgs a) {
   extern __shared__ __align__(1024) std::uint8_t smem[];
+  constexpr int kCons = Shape<TEAMS>::kConsumers;
   const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const std::uint32_t sbase = smem_u32(smem);
   const std::uint32_t lutw = (sbase + kCtl + 0xFFFFu) & ~0xFFFFu;  // 64 KiB-aligned LUT window
-  const std::uint32_t slot_bytes = (a.b_bytes + 127) & ~127u;
-  // B ring below the window when it fits, else above it
-  std::uint32_t ring = sbase + kCtl, R = (lutw - ring) / slot_bytes;
-  if (R < 2) {
-    ring = lutw + 65536;
-    R = (sbase + std::uint32_t(kSmem) - ring) / slot_bytes;
-  }
-  if (R > kMaxRing) R = kMaxRing;
-  const std::uint32_t bar_full = sbase, bar_empty = sbase + 8 * kMaxRing, ct_slot = sbase + 16 * kMaxRing;
+  // cell slot: [stage-0 records of the 8 row pairs][stage-1 records][B image]
+  const std::uint32_t rec0 = kRowPairs * kRecE8p;
+  const std::uint32_t rec1 = NST == 2 ? kRowPairs * (K1 == 0 ? kRecE8p : kRecE81) : 0u;
+  const std::uint32_t cell_bytes = rec0 + rec1 + a.b_bytes;
+  const std::uint32_t slot_bytes = (cell_bytes + 127) & ~127u;
+  // slots below the window, then above it
+  const std::uint32_t lo0 = sbase + kCtl, n_lo = lutw > lo0 ? (lutw - lo0) / slot_bytes : 0u;
+  const std::uint32_t hi0 = lutw + 65536, send = sbase + std::uint32_t(a.smem_bytes);
+  std::uint32_t S = n_lo + (send > hi0 ? (send - hi0) / slot_bytes : 0u);
+  if (S > kMaxSlots) S = kMaxSlots;
+  auto slot_addr = [&](std::uint32_t st) { return st < n_lo ? lo0 + st * slot_bytes : hi0 + (st - n_lo) * slot_bytes; };
+  const std::uint32_t bar_full = sbase, bar_empty = sbase + 8 * kMaxSlots, ct_slot = sbase + 16 * kMaxSlots;
 
   const std::uint32_t c0 = std::uint32_t((std::uint64_t(a.cells) * blockIdx.x) / gridDim.x);
   const std::uint32_t c1 = std::uint32_t((std::uint64_t(a.cells) * (blockIdx.x + 1)) / gridDim.x);
   const std::uint32_t count = c1 - c0;
   if (threadIdx.x == 0) gstamp(a, 0);
+  if (S < 2) __trap();  // host sizing bug: fail loudly
 
-  // LUT table words first: they are L2 hits, the code prefetch below is not
-  std::uint32_t tab_w = 0;
-  uint2 tab_e = make_uint2(0, 0);
-  if (threadIdx.x < 512) {
-    tab_w = __ldg(a.nib + (threadIdx.x >> 1));
-    if constexpr (NST == 2 && K1 == 1) tab_e = __ldg(a.e81 + (threadIdx.x >> 1));
-  }
-  // ---- consumers: first code records in flight ----
-  constexpr int D = NST == 1 ? Q8P_MMA_DEPTH : 1;  // cells of code records prefetched ahead
-  Bundle<NST, K1> buf[D];
-  std::uint32_t rb = c0 / (a.KSL ? a.KSL : 1), ks = c0 - rb * a.KSL;
-  const bool consumer = warp < kWarps;
-  // row pair of this warp in row block rb' and its record index for cell (rb', ks')
-  auto rec_of = [&](std::uint32_t r_b, std::uint32_t k_s) { return (r_b * a.KSL + k_s) * kWarps + std::uint32_t(warp); };
-  auto active_in = [&](std::uint32_t r_b) { return (r_b * kWarps + std::uint32_t(warp)) * 32u < a.m_local; };
-  std::uint32_t prb = rb, pks = ks;  // prefetch cursor
-  if (consumer) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      if (std::uint32_t(d) < count) {
-        if (active_in(prb)) {
-          load_half<0>(buf[d], a, rec_of(prb, pks), lane);
-          load_half<1>(buf[d], a, rec_of(prb, pks), lane);
-        }
-        if (++pks == a.KSL) pks = 0, ++prb;
-      }
+  // producer: barriers, then the first S cells' code records right away (they do
+  // not depend on K1); everyone else meets the barriers after __syncthreads
+  const bool producer = warp == kCons;
+  if (producer && lane == 0) {
+    for (std::uint32_t i = 0; i < kMaxSlots; ++i) {
+      mbar_init(bar_full + 8 * i, 1);
+      mbar_init(bar_empty + 8 * i, kRowPairs);
     }
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n" ::"r"(ct_slot), "r"(kCtLo), "r"(kCtHi) : "memory");
   }
-
-  // ---- LUT window (E8P nibble words per lane; e8-1bit rows per half-warp lane) and barriers ----
+  auto issue_codes = [&](std::uint32_t i) {
+    const std::uint32_t st = i % S, dst = slot_addr(st), cell = c0 + i;
+    mbar_arrive_expect_tx(bar_full + 8 * st, cell_bytes);
+    bulk_g2s(dst, a.codes[0] + std::size_t(cell) * rec0, rec0, bar_full + 8 * st);
+    if constexpr (NST == 2) bulk_g2s(dst + rec0, a.codes[1] + std::size_t(cell) * rec1, rec1, bar_full + 8 * st);
+  };
+  auto issue_b = [&](std::uint32_t i) {
+    const std::uint32_t st = i % S, cell = c0 + i, ks = cell % a.KSL;
+    bulk_g2s(slot_addr(st) + rec0 + rec1, a.bimg + std::size_t(ks) * a.b_bytes, a.b_bytes, bar_full + 8 * st);
+  };
+  // the first kEarly cells' codes before the CTA barrier (they overlap the previous
+  // kernel under PDL); their B images follow as soon as K1 is done, ahead of the
+  // remaining prefetch (bulk copies complete in issue order)
+  constexpr std::uint32_t kEarly = 2;
+  if (producer && lane == 0) {
+    fence_mbar_init();
+    for (std::uint32_t i = 0; i < count && i < kEarly; ++i) issue_codes(i);
+  }
+  // LUT window (E8P nibble words per lane; e8-1bit rows per half-warp lane)
   {
-    // thread i < 512: row i / 2, half i % 2 of the row's 128-byte E8P block (and of
-    // the e8-1bit block): one table load per thread, then 4 (8) 16-byte stores
     std::uint8_t* win = smem + (lutw - sbase);
-    if (threadIdx.x < 512) {
-      const int row = threadIdx.x >> 1, half = threadIdx.x & 1;
-      const std::uint32_t w = tab_w;
-      const uint2 e = tab_e;
+    for (int x = threadIdx.x; x < 512; x += Shape<TEAMS>::kThreads) {
+      const int row = x >> 1, half = x & 1;
+      const std::uint32_t w = __ldg(a.nib + row);
       uint4* d = reinterpret_cast<uint4*>(win + row * 256 + half * 64);
 #pragma unroll
       for (int k = 0; k < 4; ++k) d[k] = make_uint4(w, w, w, w);
       if constexpr (NST == 2 && K1 == 1) {
+        const uint2 e = __ldg(a.e81 + row);
 #pragma unroll
         for (int k = 0; k < 4; ++k) d[8 + k] = make_uint4(e.x, e.y, e.x, e.y);
       }
     }
   }
-  if (threadIdx.x == 0) {
-    for (std::uint32_t i = 0; i < kMaxRing; ++i) {
-      mbar_init(bar_full + 8 * i, 1);
-      mbar_init(bar_empty + 8 * i, kWarps);
-    }
-    fence_mbar_init();
-    asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n" ::"r"(ct_slot), "r"(kCtLo), "r"(kCtHi) : "memory");
-  }
   __syncthreads();
   pdl_trigger();
   if (threadIdx.x == 0) gstamp(a, 1);
 
-  if (!consumer) {
-    // ===== B-image producer: the k steps of this CTA's cells, in order =====
+  if (producer) {
+    // ===== producer: B images once K1 is done, then the rest of the cells =====
     if (lane == 0 && count > 0) {
-      pdl_wait();  // K1's B images
-      std::uint32_t k = ks;
-      for (std::uint32_t i = 0; i < count; ++i) {
-        const std::uint32_t slot = i % R;
-        if (i >= R) mbar_wait(bar_empty + 8 * slot, ((i / R) - 1) & 1);
-        mbar_arrive_expect_tx(bar_full + 8 * slot, a.b_bytes);
-        bulk_g2s(ring + slot * slot_bytes, a.bimg + std::size_t(k) * a.b_bytes, a.b_bytes, bar_full + 8 * slot);
-        if (++k == a.KSL) k = 0;
+      pdl_wait();
+      for (std::uint32_t i = 0; i < count && i < kEarly; ++i) issue_b(i);
+      for (std::uint32_t i = kEarly; i < count && i < S; ++i) {
+        issue_codes(i);
+        issue_b(i);
+      }
+      for (std::uint32_t i = S; i < count; ++i) {
+        mbar_wait(bar_empty + 8 * (i % S), ((i / S) - 1) & 1);
+        issue_codes(i);
+        issue_b(i);
       }
     }
     return;
   }
 
-  // ===== consumers =====
+  // ===== consumers: warp = (team, row pair rp) =====
+  const int team = warp / kRowPairs, rp = warp % kRowPairs;
   const int g = lane >> 2, t = lane & 3;
   const std::uint32_t lb0 = (lutw & 0xFFFF0000u) | (std::uint32_t(lane) * 4u);
   const std::uint32_t lb80 = (lutw & 0xFFFF0000u) | (128u + std::uint32_t(lane & 15) * 8u);
-  // per-lane B fragment offsets inside a ring slot (column block nb at +256 nb)
+  // per-lane B fragment offset (MMA j at + j * NB8 * 256, column block nb at + nb * 256)
   const std::uint32_t bmain = std::uint32_t((t >> 1) * 128 + g * 16 + (t & 1) * 8);
   const std::uint32_t bside = 8u * NB8 * 256u + std::uint32_t(g * 16 + 4 * t);
-  // the byte table read back from shared memory lives in ONE register each (as an
-  // immediate ptxas re-materialises it with a move in front of every PRMT)
+  // the byte table read back from shared memory lives in ONE register each
   const uint2 ct = lds64(ct_slot);
   const std::uint32_t ct_lo = ct.x, ct_hi = ct.y;
   std::uint32_t lb = lb0, lb8 = lb80;
-  // orders every LUT read (non-volatile asm) after the fill barrier: their
-  // addresses depend on this volatile asm
-  asm volatile("" : "+r"(lb), "+r"(lb8));
+  asm volatile("" : "+r"(lb), "+r"(lb8));  // LUT reads (non-volatile asm) stay after the fill barrier
   int acc[NST][2][NB8][4];
 #pragma unroll
   for (int s = 0; s < NST; ++s)
@@ -376,60 +357,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_mma_kernel(MmaArgs a) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[s][h][nb][q] = 0;
   bool waited = false;
-
-  // One cell: MMAs 0..3 (half 0 of the records), reload half 0 for the cell D ahead,
-  // MMAs 4..7 + side, reload half 1 -- the records are refilled in place as soon as
-  // each half is consumed (no register copies).
-  auto process = [&](Bundle<NST, K1>& cur, std::uint32_t i, bool act, bool reload, bool ract, std::uint32_t rrec) {
-    const std::uint32_t slot = i % R;
-    const std::uint32_t sl = ring + slot * slot_bytes;
-    mbar_wait(bar_full + 8 * slot, (i / R) & 1);
-    if (i == 0 && threadIdx.x == 0) gstamp(a, 2);
-#define Q8P_MMA_J(J)                                                                  \
-  {                                                                                   \
-    uint2 bf[NB8];                                                                    \
-    _Pragma("unroll") for (int nb = 0; nb < NB8; ++nb) bf[nb] =                       \
-        lds64(sl + (J) * NB8 * 256u + nb * 256u + bmain);                             \
-    e8p_mmas<J, NB8>(cur.e, bf, lb, ct_lo, ct_hi, acc[0]);                            \
-    if constexpr (NST == 2) {                                                         \
-      if constexpr (K1 == 0)                                                          \
-        e8p_mmas<J, NB8>(cur.e2, bf, lb, ct_lo, ct_hi, acc[NST - 1]);                 \
-      else                                                                            \
-        e81_mmas<J, NB8>(cur.b2, bf, lb8, acc[NST - 1]);                              \
-    }                                                                                 \
-  }
-#ifdef Q8P_MMA_EXP_STREAM  // experiment: loads only (records folded into one accumulator), no decode / MMA
-    if (act) acc[0][0][0][0] ^= int(cur.e.i0.x ^ cur.e.i0.y ^ cur.e.i0.z ^ cur.e.i0.w ^ cur.e.f0.x ^ cur.e.f0.y ^ cur.e.f0.z ^ cur.e.f0.w);
-    if (reload && ract) load_half<0>(cur, a, rrec, lane);
-    if (act) acc[0][0][0][1] ^= int(cur.e.i1.x ^ cur.e.i1.y ^ cur.e.i1.z ^ cur.e.i1.w ^ cur.e.f1.x ^ cur.e.f1.y ^ cur.e.f1.z ^ cur.e.f1.w ^ cur.e.sw);
-    if (reload && ract) load_half<1>(cur, a, rrec, lane);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(bar_empty + 8 * slot);
-    return;
-#endif
-    if (act) {
-      Q8P_MMA_J(0) Q8P_MMA_J(1) Q8P_MMA_J(2) Q8P_MMA_J(3)
-    }
-    if (reload && ract) load_half<0>(cur, a, rrec, lane);
-    if (act) {
-      Q8P_MMA_J(4) Q8P_MMA_J(5) Q8P_MMA_J(6) Q8P_MMA_J(7)
-      uint2 bs[NB8];
-#pragma unroll
-      for (int nb = 0; nb < NB8; ++nb) bs[nb] = make_uint2(lds32(sl + bside + nb * 256u), lds32(sl + bside + nb * 256u + 128u));
-      side_mmas<NB8>(cur.e.sw, bs, acc[0]);
-      if constexpr (NST == 2 && K1 == 0) side_mmas<NB8>(cur.e2.sw, bs, acc[NST - 1]);
-    }
-#undef Q8P_MMA_J
-    if (reload && ract) load_half<1>(cur, a, rrec, lane);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(bar_empty + 8 * slot);
-  };
-  auto flush = [&](std::uint32_t r_b) {
+  // rows of this warp's row pair in row block rb (cell = rb * KSL + ks)
+  auto flush = [&](std::uint32_t rb) {
     if (!waited) {
       pdl_wait();  // K1 zeroed the accumulators
       waited = true;
     }
-    const std::uint32_t row0 = (r_b * kWarps + std::uint32_t(warp)) * 32u + std::uint32_t(g);
+    const std::uint32_t row0 = (rb * kRowPairs + std::uint32_t(rp)) * 32u + std::uint32_t(g);
 #pragma unroll
     for (int s = 0; s < NST; ++s)
 #pragma unroll
@@ -448,40 +382,89 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_mma_kernel(MmaArgs a) {
         }
   };
 
-  for (std::uint32_t i = 0; i < count; i += D) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const std::uint32_t ii = i + d;
-      if (ii < count) {
-        const bool reload = ii + D < count;
-        const bool ract = reload && active_in(prb);
-        const std::uint32_t rrec = rec_of(prb, pks);
-        if (reload && ++pks == a.KSL) pks = 0, ++prb;
-        const bool act = active_in(rb);
-        process(buf[d], ii, act, reload, ract, rrec);
-        const bool last = ii + 1 == count || ks + 1 == a.KSL;
-        if (last && act) flush(rb);
-        if (++ks == a.KSL) ks = 0, ++rb;
+  // incremental cursors: slot st / phase ph of local cell i, its row block rb and k step ks
+  std::uint32_t st = std::uint32_t(team) % S, ph = (std::uint32_t(team) / S) & 1;
+  std::uint32_t rb = (c0 + std::uint32_t(team)) / a.KSL, ks = (c0 + std::uint32_t(team)) % a.KSL;
+  for (std::uint32_t i = std::uint32_t(team); i < count; i += TEAMS) {
+    const std::uint32_t sl = slot_addr(st);
+    mbar_wait(bar_full + 8 * st, ph);
+    if (i == 0 && threadIdx.x == 0) gstamp(a, 2);
+    const bool act = (rb * kRowPairs + std::uint32_t(rp)) * 32u < a.m_local;
+    // this warp's operands into registers, then the slot goes back to the producer
+    HalfE8p r0, r1, q0, q1;
+    uint4 e0, e1;
+    uint2 bf0[4][NB8], bf1[4][NB8], bs[NB8];
+    if (act) {
+      const std::uint32_t ra = sl + std::uint32_t(rp) * kRecE8p + lane * 16u;
+      r0.iw = lds128(ra);
+      r1.iw = lds128(ra + 512);
+      r0.fw = lds128(ra + 1024);
+      r1.fw = lds128(ra + 1536);
+      r0.sw = lds32(sl + std::uint32_t(rp) * kRecE8p + 2048u + lane * 4u);
+      if constexpr (NST == 2) {
+        if constexpr (K1 == 0) {
+          const std::uint32_t rq = sl + rec0 + std::uint32_t(rp) * kRecE8p + lane * 16u;
+          q0.iw = lds128(rq);
+          q1.iw = lds128(rq + 512);
+          q0.fw = lds128(rq + 1024);
+          q1.fw = lds128(rq + 1536);
+          q0.sw = lds32(sl + rec0 + std::uint32_t(rp) * kRecE8p + 2048u + lane * 4u);
+        } else {
+          const std::uint32_t re = sl + rec0 + std::uint32_t(rp) * kRecE81 + lane * 16u;
+          e0 = lds128(re);
+          e1 = lds128(re + 512);
+        }
       }
+      const std::uint32_t bbase = sl + rec0 + rec1;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+        for (int nb = 0; nb < NB8; ++nb) {
+          bf0[jj][nb] = lds64(bbase + jj * NB8 * 256u + nb * 256u + bmain);
+          bf1[jj][nb] = lds64(bbase + (4 + jj) * NB8 * 256u + nb * 256u + bmain);
+        }
+#pragma unroll
+      for (int nb = 0; nb < NB8; ++nb)
+        bs[nb] = make_uint2(lds32(bbase + bside + nb * 256u), lds32(bbase + bside + nb * 256u + 128u));
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar_empty + 8 * st);
+    const std::uint32_t rb_now = rb;
+    st += TEAMS;
+    if (st >= S) st -= S, ph ^= 1;
+    ks += TEAMS;
+    while (ks >= a.KSL) ks -= a.KSL, ++rb;
+    if (act) {
+      e8p_half<NB8>(r0, bf0, lb, ct_lo, ct_hi, acc[0]);
+      e8p_half<NB8>(r1, bf1, lb, ct_lo, ct_hi, acc[0]);
+      side_mma<0, NB8>(r0.sw, bs, acc[0]);
+      side_mma<1, NB8>(r0.sw, bs, acc[0]);
+      if constexpr (NST == 2) {
+        if constexpr (K1 == 0) {
+          e8p_half<NB8>(q0, bf0, lb, ct_lo, ct_hi, acc[1]);
+          e8p_half<NB8>(q1, bf1, lb, ct_lo, ct_hi, acc[1]);
+          side_mma<0, NB8>(q0.sw, bs, acc[1]);
+          side_mma<1, NB8>(q0.sw, bs, acc[1]);
+        } else {
+          e81_half<NB8>(e0, bf0, lb8, acc[1]);
+          e81_half<NB8>(e1, bf1, lb8, acc[1]);
+        }
+      }
+      if (i + TEAMS >= count || rb != rb_now) flush(rb_now);
     }
   }
   if (threadIdx.x == 0) gstamp(a, 3);
 }
 
-template <int NST, int K1, int NB8>
-void launch_k(const MmaArgs& a, cudaStream_t s) {
-  static std::once_flag once[64];
-  int dev = 0;
-  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-  std::call_once(once[dev & 63], [] {
-    cuda_check(cudaFuncSetAttribute(gemv_mma_kernel<NST, K1, NB8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(kSmem)),
-               "mma smem attr");
-  });
+template <int NST, int K1, int NB8, int TEAMS>
+void launch_k(MmaArgs a, cudaStream_t s) {
+  kernel_attrs(reinterpret_cast<const void*>(gemv_mma_kernel<NST, K1, NB8, TEAMS>), int(kSmem));
+  const int dev = current_device();
   static int sms[64] = {};
   if (!sms[dev & 63]) cuda_check(cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev), "sm count");
   const unsigned grid = unsigned(std::min<std::uint32_t>(a.cells, std::uint32_t(sms[dev & 63])));
-  launch_pdl(gemv_mma_kernel<NST, K1, NB8>, dim3(grid ? grid : 1), dim3(kThreads), kSmem, s, a);
+  a.smem_bytes = std::uint32_t(kSmem);
+  launch_pdl(gemv_mma_kernel<NST, K1, NB8, TEAMS>, dim3(grid ? grid : 1), dim3(Shape<TEAMS>::kThreads), kSmem, s, a);
 }
 
 // ---- transcode: plain codes [m_local][nb] (u16 E8P / u8 e8-1bit) -> records ----
@@ -496,8 +479,8 @@ __global__ void __launch_bounds__(256) mma_transcode_kernel(const void* __restri
        x += std::size_t(gridDim.x) * blockDim.x) {
     const std::uint32_t lane = std::uint32_t(x & 31);
     const std::size_t rec = x >> 5;  // records ordered [row block][k step][row pair in block]
-    const std::uint32_t wr = std::uint32_t(rec % kWarps), ks = std::uint32_t((rec / kWarps) % KSL),
-                        rp = std::uint32_t(rec / (std::size_t(kWarps) * KSL)) * kWarps + wr;
+    const std::uint32_t wr = std::uint32_t(rec % kRowPairs), ks = std::uint32_t((rec / kRowPairs) % KSL),
+                        rp = std::uint32_t(rec / (std::size_t(kRowPairs) * KSL)) * kRowPairs + wr;
     const std::uint32_t g = lane >> 2, t = lane & 3;
     auto word_at = [&](std::uint32_t row, std::uint32_t k) -> std::uint32_t {
       if (row >= m_local || k >= nb) return 0u;
@@ -543,14 +526,14 @@ __global__ void __launch_bounds__(256) mma_transcode_kernel(const void* __restri
 
 }  // namespace
 
-std::uint32_t mma_row_blocks(std::uint32_t m_local) { return (m_local + 32 * kWarps - 1) / (32 * kWarps); }
+std::uint32_t mma_row_blocks(std::uint32_t m_local) { return (m_local + 32 * kRowPairs - 1) / (32 * kRowPairs); }
 std::size_t mma_code_bytes(std::uint32_t m_local, std::uint32_t n, int kind) {
-  return std::size_t(mma_row_blocks(m_local)) * kWarps * tc_k_slabs(n) * (kind == 0 ? kRecE8p : kRecE81);
+  return std::size_t(mma_row_blocks(m_local)) * kRowPairs * tc_k_slabs(n) * (kind == 0 ? kRecE8p : kRecE81);
 }
 
 void mma_transcode_device(const void* codes, std::uint32_t m_local, std::uint32_t n, int kind, std::uint8_t* out,
                           const std::uint8_t* odd_parity_dev, cudaStream_t s) {
-  const std::uint32_t nb = n / 8, KSL = tc_k_slabs(n), RP = mma_row_blocks(m_local) * kWarps;
+  const std::uint32_t nb = n / 8, KSL = tc_k_slabs(n), RP = mma_row_blocks(m_local) * kRowPairs;
   const std::size_t total = std::size_t(RP) * KSL * 32;
   const unsigned grid = unsigned(std::min<std::size_t>((total + 255) / 256, 148 * 16));
   mma_transcode_kernel<<<grid, 256, 0, s>>>(codes, m_local, nb, KSL, RP, kind, out, odd_parity_dev);
@@ -603,11 +586,11 @@ void launch_gemv_mma(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t*
   const int nst = L.num_stages;
 #define Q8P_LAUNCH(NB8)                                     \
   if (nst == 1)                                             \
-    launch_k<1, 0, NB8>(a, s);                              \
+    launch_k<1, 0, NB8, NB8 == 1 ? 3 : 2>(a, s);            \
   else if (a.kind1 == 0)                                    \
-    launch_k<2, 0, NB8>(a, s);                              \
+    launch_k<2, 0, NB8, 2>(a, s);                           \
   else                                                      \
-    launch_k<2, 1, NB8>(a, s);
+    launch_k<2, 1, NB8, 2>(a, s);
   switch (N) {
     case 8: Q8P_LAUNCH(1) break;
     case 16: Q8P_LAUNCH(2) break;

@@ -776,25 +776,14 @@ constexpr std::size_t smem_for() {
 
 template <int N, int G, int T, bool FUSED, int NB>
 void set_attr() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G, T, FUSED, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(smem_for<N, FUSED>())),
-               "tc smem attr");
-    cuda_check(cudaFuncSetAttribute(gemv_tc_kernel<N, G, T, FUSED, NB>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                    100),
-               "carveout");
-  });
+  kernel_attrs(reinterpret_cast<const void*>(gemv_tc_kernel<N, G, T, FUSED, NB>), int(smem_for<N, FUSED>()));
 }
 
-int sm_count() {
-  static int v = [] {
-    int d = 0, c = 148;
-    cudaGetDevice(&d);
-    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, d);
-    return c;
-  }();
-  return v;
+int sm_count() {  // per device (layers may live on different devices of one process)
+  static int v[64] = {};
+  const int d = current_device() & 63;
+  if (!v[d]) cuda_check(cudaDeviceGetAttribute(&v[d], cudaDevAttrMultiProcessorCount, d), "sm count");
+  return v[d];
 }
 
 template <int N, int G, int T = 1, bool FUSED = false, int NB = 2>

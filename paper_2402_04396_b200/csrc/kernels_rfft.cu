@@ -236,13 +236,8 @@ void plan(const DevSide& side, RfftArgs& a) {
 }
 
 void set_smem_attrs() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cuda_check(cudaFuncSetAttribute(rfft_pass1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMaxSmem)),
-               "rfft smem attr");
-    cuda_check(cudaFuncSetAttribute(rfft_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMaxSmem)),
-               "rfft smem attr");
-  });
+  kernel_attrs(reinterpret_cast<const void*>(rfft_pass1), int(kMaxSmem));
+  kernel_attrs(reinterpret_cast<const void*>(rfft_pass2), int(kMaxSmem));
 }
 
 void launch_passes(const RfftArgs& a, int batch, std::uint32_t zero_ctas, cudaStream_t s) {

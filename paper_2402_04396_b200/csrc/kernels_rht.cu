@@ -398,13 +398,7 @@ void launch_cluster_q(const RhtArgs& a, std::uint32_t C, std::uint32_t zero_rows
   const std::size_t chunk = a.n / C;
   const std::size_t bsz = Q == 1 ? 0 : (Q <= 28 ? Q * Q * 4 : (Q * Q + 15) / 16 * 16);
   const std::size_t smem = 2 * chunk * 4 + bsz;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cuda_check(cudaFuncSetAttribute(rht_cluster<Q, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
-               "rht cluster smem attr");
-    cuda_check(cudaFuncSetAttribute(rht_cluster<Q, MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
-               "rht cluster attr");
-  });
+  kernel_attrs(reinterpret_cast<const void*>(rht_cluster<Q, MODE>), 96 * 1024, true);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(C, a.batch + zero_rows);
   cfg.blockDim = dim3(kClThreads);
@@ -533,12 +527,7 @@ bool single_ok(const DevSide& side) {
 
 template <int MODE>
 void launch_single(const RhtArgs& a, std::uint32_t zero_ctas, cudaStream_t s) {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cuda_check(cudaFuncSetAttribute(rht_single<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(kSingleMaxN * 4)),
-               "rht single smem attr");
-  });
+  kernel_attrs(reinterpret_cast<const void*>(rht_single<MODE>), int(kSingleMaxN * 4));
   launch_pdl(rht_single<MODE>, dim3(a.batch + zero_ctas), dim3(1024), std::size_t(a.n) * 4, s, a);
   cuda_check(cudaGetLastError(), "rht single launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -568,11 +557,7 @@ void launch_pass1_q(const RhtArgs& a, std::uint32_t extra_ctas, cudaStream_t s) 
   const std::size_t chunk = std::size_t(a.P2) * Q;
   const std::size_t bsz = Q == 1 ? 0 : (Q <= 28 ? Q * Q * 4 : (Q * Q + 15) / 16 * 16);
   const std::size_t smem = chunk * 4 * (Q > 1 ? 2 : 1) + bsz;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cuda_check(cudaFuncSetAttribute(rht_pass1<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
-               "rht smem attr");
-  });
+  kernel_attrs(reinterpret_cast<const void*>(rht_pass1<Q>), 96 * 1024);
   launch_pdl(rht_pass1<Q>, dim3(a.P1 + extra_ctas, a.batch), dim3(kP1Threads), smem, s, a);
 }
 
@@ -592,11 +577,7 @@ void launch_pass1(const RhtArgs& a, std::uint32_t extra, cudaStream_t s) {
 
 void launch_pass2(const RhtArgs& a, cudaStream_t s) {
   const std::uint32_t groups = a.P2 * a.q / 4;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cuda_check(cudaFuncSetAttribute(rht_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
-               "rht smem attr");
-  });
+  kernel_attrs(reinterpret_cast<const void*>(rht_pass2), 96 * 1024);
   launch_pdl(rht_pass2, dim3(groups, a.batch), dim3(128), std::size_t(a.P1) * 16, s, a);
   cuda_check(cudaGetLastError(), "rht pass2 launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -605,11 +586,7 @@ void launch_pass2(const RhtArgs& a, cudaStream_t s) {
 void launch_pass2_limbs(const RhtArgs& a, cudaStream_t s) {
   const std::uint32_t chunk = a.P2 * a.q;
   if (chunk % 8 != 0) throw SizeError("rht: chunk not a multiple of the codeword dimension");
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cuda_check(cudaFuncSetAttribute(rht_pass2_limbs, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
-               "rht smem attr");
-  });
+  kernel_attrs(reinterpret_cast<const void*>(rht_pass2_limbs), 96 * 1024);
   launch_pdl(rht_pass2_limbs, dim3(chunk / 8, a.batch), dim3(128), std::size_t(a.P1) * 32, s, a);
   cuda_check(cudaGetLastError(), "rht pass2 limbs launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -797,6 +774,7 @@ void launch_combine_acc(const std::int32_t* zacc, int zacc_stages, std::uint32_t
   a.alpha_in = alpha;
   a.tl_in = tl;
   const std::uint32_t quads = (m_local + 3) / 4;
+  kernel_attrs(reinterpret_cast<const void*>(combine_kernel), 0);
   launch_pdl(combine_kernel, dim3(std::min<std::uint32_t>((quads + 255) / 256, 148), batch), dim3(256), 0, s, a, z,
              m_local);
   cuda_check(cudaGetLastError(), "combine launch");

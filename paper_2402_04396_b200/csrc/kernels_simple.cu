@@ -22,10 +22,13 @@ struct ConstTables {
   std::int8_t e81[256][8];      // e8-1bit, doubled coordinates
 };
 __constant__ ConstTables c_tab;
-std::once_flag g_tab_once;
+// __constant__ memory is per device: one upload per device.
+std::once_flag g_tab_once[64];
 
 void upload_tables() {
-  std::call_once(g_tab_once, [] {
+  const int dev = current_device();
+  if (dev < 0 || dev >= 64) throw DeviceError("device index beyond the table cache");
+  std::call_once(g_tab_once[dev], [] {
     ConstTables h{};
     const E8PTable& t = e8p_table();
     for (int i = 0; i < 256; ++i) {
@@ -214,11 +217,7 @@ void launch_rht(const DevSide& side, const float* x, float* y, int batch, bool t
                 cudaStream_t s) {
   if (batch <= 0) return;
   const std::size_t smem = side.n * sizeof(float) + (side.q > 1 ? side.q * side.q : 0);
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cuda_check(cudaFuncSetAttribute(rht_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
-               "rht smem attr");
-  });
+  kernel_attrs(reinterpret_cast<const void*>(rht_kernel), 227 * 1024);
   if (smem > 227 * 1024) throw SizeError("rht: n too large for the single-CTA transform");
   rht_kernel<<<batch, 1024, smem, s>>>(side.n, side.p, side.q, side.signs, side.base, x, y,
                                        transpose ? 1 : 0);
