@@ -18,6 +18,8 @@
  *                         tools/latq_cli.cpp:192-215, loops it per row)
  *   q8p_decode_stage      Codebook::decode / e8p_decode  core/include/latq/
  *                         codebook.hpp:31, e8p.hpp:35 over a whole stage
+ *   q8p_k2_decode_stage   the same decode as the GEMV kernel performs it
+ *                         (parity probe of the hot-path decoder)
  *   q8p_rht               SideTransform::apply / apply_transpose
  *                         core/include/latq/transforms.hpp:30-33 (rht kind)
  *   q8p_plan_hadamard     latq::plan_hadamard  core/include/latq/hadamard.hpp:42
@@ -208,6 +210,30 @@ q8p_status q8p_infer_host(q8p_layer* layer, const double* x, double* y, int batc
 /* Unscaled incoherent-domain decode of one stage into device fp32
  * w_hat[m_local][n] (decoded values are exact quarter-integers). */
 q8p_status q8p_decode_stage(const q8p_layer* layer, int stage, float* w_hat, void* stream);
+
+/* Parity probe of the GEMV's own decoder (e8p_decode, core/src/e8p.cpp:81-100;
+ * TableCodebook::decode, codebook.cpp:65-72): runs the tensor-core K2's operand
+ * decode over the layer's transcoded slabs and writes the int8 A bytes it feeds
+ * the tensor cores, a_bytes[m_local][n] (E8P: sigma_c * doubled_c; e8-1bit: the
+ * doubled table row), and for E8P stages the shift bits shift_bits[m_local][n/8],
+ * so that the decoded value is (2 a + 2 b - 1) / 4 (E8P) or a / 2 (e8-1bit).
+ * Device pointers; stream-ordered. */
+q8p_status q8p_k2_decode_stage(const q8p_layer* layer, int stage, int8_t* a_bytes, uint8_t* shift_bits,
+                               void* stream);
+
+/* Benchmark support (the reference's bm_infer, bench/bench.cpp:103-120):
+ *  q8p_bench_gemv    `reps` back-to-back launches of the layer's decode-GEMV (K2)
+ *                    on the B images already in `ws` (run a forward with the same
+ *                    workspace and batch first); stream-ordered, chained with
+ *                    programmatic dependent launch as inside a forward.
+ *  q8p_bench_stream  `reps` launches of a plain HBM read of [src, src + bytes)
+ *                    in K2's access pattern (bulk copies into shared memory): the
+ *                    stream ceiling of the same bytes.
+ *  q8p_layer_code_region  device address / size of a stage's code slabs. */
+q8p_status q8p_bench_gemv(const q8p_layer* layer, int batch, void* workspace, size_t workspace_bytes, int reps,
+                          void* stream);
+q8p_status q8p_bench_stream(const void* src, size_t bytes, int reps, void* stream);
+q8p_status q8p_layer_code_region(const q8p_layer* layer, int stage, const void** codes, size_t* bytes);
 
 /* Randomized Hadamard transform on device fp32 vectors:
  *   transpose == 0:  y = H (S o x)          (SideTransform::apply)

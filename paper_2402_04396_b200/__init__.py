@@ -147,6 +147,10 @@ _SIGNATURES = {
     "q8p_forward_set_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                             ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "q8p_decode_stage": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
+    "q8p_bench_gemv": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]),
+    "q8p_bench_stream": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]),
+    "q8p_layer_code_region": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_size_t)]),
+    "q8p_k2_decode_stage": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "q8p_rht": (ctypes.c_int, [ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
     "q8p_qshp_inspect": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ArtifactInfo)]),
     "q8p_qshp_reserialize": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
@@ -428,6 +432,27 @@ class Layer:
         _check(lib().q8p_infer_host(self._h, x2.ctypes.data, y.ctypes.data, x2.shape[0]))
         return y[0] if squeeze else y
 
+    def bench_gemv(self, batch: int, workspace, reps: int, stream=None):
+        """`reps` back-to-back K2 launches on the B images in `workspace` (q8p_bench_gemv)."""
+        _check(lib().q8p_bench_gemv(self._h, batch, workspace.data_ptr(), workspace.numel(), reps, _stream_ptr(stream)))
+
+    def code_region(self, stage: int = 0):
+        """(device address, bytes) of a stage's code slabs (q8p_layer_code_region)."""
+        p, n = ctypes.c_void_p(), ctypes.c_size_t()
+        _check(lib().q8p_layer_code_region(self._h, stage, ctypes.byref(p), ctypes.byref(n)))
+        return p.value, n.value
+
+    def k2_decode_stage(self, stage: int, stream=None):
+        """The GEMV kernel's own operand decode of one stage (q8p_k2_decode_stage):
+        (a int8 [m_local][n], shift uint8 [m_local][n/8] or None for e8-1bit)."""
+        torch = _torch()
+        info = self.info
+        ml = info["row_end"] - info["row_begin"]
+        a = torch.empty(ml, info["n"], dtype=torch.int8, device=f"cuda:{info['device']}")
+        sh = torch.zeros(ml, info["n"] // 8, dtype=torch.uint8, device=a.device)
+        _check(lib().q8p_k2_decode_stage(self._h, stage, a.data_ptr(), sh.data_ptr(), _stream_ptr(stream)))
+        return a, sh
+
     def decode_stage(self, stage: int, stream=None):
         torch = _torch()
         info = self.info
@@ -523,6 +548,11 @@ def rvq_quantize(v, stages, stream=None):
     return out.to(torch.int32) & 0xFFFF
 
 
+def bench_stream(addr: int, nbytes: int, reps: int, stream=None):
+    """`reps` plain HBM reads of [addr, addr + nbytes) in K2's access pattern (q8p_bench_stream)."""
+    _check(lib().q8p_bench_stream(ctypes.c_void_p(addr), nbytes, reps, _stream_ptr(stream)))
+
+
 def rht_cols_f64(w, signs, stream=None):
     """SideTransform::apply (rht) on every column of a contiguous float64 CUDA
     matrix [rows, cols], in place; signs: uint8 CUDA tensor of ceil(rows/8)
@@ -547,3 +577,44 @@ def rht(x, signs, transpose: bool = False, out=None, stream=None):
     _check(lib().q8p_rht(x.shape[1], signs.data_ptr(), x.data_ptr(), out.data_ptr(), x.shape[0],
                          1 if transpose else 0, _stream_ptr(stream)))
     return out
+
+
+# RVQ schemes of the reference producer (rvq.cpp:9-21): codebook ids and rho_i.
+RVQ_SCHEMES = {2: (["e8p-2bit"], [0.9]), 3: (["e8p-2bit", "e8-1bit"], [0.98, 2.04]),
+               4: (["e8p-2bit", "e8p-2bit"], [1.03, 3.45])}
+
+
+def produce_artifact(w, signs_u, signs_v, bits: int) -> bytes:
+    """GPU producer: the reference's H = I quantize_layer route
+    (pipeline.cpp:47-107 with ldlq.cpp's nearest rounding) on a float64 CUDA weight
+    matrix w [m, n] and host sign-byte arrays -> QSHP v1 bytes, byte-identical to the
+    reference artifact for the same W and signs (tests/test_gpu_encode.py):
+    W~ = T_u W T_v^T in f64 (q8p_rht_cols_f64), r1 = ||W~|| / sqrt(mn) (column-major,
+    left-to-right sum as the reference), f32-frozen stage scales r1 / rho_i, RVQ codes
+    (q8p_rvq_quantize).  w is consumed (transformed in place)."""
+    import struct
+
+    import numpy as np
+    torch = _torch()
+    m, n = w.shape
+    if bits not in RVQ_SCHEMES:
+        raise ValidationError("bits must be 2, 3 or 4")
+    su = torch.from_numpy(np.ascontiguousarray(signs_u, dtype=np.uint8)).to(w.device)
+    sv = torch.from_numpy(np.ascontiguousarray(signs_v, dtype=np.uint8)).to(w.device)
+    rht_cols_f64(w, su)                          # transform_cols(left)
+    wt = w.t().contiguous()
+    rht_cols_f64(wt, sv)                         # transform_rows(right)
+    wt = wt.t().contiguous()
+    sq = (wt.t().contiguous().view(-1) ** 2).cpu().numpy()
+    r1 = np.sqrt(np.cumsum(sq)[-1]) / np.sqrt(float(m) * n)
+    ids, rho = RVQ_SCHEMES[bits]
+    s32 = [np.float32(r1 / r) for r in rho]
+    cbs = [CB_E8P_2BIT if i == "e8p-2bit" else CB_E8_1BIT for i in ids]
+    codes = rvq_quantize(wt.view(-1, 8), list(zip(cbs, [float(x) for x in s32]))).cpu().numpy()
+    body = b"QSHP" + struct.pack("<HIIBB", 1, m, n, 0, len(ids))
+    for i, sc in zip(ids, s32):
+        body += bytes([len(i)]) + i.encode() + struct.pack("<f", sc)
+    body += np.ascontiguousarray(signs_u, dtype=np.uint8).tobytes() + np.ascontiguousarray(signs_v, dtype=np.uint8).tobytes()
+    for cid, c in zip(ids, codes):
+        body += c.astype("<u2" if cid == "e8p-2bit" else "u1").tobytes()
+    return body

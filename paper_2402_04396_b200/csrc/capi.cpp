@@ -1117,6 +1117,63 @@ q8p_status q8p_decode_stage(const q8p_layer* L, int stage, float* w_hat, void* s
   }
 }
 
+q8p_status q8p_bench_gemv(const q8p_layer* L, int batch, void* ws, size_t ws_bytes, int reps, void* stream) {
+  try {
+    if (!L || !ws) throw q8p::ValidationError("null argument");
+    if (reps <= 0) return Q8P_OK;
+    if (!tc_supported(*L, batch)) throw q8p::UnsupportedError("bench_gemv needs the tensor-core path (batch <= 32)");
+    if (ws_bytes < workspace_size(L, batch)) throw q8p::SizeError("workspace too small");
+    DeviceGuard g(L->device);
+    Workspace w;
+    workspace_parts(L, batch, &w, ws);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (int r = 0; r < reps; ++r) {
+      if (use_mma(L, batch))
+        launch_gemv_mma(*L, w.bimg, w.zacc, w.rows_pad, batch, s);
+      else
+        launch_gemv_tc(*L, w.bimg, w.zacc, w.rows_pad, batch, s);
+    }
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_bench_stream(const void* src, size_t bytes, int reps, void* stream) {
+  try {
+    if (!src) throw q8p::ValidationError("null argument");
+    for (int r = 0; r < reps; ++r) launch_stream(src, bytes, nullptr, static_cast<cudaStream_t>(stream));
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_layer_code_region(const q8p_layer* L, int stage, const void** codes, size_t* bytes) {
+  try {
+    if (!L || !codes || !bytes) throw q8p::ValidationError("null argument");
+    if (stage < 0 || stage >= L->num_stages) throw q8p::ValidationError("stage out of range");
+    *codes = L->tc[stage].codes;
+    *bytes = tc_code_bytes(L->m_local(), L->n, L->cb[stage] == Q8P_CB_E8P_2BIT ? 0 : 1);
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_k2_decode_stage(const q8p_layer* L, int stage, int8_t* a_bytes, uint8_t* shift_bits, void* stream) {
+  try {
+    if (!L || !a_bytes) throw q8p::ValidationError("null argument");
+    if (stage < 0 || stage >= L->num_stages) throw q8p::ValidationError("stage out of range");
+    if (L->cb[stage] == Q8P_CB_E8P_2BIT && !shift_bits) throw q8p::ValidationError("E8P stage needs shift_bits");
+    DeviceGuard g(L->device);
+    launch_k2_decode(*L, stage, a_bytes, shift_bits, static_cast<cudaStream_t>(stream));
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
 q8p_status q8p_rht(size_t n, const uint8_t* signs, const float* x, float* y, int batch, int transpose,
                    void* stream) {
   try {

@@ -153,6 +153,12 @@ constexpr int kTcMaxBatch = 32;  // tensor-core path: batch <= 32 per launch (MM
 bool tc_supported(const q8p_layer& L, int batch);
 int tc_ncols_pad(int ncols);                              // MMA N for `ncols` B rows
 std::uint32_t tc_bimg_bytes(std::uint32_t n, int batch);  // B images for all k slabs
+// Benchmark support (bench_kernels.cu): bulk-copy stream of `bytes` at src (the
+// HBM read ceiling in K2's access pattern).
+void launch_stream(const void* src, std::size_t bytes, unsigned* sink, cudaStream_t s);
+// Parity probe: K2's own operand decode over the slabs of `stage` -> a[m_local][n] (s8,
+// sigma*d for E8P, doubled row for e8-1bit) and side[m_local][n/8] (E8P shift bits).
+void launch_k2_decode(const q8p_layer& L, int stage, std::int8_t* a_out, std::uint8_t* side, cudaStream_t s);
 void launch_gemv_tc(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* zacc, std::uint32_t rows_pad,
                     int batch, cudaStream_t s);
 // Warp-level tensor-core GEMV for decode batches (gemv_mma.cu): same K1 B images,

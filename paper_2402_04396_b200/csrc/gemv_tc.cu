@@ -246,6 +246,63 @@ __device__ __forceinline__ void e8p_fin(std::uint32_t nib, std::uint32_t fl, std
   hi = prmt(ct_lo, ct_hi, __umulhi(sel, 65536u));  // sel >> 16
 }
 
+// One slab row (thread = row `row_in` of a 128-row slab at smem address `sa`):
+// the K2 operand decode shared by the GEMV and the parity probe k2_decode_kernel.
+struct SlabRowE8p {
+  std::uint32_t idx[8], fl[8], sw;
+};
+__device__ __forceinline__ SlabRowE8p load_row_e8p(std::uint32_t sa, std::uint32_t row_in) {
+  SlabRowE8p r;
+  const uint4 i0 = lds128(sa + row_in * 16), i1 = lds128(sa + 2048 + row_in * 16);
+  const uint4 f0 = lds128(sa + 4096 + row_in * 16), f1 = lds128(sa + 6144 + row_in * 16);
+  r.sw = lds32(sa + 8192 + row_in * 4);
+  r.idx[0] = i0.x, r.idx[1] = i0.y, r.idx[2] = i0.z, r.idx[3] = i0.w;
+  r.idx[4] = i1.x, r.idx[5] = i1.y, r.idx[6] = i1.z, r.idx[7] = i1.w;
+  r.fl[0] = f0.x, r.fl[1] = f0.y, r.fl[2] = f0.z, r.fl[3] = f0.w;
+  r.fl[4] = f1.x, r.fl[5] = f1.y, r.fl[6] = f1.z, r.fl[7] = f1.w;
+  return r;
+}
+// A bytes of the row's 32 codewords: codeword 4 g4 + jj -> o[ob + 2 jj] (coordinates
+// 0-3), o[ob + 2 jj + 1] (4-7), ob = 16 (g4 >> 1) + 8 (g4 & 1) (the tcgen05.st column
+// order); side bytes sd[k8] byte i = shift bit of codeword 4 k8 + i.
+__device__ __forceinline__ void decode_row_e8p(const SlabRowE8p& r, std::uint32_t lb, std::uint32_t ct_lo,
+                                               std::uint32_t ct_hi, std::uint32_t (&o)[64], std::uint32_t (&sd)[8]) {
+#pragma unroll
+  for (int g4 = 0; g4 < 8; ++g4) {
+    const int ob = 16 * (g4 >> 1) + 8 * (g4 & 1);
+#ifdef Q8P_EXP_LDS_ONLY  // experiment: keep the LUT loads, drop the ALU decode
+    o[ob + 0] = e8p_nib<0>(r.idx[g4], lb); o[ob + 1] = r.fl[g4];
+    o[ob + 2] = e8p_nib<1>(r.idx[g4], lb); o[ob + 3] = r.fl[g4];
+    o[ob + 4] = e8p_nib<2>(r.idx[g4], lb); o[ob + 5] = r.fl[g4];
+    o[ob + 6] = e8p_nib<3>(r.idx[g4], lb); o[ob + 7] = r.fl[g4];
+    continue;
+#endif
+    e8p_fin<0>(e8p_nib<0>(r.idx[g4], lb), r.fl[g4], ct_lo, ct_hi, o[ob + 0], o[ob + 1]);
+    e8p_fin<1>(e8p_nib<1>(r.idx[g4], lb), r.fl[g4], ct_lo, ct_hi, o[ob + 2], o[ob + 3]);
+    e8p_fin<2>(e8p_nib<2>(r.idx[g4], lb), r.fl[g4], ct_lo, ct_hi, o[ob + 4], o[ob + 5]);
+    e8p_fin<3>(e8p_nib<3>(r.idx[g4], lb), r.fl[g4], ct_lo, ct_hi, o[ob + 6], o[ob + 7]);
+  }
+#pragma unroll
+  for (int k8 = 0; k8 < 8; ++k8)  // side A = b_k; the shift on the FMA pipe (mul.hi)
+    sd[k8] = (k8 == 0 ? r.sw : __umulhi(r.sw, 1u << (32 - k8))) & 0x01010101u;
+}
+// e8-1bit: A = the doubled table row of each code byte, same column order.
+__device__ __forceinline__ void decode_row_e81(std::uint32_t sa, std::uint32_t row_in, std::uint32_t lb8,
+                                               std::uint32_t (&o)[64]) {
+  const uint4 c0 = lds128(sa + row_in * 16), c1 = lds128(sa + 2048 + row_in * 16);
+  const std::uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+  for (int g4 = 0; g4 < 8; ++g4) {
+    const int ob = 16 * (g4 >> 1) + 8 * (g4 & 1);
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const uint2 v = lut64(prmt(cw[g4], lb8, 0x7604u | (std::uint32_t(jj) << 4)));
+      o[ob + 2 * jj] = v.x;
+      o[ob + 2 * jj + 1] = v.y;
+    }
+  }
+}
+
 template <int N, int G, int T, bool FUSED, int NB>
 __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArgs a) {
   extern __shared__ __align__(1024) std::uint8_t smem[];
@@ -537,7 +594,6 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
     // with a UR->R move in front of every PRMT: +1 instruction per codeword)
     const uint2 ct = lds64(ct_slot);
     const std::uint32_t ct_lo = ct.x, ct_hi = ct.y;
-    std::uint32_t sink = 0;
     if (count > i_first) mbar_wait(bar_lut, 0);  // the producer copies the LUT only when it has work
     if (warp == kWarpDec) tstamp(a, 10, 1, 0);
 #ifdef Q8P_STAGGER_NS
@@ -556,36 +612,13 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
       if (tw) tstamp(a, grp, i, 1);
       const std::uint32_t abuf = tbase + tl + (NB * grp + buf) * kAcols;
       if (e8p) {
-        const uint4 i0 = lds128(sa + row_in * 16), i1 = lds128(sa + 2048 + row_in * 16);
-        const uint4 f0 = lds128(sa + 4096 + row_in * 16), f1 = lds128(sa + 6144 + row_in * 16);
-        const std::uint32_t sw = lds32(sa + 8192 + row_in * 4);
-        const std::uint32_t idx[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
-        const std::uint32_t fl[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+        const SlabRowE8p row = load_row_e8p(sa, row_in);
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_empty_c + 8 * st);  // slab is in registers: hand the slot back
-#if Q8P_K2_DECODE_AHEAD
-        // Decode the whole slab into registers first, then wait for the A buffer:
+        // Decode the whole slab row into registers first, then wait for the A buffer:
         // the decode overlaps the MMA turnaround of the buffer's previous item.
-        std::uint32_t o[64];
-#pragma unroll
-        for (int g4 = 0; g4 < 8; ++g4) {
-          const int ob = 16 * (g4 >> 1) + 8 * (g4 & 1);
-#ifdef Q8P_EXP_LDS_ONLY  // experiment: keep the LUT loads, drop the ALU decode
-          o[ob + 0] = e8p_nib<0>(idx[g4], lb); o[ob + 1] = fl[g4];
-          o[ob + 2] = e8p_nib<1>(idx[g4], lb); o[ob + 3] = fl[g4];
-          o[ob + 4] = e8p_nib<2>(idx[g4], lb); o[ob + 5] = fl[g4];
-          o[ob + 6] = e8p_nib<3>(idx[g4], lb); o[ob + 7] = fl[g4];
-          continue;
-#endif
-          e8p_fin<0>(e8p_nib<0>(idx[g4], lb), fl[g4], ct_lo, ct_hi, o[ob + 0], o[ob + 1]);
-          e8p_fin<1>(e8p_nib<1>(idx[g4], lb), fl[g4], ct_lo, ct_hi, o[ob + 2], o[ob + 3]);
-          e8p_fin<2>(e8p_nib<2>(idx[g4], lb), fl[g4], ct_lo, ct_hi, o[ob + 4], o[ob + 5]);
-          e8p_fin<3>(e8p_nib<3>(idx[g4], lb), fl[g4], ct_lo, ct_hi, o[ob + 6], o[ob + 7]);
-        }
-        std::uint32_t sd[8];
-#pragma unroll
-        for (int k8 = 0; k8 < 8; ++k8)  // side A = b_k; the shift on the FMA pipe (mul.hi)
-          sd[k8] = (k8 == 0 ? sw : __umulhi(sw, 1u << (32 - k8))) & 0x01010101u;
+        std::uint32_t o[64], sd[8];
+        decode_row_e8p(row, lb, ct_lo, ct_hi, o, sd);
         // pin every result before the wait (an empty asm consuming them; no code)
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4)
@@ -601,76 +634,16 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) tmem_st16(abuf + 16 * qq, *reinterpret_cast<std::uint32_t(*)[16]>(o + 16 * qq));
         tmem_st8(abuf + 64, sd);
-#else
-        // magnitude nibbles of all 32 codewords first (LDS latency overlaps the wait)
-        std::uint32_t nib[32];
-#pragma unroll
-        for (int g4 = 0; g4 < 8; ++g4) {
-          nib[4 * g4 + 0] = e8p_nib<0>(idx[g4], lb);
-          nib[4 * g4 + 1] = e8p_nib<1>(idx[g4], lb);
-          nib[4 * g4 + 2] = e8p_nib<2>(idx[g4], lb);
-          nib[4 * g4 + 3] = e8p_nib<3>(idx[g4], lb);
-        }
-        A_EMPTY_WAIT(bar_a_empty + 8 * (NB * grp + buf), bph ^ 1);
-        if (tw) tstamp(a, grp, i, 2);
-        tc_fence_after();
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-          std::uint32_t o[16];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int g4 = 2 * qq + h;  // codewords 4 g4 .. 4 g4 + 3
-#ifdef Q8P_EXP_NO_DECODE
-            for (int z = 0; z < 8; ++z) o[8 * h + z] = idx[g4] ^ fl[g4];
-#else
-            e8p_fin<0>(nib[4 * g4 + 0], fl[g4], ct_lo, ct_hi, o[8 * h + 0], o[8 * h + 1]);
-            e8p_fin<1>(nib[4 * g4 + 1], fl[g4], ct_lo, ct_hi, o[8 * h + 2], o[8 * h + 3]);
-            e8p_fin<2>(nib[4 * g4 + 2], fl[g4], ct_lo, ct_hi, o[8 * h + 4], o[8 * h + 5]);
-            e8p_fin<3>(nib[4 * g4 + 3], fl[g4], ct_lo, ct_hi, o[8 * h + 6], o[8 * h + 7]);
-#endif
-          }
-#ifdef Q8P_EXP_NO_STTM
-          for (int z = 0; z < 16; ++z) sink ^= o[z];
-#else
-          tmem_st16(abuf + 16 * qq, o);
-#endif
-        }
-        std::uint32_t sd[8];
-        sd[0] = sw & 0x01010101u;  // side A = b_k (0/1): the side B rows are the exact S_k
-        sd[1] = (sw >> 1) & 0x01010101u;
-        sd[2] = (sw >> 2) & 0x01010101u;
-        sd[3] = (sw >> 3) & 0x01010101u;
-        sd[4] = (sw >> 4) & 0x01010101u;
-        sd[5] = (sw >> 5) & 0x01010101u;
-        sd[6] = (sw >> 6) & 0x01010101u;
-        sd[7] = (sw >> 7) & 0x01010101u;
-        tmem_st8(abuf + 64, sd);
-#endif
       } else {
-        const uint4 c0 = lds128(sa + row_in * 16), c1 = lds128(sa + 2048 + row_in * 16);
-        const std::uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        std::uint32_t o[64];
+        decode_row_e81(sa, row_in, lb8, o);
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_empty_c + 8 * st);
         A_EMPTY_WAIT(bar_a_empty + 8 * (NB * grp + buf), bph ^ 1);
         tc_fence_after();
 #pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-          std::uint32_t o[16];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-              const uint2 v = lut64(prmt(cw[2 * qq + h], lb8, 0x7604u | (std::uint32_t(jj) << 4)));
-              o[8 * h + 2 * jj] = v.x;
-              o[8 * h + 2 * jj + 1] = v.y;
-            }
-          }
-          tmem_st16(abuf + 16 * qq, o);
-        }
+        for (int qq = 0; qq < 4; ++qq) tmem_st16(abuf + 16 * qq, *reinterpret_cast<std::uint32_t(*)[16]>(o + 16 * qq));
       }
-#ifdef Q8P_EXP_NO_STTM
-      if (sink == 0x12345679u) a.zacc[0] = 1;
-#endif
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
@@ -1096,6 +1069,62 @@ void launch_layer_fused(const q8p_layer& L, const float* x, float* y, float* u_s
       std::fclose(f);
     }
   }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+
+// ---- parity probe: K2's own operand decode over the transcoded slabs -------------
+namespace {
+// One CTA per slab: the slab and the LUT window are loaded into shared memory as
+// K2 loads them, then each thread runs K2's row decode (load_row_e8p /
+// decode_row_e8p, decode_row_e81) and writes the A bytes it would store to TMEM:
+// a[row][8k + c] (s8) and, for E8P, the side byte (shift bit) side[row][k].
+__global__ void __launch_bounds__(128) k2_decode_kernel(const std::uint8_t* __restrict__ slabs, std::uint32_t slab_bytes,
+                                                        int kind, std::uint32_t m_local, std::uint32_t nb,
+                                                        std::uint32_t KSL, const std::uint8_t* __restrict__ lut_img,
+                                                        std::int8_t* __restrict__ a_out, std::uint8_t* __restrict__ side) {
+  extern __shared__ __align__(1024) std::uint8_t smem[];
+  const std::uint32_t sbase = smem_u32(smem);
+  const std::uint32_t lutw = (sbase + kE8pSlab + 0xFFFFu) & ~0xFFFFu;
+  const std::uint32_t rb = blockIdx.x / KSL, ks = blockIdx.x % KSL;
+  const std::uint8_t* src = slabs + std::size_t(blockIdx.x) * slab_bytes;
+  for (std::uint32_t i = threadIdx.x; i < slab_bytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = reinterpret_cast<const uint4*>(src)[i];
+  for (std::uint32_t i = threadIdx.x; i < 65536 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem + (lutw - sbase))[i] = reinterpret_cast<const uint4*>(lut_img)[i];
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n" ::"r"(lutw - 16), "r"(kCtLo), "r"(kCtHi) : "memory");
+  __syncthreads();
+  const std::uint32_t lane = threadIdx.x & 31, row_in = threadIdx.x;
+  const std::uint32_t lb = (lutw & 0xFFFF0000u) | (lane * 4u);
+  const std::uint32_t lb8 = (lutw & 0xFFFF0000u) | (128u + (lane & 15) * 8u);
+  const uint2 ct = lds64(lutw - 16);
+  std::uint32_t o[64], sd[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (kind == 0)
+    decode_row_e8p(load_row_e8p(sbase, row_in), lb, ct.x, ct.y, o, sd);
+  else
+    decode_row_e81(sbase, row_in, lb8, o);
+  const std::uint32_t row = rb * 128 + row_in;
+  if (row >= m_local) return;
+  for (int w = 0; w < 32; ++w) {
+    const std::uint32_t k = ks * 32 + w;
+    if (k >= nb) break;
+    const int g4 = w >> 2, jj = w & 3, ob = 16 * (g4 >> 1) + 8 * (g4 & 1);
+    *reinterpret_cast<uint2*>(a_out + (std::size_t(row) * nb + k) * 8) = make_uint2(o[ob + 2 * jj], o[ob + 2 * jj + 1]);
+    if (side) side[std::size_t(row) * nb + k] = std::uint8_t((sd[w >> 2] >> (8 * (w & 3))) & 1u);
+  }
+}
+}  // namespace
+
+void launch_k2_decode(const q8p_layer& L, int stage, std::int8_t* a_out, std::uint8_t* side, cudaStream_t s) {
+  if (!L.tc[stage].codes) throw UnsupportedError("layer has no tensor-core slabs");
+  const int kind = L.cb[stage] == Q8P_CB_E8P_2BIT ? 0 : 1;
+  const std::uint32_t KSL = tc_k_slabs(L.n), RB = tc_row_blocks(L.m_local());
+  constexpr int kSmemProbe = 140 * 1024;
+  kernel_attrs(reinterpret_cast<const void*>(k2_decode_kernel), kSmemProbe);
+  k2_decode_kernel<<<RB * KSL, 128, kSmemProbe, s>>>(static_cast<const std::uint8_t*>(L.tc[stage].codes),
+                                                    tc_slab_bytes(kind), kind, L.m_local(), L.n / 8, KSL, L.lut_img,
+                                                    a_out, kind == 0 ? side : nullptr);
+  cuda_check(cudaGetLastError(), "k2 decode probe launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 

@@ -55,29 +55,29 @@ def test_gpu_producer_equals_reference_quantize(ref, m, n, bits, seed):
     # The H = I producer route (ref_quantize_hi == quantize_layer(W, I, cfg)) with
     # every numeric step on the GPU: W~ = T_u W T_v^T in f64 (q8p_rht_cols_f64),
     # RVQ codes (q8p_rvq_quantize); the artifact bytes must equal the reference's.
-    import struct
-
     w = ref.gen_weights(m, n, ref.substream_seed(seed, 10))
     su = ref.random_signs(m, ref.substream_seed(seed, 0))
     sv = ref.random_signs(n, ref.substream_seed(seed, 1))
-    d = torch.from_numpy(w).cuda()
-    q8p.rht_cols_f64(d, torch.from_numpy(su).cuda())                 # transform_cols(left)
-    dt = d.t().contiguous()
-    q8p.rht_cols_f64(dt, torch.from_numpy(sv).cuda())                # transform_rows(right)
-    wt = dt.t().contiguous()
-    host = wt.cpu().numpy()
-    sq = host.T.ravel() ** 2                                         # column-major, left-to-right sum
-    r1 = np.sqrt(np.cumsum(sq)[-1]) / np.sqrt(float(m) * n)
-    ids = {2: ["e8p-2bit"], 3: ["e8p-2bit", "e8-1bit"], 4: ["e8p-2bit", "e8p-2bit"]}[bits]
-    rho = {2: [0.9], 3: [0.98, 2.04], 4: [1.03, 3.45]}[bits]
-    s32 = [np.float32(r1 / r) for r in rho]
-    cbs = [q8p.CB_E8P_2BIT if i == "e8p-2bit" else q8p.CB_E8_1BIT for i in ids]
-    codes = q8p.rvq_quantize(wt.view(-1, 8), list(zip(cbs, [float(x) for x in s32]))).cpu().numpy()
-    body = b"QSHP" + struct.pack("<HIIBB", 1, m, n, 0, len(ids))
-    for i, sc in zip(ids, s32):
-        body += bytes([len(i)]) + i.encode() + struct.pack("<f", sc)
-    body += su.tobytes() + sv.tobytes()
-    for cid, c in zip(ids, codes):
-        body += c.astype("<u2" if cid == "e8p-2bit" else "u1").tobytes()
+    body = q8p.produce_artifact(torch.from_numpy(w).cuda(), su, sv, bits)
     want = ref.quantize_hi(m, n, bits, seed)
     assert body == want
+
+
+def test_reference_quantized_4096_batch1(ref, oracle):
+    # BASELINE configs[0]: a single 4096 x 4096 E8P 2-bit layer of Gaussian weights
+    # quantized by the reference route (gen_weights, harness.cpp:136-146; H = I
+    # quantize_layer) -- the GPU producer's artifact is byte-identical to the
+    # reference's, and its batch-1 forward matches the reference infer.
+    m = n = 4096
+    seed = 0
+    w = ref.gen_weights(m, n, ref.substream_seed(seed, 10))
+    su = ref.random_signs(m, ref.substream_seed(seed, 0))
+    sv = ref.random_signs(n, ref.substream_seed(seed, 1))
+    art = q8p.produce_artifact(torch.from_numpy(w).cuda(), su, sv, 2)
+    assert art == ref.quantize_hi(m, n, 2, seed, threads=16)
+    x = ref.gen_weights(1, n, ref.substream_seed(seed, 12)).astype(np.float32).astype(np.float64)
+    L = q8p.Layer.from_qshp(art)
+    got = L.forward(torch.from_numpy(x.astype(np.float32)).cuda()).cpu().numpy()
+    want = ref.infer(art, x, threads=16)
+    err = np.linalg.norm(got[0] - want[0]) / np.linalg.norm(want[0])
+    assert err < 1e-5, err

@@ -40,6 +40,40 @@ def test_decode_all_65536_words_bit_exact(dev, oracle):
     assert np.array_equal(w, want)
 
 
+def test_k2_decoder_all_65536_words_bit_exact(dev, oracle):
+    # The decoder that runs on the hot path: K2's slab / LUT-nibble / negate-flag
+    # decode (gemv_tc.cu load_row_e8p + decode_row_e8p over the transcoded slabs),
+    # probed through q8p_k2_decode_stage, against the reference e8p_decode
+    # (e8p.cpp:81-100) for every 16-bit word: v = (2 a + 2 b - 1) / 4.
+    words = np.arange(65536, dtype=np.uint16)
+    art = random_artifact(256, 2048, [("e8p-2bit", 1.0)], 0, codes=[words])
+    L = q8p.Layer.from_qshp(art)
+    a, sh = L.k2_decode_stage(0)
+    a = a.cpu().numpy().astype(np.float64)
+    b = np.repeat(sh.cpu().numpy().astype(np.float64), 8, axis=1)
+    got = (2.0 * a + 2.0 * b - 1.0) / 4.0
+    want = oracle.decode_stage(art, 0)
+    assert np.array_equal(got, want), np.argwhere(got != want)[:5]
+    # ragged slabs (n / 8 not a multiple of 32) and a partial row block
+    art2 = random_artifact(160, 320, [("e8p-2bit", 1.0)], 3)  # nb = 40, rows 128 + 32
+    L2 = q8p.Layer.from_qshp(art2)
+    a2, sh2 = L2.k2_decode_stage(0)
+    got2 = (2.0 * a2.cpu().numpy() + 2.0 * np.repeat(sh2.cpu().numpy(), 8, axis=1) - 1.0) / 4.0
+    assert np.array_equal(got2, oracle.decode_stage(art2, 0))
+
+
+def test_k2_decoder_e8_1bit_all_codes_bit_exact(dev, oracle):
+    # 3-bit second stage on the hot path: K2's e8-1bit LUT rows, all 256 codes
+    c2 = np.tile(np.arange(256, dtype=np.uint8), 16)  # 128 x 256 -> 4096 codewords
+    art = random_artifact(128, 256, [("e8p-2bit", 1.0), ("e8-1bit", 0.5)], 1, codes=[None, c2])
+    L = q8p.Layer.from_qshp(art)
+    a, _ = L.k2_decode_stage(1)
+    assert np.array_equal(a.cpu().numpy().astype(np.float64) / 2.0, oracle.decode_stage(art, 1))
+    a0, s0 = L.k2_decode_stage(0)
+    got0 = (2.0 * a0.cpu().numpy() + 2.0 * np.repeat(s0.cpu().numpy(), 8, axis=1) - 1.0) / 4.0
+    assert np.array_equal(got0, oracle.decode_stage(art, 0))
+
+
 def test_decode_e8_1bit_table_bit_exact(dev, oracle):
     c2 = np.tile(np.arange(256, dtype=np.uint8), 64 * 64 // 256 // 8 * 8)[: 64 * 64 // 8]
     art = random_artifact(64, 64, [("e8p-2bit", 1.0), ("e8-1bit", 0.5)], 1, codes=[None, c2])

@@ -72,3 +72,38 @@ def test_large_layer_all_batch_variants(dev, oracle, batch):
     got = L.forward(torch.from_numpy(x.astype(np.float32)).to(dev)).cpu().numpy()
     for b in range(batch):
         assert rel_err(got[b], want[b]) < TC, (b, rel_err(got[b], want[b]))
+
+
+@pytest.mark.parametrize("bits", [3, 4])
+@pytest.mark.parametrize("m,n", [(11008, 4096), (4096, 11008), (28672, 8192)])
+def test_rvq_big_shapes_vs_oracle(dev, oracle, m, n, bits):
+    # BASELINE configs[3] (3/4-bit RVQ) on the 7B MLP and 70B MLP shapes, batch 1 and 2
+    art = random_artifact(m, n, STAGES[bits], m + 3 * n + bits)
+    L = q8p.Layer.from_qshp(art)
+    x = np.random.default_rng(bits).standard_normal((2, n)).astype(np.float32).astype(np.float64)
+    want = oracle.infer(art, x, threads=16)
+    got = L.forward(torch.from_numpy(x.astype(np.float32)).to(dev)).cpu().numpy()
+    for b in range(2):
+        assert rel_err(got[b], want[b]) < TC, (b, rel_err(got[b], want[b]))
+    assert rel_err(L.forward(torch.from_numpy(x[:1].astype(np.float32)).to(dev)).cpu().numpy()[0], want[0]) < TC
+
+
+@pytest.mark.parametrize("m,n,batch", [(8192, 8192, 1024), (8192, 8192, 2048), (28672, 8192, 1024),
+                                       (28672, 8192, 2048)])
+def test_prefill_configs(dev, oracle, m, n, batch):
+    # BASELINE configs[4] (prefill batch 128-2048) at the 70B shapes: every sampled
+    # row of the batched call equals the single-vector call bit for bit (per-vector
+    # activation scales, exact integer accumulation), and sampled rows match the oracle.
+    art = random_artifact(m, n, STAGES[2], m + batch)
+    L = q8p.Layer.from_qshp(art)
+    x = torch.randn(batch, n, generator=torch.Generator().manual_seed(batch)).to(dev)
+    y = L.forward(x)
+    assert y.shape == (batch, m) and bool(torch.isfinite(y).all())
+    rows = [0, 1, 31, 32, 511, batch // 2 + 7, batch - 33, batch - 1]
+    for b in rows:
+        assert torch.equal(y[b], L.forward(x[b:b + 1].contiguous())[0]), b
+    sample = [0, batch // 2 + 7, batch - 1]
+    xs = x[sample].cpu().numpy().astype(np.float64)
+    want = oracle.infer(art, xs, threads=16)
+    for i, b in enumerate(sample):
+        assert rel_err(y[b].cpu().numpy(), want[i]) < TC, (b, rel_err(y[b].cpu().numpy(), want[i]))
