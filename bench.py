@@ -46,6 +46,8 @@ sys.path.insert(0, ROOT)
 
 LAYERS_70B = [(8192, 8192), (28672, 8192), (8192, 28672)]
 LAYERS_7B = [(4096, 4096)] * 4 + [(11008, 4096)] * 2 + [(4096, 11008)]
+LAYERS_4096 = [(4096, 4096)]  # BASELINE configs[0]: one 4096 x 4096 layer
+WORKLOADS = {"70b": LAYERS_70B, "7b": LAYERS_7B, "4096": LAYERS_4096}
 METRIC = "E8P 2-bit quantized matvec: achieved HBM GB/s vs peak; layer tokens/s at batch 1"
 
 
@@ -80,6 +82,42 @@ def make_artifact(m: int, n: int, seed: int, scale: float = 1.11, bits: int = 2)
         else:
             body += rng.integers(0, 256, m * n // 8, dtype=np.uint8).tobytes()
     return body
+
+
+def make_artifact_gaussian(m: int, n: int, seed: int, bits: int = 2) -> bytes:
+    """North-star weights: synthetic Gaussian W (N(0,1), seeded torch generator on the
+    device) quantized by the reference's H = I producer route on the GPU
+    (q8p.produce_artifact: RHT incoherence, r1, f32-frozen default_scheme(bits)
+    scales, RVQ codes -- byte-identical to quantize_layer(W, I) for the same W,
+    tests/test_gpu_encode.py)."""
+    import torch
+    import paper_2402_04396_b200 as q8p
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    w = torch.randn(m, n, generator=g, device="cuda", dtype=torch.float64)
+    rng = np.random.default_rng(seed)
+    su = rng.integers(0, 256, (m + 7) // 8, dtype=np.uint8)
+    sv = rng.integers(0, 256, (n + 7) // 8, dtype=np.uint8)
+    if m % 8:
+        su[-1] &= (1 << (m % 8)) - 1
+    if n % 8:
+        sv[-1] &= (1 << (n % 8)) - 1
+    art = q8p.produce_artifact(w, su, sv, bits, exact_r1=False)
+    del w
+    torch.cuda.empty_cache()
+    return art
+
+
+def cpu_info():
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"cpu_model": model, "host_threads": os.cpu_count(), "compiler_flags": "-O2 (reference Release default, "
+            "proj/CMakeLists.txt:7-9), unmodified reference sources built in place by oracle/Makefile"}
 
 
 class ClockSampler:
@@ -135,8 +173,10 @@ class ClockSampler:
 def cpu_reference(layers, tokens_per_step: int, threads: int, sample_div: int, steps: int, warmup: int, bits: int = 2):
     """Time the reference latq::infer (oracle/_ref) on the host: each step runs
     `threads` vectors concurrently (one std::thread each, the reference's own
-    re-entrant infer) through row-sampled copies of the layer set (first
-    m/sample_div rows).  Returns tokens/s scaled to full layers."""
+    re-entrant infer) through the layer set (sample_div > 1: the first
+    m/sample_div rows, scaled; the decode loop is linear in m).  Returns tokens/s.
+    The CPU reads uniform-random codes of the same shapes (its decode cost is
+    independent of the code values)."""
     from oracle.refpy import Ref
     ref = Ref()
     arts = []
@@ -157,22 +197,47 @@ def cpu_reference(layers, tokens_per_step: int, threads: int, sample_div: int, s
     return threads * tokens_per_step / (step * sample_div), step
 
 
+def cpu_latency_1core(layers, sample_div: int, bits: int = 2):
+    """Single-thread latency of one token through the layer set (the reference's
+    infer is single-threaded by construction, pipeline.cpp:151-197), on the first
+    m/sample_div rows of each layer scaled x sample_div (bounded sample)."""
+    from oracle.refpy import Ref
+    ref = Ref()
+    t = 0.0
+    for i, (m, n) in enumerate(layers):
+        art = make_artifact(max(m // sample_div, 8), n, 2000 + i, bits=bits)
+        x = np.random.default_rng(i).standard_normal((1, n))
+        ref.infer(art, x, threads=1)
+        t0 = time.perf_counter()
+        ref.infer(art, x, threads=1)
+        t += (time.perf_counter() - t0) * sample_div
+    return t
+
+
+def workload_name(args) -> str:
+    if args.workload == "4096":
+        return f"single-4096x4096-{args.bits}bit-b{args.batch}"
+    return f"llama2-{args.workload}-layer-set-{args.bits}bit-b{args.batch}"
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    layers = LAYERS_70B if args.workload == "70b" else LAYERS_7B
+    layers = WORKLOADS[args.workload]
     threads = args.cpu_threads or min(os.cpu_count() or 1, 64)
     tps, step = cpu_reference(layers, 1, threads, args.sample_div, args.steps, args.warmup, args.bits)
     line = {
         "impl": "reference", "metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / tps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"llama2-{args.workload}-layer-set-{args.bits}bit-b1", "batch": 1,
+        "config": {"workload": workload_name(args), "batch": 1,
                    "layers": [f"{m}x{n}" for m, n in layers]},
-        "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "reference",
-                         "sample": f"per step {threads} concurrent latq::infer calls (1 thread each) over the "
-                                   f"first m/{args.sample_div} rows of each layer; scaled x{args.sample_div}"},
+        "cpu_baseline": dict({"value": tps, "unit": "tokens/s", "cores": threads, "kind": "reference",
+                         "sample": f"per step {threads} concurrent latq::infer calls (1 thread each, one token "
+                                   f"each) through " + ("the full layers" if args.sample_div == 1 else
+                                   f"the first m/{args.sample_div} rows of each layer, scaled x{args.sample_div}")},
+                             **cpu_info()),
         "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -191,7 +256,7 @@ def run_ours(args):
     dev = torch.device(f"cuda:{local}")
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    layers = LAYERS_70B if args.workload == "70b" else LAYERS_7B
+    layers = WORKLOADS[args.workload]
     hbm_peak, peak_kind = peaks()
     sharded = world > 1 or args.sharded  # --sharded at N=1: the row-sharded path over a 1-rank NCCL comm
 
@@ -204,10 +269,13 @@ def run_ours(args):
             dist.broadcast(uid, 0)
         comm = q8p.NcclComm(bytes(uid.cpu().numpy()), world, rank, local)
 
-    # Two full copies of the layer set rotate so every step streams from HBM
-    # (134.6 MB per copy at 2 bits vs ~126 MB L2).
+    # `copies` full copies of the layer set (distinct device buffers) rotate so
+    # every step streams its codes from HBM: 4 x 134.6 MB (70B set, 2 bits) >= 4x L2.
     copies = []
-    arts = [make_artifact(m, n, 1000 + i, bits=args.bits) for i, (m, n) in enumerate(layers)]
+    if args.codes == "gaussian":
+        arts = [make_artifact_gaussian(m, n, 1000 + i, bits=args.bits) for i, (m, n) in enumerate(layers)]
+    else:
+        arts = [make_artifact(m, n, 1000 + i, bits=args.bits) for i, (m, n) in enumerate(layers)]
     for c in range(args.copies):
         row = []
         for (m, n), art in zip(layers, arts):
@@ -250,6 +318,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     graphs, ev_graphs = [], []
     use_graph = not args.no_graph and not sharded
+    tc_path = B <= 32  # one K2 launch per forward (larger batches run in 32-vector chunks)
     if use_graph:
         # headline graphs: no event nodes (they would break the programmatic
         # dependent launch edges between kernels); instrumented twins time K2.
@@ -400,14 +469,53 @@ def run_ours(args):
                 "note": "layers declared independent (Q8P_SET_CONCURRENT): parallel streams, same kernels, "
                         "bit-identical outputs; the headline value/e2e above run them in sequence"}
 
+    # K2 chained: each layer's decode-GEMV launched back to back over the rotating
+    # copies (q8p_bench_gemv; PDL-chained as inside a forward, so a launch's
+    # prologue overlaps its predecessor's tail as K2's overlaps K1's), CUDA events
+    # around the whole sequence on the launching stream / launches.  The stream
+    # ceiling: a plain bulk-copy read of the same code-slab bytes, same harness.
+    chained, ceiling = {}, {}
+    if not sharded and tc_path:
+        reps = 5
+        for li, (m, n) in enumerate(layers):
+            with torch.cuda.stream(stream):
+                copies[0][li].forward(xs[li], out=ys[li], stream=stream, workspace=ws)  # B images for this n
+                for c in range(args.copies):
+                    copies[c][li].bench_gemv(B, ws, 1, stream=stream)  # warm
+                torch.cuda.synchronize()
+                t0.record(stream)
+                for r in range(reps):
+                    for c in range(args.copies):
+                        copies[c][li].bench_gemv(B, ws, 1, stream=stream)
+                t1.record(stream)
+                torch.cuda.synchronize()
+                chained[li] = t0.elapsed_time(t1) / (reps * args.copies)
+                regions = [copies[c][li].code_region(0) for c in range(args.copies)]
+                for addr, nb in regions:
+                    q8p.bench_stream(addr, nb, 1, stream=stream)
+                torch.cuda.synchronize()
+                t0.record(stream)
+                for r in range(reps):
+                    for addr, nb in regions:
+                        q8p.bench_stream(addr, nb, 1, stream=stream)
+                t1.record(stream)
+                torch.cuda.synchronize()
+                ceiling[li] = (t0.elapsed_time(t1) / (reps * args.copies), regions[0][1])
+
     # Roofline of the dominant kernel (K2) on the largest layer.
     roof = None
     if not sharded and all(gemv_ms[li] for li in range(n_gemv)):
         per = []
         for li, (m, n) in enumerate(layers):
             b = m * n // 8 * sum(CODE_BYTES[c] for c, _ in SCHEMES[args.bits]) + 4 * B * n + 4 * B * m
-            t = statistics.mean(gemv_ms[li])
-            per.append({"layer": f"{m}x{n}", "bytes": b, "us": t * 1e3, "gbs": b / (t * 1e-3) / 1e9})
+            t_iso = statistics.mean(gemv_ms[li])
+            t = chained.get(li, t_iso)
+            e = {"layer": f"{m}x{n}", "bytes": b, "us": t * 1e3, "gbs": b / (t * 1e-3) / 1e9,
+                 "isolated_us": t_iso * 1e3}
+            if li in ceiling:
+                cms, cb = ceiling[li]
+                e["stream_ceiling"] = {"us": cms * 1e3, "slab_bytes": cb, "gbs": cb / (cms * 1e-3) / 1e9}
+            per.append(e)
         # dominant kernel: K2 on the largest layer(s) (both 70B MLP shapes move the same bytes)
         bmax = max(p["bytes"] for p in per)
         dom = [p for p in per if p["bytes"] == bmax]
@@ -425,7 +533,10 @@ def run_ours(args):
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                 "peak_kind": peak_kind, "traffic": traffic,
                 "kernel": f"q8p gemv (K2) on {dom[0]['layer']}: algorithmic bytes (m*n/8)*2 + 4n + 4m per launch "
-                          f"/ mean CUDA-event duration",
+                          f"/ mean launch duration from CUDA events around {args.copies}x5 back-to-back launches "
+                          f"(PDL-chained, rotating copies); isolated_us = events recorded right around one "
+                          f"launch inside the forward (includes its launch latency)",
+                "stream_ceiling": dom[0].get("stream_ceiling"),
                 "per_layer": per, "gemv_share_of_step": (tot_t * 1e3) / ms}
 
     cpu = None
@@ -433,10 +544,15 @@ def run_ours(args):
         try:
             threads = args.cpu_threads or min(os.cpu_count() or 1, 64)
             tps, step_s = cpu_reference(layers, 1, threads, args.cpu_sample_div, 2, 0, args.bits)
-            cpu = {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "reference",
-                   "sample": f"{threads} concurrent latq::infer calls (1 thread each, one token each) through "
-                             f"the first m/{args.cpu_sample_div} rows of each layer, scaled x{args.cpu_sample_div}; "
-                             f"median of 2 steps, {step_s:.1f} s per step"}
+            lat = cpu_latency_1core(layers, 8, args.bits)
+            cpu = dict({"value": tps, "unit": "tokens/s", "cores": threads, "kind": "reference",
+                        "sample": f"{threads} concurrent latq::infer calls (1 thread each, one token each) through "
+                                  + ("the full layers" if args.cpu_sample_div == 1 else
+                                     f"the first m/{args.cpu_sample_div} rows of each layer, scaled x{args.cpu_sample_div}")
+                                  + f"; median of 2 steps, {step_s:.1f} s per step",
+                        "latency_1core_s": lat,
+                        "latency_1core_sample": "one token, one thread, first m/8 rows of each layer scaled x8"},
+                       **cpu_info())
         except Exception as e:  # reference .so missing etc.
             cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
@@ -445,11 +561,15 @@ def run_ours(args):
             "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "s8xs8->s32 (K2 tensor cores) + fp32 (RHT, I/O)", "data": "synthetic",
-            "config": {"workload": f"llama2-{args.workload}-layer-set-{args.bits}bit-b{B}", "batch": B,
+            "config": {"workload": workload_name(args), "batch": B,
                        "layers": [f"{m}x{n}" for m, n in layers],
                        "parallelism": f"row-shard tp{world}" if world > 1 else "single-gpu",
-                       "l2": f"{args.copies} rotating copies of the layer set (> L2 per step pair)",
-                       "codes": f"uniform-random codes, default_scheme({args.bits}) stages (perf variant, test_pipeline.cpp:256-273)",
+                       "l2": f"{args.copies} rotating copies of the layer set (distinct buffers, "
+                             f"{args.copies * sum(m * n // 4 for m, n in layers) / 1e6:.0f} MB of codes vs 126 MB L2)",
+                       "codes": (f"synthetic Gaussian W quantized by the reference H = I route on the GPU "
+                                 f"(q8p.produce_artifact), default_scheme({args.bits})" if args.codes == "gaussian" else
+                                 f"uniform-random codes, default_scheme({args.bits}) stages (perf variant, "
+                                 f"test_pipeline.cpp:256-273)"),
                        "cuda_graph": use_graph},
             "e2e": {"value": B * 1e3 / e2e_ms, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": int(launches),
@@ -471,8 +591,10 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="70b", choices=["70b", "7b"])
-    ap.add_argument("--copies", type=int, default=2)
+    ap.add_argument("--workload", default="70b", choices=["70b", "7b", "4096"])
+    ap.add_argument("--copies", type=int, default=4)
+    ap.add_argument("--codes", default="gaussian", choices=["gaussian", "random"],
+                    help="gaussian: reference-route quantized N(0,1) weights (GPU producer); random: uniform codes")
     ap.add_argument("--batch", type=int, default=1, help="vectors per layer call (BASELINE configs[1]: 1..16)")
     ap.add_argument("--bits", type=int, default=2, choices=[2, 3, 4],
                     help="2: E8P (headline); 3 / 4: RVQ variants (BASELINE configs[3])")
@@ -480,7 +602,7 @@ def main():
     ap.add_argument("--sharded", action="store_true", help="use q8p_forward_sharded even at N=1 (1-rank NCCL)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
-    ap.add_argument("--sample-div", type=int, default=8, help="row sampling of --impl reference steps")
+    ap.add_argument("--sample-div", type=int, default=1, help="row sampling of --impl reference steps (1: full rows)")
     ap.add_argument("--cpu-sample-div", type=int, default=1, help="row sampling of our line's cpu_baseline")
     args = ap.parse_args()
     if args.impl == "reference":

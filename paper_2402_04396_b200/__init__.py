@@ -584,14 +584,16 @@ RVQ_SCHEMES = {2: (["e8p-2bit"], [0.9]), 3: (["e8p-2bit", "e8-1bit"], [0.98, 2.0
                4: (["e8p-2bit", "e8p-2bit"], [1.03, 3.45])}
 
 
-def produce_artifact(w, signs_u, signs_v, bits: int) -> bytes:
+def produce_artifact(w, signs_u, signs_v, bits: int, exact_r1: bool = True) -> bytes:
     """GPU producer: the reference's H = I quantize_layer route
     (pipeline.cpp:47-107 with ldlq.cpp's nearest rounding) on a float64 CUDA weight
     matrix w [m, n] and host sign-byte arrays -> QSHP v1 bytes, byte-identical to the
     reference artifact for the same W and signs (tests/test_gpu_encode.py):
     W~ = T_u W T_v^T in f64 (q8p_rht_cols_f64), r1 = ||W~|| / sqrt(mn) (column-major,
     left-to-right sum as the reference), f32-frozen stage scales r1 / rho_i, RVQ codes
-    (q8p_rvq_quantize).  w is consumed (transformed in place)."""
+    (q8p_rvq_quantize).  w is consumed (transformed in place).  exact_r1=False sums
+    ||W~||^2 on the device instead (last-ulp differences in r1; for synthetic
+    benchmark weights only)."""
     import struct
 
     import numpy as np
@@ -605,8 +607,11 @@ def produce_artifact(w, signs_u, signs_v, bits: int) -> bytes:
     wt = w.t().contiguous()
     rht_cols_f64(wt, sv)                         # transform_rows(right)
     wt = wt.t().contiguous()
-    sq = (wt.t().contiguous().view(-1) ** 2).cpu().numpy()
-    r1 = np.sqrt(np.cumsum(sq)[-1]) / np.sqrt(float(m) * n)
+    if exact_r1:
+        sq = (wt.t().contiguous().view(-1) ** 2).cpu().numpy()
+        r1 = np.sqrt(np.cumsum(sq)[-1]) / np.sqrt(float(m) * n)
+    else:
+        r1 = float(torch.sqrt((wt * wt).sum())) / np.sqrt(float(m) * n)
     ids, rho = RVQ_SCHEMES[bits]
     s32 = [np.float32(r1 / r) for r in rho]
     cbs = [CB_E8P_2BIT if i == "e8p-2bit" else CB_E8_1BIT for i in ids]
