@@ -216,16 +216,11 @@ constexpr std::uint32_t kCtHi = 0x00FBFDFFu;  // {-1,-3,-5,0}
 template <int JJ>
 __device__ __forceinline__ std::uint32_t e8p_nib(std::uint32_t idxreg, std::uint32_t lb) {
   // volatile: issued before the A-buffer wait so the LDS latency overlaps it
-  std::uint32_t r, addr;
-  if constexpr (JJ == 3) {
-    // top byte: two FMA-pipe ops (mul.hi by 256, mad) instead of one ALU PRMT --
-    // the decode is ALU-bound, the FMA pipe has room
-    asm("{\n\t.reg .u32 t;\n\tmul.hi.u32 t, %1, 256;\n\tmad.lo.u32 %0, t, 256, %2;\n\t}\n"
-        : "=r"(addr)
-        : "r"(idxreg), "r"(lb));
-  } else {
-    addr = prmt(idxreg, lb, 0x7604u | (std::uint32_t(JJ) << 4));
-  }
+  // (measured, tools/ubench_alu.cu: PRMT / LOP3 / SHF issue to the ALU pipe at 16
+  // lanes/clk, IMAD at 16, IMAD.HI = mul.hi at only 8 -- a PRMT is the cheapest
+  // address for every slot)
+  std::uint32_t r;
+  const std::uint32_t addr = prmt(idxreg, lb, 0x7604u | (std::uint32_t(JJ) << 4));
   asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(r) : "r"(addr));
   return r;
 }
@@ -243,7 +238,8 @@ __device__ __forceinline__ void e8p_fin(std::uint32_t nib, std::uint32_t fl, std
     rs = __umulhi(fl, 0x80000000u);  // fl >> 1 on the FMA pipe
   const std::uint32_t sel = nib ^ (rs & 0x44444444u);
   lo = prmt(ct_lo, ct_hi, sel);
-  hi = prmt(ct_lo, ct_hi, __umulhi(sel, 65536u));  // sel >> 16
+  // sel >> 16: SHF (ALU pipe) for even slots, mul.hi (FMA pipe) for odd ones
+  hi = prmt(ct_lo, ct_hi, (JJ & 1) ? __umulhi(sel, 65536u) : sel >> 16);
 }
 
 // One slab row (thread = row `row_in` of a 128-row slab at smem address `sa`):
