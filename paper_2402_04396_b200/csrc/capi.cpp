@@ -202,8 +202,6 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
       L->lut_img = static_cast<const std::uint8_t*>(upload(L.get(), img.data(), img.size()));
       const std::vector<std::uint32_t> tw = mma_table_words();
       L->mma_tables = static_cast<const std::uint32_t*>(upload(L.get(), tw.data(), tw.size() * 4));
-      const unsigned zero2[2] = {0u, 0u};
-      L->gbar = static_cast<unsigned*>(upload(L.get(), zero2, sizeof(zero2)));
     }
     const std::size_t nb = d.n / 8, words = std::size_t(r1 - r0) * nb;
     const std::uint8_t* odd_dev = nullptr;  // E8P odd-parity table for the device transcode
@@ -319,21 +317,18 @@ struct Workspace {
 };
 std::uint32_t rows_pad_of(const q8p_layer* L) { return tc_row_blocks(L->m_local()) * 128; }
 // Batches above the tensor-core path's 32 vectors run as 32-vector chunks through
-// it (weights streamed once per chunk) instead of the portable fp32 GEMV;
-// Q8P_PORTABLE_BIG_BATCH=1 restores the portable path (experiment knob).
+// it (weights streamed once per chunk).
 int tc_chunk(const q8p_layer* L, int batch) {
-  static const bool portable = std::getenv("Q8P_PORTABLE_BIG_BATCH") != nullptr;
   if (tc_supported(*L, batch)) return batch;
-  if (!portable && batch > kTcMaxBatch && tc_supported(*L, kTcMaxBatch)) return kTcMaxBatch;
+  if (batch > kTcMaxBatch && tc_supported(*L, kTcMaxBatch)) return kTcMaxBatch;
   return 0;  // portable path
 }
 
 // Batches of several whole chunks run K1 once for all vectors (B images per chunk),
 // then K2 + K3 per chunk with K3 clearing the accumulators it read (multi-chunk K1).
 bool multi_chunk_k1(const q8p_layer* L, int batch) {
-  static const bool off = std::getenv("Q8P_NO_MULTI_K1") != nullptr;  // experiment knob
   const int chunk = tc_chunk(L, batch);
-  return !off && chunk > 0 && batch > chunk && batch % chunk == 0 && L->side_v.kind == 0 && L->side_u.kind == 0 &&
+  return chunk > 0 && batch > chunk && batch % chunk == 0 && L->side_v.kind == 0 && L->side_u.kind == 0 &&
          (L->n / 8) % 32 == 0;
 }
 
@@ -468,12 +463,6 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
   DeviceGuard g(L->device);
   Workspace w;
   workspace_parts(L, batch, &w, ws);
-  if (tc_fused_supported(*L, batch)) {  // one persistent launch: K1 + K2 + K3
-    if (opts) record_event(opts->gemv_start_event, s);
-    launch_layer_fused(*L, x, y, w.u, w.ssq, w.alpha, w.tl, w.bimg, w.zacc, w.rows_pad, batch, s);
-    if (opts) record_event(opts->gemv_end_event, s);
-    return;
-  }
   if (const int chunk = tc_chunk(L, batch)) {
     float zscale[2] = {L->scale[0], L->scale[1]};
     int ze8p[2] = {L->cb[0] == Q8P_CB_E8P_2BIT, L->cb[1] == Q8P_CB_E8P_2BIT};
@@ -749,19 +738,6 @@ void* mapped_ptr(const void* p) {
   return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
 }
 
-// Zero-copy step (Q8P_SET_ZERO_COPY=1): K1 reads every x straight from pinned
-// host memory over PCIe and K3 writes every y straight into it (the same bytes
-// cross the link as with copies, without copy-engine round trips).
-void forward_set_mapped_enqueue(const q8p_layer* const* layers, int count, const float* dxh, float* dyh, int batch,
-                                void* ws, std::size_t ws_bytes, cudaStream_t s) {
-  std::size_t xo = 0, yo = 0;
-  for (int i = 0; i < count; ++i) {
-    forward_impl(layers[i], dxh + xo, dyh + yo, batch, ws, ws_bytes, s);
-    xo += std::size_t(batch) * layers[i]->n;
-    yo += std::size_t(batch) * layers[i]->m;
-  }
-}
-
 void forward_set_host_impl(const q8p_layer* const* layers, int count, const float* xh, float* yh, int batch, void* ws,
                            std::size_t ws_bytes, cudaStream_t s, unsigned flags) {
   check_set(layers, count, batch);
@@ -770,25 +746,16 @@ void forward_set_host_impl(const q8p_layer* const* layers, int count, const floa
   if (!ws || ws_bytes < set_workspace_size(layers, count, batch, flags)) throw SizeError("workspace too small");
   const int dev = layers[0]->device;
   DeviceGuard g(dev);
-  static const bool no_graph = std::getenv("Q8P_NO_SET_GRAPH") != nullptr;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cuda_check(cudaStreamIsCapturing(s, &cap), "capture status");
   const auto* dxh = static_cast<const float*>(mapped_ptr(xh));
   auto* dyh = static_cast<float*>(mapped_ptr(yh));
-  // experiment knob: zero-copy (kernels read x / write y in pinned host memory over
-  // PCIe) measured no faster than the overlapped copies (109-111 us per 70B step)
-  static const bool zero_copy = std::getenv("Q8P_SET_ZERO_COPY") != nullptr;
-  static const bool no_ends = std::getenv("Q8P_SET_COPY_ENDS") != nullptr;  // experiment knob
-  const bool mapped = dxh && dyh && zero_copy;
-  const bool ends = dxh && dyh && !no_ends && !(flags & Q8P_SET_CONCURRENT);
+  const bool ends = dxh && dyh && !(flags & Q8P_SET_CONCURRENT);
   auto enqueue = [&](cudaStream_t st) {
-    if (mapped)
-      forward_set_mapped_enqueue(layers, count, dxh, dyh, batch, ws, ws_bytes, st);
-    else
-      forward_set_host_enqueue(layers, count, xh, yh, batch, ws, ws_bytes, st, flags, ends ? dxh : nullptr,
-                               ends ? dyh : nullptr);
+    forward_set_host_enqueue(layers, count, xh, yh, batch, ws, ws_bytes, st, flags, ends ? dxh : nullptr,
+                             ends ? dyh : nullptr);
   };
-  if (no_graph || cap != cudaStreamCaptureStatusNone || !dxh || !dyh || dev < 0 || dev >= 64) {
+  if (cap != cudaStreamCaptureStatusNone || !dxh || !dyh || dev < 0 || dev >= 64) {
     enqueue(s);
     cuda_check(cudaStreamSynchronize(s), "set sync");
     return;

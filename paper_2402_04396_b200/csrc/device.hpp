@@ -92,7 +92,6 @@ struct q8p_layer {
   void* mma[2] = {nullptr, nullptr};       // warp-MMA records (gemv_mma.cu), per stage
   const std::uint32_t* mma_tables = nullptr;  // device [256] E8P nibble words + [256][2] e8-1bit rows
   const std::uint8_t* lut_img = nullptr;   // device 64 KiB lane-replicated decode LUT (gemv_tc.cu)
-  unsigned* gbar = nullptr;                // device [2] grid-barrier counters of the fused layer kernel
   std::size_t device_bytes = 0;
   std::size_t code_bytes = 0;
   std::vector<void*> allocations;
@@ -145,7 +144,6 @@ std::uint32_t tc_slab_bytes(int kind);
 std::uint32_t tc_row_blocks(std::uint32_t m_local);
 std::uint32_t tc_k_slabs(std::uint32_t n);
 std::size_t tc_code_bytes(std::uint32_t m_local, std::uint32_t n, int kind);
-void tc_transcode(const std::uint16_t* codes, std::uint32_t m_local, std::uint32_t n, int kind, std::uint8_t* out);
 // tc_transcode on the device from the uploaded plain codes (u16 E8P / u8 e8-1bit).
 void tc_transcode_device(const void* codes, std::uint32_t m_local, std::uint32_t n, int kind, std::uint8_t* out,
                          const std::uint8_t* odd_parity_dev, cudaStream_t s);
@@ -182,11 +180,6 @@ void launch_rht_in_limbs(const DevSide& side, const float* x, float* u_scratch, 
                          std::uint8_t* bimg_tail, std::size_t tail_bytes, std::int32_t* zero_ptr,
                          std::size_t zero_words, int batch, cudaStream_t s, std::uint32_t chunk_vec = 0,
                          std::size_t chunk_bytes = 0);
-// Fused layer kernel (gemv_tc.cu): K1 + K2 (+ K3 when y != nullptr) in one persistent launch.
-bool tc_fused_supported(const q8p_layer& L, int batch);
-void launch_layer_fused(const q8p_layer& L, const float* x, float* y, float* u_scratch, float* ssq, float* alpha,
-                        long long* tl, std::uint8_t* bimg, std::int32_t* zacc, std::uint32_t rows_pad, int batch,
-                        cudaStream_t s);
 // Row-sharded forward: this rank's fp32 z rows [batch][m_local] from the limb accumulators.
 void launch_combine_acc(const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows, std::uint32_t zacc_cols,
                         const float zscale[2], const int ze8p[2], const float* alpha, const long long* tl, float* z,

@@ -51,14 +51,11 @@
 // 64-KiB-aligned window) + shift + LOP3 (sign flags) + 2 PRMT from the constant
 // byte table {1,3,5,_,-1,-3,-5,_}.
 //
-// Build-time switches (NVEXTRA=-D... to paper_2402_04396_b200/csrc/Makefile), all
-// measured and documented in DESIGN.md sections 6-7; defaults are the fastest:
-//   Q8P_K2_SMEM_KB (200)  Q8P_K2_TEAMS (1)  Q8P_K2_CPASYNC (0)  Q8P_K2_DECODE_AHEAD (1)
-//   Q8P_K2_N8_G2NB3 (0)   Q8P_K2_TRACE (off: per-item clock64 timeline of CTA 0)
-//   experiments that compile parts of the loop out (wrong results, timing only):
-//   Q8P_EXP_NO_DECODE / _NO_STTM / _NO_MMA / _LDS_ONLY / _ONE_MMA / _POLL_AEMPTY,
-//   Q8P_STAGGER_NS.  Run-time knobs: Q8P_FUSE (fused layer kernel),
-//   Q8P_K2_LATE_PREFETCH, Q8P_TRACE (timeline file prefix).
+// Debug builds: NVEXTRA=-DQ8P_K2_TRACE (per-item clock64 / per-CTA globaltimer
+// timeline, written when Q8P_TRACE names a file prefix; tools/tc_timeline.py).
+// The variants measured slower in round 1 (cp.async producer, fused K1+K2+K3
+// kernel, 2 x 3 A buffers, 2 decoder teams, staggered groups) live
+// in git history, not in the product.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -85,35 +82,10 @@ constexpr std::uint32_t kE81Slab = 2 * 2048;
 constexpr std::uint32_t kAcols = 72;        // TMEM columns per A buffer (64 main + 8 side)
 constexpr int kWarpProd = 0, kWarpMma = 1;  // warps 1..G: one MMA issuer per decode group; then 4G decoder warps
 constexpr int kMaxStages = 32;
-#ifndef Q8P_K2_CPASYNC
-#define Q8P_K2_CPASYNC 0  // 1: code ring filled by 2 producer warps with 16-B cp.async (LDGSTS)
-                          // instead of 1-D bulk copies from one warp.  Faster in the streaming
-                          // ubench (5.9 vs 5.2 TB/s) but slower in K2 (25.3 vs 21.3 us, the
-                          // LDGSTS compete with the decoders' shared-memory pipe).
-#endif
-#ifndef Q8P_K2_N8_G2NB3
-#define Q8P_K2_N8_G2NB3 0  // batch <= 2: 2 groups x 3 A buffers instead of 3 groups x 2
-#endif
-#ifndef Q8P_K2_DECODE_AHEAD
-#define Q8P_K2_DECODE_AHEAD 1  // decode a whole slab into registers before waiting for the A buffer
-#endif
-#ifdef Q8P_EXP_POLL_AEMPTY
-#define A_EMPTY_WAIT mbar_wait_poll
-#else
 #define A_EMPTY_WAIT mbar_wait
-#endif
-#ifndef Q8P_K2_KBG8
-#define Q8P_K2_KBG8 3  // B-image ring slots per group at N = 8 (4: neutral; G x slots <= kMaxB)
-#endif
-#ifndef Q8P_K2_TEAMS
-#define Q8P_K2_TEAMS 1  // decoder teams per group at batch <= 2 (2: +3% K2, but the register
-                         // file then leaves no room to co-reside with K1 under PDL)
-#endif
+constexpr std::uint32_t kBg8 = 3;           // B-image ring slots per group at N = 8
 constexpr std::uint32_t kCtl = 1024;        // control block (barriers) at the smem base
-#ifndef Q8P_K2_SMEM_KB
-#define Q8P_K2_SMEM_KB 200  // < 227: lets K2's prologue co-reside with K1 under PDL
-#endif
-constexpr std::size_t kSmemBytes = Q8P_K2_SMEM_KB * 1024;
+constexpr std::size_t kSmemBytes = 200 * 1024;  // < 227 KB: K2's prologue co-resides with K1 under PDL
 
 // G decode groups (one TMEM accumulator + one MMA issuer each), T teams of 4
 // decoder warps per group: team t decodes the group's items that use A buffer
@@ -121,12 +93,11 @@ constexpr std::size_t kSmemBytes = Q8P_K2_SMEM_KB * 1024;
 template <int G, int T = 1>
 struct Roles {
   static constexpr int kWarpDec = 1 + G;
-  static constexpr int kWarpProd2 = kWarpDec + 4 * G * T;  // second code producer (cp.async mode)
-  static constexpr int kThreads = (kWarpDec + 4 * G * T + (Q8P_K2_CPASYNC ? 1 : 0)) * 32;
+  static constexpr int kThreads = (kWarpDec + 4 * G * T) * 32;
   template <int N>
   // B-image ring slots per group.  >= 2: the issuer refills the slot of item
   // k - 1 with item k - 1 + kBg after issuing item k, so one slot would deadlock.
-  static constexpr std::uint32_t kBg = N <= 8 ? Q8P_K2_KBG8 : N >= 128 ? 3 : 2;
+  static constexpr std::uint32_t kBg = N <= 8 ? kBg8 : N >= 128 ? 3 : 2;
 };
 
 struct TcArgs {
@@ -144,18 +115,6 @@ struct TcArgs {
   std::uint32_t smem_bytes;
   const std::uint8_t* lut_img;    // 64 KiB LUT window image (tc_lut_image)
   unsigned long long* trace;      // debug timeline (Q8P_TRACE), CTA 0 only; nullptr = off
-  // ---- fused layer kernel (K1 + K2 [+ K3] in one launch) ----
-  int late_prefetch;              // producer waits for the previous kernel before streaming codes
-  int fuse;                       // 0: K2 only, 1: K1 + K2, 2: K1 + K2 + K3
-  int batch;
-  RhtArgs k1, k3;                 // pass arguments of the input / output transforms
-  std::uint32_t k1_p1, k1_p2, k3_p1, k3_p2;  // virtual blocks (x batch) of each pass
-  unsigned* gbar;                 // [2] grid-barrier counters of this layer (zero at rest)
-  std::uint32_t scratch_bytes;    // RHT scratch at the top of the dynamic smem
-  std::int32_t* zero_ptr;         // accumulators to zero (K1 duty)
-  std::size_t zero_words;
-  std::uint8_t* zero2_ptr;        // B-image tail to zero (ragged n)
-  std::size_t zero2_bytes;
 };
 
 // Debug timeline: trace[role][item][4] clock64 stamps (roles 0..7 decoder
@@ -266,13 +225,6 @@ __device__ __forceinline__ void decode_row_e8p(const SlabRowE8p& r, std::uint32_
 #pragma unroll
   for (int g4 = 0; g4 < 8; ++g4) {
     const int ob = 16 * (g4 >> 1) + 8 * (g4 & 1);
-#ifdef Q8P_EXP_LDS_ONLY  // experiment: keep the LUT loads, drop the ALU decode
-    o[ob + 0] = e8p_nib<0>(r.idx[g4], lb); o[ob + 1] = r.fl[g4];
-    o[ob + 2] = e8p_nib<1>(r.idx[g4], lb); o[ob + 3] = r.fl[g4];
-    o[ob + 4] = e8p_nib<2>(r.idx[g4], lb); o[ob + 5] = r.fl[g4];
-    o[ob + 6] = e8p_nib<3>(r.idx[g4], lb); o[ob + 7] = r.fl[g4];
-    continue;
-#endif
     e8p_fin<0>(e8p_nib<0>(r.idx[g4], lb), r.fl[g4], ct_lo, ct_hi, o[ob + 0], o[ob + 1]);
     e8p_fin<1>(e8p_nib<1>(r.idx[g4], lb), r.fl[g4], ct_lo, ct_hi, o[ob + 2], o[ob + 3]);
     e8p_fin<2>(e8p_nib<2>(r.idx[g4], lb), r.fl[g4], ct_lo, ct_hi, o[ob + 4], o[ob + 5]);
@@ -299,13 +251,13 @@ __device__ __forceinline__ void decode_row_e81(std::uint32_t sa, std::uint32_t r
   }
 }
 
-template <int N, int G, int T, bool FUSED, int NB>
+template <int N, int G, int T, int NB>
 __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArgs a) {
   extern __shared__ __align__(1024) std::uint8_t smem[];
   // warp index via shfl: the compiler then knows every role branch is warp-uniform
   const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const std::uint32_t sbase = smem_u32(smem);
-  const std::uint32_t send = sbase + a.smem_bytes - a.scratch_bytes;  // RHT scratch above the ring
+  const std::uint32_t send = sbase + a.smem_bytes;
   // B ring: [group][slot], b_slot bytes per k-slab image
   const std::uint32_t b_slot = (a.b_bytes + 127) & ~127u;
   constexpr std::uint32_t SBg = Roles<G>::template kBg<N>, SB = SBg * G;
@@ -354,7 +306,7 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
 #endif
   if (threadIdx.x == 0) {
     for (std::uint32_t i = 0; i < S; ++i) {
-      mbar_init(bar_full_c + 8 * i, Q8P_K2_CPASYNC ? 32 : 1);  // cp.async: one warp's noinc arrivals
+      mbar_init(bar_full_c + 8 * i, 1);
       mbar_init(bar_empty_c + 8 * i, 4);
     }
     for (std::uint32_t i = 0; i < SB; ++i) {
@@ -371,40 +323,25 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
     fence_mbar_init();
     asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n" ::"r"(ct_slot), "r"(kCtLo), "r"(kCtHi) : "memory");
   }
-  // Code producers.  Item i goes to ring slot i % S (phase i / S).  Bulk mode: warp 0
-  // issues every slab as one 1-D cp.async.bulk; cp.async mode: warps 0 and
-  // kWarpProd2 take alternate items, each lane moving 16 B per LDGSTS, completion
-  // via cp.async.mbarrier.arrive.noinc.  The first S slabs (and the LUT window)
-  // of warp 0 are issued before the TMEM allocation and the CTA barrier.
+  // Code producer.  Item i goes to ring slot i % S (phase i / S); warp 0 issues
+  // every slab as one 1-D cp.async.bulk.  The first S slabs (and the LUT window)
+  // are issued before the TMEM allocation and the CTA barrier.
   const std::uint64_t pol = policy_evict_first();
   auto issue_item = [&](std::uint32_t i) {
     const std::uint32_t it = it0 + i, u = it / nst, sidx = it - u * nst, st = i % S;
     const std::uint32_t sb = sidx ? a.slab_bytes[1] : a.slab_bytes[0];
     const std::uint8_t* src = (sidx ? a.codes[1] : a.codes[0]) + std::size_t(u) * sb;
-#if Q8P_K2_CPASYNC
-    const std::uint32_t dst = code_addr(st);
-    for (std::uint32_t o = std::uint32_t(lane) * 16u; o < sb; o += 512u)
-      // (the .L2::cache_hint form with the evict-first policy faults at run time on sm_100a)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + o), "l"(src + o) : "memory");
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar_full_c + 8 * st) : "memory");
-#else
     mbar_arrive_expect_tx_e(bar_full_c + 8 * st, sb);
     bulk_g2s_hint_e(code_addr(st), src, sb, bar_full_c + 8 * st, pol);
-#endif
   };
-  constexpr std::uint32_t NP = Q8P_K2_CPASYNC ? 2u : 1u;
   const std::uint32_t pre = count < S ? count : S;
   if (warp == kWarpProd) {
     __syncwarp();  // lane 0 initialised the barriers
-    // Q8P_K2_LATE_PREFETCH: hold the code stream until the previous kernel (K1)
-    // is done, so K1's few dependent accesses do not queue behind ~20 MB of
-    // prefetch (the prologue still overlaps K1)
-    if (a.late_prefetch) pdl_wait();
     if (count > 0) {
       issue_item(0);  // first code slab, then the (L2-resident) LUT window
       mbar_arrive_expect_tx_e(bar_lut, 65536);
       bulk_g2s_e(lutw, a.lut_img, 65536, bar_lut);
-      for (std::uint32_t i = NP; i < pre; i += NP) issue_item(i);
+      for (std::uint32_t i = 1; i < pre; ++i) issue_item(i);
     }
     tmem_alloc<512>(tmem_slot);
   }
@@ -417,74 +354,15 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
   if (threadIdx.x == 0) gstamp(1);
 #endif
 
-  // ---- fused layer: K1 on the issue + decode warps while warp 0 streams codes ----
-  __shared__ float s_red[32];
-  __shared__ long long s_redl[32];
-  __shared__ float s_alpha[2];
-  // team: MMA issuers + decoders (not the code producers)
-  const Team tm{threadIdx.x - 32u, std::uint32_t(Roles<G, T>::kWarpProd2 - 1) * 32u, 1u};
-  const bool in_team = warp != kWarpProd && warp < Roles<G, T>::kWarpProd2;
-  auto tm_tid0 = [&]() { return threadIdx.x == 32; };
-  (void)tm_tid0;
-#ifdef Q8P_K2_TRACE
-  auto pstamp = [&](int k) {  // fused-phase timeline, per CTA (globaltimer ns), team thread 0
-    if (a.trace != nullptr && blockIdx.x < 148 && tm_tid0()) {
-      std::uint64_t t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      a.trace[12 * kTraceItems * 4 + blockIdx.x * 12 + k] = t;
-    }
-  };
-#else
-  auto pstamp = [](int) {};
-#endif
-  float* const scr = reinterpret_cast<float*>(smem + (a.smem_bytes - a.scratch_bytes));
-  if constexpr (FUSED) {
-    if (in_team) {
-      pstamp(0);
-      pdl_wait();  // x (and our workspace) are the previous kernel's
-      pstamp(1);
-      {  // K1 duties: zero the accumulators, the ragged B-image tail and TL
-        const std::size_t t0 = std::size_t(blockIdx.x) * tm.n + tm.tid, ts = std::size_t(gridDim.x) * tm.n;
-        if (a.zero_ptr)
-          for (std::size_t i = t0; i < a.zero_words / 4; i += ts)
-            reinterpret_cast<int4*>(a.zero_ptr)[i] = make_int4(0, 0, 0, 0);
-        if (a.zero2_ptr)
-          for (std::size_t i = t0; i < a.zero2_bytes / 16; i += ts)
-            reinterpret_cast<int4*>(a.zero2_ptr)[i] = make_int4(0, 0, 0, 0);
-        if (blockIdx.x == 0 && tm.tid < std::uint32_t(a.batch)) a.k1.tl_out[tm.tid] = 0;
-      }
-      for (std::uint32_t vb = blockIdx.x; vb < a.k1_p1; vb += gridDim.x)
-        rht_p1_dispatch(a.k1, vb % a.k1.P1, int(vb / a.k1.P1), scr, s_red, tm);
-      pstamp(2);
-      grid_barrier(a.gbar, gridDim.x, tm);
-      pstamp(3);
-      const std::uint32_t g8 = a.k1.P2 * a.k1.q / 8;
-      for (std::uint32_t vb = blockIdx.x; vb < a.k1_p2; vb += gridDim.x)
-        rht_p2_limbs_body(a.k1, vb % g8, int(vb / g8), scr, s_redl, s_alpha, tm);
-      pstamp(4);
-      grid_barrier(a.gbar, 2 * gridDim.x, tm);  // B images, alpha, TL complete
-      pstamp(5);
-    }
-  }
-
   if (warp == kWarpProd) {
-    // ===== code producer 0 (codes do not depend on K1) =====
-    for (std::uint32_t i = pre + ((NP - pre % NP) % NP); i < count; i += NP) {
+    // ===== code producer (codes do not depend on K1) =====
+    for (std::uint32_t i = pre; i < count; ++i) {
       tstamp(a, 9, i, 0);
       mbar_wait(bar_empty_c + 8 * (i % S), ((i / S) & 1) ^ 1);
       tstamp(a, 9, i, 1);
       issue_item(i);
     }
     pdl_trigger();
-#if Q8P_K2_CPASYNC
-  } else if (warp == Roles<G, T>::kWarpProd2) {
-    // ===== code producer 1: odd items =====
-    for (std::uint32_t i = 1; i < count; i += 2) {
-      if (i >= S) mbar_wait(bar_empty_c + 8 * (i % S), ((i / S) & 1) ^ 1);
-      issue_item(i);
-    }
-    pdl_trigger();
-#endif
   } else if (warp < kWarpDec) {
     // ===== MMA issuer of group g (+ its B-image prefetch): items i = g, g + G, ... =====
     // One issuer per group keeps each accumulator's MMAs on one thread (in-order
@@ -530,27 +408,10 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
         mbar_wait(af0 + 8 * buf, bph);
         tstamp(a, 8 + (g == 0 ? 0 : 4 + g), k, 1);
         mbar_wait(fb + 8 * bslot, bphase);
-#ifndef Q8P_K2_TRACE_SYNC
         tstamp(a, 8 + (g == 0 ? 0 : 4 + g), k, 2);
-#endif
         tc_fence_after();
-#ifdef Q8P_EXP_NO_MMA
-        mma_commit_e(ae0 + 8 * buf);
-        mma_commit_e(eb + 8 * bslot);
-#else
-#ifdef Q8P_EXP_ONE_MMA  // experiment: one MMA per item (wrong results) to split per-MMA vs per-item cost
-        mma_i8_ts_e(dcol_g + s * N, acol0 + buf * kAcols, bd0 + bslot * bstep, idesc, (started >> s) & 1);
-        mma_commit_e(ae0 + 8 * buf);
-        mma_commit_e(eb + 8 * bslot);
-#else
         mma_i8_slab_e<2 * N>(dcol_g + s * N, acol0 + buf * kAcols, bd0 + bslot * bstep, idesc, (started >> s) & 1,
                              (s ? a.kind[1] : a.kind[0]) == 0, ae0 + 8 * buf, eb + 8 * bslot);
-#endif
-#endif
-#ifdef Q8P_K2_TRACE_SYNC
-        mbar_wait(ae0 + 8 * buf, bph);  // debug: serialise to time one item's MMAs
-        tstamp(a, 8 + (g == 0 ? 0 : 4 + g), k, 2);
-#endif
         started |= 1u << s;
         if ((j + G >= per_rb) || (i + G >= count)) {  // this group's last item of the row block
           mma_commit_e(bar_d_full + 8 * (g * T + team));
@@ -592,11 +453,6 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
     const std::uint32_t ct_lo = ct.x, ct_hi = ct.y;
     if (count > i_first) mbar_wait(bar_lut, 0);  // the producer copies the LUT only when it has work
     if (warp == kWarpDec) tstamp(a, 10, 1, 0);
-#ifdef Q8P_STAGGER_NS
-    // desynchronise the groups: identical loops started together stay in phase,
-    // decoding (ALU-bound) at the same time and waiting at the same time
-    if (grp > 0) __nanosleep(std::uint32_t(grp) * Q8P_STAGGER_NS);
-#endif
     for (std::uint32_t i = i_first; i < count; i += G * T) {
       const std::uint32_t s = j & (nst - 1);  // nst in {1, 2}
       const std::uint32_t buf = use % NB, bph = (use / NB) & 1;
@@ -694,34 +550,6 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
       }
     }
   }
-  if constexpr (FUSED) {
-    if (in_team) {
-      if (a.fuse == 2) {  // K3 on the full z once every CTA's accumulators are in
-        team_sync(tm);
-        pstamp(6);
-        grid_barrier(a.gbar, 3 * gridDim.x, tm);
-        pstamp(7);
-        for (std::uint32_t vb = blockIdx.x; vb < a.k3_p1; vb += gridDim.x)
-          rht_p1_dispatch(a.k3, vb % a.k3.P1, int(vb / a.k3.P1), scr, s_red, tm);
-        pstamp(8);
-        grid_barrier(a.gbar, 4 * gridDim.x, tm);
-        pstamp(9);
-        const std::uint32_t g4 = a.k3.P2 * a.k3.q / 4;
-        for (std::uint32_t vb = blockIdx.x; vb < a.k3_p2; vb += gridDim.x)
-          rht_p2_body(a.k3, vb % g4, int(vb / g4), scr, s_red, tm);
-        pstamp(10);
-      }
-      team_sync(tm);
-      if (tm.tid == 0) {  // last CTA out resets the barrier for the next launch
-        const unsigned old = atomicAdd(a.gbar + 1, 1u);
-        if (old == gridDim.x - 1) {
-          a.gbar[0] = 0;
-          a.gbar[1] = 0;
-          __threadfence();
-        }
-      }
-    }
-  }
   if (threadIdx.x == 0) tstamp(a, 10, 0, 2);
   tc_fence_before();
   __syncthreads();
@@ -736,16 +564,10 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
   }
 }
 
-constexpr std::size_t kSmemFused = 225 * 1024;  // fused layer kernel: nothing else to co-reside with
-constexpr std::size_t kSmemWide = 225 * 1024;   // N = 128 (prefill chunks of 32 vectors): 2 x 36 KB B slots
-template <int N, bool FUSED>
+constexpr std::size_t kSmemWide = 225 * 1024;   // N = 128 (prefill chunks of 32 vectors): 3 x 36 KB B slots
+template <int N>
 constexpr std::size_t smem_for() {
-  return FUSED ? kSmemFused : (N >= 128 ? kSmemWide : kSmemBytes);
-}
-
-template <int N, int G, int T, bool FUSED, int NB>
-void set_attr() {
-  kernel_attrs(reinterpret_cast<const void*>(gemv_tc_kernel<N, G, T, FUSED, NB>), int(smem_for<N, FUSED>()));
+  return N >= 128 ? kSmemWide : kSmemBytes;
 }
 
 int sm_count() {  // per device (layers may live on different devices of one process)
@@ -755,12 +577,11 @@ int sm_count() {  // per device (layers may live on different devices of one pro
   return v[d];
 }
 
-template <int N, int G, int T = 1, bool FUSED = false, int NB = 2>
+template <int N, int G, int T = 1, int NB = 2>
 void launch_ng(TcArgs a, cudaStream_t s) {
-  set_attr<N, G, T, FUSED, NB>();
-  a.smem_bytes = std::uint32_t(smem_for<N, FUSED>());
-  launch_pdl(gemv_tc_kernel<N, G, T, FUSED, NB>, dim3(sm_count()), dim3(Roles<G, T>::kThreads),
-             smem_for<N, FUSED>(), s, a);
+  kernel_attrs(reinterpret_cast<const void*>(gemv_tc_kernel<N, G, T, NB>), int(smem_for<N>()));
+  a.smem_bytes = std::uint32_t(smem_for<N>());
+  launch_pdl(gemv_tc_kernel<N, G, T, NB>, dim3(sm_count()), dim3(Roles<G, T>::kThreads), smem_for<N>(), s, a);
 }
 
 }  // namespace
@@ -793,43 +614,6 @@ std::uint32_t tc_k_slabs(std::uint32_t n) { return (n / 8 + kSlabCw - 1) / kSlab
 
 std::size_t tc_code_bytes(std::uint32_t m_local, std::uint32_t n, int kind) {
   return std::size_t(tc_row_blocks(m_local)) * tc_k_slabs(n) * tc_slab_bytes(kind);
-}
-
-void tc_transcode(const std::uint16_t* codes, std::uint32_t m_local, std::uint32_t n, int kind, std::uint8_t* out) {
-  const E8PTable& T = e8p_table();
-  const std::uint32_t nb = n / 8, RB = tc_row_blocks(m_local), KSL = tc_k_slabs(n);
-  const std::size_t SB = tc_slab_bytes(kind);
-  std::memset(out, 0, tc_code_bytes(m_local, n, kind));
-  for (std::uint32_t rb = 0; rb < RB; ++rb)
-    for (std::uint32_t ks = 0; ks < KSL; ++ks) {
-      std::uint8_t* slab = out + (std::size_t(rb) * KSL + ks) * SB;
-      for (std::uint32_t r = 0; r < 128; ++r) {
-        const std::uint32_t row = rb * 128 + r;
-        std::uint32_t fl[8] = {0, 0, 0, 0, 0, 0, 0, 0}, sw = 0;
-        for (std::uint32_t w = 0; w < 32; ++w) {
-          const std::uint32_t k = ks * 32 + w;
-          const std::uint16_t word = (row < m_local && k < nb) ? codes[std::size_t(row) * nb + k] : 0;
-          if (kind == 0) {
-            const unsigned idx = word >> 8, sb = (word >> 1) & 0x7Fu;
-            slab[(w / 16) * 2048 + r * 16 + (w % 16)] = std::uint8_t(idx);
-            // effective negate flags (e8p.cpp:88-98): word bit k (1..7) -> coordinate 8 - k,
-            // coordinate 0 restores the row's parity
-            unsigned neg[8];
-            neg[0] = unsigned(__builtin_popcount(sb) & 1) ^ T.odd_parity[idx];
-            for (int c = 1; c < 8; ++c) neg[c] = (word >> (8 - c)) & 1u;
-            for (int c = 0; c < 8; ++c) fl[w / 4] |= std::uint32_t(neg[c]) << (4 * c + (w & 3));
-            sw |= std::uint32_t(word & 1u) << ((w >> 2) + 8 * (w & 3));
-          } else {
-            slab[(w / 16) * 2048 + r * 16 + (w % 16)] = std::uint8_t(word);
-          }
-        }
-        if (kind == 0) {
-          std::memcpy(slab + 4096 + r * 16, fl, 16);
-          std::memcpy(slab + 6144 + r * 16, fl + 4, 16);
-          std::memcpy(slab + 8192 + r * 4, &sw, 4);
-        }
-      }
-    }
 }
 
 namespace {
@@ -921,12 +705,6 @@ void fill_tc_args(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* za
   a.ncols = 4 * batch;
   a.smem_bytes = std::uint32_t(kSmemBytes);
   a.lut_img = L.lut_img;
-  a.batch = batch;
-  static const int late = [] {
-    const char* e = std::getenv("Q8P_K2_LATE_PREFETCH");
-    return e ? std::atoi(e) : 0;
-  }();
-  a.late_prefetch = late;
 }
 }  // namespace
 
@@ -946,10 +724,7 @@ void launch_gemv_tc(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* 
   auto fits = [&](int G) { return G * (2 * int(kAcols) + a.nst * N) <= 512; };
   switch (N) {
     case 8:
-      if (Q8P_K2_N8_G2NB3)
-        launch_ng<8, 2, 1, false, 3>(a, s);
-      else
-        launch_ng<8, 3, Q8P_K2_TEAMS, false, 2>(a, s);
+      launch_ng<8, 3>(a, s);
       break;
     case 16: fits(3) ? launch_ng<16, 3>(a, s) : launch_ng<16, 2>(a, s); break;
     case 32: launch_ng<32, 2>(a, s); break;
@@ -973,101 +748,6 @@ void launch_gemv_tc(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* 
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
-
-bool tc_fused_supported(const q8p_layer& L, int batch) {
-  // experiment knob: the fused layer kernel is correct (GPU tests) but slower in the
-  // pipeline (grid barriers under a saturated memory system) -> opt-in
-  static const bool on = std::getenv("Q8P_FUSE") != nullptr;
-  if (!on || !tc_supported(L, batch) || tc_ncols_pad(4 * batch) != 8 || L.gbar == nullptr) return false;
-  if (L.side_u.kind != 0 || L.side_v.kind != 0) return false;  // rht only
-  // RHT scratch must leave a useful code ring
-  const std::size_t scr = std::max({rht_p1_smem_bytes(L.side_v), rht_p2_smem_bytes(L.side_v),
-                                    rht_p1_smem_bytes(L.side_u), rht_p2_smem_bytes(L.side_u)});
-  return scr <= 40 * 1024;
-}
-
-void launch_layer_fused(const q8p_layer& L, const float* x, float* y, float* u_scratch, float* ssq, float* alpha,
-                        long long* tl, std::uint8_t* bimg, std::int32_t* zacc, std::uint32_t rows_pad, int batch,
-                        cudaStream_t s) {
-  TcArgs a;
-  fill_tc_args(L, bimg, zacc, rows_pad, batch, a);
-  const std::uint32_t N = std::uint32_t(tc_ncols_pad(4 * batch)), KSL = tc_k_slabs(L.n), bb = 9u * N * 32u;
-  a.fuse = y != nullptr ? 2 : 1;
-  a.gbar = L.gbar;
-  a.smem_bytes = std::uint32_t(kSmemFused);
-  const std::size_t scr = std::max({rht_p1_smem_bytes(L.side_v), rht_p2_smem_bytes(L.side_v),
-                                    rht_p1_smem_bytes(L.side_u), rht_p2_smem_bytes(L.side_u)});
-  a.scratch_bytes = std::uint32_t((scr + 1023) & ~std::size_t(1023));
-  // K1: t = T_v x -> B images, alpha, TL (same arguments as launch_rht_in_limbs)
-  RhtArgs& k1 = a.k1;
-  rht_plan_split(L.side_v, k1);
-  k1.signs = L.side_v.signs;
-  k1.base = L.side_v.base;
-  k1.in = x;
-  k1.mid = u_scratch;
-  k1.ssq = ssq;
-  k1.alpha_out = alpha;
-  k1.tl_out = tl;
-  k1.bimg = bimg;
-  k1.b_bytes = bb;
-  k1.bcols = N;
-  k1.batch = batch;
-  k1.fwd = 1;
-  a.k1_p1 = k1.P1 * std::uint32_t(batch);
-  a.k1_p2 = (k1.P2 * k1.q / 8) * std::uint32_t(batch);
-  a.zero_ptr = zacc;
-  a.zero_words = std::size_t(L.num_stages) * N * rows_pad;
-  if ((L.n / 8) % 32 != 0) {
-    a.zero2_ptr = bimg + std::size_t(KSL - 1) * bb;
-    a.zero2_bytes = bb;
-  }
-  if (y != nullptr) {  // K3: y = T_u^T z from the limb accumulators (launch_rht_out_acc)
-    RhtArgs& k3 = a.k3;
-    rht_plan_split(L.side_u, k3);
-    k3.signs = L.side_u.signs;
-    k3.base = L.side_u.base;
-    k3.zacc = zacc;
-    k3.zrows = rows_pad;
-    k3.zcols = N;
-    k3.zstages = L.num_stages;
-    k3.zscale0 = L.scale[0];
-    k3.zscale1 = L.scale[1];
-    k3.ze8p0 = L.cb[0] == Q8P_CB_E8P_2BIT;
-    k3.ze8p1 = L.cb[1] == Q8P_CB_E8P_2BIT;
-    k3.alpha_in = alpha;
-    k3.tl_in = tl;
-    k3.mid = u_scratch;
-    k3.out = y;
-    k3.batch = batch;
-    k3.fwd = 0;
-    a.k3_p1 = k3.P1 * std::uint32_t(batch);
-    a.k3_p2 = (k3.P2 * k3.q / 4) * std::uint32_t(batch);
-  }
-  static const char* trace_env = std::getenv("Q8P_TRACE");  // debug: per-CTA phase timeline
-  unsigned long long* tr = nullptr;
-  if (trace_env != nullptr) {
-    cuda_check(cudaMalloc(&tr, 16 * kTraceItems * 4 * 8), "trace alloc");
-    cuda_check(cudaMemset(tr, 0, 16 * kTraceItems * 4 * 8), "trace memset");
-  }
-  a.trace = tr;
-  launch_ng<8, 3, 1, true>(a, s);
-  cuda_check(cudaGetLastError(), "fused layer launch");
-  if (tr != nullptr) {
-    std::vector<unsigned long long> h(16 * kTraceItems * 4);
-    cuda_check(cudaStreamSynchronize(s), "trace sync");
-    cuda_check(cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost), "trace copy");
-    cudaFree(tr);
-    static int seq = 0;
-    const std::string path = std::string(trace_env) + ".fused." + std::to_string(seq++) + "." + std::to_string(L.m) +
-                             "x" + std::to_string(L.n) + ".bin";
-    if (FILE* f = std::fopen(path.c_str(), "wb")) {
-      std::fwrite(h.data(), 8, h.size(), f);
-      std::fclose(f);
-    }
-  }
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-}
-
 
 // ---- parity probe: K2's own operand decode over the transcoded slabs -------------
 namespace {

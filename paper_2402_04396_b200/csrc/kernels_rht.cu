@@ -109,441 +109,13 @@ __global__ void __launch_bounds__(128) rht_pass2_limbs(RhtArgs a) {
 }
 
 
-// ---------------------------------------------------------------------------
-// Single-kernel cluster RHT (replaces pass1 + pass2 on the tensor-core path).
-// One thread-block cluster of C CTAs per vector (grid = (C, batch [+ zeroing])):
-//   CTA c loads the contiguous chunk of rows a in [c p/C, (c+1) p/C)
-//   (n/C floats: signs | limb-accumulator combine), applies the base B_q
-//   (B_q^T for K3) along each q-row, FWHT over the local a bits, then the
-//   chunks are transposed through distributed shared memory: CTA c takes
-//   columns [c W, (c+1) W) (W = n/C^2) of every source CTA, FWHT over the
-//   log2(C) cluster bits, and writes its part of the result.
-// Same H = (H_p (x) B_q) / sqrt(n) as had_apply (hadamard.cpp:170-210); the
-// butterflies are split differently from pass1/pass2, so fp32 rounding (not
-// the math) differs.  Smem per CTA is 2 n/C floats, small enough to co-reside
-// with the GEMV's CTAs under programmatic dependent launch.
-enum RhtMode { kK1Limbs = 0, kK3Acc = 1, kK3F32 = 2 };
-constexpr int kClThreads = 256;
-constexpr int kClMaxJ = 16;  // base-product outputs per thread (n/C <= 4096)
-
-__device__ __forceinline__ std::uint32_t cluster_ctarank() {
-  std::uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ float ld_dsmem_f32(const float* local_ptr, std::uint32_t cta) {
-  std::uint32_t a = static_cast<std::uint32_t>(__cvta_generic_to_shared(local_ptr)), r;
-  float v;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(cta));
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(r));
-  return v;
-}
-__device__ __forceinline__ float4 ld_dsmem_f32x4(const float* local_ptr, std::uint32_t cta) {
-  std::uint32_t a = static_cast<std::uint32_t>(__cvta_generic_to_shared(local_ptr)), r;
-  float4 v;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(cta));
-  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(r));
-  return v;
-}
-
-template <int Q, int MODE>
-__global__ void __launch_bounds__(kClThreads) rht_cluster(RhtArgs a, std::uint32_t C) {
-  extern __shared__ __align__(16) float smc[];
-  __shared__ float s_ss;
-  __shared__ long long s_tl;
-  __shared__ float red_f[kClThreads / 32];
-  __shared__ long long red_l[kClThreads / 32];
-  const int b = blockIdx.y;
-  const std::uint32_t c = cluster_ctarank();
-  pdl_wait();
-  pdl_trigger();
-  if (b >= a.batch) {  // K1: zero the GEMV accumulators / B-image tail (one cluster row)
-    if constexpr (MODE == kK1Limbs) {
-      const std::size_t nz = std::size_t(gridDim.x) * (gridDim.y - a.batch) * blockDim.x;
-      const std::size_t t0 = (std::size_t(b - a.batch) * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
-      if (a.zero_ptr)
-        for (std::size_t i = t0; i < a.zero_words / 4; i += nz)
-          reinterpret_cast<int4*>(a.zero_ptr)[i] = make_int4(0, 0, 0, 0);
-      if (a.zero2_ptr)
-        for (std::size_t i = t0; i < a.zero2_bytes / 16; i += nz)
-          reinterpret_cast<int4*>(a.zero2_ptr)[i] = make_int4(0, 0, 0, 0);
-    }
-    return;
-  }
-  const std::uint32_t n = a.n, chunk = n / C, P = a.p / C, W = chunk / C;
-  const std::uint32_t e0 = c * chunk;
-  float* x = smc;              // [P][Q] local chunk
-  float* T = smc + chunk;      // [C][W] gathered columns
-  float* Bs = smc + 2 * chunk; // base (float for Q <= 28, int8 for 172)
-  if constexpr (Q > 1) {
-    if constexpr (Q <= 28) {
-      for (std::uint32_t i = threadIdx.x; i < Q * Q; i += blockDim.x) Bs[i] = float(a.base[i]);
-    } else {
-      for (std::uint32_t i = threadIdx.x; i < Q * Q / 4; i += blockDim.x)
-        reinterpret_cast<std::uint32_t*>(Bs)[i] = reinterpret_cast<const std::uint32_t*>(a.base)[i];
-    }
-  }
-  float ss = 0.f;
-  for (std::uint32_t v = threadIdx.x; v < chunk / 4; v += blockDim.x) {
-    const std::uint32_t i = e0 + 4 * v;
-    float4 val;
-    if constexpr (MODE == kK3Acc) {
-      val = combine4(a, b, i);
-    } else {
-      val = *reinterpret_cast<const float4*>(a.in + std::size_t(b) * n + i);
-      if constexpr (MODE == kK1Limbs) {
-        ss += val.x * val.x + val.y * val.y + val.z * val.z + val.w * val.w;
-        val = sign4(val, (a.signs[i >> 3] >> (i & 4)) & 0xFu);
-      }
-    }
-    reinterpret_cast<float4*>(x)[v] = val;
-  }
-  if constexpr (MODE == kK1Limbs) {  // deterministic CTA partial of |x|^2 (fixed tree)
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    if ((threadIdx.x & 31) == 0) red_f[threadIdx.x >> 5] = ss;
-  }
-  __syncthreads();
-  if constexpr (MODE == kK1Limbs) {
-    if (threadIdx.x == 0) {
-      float t = 0.f;
-      for (int w = 0; w < kClThreads / 32; ++w) t += red_f[w];
-      s_ss = t;
-    }
-  }
-  if constexpr (Q > 1) {
-    // base along each q-row, two-phase through registers (in place)
-    float outv[kClMaxJ];
-#pragma unroll
-    for (int j = 0; j < kClMaxJ; ++j) {
-      const std::uint32_t e = threadIdx.x + j * kClThreads;
-      if (e < chunk) {
-        const std::uint32_t r = e / Q, cc = e - r * Q;
-        const float* xr = x + r * Q;
-        float acc = 0.f;
-        if constexpr (Q <= 28) {
-          if constexpr (MODE == kK1Limbs) {
-#pragma unroll 4
-            for (int k = 0; k < Q; ++k) acc += Bs[cc * Q + k] * xr[k];
-          } else {
-#pragma unroll 4
-            for (int k = 0; k < Q; ++k) acc += Bs[k * Q + cc] * xr[k];
-          }
-        } else {
-          const std::int8_t* B8 = reinterpret_cast<const std::int8_t*>(Bs);
-          if constexpr (MODE == kK1Limbs) {
-#pragma unroll 4
-            for (int k = 0; k < Q; ++k) acc += float(B8[cc * Q + k]) * xr[k];
-          } else {
-#pragma unroll 4
-            for (int k = 0; k < Q; ++k) acc += float(B8[k * Q + cc]) * xr[k];
-          }
-        }
-        outv[j] = acc;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kClMaxJ; ++j) {
-      const std::uint32_t e = threadIdx.x + j * kClThreads;
-      if (e < chunk) x[e] = outv[j];
-    }
-    __syncthreads();
-  }
-  fwht_rows<Q>(x, P, block_team());  // local a bits (ends with __syncthreads)
-  // -------- cluster transpose + FWHT over the C cluster bits --------
-  const float* res;    // this CTA's results: [C][W] with flat index s * chunk + c * W + w
-  std::uint32_t rstride;
-  if (C > 1) {
-    cluster_sync_all();  // every chunk is final and visible cluster-wide
-    for (std::uint32_t v = threadIdx.x; v < C * W / 4; v += blockDim.x) {
-      const std::uint32_t src = (4 * v) / W, w = (4 * v) - src * W;
-      reinterpret_cast<float4*>(T)[v] = ld_dsmem_f32x4(x + c * W + w, src);
-    }
-    __syncthreads();
-    for (std::uint32_t len = 1; len < C; len <<= 1) {  // radix-2 over the source-CTA index
-      for (std::uint32_t t = threadIdx.x; t < (C / 2) * W; t += blockDim.x) {
-        const std::uint32_t w = t % W, pr = t / W;
-        const std::uint32_t lo = ((pr / len) * 2 * len) + (pr % len), hi = lo + len;
-        const float u = T[lo * W + w], v2 = T[hi * W + w];
-        T[lo * W + w] = u + v2;
-        T[hi * W + w] = u - v2;
-      }
-      __syncthreads();
-    }
-    res = T;
-    rstride = W;
-  } else {
-    res = x;
-    rstride = chunk;
-  }
-  const float sc = rsqrtf(float(n));
-  if constexpr (MODE == kK1Limbs) {
-    // alpha: power of two >= |x|_2 / kLtMax from the cluster's |x|^2 partials (fixed order)
-    float ssum = 0.f;
-    if (C > 1) {
-      for (std::uint32_t r = 0; r < C; ++r) ssum += ld_dsmem_f32(&s_ss, r);
-    } else {
-      ssum = s_ss;
-    }
-    const float vv = sqrtf(ssum) * (1.0f + 1.0f / 1024.f) / float(kActMax);
-    int ex = 0;
-    if (vv > 0.f) frexpf(vv, &ex);
-    const float alpha = vv > 0.f ? ldexpf(1.f, ex) : 1.f, inv = vv > 0.f ? ldexpf(1.f, -ex) : 1.f;
-    if (c == 0 && threadIdx.x == 0) a.alpha_out[b] = alpha;
-    long long tl = 0;
-    const std::uint32_t N = a.bcols, cw_per_row = rstride / 8, ncw = (C > 1 ? C : 1) * cw_per_row;
-    for (std::uint32_t t = threadIdx.x; t < ncw; t += blockDim.x) {
-      const std::uint32_t srow = t / cw_per_row, wc = (t - srow * cw_per_row) * 8;
-      const float* v = res + srow * rstride + wc;
-      const std::uint32_t flat = C > 1 ? srow * chunk + c * W + wc : e0 + wc;
-      const std::uint32_t k = flat >> 3;  // codeword index
-      int lt[8];
-      long long S = 0;
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        float tt = rintf(v[cc] * sc * inv);
-        tt = fminf(fmaxf(tt, -float(kActMax)), float(kActMax));
-        lt[cc] = int(tt);
-        S += lt[cc];
-      }
-      tl += S;
-      const int qk = int(S);  // exact block sum
-      std::uint32_t wv[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        int l[4];
-        limbs4(lt[cc], l);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) wv[i][cc >> 2] |= (std::uint32_t(l[i]) & 0xFFu) << (8 * (cc & 3));
-      }
-      int ql[4];
-      limbs4(qk, ql);
-      const std::uint32_t ks = k >> 5, j = k & 31, kb = j >> 2;
-      std::uint8_t* slab = a.bimg + std::size_t(ks) * a.b_bytes;
-#pragma unroll
-      for (int l = 0; l < 4; ++l) {
-        const std::uint32_t row = 4 * b + l;
-        const std::uint32_t rowoff = (row >> 3) * 256 + (row & 7) * 16;
-        *reinterpret_cast<uint2*>(slab + kb * N * 32 + rowoff + ((j & 3) >> 1) * 128 + (j & 1) * 8) =
-            make_uint2(wv[l][0], wv[l][1]);
-        slab[8 * N * 32 + rowoff + (j >> 4) * 128 + (j & 15)] = std::uint8_t(ql[l]);
-      }
-    }
-    for (int o = 16; o > 0; o >>= 1) tl += __shfl_xor_sync(0xffffffffu, tl, o);
-    if ((threadIdx.x & 31) == 0) red_l[threadIdx.x >> 5] = tl;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      long long t = 0;
-      for (int w = 0; w < kClThreads / 32; ++w) t += red_l[w];
-      s_tl = t;
-    }
-    if (C > 1) {
-      cluster_sync_all();  // partial TLs visible; no CTA leaves while its smem is read
-      if (c == 0 && threadIdx.x == 0) {
-        long long t = 0;
-        for (std::uint32_t r = 0; r < C; ++r) {
-          std::uint32_t aa = static_cast<std::uint32_t>(__cvta_generic_to_shared(&s_tl)), rr;
-          long long v;
-          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rr) : "r"(aa), "r"(r));
-          asm volatile("ld.shared::cluster.s64 %0, [%1];" : "=l"(v) : "r"(rr));
-          t += v;
-        }
-        a.tl_out[b] = t;
-      }
-      cluster_sync_all();
-    } else {
-      __syncthreads();
-      if (threadIdx.x == 0) a.tl_out[b] = s_tl;
-    }
-  } else {
-    // K3: y_i = s_i (H^T z)_i / sqrt(n)
-    for (std::uint32_t t = threadIdx.x; t < (C > 1 ? C : 1) * rstride; t += blockDim.x) {
-      const std::uint32_t srow = t / rstride, w = t - srow * rstride;
-      const std::uint32_t flat = C > 1 ? srow * chunk + c * W + w : e0 + w;
-      float v = res[srow * rstride + w] * sc;
-      if ((a.signs[flat >> 3] >> (flat & 7)) & 1) v = -v;
-      a.out[std::size_t(b) * n + flat] = v;
-    }
-    if (C > 1) cluster_sync_all();  // no CTA leaves while its smem may still be read
-  }
-}
-
-// Cluster size for the single-kernel RHT: the largest C in {8, 4, 2, 1} with
-// C | p, (n / C^2) % 8 == 0 (codewords stay within one CTA's column block) and
-// n / C <= 4096 (register budget of the base product); 0 = unsupported.
-std::uint32_t cluster_size_for(const DevSide& side) {
-  // experiment knob: Q8P_RHT_MAXC=0 -> two-pass RHT, else the largest cluster size tried
-  static const int maxc = [] {
-    const char* e = std::getenv("Q8P_RHT_MAXC");
-    return e ? std::atoi(e) : 0;  // default: two-pass (measured faster in the pipeline)
-  }();
-  if (maxc <= 0) return 0;
-  for (std::uint32_t C = std::uint32_t(maxc); C >= 1; C >>= 1) {
-    if (side.p % C) continue;
-    const std::uint32_t chunk = side.n / C;
-    if (chunk > 4096 || chunk % 4) continue;
-    if (C > 1 && (chunk % C || (chunk / C) % 8)) continue;
-    if (C == 1 && chunk % 8) continue;
-    if ((side.q > 1) && chunk > kClThreads * kClMaxJ) continue;
-    return C;
-  }
-  return 0;
-}
-
-template <int Q, int MODE>
-void launch_cluster_q(const RhtArgs& a, std::uint32_t C, std::uint32_t zero_rows, cudaStream_t s) {
-  const std::size_t chunk = a.n / C;
-  const std::size_t bsz = Q == 1 ? 0 : (Q <= 28 ? Q * Q * 4 : (Q * Q + 15) / 16 * 16);
-  const std::size_t smem = 2 * chunk * 4 + bsz;
-  kernel_attrs(reinterpret_cast<const void*>(rht_cluster<Q, MODE>), 96 * 1024, true);
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(C, a.batch + zero_rows);
-  cfg.blockDim = dim3(kClThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  static const bool no_pdl = std::getenv("Q8P_RHT_CLUSTER_NOPDL") != nullptr;  // experiment knob
-  cfg.numAttrs = no_pdl ? 1 : 2;
-  cuda_check(cudaLaunchKernelEx(&cfg, rht_cluster<Q, MODE>, a, C), "rht cluster launch");
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-}
-
-template <int MODE>
-void launch_cluster(const RhtArgs& a, std::uint32_t C, std::uint32_t zero_rows, cudaStream_t s) {
-  switch (a.q) {
-    case 1: launch_cluster_q<1, MODE>(a, C, zero_rows, s); break;
-    case 4: launch_cluster_q<4, MODE>(a, C, zero_rows, s); break;
-    case 12: launch_cluster_q<12, MODE>(a, C, zero_rows, s); break;
-    case 20: launch_cluster_q<20, MODE>(a, C, zero_rows, s); break;
-    case 28: launch_cluster_q<28, MODE>(a, C, zero_rows, s); break;
-    case 172: launch_cluster_q<172, MODE>(a, C, zero_rows, s); break;
-    default: throw SizeError("rht: unsupported base order");
-  }
-}
-
-
-// ---------------------------------------------------------------------------
-// Single-CTA RHT for power-of-two n <= kSingleMaxN (q = 1): one 1024-thread CTA
-// per vector holds the whole vector in smem: load (signs | limb combine), all
-// log2(n) FWHT stages, then the limb B images (K1) or y (K3) straight from
-// smem -- one launch and one global round trip instead of two passes.
-constexpr std::uint32_t kSingleMaxN = 8192;
-enum SingleMode { kSingleK1 = 0, kSingleK3Acc = 1, kSingleK3F32 = 2 };
-
-template <int MODE>
-__global__ void __launch_bounds__(1024) rht_single(RhtArgs a) {
-  extern __shared__ __align__(16) float sx[];
-  __shared__ float red[32];
-  __shared__ long long redl[32];
-  __shared__ float s_ss;
-  const int b = blockIdx.x;
-  pdl_wait();
-  pdl_trigger();
-  if (b >= a.batch) {  // K1: zero the GEMV accumulators / ragged B-image tail
-    if constexpr (MODE == kSingleK1) {
-      const std::size_t nz = std::size_t(gridDim.x - a.batch) * blockDim.x;
-      const std::size_t t0 = std::size_t(b - a.batch) * blockDim.x + threadIdx.x;
-      if (a.zero_ptr)
-        for (std::size_t i = t0; i < a.zero_words / 4; i += nz)
-          reinterpret_cast<int4*>(a.zero_ptr)[i] = make_int4(0, 0, 0, 0);
-      if (a.zero2_ptr)
-        for (std::size_t i = t0; i < a.zero2_bytes / 16; i += nz)
-          reinterpret_cast<int4*>(a.zero2_ptr)[i] = make_int4(0, 0, 0, 0);
-    }
-    return;
-  }
-  const Team tm = block_team();
-  const std::uint32_t n = a.n;
-  float ss = 0.f;
-  for (std::uint32_t v = threadIdx.x; v < n / 4; v += blockDim.x) {
-    const std::uint32_t i = 4 * v;
-    float4 val;
-    if constexpr (MODE == kSingleK3Acc) {
-      val = combine4(a, b, i);
-    } else {
-      val = *reinterpret_cast<const float4*>(a.in + std::size_t(b) * n + i);
-      if constexpr (MODE == kSingleK1) {
-        ss += val.x * val.x + val.y * val.y + val.z * val.z + val.w * val.w;
-        val = sign4(val, (a.signs[i >> 3] >> (i & 4)) & 0xFu);
-      }
-    }
-    reinterpret_cast<float4*>(sx)[v] = val;
-  }
-  if constexpr (MODE == kSingleK1) {
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-  }
-  __syncthreads();
-  if constexpr (MODE == kSingleK1) {
-    if (threadIdx.x == 0) {
-      float t = 0.f;
-      for (std::uint32_t w = 0; w < blockDim.x / 32; ++w) t += red[w];
-      s_ss = t;
-    }
-  }
-  fwht_rows<1>(sx, n, tm);  // all log2(n) stages (ends with __syncthreads)
-  const float sc = rsqrtf(float(n));
-  if constexpr (MODE == kSingleK1) {
-    const float2 al = alpha_of(s_ss);
-    if (threadIdx.x == 0) a.alpha_out[b] = al.x;
-    long long tl = 0;
-    for (std::uint32_t k = threadIdx.x; k < n / 8; k += blockDim.x) tl += emit_limbs(a, b, k, sx + 8 * k, sc, al.y);
-    for (int o = 16; o > 0; o >>= 1) tl += __shfl_xor_sync(0xffffffffu, tl, o);
-    if ((threadIdx.x & 31) == 0) redl[threadIdx.x >> 5] = tl;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      long long t = 0;
-      for (std::uint32_t w = 0; w < blockDim.x / 32; ++w) t += redl[w];
-      a.tl_out[b] = t;
-    }
-  } else {
-    for (std::uint32_t v = threadIdx.x; v < n / 4; v += blockDim.x) {
-      const std::uint32_t i = 4 * v;
-      float4 val = reinterpret_cast<const float4*>(sx)[v];
-      val = make_float4(val.x * sc, val.y * sc, val.z * sc, val.w * sc);
-      val = sign4(val, (a.signs[i >> 3] >> (i & 4)) & 0xFu);
-      *reinterpret_cast<float4*>(a.out + std::size_t(b) * n + i) = val;
-    }
-  }
-}
-
-bool single_ok(const DevSide& side) {
-  // experiment knob (Q8P_RHT_SINGLE=1): correct, but one SM doing all log2(n)
-  // stages is issue-bound (~750 instructions per warp, ~3 us even at full issue)
-  // and slower in the pipeline than the two passes
-  static const bool on = std::getenv("Q8P_RHT_SINGLE") != nullptr;
-  return on && side.q == 1 && side.n <= kSingleMaxN && side.n % 8 == 0;
-}
-
-template <int MODE>
-void launch_single(const RhtArgs& a, std::uint32_t zero_ctas, cudaStream_t s) {
-  kernel_attrs(reinterpret_cast<const void*>(rht_single<MODE>), int(kSingleMaxN * 4));
-  launch_pdl(rht_single<MODE>, dim3(a.batch + zero_ctas), dim3(1024), std::size_t(a.n) * 4, s, a);
-  cuda_check(cudaGetLastError(), "rht single launch");
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-}
-
 void plan_split_impl(const DevSide& side, RhtArgs& a) {
   a.n = side.n;
   a.p = side.p;
   a.q = side.q;
   // pass-1 chunk P2 * q: ~1K floats (<= 512 for the order-172 base, whose
   // dense product dominates pass 1)
-  static const std::uint32_t tune = [] {  // experiment knob: pass-1 chunk target (floats)
-    const char* e = std::getenv("Q8P_RHT_CHUNK");
-    return e ? std::uint32_t(std::atoi(e)) : 0u;
-  }();
-  const std::uint32_t target = tune ? tune : 512;  // 512 measured best for the step (1024: +3 %)
+  const std::uint32_t target = 512;  // measured best for the step (1024: +3 %)
   std::uint32_t P2 = 1;
   while (P2 * 2 <= side.p && P2 * 2 * side.q <= target) P2 *= 2;
   if ((P2 * side.q) % 4 != 0) throw SizeError("rht: dimension too small for the float4 passes");
@@ -594,25 +166,6 @@ void launch_pass2_limbs(const RhtArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-void rht_plan_split(const DevSide& side, RhtArgs& a) { plan_split_impl(side, a); }
-std::size_t rht_p1_smem_bytes(const DevSide& side) {
-  RhtArgs a{};
-  plan_split_impl(side, a);
-  switch (side.q) {
-    case 1: return p1_smem_bytes<1>(a.P2);
-    case 4: return p1_smem_bytes<4>(a.P2);
-    case 12: return p1_smem_bytes<12>(a.P2);
-    case 20: return p1_smem_bytes<20>(a.P2);
-    case 28: return p1_smem_bytes<28>(a.P2);
-    case 172: return p1_smem_bytes<172>(a.P2);
-    default: throw SizeError("rht: unsupported base order");
-  }
-}
-std::size_t rht_p2_smem_bytes(const DevSide& side) {
-  RhtArgs a{};
-  plan_split_impl(side, a);
-  return std::size_t(a.P1) * 32;
-}
 
 void launch_rht_in(const DevSide& side, const float* x, float* t, float* u_scratch, float* amax, float* tsum,
                    std::int32_t* zero_ptr, std::size_t zero_words, int batch, cudaStream_t s) {
@@ -655,14 +208,6 @@ void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, flo
   a.out = y;
   a.batch = batch;
   a.fwd = 0;
-  if (single_ok(side)) {
-    launch_single<kSingleK3F32>(a, 0, s);
-    return;
-  }
-  if (const std::uint32_t C = cluster_size_for(side)) {
-    launch_cluster<kK3F32>(a, C, 0, s);
-    return;
-  }
   launch_pass1(a, 0, s);
   launch_pass2(a, s);
 }
@@ -699,14 +244,6 @@ void launch_rht_in_limbs(const DevSide& side, const float* x, float* u_scratch, 
   a.fwd = 1;
   a.chunk_vec = chunk_vec;
   a.chunk_bytes = chunk_bytes;
-  if (single_ok(side)) {
-    launch_single<kSingleK1>(a, (zero_ptr && zero_words) || (bimg_tail && tail_bytes) ? 16 : 0, s);
-    return;
-  }
-  if (const std::uint32_t C = cluster_size_for(side)) {
-    launch_cluster<kK1Limbs>(a, C, (zero_ptr && zero_words) || (bimg_tail && tail_bytes) ? 4 : 0, s);
-    return;
-  }
   launch_pass1(a, 32, s);
   launch_pass2_limbs(a, s);
 }
@@ -744,14 +281,6 @@ void launch_rht_out_acc(const DevSide& side, const std::int32_t* zacc, int zacc_
     if (side.kind == 1) throw UnsupportedError("rfft: zero-after K3");
     launch_pass1(a, 0, s);
     launch_pass2(a, s);
-    return;
-  }
-  if (single_ok(side)) {
-    launch_single<kSingleK3Acc>(a, 0, s);
-    return;
-  }
-  if (const std::uint32_t C = cluster_size_for(side)) {
-    launch_cluster<kK3Acc>(a, C, 0, s);
     return;
   }
   launch_pass1(a, 0, s);

@@ -408,40 +408,5 @@ __device__ void rht_p2_limbs_body(const RhtArgs& a, std::uint32_t cg, int b, flo
   team_sync(tm);
 }
 
-// Pass 1 with the base order dispatched at run time (fused layer kernel).
-__device__ __forceinline__ void rht_p1_dispatch(const RhtArgs& a, std::uint32_t ch, int b, float* sm, float* red,
-                                                const Team& tm) {
-  switch (a.q) {
-    case 1: rht_p1_body<1>(a, ch, b, sm, red, tm); break;
-    case 4: rht_p1_body<4>(a, ch, b, sm, red, tm); break;
-    case 12: rht_p1_body<12>(a, ch, b, sm, red, tm); break;
-    case 20: rht_p1_body<20>(a, ch, b, sm, red, tm); break;
-    case 28: rht_p1_body<28>(a, ch, b, sm, red, tm); break;
-    default: rht_p1_body<172>(a, ch, b, sm, red, tm); break;
-  }
-}
-
-// Grid-wide barrier over co-resident persistent CTAs (one team per CTA takes
-// part): monotone arrival counter, barrier k waits for k * gridDim.x arrivals.
-// Generic writes before it are made visible to both proxies (the async proxy
-// reads the B images through TMA afterwards).
-__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target, const Team& tm) {
-  asm volatile("fence.proxy.async.global;\n" ::: "memory");
-  team_sync(tm);
-  if (tm.tid == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
-    unsigned v;
-    while (true) {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ctr) : "memory");
-      if (v >= target) break;
-      __nanosleep(64);
-    }
-    __threadfence();
-  }
-  team_sync(tm);
-  asm volatile("fence.proxy.async.global;\n" ::: "memory");
-}
-
 }  // namespace
 }  // namespace q8p::detail
