@@ -20,6 +20,8 @@
  *                         codebook.hpp:31, e8p.hpp:35 over a whole stage
  *   q8p_k2_decode_stage   the same decode as the GEMV kernel performs it
  *                         (parity probe of the hot-path decoder)
+ *   q8p_dequantize        latq::dequantize_layer  pipeline.hpp:68
+ *                         (pipeline.cpp:142-149), dense W~ on the device
  *   q8p_rht               SideTransform::apply / apply_transpose
  *                         core/include/latq/transforms.hpp:30-33 (rht kind)
  *   q8p_plan_hadamard     latq::plan_hadamard  core/include/latq/hadamard.hpp:42
@@ -210,6 +212,15 @@ q8p_status q8p_infer_host(q8p_layer* layer, const double* x, double* y, int batc
 /* Unscaled incoherent-domain decode of one stage into device fp32
  * w_hat[m_local][n] (decoded values are exact quarter-integers). */
 q8p_status q8p_decode_stage(const q8p_layer* layer, int stage, float* w_hat, void* stream);
+
+/* latq::dequantize_layer (core/src/pipeline.cpp:142-149) on the device, rht layers:
+ * w_tilde[m][n] (f64, device) = T_u^T W_hat T_v with W_hat = sum_s scale_s *
+ * decode_s accumulated in f64 in stage order (decode_incoherent, :112-138) and
+ * the transforms applied column-wise then row-wise with the reference's
+ * butterfly / base-sum order (transform_cols / transform_rows, transforms.cpp:
+ * 66-94): bit-identical to the reference.  scratch: m * n doubles (device).
+ * Full (unsharded) layers only; rfft layers -> Q8P_ERR_UNSUPPORTED. */
+q8p_status q8p_dequantize(const q8p_layer* layer, double* w_tilde, double* scratch, void* stream);
 
 /* Parity probe of the GEMV's own decoder (e8p_decode, core/src/e8p.cpp:81-100;
  * TableCodebook::decode, codebook.cpp:65-72): runs the tensor-core K2's operand

@@ -150,6 +150,7 @@ _SIGNATURES = {
     "q8p_bench_gemv": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]),
     "q8p_bench_stream": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]),
     "q8p_layer_code_region": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_size_t)]),
+    "q8p_dequantize": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "q8p_k2_decode_stage": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "q8p_rht": (ctypes.c_int, [ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
     "q8p_qshp_inspect": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ArtifactInfo)]),
@@ -441,6 +442,16 @@ class Layer:
         p, n = ctypes.c_void_p(), ctypes.c_size_t()
         _check(lib().q8p_layer_code_region(self._h, stage, ctypes.byref(p), ctypes.byref(n)))
         return p.value, n.value
+
+    def dequantize(self, stream=None):
+        """latq::dequantize_layer on the device (q8p_dequantize): dense W~ [m, n] float64."""
+        torch = _torch()
+        info = self.info
+        dev = f"cuda:{info['device']}"
+        w = torch.empty(info["m"], info["n"], dtype=torch.float64, device=dev)
+        scratch = torch.empty_like(w)
+        _check(lib().q8p_dequantize(self._h, w.data_ptr(), scratch.data_ptr(), _stream_ptr(stream)))
+        return w
 
     def k2_decode_stage(self, stage: int, stream=None):
         """The GEMV kernel's own operand decode of one stage (q8p_k2_decode_stage):

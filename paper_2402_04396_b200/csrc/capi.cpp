@@ -113,9 +113,22 @@ void* dev_alloc(q8p_layer* L, std::size_t bytes) {
   return p;
 }
 
+void dev_free(q8p_layer* L, void* p, std::size_t bytes) {
+  auto it = std::find(L->allocations.begin(), L->allocations.end(), p);
+  if (it != L->allocations.end()) L->allocations.erase(it);
+  L->device_bytes -= bytes;
+  cuda_check(cudaFree(p), "cudaFree");
+}
+
+// Layer uploads run on the building thread's private non-blocking stream (no
+// legacy-stream or device-wide synchronisation: concurrent forwards and other
+// streams' captures are unaffected); build_layer synchronises it once at the end.
+// (cudaMemcpyAsync from pageable memory returns once the source is staged.)
+thread_local cudaStream_t t_build_stream = nullptr;
+
 void* upload(q8p_layer* L, const void* host, std::size_t bytes) {
   void* d = dev_alloc(L, bytes);
-  cuda_check(cudaMemcpy(d, host, bytes, cudaMemcpyHostToDevice), "upload");
+  cuda_check(cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, t_build_stream), "upload");
   return d;
 }
 
@@ -182,6 +195,13 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
   }
   require_sm100(device);
   DeviceGuard g(device);
+  struct BuildStream {  // this thread's upload / transcode stream for the duration of the build
+    BuildStream() { cuda_check(cudaStreamCreateWithFlags(&t_build_stream, cudaStreamNonBlocking), "build stream"); }
+    ~BuildStream() {
+      cudaStreamDestroy(t_build_stream);
+      t_build_stream = nullptr;
+    }
+  } build_stream;
   auto L = std::make_unique<q8p_layer>();
   L->device = device;
   L->m = d.m;
@@ -240,14 +260,27 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
           odd_dev = static_cast<const std::uint8_t*>(upload(L.get(), t.odd_parity.data(), 256));
         }
         void* slabs = dev_alloc(L.get(), tc_code_bytes(r1 - r0, d.n, kind));
-        tc_transcode_device(L->codes[s], r1 - r0, d.n, kind, static_cast<std::uint8_t*>(slabs), odd_dev, nullptr);
+        tc_transcode_device(L->codes[s], r1 - r0, d.n, kind, static_cast<std::uint8_t*>(slabs), odd_dev,
+                            t_build_stream);
         L->tc[s].codes = slabs;
         if (mma_k2_selected()) {  // warp-MMA records only when that kernel is selected (A/B)
           void* recs = dev_alloc(L.get(), mma_code_bytes(r1 - r0, d.n, kind));
-          mma_transcode_device(L->codes[s], r1 - r0, d.n, kind, static_cast<std::uint8_t*>(recs), odd_dev, nullptr);
+          mma_transcode_device(L->codes[s], r1 - r0, d.n, kind, static_cast<std::uint8_t*>(recs), odd_dev,
+                               t_build_stream);
           L->mma[s] = recs;
         }
-        cuda_check(cudaDeviceSynchronize(), "transcode");
+      }
+    }
+    cuda_check(cudaStreamSynchronize(t_build_stream), "layer upload");
+    cuda_check(cudaGetLastError(), "layer upload");
+    // The slabs carry every code bit: the plain copy stays only where the portable
+    // GEMV needs it (first stage not E8P), halving the code bytes held in HBM.
+    if (L->cb[0] == Q8P_CB_E8P_2BIT) {
+      for (int s = 0; s < d.num_stages; ++s) {
+        if (!L->codes[s]) continue;
+        const std::size_t bytes = words * (L->cb[s] == Q8P_CB_E8P_2BIT ? 2 : 1);
+        dev_free(L.get(), L->codes[s], bytes);
+        L->codes[s] = nullptr;
       }
     }
   } catch (...) {
@@ -1077,7 +1110,17 @@ q8p_status q8p_decode_stage(const q8p_layer* L, int stage, float* w_hat, void* s
     if (!L || !w_hat) throw q8p::ValidationError("null argument");
     if (stage < 0 || stage >= L->num_stages) throw q8p::ValidationError("stage out of range");
     DeviceGuard g(L->device);
-    launch_decode(*L, stage, w_hat, static_cast<cudaStream_t>(stream));
+    // K2's own decoder over the slabs (q8p_k2_decode_stage), then the points as fp32
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const std::size_t total = std::size_t(L->m_local()) * L->n;
+    void* tmp = nullptr;
+    cuda_check(cudaMallocAsync(&tmp, total + total / 8 + 16, s), "decode scratch");
+    auto* a = static_cast<std::int8_t*>(tmp);
+    auto* b = reinterpret_cast<std::uint8_t*>(a + total);
+    const int kind = L->cb[stage] == Q8P_CB_E8P_2BIT ? 0 : 1;
+    launch_k2_decode(*L, stage, a, b, s);
+    launch_points_f32(a, b, kind, total, w_hat, s);
+    cuda_check(cudaFreeAsync(tmp, s), "decode scratch free");
     return Q8P_OK;
   } catch (...) {
     return status_of_current_exception();
@@ -1122,6 +1165,36 @@ q8p_status q8p_layer_code_region(const q8p_layer* L, int stage, const void** cod
     if (stage < 0 || stage >= L->num_stages) throw q8p::ValidationError("stage out of range");
     *codes = L->tc[stage].codes;
     *bytes = tc_code_bytes(L->m_local(), L->n, L->cb[stage] == Q8P_CB_E8P_2BIT ? 0 : 1);
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_dequantize(const q8p_layer* L, double* w_tilde, double* scratch, void* stream) {
+  try {
+    if (!L || !w_tilde || !scratch) throw q8p::ValidationError("null argument");
+    if (L->row_begin != 0 || L->row_end != L->m) throw q8p::ValidationError("dequantize needs the full (unsharded) layer");
+    if (L->side_u.kind != 0 || L->side_v.kind != 0)
+      throw q8p::UnsupportedError("dequantize: rfft transforms are not on the f64 device path");
+    DeviceGuard g(L->device);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const std::size_t total = std::size_t(L->m) * L->n, codes = total / 8;
+    // decode_incoherent (pipeline.cpp:112-138): K2's decoder output per stage in the
+    // scratch (2 x (m n + m n / 8) bytes <= 8 m n), combined in f64
+    auto* base = reinterpret_cast<std::uint8_t*>(scratch);
+    std::int8_t* a[2] = {reinterpret_cast<std::int8_t*>(base), reinterpret_cast<std::int8_t*>(base + total)};
+    std::uint8_t* b[2] = {base + 2 * total, base + 2 * total + codes};
+    for (int st = 0; st < L->num_stages; ++st) launch_k2_decode(*L, st, a[st], b[st], s);
+    const int k0 = L->cb[0] == Q8P_CB_E8P_2BIT ? 0 : 1, k1 = L->cb[1] == Q8P_CB_E8P_2BIT ? 0 : 1;
+    launch_dequant_combine(a[0], b[0], a[1], b[1], L->num_stages, k0, k1, double(L->scale[0]), double(L->scale[1]),
+                           total, w_tilde, s);
+    // dequantize_layer (pipeline.cpp:142-149): transform_cols(left, transpose), then
+    // transform_rows(right, transpose) through an f64 transpose
+    launch_rht_cols_f64(w_tilde, scratch, L->m, L->n, L->side_u.signs, s, true);
+    launch_transpose_f64(w_tilde, scratch, L->m, L->n, s);
+    launch_rht_cols_f64(scratch, w_tilde, L->n, L->m, L->side_v.signs, s, true);
+    launch_transpose_f64(scratch, w_tilde, L->n, L->m, s);
     return Q8P_OK;
   } catch (...) {
     return status_of_current_exception();

@@ -87,7 +87,9 @@ struct q8p_layer {
   int cb[2] = {0, 0};
   float scale[2] = {1.f, 1.f};
   q8p::detail::DevSide side_u, side_v;  // left (m) / right (n)
-  void* codes[2] = {nullptr, nullptr};  // plain [m_local][n/8]: u16 (E8P) / u8 (e8-1bit)
+  // plain [m_local][n/8] codes, u16 (E8P) / u8 (e8-1bit): kept on the device only for
+  // layers the tensor-core path cannot run (first stage not E8P; portable GEMV)
+  void* codes[2] = {nullptr, nullptr};
   q8p::detail::SlabCodes tc[2];
   void* mma[2] = {nullptr, nullptr};       // warp-MMA records (gemv_mma.cu), per stage
   const std::uint32_t* mma_tables = nullptr;  // device [256] E8P nibble words + [256][2] e8-1bit rows
@@ -127,7 +129,6 @@ void launch_rht(const DevSide& side, const float* x, float* y, int batch, bool t
                 cudaStream_t s);
 void launch_gemv_simple(const q8p_layer& L, const float* t, float* z, int batch, int z_stride,
                         cudaStream_t s);
-void launch_decode(const q8p_layer& L, int stage, float* w, cudaStream_t s);
 // e8p_encode (core/src/e8p.cpp:114-156) on device, bit-identical: v [nblocks][8] f64 -> words.
 void launch_e8p_encode(const double* v, std::uint16_t* words, std::size_t nblocks, cudaStream_t s);
 // RvqQuantizer::quantize (rvq.cpp:59-79) per 8-vector, bit-identical: codes [stage][nblocks].
@@ -135,8 +136,17 @@ void launch_rvq_quantize(const double* v, std::uint16_t* codes, std::size_t nblo
                          const double* scales, cudaStream_t s);
 // SideTransform::apply (rht) on every column of a row-major L x ncols f64 matrix, in place
 // (scratch: L * ncols doubles), bit-identical to transform_cols (transforms.cpp:66-79).
+// (transpose: SideTransform::apply_transpose per column, as transform_cols(..., true)).
 void launch_rht_cols_f64(double* w, double* scratch, std::uint32_t L, std::uint32_t ncols, const std::uint8_t* signs,
-                         cudaStream_t s);
+                         cudaStream_t s, bool transpose = false);
+// dequantize_layer pieces (kernels_encode.cu): stage points from K2's decoder output
+// combined in f64 as decode_incoherent does, and an f64 transpose.
+void launch_dequant_combine(const std::int8_t* a0, const std::uint8_t* b0, const std::int8_t* a1,
+                            const std::uint8_t* b1, int nst, int kind0, int kind1, double s0, double s1,
+                            std::size_t total, double* w, cudaStream_t s);
+void launch_transpose_f64(const double* in, double* out, std::uint32_t rows, std::uint32_t cols, cudaStream_t s);
+void launch_points_f32(const std::int8_t* a, const std::uint8_t* b, int kind, std::size_t total, float* w,
+                       cudaStream_t s);
 
 // Tensor-core path (gemv_tc.cu, kernels_rht.cu).
 std::vector<std::uint8_t> tc_lut_image();  // the 64 KiB smem LUT window, bulk-copied per CTA

@@ -179,12 +179,16 @@ __global__ void __launch_bounds__(256) rvq_quantize_kernel(const double* __restr
 __global__ void __launch_bounds__(256) rht_cols_f64_kernel(double* __restrict__ w, double* __restrict__ out,
                                                           std::uint32_t L, std::uint32_t ncols, std::uint32_t p,
                                                           std::uint32_t q, const std::uint8_t* __restrict__ signs,
-                                                          const std::int8_t* __restrict__ base, double scale) {
+                                                          const std::int8_t* __restrict__ base, double scale,
+                                                          int transpose) {
   const std::uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const std::uint32_t col = blockIdx.x * 32 + lane;
   const bool on = col < ncols;
-  for (std::uint32_t i = wid; i < L; i += nw)
-    if (on && ((signs[i >> 3] >> (i & 7)) & 1u)) w[std::size_t(i) * ncols + col] = -w[std::size_t(i) * ncols + col];
+  // apply: signs, then H; apply_transpose: H^T (base transposed), then signs
+  // (SideTransform::apply / apply_transpose, transforms.cpp:28-47)
+  if (!transpose)
+    for (std::uint32_t i = wid; i < L; i += nw)
+      if (on && ((signs[i >> 3] >> (i & 7)) & 1u)) w[std::size_t(i) * ncols + col] = -w[std::size_t(i) * ncols + col];
   __syncthreads();
   for (std::uint32_t len = 1; len < p; len <<= 1) {
     for (std::uint32_t t = wid; t < (p / 2) * q; t += nw) {
@@ -201,15 +205,19 @@ __global__ void __launch_bounds__(256) rht_cols_f64_kernel(double* __restrict__ 
   }
   for (std::uint32_t e = wid; e < L; e += nw) {
     if (!on) continue;
+    double v;
     if (q == 1) {
-      out[std::size_t(e) * ncols + col] = __dmul_rn(w[std::size_t(e) * ncols + col], scale);
+      v = __dmul_rn(w[std::size_t(e) * ncols + col], scale);
     } else {
       const std::uint32_t r = e / q, a = e - r * q;
       double acc = 0.0;
       for (std::uint32_t b = 0; b < q; ++b)
-        acc = __dadd_rn(acc, __dmul_rn(double(base[a * q + b]), w[(std::size_t(r) * q + b) * ncols + col]));
-      out[std::size_t(e) * ncols + col] = __dmul_rn(acc, scale);
+        acc = __dadd_rn(acc, __dmul_rn(double(base[transpose ? b * q + a : a * q + b]),
+                                       w[(std::size_t(r) * q + b) * ncols + col]));
+      v = __dmul_rn(acc, scale);
     }
+    if (transpose && ((signs[e >> 3] >> (e & 7)) & 1u)) v = -v;
+    out[std::size_t(e) * ncols + col] = v;
   }
 }
 
@@ -246,11 +254,75 @@ unsigned grid_for(std::size_t nblocks, int dev) {
   return unsigned(std::min<std::size_t>((nblocks + 255) / 256, std::size_t(sms) * 8));
 }
 
+// Dequantize (dequantize_layer, pipeline.cpp:112-149): w[r][8k+c] =
+// sum_s scale_s * point_s[c], accumulated from 0.0 in stage order in f64 as
+// decode_incoherent does; points from K2's decoder output (a, b): E8P
+// (2a + 2b - 1) / 4, e8-1bit a / 2 (exact).
+__global__ void __launch_bounds__(256) dequant_combine_kernel(const std::int8_t* __restrict__ a0,
+                                                              const std::uint8_t* __restrict__ b0,
+                                                              const std::int8_t* __restrict__ a1,
+                                                              const std::uint8_t* __restrict__ b1, int nst, int kind0,
+                                                              int kind1, double s0, double s1, std::size_t total,
+                                                              double* __restrict__ w) {
+  for (std::size_t i = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += std::size_t(gridDim.x) * blockDim.x) {
+    double acc = 0.0;
+    for (int s = 0; s < nst; ++s) {
+      const std::int8_t* a = s ? a1 : a0;
+      const std::uint8_t* b = s ? b1 : b0;
+      const int kind = s ? kind1 : kind0;
+      const double pt = kind == 0 ? (2.0 * a[i] + 2.0 * b[i >> 3] - 1.0) * 0.25 : a[i] * 0.5;
+      acc = __dadd_rn(acc, __dmul_rn(s ? s1 : s0, pt));
+    }
+    w[i] = acc;
+  }
+}
+// Unscaled points of one stage (Codebook::decode) as fp32 from K2's decoder output.
+__global__ void __launch_bounds__(256) points_f32_kernel(const std::int8_t* __restrict__ a,
+                                                         const std::uint8_t* __restrict__ b, int kind,
+                                                         std::size_t total, float* __restrict__ w) {
+  for (std::size_t i = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += std::size_t(gridDim.x) * blockDim.x)
+    w[i] = kind == 0 ? (2.f * a[i] + 2.f * b[i >> 3] - 1.f) * 0.25f : a[i] * 0.5f;
+}
+__global__ void __launch_bounds__(256) transpose_f64_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                                            std::uint32_t rows, std::uint32_t cols) {
+  __shared__ double t[32][33];
+  const std::uint32_t bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (std::uint32_t j = threadIdx.y; j < 32; j += 8)
+    if (by + j < rows && bx + threadIdx.x < cols) t[j][threadIdx.x] = in[std::size_t(by + j) * cols + bx + threadIdx.x];
+  __syncthreads();
+  for (std::uint32_t j = threadIdx.y; j < 32; j += 8)
+    if (bx + j < cols && by + threadIdx.x < rows) out[std::size_t(bx + j) * rows + by + threadIdx.x] = t[threadIdx.x][j];
+}
+
 }  // namespace
+
+void launch_dequant_combine(const std::int8_t* a0, const std::uint8_t* b0, const std::int8_t* a1,
+                            const std::uint8_t* b1, int nst, int kind0, int kind1, double s0, double s1,
+                            std::size_t total, double* w, cudaStream_t s) {
+  dequant_combine_kernel<<<unsigned(std::min<std::size_t>((total + 255) / 256, 148 * 16)), 256, 0, s>>>(
+      a0, b0, a1, b1, nst, kind0, kind1, s0, s1, total, w);
+  cuda_check(cudaGetLastError(), "dequant combine launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void launch_points_f32(const std::int8_t* a, const std::uint8_t* b, int kind, std::size_t total, float* w,
+                       cudaStream_t s) {
+  points_f32_kernel<<<unsigned(std::min<std::size_t>((total + 255) / 256, 148 * 16)), 256, 0, s>>>(a, b, kind, total, w);
+  cuda_check(cudaGetLastError(), "points launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void launch_transpose_f64(const double* in, double* out, std::uint32_t rows, std::uint32_t cols, cudaStream_t s) {
+  transpose_f64_kernel<<<dim3((cols + 31) / 32, (rows + 31) / 32), dim3(32, 8), 0, s>>>(in, out, rows, cols);
+  cuda_check(cudaGetLastError(), "transpose launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
 
 void launch_e8p_encode(const double* v, std::uint16_t* words, std::size_t nblocks, cudaStream_t s) {
   if (nblocks == 0) return;
-  int dev = 0;
+  int dev = 0;  // set by device_tables (the calling thread's device)
   const EncodeTables& t = device_tables(dev);
   e8p_encode_kernel<<<grid_for(nblocks, dev), 256, 0, s>>>(v, words, nblocks, t.doubled, t.odd, t.e81);
   cuda_check(cudaGetLastError(), "e8p encode launch");
@@ -258,11 +330,10 @@ void launch_e8p_encode(const double* v, std::uint16_t* words, std::size_t nblock
 }
 
 void launch_rht_cols_f64(double* w, double* scratch, std::uint32_t L, std::uint32_t ncols, const std::uint8_t* signs,
-                         cudaStream_t s) {
+                         cudaStream_t s, bool transpose) {
   if (L == 0 || ncols == 0) return;
   const HadamardSpec spec = plan_hadamard(L);
-  int dev = 0;
-  cuda_check(cudaGetDevice(&dev), "get device");
+  const int dev = current_device();
   static std::mutex mu;
   static std::vector<std::pair<std::pair<int, std::size_t>, std::int8_t*>> bases;  // (device, q) -> base
   const std::int8_t* base = nullptr;
@@ -281,7 +352,8 @@ void launch_rht_cols_f64(double* w, double* scratch, std::uint32_t L, std::uint3
   }
   const double scale = 1.0 / std::sqrt(double(L));  // had_apply's 1/sqrt(n) (hadamard.cpp:188)
   rht_cols_f64_kernel<<<(ncols + 31) / 32, 256, 0, s>>>(w, scratch, L, ncols, std::uint32_t(spec.p),
-                                                        std::uint32_t(spec.q), signs, base, scale);
+                                                        std::uint32_t(spec.q), signs, base, scale,
+                                                        transpose ? 1 : 0);
   cuda_check(cudaGetLastError(), "rht f64 launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cuda_check(cudaMemcpyAsync(w, scratch, std::size_t(L) * ncols * 8, cudaMemcpyDeviceToDevice, s), "rht f64 copy");
@@ -299,7 +371,7 @@ void launch_rvq_quantize(const double* v, std::uint16_t* codes, std::size_t nblo
     st.kind[i] = kinds[i];
     st.scale[i] = scales[i];
   }
-  int dev = 0;
+  int dev = 0;  // set by device_tables (the calling thread's device)
   const EncodeTables& t = device_tables(dev);
   rvq_quantize_kernel<<<grid_for(nblocks, dev), 256, 0, s>>>(v, codes, nblocks, st, t.doubled, t.odd, t.e81);
   cuda_check(cudaGetLastError(), "rvq quantize launch");

@@ -83,21 +83,6 @@ __device__ __forceinline__ std::uint32_t load_code(const void* codes, int cb, st
                  : std::uint32_t(static_cast<const std::uint8_t*>(codes)[i]);
 }
 
-// ---- K0: decode one stage --------------------------------------------------
-__global__ void decode_kernel(const void* __restrict__ codes, int cb, std::size_t words,
-                              float* __restrict__ w) {
-  __shared__ SmemTables T;
-  load_tables(T);
-  for (std::size_t i = blockIdx.x * std::size_t(blockDim.x) + threadIdx.x; i < words;
-       i += std::size_t(gridDim.x) * blockDim.x) {
-    float v[8];
-    decode_word(T, cb, load_code(codes, cb, i), v);
-    float4* o = reinterpret_cast<float4*>(w + 8 * i);
-    o[0] = make_float4(v[0], v[1], v[2], v[3]);
-    o[1] = make_float4(v[4], v[5], v[6], v[7]);
-  }
-}
-
 // ---- K1 / K3: randomized Hadamard transform ------------------------------
 // One CTA per vector.  y = H (S o x) (forward) or y = S o (H^T x)
 // (transpose), H = (H_p (x) B_q) / sqrt(n), flat index i = a * q + b.
@@ -236,12 +221,5 @@ void launch_gemv_simple(const q8p_layer& L, const float* t, float* z, int batch,
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
-void launch_decode(const q8p_layer& L, int stage, float* w, cudaStream_t s) {
-  upload_tables();
-  const std::size_t words = std::size_t(L.m_local()) * (L.n / 8);
-  decode_kernel<<<num_sms() * 8, 256, 0, s>>>(L.codes[stage], L.cb[stage], words, w);
-  cuda_check(cudaGetLastError(), "decode launch");
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-}
 
 }  // namespace q8p::detail

@@ -170,3 +170,26 @@ def test_linearity_and_batch_consistency(dev):
     assert rel_err((2.0 * y[0] - 0.5 * y[1]).cpu().numpy(), y2.cpu().numpy()) < TC
     for b in range(2):  # per-vector limb scales: batched == single, bit for bit
         assert torch.equal(L.forward(x[b].contiguous()), y[b])
+
+
+@pytest.mark.parametrize("m,n,bits", [(64, 64, 2), (96, 160, 3), (224, 112, 4), (128, 256, 2)])
+def test_dequantize_bit_exact_vs_reference(dev, ref, m, n, bits):
+    # q8p_dequantize == latq::dequantize_layer (pipeline.cpp:142-149) bit for bit:
+    # K2's decoder, decode_incoherent's f64 stage accumulation, transform_cols /
+    # transform_rows with apply_transpose (bases 1, 12, 20, 28)
+    stages = {2: [("e8p-2bit", 1.11)], 3: [("e8p-2bit", 1.02), ("e8-1bit", 0.49)],
+              4: [("e8p-2bit", 0.97), ("e8p-2bit", 0.29)]}[bits]
+    art = random_artifact(m, n, stages, m * n + bits)
+    L = q8p.Layer.from_qshp(art)
+    got = L.dequantize().cpu().numpy()
+    want = ref.dequantize(art)
+    assert got.shape == want.shape
+    assert np.array_equal(got, want), np.abs(got - want).max()
+
+
+def test_plain_codes_not_kept(dev):
+    # the slabs carry every code bit: only slab bytes stay in HBM for E8P-first layers
+    art = random_artifact(1024, 2048, [("e8p-2bit", 1.0)], 4)
+    L = q8p.Layer.from_qshp(art)
+    info = L.info
+    assert info["device_bytes"] < 1.2 * (1024 * 2048 // 8) * 2.125 + (1 << 20), info
