@@ -368,21 +368,36 @@ class Layer:
             d = self.__dict__["_dims_cache"] = (i["m"], i["n"])
         return d
 
+    def _check_x(self, x, n):
+        torch = _torch()
+        if x.dim() != 2 or x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous():
+            raise ValidationError("x must be a contiguous float32 CUDA tensor [batch, n]")
+        if x.device.index != self.info["device"]:
+            raise ValidationError("x is on another device than the layer")
+        if x.shape[1] != n:
+            raise SizeError("infer: input length != n")
+
+    @staticmethod
+    def _out(out, x, rows):
+        torch = _torch()
+        if out is None:
+            return torch.empty(x.shape[0], rows, dtype=torch.float32, device=x.device)
+        if (out.dtype != torch.float32 or not out.is_contiguous() or out.device != x.device
+                or tuple(out.shape) != (x.shape[0], rows)):
+            raise ValidationError(f"out must be a contiguous float32 tensor [{x.shape[0]}, {rows}] on x's device")
+        return out
+
     def forward(self, x, out=None, stream=None, workspace=None, gemv_events=None):
         """y = W_tilde x for a [batch, n] fp32 CUDA tensor -> [batch, m].
         gemv_events: optional (start, end) torch.cuda.Event pair recorded
         around the decode-GEMV kernel."""
-        torch = _torch()
         m, n = self._dims()
         if x.dim() == 1:
-            return self.forward(x.view(1, -1), None if out is None else out.view(1, -1), stream, workspace).view(-1)
-        if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous():
-            raise ValidationError("x must be a contiguous float32 CUDA tensor")
-        if x.shape[1] != n:
-            raise SizeError("infer: input length != n")
+            return self.forward(x.view(1, -1), None if out is None else out.view(1, -1), stream, workspace,
+                                gemv_events).view(-1)
+        self._check_x(x, n)
         batch = x.shape[0]
-        if out is None:
-            out = torch.empty(batch, m, dtype=torch.float32, device=x.device)
+        out = self._out(out, x, m)
         ws = workspace if workspace is not None else self.workspace(batch)
         if gemv_events is None:
             _check(lib().q8p_forward(self._h, x.data_ptr(), out.data_ptr(), batch, ws.data_ptr(),
@@ -396,10 +411,10 @@ class Layer:
     def rows_z(self, x, stream=None, workspace=None):
         """This handle's rows of z = W_hat T_v x ([batch, rows]); the slice a
         row-sharded forward all-gathers before y = T_u^T z."""
-        torch = _torch()
         info = self.info
+        self._check_x(x, info["n"])
         batch = x.shape[0]
-        z = torch.empty(batch, info["row_end"] - info["row_begin"], dtype=torch.float32, device=x.device)
+        z = self._out(None, x, info["row_end"] - info["row_begin"])
         ws = workspace if workspace is not None else self.workspace(batch)
         _check(lib().q8p_forward_rows_z(self._h, x.data_ptr(), z.data_ptr(), batch, ws.data_ptr(), ws.numel(),
                                         _stream_ptr(stream)))
@@ -411,11 +426,10 @@ class Layer:
         (NcclComm or a raw ncclComm_t pointer) and every rank gets the full y."""
         if isinstance(comm, NcclComm):
             comm = comm.handle
-        torch = _torch()
         info = self.info
+        self._check_x(x, info["n"])
         batch = x.shape[0]
-        if out is None:
-            out = torch.empty(batch, info["m"], dtype=torch.float32, device=x.device)
+        out = self._out(out, x, info["m"])
         ws = workspace if workspace is not None else self.workspace(batch)
         _check(lib().q8p_forward_sharded(self._h, x.data_ptr(), out.data_ptr(), batch, ws.data_ptr(),
                                          ws.numel(), comm, _stream_ptr(stream)))

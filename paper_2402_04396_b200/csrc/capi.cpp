@@ -929,9 +929,12 @@ void q8p_layer_destroy(q8p_layer* L) {
   forget_set_graphs(L);
   if (L->capture_stream) cudaStreamDestroy(L->capture_stream);
   for (void* p : L->allocations) cudaFree(p);
-  if (L->dev_stage) cudaFree(L->dev_stage);
-  if (L->host_stage) cudaFreeHost(L->host_stage);
-  if (L->stream) cudaStreamDestroy(L->stream);
+  for (q8p_layer::Stage* st : L->stage_all) {
+    if (st->dev) cudaFree(st->dev);
+    if (st->host) cudaFreeHost(st->host);
+    if (st->stream) cudaStreamDestroy(st->stream);
+    delete st;
+  }
   cudaSetDevice(prev);
   delete L;
 }
@@ -1070,34 +1073,56 @@ q8p_status q8p_infer_host(q8p_layer* L, const double* x, double* y, int batch) {
   try {
     if (!L || !x || !y) throw q8p::ValidationError("null argument");
     if (batch <= 0) return Q8P_OK;
-    std::scoped_lock lock(L->mu);
     DeviceGuard g(L->device);
-    if (!L->stream) cuda_check(cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking), "stream");
+    q8p_layer::Stage* st = nullptr;
+    {
+      std::scoped_lock lock(L->stage_mu);
+      if (!L->stage_free.empty()) {
+        st = L->stage_free.back();
+        L->stage_free.pop_back();
+      } else {
+        st = new q8p_layer::Stage();
+        L->stage_all.push_back(st);
+      }
+    }
+    struct Release {  // the context goes back to the pool on every exit path
+      q8p_layer* L;
+      q8p_layer::Stage* st;
+      ~Release() {
+        std::scoped_lock lock(L->stage_mu);
+        L->stage_free.push_back(st);
+      }
+    } release{L, st};
+    if (!st->stream) cuda_check(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking), "stream");
     const std::size_t xin = std::size_t(batch) * L->n, yout = std::size_t(batch) * L->m;
     const std::size_t host_need = (xin + yout) * sizeof(float);
-    if (L->host_stage_bytes < host_need) {
-      if (L->host_stage) cudaFreeHost(L->host_stage);
-      cuda_check(cudaMallocHost(&L->host_stage, host_need), "cudaMallocHost");
-      L->host_stage_bytes = host_need;
+    if (st->host_bytes < host_need) {
+      if (st->host) cudaFreeHost(st->host);
+      st->host = nullptr;
+      st->host_bytes = 0;
+      cuda_check(cudaMallocHost(&st->host, host_need), "cudaMallocHost");
+      st->host_bytes = host_need;
     }
     const std::size_t ws = workspace_size(L, batch);
     const std::size_t dev_need = round_up(xin * 4, 256) + round_up(yout * 4, 256) + ws;
-    if (L->dev_stage_bytes < dev_need) {
-      if (L->dev_stage) cudaFree(L->dev_stage);
-      cuda_check(cudaMalloc(&L->dev_stage, dev_need), "cudaMalloc stage");
-      L->dev_stage_bytes = dev_need;
+    if (st->dev_bytes < dev_need) {
+      if (st->dev) cudaFree(st->dev);
+      st->dev = nullptr;
+      st->dev_bytes = 0;
+      cuda_check(cudaMalloc(&st->dev, dev_need), "cudaMalloc stage");
+      st->dev_bytes = dev_need;
     }
-    float* hx = static_cast<float*>(L->host_stage);
+    float* hx = static_cast<float*>(st->host);
     float* hy = hx + xin;
     for (std::size_t i = 0; i < xin; ++i) hx[i] = static_cast<float>(x[i]);
-    auto* dbase = static_cast<std::uint8_t*>(L->dev_stage);
+    auto* dbase = static_cast<std::uint8_t*>(st->dev);
     float* dx = reinterpret_cast<float*>(dbase);
     float* dy = reinterpret_cast<float*>(dbase + round_up(xin * 4, 256));
     void* dws = dbase + round_up(xin * 4, 256) + round_up(yout * 4, 256);
-    cuda_check(cudaMemcpyAsync(dx, hx, xin * 4, cudaMemcpyHostToDevice, L->stream), "H2D");
-    forward_impl(L, dx, dy, batch, dws, ws, L->stream);
-    cuda_check(cudaMemcpyAsync(hy, dy, yout * 4, cudaMemcpyDeviceToHost, L->stream), "D2H");
-    cuda_check(cudaStreamSynchronize(L->stream), "sync");
+    cuda_check(cudaMemcpyAsync(dx, hx, xin * 4, cudaMemcpyHostToDevice, st->stream), "H2D");
+    forward_impl(L, dx, dy, batch, dws, ws, st->stream);
+    cuda_check(cudaMemcpyAsync(hy, dy, yout * 4, cudaMemcpyDeviceToHost, st->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(st->stream), "sync");
     for (std::size_t i = 0; i < yout; ++i) y[i] = static_cast<double>(hy[i]);
     return Q8P_OK;
   } catch (...) {

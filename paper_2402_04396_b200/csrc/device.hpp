@@ -97,13 +97,19 @@ struct q8p_layer {
   std::size_t device_bytes = 0;
   std::size_t code_bytes = 0;
   std::vector<void*> allocations;
-  // q8p_infer_host staging (serialized by `mu`).
-  std::mutex mu;
-  void* host_stage = nullptr;
-  std::size_t host_stage_bytes = 0;
-  void* dev_stage = nullptr;
-  std::size_t dev_stage_bytes = 0;
-  cudaStream_t stream = nullptr;
+  // q8p_infer_host staging: a pool of per-call contexts (stream, pinned host and
+  // device buffers); concurrent callers each take one, so infer is re-entrant as
+  // the reference's and calls on one layer run in parallel.
+  struct Stage {
+    cudaStream_t stream = nullptr;
+    void* host = nullptr;
+    std::size_t host_bytes = 0;
+    void* dev = nullptr;
+    std::size_t dev_bytes = 0;
+  };
+  std::mutex stage_mu;
+  std::vector<Stage*> stage_free;  // idle contexts
+  std::vector<Stage*> stage_all;   // every context (freed by q8p_layer_destroy)
   // q8p_forward graph cache (capi.cpp): the forward's kernel chain captured once per
   // (x, y, batch, workspace) and replayed with one cudaGraphLaunch.
   struct GraphEntry {

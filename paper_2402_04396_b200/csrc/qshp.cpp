@@ -228,6 +228,11 @@ void throw_status(q8p_status s) {
 // ---- DeviceLayer -----------------------------------------------------------
 namespace {
 q8p_layer* make_from(const QuantizedLinear& a, int device) {
+  // the checks decode_incoherent / serialize make (pipeline.cpp:116-117, 126-127)
+  if (a.codes.size() != a.stages.size()) throw FormatError("artifact: stage/code count mismatch");
+  if (a.n % 8 != 0) throw FormatError("artifact: n not divisible by codeword dimension");
+  for (const auto& c : a.codes)
+    if (c.size() != std::size_t(a.m) * (a.n / 8)) throw FormatError("artifact: codeword count mismatch");
   std::vector<q8p_stage_desc> st(a.stages.size());
   for (std::size_t s = 0; s < st.size(); ++s) {
     st[s].codebook = a.stages[s].codebook == "e8p-2bit" ? Q8P_CB_E8P_2BIT : Q8P_CB_E8_1BIT;

@@ -193,3 +193,32 @@ def test_plain_codes_not_kept(dev):
     L = q8p.Layer.from_qshp(art)
     info = L.info
     assert info["device_bytes"] < 1.2 * (1024 * 2048 // 8) * 2.125 + (1 << 20), info
+
+
+def test_infer_host_reentrant(dev):
+    # latq::infer is safe for concurrent calls on a shared artifact:
+    # q8p_infer_host from 8 threads at once (ctypes drops the GIL) gives the
+    # single-threaded results bit for bit
+    from concurrent.futures import ThreadPoolExecutor
+    art, x, y = load_case("rvq3_256x128")
+    L = q8p.Layer.from_qshp(art)
+    want = [L.infer_host(x[b % x.shape[0]]) for b in range(16)]
+    with ThreadPoolExecutor(8) as ex:
+        got = list(ex.map(lambda b: L.infer_host(x[b % x.shape[0]]), range(16)))
+    for b in range(16):
+        assert np.array_equal(got[b], want[b])
+        assert rel_err(got[b], y[b % x.shape[0]]) < TC
+
+
+def test_forward_argument_validation(dev):
+    art, x, _ = load_case("e8p2_64x64")
+    L = q8p.Layer.from_qshp(art)
+    xd = torch.from_numpy(x.astype(np.float32)).to(dev)
+    with pytest.raises(q8p.ValidationError):
+        L.forward(xd, out=torch.empty(x.shape[0], 63, device=dev))
+    with pytest.raises(q8p.ValidationError):
+        L.forward(xd, out=torch.empty(x.shape[0], 64, device=dev, dtype=torch.float64))
+    with pytest.raises(q8p.ValidationError):
+        L.rows_z(xd.double())
+    with pytest.raises(q8p.SizeError):
+        L.rows_z(torch.zeros(1, 65, device=dev))
