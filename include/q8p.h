@@ -274,6 +274,14 @@ q8p_status q8p_e8p_decode_host(uint16_t word, float out[8]);
 q8p_status q8p_codebook_table(q8p_codebook cb, int8_t* doubled, uint8_t* parity_out);
 q8p_status q8p_hadamard_base(size_t q, int8_t* out);
 
+/* Test support for the row-sharded path on one GPU: runs every rank's part of
+ * q8p_forward_sharded in turn (K1, K2 on the shard's rows, K3 pass 1 into the
+ * send buffer) with the all-gather replaced by device copies into the gathered
+ * buffer, then K3 pass 2 -> y [batch][m].  shards[r] = rows shard_rows(m, world, r)
+ * of one layer, all on one device; batch <= 32; ws sized for shards[0]. */
+q8p_status q8p_forward_sharded_sim(const q8p_layer* const* shards, int world, const float* x, float* y, int batch,
+                                   void* workspace, size_t workspace_bytes, void* stream);
+
 /* NCCL plumbing for q8p_forward_sharded (wraps ncclGetUniqueId /
  * ncclCommInitRank so callers need no NCCL headers). */
 q8p_status q8p_nccl_unique_id(uint8_t out[128]);

@@ -150,6 +150,7 @@ _SIGNATURES = {
     "q8p_bench_gemv": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]),
     "q8p_bench_stream": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]),
     "q8p_layer_code_region": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_size_t)]),
+    "q8p_forward_sharded_sim": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "q8p_dequantize": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "q8p_k2_decode_stage": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "q8p_rht": (ctypes.c_int, [ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
@@ -571,6 +572,20 @@ def rvq_quantize(v, stages, stream=None):
     _check(lib().q8p_rvq_quantize(v.data_ptr(), out.data_ptr(), v.shape[0], len(stages), cbs, scs,
                                   v.device.index or 0, _stream_ptr(stream)))
     return out.to(torch.int32) & 0xFFFF
+
+
+def forward_sharded_sim(shards, x, stream=None):
+    """q8p_forward_sharded_sim: the row-sharded forward of `shards` (rank-ordered
+    row-range handles of one layer on one GPU) with the all-gather simulated by copies."""
+    torch = _torch()
+    info = shards[0].info
+    shards[0]._check_x(x, info["n"])
+    y = torch.empty(x.shape[0], info["m"], dtype=torch.float32, device=x.device)
+    ws = shards[0].workspace(x.shape[0])
+    arr = (ctypes.c_void_p * len(shards))(*[S._h.value for S in shards])
+    _check(lib().q8p_forward_sharded_sim(arr, len(shards), x.data_ptr(), y.data_ptr(), x.shape[0], ws.data_ptr(),
+                                         ws.numel(), _stream_ptr(stream)))
+    return y
 
 
 def bench_stream(addr: int, nbytes: int, reps: int, stream=None):

@@ -34,7 +34,12 @@ void kernel_attrs(const void* fn, int max_dyn_smem, bool cluster) {
   for (const auto& e : done)
     if (e.first == fn && e.second == dev) return;
   cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn_smem), "smem attr");
+#ifndef Q8P_DBG_NO_CARVEOUT
   cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout attr");
+#else
+  if (max_dyn_smem > 150 * 1024)
+    cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout attr");
+#endif
   if (cluster) cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1), "cluster attr");
   done.emplace_back(fn, dev);
 }
@@ -389,8 +394,8 @@ std::size_t workspace_parts(const q8p_layer* L, int batch, Workspace* w, void* b
     v.tl = reinterpret_cast<long long*>(take(BK * 8));
     v.bimg = take(tc_bimg_bytes(L->n, batch) * (BK / B));
     v.zacc = reinterpret_cast<std::int32_t*>(take(std::size_t(L->num_stages) * v.zcols * v.rows_pad * 4));
-    v.z_full = reinterpret_cast<float*>(take(B * L->m * 4));  // q8p_forward_sharded
-    if (L->row_begin != 0 || L->row_end != L->m) v.z_loc = reinterpret_cast<float*>(take(B * L->m_local() * 4));
+    v.z_full = reinterpret_cast<float*>(take(B * L->m * 4));      // q8p_forward_sharded: gathered rows
+    v.z_loc = reinterpret_cast<float*>(take(B * L->m_local() * 4));  // this rank's rows (send buffer)
   } else {
     v.t = reinterpret_cast<float*>(take(B * L->n * 4));
     v.z = reinterpret_cast<float*>(take(B * L->m * 4));
@@ -444,10 +449,18 @@ inline void nccl_check(ncclResult_t r, const char* what) {
   if (r != ncclSuccess) throw_nccl(r, what);
 }
 
-// Row-sharded forward: K1 (replicated) -> K2 on this rank's rows ->
-// combine -> ncclAllGather of the z slices over NVLink -> K3 on the full z.  Each
-// row's integer accumulation is unchanged by sharding, and the combine / K3
-// arithmetic is the unsharded one, so sharded y equals unsharded y bit for bit.
+// Row-sharded forward.  Per chunk of vectors:
+//   K1 (replicated) -> K2 on this rank's rows -> K3 pass 1 on this rank's rows,
+//   straight from its accumulators into the send buffer [nb][m_local] (the rows of
+//   a rank are whole pass-1 chunks) -> ONE ncclAllGather of nb * m_local floats
+//   (rank-major [world][nb][m_local]) over NVLink -> K3 pass 2 on the gathered rows.
+// Pass 1 acts on contiguous chunks independently, so each rank computes exactly
+// the values the unsharded pass 1 computes for its chunks, and pass 2 is
+// unchanged: sharded y equals unsharded y bit for bit.  When the rank's rows are
+// not whole chunks (or transform = rfft): combine -> the same single all-gather ->
+// both K3 passes on the gathered z (rank-major reads; rfft: one call per vector).
+// No host synchronisation: the whole forward is stream-ordered and capturable
+// in a CUDA graph (NCCL collectives capture as graph nodes).
 void forward_sharded_impl(const q8p_layer* L, const float* x, float* y, int batch, void* ws, std::size_t ws_bytes,
                           ncclComm_t comm, cudaStream_t s) {
   if (!L) throw ValidationError("null layer");
@@ -463,24 +476,39 @@ void forward_sharded_impl(const q8p_layer* L, const float* x, float* y, int batc
   const std::uint32_t ml = L->m_local();
   if (std::size_t(ml) * std::size_t(world) != L->m || L->row_begin != std::uint32_t(rank) * ml)
     throw ValidationError("row shards must be equal-sized and ordered by rank");
+  if (ml % 4 != 0) throw UnsupportedError("row shards must be multiples of 4 rows");
   if (!ws || ws_bytes < workspace_size(L, batch)) throw SizeError("workspace too small");
   DeviceGuard g(L->device);
   Workspace w;
   workspace_parts(L, batch, &w, ws);
   float zscale[2] = {L->scale[0], L->scale[1]};
   int ze8p[2] = {L->cb[0] == Q8P_CB_E8P_2BIT, L->cb[1] == Q8P_CB_E8P_2BIT};
-  float* zl = L->row_begin == 0 && L->row_end == L->m ? w.z_full : w.z_loc;
+  const bool local_p1 = rht_sharded_k3_ok(L->side_u, L->row_begin, ml);
   for (int b0 = 0; b0 < batch; b0 += chunk) {
     const int nb = std::min(chunk, batch - b0);
+    float* yb = y + std::size_t(b0) * L->m;
     forward_local(L, x + std::size_t(b0) * L->n, nb, w, s, nullptr);
+    if (local_p1) {
+      launch_rht_out_acc_local(L->side_u, w.zacc, L->num_stages, w.rows_pad, std::uint32_t(tc_ncols_pad(4 * nb)),
+                               zscale, ze8p, w.alpha, w.tl, L->row_begin, ml, w.z_loc, nb, s);
+      nccl_check(ncclAllGather(w.z_loc, w.z_full, std::size_t(nb) * ml, ncclFloat32, comm, s), "ncclAllGather");
+      launch_rht_out_pass2_gathered(L->side_u, w.z_full, ml, yb, nb, s);
+      continue;
+    }
     launch_combine_acc(w.zacc, L->num_stages, w.rows_pad, std::uint32_t(tc_ncols_pad(4 * nb)), zscale, ze8p, w.alpha,
-                       w.tl, zl, ml, nb, s);
-    nccl_check(ncclGroupStart(), "ncclGroupStart");
-    for (int b = 0; b < nb; ++b)
-      nccl_check(ncclAllGather(zl + std::size_t(b) * ml, w.z_full + std::size_t(b) * L->m, ml, ncclFloat32, comm, s),
-                 "ncclAllGather");
-    nccl_check(ncclGroupEnd(), "ncclGroupEnd");
-    launch_rht_out(L->side_u, w.z_full, w.u, y + std::size_t(b0) * L->m, nb, s);
+                       w.tl, w.z_loc, ml, nb, s);
+    if (L->side_u.kind == 0) {
+      nccl_check(ncclAllGather(w.z_loc, w.z_full, std::size_t(nb) * ml, ncclFloat32, comm, s), "ncclAllGather");
+      launch_rht_out_gathered(L->side_u, w.z_full, ml, w.u, yb, nb, s);
+    } else {  // rfft K3 reads natural-layout z: one gather per vector
+      nccl_check(ncclGroupStart(), "ncclGroupStart");
+      for (int b = 0; b < nb; ++b)
+        nccl_check(ncclAllGather(w.z_loc + std::size_t(b) * ml, w.z_full + std::size_t(b) * L->m, ml, ncclFloat32,
+                                 comm, s),
+                   "ncclAllGather");
+      nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+      launch_rht_out(L->side_u, w.z_full, w.u, yb, nb, s);
+    }
   }
 }
 
@@ -1406,6 +1434,47 @@ q8p_status q8p_forward_sharded(const q8p_layer* L, const float* x, float* y, int
     return status_of_current_exception();
   }
 }
+q8p_status q8p_forward_sharded_sim(const q8p_layer* const* shards, int world, const float* x, float* y, int batch,
+                                   void* ws, size_t ws_bytes, void* stream) {
+  try {
+    if (!shards || world < 1 || !x || !y || !ws) throw q8p::ValidationError("null argument");
+    if (batch <= 0) return Q8P_OK;
+    const q8p_layer* L0 = shards[0];
+    if (!L0) throw q8p::ValidationError("null layer");
+    const std::uint32_t ml = L0->m_local();
+    for (int r = 0; r < world; ++r) {
+      const q8p_layer* L = shards[r];
+      if (!L || L->m != L0->m || L->n != L0->n || L->m_local() != ml || L->row_begin != std::uint32_t(r) * ml ||
+          L->device != L0->device)
+        throw q8p::ValidationError("shards must be the equal, rank-ordered row ranges of one layer");
+    }
+    if (std::size_t(ml) * world != L0->m) throw q8p::ValidationError("shards do not cover the layer");
+    if (!tc_supported(*L0, batch)) throw q8p::UnsupportedError("sharded simulation: batch <= 32 on the tensor-core path");
+    if (!rht_sharded_k3_ok(L0->side_u, 0, ml)) throw q8p::UnsupportedError("sharded simulation: rows not whole chunks");
+    if (ws_bytes < workspace_size(L0, batch)) throw q8p::SizeError("workspace too small");
+    DeviceGuard g(L0->device);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    float zscale[2] = {L0->scale[0], L0->scale[1]};
+    int ze8p[2] = {L0->cb[0] == Q8P_CB_E8P_2BIT, L0->cb[1] == Q8P_CB_E8P_2BIT};
+    Workspace w;
+    for (int r = 0; r < world; ++r) {  // each rank's part of q8p_forward_sharded, in turn
+      const q8p_layer* L = shards[r];
+      workspace_parts(L, batch, &w, ws);
+      forward_local(L, x, batch, w, s, nullptr);
+      launch_rht_out_acc_local(L->side_u, w.zacc, L->num_stages, w.rows_pad, std::uint32_t(tc_ncols_pad(4 * batch)),
+                               zscale, ze8p, w.alpha, w.tl, L->row_begin, ml, w.z_loc, batch, s);
+      // the all-gather's data movement: rank r's slice -> [r][batch][m_local]
+      cuda_check(cudaMemcpyAsync(w.z_full + std::size_t(r) * batch * ml, w.z_loc, std::size_t(batch) * ml * 4,
+                                 cudaMemcpyDeviceToDevice, s),
+                 "gather copy");
+    }
+    launch_rht_out_pass2_gathered(L0->side_u, w.z_full, ml, y, batch, s);
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
 q8p_status q8p_nccl_unique_id(uint8_t out[128]) {
   try {
     if (!out) throw q8p::ValidationError("null argument");

@@ -196,6 +196,20 @@ void launch_rht_in_limbs(const DevSide& side, const float* x, float* u_scratch, 
                          std::uint8_t* bimg_tail, std::size_t tail_bytes, std::int32_t* zero_ptr,
                          std::size_t zero_words, int batch, cudaStream_t s, std::uint32_t chunk_vec = 0,
                          std::size_t chunk_bytes = 0);
+// Row-sharded K3 (q8p_forward_sharded): pass 1 on this rank's rows straight from
+// its accumulators into the all-gather send buffer [batch][m_local] (when the rank's
+// rows are whole pass-1 chunks: rht_sharded_k3_ok), pass 2 over the gathered
+// rank-major [world][batch][m_local] buffer; launch_rht_out_gathered = both passes
+// from gathered fp32 z (the fallback after combine).
+bool rht_sharded_k3_ok(const DevSide& side, std::uint32_t row0, std::uint32_t m_local);
+void launch_rht_out_acc_local(const DevSide& side, const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows,
+                              std::uint32_t zacc_cols, const float zscale[2], const int ze8p[2], const float* alpha,
+                              const long long* tl, std::uint32_t row0, std::uint32_t m_local, float* z_send, int batch,
+                              cudaStream_t s);
+void launch_rht_out_pass2_gathered(const DevSide& side, const float* mid_gathered, std::uint32_t m_local, float* y,
+                                   int batch, cudaStream_t s);
+void launch_rht_out_gathered(const DevSide& side, const float* z_gathered, std::uint32_t m_local, float* u_scratch,
+                             float* y, int batch, cudaStream_t s);
 // Row-sharded forward: this rank's fp32 z rows [batch][m_local] from the limb accumulators.
 void launch_combine_acc(const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows, std::uint32_t zacc_cols,
                         const float zscale[2], const int ze8p[2], const float* alpha, const long long* tl, float* z,

@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(Shape<TEAMS>::kThreads, 1) gemv_mma_kernel(Mma
     mbar_wait(bar_full + 8 * st, ph);
     if (i == 0 && threadIdx.x == 0) gstamp(a, 2);
     const bool act = (rb * kRowPairs + std::uint32_t(rp)) * 32u < a.m_local;
-    // this warp's operands into registers, then the slot goes back to the producer
+    // this warp's operands into registers
     HalfE8p r0, r1, q0, q1;
     uint4 e0, e1;
     uint2 bf0[4][NB8], bf1[4][NB8], bs[NB8];
@@ -427,9 +427,7 @@ __global__ void __launch_bounds__(Shape<TEAMS>::kThreads, 1) gemv_mma_kernel(Mma
       for (int nb = 0; nb < NB8; ++nb)
         bs[nb] = make_uint2(lds32(bbase + bside + nb * 256u), lds32(bbase + bside + nb * 256u + 128u));
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(bar_empty + 8 * st);
-    const std::uint32_t rb_now = rb;
+    const std::uint32_t rb_now = rb, st_now = st;
     st += TEAMS;
     if (st >= S) st -= S, ph ^= 1;
     ks += TEAMS;
@@ -450,8 +448,12 @@ __global__ void __launch_bounds__(Shape<TEAMS>::kThreads, 1) gemv_mma_kernel(Mma
           e81_half<NB8>(e1, bf1, lb8, acc[1]);
         }
       }
-      if (i + TEAMS >= count || rb != rb_now) flush(rb_now);
     }
+    // the slot goes back only after the MMAs consumed every register loaded from it
+    // (an arrive right after the LDS could overtake them; WAR race with the refill)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar_empty + 8 * st_now);
+    if (act && (i + TEAMS >= count || rb != rb_now)) flush(rb_now);
   }
   if (threadIdx.x == 0) gstamp(a, 3);
 }

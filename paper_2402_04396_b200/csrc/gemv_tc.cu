@@ -393,6 +393,9 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
         if (++bslot_n == SBg) bslot_n = 0;
       };
       pdl_wait();  // K1's B images (and zeroed accumulators) are visible from here on
+#ifdef Q8P_DBG_PROXY_FENCE
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");
+#endif
       while (bnext < n_g && bnext < SBg) issue_b();
       std::uint32_t j = (it0 + g) % per_rb;
       std::uint32_t buf = 0, bph = 0, started = 0, seg = 0, team = 0;
@@ -465,12 +468,17 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
       const std::uint32_t abuf = tbase + tl + (NB * grp + buf) * kAcols;
       if (e8p) {
         const SlabRowE8p row = load_row_e8p(sa, row_in);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_empty_c + 8 * st);  // slab is in registers: hand the slot back
         // Decode the whole slab row into registers first, then wait for the A buffer:
         // the decode overlaps the MMA turnaround of the buffer's previous item.
         std::uint32_t o[64], sd[8];
         decode_row_e8p(row, lb, ct_lo, ct_hi, o, sd);
+        // Hand the slot back only now: the decode has consumed every loaded register,
+        // so the warp's LDS of the slot have completed.  (An arrive right after the
+        // LDS instructions can overtake them -- the loads are asynchronous until a
+        // register is read -- and the producer's bulk copy for item i + S then
+        // overwrites the slot under them: a WAR race when the ring wraps.)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_empty_c + 8 * st);
         // pin every result before the wait (an empty asm consuming them; no code)
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4)
@@ -489,7 +497,7 @@ __global__ void __launch_bounds__(Roles<G, T>::kThreads, 1) gemv_tc_kernel(TcArg
       } else {
         std::uint32_t o[64];
         decode_row_e81(sa, row_in, lb8, o);
-        __syncwarp();
+        __syncwarp();  // (after the decode consumed the slot's loads, as above)
         if (lane == 0) mbar_arrive(bar_empty_c + 8 * st);
         A_EMPTY_WAIT(bar_a_empty + 8 * (NB * grp + buf), bph ^ 1);
         tc_fence_after();
@@ -672,9 +680,11 @@ void tc_transcode_device(const void* codes, std::uint32_t m_local, std::uint32_t
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
-// MMA N for `ncols` B rows (4 limbs x batch): 8, 16, 32, 48, 64, then 128 (batch 17..32).
+// MMA N for `ncols` B rows (4 limbs x batch): 8, 16, 32, 64, then 128 (batch 17..32).
+// (Batches 9-12 run at N = 64: the N = 48 variant showed rare run-to-run differences
+// on long-k layers that no other N shows -- tools/dbg_repeat3.py.)
 int tc_ncols_pad(int ncols) {
-  return ncols <= 8 ? 8 : ncols <= 16 ? 16 : ncols <= 64 ? (ncols + 15) / 16 * 16 : 128;
+  return ncols <= 8 ? 8 : ncols <= 16 ? 16 : ncols <= 32 ? 32 : ncols <= 64 ? 64 : 128;
 }
 bool tc_supported(const q8p_layer& L, int batch) {
   return batch >= 1 && batch <= kTcMaxBatch && L.tc[0].codes != nullptr && L.cb[0] == Q8P_CB_E8P_2BIT &&
@@ -728,7 +738,6 @@ void launch_gemv_tc(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* 
       break;
     case 16: fits(3) ? launch_ng<16, 3>(a, s) : launch_ng<16, 2>(a, s); break;
     case 32: launch_ng<32, 2>(a, s); break;
-    case 48: launch_ng<48, 2>(a, s); break;
     case 64: fits(2) ? launch_ng<64, 2>(a, s) : launch_ng<64, 1>(a, s); break;
     default: launch_ng<128, 1>(a, s); break;  // prefill chunks: one decode group, 400 TMEM columns
   }

@@ -50,10 +50,11 @@ __global__ void __launch_bounds__(kP1Threads) rht_pass1(RhtArgs a) {
   const int b = blockIdx.y;
   pdl_wait();
   pdl_trigger();
-  if (blockIdx.x >= a.P1) {
+  const std::uint32_t nch = a.p1_count ? a.p1_count : a.P1;  // chunk CTAs (this rank's, when sharded)
+  if (blockIdx.x >= nch) {
     if (b == 0) {
-      const std::size_t nz = gridDim.x - a.P1;
-      const std::size_t t0 = (blockIdx.x - a.P1) * std::size_t(blockDim.x) + threadIdx.x;
+      const std::size_t nz = gridDim.x - nch;
+      const std::size_t t0 = (blockIdx.x - nch) * std::size_t(blockDim.x) + threadIdx.x;
       if (a.zero_ptr) {
         int4* zp = reinterpret_cast<int4*>(a.zero_ptr);
         for (std::size_t i = t0; i < a.zero_words / 4; i += nz * blockDim.x) zp[i] = make_int4(0, 0, 0, 0);
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(kP1Threads) rht_pass1(RhtArgs a) {
     }
   }
   __shared__ float red1[32];
-  rht_p1_body<Q>(a, blockIdx.x, b, sm1, red1, block_team());
+  rht_p1_body<Q>(a, a.ch0 + blockIdx.x, b, sm1, red1, block_team());
 }
 
 // Pass 2.  grid = (P2 * q / 4 column groups, batch); block = 128 threads.
@@ -130,7 +131,8 @@ void launch_pass1_q(const RhtArgs& a, std::uint32_t extra_ctas, cudaStream_t s) 
   const std::size_t bsz = Q == 1 ? 0 : (Q <= 28 ? Q * Q * 4 : (Q * Q + 15) / 16 * 16);
   const std::size_t smem = chunk * 4 * (Q > 1 ? 2 : 1) + bsz;
   kernel_attrs(reinterpret_cast<const void*>(rht_pass1<Q>), 96 * 1024);
-  launch_pdl(rht_pass1<Q>, dim3(a.P1 + extra_ctas, a.batch), dim3(kP1Threads), smem, s, a);
+  launch_pdl(rht_pass1<Q>, dim3((a.p1_count ? a.p1_count : a.P1) + extra_ctas, a.batch), dim3(kP1Threads), smem, s,
+             a);
 }
 
 void launch_pass1(const RhtArgs& a, std::uint32_t extra, cudaStream_t s) {
@@ -246,6 +248,73 @@ void launch_rht_in_limbs(const DevSide& side, const float* x, float* u_scratch, 
   a.chunk_bytes = chunk_bytes;
   launch_pass1(a, 32, s);
   launch_pass2_limbs(a, s);
+}
+
+bool rht_sharded_k3_ok(const DevSide& side, std::uint32_t row0, std::uint32_t m_local) {
+  if (side.kind != 0) return false;
+  RhtArgs a{};
+  plan_split_impl(side, a);
+  const std::uint32_t chunk = a.P2 * a.q;
+  return m_local % chunk == 0 && row0 % chunk == 0;
+}
+
+void launch_rht_out_acc_local(const DevSide& side, const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows,
+                              std::uint32_t zacc_cols, const float zscale[2], const int ze8p[2], const float* alpha,
+                              const long long* tl, std::uint32_t row0, std::uint32_t m_local, float* z_send, int batch,
+                              cudaStream_t s) {
+  RhtArgs a{};
+  plan_split_impl(side, a);
+  const std::uint32_t chunk = a.P2 * a.q;
+  a.signs = side.signs;
+  a.base = side.base;
+  a.zacc = zacc;
+  a.zrows = zacc_rows;
+  a.zcols = zacc_cols;
+  a.zstages = zacc_stages;
+  a.zscale0 = zscale[0];
+  a.zscale1 = zscale[1];
+  a.ze8p0 = ze8p[0];
+  a.ze8p1 = ze8p[1];
+  a.alpha_in = alpha;
+  a.tl_in = tl;
+  a.mid = z_send;
+  a.batch = batch;
+  a.fwd = 0;
+  a.ch0 = row0 / chunk;
+  a.p1_count = m_local / chunk;
+  a.row0 = row0;
+  a.p1_out_rows = m_local;
+  launch_pass1(a, 0, s);
+}
+
+void launch_rht_out_pass2_gathered(const DevSide& side, const float* mid_gathered, std::uint32_t m_local, float* y,
+                                   int batch, cudaStream_t s) {
+  RhtArgs a{};
+  plan_split_impl(side, a);
+  a.signs = side.signs;
+  a.base = side.base;
+  a.mid = const_cast<float*>(mid_gathered);
+  a.mid_rows = m_local;
+  a.out = y;
+  a.batch = batch;
+  a.fwd = 0;
+  launch_pass2(a, s);
+}
+
+void launch_rht_out_gathered(const DevSide& side, const float* z_gathered, std::uint32_t m_local, float* u_scratch,
+                             float* y, int batch, cudaStream_t s) {
+  RhtArgs a{};
+  plan_split_impl(side, a);
+  a.signs = side.signs;
+  a.base = side.base;
+  a.in = z_gathered;
+  a.in_rows = m_local;
+  a.mid = u_scratch;
+  a.out = y;
+  a.batch = batch;
+  a.fwd = 0;
+  launch_pass1(a, 0, s);
+  launch_pass2(a, s);
 }
 
 void launch_rht_out_acc(const DevSide& side, const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows,

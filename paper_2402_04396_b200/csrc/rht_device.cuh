@@ -50,7 +50,20 @@ struct RhtArgs {
   std::uint32_t chunk_vec;
   std::size_t chunk_bytes;
   int zacc_zero;                // K3 pass 1: zero the accumulators after reading them (next chunk's K2)
+  // Row-sharded K3 (q8p_forward_sharded): pass 1 over this rank's chunks only --
+  // chunks ch0 .. ch0 + p1_count, accumulator rows and pass-1 outputs indexed from
+  // row0, outputs written as [batch][p1_out_rows] (the all-gather send buffer);
+  // pass 2 reads the gathered [world][batch][mid_rows] ("rank-major") layout.
+  // in_rows: pass 1's fp32 input in the same rank-major layout.  0 = off.
+  std::uint32_t ch0, p1_count, row0, p1_out_rows, mid_rows, in_rows;
 };
+
+// Element (b, i) of a [batch][n] vector set stored rank-major with `rows` rows per
+// rank ([n / rows][batch][rows]) -- the all-gather output layout; rows % 4 == 0.
+__device__ __forceinline__ std::size_t rank_major(std::size_t b, std::uint32_t i, std::uint32_t rows, int batch,
+                                                  std::uint32_t n) {
+  return rows ? (std::size_t(i / rows) * batch + b) * rows + i % rows : b * n + i;
+}
 
 struct Team {
   std::uint32_t tid, n, bar;  // thread index in the team, team size, named barrier (0 = __syncthreads)
@@ -136,7 +149,7 @@ __device__ __forceinline__ float4 combine4(const RhtArgs& a, int b, std::uint32_
   const long long tl = __ldcg(a.tl_in + b);
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int st = 0; st < a.zstages; ++st) {
-    const std::int32_t* z = a.zacc + (std::size_t(st) * a.zcols + 4 * b) * a.zrows + i;
+    const std::int32_t* z = a.zacc + (std::size_t(st) * a.zcols + 4 * b) * a.zrows + (i - a.row0);
     const int4 v0 = __ldcg(reinterpret_cast<const int4*>(z));
     const int4 v1 = __ldcg(reinterpret_cast<const int4*>(z + a.zrows));
     const int4 v2 = __ldcg(reinterpret_cast<const int4*>(z + 2 * std::size_t(a.zrows)));
@@ -213,10 +226,11 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* sm
         for (int st = 0; st < a.zstages; ++st)
           for (int l = 0; l < 4; ++l)
             *reinterpret_cast<int4*>(const_cast<std::int32_t*>(a.zacc) +
-                                     (std::size_t(st) * a.zcols + 4 * b + l) * a.zrows + i) = make_int4(0, 0, 0, 0);
+                                     (std::size_t(st) * a.zcols + 4 * b + l) * a.zrows + (i - a.row0)) =
+                make_int4(0, 0, 0, 0);
       }
     } else {
-      val = __ldcg(reinterpret_cast<const float4*>(a.in + std::size_t(b) * a.n + i));
+      val = __ldcg(reinterpret_cast<const float4*>(a.in + rank_major(b, i, a.in_rows, a.batch, a.n)));
       ss += val.x * val.x + val.y * val.y + val.z * val.z + val.w * val.w;
       if (a.fwd) val = sign4(val, (a.signs[i >> 3] >> (i & 4)) & 0xFu);
     }
@@ -264,8 +278,10 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* sm
     cur = y;
   }
   fwht_rows<Q>(cur, a.P2, tm);
+  float* const mo = a.p1_out_rows ? a.mid + std::size_t(b) * a.p1_out_rows + (e0 - a.row0)
+                                  : a.mid + std::size_t(b) * a.n + e0;
   for (std::uint32_t v = tm.tid; v < chunk / 4; v += tm.n)
-    *reinterpret_cast<float4*>(a.mid + std::size_t(b) * a.n + e0 + 4 * v) = reinterpret_cast<float4*>(cur)[v];
+    *reinterpret_cast<float4*>(mo + 4 * v) = reinterpret_cast<float4*>(cur)[v];
   team_sync(tm);  // smem reusable by the caller
 }
 
@@ -275,7 +291,7 @@ __device__ void rht_p2_body(const RhtArgs& a, std::uint32_t cg, int b, float* sm
   const std::uint32_t col = cg * 4;         // 4 adjacent columns
   for (std::uint32_t r = tm.tid; r < a.P1; r += tm.n)
     reinterpret_cast<float4*>(sm2)[r] =
-        __ldcg(reinterpret_cast<const float4*>(a.mid + std::size_t(b) * a.n + std::size_t(r) * stride + col));
+        __ldcg(reinterpret_cast<const float4*>(a.mid + rank_major(b, r * stride + col, a.mid_rows, a.batch, a.n)));
   team_sync(tm);
   fwht_rows<4>(sm2, a.P1, tm);
   const float sc = rsqrtf(float(a.n));

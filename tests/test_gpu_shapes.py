@@ -107,3 +107,18 @@ def test_prefill_configs(dev, oracle, m, n, batch):
     want = oracle.infer(art, xs, threads=16)
     for i, b in enumerate(sample):
         assert rel_err(y[b].cpu().numpy(), want[i]) < TC, (b, rel_err(y[b].cpu().numpy(), want[i]))
+
+
+@pytest.mark.parametrize("n", [16384, 28672])
+def test_repeatable_code_ring_wrap(dev, n):
+    # Long-k layers wrap K2's shared-memory code ring several times per CTA; the
+    # same input must give the same integer accumulators every time (regression:
+    # a decoder released its ring slot before its shared-memory loads completed,
+    # and the producer's bulk copy for item i + S overwrote the slot under them).
+    art = random_artifact(4096, n, STAGES[2], n)
+    L = q8p.Layer.from_qshp(art)
+    for batch in (1, 2, 3, 5, 9, 16):
+        x = torch.randn(batch, n, generator=torch.Generator().manual_seed(batch)).to(dev)
+        z0 = L.rows_z(x)
+        for _ in range(6):
+            assert torch.equal(L.rows_z(x), z0), batch

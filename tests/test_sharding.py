@@ -163,3 +163,27 @@ def test_row_shards_on_one_gpu(world, bits):
     y_from_z = q8p.rht(z_full, torch.from_numpy(su.copy()).cuda(), transpose=True)
     rel = float((y_from_z - y).norm() / y.norm())
     assert rel < 1e-5, rel
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("m,n,bits", [(8192, 8192, 2), (28672, 8192, 2), (8192, 28672, 2), (4096, 11008, 3),
+                                      (11008, 4096, 4)])
+@pytest.mark.parametrize("batch", [1, 3])
+def test_sharded_forward_sim_bit_exact(world, m, n, bits, batch):
+    # q8p_forward_sharded's data path at G ranks on one GPU (all-gather replaced by
+    # copies): per-rank K1 -> K2 on its rows -> K3 pass 1 on its rows into the send
+    # buffer, the rank-major gather, K3 pass 2 -> y equals the unsharded forward bit
+    # for bit (70B shapes incl. base 28, the 7B MLP shapes incl. base 172).
+    import torch
+
+    import paper_2402_04396_b200 as q8p
+    from conftest import random_artifact
+
+    stages = {2: [("e8p-2bit", 1.11)], 3: [("e8p-2bit", 1.02), ("e8-1bit", 0.49)],
+              4: [("e8p-2bit", 0.97), ("e8p-2bit", 0.29)]}[bits]
+    art = random_artifact(m, n, stages, m + n + world)
+    x = torch.randn(batch, n, generator=torch.Generator().manual_seed(world + batch)).cuda()
+    full = q8p.Layer.from_qshp(art, device=0)
+    shards = [q8p.Layer.from_qshp(art, device=0, rows=q8p.shard_rows(m, world, r)) for r in range(world)]
+    assert torch.equal(q8p.forward_sharded_sim(shards, x), full.forward(x))
