@@ -317,7 +317,7 @@ def run_ours(args):
                 step(c, events=False)
     torch.cuda.synchronize()
     graphs, ev_graphs = [], []
-    use_graph = not args.no_graph and not sharded
+    use_graph = not args.no_graph  # sharded too: the NCCL all-gather captures as a graph node
     tc_path = B <= 32  # one K2 launch per forward (larger batches run in 32-vector chunks)
     if use_graph:
         # headline graphs: no event nodes (they would break the programmatic
@@ -329,14 +329,16 @@ def run_ours(args):
                 step(c, events=False)
             launches_per_step = q8p.kernel_launches() - k0  # q8p kernels captured per step
             graphs.append(g)
-            g2 = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g2, stream=stream):
-                step(c, events=True)
-            ev_graphs.append(g2)
+            if not sharded:
+                g2 = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g2, stream=stream):
+                    step(c, events=True)
+                ev_graphs.append(g2)
         torch.cuda.synchronize()
         for c in range(args.copies):
             graphs[c].replay()
-            ev_graphs[c].replay()
+            if ev_graphs:
+                ev_graphs[c].replay()
         torch.cuda.synchronize()
 
     launches0 = q8p.kernel_launches()
@@ -475,7 +477,7 @@ def run_ours(args):
     # around the whole sequence on the launching stream / launches.  The stream
     # ceiling: a plain bulk-copy read of the same code-slab bytes, same harness.
     chained, ceiling = {}, {}
-    if not sharded and tc_path:
+    if tc_path:
         reps = 5
         for li, (m, n) in enumerate(layers):
             with torch.cuda.stream(stream):
@@ -501,17 +503,25 @@ def run_ours(args):
                 t1.record(stream)
                 torch.cuda.synchronize()
                 ceiling[li] = (t0.elapsed_time(t1) / (reps * args.copies), regions[0][1])
+        if world > 1:  # per-rank kernel times: the max over ranks
+            keys = sorted(chained)
+            t = torch.tensor([chained[k] for k in keys] + [ceiling[k][0] for k in keys], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            for i, k in enumerate(keys):
+                chained[k] = float(t[i])
+                ceiling[k] = (float(t[len(keys) + i]), ceiling[k][1])
 
     # Roofline of the dominant kernel (K2) on the largest layer.
     roof = None
-    if not sharded and all(gemv_ms[li] for li in range(n_gemv)):
+    if chained or all(gemv_ms[li] for li in range(n_gemv)):
         per = []
         for li, (m, n) in enumerate(layers):
-            b = m * n // 8 * sum(CODE_BYTES[c] for c, _ in SCHEMES[args.bits]) + 4 * B * n + 4 * B * m
-            t_iso = statistics.mean(gemv_ms[li])
+            ml = m // world  # this rank's rows (row-sharded: the per-rank K2)
+            b = ml * n // 8 * sum(CODE_BYTES[c] for c, _ in SCHEMES[args.bits]) + 4 * B * n + 4 * B * ml
+            t_iso = statistics.mean(gemv_ms[li]) if gemv_ms[li] else None
             t = chained.get(li, t_iso)
-            e = {"layer": f"{m}x{n}", "bytes": b, "us": t * 1e3, "gbs": b / (t * 1e-3) / 1e9,
-                 "isolated_us": t_iso * 1e3}
+            e = {"layer": f"{m}x{n}" + (f" rows/{world}" if world > 1 else ""), "bytes": b, "us": t * 1e3,
+                 "gbs": b / (t * 1e-3) / 1e9, "isolated_us": t_iso * 1e3 if t_iso is not None else None}
             if li in ceiling:
                 cms, cb = ceiling[li]
                 e["stream_ceiling"] = {"us": cms * 1e3, "slab_bytes": cb, "gbs": cb / (cms * 1e-3) / 1e9}
@@ -525,7 +535,7 @@ def run_ours(args):
         try:  # dram bytes per launch of the same kernel from the committed ncu --set full capture
             with open(os.path.join(ROOT, "profiles", "r01", "k2_traffic.json")) as f:
                 tj = json.load(f)
-            if int(tj.get("algorithmic_bytes_per_launch", -1)) == bmax:
+            if int(tj.get("algorithmic_bytes_per_launch", -1)) == bmax and world == 1:
                 traffic = float(tj["dram_bytes_per_launch"])
         except Exception:
             traffic = None

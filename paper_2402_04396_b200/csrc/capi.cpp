@@ -491,6 +491,10 @@ void forward_sharded_impl(const q8p_layer* L, const float* x, float* y, int batc
     if (local_p1) {
       launch_rht_out_acc_local(L->side_u, w.zacc, L->num_stages, w.rows_pad, std::uint32_t(tc_ncols_pad(4 * nb)),
                                zscale, ze8p, w.alpha, w.tl, L->row_begin, ml, w.z_loc, nb, s);
+      if (world == 1) {  // a one-rank all-gather is the identity: pass 2 reads the send buffer
+        launch_rht_out_pass2_gathered(L->side_u, w.z_loc, ml, yb, nb, s);
+        continue;
+      }
       nccl_check(ncclAllGather(w.z_loc, w.z_full, std::size_t(nb) * ml, ncclFloat32, comm, s), "ncclAllGather");
       launch_rht_out_pass2_gathered(L->side_u, w.z_full, ml, yb, nb, s);
       continue;

@@ -7,5 +7,5 @@ python - gpurun_out/$TAG/bench.json <<'PY'
 import json,sys
 d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); r=d.get("roofline") or {}
 print("value", round(d["value"]), "e2e", round(d["e2e"]["value"]), "us/step", round(d["ms_per_step"]*1e3,1), "frac", round(r.get("frac",0),3))
-for p in r.get("per_layer",[]): print(p["layer"], "chained", round(p["us"],2), "iso", round(p["isolated_us"],2), "GB/s", round(p["gbs"]), "ceil_us", round((p.get("stream_ceiling") or {}).get("us",0),2))
+for p in r.get("per_layer",[]): print(p["layer"], "chained", round(p["us"],2), "iso", round(p["isolated_us"] or 0,2), "GB/s", round(p["gbs"]), "ceil_us", round((p.get("stream_ceiling") or {}).get("us",0),2))
 PY
