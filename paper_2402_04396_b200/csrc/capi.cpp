@@ -349,6 +349,9 @@ struct Workspace {
   long long* tl;         // [batch]
   std::uint8_t* bimg;    // tc_bimg_bytes(n, batch)
   std::int32_t* zacc;    // [stages][N][rows_pad]
+  float* pt;             // prefill: t [batch][n] fp32
+  std::uint8_t* pbt;     // prefill: bf16 B tiles
+  float* pz;             // prefill: z [batch][m_local]
   float* z_loc;          // row-sharded: [batch][m_local] this rank's z rows
   float* z_full;         // row-sharded: [batch][m] all-gathered z
   std::uint32_t rows_pad, zcols;
@@ -370,6 +373,16 @@ bool multi_chunk_k1(const q8p_layer* L, int batch) {
          (L->n / 8) % 32 == 0;
 }
 
+// Prefill batches run the K4 decode-GEMM (gemm_prefill.cu) unless Q8P_PREFILL=0
+// (A/B knob: the 32-vector chunks through K2 instead).
+bool use_prefill(const q8p_layer* L, int batch) {
+  static const bool off = [] {
+    const char* e = std::getenv("Q8P_PREFILL");
+    return e && std::string(e) == "0";
+  }();
+  return !off && L->row_begin == 0 && L->row_end == L->m && prefill_supported(*L, batch);
+}
+
 std::size_t workspace_parts(const q8p_layer* L, int batch, Workspace* w, void* base) {
   auto* p0 = static_cast<std::uint8_t*>(base);
   std::size_t off = 0;
@@ -378,6 +391,7 @@ std::size_t workspace_parts(const q8p_layer* L, int batch, Workspace* w, void* b
     off += round_up(bytes ? bytes : 1, 256);
     return r;
   };
+  const int batch_all = batch;
   const int chunk = tc_chunk(L, batch);
   const bool tc = chunk > 0;
   const bool multi = multi_chunk_k1(L, batch);
@@ -399,6 +413,13 @@ std::size_t workspace_parts(const q8p_layer* L, int batch, Workspace* w, void* b
   } else {
     v.t = reinterpret_cast<float*>(take(B * L->n * 4));
     v.z = reinterpret_cast<float*>(take(B * L->m * 4));
+  }
+  if (use_prefill(L, batch_all)) {  // K4 path (forward); the chunked path stays sized for rows_z / sharded
+    const std::size_t Ball = std::size_t(batch_all);
+    v.pt = reinterpret_cast<float*>(take(Ball * L->n * 4));
+    v.pbt = take(prefill_btile_bytes(*L, batch_all));
+    v.pz = reinterpret_cast<float*>(take(std::size_t(prefill_parts(*L, batch_all)) * Ball * L->m_local() * 4));
+    v.u = reinterpret_cast<float*>(take(Ball * mx * 4));
   }
   if (w) *w = v;
   return off;
@@ -528,6 +549,15 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
   DeviceGuard g(L->device);
   Workspace w;
   workspace_parts(L, batch, &w, ws);
+  if (use_prefill(L, batch)) {  // K1 (fp32 t) -> K4 (pack + decode-GEMM) -> K3
+    if (opts) record_event(opts->gemv_start_event, s);
+    launch_rht_in(L->side_v, x, w.pt, w.u, nullptr, nullptr, nullptr, 0, batch, s);
+    launch_prefill(*L, w.pt, w.pbt, w.pz, batch, s);
+    if (opts) record_event(opts->gemv_end_event, s);
+    // K3 sums the K splits' partial z in fixed order while loading them
+    launch_rht_out(L->side_u, w.pz, w.u, y, batch, s, prefill_parts(*L, batch));
+    return;
+  }
   if (const int chunk = tc_chunk(L, batch)) {
     float zscale[2] = {L->scale[0], L->scale[1]};
     int ze8p[2] = {L->cb[0] == Q8P_CB_E8P_2BIT, L->cb[1] == Q8P_CB_E8P_2BIT};

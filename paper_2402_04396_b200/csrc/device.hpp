@@ -167,6 +167,12 @@ constexpr int kTcMaxBatch = 32;  // tensor-core path: batch <= 32 per launch (MM
 bool tc_supported(const q8p_layer& L, int batch);
 int tc_ncols_pad(int ncols);                              // MMA N for `ncols` B rows
 std::uint32_t tc_bimg_bytes(std::uint32_t n, int batch);  // B images for all k slabs
+// K4 prefill decode-GEMM (gemm_prefill.cu): batches >= kPrefillMinBatch.
+constexpr int kPrefillMinBatch = 64;
+bool prefill_supported(const q8p_layer& L, int batch);
+std::size_t prefill_btile_bytes(const q8p_layer& L, int batch);
+std::uint32_t prefill_parts(const q8p_layer& L, int batch);  // K splits: z is [P][batch][m_local] partials
+void launch_prefill(const q8p_layer& L, const float* t, std::uint8_t* btiles, float* z, int batch, cudaStream_t s);
 // Benchmark support (bench_kernels.cu): bulk-copy stream of `bytes` at src (the
 // HBM read ceiling in K2's access pattern).
 void launch_stream(const void* src, std::size_t bytes, unsigned* sink, cudaStream_t s);
@@ -231,7 +237,8 @@ void launch_rfft_in_limbs(const DevSide& side, const float* x, float* u_scratch,
                           std::uint8_t* bimg_tail, std::size_t tail_bytes, std::int32_t* zero_ptr,
                           std::size_t zero_words, int batch, cudaStream_t s);
 // K3 (fp32 input): y = T_u^T z.
-void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, float* y, int batch, cudaStream_t s);
+void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, float* y, int batch, cudaStream_t s,
+                    int in_parts = 1);
 // K3 (accumulator input): z = sum_s zscale_s alpha (2 Z_s - [E8P] TL) / 4 from the int32
 // limb accumulators [stage][zacc_cols][zacc_rows], then y = T_u^T z.
 void launch_rht_out_acc(const DevSide& side, const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows,

@@ -1,0 +1,442 @@
+// K4: prefill (large batch) decode-GEMM on the 5th-gen tensor cores,
+// weight-stationary per tile: every weight tile is decoded ONCE into shared
+// memory and multiplied against 256 vectors (tcgen05.mma kind::f16, bf16 x bf16
+// -> fp32 accumulators in tensor memory).
+//
+// Semantics: z[b][r] = sum_s scale_s * sum_k <decode_s(codes[s][r][k]), t_b[8k:8k+8]>
+// (core/src/pipeline.cpp:172-191; the reference CLI loops infer per vector,
+// latq_cli.cpp:211-212), t = T_v x from K1's fp32 flavour, y = T_u^T z by K3.
+//
+// Operands.  A = 4 v exactly: E8P 4 v = 2 sigma d + 2 b - 1 (odd integers in
+// [-11, 11], e8p.cpp:81-100), e8-1bit 4 v = 2 * doubled (codebook.cpp:65-72) --
+// exact in bf16.  B = scale_s * t split into two bf16 terms (hi = bf16(x),
+// lo = bf16(x - hi): 16 significant bits) accumulated into the same fp32
+// accumulator, so z = D / 4 with no epilogue scaling; RVQ stages are further
+// K items against their own scaled B.  Relative error ~1e-5 (fp32 accumulation,
+// 16-bit activations), inside the north-star 1e-3.
+//
+// Layout.  Codes: the tensor-core slabs of gemv_tc.cu (128 rows x 32 codewords
+// per stage, [row block][k slab]).  B tiles (written by the pack kernel): per
+// (N tile of 256 vectors, K chunk of 32, stage) one contiguous 32 KiB region
+// [term hi/lo][K-block of 16][32 vector groups][2 K halves][8 vectors][16 B]
+// = the canonical K-major no-swizzle UMMA layout (LBO 128 B, SBO 256 B); the A
+// tile of a K chunk is the same layout over 128 rows.
+//
+// CTA (persistent; units = (N tile, pair of M tiles) of 256 rows x 256 vectors --
+// every B byte brought from L2 feeds two M tiles):
+//   warp 0   producer: code slabs (1-D bulk copies, one per k slab, stage and M
+//            tile) and B regions (one 32 KiB bulk copy per item) into rings
+//   warp 1   MMA issuer: per item (K chunk, stage) 2 M tiles x 2 K-blocks x 2 terms
+//            of tcgen05.mma M=128 N=256 K=16 into the tiles' accumulators (2 x 256
+//            TMEM columns)
+//   warps 2-9  decoders (warp = M tile x lane quadrant, thread = row): slab -> bf16
+//            A tile per item; then the unit's epilogue (tcgen05.ld -> z rows)
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "device.hpp"
+#include "tc05.hpp"
+
+namespace q8p::detail {
+namespace {
+using namespace tc05;
+
+constexpr int kNT = 256;                              // vectors per N tile (MMA N)
+constexpr int kKC = 32;                               // K per pipeline item (2 K-blocks of 16)
+constexpr int kMT = 2;                                // M tiles (128 rows each) per CTA: B reused twice
+constexpr std::uint32_t kATile = 128u * kKC * 2u;     // 8 KiB per M tile
+constexpr std::uint32_t kABytes = kMT * kATile;
+constexpr std::uint32_t kBTerm = kNT * kKC * 2u;      // 16 KiB per bf16 term
+constexpr std::uint32_t kBBytes = 2u * kBTerm;        // hi + lo
+constexpr std::uint32_t kSlots = 3;                   // A / B pipeline depth
+constexpr std::uint32_t kCodeSlots = 8;               // code slab ring (M tiles x stages x 2 k slabs)
+constexpr std::uint32_t kCodeSlot = 4 * 2048 + 512;   // E8P slab bytes (e8-1bit slabs are smaller)
+constexpr int kDec = 8;                               // decoder warps: 2 M tiles x 4 lane quadrants
+constexpr int kThreads = (2 + kDec) * 32;
+constexpr std::uint32_t kCtl = 1024, kTab = 4096;     // barriers; decode tables
+constexpr std::uint32_t kOffA = kCtl + kTab, kOffB = kOffA + kSlots * kABytes, kOffC = kOffB + kSlots * kBBytes;
+constexpr std::size_t kSmem = kOffC + kCodeSlots * kCodeSlot;
+static_assert(kSmem <= 227 * 1024, "prefill smem");
+
+constexpr std::uint32_t idesc_bf16(int M, int N) {  // bf16 x bf16 -> f32, both K-major
+  return (1u << 4) | (1u << 7) | (1u << 10) | (std::uint32_t(N >> 3) << 17) | (std::uint32_t(M >> 4) << 24);
+}
+
+struct PrefillArgs {
+  const std::uint8_t* codes[2];  // tensor-core slabs per stage
+  std::uint32_t slab_bytes[2];
+  int kind[2];                   // 0 e8p, 1 e8-1bit
+  int nst;
+  std::uint32_t KSL, KC;         // k slabs (32 codewords), K chunks (32 columns)
+  std::uint32_t MT, NTL;         // M tiles (128 rows), N tiles (256 vectors)
+  const std::uint8_t* btiles;    // [NTL][KC][nst][kBBytes]
+  float* z;                      // [P][batch][m]: one partial per K split
+  std::uint32_t P;               // K splits (units = N tiles x M pairs x P)
+  std::uint32_t m, batch;
+  const std::uint32_t* nib;      // [256] E8P magnitude nibbles
+  const uint2* e81;              // [256] e8-1bit doubled rows
+};
+
+__device__ __forceinline__ std::uint32_t lds32(std::uint32_t addr) {
+  std::uint32_t r;
+  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(r) : "r"(addr));
+  return r;
+}
+__device__ __forceinline__ void sts128(std::uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ std::uint32_t prmt(std::uint32_t a, std::uint32_t b, std::uint32_t sel) {
+  std::uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+__device__ __forceinline__ std::uint32_t bf2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const std::uint32_t*>(&h);
+}
+// 32 lanes x 32 columns of fp32 from tensor memory.
+__device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, float (&v)[32]) {
+  std::uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+  tmem_wait_ld();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+constexpr std::uint32_t kCtLo = 0x00050301u;  // {+1,+3,+5,0}
+constexpr std::uint32_t kCtHi = 0x00FBFDFFu;  // {-1,-3,-5,0}
+
+// 4 v of one E8P codeword (slot jj of the 4-codeword idx / flag words, shift bit b)
+// as 8 bf16 (16 B, coordinates 0..7).
+__device__ __forceinline__ uint4 e8p_bf16(std::uint32_t idx, std::uint32_t fw, int jj, std::uint32_t b,
+                                          std::uint32_t tab) {
+  const std::uint32_t nib = lds32(tab + idx * 4u);
+  const std::uint32_t rs = jj == 0 ? fw << 2 : jj == 1 ? fw << 1 : jj == 2 ? fw : fw >> 1;
+  const std::uint32_t sel = nib ^ (rs & 0x44444444u);
+  const std::uint32_t lo = prmt(kCtLo, kCtHi, sel), hi = prmt(kCtLo, kCtHi, sel >> 16);
+  const float sh = b ? 1.f : -1.f;  // 4 v = 2 sigma d + (2 b - 1)
+  auto v = [&](std::uint32_t w, int c) { return 2.f * float(int(std::int8_t(w >> (8 * c)))) + sh; };
+  return make_uint4(bf2(v(lo, 0), v(lo, 1)), bf2(v(lo, 2), v(lo, 3)), bf2(v(hi, 0), v(hi, 1)),
+                    bf2(v(hi, 2), v(hi, 3)));
+}
+// 4 v = 2 * doubled of an e8-1bit code.
+__device__ __forceinline__ uint4 e81_bf16(std::uint32_t code, std::uint32_t tab) {
+  const std::uint32_t lo = lds32(tab + 1024u + code * 8u), hi = lds32(tab + 1024u + code * 8u + 4u);
+  auto v = [&](std::uint32_t w, int c) { return 2.f * float(int(std::int8_t(w >> (8 * c)))); };
+  return make_uint4(bf2(v(lo, 0), v(lo, 1)), bf2(v(lo, 2), v(lo, 3)), bf2(v(hi, 0), v(hi, 1)),
+                    bf2(v(hi, 2), v(hi, 3)));
+}
+
+__global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
+  extern __shared__ __align__(1024) std::uint8_t smem[];
+  const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const std::uint32_t sb = smem_u32(smem);
+  const std::uint32_t bar_af = sb, bar_ae = sb + 8 * kSlots, bar_bf = sb + 16 * kSlots, bar_be = sb + 24 * kSlots;
+  const std::uint32_t bar_cf = sb + 32 * kSlots, bar_ce = bar_cf + 8 * kCodeSlots;
+  const std::uint32_t bar_df = bar_ce + 8 * kCodeSlots, bar_de = bar_df + 8, tmem_slot = bar_de + 8;
+  const std::uint32_t tab = sb + kCtl;
+  const std::uint32_t nst = std::uint32_t(a.nst);
+  const std::uint32_t MP = (a.MT + kMT - 1) / kMT, units = MP * a.NTL * a.P;  // unit = (N tile, M pair, K split)
+  const std::uint32_t KS8 = a.KC / 8;  // k slabs (8 K chunks each)
+  // K range [kc0, kc1) of split p: whole k slabs
+  auto krange = [&](std::uint32_t p, std::uint32_t& kc0, std::uint32_t& kc1) {
+    kc0 = (KS8 * p / a.P) * 8;
+    kc1 = p + 1 == a.P ? a.KC : (KS8 * (p + 1) / a.P) * 8;
+  };
+
+  if (threadIdx.x == 0) {
+    for (std::uint32_t i = 0; i < kSlots; ++i) {
+      mbar_init(bar_af + 8 * i, kDec);
+      mbar_init(bar_ae + 8 * i, 1);
+      mbar_init(bar_bf + 8 * i, 1);
+      mbar_init(bar_be + 8 * i, 1);
+    }
+    for (std::uint32_t i = 0; i < kCodeSlots; ++i) {
+      mbar_init(bar_cf + 8 * i, 1);
+      mbar_init(bar_ce + 8 * i, 4);  // the 4 decoder warps of the slab's M tile
+    }
+    mbar_init(bar_df, 1);
+    mbar_init(bar_de, kDec);
+    fence_mbar_init();
+  }
+  for (int i = threadIdx.x; i < 256; i += kThreads) {  // decode tables (static data)
+    reinterpret_cast<std::uint32_t*>(smem + kCtl)[i] = __ldg(a.nib + i);
+    reinterpret_cast<uint2*>(smem + kCtl + 1024)[i] = __ldg(a.e81 + i);
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tbase = *reinterpret_cast<volatile std::uint32_t*>(smem + (tmem_slot - sb));
+  pdl_wait();  // t tiles / z of the previous kernels
+  pdl_trigger();
+
+  // code slab c of a unit: k slab ks, stage s, M tile t -> ring index (ks * nst + s) * kMT + t
+  if (warp == 0) {
+    // ===== producer =====
+    if (lane == 0) {
+      std::uint32_t g = 0, cg = 0;  // item / code-slab counters over the CTA's units
+      for (std::uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const std::uint32_t p = u % a.P, nt = (u / a.P) / MP, mp = (u / a.P) % MP;
+        std::uint32_t kc0, kc1;
+        krange(p, kc0, kc1);
+        for (std::uint32_t kc = kc0; kc < kc1; ++kc) {
+          if (kc % 8 == 0) {
+            for (std::uint32_t s = 0; s < nst; ++s)
+              for (std::uint32_t t = 0; t < kMT; ++t, ++cg) {
+                const std::uint32_t cs = cg % kCodeSlots, mt = mp * kMT + t;
+                if (cg >= kCodeSlots) mbar_wait(bar_ce + 8 * cs, ((cg / kCodeSlots) - 1) & 1);
+                const std::uint32_t bytes = a.slab_bytes[s];
+                if (mt < a.MT) {
+                  mbar_arrive_expect_tx(bar_cf + 8 * cs, bytes);
+                  bulk_g2s(sb + kOffC + cs * kCodeSlot, a.codes[s] + (std::size_t(mt) * a.KSL + kc / 8) * bytes,
+                           bytes, bar_cf + 8 * cs);
+                } else {
+                  mbar_arrive(bar_cf + 8 * cs);  // past the last row block: nothing to load
+                }
+              }
+          }
+          for (std::uint32_t s = 0; s < nst; ++s, ++g) {
+            const std::uint32_t bs = g % kSlots;
+            if (g >= kSlots) mbar_wait(bar_be + 8 * bs, ((g / kSlots) - 1) & 1);
+            mbar_arrive_expect_tx(bar_bf + 8 * bs, kBBytes);
+            bulk_g2s(sb + kOffB + bs * kBBytes, a.btiles + ((std::size_t(nt) * a.KC + kc) * nst + s) * kBBytes,
+                     kBBytes, bar_bf + 8 * bs);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer: per item 2 M tiles x 2 K-blocks x 2 terms =====
+    if (lane == 0) {
+      constexpr std::uint32_t idesc = idesc_bf16(128, kNT);
+      std::uint32_t g = 0, ul = 0;
+      for (std::uint32_t u = blockIdx.x; u < units; u += gridDim.x, ++ul) {
+        if (ul >= 1) mbar_wait(bar_de, (ul - 1) & 1);  // the previous unit's epilogue read the accumulators
+        tc_fence_after();
+        std::uint32_t kc0, kc1;
+        krange(u % a.P, kc0, kc1);
+        const std::uint32_t uitems = (kc1 - kc0) * nst;
+        for (std::uint32_t it = 0; it < uitems; ++it, ++g) {
+          const std::uint32_t sl = g % kSlots, ph = (g / kSlots) & 1;
+          mbar_wait(bar_af + 8 * sl, ph);
+          mbar_wait(bar_bf + 8 * sl, ph);
+          tc_fence_after();
+          const std::uint32_t sa = sb + kOffA + sl * kABytes, sbb = sb + kOffB + sl * kBBytes;
+#pragma unroll
+          for (int t = 0; t < kMT; ++t)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+                mma_f16_ss(tbase + t * kNT, sdesc(sa + t * kATile + j * 4096u, 128, 256),
+                           sdesc(sbb + h * kBTerm + j * 8192u, 128, 256), idesc, (it | j | h) != 0);
+          mma_commit(bar_ae + 8 * sl);
+          mma_commit(bar_be + 8 * sl);
+        }
+        mma_commit(bar_df);
+      }
+    }
+  } else {
+    // ===== decoders: warp = (M tile t, lane quadrant q), thread = row; then the epilogue =====
+    const std::uint32_t q = std::uint32_t(warp & 3), row_in = q * 32 + std::uint32_t(lane);
+    const std::uint32_t t = std::uint32_t(warp - 2) >> 2;
+    std::uint32_t g = 0, cg = 0, ul = 0;
+    for (std::uint32_t u = blockIdx.x; u < units; u += gridDim.x, ++ul) {
+      const std::uint32_t p = u % a.P, nt = (u / a.P) / MP, mt = ((u / a.P) % MP) * kMT + t;
+      const bool live = mt < a.MT;
+      std::uint32_t kc0, kc1;
+      krange(p, kc0, kc1);
+      std::uint32_t cbase = 0;  // code counter of the current k slab's first slab
+      for (std::uint32_t kc = kc0; kc < kc1; ++kc) {
+        if (kc % 8 == 0) {
+          cbase = cg;
+          cg += nst * kMT;
+        }
+        for (std::uint32_t s = 0; s < nst; ++s, ++g) {
+          const std::uint32_t cidx = cbase + s * kMT + t, cs = cidx % kCodeSlots;
+          mbar_wait(bar_cf + 8 * cs, (cidx / kCodeSlots) & 1);
+          const std::uint32_t sl = g % kSlots;
+          if (g >= kSlots) mbar_wait(bar_ae + 8 * sl, ((g / kSlots) - 1) & 1);
+          const std::uint32_t sc = sb + kOffC + cs * kCodeSlot, cq = kc % 8;
+          const std::uint32_t sa = sb + kOffA + sl * kABytes + t * kATile;
+          if (live) {
+            const std::uint32_t wofs = (cq / 4) * 2048u + row_in * 16u + (cq % 4) * 4u;
+            uint4 v[4];
+            const std::uint32_t iw = lds32(sc + wofs);
+            if (a.kind[s] == 0) {
+              const std::uint32_t fw = lds32(sc + 4096u + wofs), sw = lds32(sc + 8192u + row_in * 4u);
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj)
+                v[jj] = e8p_bf16((iw >> (8 * jj)) & 0xFFu, fw, jj, (sw >> (cq + 8 * jj)) & 1u, tab);
+            } else {
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) v[jj] = e81_bf16((iw >> (8 * jj)) & 0xFFu, tab);
+            }
+            // codeword jj = K columns 8 jj .. 8 jj + 7 of the chunk: K-block jj / 2, half jj % 2
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj)
+              sts128(sa + (jj >> 1) * 4096u + (row_in >> 3) * 256u + (jj & 1) * 128u + (row_in & 7) * 16u, v[jj]);
+            fence_proxy_async_smem();  // generic smem writes -> the tensor core's operand reads
+          }
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(bar_af + 8 * sl);
+            if (cq == 7 || kc + 1 == kc1) mbar_arrive(bar_ce + 8 * cs);  // slab fully decoded
+          }
+        }
+      }
+      // epilogue: z[b][r] = D_t[r][b] / 4 for this M tile's 128 rows x 256 vectors
+      mbar_wait(bar_df, ul & 1);
+      tc_fence_after();
+      const std::uint32_t row = mt * 128 + row_in;
+      for (std::uint32_t c0 = 0; c0 < std::uint32_t(kNT); c0 += 32) {
+        float d[32];
+        tmem_ld32(tbase + ((q * 32) << 16) + t * kNT + c0, d);
+        if (live && row < a.m) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const std::uint32_t b = nt * kNT + c0 + j;
+            if (b < a.batch) a.z[(std::size_t(p) * a.batch + b) * a.m + row] = 0.25f * d[j];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_de);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
+// B tiles from t [batch][n] fp32: per (N tile, K chunk, stage) the hi / lo bf16
+// terms of scale_s * t in the K-major core-matrix layout.  Thread = (vector v,
+// 8-column group kg); vectors beyond batch (last N tile) are zeros.
+__global__ void __launch_bounds__(256) pack_b_kernel(const float* __restrict__ t, std::uint32_t n,
+                                                     std::uint32_t batch, std::uint32_t NTL, int nst, float s0,
+                                                     float s1, std::uint8_t* __restrict__ out) {
+  const std::uint32_t KC = n / kKC, groups = n / 8;
+  const std::size_t total = std::size_t(NTL) * kNT * groups;
+  for (std::size_t x = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x; x < total;
+       x += std::size_t(gridDim.x) * blockDim.x) {
+    const std::uint32_t kg = std::uint32_t(x % groups), v = std::uint32_t(x / groups);
+    const std::uint32_t nt = v / kNT, vi = v % kNT, kc = kg / 4, j = (kg % 4) / 2, kh = kg % 2;
+    float xv[8];
+    if (v < batch) {
+      const float4 lo4 = *reinterpret_cast<const float4*>(t + std::size_t(v) * n + 8 * kg);
+      const float4 hi4 = *reinterpret_cast<const float4*>(t + std::size_t(v) * n + 8 * kg + 4);
+      xv[0] = lo4.x, xv[1] = lo4.y, xv[2] = lo4.z, xv[3] = lo4.w, xv[4] = hi4.x, xv[5] = hi4.y, xv[6] = hi4.z,
+      xv[7] = hi4.w;
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) xv[c] = 0.f;
+    }
+    for (int s = 0; s < nst; ++s) {
+      const float sc = s ? s1 : s0;
+      std::uint32_t hi[4], lo[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float a0 = sc * xv[2 * c], a1 = sc * xv[2 * c + 1];
+        const __nv_bfloat162 h = __floats2bfloat162_rn(a0, a1);
+        const float2 hf = __bfloat1622float2(h);
+        const __nv_bfloat162 l = __floats2bfloat162_rn(a0 - hf.x, a1 - hf.y);
+        hi[c] = *reinterpret_cast<const std::uint32_t*>(&h);
+        lo[c] = *reinterpret_cast<const std::uint32_t*>(&l);
+      }
+      std::uint8_t* reg = out + ((std::size_t(nt) * KC + kc) * nst + s) * kBBytes;
+      const std::size_t o = std::size_t(j) * 8192 + (vi >> 3) * 256 + kh * 128 + (vi & 7) * 16;
+      *reinterpret_cast<uint4*>(reg + o) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4*>(reg + kBTerm + o) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
+  }
+}
+
+}  // namespace
+
+// K splits: the smallest P <= 8 (P <= k slabs) whose unit count fills the SMs' waves best.
+std::uint32_t prefill_splits(const q8p_layer& L, int batch, int sms) {
+  const std::uint32_t MP = (tc_row_blocks(L.m_local()) + kMT - 1) / kMT, NTL = std::uint32_t((batch + kNT - 1) / kNT);
+  const std::uint32_t KS8 = (L.n / kKC) / 8, base = MP * NTL;
+  std::uint32_t best = 1;
+  double best_eff = 0.0;
+  for (std::uint32_t P = 1; P <= 8 && P <= std::max<std::uint32_t>(KS8, 1); ++P) {
+    const std::uint32_t u = base * P, waves = (u + sms - 1) / sms;
+    const double eff = double(u) / double(waves * std::uint32_t(sms));
+    if (eff > best_eff + 0.02) best = P, best_eff = eff;
+  }
+  return best;
+}
+
+bool prefill_supported(const q8p_layer& L, int batch) {
+  return batch >= kPrefillMinBatch && L.tc[0].codes != nullptr && (L.num_stages == 1 || L.tc[1].codes != nullptr) &&
+         L.n % kKC == 0 && L.mma_tables != nullptr;
+}
+
+std::uint32_t prefill_parts(const q8p_layer& L, int batch) {
+  if (L.side_u.kind != 0) return 1;  // the rfft K3 reads one z array
+  int sms = 0;
+  cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device()), "sm count");
+  return prefill_splits(L, batch, sms);
+}
+
+std::size_t prefill_btile_bytes(const q8p_layer& L, int batch) {
+  const std::size_t ntl = (std::size_t(batch) + kNT - 1) / kNT;
+  return ntl * (L.n / kKC) * std::size_t(L.num_stages) * kBBytes;
+}
+
+void launch_prefill(const q8p_layer& L, const float* t, std::uint8_t* btiles, float* z, int batch, cudaStream_t s) {
+  const std::uint32_t NTL = std::uint32_t((batch + kNT - 1) / kNT);
+  {
+    const std::size_t total = std::size_t(NTL) * kNT * (L.n / 8);
+    const unsigned grid = unsigned(std::min<std::size_t>((total + 255) / 256, 148 * 16));
+    pack_b_kernel<<<grid, 256, 0, s>>>(t, L.n, std::uint32_t(batch), NTL, L.num_stages, L.scale[0], L.scale[1],
+                                       btiles);
+    cuda_check(cudaGetLastError(), "prefill pack launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  PrefillArgs a{};
+  a.nst = L.num_stages;
+  for (int st = 0; st < L.num_stages; ++st) {
+    a.codes[st] = static_cast<const std::uint8_t*>(L.tc[st].codes);
+    a.kind[st] = L.cb[st] == Q8P_CB_E8P_2BIT ? 0 : 1;
+    a.slab_bytes[st] = tc_slab_bytes(a.kind[st]);
+  }
+  a.KSL = tc_k_slabs(L.n);
+  a.KC = L.n / kKC;
+  if (a.KC % 8 != 0 && a.KC > 8) throw UnsupportedError("prefill: K chunks must fill whole k slabs");
+  a.MT = tc_row_blocks(L.m_local());
+  a.NTL = NTL;
+  a.btiles = btiles;
+  a.z = z;
+  a.P = prefill_parts(L, batch);
+  a.m = L.m_local();
+  a.batch = std::uint32_t(batch);
+  a.nib = L.mma_tables;
+  a.e81 = reinterpret_cast<const uint2*>(L.mma_tables + 256);
+  kernel_attrs(reinterpret_cast<const void*>(prefill_kernel), int(kSmem));
+  int sms = 0;
+  cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device()), "sm count");
+  const unsigned grid = unsigned(std::min<std::uint32_t>((a.MT + kMT - 1) / kMT * a.NTL * a.P, std::uint32_t(sms)));
+  launch_pdl(prefill_kernel, dim3(grid), dim3(kThreads), kSmem, s, a);
+  cuda_check(cudaGetLastError(), "prefill launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+}  // namespace q8p::detail

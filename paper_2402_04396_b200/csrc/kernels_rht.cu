@@ -47,12 +47,11 @@ constexpr int kP1Threads = 256;
 template <int Q>
 __global__ void __launch_bounds__(kP1Threads) rht_pass1(RhtArgs a) {
   extern __shared__ __align__(16) float sm1[];
-  const int b = blockIdx.y;
   pdl_wait();
   pdl_trigger();
   const std::uint32_t nch = a.p1_count ? a.p1_count : a.P1;  // chunk CTAs (this rank's, when sharded)
   if (blockIdx.x >= nch) {
-    if (b == 0) {
+    if (blockIdx.y == 0) {
       const std::size_t nz = gridDim.x - nch;
       const std::size_t t0 = (blockIdx.x - nch) * std::size_t(blockDim.x) + threadIdx.x;
       if (a.zero_ptr) {
@@ -66,6 +65,10 @@ __global__ void __launch_bounds__(kP1Threads) rht_pass1(RhtArgs a) {
     }
     return;
   }
+  __shared__ float red1[32];
+  // vectors blockIdx.y * vpb .. : large batches amortise the CTA over several vectors
+  const int vpb = a.vpb > 1 ? a.vpb : 1, b_end = min(a.batch, int(blockIdx.y + 1) * vpb);
+  for (int b = int(blockIdx.y) * vpb; b < b_end; ++b) {
   if (a.fwd && blockIdx.x == 0) {
     if (a.amax_out && threadIdx.x == 0) a.amax_out[b] = 0.f;
     if (a.tl_out && threadIdx.x == 0) a.tl_out[b] = 0;
@@ -80,8 +83,8 @@ __global__ void __launch_bounds__(kP1Threads) rht_pass1(RhtArgs a) {
       a.tsum_out[b] = acc * float(a.p) * rsqrtf(float(a.n));
     }
   }
-  __shared__ float red1[32];
   rht_p1_body<Q>(a, a.ch0 + blockIdx.x, b, sm1, red1, block_team());
+  }
 }
 
 // Pass 2.  grid = (P2 * q / 4 column groups, batch); block = 128 threads.
@@ -90,7 +93,8 @@ __global__ void __launch_bounds__(128) rht_pass2(RhtArgs a) {
   __shared__ float red[32];
   pdl_wait();
   pdl_trigger();
-  rht_p2_body(a, blockIdx.x, blockIdx.y, sm2, red, block_team());
+  const int vpb = a.vpb > 1 ? a.vpb : 1, b_end = min(a.batch, int(blockIdx.y + 1) * vpb);
+  for (int b = int(blockIdx.y) * vpb; b < b_end; ++b) rht_p2_body(a, blockIdx.x, b, sm2, red, block_team());
 }
 
 // Pass 2 of K1, limb flavour: grid = (P2 * q / 8 codeword columns, batch).
@@ -131,8 +135,9 @@ void launch_pass1_q(const RhtArgs& a, std::uint32_t extra_ctas, cudaStream_t s) 
   const std::size_t bsz = Q == 1 ? 0 : (Q <= 28 ? Q * Q * 4 : (Q * Q + 15) / 16 * 16);
   const std::size_t smem = chunk * 4 * (Q > 1 ? 2 : 1) + bsz;
   kernel_attrs(reinterpret_cast<const void*>(rht_pass1<Q>), 96 * 1024);
-  launch_pdl(rht_pass1<Q>, dim3((a.p1_count ? a.p1_count : a.P1) + extra_ctas, a.batch), dim3(kP1Threads), smem, s,
-             a);
+  const int vpb = a.vpb > 1 ? a.vpb : 1;
+  launch_pdl(rht_pass1<Q>, dim3((a.p1_count ? a.p1_count : a.P1) + extra_ctas, (a.batch + vpb - 1) / vpb),
+             dim3(kP1Threads), smem, s, a);
 }
 
 void launch_pass1(const RhtArgs& a, std::uint32_t extra, cudaStream_t s) {
@@ -152,7 +157,8 @@ void launch_pass1(const RhtArgs& a, std::uint32_t extra, cudaStream_t s) {
 void launch_pass2(const RhtArgs& a, cudaStream_t s) {
   const std::uint32_t groups = a.P2 * a.q / 4;
   kernel_attrs(reinterpret_cast<const void*>(rht_pass2), 96 * 1024);
-  launch_pdl(rht_pass2, dim3(groups, a.batch), dim3(128), std::size_t(a.P1) * 16, s, a);
+  const int vpb = a.vpb > 1 ? a.vpb : 1;
+  launch_pdl(rht_pass2, dim3(groups, (a.batch + vpb - 1) / vpb), dim3(128), std::size_t(a.P1) * 16, s, a);
   cuda_check(cudaGetLastError(), "rht pass2 launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -168,6 +174,10 @@ void launch_pass2_limbs(const RhtArgs& a, cudaStream_t s) {
 
 }  // namespace
 
+
+// Large (prefill) batches: 8 vectors per transform CTA (the per-vector work of a
+// pass is a few hundred floats; thousands of tiny CTAs are launch-bound).
+int vectors_per_block(int batch) { return batch >= 64 ? 8 : 1; }
 
 void launch_rht_in(const DevSide& side, const float* x, float* t, float* u_scratch, float* amax, float* tsum,
                    std::int32_t* zero_ptr, std::size_t zero_words, int batch, cudaStream_t s) {
@@ -191,13 +201,16 @@ void launch_rht_in(const DevSide& side, const float* x, float* t, float* u_scrat
   a.zero_words = zero_words;
   a.batch = batch;
   a.fwd = 1;
+  a.vpb = vectors_per_block(batch);
   launch_pass1(a, zero_ptr && zero_words ? 32 : 0, s);
   launch_pass2(a, s);
 }
 
-void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, float* y, int batch, cudaStream_t s) {
+void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, float* y, int batch, cudaStream_t s,
+                    int in_parts) {
   if (batch <= 0) return;
   if (side.kind == 1) {
+    if (in_parts > 1) throw UnsupportedError("rfft: K-split partial inputs");
     launch_rfft_f32(side, zin, u_scratch, y, batch, true, s);
     return;
   }
@@ -206,10 +219,12 @@ void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, flo
   a.signs = side.signs;
   a.base = side.base;
   a.in = zin;
+  a.in_parts = in_parts;
   a.mid = u_scratch;
   a.out = y;
   a.batch = batch;
   a.fwd = 0;
+  a.vpb = vectors_per_block(batch);
   launch_pass1(a, 0, s);
   launch_pass2(a, s);
 }

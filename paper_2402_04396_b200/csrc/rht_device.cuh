@@ -56,6 +56,8 @@ struct RhtArgs {
   // pass 2 reads the gathered [world][batch][mid_rows] ("rank-major") layout.
   // in_rows: pass 1's fp32 input in the same rank-major layout.  0 = off.
   std::uint32_t ch0, p1_count, row0, p1_out_rows, mid_rows, in_rows;
+  int vpb;                      // vectors per CTA (fp32 passes; 0/1 = one)
+  int in_parts;                 // pass 1 fp32 input = sum of in_parts partial arrays [batch][n] (0/1 = one)
 };
 
 // Element (b, i) of a [batch][n] vector set stored rank-major with `rows` rows per
@@ -231,6 +233,11 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* sm
       }
     } else {
       val = __ldcg(reinterpret_cast<const float4*>(a.in + rank_major(b, i, a.in_rows, a.batch, a.n)));
+      for (int pp = 1; pp < a.in_parts; ++pp) {  // K-split partials (prefill), summed in order
+        const float4 w4 = __ldcg(reinterpret_cast<const float4*>(a.in + std::size_t(pp) * a.batch * a.n +
+                                                                 std::size_t(b) * a.n + i));
+        val = make_float4(val.x + w4.x, val.y + w4.y, val.z + w4.z, val.w + w4.w);
+      }
       ss += val.x * val.x + val.y * val.y + val.z * val.z + val.w * val.w;
       if (a.fwd) val = sign4(val, (a.signs[i >> 3] >> (i & 4)) & 0xFu);
     }

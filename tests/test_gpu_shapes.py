@@ -13,6 +13,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 TC = 1e-5    # tensor-core path: 25-bit integer activations (see test_gpu_parity.py)
+PREFILL = 1e-4  # K4 prefill (batch >= 64): bf16 hi/lo activations (16 bits), fp32 tensor-core accumulation
 TOL = 1e-3   # portable fp32 path / north-star bar
 
 STAGES = {2: [("e8p-2bit", 1.11)], 3: [("e8p-2bit", 1.02), ("e8-1bit", 0.49)],
@@ -34,7 +35,7 @@ def test_batches_vs_oracle(dev, oracle, bits, batch):
     x = np.random.default_rng(batch).standard_normal((batch, n)).astype(np.float32).astype(np.float64)
     want = oracle.infer(art, x, threads=8)
     got = L.forward(torch.from_numpy(x.astype(np.float32)).to(dev)).cpu().numpy()
-    bar = TC  # batches 17..32 run with MMA N = 128; above 32 as 32-vector chunks (one K1 when whole)
+    bar = TC if batch < 64 else PREFILL  # batches 17..32: MMA N = 128; 33..63: 32-vector chunks; >= 64: K4
     for b in range(batch):
         assert rel_err(got[b], want[b]) < bar, (b, rel_err(got[b], want[b]))
 
@@ -55,7 +56,7 @@ def test_batched_equals_single_all_variants(dev):
     art = random_artifact(512, 1024, STAGES[3], 5)
     L = q8p.Layer.from_qshp(art)
     x = torch.randn(96, 1024, generator=torch.Generator().manual_seed(1)).to(dev)
-    for batch in (2, 4, 8, 16, 20, 32, 64, 96):  # 64 / 96: one K1 for all chunks
+    for batch in (2, 4, 8, 16, 20, 32, 40):  # tensor-core GEMV variants and the 32-vector chunks
         y = L.forward(x[:batch].contiguous())
         for b in (0, batch - 1):
             assert torch.equal(y[b], L.forward(x[b:b + 1].contiguous())[0])
@@ -70,8 +71,9 @@ def test_large_layer_all_batch_variants(dev, oracle, batch):
     x = np.random.default_rng(batch).standard_normal((batch, n)).astype(np.float32).astype(np.float64)
     want = oracle.infer(art, x, threads=16)
     got = L.forward(torch.from_numpy(x.astype(np.float32)).to(dev)).cpu().numpy()
+    bar = TC if batch < 64 else PREFILL
     for b in range(batch):
-        assert rel_err(got[b], want[b]) < TC, (b, rel_err(got[b], want[b]))
+        assert rel_err(got[b], want[b]) < bar, (b, rel_err(got[b], want[b]))
 
 
 @pytest.mark.parametrize("bits", [3, 4])
@@ -91,22 +93,22 @@ def test_rvq_big_shapes_vs_oracle(dev, oracle, m, n, bits):
 @pytest.mark.parametrize("m,n,batch", [(8192, 8192, 1024), (8192, 8192, 2048), (28672, 8192, 1024),
                                        (28672, 8192, 2048)])
 def test_prefill_configs(dev, oracle, m, n, batch):
-    # BASELINE configs[4] (prefill batch 128-2048) at the 70B shapes: every sampled
-    # row of the batched call equals the single-vector call bit for bit (per-vector
-    # activation scales, exact integer accumulation), and sampled rows match the oracle.
+    # BASELINE configs[4] (prefill batch 128-2048) at the 70B shapes through K4:
+    # sampled rows match the oracle (and the batch-1 tensor-core GEMV) within the
+    # prefill bar, and a repeated call gives the same bits.
     art = random_artifact(m, n, STAGES[2], m + batch)
     L = q8p.Layer.from_qshp(art)
     x = torch.randn(batch, n, generator=torch.Generator().manual_seed(batch)).to(dev)
     y = L.forward(x)
     assert y.shape == (batch, m) and bool(torch.isfinite(y).all())
-    rows = [0, 1, 31, 32, 511, batch // 2 + 7, batch - 33, batch - 1]
-    for b in rows:
-        assert torch.equal(y[b], L.forward(x[b:b + 1].contiguous())[0]), b
+    assert torch.equal(L.forward(x), y)
+    for b in [0, 255, 256, batch - 1]:
+        assert rel_err(y[b].cpu().numpy(), L.forward(x[b:b + 1].contiguous())[0].cpu().numpy()) < PREFILL, b
     sample = [0, batch // 2 + 7, batch - 1]
     xs = x[sample].cpu().numpy().astype(np.float64)
     want = oracle.infer(art, xs, threads=16)
     for i, b in enumerate(sample):
-        assert rel_err(y[b].cpu().numpy(), want[i]) < TC, (b, rel_err(y[b].cpu().numpy(), want[i]))
+        assert rel_err(y[b].cpu().numpy(), want[i]) < PREFILL, (b, rel_err(y[b].cpu().numpy(), want[i]))
 
 
 @pytest.mark.parametrize("n", [16384, 28672])
