@@ -270,7 +270,11 @@ def run_ours(args):
         comm = q8p.NcclComm(bytes(uid.cpu().numpy()), world, rank, local)
 
     # `copies` full copies of the layer set (distinct device buffers) rotate so
-    # every step streams its codes from HBM: 4 x 134.6 MB (70B set, 2 bits) >= 4x L2.
+    # every step streams its codes from HBM: at least 4x the L2 capacity of codes
+    # (70B set, 2 bits: 4 x 134.6 MB; 7B set: 10 copies; one 4096^2 layer: 120).
+    set_code_bytes = sum(m * n // 8 * sum(CODE_BYTES[c] for c, _ in SCHEMES[args.bits]) for m, n in layers)
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    args.copies = max(args.copies, -(-4 * l2_bytes // set_code_bytes))
     copies = []
     if args.codes == "gaussian":
         arts = [make_artifact_gaussian(m, n, 1000 + i, bits=args.bits) for i, (m, n) in enumerate(layers)]
@@ -549,6 +553,26 @@ def run_ours(args):
                 "stream_ceiling": dom[0].get("stream_ceiling"),
                 "per_layer": per, "gemv_share_of_step": (tot_t * 1e3) / ms}
 
+    if B >= 64 and all(gemv_ms[li] for li in range(n_gemv)):  # prefill: the K4 decode-GEMM is tensor-bound
+        tf_peak = None
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                tf_peak = float(json.load(f)["bf16_tflops"])
+        except Exception:
+            tf_peak = 2250.0
+        per = []
+        for li, (m, n) in enumerate(layers):
+            t = statistics.mean(gemv_ms[li]) * 1e-3
+            fl = 2.0 * m * n * B  # one effective matrix; the MMAs issued are 2x (bf16 hi/lo)
+            per.append({"layer": f"{m}x{n}", "flops": fl, "us": t * 1e6, "tflops": fl / t / 1e12,
+                        "tflops_issued": 2 * fl * sum(1 for _ in SCHEMES[args.bits]) / t / 1e12})
+        dom = max(per, key=lambda p: p["flops"])
+        roof = {"bound": "tensor", "achieved": dom["tflops"], "peak": tf_peak, "unit": "TFLOP/s",
+                "frac": dom["tflops"] / tf_peak, "traffic": None,
+                "kernel": f"q8p prefill decode-GEMM (pack + K4) on {dom['layer']} at batch {B}: 2 m n B flops / "
+                          f"mean CUDA-event duration (tflops_issued counts the bf16 hi/lo MMAs actually run)",
+                "per_layer": per}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
@@ -575,7 +599,7 @@ def run_ours(args):
                        "layers": [f"{m}x{n}" for m, n in layers],
                        "parallelism": f"row-shard tp{world}" if world > 1 else "single-gpu",
                        "l2": f"{args.copies} rotating copies of the layer set (distinct buffers, "
-                             f"{args.copies * sum(m * n // 4 for m, n in layers) / 1e6:.0f} MB of codes vs 126 MB L2)",
+                             f"{args.copies * set_code_bytes / 1e6:.0f} MB of codes >= 4x the {l2_bytes / 1e6:.0f} MB L2)",
                        "codes": (f"synthetic Gaussian W quantized by the reference H = I route on the GPU "
                                  f"(q8p.produce_artifact), default_scheme({args.bits})" if args.codes == "gaussian" else
                                  f"uniform-random codes, default_scheme({args.bits}) stages (perf variant, "

@@ -550,8 +550,8 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
   Workspace w;
   workspace_parts(L, batch, &w, ws);
   if (use_prefill(L, batch)) {  // K1 (fp32 t) -> K4 (pack + decode-GEMM) -> K3
-    if (opts) record_event(opts->gemv_start_event, s);
     launch_rht_in(L->side_v, x, w.pt, w.u, nullptr, nullptr, nullptr, 0, batch, s);
+    if (opts) record_event(opts->gemv_start_event, s);  // the events bracket pack + K4
     launch_prefill(*L, w.pt, w.pbt, w.pz, batch, s);
     if (opts) record_event(opts->gemv_end_event, s);
     // K3 sums the K splits' partial z in fixed order while loading them
@@ -881,7 +881,7 @@ void forward_set_host_impl(const q8p_layer* const* layers, int count, const floa
       const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
       cudaGraphDestroy(graph);
       cuda_check(ie, "graph instantiate");
-      if (g_set_graphs.size() >= 16) {  // bounded: evict the oldest
+      if (g_set_graphs.size() >= 256) {  // bounded (a model's layer sets x rotating copies): evict the oldest
         cudaGraphExecDestroy(g_set_graphs.front().exec);
         g_set_graphs.erase(g_set_graphs.begin());
       }
