@@ -537,7 +537,7 @@ def run_ours(args):
         achieved = bmax / (dom_us * 1e-6) / 1e9
         traffic = None
         try:  # dram bytes per launch of the same kernel from the committed ncu --set full capture
-            with open(os.path.join(ROOT, "profiles", "r01", "k2_traffic.json")) as f:
+            with open(os.path.join(ROOT, "profiles", "r02", "k2_traffic.json")) as f:
                 tj = json.load(f)
             if int(tj.get("algorithmic_bytes_per_launch", -1)) == bmax and world == 1:
                 traffic = float(tj["dram_bytes_per_launch"])
