@@ -370,16 +370,20 @@ __global__ void __launch_bounds__(256) pack_b_kernel(const float* __restrict__ t
 
 }  // namespace
 
-// K splits: the smallest P <= 8 (P <= k slabs) whose unit count fills the SMs' waves best.
+// K splits P <= 8 (whole k slabs per split) minimising a two-term cost: the
+// GEMM's critical path (waves of units x the longest split's K chunks, ~0.93 us
+// per chunk and stage, measured on 28672 x 8192) plus the (P - 1) extra partial
+// z arrays K4 writes and K3 reads back (8 B per vector-row at ~6.5 TB/s).
 std::uint32_t prefill_splits(const q8p_layer& L, int batch, int sms) {
   const std::uint32_t MP = (tc_row_blocks(L.m_local()) + kMT - 1) / kMT, NTL = std::uint32_t((batch + kNT - 1) / kNT);
-  const std::uint32_t KS8 = (L.n / kKC) / 8, base = MP * NTL;
+  const std::uint32_t KS8 = std::max<std::uint32_t>((L.n / kKC) / 8, 1), base = MP * NTL;
+  const double chunk_us = 0.93 * L.num_stages, part_us = 8.0 * batch * L.m_local() / 6.5e6;
   std::uint32_t best = 1;
-  double best_eff = 0.0;
-  for (std::uint32_t P = 1; P <= 8 && P <= std::max<std::uint32_t>(KS8, 1); ++P) {
-    const std::uint32_t u = base * P, waves = (u + sms - 1) / sms;
-    const double eff = double(u) / double(waves * std::uint32_t(sms));
-    if (eff > best_eff + 0.02) best = P, best_eff = eff;
+  double best_t = 0.0;
+  for (std::uint32_t P = 1; P <= 8 && P <= KS8; ++P) {
+    const std::uint32_t waves = (base * P + sms - 1) / sms, chunks = (KS8 + P - 1) / P * 8;
+    const double t = waves * chunks * chunk_us + (P - 1) * part_us;
+    if (P == 1 || t < best_t) best = P, best_t = t;
   }
   return best;
 }

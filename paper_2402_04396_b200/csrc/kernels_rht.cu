@@ -66,35 +66,100 @@ __global__ void __launch_bounds__(kP1Threads) rht_pass1(RhtArgs a) {
     return;
   }
   __shared__ float red1[32];
-  // vectors blockIdx.y * vpb .. : large batches amortise the CTA over several vectors
+  float* const Bs = sm1;
+  p1_load_base<Q>(a, Bs);
+  __syncthreads();
+  // vectors blockIdx.y * vpb .. : large batches amortise the CTA over several vectors,
+  // one per warp (warp_teams) so a pass's barriers are warp-local
+  const Team tm = a.warp_teams ? warp_team() : block_team();
+  const int team = a.warp_teams ? int(threadIdx.x >> 5) : 0, teams = a.warp_teams ? int(blockDim.x >> 5) : 1;
+  float* const xs = sm1 + p1_base_bytes<Q>() / 4 + std::size_t(team) * (p1_team_bytes<Q>(a.P2) / 4);
   const int vpb = a.vpb > 1 ? a.vpb : 1, b_end = min(a.batch, int(blockIdx.y + 1) * vpb);
-  for (int b = int(blockIdx.y) * vpb; b < b_end; ++b) {
-  if (a.fwd && blockIdx.x == 0) {
-    if (a.amax_out && threadIdx.x == 0) a.amax_out[b] = 0.f;
-    if (a.tl_out && threadIdx.x == 0) a.tl_out[b] = 0;
-    // sum_i t_i = (p / sqrt(n)) sum_{b' < q} colsum[b'] s_b' x_b'  (Sylvester columns sum to p * delta)
-    if (a.tsum_out && threadIdx.x == 32) {
-      float acc = 0.f;
-      for (std::uint32_t j = 0; j < Q; ++j) {
-        float v = a.in[std::size_t(b) * a.n + j];
-        if ((a.signs[j >> 3] >> (j & 7)) & 1) v = -v;
-        acc += a.colsum[j] * v;
+  for (int b = int(blockIdx.y) * vpb + team; b < b_end; b += teams) {
+    if (a.fwd && blockIdx.x == 0) {
+      if (a.amax_out && tm.tid == 0) a.amax_out[b] = 0.f;
+      if (a.tl_out && tm.tid == 0) a.tl_out[b] = 0;
+      // sum_i t_i = (p / sqrt(n)) sum_{b' < q} colsum[b'] s_b' x_b'  (Sylvester columns sum to p * delta)
+      if (a.tsum_out && tm.tid == (tm.warp ? 1u : 32u)) {
+        float acc = 0.f;
+        for (std::uint32_t j = 0; j < Q; ++j) {
+          float v = a.in[std::size_t(b) * a.n + j];
+          if ((a.signs[j >> 3] >> (j & 7)) & 1) v = -v;
+          acc += a.colsum[j] * v;
+        }
+        a.tsum_out[b] = acc * float(a.p) * rsqrtf(float(a.n));
       }
-      a.tsum_out[b] = acc * float(a.p) * rsqrtf(float(a.n));
     }
-  }
-  rht_p1_body<Q>(a, a.ch0 + blockIdx.x, b, sm1, red1, block_team());
+    rht_p1_body<Q>(a, a.ch0 + blockIdx.x, b, xs, Bs, red1, tm);
   }
 }
 
-// Pass 2.  grid = (P2 * q / 4 column groups, batch); block = 128 threads.
-__global__ void __launch_bounds__(128) rht_pass2(RhtArgs a) {
+// Pass 2.  grid = (P2 * q / 4 column groups, batch / vpb); block = 128 threads,
+// or one warp per vector (warp_teams).
+__global__ void __launch_bounds__(256) rht_pass2(RhtArgs a) {
   extern __shared__ __align__(16) float sm2[];
   __shared__ float red[32];
   pdl_wait();
   pdl_trigger();
+  const Team tm = a.warp_teams ? warp_team() : block_team();
+  const int team = a.warp_teams ? int(threadIdx.x >> 5) : 0, teams = a.warp_teams ? int(blockDim.x >> 5) : 1;
+  float* const s = sm2 + std::size_t(team) * a.P1 * 4;
   const int vpb = a.vpb > 1 ? a.vpb : 1, b_end = min(a.batch, int(blockIdx.y + 1) * vpb);
-  for (int b = int(blockIdx.y) * vpb; b < b_end; ++b) rht_p2_body(a, blockIdx.x, b, sm2, red, block_team());
+  for (int b = int(blockIdx.y) * vpb + team; b < b_end; b += teams) rht_p2_body(a, blockIdx.x, b, s, red, tm);
+}
+
+// Pass 2 for prefill batches (P1 <= 64): one warp per (vector, 32 adjacent flat
+// columns), lane = column, the FWHT over a_hi entirely in registers -- every row
+// is one coalesced 128 B segment and there is no shared memory or barrier.  Same
+// butterfly order as fwht_rows (stages by increasing index bit), so the output
+// is bitwise that of rht_pass2.  grid = ceil(batch * ceil(P2 q / 32) / 8); 256 threads.
+template <int P1>
+__global__ void __launch_bounds__(256) rht_pass2_reg(RhtArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  const std::uint32_t stride = a.P2 * a.q, ncg = (stride + 31) / 32;
+  const std::uint32_t w = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (w >= ncg * std::uint32_t(a.batch)) return;  // whole warps
+  const int b = int(w / ncg);
+  const std::uint32_t col = (w % ncg) * 32 + (threadIdx.x & 31u);
+  const bool live = col < stride;
+  float v[P1];
+#pragma unroll
+  for (int r = 0; r < P1; ++r)
+    v[r] = live ? __ldcg(a.mid + rank_major(b, r * stride + col, a.mid_rows, a.batch, a.n)) : 0.f;
+  // K3's output signs, fetched alongside the data (bit r = row r's sign)
+  unsigned long long neg = 0;
+  if (!a.fwd && live)
+#pragma unroll
+    for (int r = 0; r < P1; ++r) {
+      const std::uint32_t i = r * stride + col;
+      neg |= static_cast<unsigned long long>((a.signs[i >> 3] >> (i & 7)) & 1) << r;
+    }
+#pragma unroll
+  for (int len = 1; len < P1; len <<= 1)
+#pragma unroll
+    for (int k = 0; k < P1; ++k)
+      if (!(k & len)) {
+        const float x = v[k], y = v[k + len];
+        v[k] = x + y;
+        v[k + len] = x - y;
+      }
+  const float sc = rsqrtf(float(a.n));
+  float mx = 0.f;
+  if (live) {
+#pragma unroll
+    for (int r = 0; r < P1; ++r) {
+      const std::uint32_t i = r * stride + col;
+      float o = v[r] * sc;
+      if ((neg >> r) & 1) o = -o;
+      a.out[std::size_t(b) * a.n + i] = o;
+      mx = fmaxf(mx, fabsf(o));
+    }
+  }
+  if (a.fwd && a.amax_out) {
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomic_max_pos(a.amax_out + b, mx);
+  }
 }
 
 // Pass 2 of K1, limb flavour: grid = (P2 * q / 8 codeword columns, batch).
@@ -131,13 +196,13 @@ void plan_split_impl(const DevSide& side, RhtArgs& a) {
 
 template <int Q>
 void launch_pass1_q(const RhtArgs& a, std::uint32_t extra_ctas, cudaStream_t s) {
-  const std::size_t chunk = std::size_t(a.P2) * Q;
-  const std::size_t bsz = Q == 1 ? 0 : (Q <= 28 ? Q * Q * 4 : (Q * Q + 15) / 16 * 16);
-  const std::size_t smem = chunk * 4 * (Q > 1 ? 2 : 1) + bsz;
-  kernel_attrs(reinterpret_cast<const void*>(rht_pass1<Q>), 96 * 1024);
+  RhtArgs b = a;
   const int vpb = a.vpb > 1 ? a.vpb : 1;
+  b.warp_teams = vpb == kP1Threads / 32;  // prefill batches: one vector per warp
+  const std::size_t smem = p1_base_bytes<Q>() + (b.warp_teams ? vpb : 1) * p1_team_bytes<Q>(a.P2);
+  kernel_attrs(reinterpret_cast<const void*>(rht_pass1<Q>), 96 * 1024);
   launch_pdl(rht_pass1<Q>, dim3((a.p1_count ? a.p1_count : a.P1) + extra_ctas, (a.batch + vpb - 1) / vpb),
-             dim3(kP1Threads), smem, s, a);
+             dim3(kP1Threads), smem, s, b);
 }
 
 void launch_pass1(const RhtArgs& a, std::uint32_t extra, cudaStream_t s) {
@@ -154,11 +219,33 @@ void launch_pass1(const RhtArgs& a, std::uint32_t extra, cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
+template <int P1>
+void launch_pass2_reg(const RhtArgs& a, cudaStream_t s) {
+  const std::uint32_t warps = (a.P2 * a.q + 31) / 32 * std::uint32_t(a.batch);
+  launch_pdl(rht_pass2_reg<P1>, dim3((warps + 7) / 8), dim3(256), 0, s, a);
+}
+
 void launch_pass2(const RhtArgs& a, cudaStream_t s) {
-  const std::uint32_t groups = a.P2 * a.q / 4;
-  kernel_attrs(reinterpret_cast<const void*>(rht_pass2), 96 * 1024);
-  const int vpb = a.vpb > 1 ? a.vpb : 1;
-  launch_pdl(rht_pass2, dim3(groups, (a.batch + vpb - 1) / vpb), dim3(128), std::size_t(a.P1) * 16, s, a);
+  if (a.vpb > 1 && a.P1 <= 64) {  // prefill batches: register FWHT, one warp per 32 columns
+    switch (a.P1) {
+      case 1: launch_pass2_reg<1>(a, s); break;
+      case 2: launch_pass2_reg<2>(a, s); break;
+      case 4: launch_pass2_reg<4>(a, s); break;
+      case 8: launch_pass2_reg<8>(a, s); break;
+      case 16: launch_pass2_reg<16>(a, s); break;
+      case 32: launch_pass2_reg<32>(a, s); break;
+      default: launch_pass2_reg<64>(a, s); break;
+    }
+  } else {
+    const std::uint32_t groups = a.P2 * a.q / 4;
+    kernel_attrs(reinterpret_cast<const void*>(rht_pass2), 96 * 1024);
+    RhtArgs b = a;
+    const int vpb = a.vpb > 1 ? a.vpb : 1;
+    b.warp_teams = vpb > 1 && a.P1 <= 512;  // one vector per warp while a warp's share stays small
+    const int threads = b.warp_teams ? 32 * vpb : 128;
+    launch_pdl(rht_pass2, dim3(groups, (a.batch + vpb - 1) / vpb), dim3(threads),
+               std::size_t(a.P1) * 16 * (b.warp_teams ? vpb : 1), s, b);
+  }
   cuda_check(cudaGetLastError(), "rht pass2 launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }

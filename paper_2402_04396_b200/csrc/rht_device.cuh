@@ -1,9 +1,8 @@
-// Device-side pieces of the randomized Hadamard transforms (K1 / K3), shared
-// by the standalone RHT kernels (kernels_rht.cu) and the fused layer kernel
-// (gemv_tc.cu).  The pass bodies run on a "team" of threads (a whole CTA with
-// __syncthreads, or a subset of a CTA's warps with a named barrier), so the
-// fused kernel can run them on its decode/issue warps while its producer warp
-// streams codes.
+// Device-side pieces of the randomized Hadamard transforms (K1 / K3) of the
+// RHT kernels (kernels_rht.cu).  The pass bodies run on a "team" of threads: a
+// whole CTA (__syncthreads) for small batches, where one vector's pass is
+// spread over the CTA, or a single warp (__syncwarp) for prefill batches, where
+// each warp of a CTA carries its own vector and the CTA has 8 in flight.
 //
 // SideTransform (core/src/transforms.cpp:28-47) with had_apply
 // (core/src/hadamard.cpp:170-210):  H = (H_p (x) B_q) / sqrt(n), flat index
@@ -58,6 +57,7 @@ struct RhtArgs {
   std::uint32_t ch0, p1_count, row0, p1_out_rows, mid_rows, in_rows;
   int vpb;                      // vectors per CTA (fp32 passes; 0/1 = one)
   int in_parts;                 // pass 1 fp32 input = sum of in_parts partial arrays [batch][n] (0/1 = one)
+  int warp_teams;               // fp32 passes: one vector per warp (vpb > 1; set by the launchers)
 };
 
 // Element (b, i) of a [batch][n] vector set stored rank-major with `rows` rows per
@@ -68,23 +68,34 @@ __device__ __forceinline__ std::size_t rank_major(std::size_t b, std::uint32_t i
 }
 
 struct Team {
-  std::uint32_t tid, n, bar;  // thread index in the team, team size, named barrier (0 = __syncthreads)
+  std::uint32_t tid, n, warp;  // thread index in the team, team size, 1 = the team is one warp
 };
-
-// Host helpers (kernels_rht.cu): pass geometry / arguments for the fused layer kernel.
-void rht_plan_split(const DevSide& side, RhtArgs& a);  // n, p, q, P2, P1
-std::size_t rht_p1_smem_bytes(const DevSide& side);     // pass-1 scratch of this side
-std::size_t rht_p2_smem_bytes(const DevSide& side);     // pass-2 scratch (limb flavour, the larger)
 
 namespace {
 
 
 __device__ __forceinline__ Team block_team() { return Team{threadIdx.x, blockDim.x, 0u}; }
+__device__ __forceinline__ Team warp_team() { return Team{threadIdx.x & 31u, 32u, 1u}; }
 __device__ __forceinline__ void team_sync(const Team& t) {
-  if (t.bar == 0)
-    __syncthreads();
+  if (t.warp)
+    __syncwarp();
   else
-    asm volatile("bar.sync %0, %1;\n" ::"r"(t.bar), "r"(t.n) : "memory");
+    __syncthreads();
+}
+// Team-wide sum / max; red: >= 32 floats of team-shared smem (unused by warp teams).
+// The reduction tree is fixed, so the result is deterministic.
+template <bool kMax>
+__device__ __forceinline__ float team_reduce(float v, float* red, const Team& tm) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const float w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = kMax ? fmaxf(v, w) : v + w;
+  }
+  if (tm.warp) return v;
+  if ((tm.tid & 31) == 0) red[tm.tid >> 5] = v;
+  team_sync(tm);
+  float t = 0.f;
+  for (std::uint32_t w = 0; w < (tm.n + 31) / 32; ++w) t = kMax ? fmaxf(t, red[w]) : t + red[w];
+  return t;
 }
 
 __device__ __forceinline__ void atomic_max_pos(float* addr, float v) {
@@ -195,35 +206,43 @@ __device__ __forceinline__ float2 combine2(const RhtArgs& a, int b, std::uint32_
 }
 
 
-// Pass-1 smem bytes for chunk P2 * Q (x, base output, base).
+// Pass-1 smem: the Q x Q base (float for Q <= 28, int8 for the order-172 one;
+// shared by the CTA's teams), then per team the chunk x and the base output y.
 template <int Q>
-__host__ __device__ constexpr std::size_t p1_smem_bytes(std::uint32_t P2) {
-  return std::size_t(P2) * Q * 4 * (Q > 1 ? 2 : 1) + (Q == 1 ? 0 : (Q <= 28 ? Q * Q * 4 : (Q * Q + 15) / 16 * 16));
+__host__ __device__ constexpr std::size_t p1_base_bytes() {
+  return Q == 1 ? 0 : (Q <= 28 ? Q * Q * 4 : (Q * Q + 15) / 16 * 16);
 }
-
-// Pass 1 on chunk `ch` of vector b.  red: >= 32 floats of team-shared smem.
 template <int Q>
-__device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* sm1, float* red, const Team& tm) {
-  const std::uint32_t chunk = a.P2 * Q;  // floats, multiple of 4
-  const std::uint32_t e0 = ch * chunk;
-  float* x = sm1;                         // [P2][Q]
-  float* y = sm1 + chunk;                 // base output (Q > 1)
-  float* Bs = sm1 + 2 * chunk;            // Q x Q base as float (Q <= 28) / int8 (Q = 172)
+__host__ __device__ constexpr std::size_t p1_team_bytes(std::uint32_t P2) {
+  return std::size_t(P2) * Q * 4 * (Q > 1 ? 2 : 1);
+}
+// Base into smem (whole CTA; the caller syncs).
+template <int Q>
+__device__ void p1_load_base(const RhtArgs& a, float* Bs) {
   if constexpr (Q > 1) {
     if constexpr (Q <= 28) {
-      for (std::uint32_t i = tm.tid; i < Q * Q; i += tm.n) Bs[i] = float(a.base[i]);
+      for (std::uint32_t i = threadIdx.x; i < Q * Q; i += blockDim.x) Bs[i] = float(a.base[i]);
     } else {
-      std::int8_t* B8 = reinterpret_cast<std::int8_t*>(Bs);
-      for (std::uint32_t i = tm.tid; i < Q * Q / 4; i += tm.n)
-        reinterpret_cast<std::uint32_t*>(B8)[i] = reinterpret_cast<const std::uint32_t*>(a.base)[i];
+      for (std::uint32_t i = threadIdx.x; i < Q * Q / 4; i += blockDim.x)
+        reinterpret_cast<std::uint32_t*>(Bs)[i] = reinterpret_cast<const std::uint32_t*>(a.base)[i];
     }
   }
+}
+
+// Pass 1 on chunk `ch` of vector b.  xs: the team's [2][chunk] floats; Bs: the
+// base (p1_load_base); red: >= 32 floats of team-shared smem.
+template <int Q>
+__device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* xs, const float* Bs, float* red,
+                            const Team& tm) {
+  const std::uint32_t chunk = a.P2 * Q;  // floats, multiple of 4
+  const std::uint32_t e0 = ch * chunk;
+  float* x = xs;                          // [P2][Q]
+  float* y = xs + chunk;                  // base output (Q > 1)
   float ss = 0.f;
-  for (std::uint32_t v = tm.tid; v < chunk / 4; v += tm.n) {
-    const std::uint32_t i = e0 + 4 * v;
-    float4 val;
-    if (a.zacc) {
-      val = combine4(a, b, i);
+  if (a.zacc) {
+    for (std::uint32_t v = tm.tid; v < chunk / 4; v += tm.n) {
+      const std::uint32_t i = e0 + 4 * v;
+      reinterpret_cast<float4*>(x)[v] = combine4(a, b, i);
       if (a.zacc_zero) {  // each (vector, row quad) is read by exactly one thread: clear it for the next chunk
         for (int st = 0; st < a.zstages; ++st)
           for (int l = 0; l < 4; ++l)
@@ -231,46 +250,79 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* sm
                                      (std::size_t(st) * a.zcols + 4 * b + l) * a.zrows + (i - a.row0)) =
                 make_int4(0, 0, 0, 0);
       }
-    } else {
-      val = __ldcg(reinterpret_cast<const float4*>(a.in + rank_major(b, i, a.in_rows, a.batch, a.n)));
-      for (int pp = 1; pp < a.in_parts; ++pp) {  // K-split partials (prefill), summed in order
-        const float4 w4 = __ldcg(reinterpret_cast<const float4*>(a.in + std::size_t(pp) * a.batch * a.n +
-                                                                 std::size_t(b) * a.n + i));
-        val = make_float4(val.x + w4.x, val.y + w4.y, val.z + w4.z, val.w + w4.w);
+    }
+  } else {
+    // kU float4s per thread per round, so every input array's loads are in flight together
+    constexpr int kU = 4;
+    const std::uint32_t nv = chunk / 4;
+    for (std::uint32_t v0 = tm.tid; v0 < nv; v0 += kU * tm.n) {
+      float4 val[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const std::uint32_t v = v0 + u * tm.n;
+        if (v < nv) val[u] = __ldcg(reinterpret_cast<const float4*>(a.in + rank_major(b, e0 + 4 * v, a.in_rows,
+                                                                                    a.batch, a.n)));
       }
-      ss += val.x * val.x + val.y * val.y + val.z * val.z + val.w * val.w;
-      if (a.fwd) val = sign4(val, (a.signs[i >> 3] >> (i & 4)) & 0xFu);
+      for (int pp = 1; pp < a.in_parts; ++pp) {  // K-split partials (prefill), summed in order
+        const float* part = a.in + (std::size_t(pp) * a.batch + b) * a.n + e0;
+        float4 w4[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const std::uint32_t v = v0 + u * tm.n;
+          if (v < nv) w4[u] = __ldcg(reinterpret_cast<const float4*>(part + 4 * v));
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          val[u] = make_float4(val[u].x + w4[u].x, val[u].y + w4[u].y, val[u].z + w4[u].z, val[u].w + w4[u].w);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const std::uint32_t v = v0 + u * tm.n, i = e0 + 4 * v;
+        if (v < nv) {
+          float4 w = val[u];
+          ss += w.x * w.x + w.y * w.y + w.z * w.z + w.w * w.w;
+          if (a.fwd) w = sign4(w, (a.signs[i >> 3] >> (i & 4)) & 0xFu);
+          reinterpret_cast<float4*>(x)[v] = w;
+        }
+      }
     }
-    reinterpret_cast<float4*>(x)[v] = val;
   }
-  if (a.ssq) {  // deterministic per-chunk sum of squares (fixed reduction tree)
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    if ((tm.tid & 31) == 0) red[tm.tid >> 5] = ss;
-    team_sync(tm);
-    if (tm.tid == 0) {
-      float t = 0.f;
-      for (std::uint32_t w = 0; w < (tm.n + 31) / 32; ++w) t += red[w];
-      a.ssq[std::size_t(b) * a.P1 + ch] = t;
-    }
+  if (a.ssq) {  // deterministic per-chunk sum of squares
+    const float t = team_reduce<false>(ss, red, tm);
+    if (tm.tid == 0) a.ssq[std::size_t(b) * a.P1 + ch] = t;
   }
   team_sync(tm);
   float* cur = x;
   if constexpr (Q > 1) {
     // base along each contiguous q-row: y[r][c] = sum_k B[c][k] x[r][k] (fwd) or B[k][c] (K3)
-    for (std::uint32_t e = tm.tid; e < chunk; e += tm.n) {
-      const std::uint32_t r = e / Q, c = e - r * Q;
-      const float* xr = x + r * Q;
-      float acc = 0.f;
-      if constexpr (Q <= 28) {
-        if (a.fwd) {
-#pragma unroll 4
-          for (int k = 0; k < Q; ++k) acc += Bs[c * Q + k] * xr[k];
-        } else {
-#pragma unroll 4
-          for (int k = 0; k < Q; ++k) acc += Bs[k * Q + c] * xr[k];
+    if constexpr (Q <= 28) {
+      // lane = output column c with its base row (fwd) / column in registers; each
+      // x row is Q / 4 broadcast float4 reads; the team's warps take rows round robin
+      const std::uint32_t c = tm.tid & 31u, nw = tm.n >> 5;
+      if (c < std::uint32_t(Q)) {
+        float bc[Q];
+#pragma unroll
+        for (int k = 0; k < Q; ++k) bc[k] = a.fwd ? Bs[c * Q + k] : Bs[k * Q + c];
+        for (std::uint32_t r = tm.tid >> 5; r < a.P2; r += nw) {
+          const float4* xr = reinterpret_cast<const float4*>(x + r * Q);
+          float acc = 0.f;
+#pragma unroll
+          for (int j = 0; j < Q / 4; ++j) {
+            const float4 x4 = xr[j];
+            acc += bc[4 * j] * x4.x;
+            acc += bc[4 * j + 1] * x4.y;
+            acc += bc[4 * j + 2] * x4.z;
+            acc += bc[4 * j + 3] * x4.w;
+          }
+          y[r * Q + c] = acc;
         }
-      } else {
-        const std::int8_t* B8 = reinterpret_cast<const std::int8_t*>(Bs);
+      }
+    } else {
+      const std::int8_t* B8 = reinterpret_cast<const std::int8_t*>(Bs);
+      for (std::uint32_t e = tm.tid; e < chunk; e += tm.n) {
+        const std::uint32_t r = e / Q, c = e - r * Q;
+        const float* xr = x + r * Q;
+        float acc = 0.f;
         if (a.fwd) {
 #pragma unroll 4
           for (int k = 0; k < Q; ++k) acc += float(B8[c * Q + k]) * xr[k];
@@ -278,8 +330,8 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* sm
 #pragma unroll 4
           for (int k = 0; k < Q; ++k) acc += float(B8[k * Q + c]) * xr[k];
         }
+        y[e] = acc;
       }
-      y[e] = acc;
     }
     team_sync(tm);
     cur = y;
@@ -312,14 +364,8 @@ __device__ void rht_p2_body(const RhtArgs& a, std::uint32_t cg, int b, float* sm
     mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
   }
   if (a.fwd && a.amax_out) {
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((tm.tid & 31) == 0) red[tm.tid >> 5] = mx;
-    team_sync(tm);
-    if (tm.tid == 0) {
-      float m = 0.f;
-      for (std::uint32_t w = 0; w < (tm.n + 31) / 32; ++w) m = fmaxf(m, red[w]);
-      atomic_max_pos(a.amax_out + b, m);
-    }
+    const float m = team_reduce<true>(mx, red, tm);
+    if (tm.tid == 0) atomic_max_pos(a.amax_out + b, m);
   }
   team_sync(tm);
 }

@@ -96,6 +96,22 @@ def test_rht_matches_oracle(dev, oracle, n):
             assert rel_err(got[b], want) < 1e-5, (n, tr, rel_err(got[b], want))
 
 
+@pytest.mark.parametrize("n", [112, 4096, 8192, 11008, 28672, 1 << 16])
+def test_rht_prefill_batch_bitwise_equals_single(dev, oracle, n):
+    """Batches >= 64 run the transform passes one vector per warp (pass 2 as a
+    register FWHT); every row must be bitwise the batch-1 (whole-CTA) result."""
+    rng = np.random.default_rng(n + 1)
+    signs = torch.from_numpy(rng.integers(0, 256, (n + 7) // 8, dtype=np.uint8)).to(dev)
+    x = torch.from_numpy(rng.standard_normal((70, n)).astype(np.float32)).to(dev)
+    for tr in (False, True):
+        got = q8p.rht(x, signs, transpose=tr)
+        for b in (0, 9, 69):
+            one = q8p.rht(x[b:b + 1].contiguous(), signs, transpose=tr)
+            assert torch.equal(got[b], one[0]), (n, tr, b)
+        want = oracle.side_apply(signs.cpu().numpy(), x[33].cpu().numpy().astype(np.float64), tr)
+        assert rel_err(got[33].cpu().numpy(), want) < 1e-5
+
+
 @pytest.mark.parametrize("name", golden_names())
 def test_forward_matches_reference_golden(dev, name):
     art, x, y = load_case(name)
