@@ -21,8 +21,10 @@ each layer y = S_U H^T W_hat H S_V x (K1 -> K2 -> K3).
            reference sources) on the box's host cores, bounded sample.
 
 N > 1 (torchrun): the layers are row-sharded across ranks (each rank holds
-m/N rows), z is all-gathered with NCCL before the output RHT; total work is
-fixed -> "scaling": "strong".
+m/N rows); by default K3 pass 1 pushes every rank's rows straight into every
+rank's window over NVLink (q8p_forward_sharded_push, after a bit-exact self-check
+against the NCCL all-gather path; --allgather nccl selects q8p_forward_sharded);
+total work is fixed -> "scaling": "strong".
 
 `--impl reference` times the reference CPU implementation instead (rank 0
 only; other ranks exit 0).
@@ -261,6 +263,7 @@ def run_ours(args):
     sharded = world > 1 or args.sharded  # --sharded at N=1: the row-sharded path over a 1-rank NCCL comm
 
     comm = None
+    peers = None
     if sharded:
         uid = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
@@ -268,6 +271,15 @@ def run_ours(args):
         if world > 1:
             dist.broadcast(uid, 0)
         comm = q8p.NcclComm(bytes(uid.cpu().numpy()), world, rank, local)
+        if args.allgather == "push":
+            # push all-gather group: one window per rank, IPC handles exchanged over the process group
+            peers = q8p.PeerGroup(local, world, rank, min(args.batch, 32) * max(m // world for m, _ in layers))
+            handles = [None] * world
+            if world > 1:
+                dist.all_gather_object(handles, peers.handle)
+            else:
+                handles = [peers.handle]
+            peers.connect(handles)
 
     # `copies` full copies of the layer set (distinct device buffers) rotate so
     # every step streams its codes from HBM: at least 4x the L2 capacity of codes
@@ -300,11 +312,38 @@ def run_ours(args):
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_gemv)]
           for _ in range(args.copies)]
 
+    def sharded_forward(L, x, y):
+        if peers is not None:
+            L.forward_sharded_push(x, peers, out=y, stream=stream, workspace=ws)
+        else:
+            L.forward_sharded(x, comm, out=y, stream=stream, workspace=ws)
+
+    allgather = None
+    if sharded and peers is not None:
+        # self-check: the push all-gather's y equals the NCCL all-gather's bit for bit
+        ok = True
+        with torch.cuda.stream(stream):
+            for li, L in enumerate(copies[0]):
+                ya = L.forward_sharded_push(xs[li], peers, stream=stream, workspace=ws)
+                yb = L.forward_sharded(xs[li], comm, stream=stream, workspace=ws)
+                stream.synchronize()
+                ok &= bool(torch.equal(ya, yb))
+        flag = torch.tensor([1 if ok else 0], device=dev)
+        if world > 1:
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            peers = None
+            allgather = "nccl (push all-gather self-check failed)"
+        else:
+            allgather = "push (K3 pass 1 stores into peers' windows over NVLink)"
+    elif sharded:
+        allgather = "nccl"
+
     def step(c, events=True):
         for li, L in enumerate(copies[c]):
             e = ev[c][li] if events else None
             if sharded:
-                L.forward_sharded(xs[li], comm, out=ys[li], stream=stream, workspace=ws)
+                sharded_forward(L, xs[li], ys[li])
             else:
                 L.forward(xs[li], out=ys[li], stream=stream, workspace=ws, gemv_events=e)
 
@@ -406,7 +445,7 @@ def run_ours(args):
         if sharded:
             dx.copy_(hx, non_blocking=True)
             for li, L in enumerate(copies[c]):
-                L.forward_sharded(xv[li], comm, out=yv[li], stream=stream, workspace=ws)
+                sharded_forward(L, xv[li], yv[li])
             hy.copy_(dy, non_blocking=True)
             stream.synchronize()
         else:
@@ -597,7 +636,8 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "s8xs8->s32 (K2 tensor cores) + fp32 (RHT, I/O)", "data": "synthetic",
             "config": {"workload": workload_name(args), "batch": B,
                        "layers": [f"{m}x{n}" for m, n in layers],
-                       "parallelism": f"row-shard tp{world}" if world > 1 else "single-gpu",
+                       "parallelism": f"row-shard tp{world}" if world > 1 else ("row-shard tp1" if sharded else "single-gpu"),
+                       **({"allgather": allgather} if sharded else {}),
                        "l2": f"{args.copies} rotating copies of the layer set (distinct buffers, "
                              f"{args.copies * set_code_bytes / 1e6:.0f} MB of codes >= 4x the {l2_bytes / 1e6:.0f} MB L2)",
                        "codes": (f"synthetic Gaussian W quantized by the reference H = I route on the GPU "
@@ -633,7 +673,10 @@ def main():
     ap.add_argument("--bits", type=int, default=2, choices=[2, 3, 4],
                     help="2: E8P (headline); 3 / 4: RVQ variants (BASELINE configs[3])")
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--sharded", action="store_true", help="use q8p_forward_sharded even at N=1 (1-rank NCCL)")
+    ap.add_argument("--sharded", action="store_true", help="use the row-sharded path even at N=1 (1-rank group)")
+    ap.add_argument("--allgather", choices=["push", "nccl"], default="push",
+                    help="sharded z exchange: push = q8p_forward_sharded_push (K3 pass 1 stores into the peers' "
+                         "windows), nccl = q8p_forward_sharded (ncclAllGather between the K3 passes)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--sample-div", type=int, default=1, help="row sampling of --impl reference steps (1: full rows)")

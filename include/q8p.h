@@ -27,6 +27,7 @@
  *   q8p_plan_hadamard     latq::plan_hadamard  core/include/latq/hadamard.hpp:42
  *                         (registry extended with order 172)
  *   q8p_forward_sharded   (new) row-sharded forward with an NCCL all-gather
+ *   q8p_forward_sharded_push  (new) the same with the all-gather fused into K3 pass 1
  * Error mapping: SizeError -> Q8P_ERR_SIZE, ValidationError ->
  * Q8P_ERR_VALIDATION, FormatError -> Q8P_ERR_FORMAT, BadMagicError ->
  * Q8P_ERR_BAD_MAGIC, UnsupportedVersionError -> Q8P_ERR_UNSUPPORTED_VERSION,
@@ -281,6 +282,41 @@ q8p_status q8p_hadamard_base(size_t q, int8_t* out);
  * of one layer, all on one device; batch <= 32; ws sized for shards[0]. */
 q8p_status q8p_forward_sharded_sim(const q8p_layer* const* shards, int world, const float* x, float* y, int batch,
                                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* Push all-gather (replaces the all-gather between
+ * q8p_forward_sharded's K3 passes).  The reference's rows are independent
+ * (core/src/pipeline.cpp:176-191), so each rank computes its rows' K3 pass 1
+ * and stores them straight into every rank's window over NVLink (CUDA IPC
+ * mappings) as 8-byte {value, call tag} words; K3 pass 2 reads its own window
+ * as the tagged words arrive -- no collective launch, no fences, the transfer
+ * overlaps pass 1 tile by tile.  Setup: every rank calls q8p_peers_create (one
+ * device allocation of 256 B + 16 * world * slice_floats bytes; `handle`
+ * receives its Q8P_PEER_HANDLE_BYTES IPC handle), the handles are exchanged out
+ * of band (e.g. torch.distributed all_gather_object) and concatenated in rank
+ * order, then every rank calls q8p_peers_connect.  world <= 16;
+ * slice_floats >= min(batch, 32) * m_local for every layer / batch used.
+ * Requirements as q8p_forward_sharded's fast path: equal rank-ordered row
+ * shards that are whole K3 pass-1 chunks (rht layers), batches on the
+ * tensor-core path; else Q8P_ERR_UNSUPPORTED.  All ranks must issue the same
+ * sequence of push forwards (a rank whose peer never writes traps after ~20 s). */
+#define Q8P_PEER_HANDLE_BYTES 64
+typedef struct q8p_peers q8p_peers;
+q8p_status q8p_peers_create(int device, int world, int rank, size_t slice_floats, q8p_peers** out,
+                            uint8_t handle[Q8P_PEER_HANDLE_BYTES]);
+q8p_status q8p_peers_connect(q8p_peers* peers, const uint8_t* handles /* world * Q8P_PEER_HANDLE_BYTES */);
+q8p_status q8p_peers_destroy(q8p_peers* peers);
+/* Diagnostics (synchronous): the number of push calls (K3 chunks) completed on this rank. */
+q8p_status q8p_peers_state(const q8p_peers* peers, uint64_t* epoch);
+q8p_status q8p_forward_sharded_push(const q8p_layer* layer, q8p_peers* peers, const float* x, float* y, int batch,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+/* Test support: the `world` members of one group created in ONE process on one
+ * device, wired to each other directly (no IPC); q8p_forward_sharded_push_sim
+ * runs every rank's K1, K2 and pushing pass 1, then every rank's pass 2, in
+ * stream order; y = [world][batch][m] (each rank's full output). */
+q8p_status q8p_peers_connect_local(q8p_peers* const* group, int world);
+q8p_status q8p_forward_sharded_push_sim(const q8p_layer* const* shards, q8p_peers* const* peers, int world,
+                                        const float* x, float* y, int batch, void* workspace,
+                                        size_t workspace_bytes, void* stream);
 
 /* NCCL plumbing for q8p_forward_sharded (wraps ncclGetUniqueId /
  * ncclCommInitRank so callers need no NCCL headers). */

@@ -159,6 +159,13 @@ _SIGNATURES = {
     "q8p_e8p_decode_host": (ctypes.c_int, [ctypes.c_uint16, ctypes.c_void_p]),
     "q8p_codebook_table": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
     "q8p_hadamard_base": (ctypes.c_int, [ctypes.c_size_t, ctypes.c_void_p]),
+    "q8p_peers_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p), ctypes.c_void_p]),
+    "q8p_peers_connect": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p]),
+    "q8p_peers_connect_local": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "q8p_peers_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "q8p_peers_state": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "q8p_forward_sharded_push": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "q8p_forward_sharded_push_sim": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "q8p_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
     "q8p_nccl_comm_init": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
     "q8p_nccl_comm_destroy": (ctypes.c_int, [ctypes.c_void_p]),
@@ -269,6 +276,52 @@ class NcclComm:
         if self.handle:
             _check(lib().q8p_nccl_comm_destroy(self.handle))
             self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+PEER_HANDLE_BYTES = 64
+
+
+class PeerGroup:
+    """One rank's member of a push all-gather group (q8p_peers_*): a window in
+    this GPU's memory that the other ranks write into over NVLink.  Exchange
+    `handle` (bytes) among the ranks out of band, then `connect(handles)` with the
+    rank-ordered list.  slice_floats >= min(batch, 32) * m_local of every layer used."""
+
+    def __init__(self, device: int, world: int, rank: int, slice_floats: int):
+        h = ctypes.c_void_p()
+        buf = (ctypes.c_uint8 * PEER_HANDLE_BYTES)()
+        _check(lib().q8p_peers_create(device, world, rank, slice_floats, ctypes.byref(h), buf))
+        self._h = h
+        self.handle = bytes(buf)
+        self.device, self.world, self.rank = device, world, rank
+
+    def connect(self, handles) -> None:
+        if len(handles) != self.world or any(len(b) != PEER_HANDLE_BYTES for b in handles):
+            raise ValidationError(f"need {self.world} handles of {PEER_HANDLE_BYTES} bytes")
+        _check(lib().q8p_peers_connect(self._h, b"".join(handles)))
+
+    @staticmethod
+    def connect_local(group) -> None:
+        """Wire the members of one group created in this process (tests, one GPU)."""
+        arr = (ctypes.c_void_p * len(group))(*[g._h.value for g in group])
+        _check(lib().q8p_peers_connect_local(arr, len(group)))
+
+    def state(self) -> int:
+        """Push calls (K3 chunks) completed on this rank."""
+        ep = ctypes.c_uint64()
+        _check(lib().q8p_peers_state(self._h, ctypes.byref(ep)))
+        return ep.value
+
+    def close(self) -> None:
+        if self._h:
+            _check(lib().q8p_peers_destroy(self._h))
+            self._h = None
 
     def __del__(self):
         try:
@@ -436,6 +489,19 @@ class Layer:
                                          ws.numel(), comm, _stream_ptr(stream)))
         return out
 
+    def forward_sharded_push(self, x, peers: "PeerGroup", out=None, stream=None, workspace=None):
+        """Row-sharded forward with the all-gather fused into K3 pass 1
+        (q8p_forward_sharded_push): every rank's rows are pushed into every rank's
+        PeerGroup window over NVLink; every rank gets the full y."""
+        info = self.info
+        self._check_x(x, info["n"])
+        batch = x.shape[0]
+        out = self._out(out, x, info["m"])
+        ws = workspace if workspace is not None else self.workspace(batch)
+        _check(lib().q8p_forward_sharded_push(self._h, peers._h, x.data_ptr(), out.data_ptr(), batch, ws.data_ptr(),
+                                              ws.numel(), _stream_ptr(stream)))
+        return out
+
     def infer_host(self, x: np.ndarray) -> np.ndarray:
         """latq::infer calling convention: host f64 [batch, n] -> host f64 [batch, m]."""
         info = self.info
@@ -585,6 +651,21 @@ def forward_sharded_sim(shards, x, stream=None):
     arr = (ctypes.c_void_p * len(shards))(*[S._h.value for S in shards])
     _check(lib().q8p_forward_sharded_sim(arr, len(shards), x.data_ptr(), y.data_ptr(), x.shape[0], ws.data_ptr(),
                                          ws.numel(), _stream_ptr(stream)))
+    return y
+
+
+def forward_sharded_push_sim(shards, peers, x, stream=None):
+    """q8p_forward_sharded_push_sim: every rank's push forward on one GPU (peers
+    wired by PeerGroup.connect_local); returns [world, batch, m] (each rank's y)."""
+    torch = _torch()
+    info = shards[0].info
+    shards[0]._check_x(x, info["n"])
+    y = torch.empty(len(shards), x.shape[0], info["m"], dtype=torch.float32, device=x.device)
+    ws = shards[0].workspace(x.shape[0])
+    arr = (ctypes.c_void_p * len(shards))(*[S._h.value for S in shards])
+    parr = (ctypes.c_void_p * len(peers))(*[p._h.value for p in peers])
+    _check(lib().q8p_forward_sharded_push_sim(arr, parr, len(shards), x.data_ptr(), y.data_ptr(), x.shape[0],
+                                              ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
     return y
 
 

@@ -537,6 +537,85 @@ void forward_sharded_impl(const q8p_layer* L, const float* x, float* y, int batc
   }
 }
 
+// K3 pass 1 of one rank for the push all-gather (q8p_forward_sharded_push): the
+// rank's rows straight into every rank's window.
+void k3_push(const q8p_layer* L, const Workspace& w, const PushArgs& pa, int nb, cudaStream_t s) {
+  float zscale[2] = {L->scale[0], L->scale[1]};
+  int ze8p[2] = {L->cb[0] == Q8P_CB_E8P_2BIT, L->cb[1] == Q8P_CB_E8P_2BIT};
+  launch_rht_out_acc_push(L->side_u, w.zacc, L->num_stages, w.rows_pad, std::uint32_t(tc_ncols_pad(4 * nb)), zscale,
+                          ze8p, w.alpha, w.tl, L->row_begin, L->m_local(), pa, nb, s);
+}
+
+}  // namespace
+}  // namespace q8p::detail
+
+// Peer group of the push all-gather (device.hpp PeerCtl / PushArgs).
+struct q8p_peers {
+  int device = 0, world = 1, rank = 0;
+  std::size_t slice_floats = 0;          // per-rank slice capacity of one parity (values)
+  void* base = nullptr;                  // local allocation [PeerCtl][2][world][slice] words
+  std::vector<void*> opened;             // peers' bases mapped by CUDA IPC (closed at destroy)
+  std::vector<void*> bases;              // every rank's base as this process maps it
+  bool connected = false;
+  q8p::detail::PushArgs args() const {
+    q8p::detail::PushArgs a{};
+    for (int r = 0; r < world; ++r)
+      a.win[r] = reinterpret_cast<unsigned long long*>(static_cast<std::uint8_t*>(bases[r]) +
+                                                        q8p::detail::kPeerCtlBytes);
+    a.ctl = static_cast<q8p::detail::PeerCtl*>(base);
+    a.rank = rank;
+    a.world = world;
+    a.win_words = std::size_t(world) * slice_floats;
+    return a;
+  }
+};
+
+namespace q8p::detail {
+namespace {
+
+std::size_t peer_bytes(int world, std::size_t slice_floats) {
+  return kPeerCtlBytes + 2 * std::size_t(world) * slice_floats * 8;  // tagged 8-byte words
+}
+
+void peers_set_bases(q8p_peers* p, const std::vector<void*>& bases) {
+  p->bases = bases;
+  p->connected = true;
+}
+
+void check_push_layer(const q8p_layer* L, const q8p_peers* p, int batch) {
+  if (!L || !p) throw ValidationError("null layer / peers");
+  if (!p->connected) throw ValidationError("peers not connected");
+  if (L->device != p->device) throw ValidationError("layer and peers on different devices");
+  const std::uint32_t ml = L->m_local();
+  if (std::size_t(ml) * std::size_t(p->world) != L->m || L->row_begin != std::uint32_t(p->rank) * ml)
+    throw ValidationError("row shards must be equal-sized and ordered by rank");
+  if (tc_chunk(L, batch) == 0) throw UnsupportedError("push all-gather needs the tensor-core path");
+  if (!rht_sharded_k3_ok(L->side_u, L->row_begin, ml))
+    throw UnsupportedError("push all-gather: a rank's rows must be whole K3 pass-1 chunks (rht layers)");
+  if (std::size_t(std::min(tc_chunk(L, batch), batch)) * ml > p->slice_floats)
+    throw SizeError("push all-gather: window slice too small for this layer / batch");
+}
+
+void forward_push_impl(const q8p_layer* L, q8p_peers* p, const float* x, float* y, int batch, void* ws,
+                       std::size_t ws_bytes, cudaStream_t s) {
+  if (batch < 0) throw ValidationError("negative batch");
+  if (batch == 0) return;
+  if (!x || !y) throw ValidationError("null x / y");
+  check_push_layer(L, p, batch);
+  if (!ws || ws_bytes < workspace_size(L, batch)) throw SizeError("workspace too small");
+  DeviceGuard g(L->device);
+  Workspace w;
+  workspace_parts(L, batch, &w, ws);
+  const PushArgs pa = p->args();
+  const int chunk = tc_chunk(L, batch);
+  for (int b0 = 0; b0 < batch; b0 += chunk) {  // one push epoch per chunk
+    const int nb = std::min(chunk, batch - b0);
+    forward_local(L, x + std::size_t(b0) * L->n, nb, w, s, nullptr);
+    k3_push(L, w, pa, nb, s);
+    launch_rht_out_pass2_push(L->side_u, L->m_local(), pa, y + std::size_t(b0) * L->m, nb, s);
+  }
+}
+
 void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void* ws, std::size_t ws_bytes,
                   cudaStream_t s, const q8p_forward_opts* opts = nullptr) {
   if (!L) throw ValidationError("null layer");
@@ -1503,6 +1582,155 @@ q8p_status q8p_forward_sharded_sim(const q8p_layer* const* shards, int world, co
                  "gather copy");
     }
     launch_rht_out_pass2_gathered(L0->side_u, w.z_full, ml, y, batch, s);
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_peers_create(int device, int world, int rank, size_t slice_floats, q8p_peers** out,
+                            uint8_t handle[Q8P_PEER_HANDLE_BYTES]) {
+  q8p_peers* p = nullptr;
+  try {
+    if (!out || !handle) throw q8p::ValidationError("null argument");
+    *out = nullptr;
+    if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world) throw q8p::ValidationError("bad world / rank");
+    if (slice_floats == 0 || slice_floats % 4 != 0) throw q8p::ValidationError("slice_floats must be a positive multiple of 4");
+    DeviceGuard g(device);
+    p = new q8p_peers;
+    p->device = device;
+    p->world = world;
+    p->rank = rank;
+    p->slice_floats = slice_floats;
+    const std::size_t bytes = peer_bytes(world, slice_floats);
+    cuda_check(cudaMalloc(&p->base, bytes), "cudaMalloc peer window");
+    cuda_check(cudaMemset(p->base, 0, bytes), "peer window init");  // tag 0: never a call's tag
+    static_assert(sizeof(cudaIpcMemHandle_t) <= Q8P_PEER_HANDLE_BYTES, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    cuda_check(cudaIpcGetMemHandle(&h, p->base), "cudaIpcGetMemHandle");
+    std::memset(handle, 0, Q8P_PEER_HANDLE_BYTES);
+    std::memcpy(handle, &h, sizeof(h));
+    cuda_check(cudaDeviceSynchronize(), "peer window init");
+    *out = p;
+    return Q8P_OK;
+  } catch (...) {
+    if (p) q8p_peers_destroy(p);
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_peers_connect(q8p_peers* p, const uint8_t* handles) {
+  try {
+    if (!p || !handles) throw q8p::ValidationError("null argument");
+    if (p->connected) throw q8p::ValidationError("peers already connected");
+    DeviceGuard g(p->device);
+    std::vector<void*> bases(p->world);
+    for (int r = 0; r < p->world; ++r) {
+      if (r == p->rank) {
+        bases[r] = p->base;
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles + std::size_t(r) * Q8P_PEER_HANDLE_BYTES, sizeof(h));
+      void* ptr = nullptr;
+      cuda_check(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+      p->opened.push_back(ptr);
+      bases[r] = ptr;
+    }
+    peers_set_bases(p, bases);
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_peers_connect_local(q8p_peers* const* group, int world) {
+  try {
+    if (!group || world < 1) throw q8p::ValidationError("null argument");
+    std::vector<void*> bases(world);
+    for (int r = 0; r < world; ++r) {
+      if (!group[r] || group[r]->world != world || group[r]->rank != r || group[r]->device != group[0]->device ||
+          group[r]->slice_floats != group[0]->slice_floats || group[r]->connected)
+        throw q8p::ValidationError("peers must be the unconnected, rank-ordered members of one group on one device");
+      bases[r] = group[r]->base;
+    }
+    DeviceGuard g(group[0]->device);
+    for (int r = 0; r < world; ++r) peers_set_bases(group[r], bases);
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_peers_state(const q8p_peers* p, uint64_t* epoch) {
+  try {
+    if (!p || !epoch) throw q8p::ValidationError("null argument");
+    DeviceGuard g(p->device);
+    PeerCtl c;
+    cuda_check(cudaMemcpy(&c, p->base, sizeof(c), cudaMemcpyDeviceToHost), "peer state read");
+    *epoch = c.epoch;
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_peers_destroy(q8p_peers* p) {
+  if (!p) return Q8P_OK;
+  try {
+    DeviceGuard g(p->device);
+    cudaDeviceSynchronize();
+    for (void* ptr : p->opened) cudaIpcCloseMemHandle(ptr);
+    if (p->base) cudaFree(p->base);
+    delete p;
+    return Q8P_OK;
+  } catch (...) {
+    delete p;
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_forward_sharded_push(const q8p_layer* L, q8p_peers* peers, const float* x, float* y, int batch,
+                                    void* ws, size_t ws_bytes, void* stream) {
+  try {
+    forward_push_impl(L, peers, x, y, batch, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+    return Q8P_OK;
+  } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_forward_sharded_push_sim(const q8p_layer* const* shards, q8p_peers* const* peers, int world,
+                                        const float* x, float* y, int batch, void* ws, size_t ws_bytes,
+                                        void* stream) {
+  try {
+    if (!shards || !peers || world < 1 || !x || !y || !ws) throw q8p::ValidationError("null argument");
+    if (batch <= 0) return Q8P_OK;
+    for (int r = 0; r < world; ++r) {
+      if (!peers[r] || peers[r]->world != world || peers[r]->rank != r) throw q8p::ValidationError("peers out of order");
+      check_push_layer(shards[r], peers[r], batch);
+      if (shards[r]->m != shards[0]->m || shards[r]->n != shards[0]->n)
+        throw q8p::ValidationError("shards of different layers");
+      if (ws_bytes < workspace_size(shards[r], batch)) throw q8p::SizeError("workspace too small");
+    }
+    const q8p_layer* L0 = shards[0];
+    DeviceGuard g(L0->device);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int chunk = tc_chunk(L0, batch);
+    Workspace w;
+    for (int b0 = 0; b0 < batch; b0 += chunk) {
+      const int nb = std::min(chunk, batch - b0);
+      // every rank's K1, K2 and pushing pass 1 in turn, then every rank's pass 2
+      // (each waits for all ranks' arrivals, already complete in stream order)
+      for (int r = 0; r < world; ++r) {
+        workspace_parts(shards[r], batch, &w, ws);
+        forward_local(shards[r], x + std::size_t(b0) * L0->n, nb, w, s, nullptr);
+        k3_push(shards[r], w, peers[r]->args(), nb, s);
+      }
+      for (int r = 0; r < world; ++r)
+        launch_rht_out_pass2_push(L0->side_u, L0->m_local(), peers[r]->args(),
+                                  y + (std::size_t(r) * batch + b0) * L0->m, nb, s);
+    }
     return Q8P_OK;
   } catch (...) {
     return status_of_current_exception();

@@ -216,6 +216,36 @@ void launch_rht_out_pass2_gathered(const DevSide& side, const float* mid_gathere
                                    int batch, cudaStream_t s);
 void launch_rht_out_gathered(const DevSide& side, const float* z_gathered, std::uint32_t m_local, float* u_scratch,
                              float* y, int batch, cudaStream_t s);
+// Push all-gather (q8p_forward_sharded_push).  Each rank owns
+// one device allocation [PeerCtl][2 parities][world][slice] of 8-byte words
+// {float bits, call tag} whose base the other ranks map (CUDA IPC over NVLink /
+// NVSwitch).  K3 pass 1 stores every value of its rows, tagged with the call
+// number, straight into every rank's window of the call's parity; an aligned
+// 8-byte store is single-copy atomic, so a reader that sees the tag sees the value
+// (the LL protocol: no fences, no counters).  K3 pass 2 polls its own window until
+// every word it needs carries this call's tag; its last CTA advances the rank's
+// call counter (epoch).  Two parities: a rank runs at most one call ahead of a
+// peer (its pass 2 needs the peer's pass 1 of the same call), so a parity is never
+// overwritten while it is read.
+constexpr int kMaxPeers = 16;
+struct PeerCtl {
+  unsigned long long epoch;  // calls completed on this rank (parity = epoch & 1, tag = epoch + 1)
+  unsigned long long done;   // pass-2 CTAs finished in the current call
+};
+constexpr std::size_t kPeerCtlBytes = 256;
+static_assert(sizeof(PeerCtl) <= kPeerCtlBytes, "peer control block");
+struct PushArgs {
+  unsigned long long* win[kMaxPeers];  // every rank's window (parity 0) as this process maps it
+  PeerCtl* ctl;                        // this rank's control block
+  int rank, world;
+  std::size_t win_words;               // words per parity (world * slice)
+};
+void launch_rht_out_acc_push(const DevSide& side, const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows,
+                             std::uint32_t zacc_cols, const float zscale[2], const int ze8p[2], const float* alpha,
+                             const long long* tl, std::uint32_t row0, std::uint32_t m_local, const PushArgs& push,
+                             int batch, cudaStream_t s);
+void launch_rht_out_pass2_push(const DevSide& side, std::uint32_t m_local, const PushArgs& push, float* y, int batch,
+                               cudaStream_t s);
 // Row-sharded forward: this rank's fp32 z rows [batch][m_local] from the limb accumulators.
 void launch_combine_acc(const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows, std::uint32_t zacc_cols,
                         const float zscale[2], const int ze8p[2], const float* alpha, const long long* tl, float* z,

@@ -49,6 +49,8 @@ __global__ void __launch_bounds__(kP1Threads) rht_pass1(RhtArgs a) {
   extern __shared__ __align__(16) float sm1[];
   pdl_wait();
   pdl_trigger();
+  // push all-gather: this call's tag (the previous call's pass 2 finished before our predecessors)
+  if (a.push.ctl) a.ll_tag = std::uint32_t(ld_epoch(a.push.ctl) + 1);
   const std::uint32_t nch = a.p1_count ? a.p1_count : a.P1;  // chunk CTAs (this rank's, when sharded)
   if (blockIdx.x >= nch) {
     if (blockIdx.y == 0) {
@@ -105,6 +107,16 @@ __global__ void __launch_bounds__(256) rht_pass2(RhtArgs a) {
   const int team = a.warp_teams ? int(threadIdx.x >> 5) : 0, teams = a.warp_teams ? int(blockDim.x >> 5) : 1;
   float* const s = sm2 + std::size_t(team) * a.P1 * 4;
   const int vpb = a.vpb > 1 ? a.vpb : 1, b_end = min(a.batch, int(blockIdx.y + 1) * vpb);
+  if (a.push.ctl) {  // push all-gather: read this call's window as its tagged words arrive
+    // (the epoch was advanced by the previous call's pass 2, complete before our predecessors ran)
+    const unsigned long long e = ld_epoch(a.push.ctl);
+    RhtArgs w = a;
+    w.ll_mid = a.push.win[a.push.rank] + (e & 1) * a.push.win_words;
+    w.ll_tag = std::uint32_t(e + 1);
+    for (int b = int(blockIdx.y) * vpb + team; b < b_end; b += teams) rht_p2_body(w, blockIdx.x, b, s, red, tm);
+    push_done(a, e);
+    return;
+  }
   for (int b = int(blockIdx.y) * vpb + team; b < b_end; b += teams) rht_p2_body(a, blockIdx.x, b, s, red, tm);
 }
 
@@ -387,6 +399,53 @@ void launch_rht_out_acc_local(const DevSide& side, const std::int32_t* zacc, int
   a.row0 = row0;
   a.p1_out_rows = m_local;
   launch_pass1(a, 0, s);
+}
+
+void launch_rht_out_acc_push(const DevSide& side, const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows,
+                             std::uint32_t zacc_cols, const float zscale[2], const int ze8p[2], const float* alpha,
+                             const long long* tl, std::uint32_t row0, std::uint32_t m_local, const PushArgs& push,
+                             int batch, cudaStream_t s) {
+  RhtArgs a{};
+  plan_split_impl(side, a);
+  const std::uint32_t chunk = a.P2 * a.q;
+  a.signs = side.signs;
+  a.base = side.base;
+  a.zacc = zacc;
+  a.zrows = zacc_rows;
+  a.zcols = zacc_cols;
+  a.zstages = zacc_stages;
+  a.zscale0 = zscale[0];
+  a.zscale1 = zscale[1];
+  a.ze8p0 = ze8p[0];
+  a.ze8p1 = ze8p[1];
+  a.alpha_in = alpha;
+  a.tl_in = tl;
+  a.batch = batch;
+  a.fwd = 0;
+  a.ch0 = row0 / chunk;
+  a.p1_count = m_local / chunk;
+  a.row0 = row0;
+  a.p1_out_rows = m_local;
+  a.push = push;
+  launch_pass1(a, 0, s);
+}
+
+void launch_rht_out_pass2_push(const DevSide& side, std::uint32_t m_local, const PushArgs& push, float* y, int batch,
+                               cudaStream_t s) {
+  RhtArgs a{};
+  plan_split_impl(side, a);
+  const std::uint32_t chunk = a.P2 * a.q;
+  a.signs = side.signs;
+  a.base = side.base;
+  a.mid_rows = m_local;
+  a.out = y;
+  a.batch = batch;
+  a.fwd = 0;
+  a.push = push;
+  const int vpb = vectors_per_block(batch);
+  a.vpb = vpb;
+  if (vpb > 1) throw UnsupportedError("push all-gather: batches of at most 32 vectors per call");
+  launch_pass2(a, s);
 }
 
 void launch_rht_out_pass2_gathered(const DevSide& side, const float* mid_gathered, std::uint32_t m_local, float* y,

@@ -13,6 +13,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 
 namespace q8p::detail {
 
@@ -57,6 +58,13 @@ struct RhtArgs {
   std::uint32_t ch0, p1_count, row0, p1_out_rows, mid_rows, in_rows;
   int vpb;                      // vectors per CTA (fp32 passes; 0/1 = one)
   int in_parts;                 // pass 1 fp32 input = sum of in_parts partial arrays [batch][n] (0/1 = one)
+  // Push all-gather (device.hpp PushArgs; push.ctl == nullptr = off): pass 1 stores
+  // its rows as tagged words into every rank's window (rank-major
+  // [world][batch][p1_out_rows]); pass 2 reads its own window (ll_mid, set by the
+  // kernel for the call's parity) once the words carry the call's tag ll_tag.
+  PushArgs push;
+  const unsigned long long* ll_mid;
+  std::uint32_t ll_tag;
   int warp_teams;               // fp32 passes: one vector per warp (vpb > 1; set by the launchers)
 };
 
@@ -73,6 +81,50 @@ struct Team {
 
 namespace {
 
+
+// Push all-gather, LL protocol (device.hpp).  A tagged word = float bits | tag << 32.
+__device__ __forceinline__ unsigned long long ll_word(float v, std::uint32_t tag) {
+  return (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(v);
+}
+__device__ __forceinline__ unsigned long long ld_epoch(const PeerCtl* c) {
+  return *reinterpret_cast<const volatile unsigned long long*>(&c->epoch);
+}
+// Four consecutive tagged words (16 B aligned) once all carry `tag`; a peer that
+// never writes them makes the reader trap after ~20 s.
+__device__ __forceinline__ float4 ll_load4(const unsigned long long* p, std::uint32_t tag, int rank) {
+  unsigned long long w0, w1, w2, w3;
+  std::uint64_t t0 = 0;
+  for (int spin = 0;; ++spin) {
+    asm volatile("ld.volatile.v2.u64 {%0, %1}, [%2];\n" : "=l"(w0), "=l"(w1) : "l"(p));
+    asm volatile("ld.volatile.v2.u64 {%0, %1}, [%2];\n" : "=l"(w2), "=l"(w3) : "l"(p + 2));
+    if (std::uint32_t(w0 >> 32) == tag && std::uint32_t(w1 >> 32) == tag && std::uint32_t(w2 >> 32) == tag &&
+        std::uint32_t(w3 >> 32) == tag)
+      break;
+    std::uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (spin == 0) t0 = t;
+    if (t - t0 > 20000000000ull) {
+      printf("q8p push all-gather: rank %d waited 20 s for call tag %u (word has tag %u)\n", rank, tag,
+             std::uint32_t(w0 >> 32));
+      __trap();
+    }
+    __nanosleep(32);
+  }
+  return make_float4(__uint_as_float(std::uint32_t(w0)), __uint_as_float(std::uint32_t(w1)),
+                     __uint_as_float(std::uint32_t(w2)), __uint_as_float(std::uint32_t(w3)));
+}
+// End of a pass-2 CTA: the last one of the call advances the rank's epoch.
+__device__ __forceinline__ void push_done(const RhtArgs& a, unsigned long long e) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long total = std::uint64_t(gridDim.x) * gridDim.y;
+    if (atomicAdd(&a.push.ctl->done, 1ull) == total - 1) {
+      a.push.ctl->done = 0;
+      __threadfence();
+      *reinterpret_cast<volatile unsigned long long*>(&a.push.ctl->epoch) = e + 1;
+    }
+  }
+}
 
 __device__ __forceinline__ Team block_team() { return Team{threadIdx.x, blockDim.x, 0u}; }
 __device__ __forceinline__ Team warp_team() { return Team{threadIdx.x & 31u, 32u, 1u}; }
@@ -337,10 +389,24 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* xs
     cur = y;
   }
   fwht_rows<Q>(cur, a.P2, tm);
-  float* const mo = a.p1_out_rows ? a.mid + std::size_t(b) * a.p1_out_rows + (e0 - a.row0)
-                                  : a.mid + std::size_t(b) * a.n + e0;
-  for (std::uint32_t v = tm.tid; v < chunk / 4; v += tm.n)
-    *reinterpret_cast<float4*>(mo + 4 * v) = reinterpret_cast<float4*>(cur)[v];
+  if (a.push.ctl) {
+    // push all-gather: this rank's slice of every rank's window, tagged words (NVLink stores)
+    const std::size_t off = (a.ll_tag & 1 ? 0 : a.push.win_words) +  // parity = epoch & 1 = (tag - 1) & 1
+                            (std::size_t(a.push.rank) * a.batch + b) * a.p1_out_rows + (e0 - a.row0);
+    for (int r = 0; r < a.push.world; ++r) {
+      unsigned long long* const mo = a.push.win[r] + off;
+      for (std::uint32_t v = tm.tid; v < chunk / 4; v += tm.n) {
+        const float4 c = reinterpret_cast<float4*>(cur)[v];
+        reinterpret_cast<ulonglong2*>(mo + 4 * v)[0] = make_ulonglong2(ll_word(c.x, a.ll_tag), ll_word(c.y, a.ll_tag));
+        reinterpret_cast<ulonglong2*>(mo + 4 * v)[1] = make_ulonglong2(ll_word(c.z, a.ll_tag), ll_word(c.w, a.ll_tag));
+      }
+    }
+  } else {
+    float* const mo = a.p1_out_rows ? a.mid + std::size_t(b) * a.p1_out_rows + (e0 - a.row0)
+                                    : a.mid + std::size_t(b) * a.n + e0;
+    for (std::uint32_t v = tm.tid; v < chunk / 4; v += tm.n)
+      *reinterpret_cast<float4*>(mo + 4 * v) = reinterpret_cast<float4*>(cur)[v];
+  }
   team_sync(tm);  // smem reusable by the caller
 }
 
@@ -348,9 +414,11 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* xs
 __device__ void rht_p2_body(const RhtArgs& a, std::uint32_t cg, int b, float* sm2, float* red, const Team& tm) {
   const std::uint32_t stride = a.P2 * a.q;  // elements between consecutive a_hi
   const std::uint32_t col = cg * 4;         // 4 adjacent columns
-  for (std::uint32_t r = tm.tid; r < a.P1; r += tm.n)
-    reinterpret_cast<float4*>(sm2)[r] =
-        __ldcg(reinterpret_cast<const float4*>(a.mid + rank_major(b, r * stride + col, a.mid_rows, a.batch, a.n)));
+  for (std::uint32_t r = tm.tid; r < a.P1; r += tm.n) {
+    const std::size_t idx = rank_major(b, r * stride + col, a.mid_rows, a.batch, a.n);
+    reinterpret_cast<float4*>(sm2)[r] = a.ll_mid ? ll_load4(a.ll_mid + idx, a.ll_tag, a.push.rank)
+                                                 : __ldcg(reinterpret_cast<const float4*>(a.mid + idx));
+  }
   team_sync(tm);
   fwht_rows<4>(sm2, a.P1, tm);
   const float sc = rsqrtf(float(a.n));
