@@ -555,13 +555,12 @@ struct q8p_peers {
   std::size_t slice_floats = 0;          // per-rank slice capacity of one parity (values)
   void* base = nullptr;                  // local allocation [PeerCtl][2][world][slice] words
   std::vector<void*> opened;             // peers' bases mapped by CUDA IPC (closed at destroy)
-  std::vector<void*> bases;              // every rank's base as this process maps it
+  unsigned long long** d_wins = nullptr; // device table [world] of the ranks' windows
   bool connected = false;
   q8p::detail::PushArgs args() const {
     q8p::detail::PushArgs a{};
-    for (int r = 0; r < world; ++r)
-      a.win[r] = reinterpret_cast<unsigned long long*>(static_cast<std::uint8_t*>(bases[r]) +
-                                                        q8p::detail::kPeerCtlBytes);
+    a.wins = d_wins;
+    a.self_win = reinterpret_cast<unsigned long long*>(static_cast<std::uint8_t*>(base) + q8p::detail::kPeerCtlBytes);
     a.ctl = static_cast<q8p::detail::PeerCtl*>(base);
     a.rank = rank;
     a.world = world;
@@ -578,7 +577,10 @@ std::size_t peer_bytes(int world, std::size_t slice_floats) {
 }
 
 void peers_set_bases(q8p_peers* p, const std::vector<void*>& bases) {
-  p->bases = bases;
+  std::vector<unsigned long long*> w(p->world);
+  for (int r = 0; r < p->world; ++r)
+    w[r] = reinterpret_cast<unsigned long long*>(static_cast<std::uint8_t*>(bases[r]) + kPeerCtlBytes);
+  cuda_check(cudaMemcpy(p->d_wins, w.data(), sizeof(void*) * p->world, cudaMemcpyHostToDevice), "peer table");
   p->connected = true;
 }
 
@@ -1605,6 +1607,7 @@ q8p_status q8p_peers_create(int device, int world, int rank, size_t slice_floats
     const std::size_t bytes = peer_bytes(world, slice_floats);
     cuda_check(cudaMalloc(&p->base, bytes), "cudaMalloc peer window");
     cuda_check(cudaMemset(p->base, 0, bytes), "peer window init");  // tag 0: never a call's tag
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&p->d_wins), sizeof(void*) * world), "cudaMalloc peer table");
     static_assert(sizeof(cudaIpcMemHandle_t) <= Q8P_PEER_HANDLE_BYTES, "IPC handle size");
     cudaIpcMemHandle_t h;
     cuda_check(cudaIpcGetMemHandle(&h, p->base), "cudaIpcGetMemHandle");
@@ -1681,6 +1684,7 @@ q8p_status q8p_peers_destroy(q8p_peers* p) {
     DeviceGuard g(p->device);
     cudaDeviceSynchronize();
     for (void* ptr : p->opened) cudaIpcCloseMemHandle(ptr);
+    if (p->d_wins) cudaFree(p->d_wins);
     if (p->base) cudaFree(p->base);
     delete p;
     return Q8P_OK;

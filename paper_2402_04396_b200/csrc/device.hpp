@@ -235,7 +235,8 @@ struct PeerCtl {
 constexpr std::size_t kPeerCtlBytes = 256;
 static_assert(sizeof(PeerCtl) <= kPeerCtlBytes, "peer control block");
 struct PushArgs {
-  unsigned long long* win[kMaxPeers];  // every rank's window (parity 0) as this process maps it
+  unsigned long long* const* wins;     // device table [world]: every rank's window (parity 0) as mapped here
+  unsigned long long* self_win;        // this rank's window (parity 0)
   PeerCtl* ctl;                        // this rank's control block
   int rank, world;
   std::size_t win_words;               // words per parity (world * slice)

@@ -43,14 +43,16 @@ __global__ void __launch_bounds__(256) combine_kernel(RhtArgs a, float* z, std::
 
 constexpr int kP1Threads = 256;
 
-// Pass 1.  grid = (P1 chunks [+ zeroing CTAs], batch).
-template <int Q>
+// Pass 1.  grid = (P1 chunks [+ zeroing CTAs], batch / vpb).  kWarp: one vector
+// per warp (prefill batches, a.warp_teams), else the whole CTA on one vector
+// (compile-time, so each flavour's barriers and loops specialise).
+template <int Q, bool kWarp>
 __global__ void __launch_bounds__(kP1Threads) rht_pass1(RhtArgs a) {
   extern __shared__ __align__(16) float sm1[];
   pdl_wait();
   pdl_trigger();
   // push all-gather: this call's tag (the previous call's pass 2 finished before our predecessors)
-  if (a.push.ctl) a.ll_tag = std::uint32_t(ld_epoch(a.push.ctl) + 1);
+  const std::uint32_t ll_tag = a.push.ctl ? std::uint32_t(ld_epoch(a.push.ctl) + 1) : 0u;
   const std::uint32_t nch = a.p1_count ? a.p1_count : a.P1;  // chunk CTAs (this rank's, when sharded)
   if (blockIdx.x >= nch) {
     if (blockIdx.y == 0) {
@@ -69,12 +71,14 @@ __global__ void __launch_bounds__(kP1Threads) rht_pass1(RhtArgs a) {
   }
   __shared__ float red1[32];
   float* const Bs = sm1;
-  p1_load_base<Q>(a, Bs);
-  __syncthreads();
+  if constexpr (kWarp) {  // shared by the CTA's warp teams: once, up front (else the body loads it)
+    p1_load_base<Q>(a, Bs);
+    __syncthreads();
+  }
   // vectors blockIdx.y * vpb .. : large batches amortise the CTA over several vectors,
-  // one per warp (warp_teams) so a pass's barriers are warp-local
-  const Team tm = a.warp_teams ? warp_team() : block_team();
-  const int team = a.warp_teams ? int(threadIdx.x >> 5) : 0, teams = a.warp_teams ? int(blockDim.x >> 5) : 1;
+  // one per warp so a pass's barriers are warp-local
+  const Team tm = kWarp ? warp_team() : block_team();
+  const int team = kWarp ? int(threadIdx.x >> 5) : 0, teams = kWarp ? int(blockDim.x >> 5) : 1;
   float* const xs = sm1 + p1_base_bytes<Q>() / 4 + std::size_t(team) * (p1_team_bytes<Q>(a.P2) / 4);
   const int vpb = a.vpb > 1 ? a.vpb : 1, b_end = min(a.batch, int(blockIdx.y + 1) * vpb);
   for (int b = int(blockIdx.y) * vpb + team; b < b_end; b += teams) {
@@ -92,12 +96,14 @@ __global__ void __launch_bounds__(kP1Threads) rht_pass1(RhtArgs a) {
         a.tsum_out[b] = acc * float(a.p) * rsqrtf(float(a.n));
       }
     }
-    rht_p1_body<Q>(a, a.ch0 + blockIdx.x, b, xs, Bs, red1, tm);
+    rht_p1_body<Q>(a, a.ch0 + blockIdx.x, b, xs, Bs, red1, tm, ll_tag);
   }
 }
 
 // Pass 2.  grid = (P2 * q / 4 column groups, batch / vpb); block = 128 threads,
-// or one warp per vector (warp_teams).
+// or one warp per vector (warp_teams).  kPush: the push all-gather's flavour
+// (its own instantiation, so the polling path costs the plain one nothing).
+template <bool kPush>
 __global__ void __launch_bounds__(256) rht_pass2(RhtArgs a) {
   extern __shared__ __align__(16) float sm2[];
   __shared__ float red[32];
@@ -107,17 +113,16 @@ __global__ void __launch_bounds__(256) rht_pass2(RhtArgs a) {
   const int team = a.warp_teams ? int(threadIdx.x >> 5) : 0, teams = a.warp_teams ? int(blockDim.x >> 5) : 1;
   float* const s = sm2 + std::size_t(team) * a.P1 * 4;
   const int vpb = a.vpb > 1 ? a.vpb : 1, b_end = min(a.batch, int(blockIdx.y + 1) * vpb);
-  if (a.push.ctl) {  // push all-gather: read this call's window as its tagged words arrive
+  if constexpr (kPush) {  // push all-gather: read this call's window as its tagged words arrive
     // (the epoch was advanced by the previous call's pass 2, complete before our predecessors ran)
     const unsigned long long e = ld_epoch(a.push.ctl);
-    RhtArgs w = a;
-    w.ll_mid = a.push.win[a.push.rank] + (e & 1) * a.push.win_words;
-    w.ll_tag = std::uint32_t(e + 1);
-    for (int b = int(blockIdx.y) * vpb + team; b < b_end; b += teams) rht_p2_body(w, blockIdx.x, b, s, red, tm);
+    const unsigned long long* const win = a.push.self_win + (e & 1) * a.push.win_words;
+    for (int b = int(blockIdx.y) * vpb + team; b < b_end; b += teams)
+      rht_p2_body(a, blockIdx.x, b, s, red, tm, win, std::uint32_t(e + 1));
     push_done(a, e);
-    return;
+  } else {
+    for (int b = int(blockIdx.y) * vpb + team; b < b_end; b += teams) rht_p2_body(a, blockIdx.x, b, s, red, tm);
   }
-  for (int b = int(blockIdx.y) * vpb + team; b < b_end; b += teams) rht_p2_body(a, blockIdx.x, b, s, red, tm);
 }
 
 // Pass 2 for prefill batches (P1 <= 64): one warp per (vector, 32 adjacent flat
@@ -212,9 +217,10 @@ void launch_pass1_q(const RhtArgs& a, std::uint32_t extra_ctas, cudaStream_t s) 
   const int vpb = a.vpb > 1 ? a.vpb : 1;
   b.warp_teams = vpb == kP1Threads / 32;  // prefill batches: one vector per warp
   const std::size_t smem = p1_base_bytes<Q>() + (b.warp_teams ? vpb : 1) * p1_team_bytes<Q>(a.P2);
-  kernel_attrs(reinterpret_cast<const void*>(rht_pass1<Q>), 96 * 1024);
-  launch_pdl(rht_pass1<Q>, dim3((a.p1_count ? a.p1_count : a.P1) + extra_ctas, (a.batch + vpb - 1) / vpb),
-             dim3(kP1Threads), smem, s, b);
+  auto* k = b.warp_teams ? rht_pass1<Q, true> : rht_pass1<Q, false>;
+  kernel_attrs(reinterpret_cast<const void*>(k), 96 * 1024);
+  launch_pdl(k, dim3((a.p1_count ? a.p1_count : a.P1) + extra_ctas, (a.batch + vpb - 1) / vpb), dim3(kP1Threads),
+             smem, s, b);
 }
 
 void launch_pass1(const RhtArgs& a, std::uint32_t extra, cudaStream_t s) {
@@ -250,12 +256,13 @@ void launch_pass2(const RhtArgs& a, cudaStream_t s) {
     }
   } else {
     const std::uint32_t groups = a.P2 * a.q / 4;
-    kernel_attrs(reinterpret_cast<const void*>(rht_pass2), 96 * 1024);
+    auto* k = a.push.ctl ? rht_pass2<true> : rht_pass2<false>;
+    kernel_attrs(reinterpret_cast<const void*>(k), 96 * 1024);
     RhtArgs b = a;
     const int vpb = a.vpb > 1 ? a.vpb : 1;
     b.warp_teams = vpb > 1 && a.P1 <= 512;  // one vector per warp while a warp's share stays small
     const int threads = b.warp_teams ? 32 * vpb : 128;
-    launch_pdl(rht_pass2, dim3(groups, (a.batch + vpb - 1) / vpb), dim3(threads),
+    launch_pdl(k, dim3(groups, (a.batch + vpb - 1) / vpb), dim3(threads),
                std::size_t(a.P1) * 16 * (b.warp_teams ? vpb : 1), s, b);
   }
   cuda_check(cudaGetLastError(), "rht pass2 launch");

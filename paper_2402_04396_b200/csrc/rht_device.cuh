@@ -60,11 +60,10 @@ struct RhtArgs {
   int in_parts;                 // pass 1 fp32 input = sum of in_parts partial arrays [batch][n] (0/1 = one)
   // Push all-gather (device.hpp PushArgs; push.ctl == nullptr = off): pass 1 stores
   // its rows as tagged words into every rank's window (rank-major
-  // [world][batch][p1_out_rows]); pass 2 reads its own window (ll_mid, set by the
-  // kernel for the call's parity) once the words carry the call's tag ll_tag.
+  // [world][batch][p1_out_rows]); pass 2 reads its own window of the call's parity
+  // once the words carry the call's tag (the kernels pass window and tag to the
+  // bodies: the kernel parameters are never written, so they stay in the constant bank).
   PushArgs push;
-  const unsigned long long* ll_mid;
-  std::uint32_t ll_tag;
   int warp_teams;               // fp32 passes: one vector per warp (vpb > 1; set by the launchers)
 };
 
@@ -89,6 +88,26 @@ __device__ __forceinline__ unsigned long long ll_word(float v, std::uint32_t tag
 __device__ __forceinline__ unsigned long long ld_epoch(const PeerCtl* c) {
   return *reinterpret_cast<const volatile unsigned long long*>(&c->epoch);
 }
+// Pass 1's output float4s [0, nv) from smem `cur` into every rank's window at word
+// offset `off`, as tagged words (NVLink stores).
+__device__ __forceinline__ void push_store(unsigned long long* const* wins, int world, const float* cur,
+                                           std::size_t off, std::uint32_t nv, std::uint32_t tag, std::uint32_t tid,
+                                           std::uint32_t nthreads) {
+#pragma unroll 1
+  for (int r = 0; r < world; ++r) {
+    unsigned long long* const mo = wins[r] + off;
+    for (std::uint32_t v = tid; v < nv; v += nthreads) {
+      const float4 c = reinterpret_cast<const float4*>(cur)[v];
+      reinterpret_cast<ulonglong2*>(mo + 4 * v)[0] = make_ulonglong2(ll_word(c.x, tag), ll_word(c.y, tag));
+      reinterpret_cast<ulonglong2*>(mo + 4 * v)[1] = make_ulonglong2(ll_word(c.z, tag), ll_word(c.w, tag));
+    }
+  }
+}
+// Cold path of ll_load4: a peer never wrote this call's words.
+__device__ __noinline__ void ll_timeout(int rank, std::uint32_t tag, std::uint32_t have) {
+  printf("q8p push all-gather: rank %d waited 20 s for call tag %u (word has tag %u)\n", rank, tag, have);
+  __trap();
+}
 // Four consecutive tagged words (16 B aligned) once all carry `tag`; a peer that
 // never writes them makes the reader trap after ~20 s.
 __device__ __forceinline__ float4 ll_load4(const unsigned long long* p, std::uint32_t tag, int rank) {
@@ -103,11 +122,7 @@ __device__ __forceinline__ float4 ll_load4(const unsigned long long* p, std::uin
     std::uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (spin == 0) t0 = t;
-    if (t - t0 > 20000000000ull) {
-      printf("q8p push all-gather: rank %d waited 20 s for call tag %u (word has tag %u)\n", rank, tag,
-             std::uint32_t(w0 >> 32));
-      __trap();
-    }
+    if (t - t0 > 20000000000ull) ll_timeout(rank, tag, std::uint32_t(w0 >> 32));
     __nanosleep(32);
   }
   return make_float4(__uint_as_float(std::uint32_t(w0)), __uint_as_float(std::uint32_t(w1)),
@@ -268,7 +283,7 @@ template <int Q>
 __host__ __device__ constexpr std::size_t p1_team_bytes(std::uint32_t P2) {
   return std::size_t(P2) * Q * 4 * (Q > 1 ? 2 : 1);
 }
-// Base into smem (whole CTA; the caller syncs).
+// Base into smem (whole CTA; synced by the caller or by the body's first team sync).
 template <int Q>
 __device__ void p1_load_base(const RhtArgs& a, float* Bs) {
   if constexpr (Q > 1) {
@@ -283,13 +298,16 @@ __device__ void p1_load_base(const RhtArgs& a, float* Bs) {
 
 // Pass 1 on chunk `ch` of vector b.  xs: the team's [2][chunk] floats; Bs: the
 // base (p1_load_base); red: >= 32 floats of team-shared smem.
+// ll_tag: the push all-gather's call tag (a.push.ctl set), else unused.
 template <int Q>
 __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* xs, const float* Bs, float* red,
-                            const Team& tm) {
+                            const Team& tm, std::uint32_t ll_tag = 0) {
   const std::uint32_t chunk = a.P2 * Q;  // floats, multiple of 4
   const std::uint32_t e0 = ch * chunk;
   float* x = xs;                          // [P2][Q]
   float* y = xs + chunk;                  // base output (Q > 1)
+  // whole-CTA team: the base load overlaps the chunk loads (the sync below covers both)
+  if (!tm.warp) p1_load_base<Q>(a, const_cast<float*>(Bs));
   float ss = 0.f;
   if (a.zacc) {
     for (std::uint32_t v = tm.tid; v < chunk / 4; v += tm.n) {
@@ -304,39 +322,16 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* xs
       }
     }
   } else {
-    // kU float4s per thread per round, so every input array's loads are in flight together
-    constexpr int kU = 4;
-    const std::uint32_t nv = chunk / 4;
-    for (std::uint32_t v0 = tm.tid; v0 < nv; v0 += kU * tm.n) {
-      float4 val[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const std::uint32_t v = v0 + u * tm.n;
-        if (v < nv) val[u] = __ldcg(reinterpret_cast<const float4*>(a.in + rank_major(b, e0 + 4 * v, a.in_rows,
-                                                                                    a.batch, a.n)));
-      }
+    for (std::uint32_t v = tm.tid; v < chunk / 4; v += tm.n) {
+      const std::uint32_t i = e0 + 4 * v;
+      float4 val = __ldcg(reinterpret_cast<const float4*>(a.in + rank_major(b, i, a.in_rows, a.batch, a.n)));
       for (int pp = 1; pp < a.in_parts; ++pp) {  // K-split partials (prefill), summed in order
-        const float* part = a.in + (std::size_t(pp) * a.batch + b) * a.n + e0;
-        float4 w4[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const std::uint32_t v = v0 + u * tm.n;
-          if (v < nv) w4[u] = __ldcg(reinterpret_cast<const float4*>(part + 4 * v));
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u)
-          val[u] = make_float4(val[u].x + w4[u].x, val[u].y + w4[u].y, val[u].z + w4[u].z, val[u].w + w4[u].w);
+        const float4 w4 = __ldcg(reinterpret_cast<const float4*>(a.in + (std::size_t(pp) * a.batch + b) * a.n + i));
+        val = make_float4(val.x + w4.x, val.y + w4.y, val.z + w4.z, val.w + w4.w);
       }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const std::uint32_t v = v0 + u * tm.n, i = e0 + 4 * v;
-        if (v < nv) {
-          float4 w = val[u];
-          ss += w.x * w.x + w.y * w.y + w.z * w.z + w.w * w.w;
-          if (a.fwd) w = sign4(w, (a.signs[i >> 3] >> (i & 4)) & 0xFu);
-          reinterpret_cast<float4*>(x)[v] = w;
-        }
-      }
+      ss += val.x * val.x + val.y * val.y + val.z * val.z + val.w * val.w;
+      if (a.fwd) val = sign4(val, (a.signs[i >> 3] >> (i & 4)) & 0xFu);
+      reinterpret_cast<float4*>(x)[v] = val;
     }
   }
   if (a.ssq) {  // deterministic per-chunk sum of squares
@@ -348,25 +343,44 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* xs
   if constexpr (Q > 1) {
     // base along each contiguous q-row: y[r][c] = sum_k B[c][k] x[r][k] (fwd) or B[k][c] (K3)
     if constexpr (Q <= 28) {
-      // lane = output column c with its base row (fwd) / column in registers; each
-      // x row is Q / 4 broadcast float4 reads; the team's warps take rows round robin
-      const std::uint32_t c = tm.tid & 31u, nw = tm.n >> 5;
-      if (c < std::uint32_t(Q)) {
-        float bc[Q];
+      if (tm.warp) {
+        // warp teams (prefill): lane = output column c with its base row (fwd) / column
+        // in registers; each x row is Q / 4 broadcast float4 reads.  Same FMA order as
+        // the per-element loop below, so both give the same bits.
+        const std::uint32_t c = tm.tid & 31u;
+        if (c < std::uint32_t(Q)) {
+          float bc[Q];
 #pragma unroll
-        for (int k = 0; k < Q; ++k) bc[k] = a.fwd ? Bs[c * Q + k] : Bs[k * Q + c];
-        for (std::uint32_t r = tm.tid >> 5; r < a.P2; r += nw) {
-          const float4* xr = reinterpret_cast<const float4*>(x + r * Q);
-          float acc = 0.f;
+          for (int k = 0; k < Q; ++k) bc[k] = a.fwd ? Bs[c * Q + k] : Bs[k * Q + c];
+          for (std::uint32_t r = 0; r < a.P2; ++r) {
+            const float4* xr = reinterpret_cast<const float4*>(x + r * Q);
+            float acc = 0.f;
 #pragma unroll
-          for (int j = 0; j < Q / 4; ++j) {
-            const float4 x4 = xr[j];
-            acc += bc[4 * j] * x4.x;
-            acc += bc[4 * j + 1] * x4.y;
-            acc += bc[4 * j + 2] * x4.z;
-            acc += bc[4 * j + 3] * x4.w;
+            for (int j = 0; j < Q / 4; ++j) {
+              const float4 x4 = xr[j];
+              acc += bc[4 * j] * x4.x;
+              acc += bc[4 * j + 1] * x4.y;
+              acc += bc[4 * j + 2] * x4.z;
+              acc += bc[4 * j + 3] * x4.w;
+            }
+            y[r * Q + c] = acc;
           }
-          y[r * Q + c] = acc;
+        }
+      } else {
+        // whole-CTA teams (decode batches): one output per thread and step (more
+        // parallel chains than the broadcast form for a single vector)
+        for (std::uint32_t e = tm.tid; e < chunk; e += tm.n) {
+          const std::uint32_t r = e / Q, c = e - r * Q;
+          const float* xr = x + r * Q;
+          float acc = 0.f;
+          if (a.fwd) {
+#pragma unroll 4
+            for (int k = 0; k < Q; ++k) acc += Bs[c * Q + k] * xr[k];
+          } else {
+#pragma unroll 4
+            for (int k = 0; k < Q; ++k) acc += Bs[k * Q + c] * xr[k];
+          }
+          y[e] = acc;
         }
       }
     } else {
@@ -390,17 +404,10 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* xs
   }
   fwht_rows<Q>(cur, a.P2, tm);
   if (a.push.ctl) {
-    // push all-gather: this rank's slice of every rank's window, tagged words (NVLink stores)
-    const std::size_t off = (a.ll_tag & 1 ? 0 : a.push.win_words) +  // parity = epoch & 1 = (tag - 1) & 1
-                            (std::size_t(a.push.rank) * a.batch + b) * a.p1_out_rows + (e0 - a.row0);
-    for (int r = 0; r < a.push.world; ++r) {
-      unsigned long long* const mo = a.push.win[r] + off;
-      for (std::uint32_t v = tm.tid; v < chunk / 4; v += tm.n) {
-        const float4 c = reinterpret_cast<float4*>(cur)[v];
-        reinterpret_cast<ulonglong2*>(mo + 4 * v)[0] = make_ulonglong2(ll_word(c.x, a.ll_tag), ll_word(c.y, a.ll_tag));
-        reinterpret_cast<ulonglong2*>(mo + 4 * v)[1] = make_ulonglong2(ll_word(c.z, a.ll_tag), ll_word(c.w, a.ll_tag));
-      }
-    }
+    push_store(a.push.wins, a.push.world, cur,
+               (ll_tag & 1 ? 0 : a.push.win_words) +  // parity = epoch & 1 = (tag - 1) & 1
+                   (std::size_t(a.push.rank) * a.batch + b) * a.p1_out_rows + (e0 - a.row0),
+               chunk / 4, ll_tag, tm.tid, tm.n);
   } else {
     float* const mo = a.p1_out_rows ? a.mid + std::size_t(b) * a.p1_out_rows + (e0 - a.row0)
                                     : a.mid + std::size_t(b) * a.n + e0;
@@ -411,13 +418,15 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* xs
 }
 
 // Pass 2 (fp32 output) on the 4-column group `cg` of vector b.  red: >= 32 floats.
-__device__ void rht_p2_body(const RhtArgs& a, std::uint32_t cg, int b, float* sm2, float* red, const Team& tm) {
+// ll_mid: the push all-gather's window of this call (tagged words, tag ll_tag), else nullptr.
+__device__ void rht_p2_body(const RhtArgs& a, std::uint32_t cg, int b, float* sm2, float* red, const Team& tm,
+                            const unsigned long long* ll_mid = nullptr, std::uint32_t ll_tag = 0) {
   const std::uint32_t stride = a.P2 * a.q;  // elements between consecutive a_hi
   const std::uint32_t col = cg * 4;         // 4 adjacent columns
   for (std::uint32_t r = tm.tid; r < a.P1; r += tm.n) {
     const std::size_t idx = rank_major(b, r * stride + col, a.mid_rows, a.batch, a.n);
-    reinterpret_cast<float4*>(sm2)[r] = a.ll_mid ? ll_load4(a.ll_mid + idx, a.ll_tag, a.push.rank)
-                                                 : __ldcg(reinterpret_cast<const float4*>(a.mid + idx));
+    reinterpret_cast<float4*>(sm2)[r] = ll_mid ? ll_load4(ll_mid + idx, ll_tag, a.push.rank)
+                                               : __ldcg(reinterpret_cast<const float4*>(a.mid + idx));
   }
   team_sync(tm);
   fwht_rows<4>(sm2, a.P1, tm);
