@@ -35,6 +35,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "device.hpp"
@@ -78,7 +81,18 @@ struct PrefillArgs {
   std::uint32_t m, batch;
   const std::uint32_t* nib;      // [256] E8P magnitude nibbles
   const uint2* e81;              // [256] e8-1bit doubled rows
+  unsigned long long* trace;     // debug timeline (Q8P_K4_TRACE builds + Q8P_TRACE): CTA 0, nullptr = off
 };
+
+// Debug timeline: trace[role][item][8] clock64 stamps of CTA 0 (role 0 MMA issuer,
+// 1 producer, 2 + w decoder warp w); compiled in only with -DQ8P_K4_TRACE.
+constexpr int kK4TraceItems = 512;
+__device__ __forceinline__ void k4_stamp(const PrefillArgs& a, int role, std::uint32_t item, int ev) {
+#ifdef Q8P_K4_TRACE
+  if (a.trace != nullptr && blockIdx.x == 0 && item < kK4TraceItems && (threadIdx.x & 31) == 0)
+    a.trace[(role * kK4TraceItems + item) * 8 + ev] = clock64();
+#endif
+}
 
 __device__ __forceinline__ std::uint32_t lds32(std::uint32_t addr) {
   std::uint32_t r;
@@ -115,8 +129,16 @@ __device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-constexpr std::uint32_t kCtLo = 0x00050301u;  // {+1,+3,+5,0}
-constexpr std::uint32_t kCtHi = 0x00FBFDFFu;  // {-1,-3,-5,0}
+// bf16 bytes of 4 v = 2 sigma d + 2 b - 1 (odd integers in [-11, 11]), looked up by
+// PRMT with the nibble sel = m | sigma << 2 (m = 0, 1, 2 for d = 1, 3, 5; the LUT
+// nibble XOR the negate flag, as in K2):
+//   high bytes, b = 0:  [3F 40 41 _ | C0 C0 C1 _]  (1, 5, 9 | -3, -7, -11)
+//               b = 1:  [40 40 41 _ | BF C0 C1 _]  (3, 7, 11 | -1, -5, -9)
+//     = the b = 0 table with byte 0 + b and byte 4 - b (no carries);
+//   low bytes,  b = 0:  [80 A0 10 _ | 40 E0 30 _]; b = 1 is the b = 0 table with the
+//     sigma slot flipped (3, 7, 11 have the low bytes of -3, -7, -11, and so on).
+constexpr std::uint32_t kHiLo = 0x0041403Fu, kHiHi = 0x00C1C0C0u;
+constexpr std::uint32_t kLoLo = 0x0010A080u, kLoHi = 0x0030E040u;
 
 // 4 v of one E8P codeword (slot jj of the 4-codeword idx / flag words, shift bit b)
 // as 8 bf16 (16 B, coordinates 0..7).
@@ -124,12 +146,14 @@ __device__ __forceinline__ uint4 e8p_bf16(std::uint32_t idx, std::uint32_t fw, i
                                           std::uint32_t tab) {
   const std::uint32_t nib = lds32(tab + idx * 4u);
   const std::uint32_t rs = jj == 0 ? fw << 2 : jj == 1 ? fw << 1 : jj == 2 ? fw : fw >> 1;
-  const std::uint32_t sel = nib ^ (rs & 0x44444444u);
-  const std::uint32_t lo = prmt(kCtLo, kCtHi, sel), hi = prmt(kCtLo, kCtHi, sel >> 16);
-  const float sh = b ? 1.f : -1.f;  // 4 v = 2 sigma d + (2 b - 1)
-  auto v = [&](std::uint32_t w, int c) { return 2.f * float(int(std::int8_t(w >> (8 * c)))) + sh; };
-  return make_uint4(bf2(v(lo, 0), v(lo, 1)), bf2(v(lo, 2), v(lo, 3)), bf2(v(hi, 0), v(hi, 1)),
-                    bf2(v(hi, 2), v(hi, 3)));
+  const std::uint32_t sel = nib ^ (rs & 0x44444444u);       // high-byte selectors
+  const std::uint32_t sel_l = sel ^ (b * 0x44444444u);      // low-byte selectors (b flips the sigma slot)
+  const std::uint32_t h_lo = kHiLo + b, h_hi = kHiHi - b;   // the b table of high bytes
+  const std::uint32_t h03 = prmt(h_lo, h_hi, sel), h47 = prmt(h_lo, h_hi, sel >> 16);
+  const std::uint32_t l03 = prmt(kLoLo, kLoHi, sel_l), l47 = prmt(kLoLo, kLoHi, sel_l >> 16);
+  // interleave (low, high) byte pairs: element c = bytes 2c, 2c + 1
+  return make_uint4(prmt(l03, h03, 0x5140u), prmt(l03, h03, 0x7362u), prmt(l47, h47, 0x5140u),
+                    prmt(l47, h47, 0x7362u));
 }
 // 4 v = 2 * doubled of an e8-1bit code.
 __device__ __forceinline__ uint4 e81_bf16(std::uint32_t code, std::uint32_t tab) {
@@ -198,10 +222,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
               for (std::uint32_t t = 0; t < kMT; ++t, ++cg) {
                 const std::uint32_t cs = cg % kCodeSlots, mt = mp * kMT + t;
                 if (cg >= kCodeSlots) mbar_wait(bar_ce + 8 * cs, ((cg / kCodeSlots) - 1) & 1);
-                const std::uint32_t bytes = a.slab_bytes[s];
+                const std::uint32_t bytes = s ? a.slab_bytes[1] : a.slab_bytes[0];
                 if (mt < a.MT) {
                   mbar_arrive_expect_tx(bar_cf + 8 * cs, bytes);
-                  bulk_g2s(sb + kOffC + cs * kCodeSlot, a.codes[s] + (std::size_t(mt) * a.KSL + kc / 8) * bytes,
+                  bulk_g2s(sb + kOffC + cs * kCodeSlot,
+                           (s ? a.codes[1] : a.codes[0]) + (std::size_t(mt) * a.KSL + kc / 8) * bytes,
                            bytes, bar_cf + 8 * cs);
                 } else {
                   mbar_arrive(bar_cf + 8 * cs);  // past the last row block: nothing to load
@@ -231,8 +256,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
         const std::uint32_t uitems = (kc1 - kc0) * nst;
         for (std::uint32_t it = 0; it < uitems; ++it, ++g) {
           const std::uint32_t sl = g % kSlots, ph = (g / kSlots) & 1;
+          k4_stamp(a, 0, g, 0);
           mbar_wait(bar_af + 8 * sl, ph);
+          k4_stamp(a, 0, g, 1);
           mbar_wait(bar_bf + 8 * sl, ph);
+          k4_stamp(a, 0, g, 2);
           tc_fence_after();
           const std::uint32_t sa = sb + kOffA + sl * kABytes, sbb = sb + kOffB + sl * kBBytes;
 #pragma unroll
@@ -245,6 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
                            sdesc(sbb + h * kBTerm + j * 8192u, 128, 256), idesc, (it | j | h) != 0);
           mma_commit(bar_ae + 8 * sl);
           mma_commit(bar_be + 8 * sl);
+          k4_stamp(a, 0, g, 3);
         }
         mma_commit(bar_df);
       }
@@ -254,50 +283,78 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
     const std::uint32_t q = std::uint32_t(warp & 3), row_in = q * 32 + std::uint32_t(lane);
     const std::uint32_t t = std::uint32_t(warp - 2) >> 2;
     std::uint32_t g = 0, cg = 0, ul = 0;
+    const int kind0 = a.kind[0], kind1 = a.kind[1];  // (no runtime indexing of the parameter block)
+    // One item = (K chunk kc, stage s): 4 codewords per thread into the item's A slot.
+    struct Item {
+      std::uint32_t kc, s, cs, cph, sl, g;
+    };
     for (std::uint32_t u = blockIdx.x; u < units; u += gridDim.x, ++ul) {
       const std::uint32_t p = u % a.P, nt = (u / a.P) / MP, mt = ((u / a.P) % MP) * kMT + t;
       const bool live = mt < a.MT;
       std::uint32_t kc0, kc1;
       krange(p, kc0, kc1);
-      std::uint32_t cbase = 0;  // code counter of the current k slab's first slab
-      for (std::uint32_t kc = kc0; kc < kc1; ++kc) {
-        if (kc % 8 == 0) {
-          cbase = cg;
-          cg += nst * kMT;
+      const std::uint32_t uitems = (kc1 - kc0) * nst;
+      auto item = [&](std::uint32_t i) {
+        Item it;
+        it.kc = kc0 + i / nst;
+        it.s = i % nst;
+        const std::uint32_t cidx = cg + ((it.kc - kc0) / 8) * nst * kMT + it.s * kMT + t;
+        it.cs = cidx % kCodeSlots;
+        it.cph = (cidx / kCodeSlots) & 1;
+        it.g = g + i;
+        it.sl = it.g % kSlots;
+        return it;
+      };
+      auto wait_item = [&](const Item& it) {
+        mbar_wait(bar_cf + 8 * it.cs, it.cph);
+        if (it.g >= kSlots) mbar_wait(bar_ae + 8 * it.sl, ((it.g / kSlots) - 1) & 1);
+      };
+      // decode one item's 4 codewords of this row into bf16 A bytes
+      auto decode = [&](const Item& it, uint4 (&v)[4]) {
+        const std::uint32_t sc = sb + kOffC + it.cs * kCodeSlot, cq = it.kc % 8;
+        const std::uint32_t wofs = (cq / 4) * 2048u + row_in * 16u + (cq % 4) * 4u;
+        const std::uint32_t iw = lds32(sc + wofs);
+        if ((it.s ? kind1 : kind0) == 0) {
+          const std::uint32_t fw = lds32(sc + 4096u + wofs), sw = lds32(sc + 8192u + row_in * 4u);
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+            v[jj] = e8p_bf16((iw >> (8 * jj)) & 0xFFu, fw, jj, (sw >> (cq + 8 * jj)) & 1u, tab);
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) v[jj] = e81_bf16((iw >> (8 * jj)) & 0xFFu, tab);
         }
-        for (std::uint32_t s = 0; s < nst; ++s, ++g) {
-          const std::uint32_t cidx = cbase + s * kMT + t, cs = cidx % kCodeSlots;
-          mbar_wait(bar_cf + 8 * cs, (cidx / kCodeSlots) & 1);
-          const std::uint32_t sl = g % kSlots;
-          if (g >= kSlots) mbar_wait(bar_ae + 8 * sl, ((g / kSlots) - 1) & 1);
-          const std::uint32_t sc = sb + kOffC + cs * kCodeSlot, cq = kc % 8;
-          const std::uint32_t sa = sb + kOffA + sl * kABytes + t * kATile;
-          if (live) {
-            const std::uint32_t wofs = (cq / 4) * 2048u + row_in * 16u + (cq % 4) * 4u;
-            uint4 v[4];
-            const std::uint32_t iw = lds32(sc + wofs);
-            if (a.kind[s] == 0) {
-              const std::uint32_t fw = lds32(sc + 4096u + wofs), sw = lds32(sc + 8192u + row_in * 4u);
+      };
+      // codeword jj = K columns 8 jj .. 8 jj + 7 of the chunk: K-block jj / 2, half jj % 2
+      auto store = [&](const Item& it, const uint4 (&v)[4]) {
+        const std::uint32_t sa = sb + kOffA + it.sl * kABytes + t * kATile;
 #pragma unroll
-              for (int jj = 0; jj < 4; ++jj)
-                v[jj] = e8p_bf16((iw >> (8 * jj)) & 0xFFu, fw, jj, (sw >> (cq + 8 * jj)) & 1u, tab);
-            } else {
-#pragma unroll
-              for (int jj = 0; jj < 4; ++jj) v[jj] = e81_bf16((iw >> (8 * jj)) & 0xFFu, tab);
-            }
-            // codeword jj = K columns 8 jj .. 8 jj + 7 of the chunk: K-block jj / 2, half jj % 2
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj)
-              sts128(sa + (jj >> 1) * 4096u + (row_in >> 3) * 256u + (jj & 1) * 128u + (row_in & 7) * 16u, v[jj]);
-            fence_proxy_async_smem();  // generic smem writes -> the tensor core's operand reads
-          }
-          __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(bar_af + 8 * sl);
-            if (cq == 7 || kc + 1 == kc1) mbar_arrive(bar_ce + 8 * cs);  // slab fully decoded
-          }
+        for (int jj = 0; jj < 4; ++jj)
+          sts128(sa + (jj >> 1) * 4096u + (row_in >> 3) * 256u + (jj & 1) * 128u + (row_in & 7) * 16u, v[jj]);
+      };
+      auto release = [&](const Item& it) {  // lane 0, after the warp's stores are fenced
+        mbar_arrive(bar_af + 8 * it.sl);
+        if (it.kc % 8 == 7 || it.kc + 1 == kc1) mbar_arrive(bar_ce + 8 * it.cs);  // slab fully decoded
+      };
+      // One item at a time: with kSlots = 3 A buffers, pairing items (two decodes in
+      // flight, one proxy fence per pair) starved the MMA issuer (K4 387 -> 410 us).
+      for (std::uint32_t i = 0; i < uitems; ++i) {
+        const Item it = item(i);
+        k4_stamp(a, 2 + warp - 2, it.g, 0);
+        wait_item(it);
+        k4_stamp(a, 2 + warp - 2, it.g, 2);
+        if (live) {
+          uint4 v[4];
+          decode(it, v);
+          store(it, v);
+          k4_stamp(a, 2 + warp - 2, it.g, 4);
+          fence_proxy_async_smem();  // generic smem writes -> the tensor core's operand reads
         }
+        __syncwarp();
+        k4_stamp(a, 2 + warp - 2, it.g, 3);
+        if (lane == 0) release(it);
       }
+      g += uitems;
+      cg += ((kc1 - kc0 + 7) / 8) * nst * kMT;
       // epilogue: z[b][r] = D_t[r][b] / 4 for this M tile's 128 rows x 256 vectors
       mbar_wait(bar_df, ul & 1);
       tc_fence_after();
@@ -434,12 +491,32 @@ void launch_prefill(const q8p_layer& L, const float* t, std::uint8_t* btiles, fl
   a.batch = std::uint32_t(batch);
   a.nib = L.mma_tables;
   a.e81 = reinterpret_cast<const uint2*>(L.mma_tables + 256);
+#ifdef Q8P_K4_TRACE
+  static const char* trace_env = std::getenv("Q8P_TRACE");
+  if (trace_env) {
+    constexpr std::size_t words = 10 * kK4TraceItems * 8;
+    cuda_check(cudaMalloc(&a.trace, words * 8), "trace alloc");
+    cuda_check(cudaMemset(a.trace, 0, words * 8), "trace memset");
+  }
+#endif
   kernel_attrs(reinterpret_cast<const void*>(prefill_kernel), int(kSmem));
   int sms = 0;
   cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device()), "sm count");
   const unsigned grid = unsigned(std::min<std::uint32_t>((a.MT + kMT - 1) / kMT * a.NTL * a.P, std::uint32_t(sms)));
   launch_pdl(prefill_kernel, dim3(grid), dim3(kThreads), kSmem, s, a);
   cuda_check(cudaGetLastError(), "prefill launch");
+#ifdef Q8P_K4_TRACE
+  if (a.trace) {
+    std::vector<unsigned long long> h(10 * kK4TraceItems * 8);
+    cuda_check(cudaStreamSynchronize(s), "trace sync");
+    cuda_check(cudaMemcpy(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost), "trace copy");
+    cudaFree(a.trace);
+    if (FILE* f = std::fopen((std::string(trace_env) + ".k4.bin").c_str(), "wb")) {
+      std::fwrite(h.data(), 8, h.size(), f);
+      std::fclose(f);
+    }
+  }
+#endif
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 

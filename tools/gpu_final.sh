@@ -11,6 +11,7 @@ timeout 300 python bench.py --no-cpu --batch 16 > $OUT/bench_b16.json 2> $OUT/be
 timeout 300 python bench.py --no-cpu --batch 512 --steps 10 > $OUT/bench_b512.json 2> $OUT/bench_b512.err
 timeout 300 python bench.py --no-cpu --workload 7b --bits 3 > $OUT/bench_7b_3bit.json 2> $OUT/bench_7b_3bit.err
 timeout 300 python bench.py --no-cpu --workload 7b --bits 4 > $OUT/bench_7b_4bit.json 2> $OUT/bench_7b_4bit.err
+timeout 300 python bench.py --no-cpu --sharded > $OUT/bench_sharded_push.json 2> $OUT/bench_sharded_push.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu --no-graph --copies 2 > $OUT/ncu_launch_bench.log 2>&1
