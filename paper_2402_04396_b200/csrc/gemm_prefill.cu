@@ -29,8 +29,9 @@
 //   warp 1   MMA issuer: per item (K chunk, stage) 2 M tiles x 2 K-blocks x 2 terms
 //            of tcgen05.mma M=128 N=256 K=16 into the tiles' accumulators (2 x 256
 //            TMEM columns)
-//   warps 2-9  decoders (warp = M tile x lane quadrant, thread = row): slab -> bf16
-//            A tile per item; then the unit's epilogue (tcgen05.ld -> z rows)
+//   warps 2-17 decoders, two teams of 8 (warp = team x M tile x lane quadrant,
+//            thread = row; team = K chunk parity): slab -> bf16 A tile per item;
+//            then the unit's epilogue (tcgen05.ld -> z rows, a team per 128 columns)
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -57,7 +58,9 @@ constexpr std::uint32_t kBBytes = 2u * kBTerm;        // hi + lo
 constexpr std::uint32_t kSlots = 3;                   // A / B pipeline depth
 constexpr std::uint32_t kCodeSlots = 8;               // code slab ring (M tiles x stages x 2 k slabs)
 constexpr std::uint32_t kCodeSlot = 4 * 2048 + 512;   // E8P slab bytes (e8-1bit slabs are smaller)
-constexpr int kDec = 8;                               // decoder warps: 2 M tiles x 4 lane quadrants
+constexpr int kTeams = 2;                             // decoder teams: K chunks alternate between them
+constexpr int kDecTeam = 8;                           // decoder warps per team: 2 M tiles x 4 lane quadrants
+constexpr int kDec = kTeams * kDecTeam;
 constexpr int kThreads = (2 + kDec) * 32;
 constexpr std::uint32_t kCtl = 1024, kTab = 4096;     // barriers; decode tables
 constexpr std::uint32_t kOffA = kCtl + kTab, kOffB = kOffA + kSlots * kABytes, kOffC = kOffB + kSlots * kBBytes;
@@ -182,14 +185,14 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
 
   if (threadIdx.x == 0) {
     for (std::uint32_t i = 0; i < kSlots; ++i) {
-      mbar_init(bar_af + 8 * i, kDec);
+      mbar_init(bar_af + 8 * i, kDecTeam);  // an item is decoded by one team
       mbar_init(bar_ae + 8 * i, 1);
       mbar_init(bar_bf + 8 * i, 1);
       mbar_init(bar_be + 8 * i, 1);
     }
     for (std::uint32_t i = 0; i < kCodeSlots; ++i) {
       mbar_init(bar_cf + 8 * i, 1);
-      mbar_init(bar_ce + 8 * i, 4);  // the 4 decoder warps of the slab's M tile
+      mbar_init(bar_ce + 8 * i, 4 * kTeams);  // the 4 decoder warps of the slab's M tile, per team
     }
     mbar_init(bar_df, 1);
     mbar_init(bar_de, kDec);
@@ -281,7 +284,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
   } else {
     // ===== decoders: warp = (M tile t, lane quadrant q), thread = row; then the epilogue =====
     const std::uint32_t q = std::uint32_t(warp & 3), row_in = q * 32 + std::uint32_t(lane);
-    const std::uint32_t t = std::uint32_t(warp - 2) >> 2;
+    const std::uint32_t t = (std::uint32_t(warp - 2) >> 2) & 1;  // M tile
+    const std::uint32_t team = std::uint32_t(warp - 2) >> 3;     // K chunks kc with kc % 2 == team
     std::uint32_t g = 0, cg = 0, ul = 0;
     const int kind0 = a.kind[0], kind1 = a.kind[1];  // (no runtime indexing of the parameter block)
     // One item = (K chunk kc, stage s): 4 codewords per thread into the item's A slot.
@@ -333,11 +337,13 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
       };
       auto release = [&](const Item& it) {  // lane 0, after the warp's stores are fenced
         mbar_arrive(bar_af + 8 * it.sl);
-        if (it.kc % 8 == 7 || it.kc + 1 == kc1) mbar_arrive(bar_ce + 8 * it.cs);  // slab fully decoded
+        if (it.kc % 8 >= 6) mbar_arrive(bar_ce + 8 * it.cs);  // this team's last chunk of the slab
       };
-      // One item at a time: with kSlots = 3 A buffers, pairing items (two decodes in
-      // flight, one proxy fence per pair) starved the MMA issuer (K4 387 -> 410 us).
-      for (std::uint32_t i = 0; i < uitems; ++i) {
+      // One item at a time per warp, the two teams on alternate K chunks: a single
+      // item's chain (slab load -> LUT load -> PRMTs -> stores -> proxy fence) is
+      // latency-bound, so two teams keep two items in flight per (M tile, quadrant).
+      // (Pairing items within one warp starved the 3-slot A ring: 387 -> 410 us.)
+      for (std::uint32_t i = team * nst; i < uitems; i += (i % nst == nst - 1) ? 1 + nst : 1) {
         const Item it = item(i);
         k4_stamp(a, 2 + warp - 2, it.g, 0);
         wait_item(it);
@@ -359,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
       mbar_wait(bar_df, ul & 1);
       tc_fence_after();
       const std::uint32_t row = mt * 128 + row_in;
-      for (std::uint32_t c0 = 0; c0 < std::uint32_t(kNT); c0 += 32) {
+      for (std::uint32_t c0 = team * (kNT / kTeams); c0 < (team + 1) * (kNT / kTeams); c0 += 32) {  // team's columns
         float d[32];
         tmem_ld32(tbase + ((q * 32) << 16) + t * kNT + c0, d);
         if (live && row < a.m) {
@@ -428,13 +434,13 @@ __global__ void __launch_bounds__(256) pack_b_kernel(const float* __restrict__ t
 }  // namespace
 
 // K splits P <= 8 (whole k slabs per split) minimising a two-term cost: the
-// GEMM's critical path (waves of units x the longest split's K chunks, ~0.93 us
+// GEMM's critical path (waves of units x the longest split's K chunks, ~0.82 us
 // per chunk and stage, measured on 28672 x 8192) plus the (P - 1) extra partial
 // z arrays K4 writes and K3 reads back (8 B per vector-row at ~6.5 TB/s).
 std::uint32_t prefill_splits(const q8p_layer& L, int batch, int sms) {
   const std::uint32_t MP = (tc_row_blocks(L.m_local()) + kMT - 1) / kMT, NTL = std::uint32_t((batch + kNT - 1) / kNT);
   const std::uint32_t KS8 = std::max<std::uint32_t>((L.n / kKC) / 8, 1), base = MP * NTL;
-  const double chunk_us = 0.93 * L.num_stages, part_us = 8.0 * batch * L.m_local() / 6.5e6;
+  const double chunk_us = 0.82 * L.num_stages, part_us = 8.0 * batch * L.m_local() / 6.5e6;
   std::uint32_t best = 1;
   double best_t = 0.0;
   for (std::uint32_t P = 1; P <= 8 && P <= KS8; ++P) {
@@ -446,8 +452,9 @@ std::uint32_t prefill_splits(const q8p_layer& L, int batch, int sms) {
 }
 
 bool prefill_supported(const q8p_layer& L, int batch) {
+  // whole k slabs of 8 K chunks (both decoder teams have chunks in every slab)
   return batch >= kPrefillMinBatch && L.tc[0].codes != nullptr && (L.num_stages == 1 || L.tc[1].codes != nullptr) &&
-         L.n % kKC == 0 && L.mma_tables != nullptr;
+         L.n % (8 * kKC) == 0 && L.mma_tables != nullptr;
 }
 
 std::uint32_t prefill_parts(const q8p_layer& L, int batch) {
