@@ -501,7 +501,7 @@ void launch_prefill(const q8p_layer& L, const float* t, std::uint8_t* btiles, fl
 #ifdef Q8P_K4_TRACE
   static const char* trace_env = std::getenv("Q8P_TRACE");
   if (trace_env) {
-    constexpr std::size_t words = 10 * kK4TraceItems * 8;
+    constexpr std::size_t words = (2 + kDec) * kK4TraceItems * 8;
     cuda_check(cudaMalloc(&a.trace, words * 8), "trace alloc");
     cuda_check(cudaMemset(a.trace, 0, words * 8), "trace memset");
   }
@@ -514,7 +514,7 @@ void launch_prefill(const q8p_layer& L, const float* t, std::uint8_t* btiles, fl
   cuda_check(cudaGetLastError(), "prefill launch");
 #ifdef Q8P_K4_TRACE
   if (a.trace) {
-    std::vector<unsigned long long> h(10 * kK4TraceItems * 8);
+    std::vector<unsigned long long> h((2 + kDec) * kK4TraceItems * 8);
     cuda_check(cudaStreamSynchronize(s), "trace sync");
     cuda_check(cudaMemcpy(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost), "trace copy");
     cudaFree(a.trace);

@@ -16,7 +16,7 @@ for _ in range(2):
     L.forward(x)
 torch.cuda.synchronize()
 K = 512
-t = np.fromfile(out + ".k4.bin", dtype=np.uint64).astype(np.int64).reshape(10, K, 8)
+t = np.fromfile(out + ".k4.bin", dtype=np.uint64).astype(np.int64).reshape(18, K, 8)
 base = t[t > 0].min()
 iss = t[0][:, :4]; iss = iss[(iss > 0).all(axis=1)] - base
 ph = np.diff(iss, axis=1)
@@ -24,7 +24,7 @@ per = np.diff(iss[:, 0])
 print(f"issuer: items {len(iss)} | A wait {np.median(ph[:,0]):.0f} (mean {ph[:,0].mean():.0f}) | B wait {np.median(ph[:,1]):.0f} (mean {ph[:,1].mean():.0f}) | issue {np.median(ph[:,2]):.0f} | per item median {np.median(per):.0f} mean {per.mean():.0f} cyc")
 big = per > 3 * np.median(per)
 print("  long gaps (> 3x median):", int(big.sum()), "total cyc", int(per[big].sum()), "of", int(per.sum()))
-for w in range(8):
+for w in range(16):
     d = t[2 + w][:, [0, 1, 2, 4, 3]]; d = d[(d > 0).all(axis=1)] - base
     if len(d) < 3: continue
     ph = np.diff(d, axis=1); per = np.diff(d[:, 0])
