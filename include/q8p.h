@@ -108,6 +108,14 @@ q8p_status q8p_plan_hadamard(size_t n, size_t* p, size_t* q);
  * each call gets its own workspace. */
 q8p_status q8p_layer_create(const q8p_layer_desc* desc, int device, q8p_layer** out);
 q8p_status q8p_layer_from_qshp(const uint8_t* bytes, size_t len, int device, q8p_layer** out);
+/* Multi-layer loading (a model's artifacts, latq::deserialize
+ * pipeline.cpp:323-383 per artifact): every artifact is parsed and uploaded on its
+ * own worker thread and private stream (at most 4 in flight), so one layer's
+ * host-side deserialize overlaps another's H2D copies and device transcode.
+ * out[i] = the layer of bytes[i]; on any failure no layer is kept and the first
+ * error is returned. */
+q8p_status q8p_layers_from_qshp(const uint8_t* const* bytes, const size_t* lens, int count, int device,
+                                q8p_layer** out);
 /* Row shard [row_begin, row_end) of a full artifact for row-sharded
  * tensor parallelism; S_U / S_V stay full. */
 q8p_status q8p_layer_from_qshp_rows(const uint8_t* bytes, size_t len, uint32_t row_begin,

@@ -159,6 +159,7 @@ _SIGNATURES = {
     "q8p_e8p_decode_host": (ctypes.c_int, [ctypes.c_uint16, ctypes.c_void_p]),
     "q8p_codebook_table": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
     "q8p_hadamard_base": (ctypes.c_int, [ctypes.c_size_t, ctypes.c_void_p]),
+    "q8p_layers_from_qshp": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
     "q8p_peers_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p), ctypes.c_void_p]),
     "q8p_peers_connect": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p]),
     "q8p_peers_connect_local": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
@@ -359,6 +360,18 @@ class Layer:
         else:
             _check(lib().q8p_layer_from_qshp_rows(data, len(data), rows[0], rows[1], device, ctypes.byref(h)))
         return cls(h.value)
+
+    @classmethod
+    def many_from_qshp(cls, artifacts: Sequence[bytes], device: int = 0) -> list["Layer"]:
+        """q8p_layers_from_qshp: a model's artifacts loaded concurrently (parse / H2D /
+        device transcode of different layers overlap)."""
+        k = len(artifacts)
+        arts = [bytes(a) for a in artifacts]  # no copy for bytes; kept alive for the call
+        ptrs = (ctypes.c_char_p * k)(*arts)
+        lens = (ctypes.c_size_t * k)(*[len(a) for a in artifacts])
+        out = (ctypes.c_void_p * k)()
+        _check(lib().q8p_layers_from_qshp(ptrs, lens, k, device, out))
+        return [cls(out[i]) for i in range(k)]
 
     @classmethod
     def create(cls, m: int, n: int, stages: Sequence[tuple[int, float, np.ndarray]],

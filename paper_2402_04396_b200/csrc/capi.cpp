@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <string>
 
 #include "device.hpp"
@@ -1047,6 +1048,50 @@ q8p_status q8p_layer_from_qshp(const uint8_t* bytes, size_t len, int device, q8p
     *out = layer_from_bytes(bytes, len, 0, 0, true, device);
     return Q8P_OK;
   } catch (...) {
+    return status_of_current_exception();
+  }
+}
+
+q8p_status q8p_layers_from_qshp(const uint8_t* const* bytes, const size_t* lens, int count, int device,
+                                q8p_layer** out) {
+  std::vector<q8p_layer*> made;
+  try {
+    if (count < 0) throw q8p::ValidationError("negative layer count");
+    if (count > 0 && (!bytes || !lens || !out)) throw q8p::ValidationError("null argument");
+    for (int i = 0; i < count; ++i) {
+      if (!bytes[i]) throw q8p::ValidationError("null artifact");
+      out[i] = nullptr;
+    }
+    // Every artifact is parsed and uploaded on its own worker thread (its own
+    // private upload stream): one layer's host-side deserialize overlaps another's
+    // H2D copies and device transcode.  At most kLoadWorkers in flight.
+    constexpr int kLoadWorkers = 4;
+    std::vector<std::future<q8p_layer*>> jobs;
+    std::string first_error;
+    q8p_status first_status = Q8P_OK;
+    auto collect = [&](std::future<q8p_layer*>& f) {
+      try {
+        made.push_back(f.get());
+      } catch (...) {
+        const q8p_status st = status_of_current_exception();
+        if (first_status == Q8P_OK) first_status = st, first_error = q8p_last_error();
+        made.push_back(nullptr);
+      }
+    };
+    for (int i = 0; i < count; ++i) {
+      if (int(jobs.size()) - int(made.size()) >= kLoadWorkers) collect(jobs[made.size()]);
+      jobs.push_back(std::async(std::launch::async, [=] { return layer_from_bytes(bytes[i], lens[i], 0, 0, true, device); }));
+    }
+    while (made.size() < jobs.size()) collect(jobs[made.size()]);
+    if (first_status != Q8P_OK) {
+      for (q8p_layer* L : made) q8p_layer_destroy(L);
+      set_last_error(first_error);
+      return first_status;
+    }
+    for (int i = 0; i < count; ++i) out[i] = made[i];
+    return Q8P_OK;
+  } catch (...) {
+    for (q8p_layer* L : made) q8p_layer_destroy(L);
     return status_of_current_exception();
   }
 }
