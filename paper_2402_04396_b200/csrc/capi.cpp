@@ -1440,19 +1440,25 @@ q8p_status q8p_rht(size_t n, const uint8_t* signs, const float* x, float* y, int
     side.q = static_cast<std::uint32_t>(spec.q);
     side.signs = signs;
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
-    // Per-order device copies of the base, cached per process (single device per process).
+    // Per-(device, order) copies of the base, cached per process.
     static std::mutex mu;
-    static std::vector<std::pair<std::size_t, void*>> bases;
+    struct BaseCopy {
+      int device;
+      std::size_t q;
+      void* ptr;
+    };
+    static std::vector<BaseCopy> bases;
     if (spec.q > 1) {
+      const int dev = current_device();
       std::scoped_lock lock(mu);
-      for (auto& [q, ptr] : bases)
-        if (q == spec.q) side.base = static_cast<const std::int8_t*>(ptr);
+      for (const BaseCopy& e : bases)
+        if (e.device == dev && e.q == spec.q) side.base = static_cast<const std::int8_t*>(e.ptr);
       if (!side.base) {
         const auto& b = q8p::detail::hadamard_base(spec.q);
         void* d = nullptr;
         cuda_check(cudaMalloc(&d, b.size()), "cudaMalloc base");
         cuda_check(cudaMemcpy(d, b.data(), b.size(), cudaMemcpyHostToDevice), "base upload");
-        bases.emplace_back(spec.q, d);
+        bases.push_back({dev, spec.q, d});
         side.base = static_cast<const std::int8_t*>(d);
       }
     }
@@ -1460,25 +1466,25 @@ q8p_status q8p_rht(size_t n, const uint8_t* signs, const float* x, float* y, int
       launch_rht(side, x, y, batch, transpose != 0, s);
       return Q8P_OK;
     }
-    // Scratch for the two-pass transforms (and the amax the forward pass reports).
-    struct Scratch {
-      void* p = nullptr;
-      std::size_t bytes = 0;
-    };
-    static thread_local Scratch scratch;
+    // Scratch for the two-pass transforms (and the amax the forward pass reports):
+    // stream-ordered (cudaMallocAsync / cudaFreeAsync on `s`), so calls on other
+    // streams or devices never share it and it is capturable in a graph.
     const std::size_t need = std::size_t(batch) * n * 4 + 256;
-    if (scratch.bytes < need) {
-      if (scratch.p) cudaFree(scratch.p);
-      cuda_check(cudaMalloc(&scratch.p, need), "cudaMalloc rht scratch");
-      scratch.bytes = need;
+    void* scratch = nullptr;
+    cuda_check(cudaMallocAsync(&scratch, need, s), "cudaMallocAsync rht scratch");
+    float* u = static_cast<float*>(scratch);
+    float* amax = reinterpret_cast<float*>(static_cast<std::uint8_t*>(scratch) + std::size_t(batch) * n * 4);
+    try {
+      if (!transpose) {
+        launch_rht_in(side, x, y, u, amax, nullptr, nullptr, 0, batch, s);
+      } else {
+        launch_rht_out(side, x, u, y, batch, s);
+      }
+    } catch (...) {
+      cudaFreeAsync(scratch, s);
+      throw;
     }
-    float* u = static_cast<float*>(scratch.p);
-    float* amax = reinterpret_cast<float*>(static_cast<std::uint8_t*>(scratch.p) + std::size_t(batch) * n * 4);
-    if (!transpose) {
-      launch_rht_in(side, x, y, u, amax, nullptr, nullptr, 0, batch, s);
-    } else {
-      launch_rht_out(side, x, u, y, batch, s);
-    }
+    cuda_check(cudaFreeAsync(scratch, s), "cudaFreeAsync rht scratch");
     return Q8P_OK;
   } catch (...) {
     return status_of_current_exception();
