@@ -1657,14 +1657,21 @@ q8p_status q8p_peers_create(int device, int world, int rank, size_t slice_floats
     p->slice_floats = slice_floats;
     const std::size_t bytes = peer_bytes(world, slice_floats);
     cuda_check(cudaMalloc(&p->base, bytes), "cudaMalloc peer window");
-    cuda_check(cudaMemset(p->base, 0, bytes), "peer window init");  // tag 0: never a call's tag
+    {  // tag 0 is never a call's tag; private stream: no legacy-stream / device-wide sync
+      cudaStream_t st = nullptr;
+      cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "peer init stream");
+      const cudaError_t e1 = cudaMemsetAsync(p->base, 0, bytes, st);
+      const cudaError_t e2 = cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+      cuda_check(e1, "peer window init");
+      cuda_check(e2, "peer window init");
+    }
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&p->d_wins), sizeof(void*) * world), "cudaMalloc peer table");
     static_assert(sizeof(cudaIpcMemHandle_t) <= Q8P_PEER_HANDLE_BYTES, "IPC handle size");
     cudaIpcMemHandle_t h;
     cuda_check(cudaIpcGetMemHandle(&h, p->base), "cudaIpcGetMemHandle");
     std::memset(handle, 0, Q8P_PEER_HANDLE_BYTES);
     std::memcpy(handle, &h, sizeof(h));
-    cuda_check(cudaDeviceSynchronize(), "peer window init");
     *out = p;
     return Q8P_OK;
   } catch (...) {
