@@ -273,7 +273,7 @@ def run_ours(args):
         comm = q8p.NcclComm(bytes(uid.cpu().numpy()), world, rank, local)
         if args.allgather == "push":
             # push all-gather group: one window per rank, IPC handles exchanged over the process group
-            peers = q8p.PeerGroup(local, world, rank, min(args.batch, 32) * max(m // world for m, _ in layers))
+            peers = q8p.PeerGroup(local, world, rank, args.batch * max(m // world for m, _ in layers))
             handles = [None] * world
             if world > 1:
                 dist.all_gather_object(handles, peers.handle)

@@ -302,7 +302,8 @@ q8p_status q8p_forward_sharded_sim(const q8p_layer* const* shards, int world, co
  * receives its Q8P_PEER_HANDLE_BYTES IPC handle), the handles are exchanged out
  * of band (e.g. torch.distributed all_gather_object) and concatenated in rank
  * order, then every rank calls q8p_peers_connect.  world <= 16;
- * slice_floats >= min(batch, 32) * m_local for every layer / batch used.
+ * slice_floats >= min(batch, 32) * m_local for every layer / batch used
+ * (batch * m_local for prefill batches, >= 64, which run K4 + one push).
  * Requirements as q8p_forward_sharded's fast path: equal rank-ordered row
  * shards that are whole K3 pass-1 chunks (rht layers), batches on the
  * tensor-core path; else Q8P_ERR_UNSUPPORTED.  All ranks must issue the same

@@ -294,7 +294,8 @@ class PeerGroup:
     """One rank's member of a push all-gather group (q8p_peers_*): a window in
     this GPU's memory that the other ranks write into over NVLink.  Exchange
     `handle` (bytes) among the ranks out of band, then `connect(handles)` with the
-    rank-ordered list.  slice_floats >= min(batch, 32) * m_local of every layer used."""
+    rank-ordered list.  slice_floats >= min(batch, 32) * m_local of every layer used
+    (batch * m_local for prefill batches >= 64)."""
 
     def __init__(self, device: int, world: int, rank: int, slice_floats: int):
         h = ctypes.c_void_p()

@@ -355,6 +355,7 @@ struct Workspace {
   float* pz;             // prefill: z [batch][m_local]
   float* z_loc;          // row-sharded: [batch][m_local] this rank's z rows
   float* z_full;         // row-sharded: [batch][m] all-gathered z
+  float* pz_full;        // row-sharded prefill: [batch][m] all-gathered K3 pass-1 rows (row shards only)
   std::uint32_t rows_pad, zcols;
 };
 std::uint32_t rows_pad_of(const q8p_layer* L) { return tc_row_blocks(L->m_local()) * 128; }
@@ -376,12 +377,17 @@ bool multi_chunk_k1(const q8p_layer* L, int batch) {
 
 // Prefill batches run the K4 decode-GEMM (gemm_prefill.cu) unless Q8P_PREFILL=0
 // (A/B knob: the 32-vector chunks through K2 instead).
-bool use_prefill(const q8p_layer* L, int batch) {
+// K4 for this layer (or row shard) at this batch (Q8P_PREFILL=0: the 32-vector
+// chunked GEMV instead, an A/B and debugging switch).
+bool use_prefill_rows(const q8p_layer* L, int batch) {
   static const bool off = [] {
     const char* e = std::getenv("Q8P_PREFILL");
     return e && std::string(e) == "0";
   }();
-  return !off && L->row_begin == 0 && L->row_end == L->m && prefill_supported(*L, batch);
+  return !off && prefill_supported(*L, batch);
+}
+bool use_prefill(const q8p_layer* L, int batch) {  // the unsharded forward
+  return L->row_begin == 0 && L->row_end == L->m && use_prefill_rows(L, batch);
 }
 
 std::size_t workspace_parts(const q8p_layer* L, int batch, Workspace* w, void* base) {
@@ -415,12 +421,13 @@ std::size_t workspace_parts(const q8p_layer* L, int batch, Workspace* w, void* b
     v.t = reinterpret_cast<float*>(take(B * L->n * 4));
     v.z = reinterpret_cast<float*>(take(B * L->m * 4));
   }
-  if (use_prefill(L, batch_all)) {  // K4 path (forward); the chunked path stays sized for rows_z / sharded
+  if (use_prefill_rows(L, batch_all)) {  // K4 path; the chunked path stays sized for rows_z
     const std::size_t Ball = std::size_t(batch_all);
     v.pt = reinterpret_cast<float*>(take(Ball * L->n * 4));
     v.pbt = take(prefill_btile_bytes(*L, batch_all));
     v.pz = reinterpret_cast<float*>(take(std::size_t(prefill_parts(*L, batch_all)) * Ball * L->m_local() * 4));
-    v.u = reinterpret_cast<float*>(take(Ball * mx * 4));
+    v.u = reinterpret_cast<float*>(take(Ball * mx * 4));  // also the sharded pass 1's send buffer
+    if (L->m_local() != L->m) v.pz_full = reinterpret_cast<float*>(take(Ball * L->m * 4));
   }
   if (w) *w = v;
   return off;
@@ -506,6 +513,21 @@ void forward_sharded_impl(const q8p_layer* L, const float* x, float* y, int batc
   float zscale[2] = {L->scale[0], L->scale[1]};
   int ze8p[2] = {L->cb[0] == Q8P_CB_E8P_2BIT, L->cb[1] == Q8P_CB_E8P_2BIT};
   const bool local_p1 = rht_sharded_k3_ok(L->side_u, L->row_begin, ml);
+  if (local_p1 && use_prefill_rows(L, batch)) {
+    // prefill: K1 (replicated) -> K4 on this rank's rows -> K3 pass 1 on them (summing
+    // the K-split partials) -> one all-gather -> K3 pass 2
+    launch_rht_in(L->side_v, x, w.pt, w.u, nullptr, nullptr, nullptr, 0, batch, s);
+    launch_prefill(*L, w.pt, w.pbt, w.pz, batch, s);
+    launch_rht_out_local_f32(L->side_u, w.pz, int(prefill_parts(*L, batch)), L->row_begin, ml, w.u, nullptr, batch,
+                             s);
+    if (world == 1) {
+      launch_rht_out_pass2_gathered(L->side_u, w.u, ml, y, batch, s);
+      return;
+    }
+    nccl_check(ncclAllGather(w.u, w.pz_full, std::size_t(batch) * ml, ncclFloat32, comm, s), "ncclAllGather");
+    launch_rht_out_pass2_gathered(L->side_u, w.pz_full, ml, y, batch, s);
+    return;
+  }
   for (int b0 = 0; b0 < batch; b0 += chunk) {
     const int nb = std::min(chunk, batch - b0);
     float* yb = y + std::size_t(b0) * L->m;
@@ -595,7 +617,8 @@ void check_push_layer(const q8p_layer* L, const q8p_peers* p, int batch) {
   if (tc_chunk(L, batch) == 0) throw UnsupportedError("push all-gather needs the tensor-core path");
   if (!rht_sharded_k3_ok(L->side_u, L->row_begin, ml))
     throw UnsupportedError("push all-gather: a rank's rows must be whole K3 pass-1 chunks (rht layers)");
-  if (std::size_t(std::min(tc_chunk(L, batch), batch)) * ml > p->slice_floats)
+  const std::size_t per_call = use_prefill_rows(L, batch) ? std::size_t(batch) : std::size_t(std::min(tc_chunk(L, batch), batch));
+  if (per_call * ml > p->slice_floats)
     throw SizeError("push all-gather: window slice too small for this layer / batch");
 }
 
@@ -610,6 +633,14 @@ void forward_push_impl(const q8p_layer* L, q8p_peers* p, const float* x, float* 
   Workspace w;
   workspace_parts(L, batch, &w, ws);
   const PushArgs pa = p->args();
+  if (use_prefill_rows(L, batch)) {  // prefill: K1 -> K4 on this rank's rows -> pushing K3 pass 1 -> pass 2
+    launch_rht_in(L->side_v, x, w.pt, w.u, nullptr, nullptr, nullptr, 0, batch, s);
+    launch_prefill(*L, w.pt, w.pbt, w.pz, batch, s);
+    launch_rht_out_local_f32(L->side_u, w.pz, int(prefill_parts(*L, batch)), L->row_begin, L->m_local(), nullptr,
+                             &pa, batch, s);
+    launch_rht_out_pass2_push(L->side_u, L->m_local(), pa, y, batch, s);
+    return;
+  }
   const int chunk = tc_chunk(L, batch);
   for (int b0 = 0; b0 < batch; b0 += chunk) {  // one push epoch per chunk
     const int nb = std::min(chunk, batch - b0);
@@ -1778,8 +1809,23 @@ q8p_status q8p_forward_sharded_push_sim(const q8p_layer* const* shards, q8p_peer
     const q8p_layer* L0 = shards[0];
     DeviceGuard g(L0->device);
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int chunk = tc_chunk(L0, batch);
     Workspace w;
+    if (use_prefill_rows(L0, batch)) {  // prefill: every rank's K1, K4, pushing pass 1; then every pass 2
+      for (int r = 0; r < world; ++r) {
+        const q8p_layer* L = shards[r];
+        workspace_parts(L, batch, &w, ws);
+        const PushArgs pa = peers[r]->args();
+        launch_rht_in(L->side_v, x, w.pt, w.u, nullptr, nullptr, nullptr, 0, batch, s);
+        launch_prefill(*L, w.pt, w.pbt, w.pz, batch, s);
+        launch_rht_out_local_f32(L->side_u, w.pz, int(prefill_parts(*L, batch)), L->row_begin, L->m_local(), nullptr,
+                                 &pa, batch, s);
+      }
+      for (int r = 0; r < world; ++r)
+        launch_rht_out_pass2_push(L0->side_u, L0->m_local(), peers[r]->args(), y + std::size_t(r) * batch * L0->m,
+                                  batch, s);
+      return Q8P_OK;
+    }
+    const int chunk = tc_chunk(L0, batch);
     for (int b0 = 0; b0 < batch; b0 += chunk) {
       const int nb = std::min(chunk, batch - b0);
       // every rank's K1, K2 and pushing pass 1 in turn, then every rank's pass 2

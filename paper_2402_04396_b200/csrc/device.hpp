@@ -245,6 +245,12 @@ void launch_rht_out_acc_push(const DevSide& side, const std::int32_t* zacc, int 
                              std::uint32_t zacc_cols, const float zscale[2], const int ze8p[2], const float* alpha,
                              const long long* tl, std::uint32_t row0, std::uint32_t m_local, const PushArgs& push,
                              int batch, cudaStream_t s);
+// Row-sharded prefill K3 pass 1: this rank's rows from K4's K-split partials
+// [parts][batch][m_local] (summed in split order) into the send buffer
+// [batch][m_local], or pushed into every rank's window when `push` is set.
+void launch_rht_out_local_f32(const DevSide& side, const float* zparts, int parts, std::uint32_t row0,
+                              std::uint32_t m_local, float* z_send, const PushArgs* push, int batch,
+                              cudaStream_t s);
 void launch_rht_out_pass2_push(const DevSide& side, std::uint32_t m_local, const PushArgs& push, float* y, int batch,
                                cudaStream_t s);
 // Row-sharded forward: this rank's fp32 z rows [batch][m_local] from the limb accumulators.

@@ -130,20 +130,48 @@ __global__ void __launch_bounds__(256) rht_pass2(RhtArgs a) {
 // is one coalesced 128 B segment and there is no shared memory or barrier.  Same
 // butterfly order as fwht_rows (stages by increasing index bit), so the output
 // is bitwise that of rht_pass2.  grid = ceil(batch * ceil(P2 q / 32) / 8); 256 threads.
-template <int P1>
+// kPush: the push all-gather's flavour -- the column is read from this rank's window
+// of the call's parity as tagged words (polled until every word carries the tag).
+template <int P1, bool kPush>
 __global__ void __launch_bounds__(256) rht_pass2_reg(RhtArgs a) {
   pdl_wait();
   pdl_trigger();
   const std::uint32_t stride = a.P2 * a.q, ncg = (stride + 31) / 32;
   const std::uint32_t w = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (w >= ncg * std::uint32_t(a.batch)) return;  // whole warps
-  const int b = int(w / ncg);
+  const bool warp_live = w < ncg * std::uint32_t(a.batch);  // (no early return: push_done syncs the CTA)
+  const int b = warp_live ? int(w / ncg) : 0;
   const std::uint32_t col = (w % ncg) * 32 + (threadIdx.x & 31u);
-  const bool live = col < stride;
+  const bool live = warp_live && col < stride;
+  unsigned long long e = 0;
+  const unsigned long long* win = nullptr;
+  if constexpr (kPush) {
+    e = ld_epoch(a.push.ctl);
+    win = a.push.self_win + (e & 1) * a.push.win_words;
+  }
   float v[P1];
+  if constexpr (kPush) {
+    const std::uint32_t tag = std::uint32_t(e + 1);
+    bool ok = true;
 #pragma unroll
-  for (int r = 0; r < P1; ++r)
-    v[r] = live ? __ldcg(a.mid + rank_major(b, r * stride + col, a.mid_rows, a.batch, a.n)) : 0.f;
+    for (int r = 0; r < P1; ++r) {
+      unsigned long long wd = 0;
+      if (live)
+        asm volatile("ld.volatile.u64 %0, [%1];\n"
+                     : "=l"(wd)
+                     : "l"(win + rank_major(b, r * stride + col, a.mid_rows, a.batch, a.n)));
+      ok &= !live || std::uint32_t(wd >> 32) == tag;
+      v[r] = __uint_as_float(std::uint32_t(wd));
+    }
+    if (!ok) {  // a peer's words not all here yet: poll them one by one
+#pragma unroll
+      for (int r = 0; r < P1; ++r)
+        v[r] = ll_load1(win + rank_major(b, r * stride + col, a.mid_rows, a.batch, a.n), tag, a.push.rank);
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < P1; ++r)
+      v[r] = live ? __ldcg(a.mid + rank_major(b, r * stride + col, a.mid_rows, a.batch, a.n)) : 0.f;
+  }
   // K3's output signs, fetched alongside the data (bit r = row r's sign)
   unsigned long long neg = 0;
   if (!a.fwd && live)
@@ -173,10 +201,11 @@ __global__ void __launch_bounds__(256) rht_pass2_reg(RhtArgs a) {
       mx = fmaxf(mx, fabsf(o));
     }
   }
-  if (a.fwd && a.amax_out) {
+  if (a.fwd && a.amax_out && warp_live) {
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((threadIdx.x & 31) == 0) atomic_max_pos(a.amax_out + b, mx);
   }
+  if constexpr (kPush) push_done(a, e);
 }
 
 // Pass 2 of K1, limb flavour: grid = (P2 * q / 8 codeword columns, batch).
@@ -240,7 +269,8 @@ void launch_pass1(const RhtArgs& a, std::uint32_t extra, cudaStream_t s) {
 template <int P1>
 void launch_pass2_reg(const RhtArgs& a, cudaStream_t s) {
   const std::uint32_t warps = (a.P2 * a.q + 31) / 32 * std::uint32_t(a.batch);
-  launch_pdl(rht_pass2_reg<P1>, dim3((warps + 7) / 8), dim3(256), 0, s, a);
+  launch_pdl(a.push.ctl ? rht_pass2_reg<P1, true> : rht_pass2_reg<P1, false>, dim3((warps + 7) / 8), dim3(256), 0, s,
+             a);
 }
 
 void launch_pass2(const RhtArgs& a, cudaStream_t s) {
@@ -437,6 +467,29 @@ void launch_rht_out_acc_push(const DevSide& side, const std::int32_t* zacc, int 
   launch_pass1(a, 0, s);
 }
 
+void launch_rht_out_local_f32(const DevSide& side, const float* zparts, int parts, std::uint32_t row0,
+                              std::uint32_t m_local, float* z_send, const PushArgs* push, int batch,
+                              cudaStream_t s) {
+  RhtArgs a{};
+  plan_split_impl(side, a);
+  const std::uint32_t chunk = a.P2 * a.q;
+  a.signs = side.signs;
+  a.base = side.base;
+  a.in = zparts;
+  a.in_parts = parts;
+  a.in_local = 1;
+  a.mid = z_send;
+  a.batch = batch;
+  a.fwd = 0;
+  a.ch0 = row0 / chunk;
+  a.p1_count = m_local / chunk;
+  a.row0 = row0;
+  a.p1_out_rows = m_local;
+  a.vpb = vectors_per_block(batch);
+  if (push) a.push = *push;
+  launch_pass1(a, 0, s);
+}
+
 void launch_rht_out_pass2_push(const DevSide& side, std::uint32_t m_local, const PushArgs& push, float* y, int batch,
                                cudaStream_t s) {
   RhtArgs a{};
@@ -449,9 +502,7 @@ void launch_rht_out_pass2_push(const DevSide& side, std::uint32_t m_local, const
   a.batch = batch;
   a.fwd = 0;
   a.push = push;
-  const int vpb = vectors_per_block(batch);
-  a.vpb = vpb;
-  if (vpb > 1) throw UnsupportedError("push all-gather: batches of at most 32 vectors per call");
+  a.vpb = vectors_per_block(batch);
   launch_pass2(a, s);
 }
 
@@ -466,6 +517,7 @@ void launch_rht_out_pass2_gathered(const DevSide& side, const float* mid_gathere
   a.out = y;
   a.batch = batch;
   a.fwd = 0;
+  a.vpb = vectors_per_block(batch);
   launch_pass2(a, s);
 }
 

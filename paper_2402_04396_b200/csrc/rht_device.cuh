@@ -58,6 +58,8 @@ struct RhtArgs {
   std::uint32_t ch0, p1_count, row0, p1_out_rows, mid_rows, in_rows;
   int vpb;                      // vectors per CTA (fp32 passes; 0/1 = one)
   int in_parts;                 // pass 1 fp32 input = sum of in_parts partial arrays [batch][n] (0/1 = one)
+  int in_local;                 // row-sharded prefill: the fp32 input holds this rank's rows only,
+                                // [in_parts][batch][p1_out_rows] (row i at i - row0)
   // Push all-gather (device.hpp PushArgs; push.ctl == nullptr = off): pass 1 stores
   // its rows as tagged words into every rank's window (rank-major
   // [world][batch][p1_out_rows]); pass 2 reads its own window of the call's parity
@@ -127,6 +129,21 @@ __device__ __forceinline__ float4 ll_load4(const unsigned long long* p, std::uin
   }
   return make_float4(__uint_as_float(std::uint32_t(w0)), __uint_as_float(std::uint32_t(w1)),
                      __uint_as_float(std::uint32_t(w2)), __uint_as_float(std::uint32_t(w3)));
+}
+// One tagged word once it carries `tag` (as ll_load4).
+__device__ __forceinline__ float ll_load1(const unsigned long long* p, std::uint32_t tag, int rank) {
+  unsigned long long w;
+  std::uint64_t t0 = 0;
+  for (int spin = 0;; ++spin) {
+    asm volatile("ld.volatile.u64 %0, [%1];\n" : "=l"(w) : "l"(p));
+    if (std::uint32_t(w >> 32) == tag) break;
+    std::uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (spin == 0) t0 = t;
+    if (t - t0 > 20000000000ull) ll_timeout(rank, tag, std::uint32_t(w >> 32));
+    __nanosleep(32);
+  }
+  return __uint_as_float(std::uint32_t(w));
 }
 // End of a pass-2 CTA: the last one of the call advances the rank's epoch.
 __device__ __forceinline__ void push_done(const RhtArgs& a, unsigned long long e) {
@@ -324,9 +341,13 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* xs
   } else {
     for (std::uint32_t v = tm.tid; v < chunk / 4; v += tm.n) {
       const std::uint32_t i = e0 + 4 * v;
-      float4 val = __ldcg(reinterpret_cast<const float4*>(a.in + rank_major(b, i, a.in_rows, a.batch, a.n)));
+      // element (part pp, vector b, row i) of the input
+      const std::uint32_t rows = a.in_local ? a.p1_out_rows : a.n, ri = a.in_local ? i - a.row0 : i;
+      float4 val = __ldcg(reinterpret_cast<const float4*>(
+          a.in + (a.in_local ? std::size_t(b) * rows + ri : rank_major(b, i, a.in_rows, a.batch, a.n))));
       for (int pp = 1; pp < a.in_parts; ++pp) {  // K-split partials (prefill), summed in order
-        const float4 w4 = __ldcg(reinterpret_cast<const float4*>(a.in + (std::size_t(pp) * a.batch + b) * a.n + i));
+        const float4 w4 =
+            __ldcg(reinterpret_cast<const float4*>(a.in + (std::size_t(pp) * a.batch + b) * rows + ri));
         val = make_float4(val.x + w4.x, val.y + w4.y, val.z + w4.z, val.w + w4.w);
       }
       ss += val.x * val.x + val.y * val.y + val.z * val.z + val.w * val.w;

@@ -51,6 +51,33 @@ def test_push_sim_bit_exact_repeated(world, m, n, bits):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("m,n,bits,batch", [(8192, 8192, 2, 96), (28672, 8192, 2, 256), (4096, 4096, 3, 64)])
+def test_push_sim_prefill(world, m, n, bits, batch):
+    # batches >= 64: K1 -> K4 on each rank's rows -> K3 pass 1 summing the rank's K-split
+    # partials and pushing -> pass 2.  The K split is chosen per shard, so the fp32
+    # partial sums may round differently from the unsharded forward: prefill bar 1e-4.
+    import torch
+
+    import paper_2402_04396_b200 as q8p
+    from conftest import random_artifact
+
+    art = random_artifact(m, n, STAGES[bits], m + n + world)
+    full = q8p.Layer.from_qshp(art, device=0)
+    shards = [q8p.Layer.from_qshp(art, device=0, rows=q8p.shard_rows(m, world, r)) for r in range(world)]
+    group = [q8p.PeerGroup(0, world, r, batch * (m // world)) for r in range(world)]
+    q8p.PeerGroup.connect_local(group)
+    for it in range(3):  # both window parities
+        x = torch.randn(batch, n, generator=torch.Generator().manual_seed(it)).cuda()
+        ys = q8p.forward_sharded_push_sim(shards, group, x)
+        want = full.forward(x)
+        for r in range(world):
+            assert torch.equal(ys[r], ys[0])
+        rel = float((ys[0] - want).norm() / want.norm())
+        assert rel < 1e-4, (it, rel)
+
+
+@pytest.mark.gpu
 def test_push_world1_public_api():
     import torch
 
@@ -60,9 +87,9 @@ def test_push_world1_public_api():
     m, n = 4096, 4096
     art = random_artifact(m, n, STAGES[2], 11)
     L = q8p.Layer.from_qshp(art, device=0)
-    g = q8p.PeerGroup(0, 1, 0, 32 * m)
+    g = q8p.PeerGroup(0, 1, 0, 128 * m)
     g.connect([g.handle])
-    for it, batch in enumerate([1, 7, 1, 33]):
+    for it, batch in enumerate([1, 7, 1, 33, 128, 2]):  # 128: the K4 prefill chain
         x = torch.randn(batch, n, generator=torch.Generator().manual_seed(it)).cuda()
         assert torch.equal(L.forward_sharded_push(x, g), L.forward(x)), it
 

@@ -138,6 +138,26 @@ def test_forward_sharded_world1_batches(batch):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("batch", [64, 200])
+def test_forward_sharded_world1_prefill(batch):
+    # batches >= 64 take K4 on the rank's rows + K3 pass 1 on them + one all-gather:
+    # at world 1 that is the unsharded prefill forward, bit for bit
+    import torch
+
+    import paper_2402_04396_b200 as q8p
+    from conftest import random_artifact
+
+    art = random_artifact(8192, 4096, [("e8p-2bit", 1.11)], 77)
+    x = torch.randn(batch, 4096, generator=torch.Generator().manual_seed(batch)).cuda()
+    comm = q8p.NcclComm(q8p.NcclComm.unique_id(), 1, 0, 0)
+    try:
+        L = q8p.Layer.from_qshp(art, device=0)
+        assert torch.equal(L.forward(x), L.forward_sharded(x, comm))
+    finally:
+        comm.close()
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("bits", [2, 3])
 def test_row_shards_on_one_gpu(world, bits):
