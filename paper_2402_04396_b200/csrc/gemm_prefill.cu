@@ -212,8 +212,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
 
   // code slab c of a unit: k slab ks, stage s, M tile t -> ring index (ks * nst + s) * kMT + t
   if (warp == 0) {
-    // ===== producer =====
-    if (lane == 0) {
+    // ===== producer (the whole warp, converged; elected lanes issue the copies) =====
+    {
       std::uint32_t g = 0, cg = 0;  // item / code-slab counters over the CTA's units
       for (std::uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
         const std::uint32_t p = u % a.P, nt = (u / a.P) / MP, mp = (u / a.P) % MP;
@@ -227,20 +227,20 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
                 if (cg >= kCodeSlots) mbar_wait(bar_ce + 8 * cs, ((cg / kCodeSlots) - 1) & 1);
                 const std::uint32_t bytes = s ? a.slab_bytes[1] : a.slab_bytes[0];
                 if (mt < a.MT) {
-                  mbar_arrive_expect_tx(bar_cf + 8 * cs, bytes);
-                  bulk_g2s(sb + kOffC + cs * kCodeSlot,
+                  mbar_arrive_expect_tx_e(bar_cf + 8 * cs, bytes);
+                  bulk_g2s_e(sb + kOffC + cs * kCodeSlot,
                            (s ? a.codes[1] : a.codes[0]) + (std::size_t(mt) * a.KSL + kc / 8) * bytes,
                            bytes, bar_cf + 8 * cs);
                 } else {
-                  mbar_arrive(bar_cf + 8 * cs);  // past the last row block: nothing to load
+                  mbar_arrive_e(bar_cf + 8 * cs);  // past the last row block: nothing to load
                 }
               }
           }
           for (std::uint32_t s = 0; s < nst; ++s, ++g) {
             const std::uint32_t bs = g % kSlots;
             if (g >= kSlots) mbar_wait(bar_be + 8 * bs, ((g / kSlots) - 1) & 1);
-            mbar_arrive_expect_tx(bar_bf + 8 * bs, kBBytes);
-            bulk_g2s(sb + kOffB + bs * kBBytes, a.btiles + ((std::size_t(nt) * a.KC + kc) * nst + s) * kBBytes,
+            mbar_arrive_expect_tx_e(bar_bf + 8 * bs, kBBytes);
+            bulk_g2s_e(sb + kOffB + bs * kBBytes, a.btiles + ((std::size_t(nt) * a.KC + kc) * nst + s) * kBBytes,
                      kBBytes, bar_bf + 8 * bs);
           }
         }
@@ -248,38 +248,31 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
     }
   } else if (warp == 1) {
     // ===== MMA issuer: per item 2 M tiles x 2 K-blocks x 2 terms =====
-    if (lane == 0) {
-      constexpr std::uint32_t idesc = idesc_bf16(128, kNT);
-      std::uint32_t g = 0, ul = 0;
-      for (std::uint32_t u = blockIdx.x; u < units; u += gridDim.x, ++ul) {
-        if (ul >= 1) mbar_wait(bar_de, (ul - 1) & 1);  // the previous unit's epilogue read the accumulators
+    // The whole warp runs the loop (converged, uniform operands); one elected lane
+    // issues each item's 8 MMAs + 2 commits in a single asm block.  (Issued from a
+    // divergent `lane == 0` branch they cost ~100 cycles each: R2UR waterfalls.)
+    constexpr std::uint32_t idesc = idesc_bf16(128, kNT);
+    std::uint32_t g = 0, ul = 0;
+    for (std::uint32_t u = blockIdx.x; u < units; u += gridDim.x, ++ul) {
+      if (ul >= 1) mbar_wait(bar_de, (ul - 1) & 1);  // the previous unit's epilogue read the accumulators
+      tc_fence_after();
+      std::uint32_t kc0, kc1;
+      krange(u % a.P, kc0, kc1);
+      const std::uint32_t uitems = (kc1 - kc0) * nst;
+      for (std::uint32_t it = 0; it < uitems; ++it, ++g) {
+        const std::uint32_t sl = g % kSlots, ph = (g / kSlots) & 1;
+        k4_stamp(a, 0, g, 0);
+        mbar_wait(bar_af + 8 * sl, ph);
+        k4_stamp(a, 0, g, 1);
+        mbar_wait(bar_bf + 8 * sl, ph);
+        k4_stamp(a, 0, g, 2);
         tc_fence_after();
-        std::uint32_t kc0, kc1;
-        krange(u % a.P, kc0, kc1);
-        const std::uint32_t uitems = (kc1 - kc0) * nst;
-        for (std::uint32_t it = 0; it < uitems; ++it, ++g) {
-          const std::uint32_t sl = g % kSlots, ph = (g / kSlots) & 1;
-          k4_stamp(a, 0, g, 0);
-          mbar_wait(bar_af + 8 * sl, ph);
-          k4_stamp(a, 0, g, 1);
-          mbar_wait(bar_bf + 8 * sl, ph);
-          k4_stamp(a, 0, g, 2);
-          tc_fence_after();
-          const std::uint32_t sa = sb + kOffA + sl * kABytes, sbb = sb + kOffB + sl * kBBytes;
-#pragma unroll
-          for (int t = 0; t < kMT; ++t)
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-              for (int h = 0; h < 2; ++h)
-                mma_f16_ss(tbase + t * kNT, sdesc(sa + t * kATile + j * 4096u, 128, 256),
-                           sdesc(sbb + h * kBTerm + j * 8192u, 128, 256), idesc, (it | j | h) != 0);
-          mma_commit(bar_ae + 8 * sl);
-          mma_commit(bar_be + 8 * sl);
-          k4_stamp(a, 0, g, 3);
-        }
-        mma_commit(bar_df);
+        const std::uint32_t sa = sb + kOffA + sl * kABytes, sbb = sb + kOffB + sl * kBBytes;
+        mma_f16_item_e<kNT, kATile / 16, 4096 / 16, 8192 / 16, kBTerm / 16>(
+            tbase, sdesc(sa, 128, 256), sdesc(sbb, 128, 256), idesc, it != 0, bar_ae + 8 * sl, bar_be + 8 * sl);
+        k4_stamp(a, 0, g, 3);
       }
+      mma_commit_e(bar_df);
     }
   } else {
     // ===== decoders: warp = (M tile t, lane quadrant q), thread = row; then the epilogue =====

@@ -261,6 +261,49 @@ __device__ __forceinline__ void bulk_g2s_hint_e(std::uint32_t dst, const void* s
       "l"(src), "r"(bytes), "r"(bar), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_e(std::uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b64 st;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e mbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(bar)
+      : "memory");
+}
+// One K4 item (gemm_prefill.cu), lane-elected once: for M tiles t = 0, 1, K-blocks
+// j = 0, 1 and bf16 terms h = hi, lo, tcgen05.mma kind::f16 into D_t = d + t * DStep
+// with A at a_desc + t * AStep + j * AKStep and B at b_desc + j * BKStep + h * BTerm
+// (descriptor units of 16 B); the first MMA of each tile accumulates iff `acc`.
+// Then two commits.
+template <int DStep, int AStep, int AKStep, int BKStep, int BTerm>
+__device__ __forceinline__ void mma_f16_item_e(std::uint32_t d, std::uint64_t a_desc, std::uint64_t b_desc,
+                                               std::uint32_t idesc, std::uint32_t acc, std::uint32_t bar0,
+                                               std::uint32_t bar1) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b64 a, b;\n\t.reg .b32 x;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      // tile 0
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "add.s64 b, %2, %10;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, b, %3, 1;\n\t"
+      "add.s64 a, %1, %8;\n\tadd.s64 b, %2, %9;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 b, b, %10;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      // tile 1
+      "add.s32 x, %0, %11;\n\tadd.s64 a, %1, %7;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [x], a, %2, %3, p;\n\t"
+      "add.s64 b, %2, %10;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [x], a, b, %3, 1;\n\t"
+      "add.s64 a, a, %8;\n\tadd.s64 b, %2, %9;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [x], a, b, %3, 1;\n\t"
+      "add.s64 b, b, %10;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [x], a, b, %3, 1;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t"
+      "}\n" ::"r"(d),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc), "r"(bar0), "r"(bar1), "n"(AStep), "n"(AKStep), "n"(BKStep),
+      "n"(BTerm), "n"(DStep)
+      : "memory");
+}
 #endif  // __CUDACC__
 
 }  // namespace q8p::detail::tc05
