@@ -25,7 +25,7 @@ print(f"issuer: items {len(iss)} | A wait {np.median(ph[:,0]):.0f} (mean {ph[:,0
 big = per > 3 * np.median(per)
 print("  long gaps (> 3x median):", int(big.sum()), "total cyc", int(per[big].sum()), "of", int(per.sum()))
 for w in range(16):
-    d = t[2 + w][:, [0, 1, 2, 4, 3]]; d = d[(d > 0).all(axis=1)] - base
+    d = t[2 + w][:, [0, 2, 2, 4, 3]]; d = d[(d[:, [0, 2, 3, 4]] > 0).all(axis=1)] - base
     if len(d) < 3: continue
     ph = np.diff(d, axis=1); per = np.diff(d[:, 0])
     print(f"   w{w}: decode+sts {np.median(ph[:,2]):.0f} | fence+syncwarp {np.median(ph[:,3]):.0f}")
