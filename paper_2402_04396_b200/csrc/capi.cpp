@@ -518,8 +518,8 @@ void forward_sharded_impl(const q8p_layer* L, const float* x, float* y, int batc
     // the K-split partials) -> one all-gather -> K3 pass 2
     launch_rht_in(L->side_v, x, w.pt, w.u, nullptr, nullptr, nullptr, 0, batch, s);
     launch_prefill(*L, w.pt, w.pbt, w.pz, batch, s);
-    launch_rht_out_local_f32(L->side_u, w.pz, int(prefill_parts(*L, batch)), L->row_begin, ml, w.u, nullptr, batch,
-                             s);
+    const K4Sched ks = prefill_sched(*L, batch);
+    launch_rht_out_local_f32(L->side_u, w.pz, int(ks.slices), L->row_begin, ml, w.u, nullptr, batch, s, &ks);
     if (world == 1) {
       launch_rht_out_pass2_gathered(L->side_u, w.u, ml, y, batch, s);
       return;
@@ -636,8 +636,9 @@ void forward_push_impl(const q8p_layer* L, q8p_peers* p, const float* x, float* 
   if (use_prefill_rows(L, batch)) {  // prefill: K1 -> K4 on this rank's rows -> pushing K3 pass 1 -> pass 2
     launch_rht_in(L->side_v, x, w.pt, w.u, nullptr, nullptr, nullptr, 0, batch, s);
     launch_prefill(*L, w.pt, w.pbt, w.pz, batch, s);
-    launch_rht_out_local_f32(L->side_u, w.pz, int(prefill_parts(*L, batch)), L->row_begin, L->m_local(), nullptr,
-                             &pa, batch, s);
+    const K4Sched ks = prefill_sched(*L, batch);
+    launch_rht_out_local_f32(L->side_u, w.pz, int(ks.slices), L->row_begin, L->m_local(), nullptr, &pa, batch, s,
+                             &ks);
     launch_rht_out_pass2_push(L->side_u, L->m_local(), pa, y, batch, s);
     return;
   }
@@ -668,7 +669,8 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
     launch_prefill(*L, w.pt, w.pbt, w.pz, batch, s);
     if (opts) record_event(opts->gemv_end_event, s);
     // K3 sums the K splits' partial z in fixed order while loading them
-    launch_rht_out(L->side_u, w.pz, w.u, y, batch, s, prefill_parts(*L, batch));
+    const K4Sched ks = prefill_sched(*L, batch);
+    launch_rht_out(L->side_u, w.pz, w.u, y, batch, s, int(ks.slices), &ks);
     return;
   }
   if (const int chunk = tc_chunk(L, batch)) {
@@ -1817,8 +1819,9 @@ q8p_status q8p_forward_sharded_push_sim(const q8p_layer* const* shards, q8p_peer
         const PushArgs pa = peers[r]->args();
         launch_rht_in(L->side_v, x, w.pt, w.u, nullptr, nullptr, nullptr, 0, batch, s);
         launch_prefill(*L, w.pt, w.pbt, w.pz, batch, s);
-        launch_rht_out_local_f32(L->side_u, w.pz, int(prefill_parts(*L, batch)), L->row_begin, L->m_local(), nullptr,
-                                 &pa, batch, s);
+        const K4Sched ks = prefill_sched(*L, batch);
+        launch_rht_out_local_f32(L->side_u, w.pz, int(ks.slices), L->row_begin, L->m_local(), nullptr, &pa, batch,
+                                 s, &ks);
       }
       for (int r = 0; r < world; ++r)
         launch_rht_out_pass2_push(L0->side_u, L0->m_local(), peers[r]->args(), y + std::size_t(r) * batch * L0->m,

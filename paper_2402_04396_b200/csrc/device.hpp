@@ -171,7 +171,38 @@ std::uint32_t tc_bimg_bytes(std::uint32_t n, int batch);  // B images for all k 
 constexpr int kPrefillMinBatch = 64;
 bool prefill_supported(const q8p_layer& L, int batch);
 std::size_t prefill_btile_bytes(const q8p_layer& L, int batch);
-std::uint32_t prefill_parts(const q8p_layer& L, int batch);  // K splits: z is [P][batch][m_local] partials
+// K4's stream-K schedule.  Tiles (N tile of `nt` vectors x M pair of `mrows` rows,
+// tile = nt_index * MP + mp) each have KS8 k-slab steps; the `grid` CTAs own equal
+// contiguous ranges of the tiles x KS8 steps in that order, so a tile is split
+// into pieces at CTA boundaries.  Piece k of a tile writes z slice k; K3 sums a
+// tile's pieces in piece order (k4_pieces, rht_device.cuh).  `slices` = the most
+// pieces any tile has (the z allocation).
+struct K4Sched {
+  std::uint32_t KS8 = 0, MP = 0, NTL = 0, grid = 0, slices = 1;
+  std::uint32_t nt = 256, mrows = 256;
+};
+#ifdef __CUDACC__
+#define Q8P_HD __host__ __device__
+#else
+#define Q8P_HD
+#endif
+// (32-bit arithmetic: prefill_sched guarantees total * grid < 2^32.)
+Q8P_HD inline std::uint32_t k4_total(const K4Sched& s) { return s.MP * s.NTL * s.KS8; }
+Q8P_HD inline std::uint32_t k4_bound(const K4Sched& s, std::uint32_t c) {  // first step of CTA c
+  return c * k4_total(s) / s.grid;
+}
+Q8P_HD inline std::uint32_t k4_cta_of(const K4Sched& s, std::uint32_t step) {  // the CTA owning `step`
+  std::uint32_t c = step * s.grid / k4_total(s);
+  while (c + 1 < s.grid && k4_bound(s, c + 1) <= step) ++c;
+  while (c > 0 && k4_bound(s, c) > step) --c;
+  return c;
+}
+Q8P_HD inline std::uint32_t k4_pieces(const K4Sched& s, std::uint32_t tile) {  // pieces of a tile
+  const std::uint32_t t0 = tile * s.KS8;
+  return k4_cta_of(s, t0 + s.KS8 - 1) - k4_cta_of(s, t0) + 1;
+}
+K4Sched prefill_sched(const q8p_layer& L, int batch);
+std::uint32_t prefill_parts(const q8p_layer& L, int batch);  // = prefill_sched().slices: z is [P][batch][m_local]
 void launch_prefill(const q8p_layer& L, const float* t, std::uint8_t* btiles, float* z, int batch, cudaStream_t s);
 // Benchmark support (bench_kernels.cu): bulk-copy stream of `bytes` at src (the
 // HBM read ceiling in K2's access pattern).
@@ -250,7 +281,7 @@ void launch_rht_out_acc_push(const DevSide& side, const std::int32_t* zacc, int 
 // [batch][m_local], or pushed into every rank's window when `push` is set.
 void launch_rht_out_local_f32(const DevSide& side, const float* zparts, int parts, std::uint32_t row0,
                               std::uint32_t m_local, float* z_send, const PushArgs* push, int batch,
-                              cudaStream_t s);
+                              cudaStream_t s, const K4Sched* sched = nullptr);
 void launch_rht_out_pass2_push(const DevSide& side, std::uint32_t m_local, const PushArgs& push, float* y, int batch,
                                cudaStream_t s);
 // Row-sharded forward: this rank's fp32 z rows [batch][m_local] from the limb accumulators.
@@ -275,7 +306,7 @@ void launch_rfft_in_limbs(const DevSide& side, const float* x, float* u_scratch,
                           std::size_t zero_words, int batch, cudaStream_t s);
 // K3 (fp32 input): y = T_u^T z.
 void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, float* y, int batch, cudaStream_t s,
-                    int in_parts = 1);
+                    int in_parts = 1, const K4Sched* sched = nullptr);
 // K3 (accumulator input): z = sum_s zscale_s alpha (2 Z_s - [E8P] TL) / 4 from the int32
 // limb accumulators [stage][zacc_cols][zacc_rows], then y = T_u^T z.
 void launch_rht_out_acc(const DevSide& side, const std::int32_t* zacc, int zacc_stages, std::uint32_t zacc_rows,

@@ -22,7 +22,9 @@
 // = the canonical K-major no-swizzle UMMA layout (LBO 128 B, SBO 256 B); the A
 // tile of a K chunk is the same layout over 128 rows.
 //
-// CTA (persistent; units = (N tile, pair of M tiles) of 256 rows x 256 vectors --
+// CTA (persistent, stream-K: equal shares of the tiles' k-slab steps; a tile = (N
+// tile, pair of M tiles) of 256 rows x 256 vectors, split at CTA boundaries into
+// pieces that K3 sums --
 // every B byte brought from L2 feeds two M tiles):
 //   warp 0   producer: code slabs (1-D bulk copies, one per k slab, stage and M
 //            tile) and B regions (one 32 KiB bulk copy per item) into rings
@@ -79,8 +81,8 @@ struct PrefillArgs {
   std::uint32_t KSL, KC;         // k slabs (32 codewords), K chunks (32 columns)
   std::uint32_t MT, NTL;         // M tiles (128 rows), N tiles (256 vectors)
   const std::uint8_t* btiles;    // [NTL][KC][nst][kBBytes]
-  float* z;                      // [P][batch][m]: one partial per K split
-  std::uint32_t P;               // K splits (units = N tiles x M pairs x P)
+  float* z;                      // [slices][batch][m]: piece k of a tile writes slice k
+  K4Sched sched;                 // stream-K schedule (device.hpp)
   std::uint32_t m, batch;
   const std::uint32_t* nib;      // [256] E8P magnitude nibbles
   const uint2* e81;              // [256] e8-1bit doubled rows
@@ -175,12 +177,28 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
   const std::uint32_t bar_df = bar_ce + 8 * kCodeSlots, bar_de = bar_df + 8, tmem_slot = bar_de + 8;
   const std::uint32_t tab = sb + kCtl;
   const std::uint32_t nst = std::uint32_t(a.nst);
-  const std::uint32_t MP = (a.MT + kMT - 1) / kMT, units = MP * a.NTL * a.P;  // unit = (N tile, M pair, K split)
-  const std::uint32_t KS8 = a.KC / 8;  // k slabs (8 K chunks each)
-  // K range [kc0, kc1) of split p: whole k slabs
-  auto krange = [&](std::uint32_t p, std::uint32_t& kc0, std::uint32_t& kc1) {
-    kc0 = (KS8 * p / a.P) * 8;
-    kc1 = p + 1 == a.P ? a.KC : (KS8 * (p + 1) / a.P) * 8;
+  const std::uint32_t MP = a.sched.MP, KS8 = a.sched.KS8;  // M pairs; k slabs (8 K chunks) per tile
+  // Stream-K: this CTA's steps [s_begin, s_end) of the tiles x KS8 k-slab steps; a
+  // "unit" = the part of one tile inside that range (tile = nt * MP + mp), its K
+  // chunks [kc0, kc1) and its piece index p (z slice).
+  const std::uint32_t s_begin = k4_bound(a.sched, blockIdx.x), s_end = k4_bound(a.sched, blockIdx.x + 1);
+  struct Unit {
+    std::uint32_t nt, mp, p, kc0, kc1;
+  };
+  auto unit_at = [&](std::uint32_t step) {  // the unit starting at `step` (inside this CTA's range)
+    Unit un;
+    const std::uint32_t tile = step / KS8;
+    const std::uint32_t t0 = tile * KS8;
+    un.nt = tile / MP;
+    un.mp = tile % MP;
+    un.p = blockIdx.x - k4_cta_of(a.sched, t0);
+    un.kc0 = (step - t0) * 8;
+    un.kc1 = ((s_end < t0 + KS8 ? s_end : t0 + KS8) - t0) * 8;
+    return un;
+  };
+  auto next_step = [&](std::uint32_t step) {  // first step after the unit starting at `step`
+    const std::uint32_t t1 = (step / KS8 + 1) * KS8;
+    return t1 < s_end ? t1 : s_end;
   };
 
   if (threadIdx.x == 0) {
@@ -215,10 +233,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
     // ===== producer (the whole warp, converged; elected lanes issue the copies) =====
     {
       std::uint32_t g = 0, cg = 0;  // item / code-slab counters over the CTA's units
-      for (std::uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
-        const std::uint32_t p = u % a.P, nt = (u / a.P) / MP, mp = (u / a.P) % MP;
-        std::uint32_t kc0, kc1;
-        krange(p, kc0, kc1);
+      for (std::uint32_t st = s_begin; st < s_end; st = next_step(st)) {
+        const Unit un = unit_at(st);
+        const std::uint32_t nt = un.nt, mp = un.mp, kc0 = un.kc0, kc1 = un.kc1;
         for (std::uint32_t kc = kc0; kc < kc1; ++kc) {
           if (kc % 8 == 0) {
             for (std::uint32_t s = 0; s < nst; ++s)
@@ -253,12 +270,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
     // divergent `lane == 0` branch they cost ~100 cycles each: R2UR waterfalls.)
     constexpr std::uint32_t idesc = idesc_bf16(128, kNT);
     std::uint32_t g = 0, ul = 0;
-    for (std::uint32_t u = blockIdx.x; u < units; u += gridDim.x, ++ul) {
+    for (std::uint32_t st = s_begin; st < s_end; st = next_step(st), ++ul) {
       if (ul >= 1) mbar_wait(bar_de, (ul - 1) & 1);  // the previous unit's epilogue read the accumulators
       tc_fence_after();
-      std::uint32_t kc0, kc1;
-      krange(u % a.P, kc0, kc1);
-      const std::uint32_t uitems = (kc1 - kc0) * nst;
+      const Unit un = unit_at(st);
+      const std::uint32_t uitems = (un.kc1 - un.kc0) * nst;
       for (std::uint32_t it = 0; it < uitems; ++it, ++g) {
         const std::uint32_t sl = g % kSlots, ph = (g / kSlots) & 1;
         k4_stamp(a, 0, g, 0);
@@ -285,11 +301,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
     struct Item {
       std::uint32_t kc, s, cs, cph, sl, g;
     };
-    for (std::uint32_t u = blockIdx.x; u < units; u += gridDim.x, ++ul) {
-      const std::uint32_t p = u % a.P, nt = (u / a.P) / MP, mt = ((u / a.P) % MP) * kMT + t;
+    for (std::uint32_t su = s_begin; su < s_end; su = next_step(su), ++ul) {
+      const Unit un = unit_at(su);
+      const std::uint32_t p = un.p, nt = un.nt, mt = un.mp * kMT + t, kc0 = un.kc0, kc1 = un.kc1;
       const bool live = mt < a.MT;
-      std::uint32_t kc0, kc1;
-      krange(p, kc0, kc1);
       const std::uint32_t uitems = (kc1 - kc0) * nst;
       auto item = [&](std::uint32_t i) {
         Item it;
@@ -426,36 +441,32 @@ __global__ void __launch_bounds__(256) pack_b_kernel(const float* __restrict__ t
 
 }  // namespace
 
-// K splits P <= 8 (whole k slabs per split) minimising a two-term cost: the
-// GEMM's critical path (waves of units x the longest split's K chunks, ~0.82 us
-// per chunk and stage, measured on 28672 x 8192) plus the (P - 1) extra partial
-// z arrays K4 writes and K3 reads back (8 B per vector-row at ~6.5 TB/s).
-std::uint32_t prefill_splits(const q8p_layer& L, int batch, int sms) {
-  const std::uint32_t MP = (tc_row_blocks(L.m_local()) + kMT - 1) / kMT, NTL = std::uint32_t((batch + kNT - 1) / kNT);
-  const std::uint32_t KS8 = std::max<std::uint32_t>((L.n / kKC) / 8, 1), base = MP * NTL;
-  const double chunk_us = 0.82 * L.num_stages, part_us = 8.0 * batch * L.m_local() / 6.5e6;
-  std::uint32_t best = 1;
-  double best_t = 0.0;
-  for (std::uint32_t P = 1; P <= 8 && P <= KS8; ++P) {
-    const std::uint32_t waves = (base * P + sms - 1) / sms, chunks = (KS8 + P - 1) / P * 8;
-    const double t = waves * chunks * chunk_us + (P - 1) * part_us;
-    if (P == 1 || t < best_t) best = P, best_t = t;
-  }
-  return best;
-}
-
 bool prefill_supported(const q8p_layer& L, int batch) {
-  // whole k slabs of 8 K chunks (both decoder teams have chunks in every slab)
-  return batch >= kPrefillMinBatch && L.tc[0].codes != nullptr && (L.num_stages == 1 || L.tc[1].codes != nullptr) &&
+  // whole k slabs of 8 K chunks (both decoder teams have chunks in every slab); rht
+  // output side (K3 sums the stream-K pieces; the rfft K3 reads one z array)
+  return batch >= kPrefillMinBatch && L.side_u.kind == 0 && L.tc[0].codes != nullptr &&
+         (L.num_stages == 1 || L.tc[1].codes != nullptr) &&
          L.n % (8 * kKC) == 0 && L.mma_tables != nullptr;
 }
 
-std::uint32_t prefill_parts(const q8p_layer& L, int batch) {
-  if (L.side_u.kind != 0) return 1;  // the rfft K3 reads one z array
+K4Sched prefill_sched(const q8p_layer& L, int batch) {
+  K4Sched s;
+  s.MP = (tc_row_blocks(L.m_local()) + kMT - 1) / kMT;
+  s.NTL = std::uint32_t((batch + kNT - 1) / kNT);
+  s.KS8 = (L.n / kKC) / 8;
+  s.nt = kNT;
+  s.mrows = kMT * 128;
   int sms = 0;
   cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device()), "sm count");
-  return prefill_splits(L, batch, sms);
+  if (std::uint64_t(s.MP) * s.NTL * s.KS8 * std::uint64_t(sms) >= (1ull << 32))
+    throw SizeError("prefill: layer x batch too large for the stream-K schedule");
+  s.grid = std::min(std::uint32_t(sms), k4_total(s));
+  s.slices = 1;
+  for (std::uint32_t tile = 0; tile < s.MP * s.NTL; ++tile) s.slices = std::max(s.slices, k4_pieces(s, tile));
+  return s;
 }
+
+std::uint32_t prefill_parts(const q8p_layer& L, int batch) { return prefill_sched(L, batch).slices; }
 
 std::size_t prefill_btile_bytes(const q8p_layer& L, int batch) {
   const std::size_t ntl = (std::size_t(batch) + kNT - 1) / kNT;
@@ -486,7 +497,7 @@ void launch_prefill(const q8p_layer& L, const float* t, std::uint8_t* btiles, fl
   a.NTL = NTL;
   a.btiles = btiles;
   a.z = z;
-  a.P = prefill_parts(L, batch);
+  a.sched = prefill_sched(L, batch);
   a.m = L.m_local();
   a.batch = std::uint32_t(batch);
   a.nib = L.mma_tables;
@@ -500,10 +511,7 @@ void launch_prefill(const q8p_layer& L, const float* t, std::uint8_t* btiles, fl
   }
 #endif
   kernel_attrs(reinterpret_cast<const void*>(prefill_kernel), int(kSmem));
-  int sms = 0;
-  cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device()), "sm count");
-  const unsigned grid = unsigned(std::min<std::uint32_t>((a.MT + kMT - 1) / kMT * a.NTL * a.P, std::uint32_t(sms)));
-  launch_pdl(prefill_kernel, dim3(grid), dim3(kThreads), kSmem, s, a);
+  launch_pdl(prefill_kernel, dim3(a.sched.grid), dim3(kThreads), kSmem, s, a);
   cuda_check(cudaGetLastError(), "prefill launch");
 #ifdef Q8P_K4_TRACE
   if (a.trace) {

@@ -343,7 +343,7 @@ void launch_rht_in(const DevSide& side, const float* x, float* t, float* u_scrat
 }
 
 void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, float* y, int batch, cudaStream_t s,
-                    int in_parts) {
+                    int in_parts, const K4Sched* sched) {
   if (batch <= 0) return;
   if (side.kind == 1) {
     if (in_parts > 1) throw UnsupportedError("rfft: K-split partial inputs");
@@ -356,6 +356,10 @@ void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, flo
   a.base = side.base;
   a.in = zin;
   a.in_parts = in_parts;
+  if (sched) {
+    if (a.P2 * a.q > 512 || sched->mrows < 256) throw UnsupportedError("rht: K4 pieces need chunks <= 2 M pairs");
+    a.sched = *sched, a.in_sched = 1;
+  }
   a.mid = u_scratch;
   a.out = y;
   a.batch = batch;
@@ -469,7 +473,7 @@ void launch_rht_out_acc_push(const DevSide& side, const std::int32_t* zacc, int 
 
 void launch_rht_out_local_f32(const DevSide& side, const float* zparts, int parts, std::uint32_t row0,
                               std::uint32_t m_local, float* z_send, const PushArgs* push, int batch,
-                              cudaStream_t s) {
+                              cudaStream_t s, const K4Sched* sched) {
   RhtArgs a{};
   plan_split_impl(side, a);
   const std::uint32_t chunk = a.P2 * a.q;
@@ -478,6 +482,10 @@ void launch_rht_out_local_f32(const DevSide& side, const float* zparts, int part
   a.in = zparts;
   a.in_parts = parts;
   a.in_local = 1;
+  if (sched) {
+    if (a.P2 * a.q > 512 || sched->mrows < 256) throw UnsupportedError("rht: K4 pieces need chunks <= 2 M pairs");
+    a.sched = *sched, a.in_sched = 1;
+  }
   a.mid = z_send;
   a.batch = batch;
   a.fwd = 0;

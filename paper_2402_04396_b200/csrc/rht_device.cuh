@@ -58,6 +58,8 @@ struct RhtArgs {
   std::uint32_t ch0, p1_count, row0, p1_out_rows, mid_rows, in_rows;
   int vpb;                      // vectors per CTA (fp32 passes; 0/1 = one)
   int in_parts;                 // pass 1 fp32 input = sum of in_parts partial arrays [batch][n] (0/1 = one)
+  K4Sched sched;                // in_sched: the input is K4's z slices; a row/vector tile's piece
+  int in_sched;                 //   count (k4_pieces) says how many of the in_parts slices it sums
   int in_local;                 // row-sharded prefill: the fp32 input holds this rank's rows only,
                                 // [in_parts][batch][p1_out_rows] (row i at i - row0)
   // Push all-gather (device.hpp PushArgs; push.ctl == nullptr = off): pass 1 stores
@@ -339,13 +341,33 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* xs
       }
     }
   } else {
+    // K4 stream-K pieces of the (<= 4) M-pair tiles this chunk's rows touch (chunk <= 512 rows)
+    // (scalars, not an array: a runtime-indexed local array would live in local memory)
+    int pc0 = 1, pc1 = 1, pc2 = 1, pc3 = 1;
+    std::uint32_t mp_first = 0;
+    if (a.in_sched) {
+      const std::uint32_t r0 = a.in_local ? e0 - a.row0 : e0;
+      mp_first = r0 / a.sched.mrows;
+      const std::uint32_t mp_last = (r0 + chunk - 1) / a.sched.mrows, tb = (std::uint32_t(b) / a.sched.nt) * a.sched.MP;
+      pc0 = int(k4_pieces(a.sched, tb + mp_first));
+      if (mp_first + 1 <= mp_last) pc1 = int(k4_pieces(a.sched, tb + mp_first + 1));
+      if (mp_first + 2 <= mp_last) pc2 = int(k4_pieces(a.sched, tb + mp_first + 2));
+      if (mp_first + 3 <= mp_last) pc3 = int(k4_pieces(a.sched, tb + mp_first + 3));
+    }
     for (std::uint32_t v = tm.tid; v < chunk / 4; v += tm.n) {
       const std::uint32_t i = e0 + 4 * v;
       // element (part pp, vector b, row i) of the input
       const std::uint32_t rows = a.in_local ? a.p1_out_rows : a.n, ri = a.in_local ? i - a.row0 : i;
       float4 val = __ldcg(reinterpret_cast<const float4*>(
           a.in + (a.in_local ? std::size_t(b) * rows + ri : rank_major(b, i, a.in_rows, a.batch, a.n))));
-      for (int pp = 1; pp < a.in_parts; ++pp) {  // K-split partials (prefill), summed in order
+      // K-split partials (prefill), summed in piece order: all in_parts slices, or the
+      // pieces of this (vector, row) tile under K4's stream-K schedule
+      int parts = a.in_parts;
+      if (a.in_sched) {
+        const std::uint32_t k = ri / a.sched.mrows - mp_first;
+        parts = k == 0 ? pc0 : k == 1 ? pc1 : k == 2 ? pc2 : pc3;
+      }
+      for (int pp = 1; pp < parts; ++pp) {
         const float4 w4 =
             __ldcg(reinterpret_cast<const float4*>(a.in + (std::size_t(pp) * a.batch + b) * rows + ri));
         val = make_float4(val.x + w4.x, val.y + w4.y, val.z + w4.z, val.w + w4.w);
