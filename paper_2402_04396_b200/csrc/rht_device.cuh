@@ -292,6 +292,19 @@ __device__ __forceinline__ float2 combine2(const RhtArgs& a, int b, std::uint32_
 }
 
 
+// K4 stream-K piece counts for pass 1's CTA (in_sched): the (<= 4) M-pair tiles of
+// chunk `ch` for the N tile of vector b0 (a CTA's vectors share it: vpb divides the
+// N tile).  Threads 0..3 write s_pieces[0..3]; the caller syncs.
+__device__ __forceinline__ void p1_tile_pieces(const RhtArgs& a, std::uint32_t ch, std::uint32_t chunk, int b0,
+                                               int* s_pieces) {
+  if (threadIdx.x < 4) {
+    const std::uint32_t e0 = ch * chunk, r0 = a.in_local ? e0 - a.row0 : e0;
+    const std::uint32_t mp = r0 / a.sched.mrows + threadIdx.x, mp_last = (r0 + chunk - 1) / a.sched.mrows;
+    s_pieces[threadIdx.x] =
+        mp <= mp_last ? int(k4_pieces(a.sched, (std::uint32_t(b0) / a.sched.nt) * a.sched.MP + mp)) : 1;
+  }
+}
+
 // Pass-1 smem: the Q x Q base (float for Q <= 28, int8 for the order-172 one;
 // shared by the CTA's teams), then per team the chunk x and the base output y.
 template <int Q>
@@ -318,9 +331,11 @@ __device__ void p1_load_base(const RhtArgs& a, float* Bs) {
 // Pass 1 on chunk `ch` of vector b.  xs: the team's [2][chunk] floats; Bs: the
 // base (p1_load_base); red: >= 32 floats of team-shared smem.
 // ll_tag: the push all-gather's call tag (a.push.ctl set), else unused.
+// pieces (in_sched): K4 stream-K piece counts of the (<= 4) M-pair tiles the chunk's rows
+// touch, for this vector's N tile, from M pair p1_mp_first on (p1_tile_pieces).
 template <int Q>
 __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* xs, const float* Bs, float* red,
-                            const Team& tm, std::uint32_t ll_tag = 0) {
+                            const Team& tm, std::uint32_t ll_tag = 0, const int* pieces = nullptr) {
   const std::uint32_t chunk = a.P2 * Q;  // floats, multiple of 4
   const std::uint32_t e0 = ch * chunk;
   float* x = xs;                          // [P2][Q]
@@ -341,19 +356,7 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* xs
       }
     }
   } else {
-    // K4 stream-K pieces of the (<= 4) M-pair tiles this chunk's rows touch (chunk <= 512 rows)
-    // (scalars, not an array: a runtime-indexed local array would live in local memory)
-    int pc0 = 1, pc1 = 1, pc2 = 1, pc3 = 1;
-    std::uint32_t mp_first = 0;
-    if (a.in_sched) {
-      const std::uint32_t r0 = a.in_local ? e0 - a.row0 : e0;
-      mp_first = r0 / a.sched.mrows;
-      const std::uint32_t mp_last = (r0 + chunk - 1) / a.sched.mrows, tb = (std::uint32_t(b) / a.sched.nt) * a.sched.MP;
-      pc0 = int(k4_pieces(a.sched, tb + mp_first));
-      if (mp_first + 1 <= mp_last) pc1 = int(k4_pieces(a.sched, tb + mp_first + 1));
-      if (mp_first + 2 <= mp_last) pc2 = int(k4_pieces(a.sched, tb + mp_first + 2));
-      if (mp_first + 3 <= mp_last) pc3 = int(k4_pieces(a.sched, tb + mp_first + 3));
-    }
+    const std::uint32_t mp_first = a.in_sched ? (a.in_local ? e0 - a.row0 : e0) / a.sched.mrows : 0;
     for (std::uint32_t v = tm.tid; v < chunk / 4; v += tm.n) {
       const std::uint32_t i = e0 + 4 * v;
       // element (part pp, vector b, row i) of the input
@@ -362,11 +365,7 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* xs
           a.in + (a.in_local ? std::size_t(b) * rows + ri : rank_major(b, i, a.in_rows, a.batch, a.n))));
       // K-split partials (prefill), summed in piece order: all in_parts slices, or the
       // pieces of this (vector, row) tile under K4's stream-K schedule
-      int parts = a.in_parts;
-      if (a.in_sched) {
-        const std::uint32_t k = ri / a.sched.mrows - mp_first;
-        parts = k == 0 ? pc0 : k == 1 ? pc1 : k == 2 ? pc2 : pc3;
-      }
+      const int parts = a.in_sched ? pieces[ri / a.sched.mrows - mp_first] : a.in_parts;
       for (int pp = 1; pp < parts; ++pp) {
         const float4 w4 =
             __ldcg(reinterpret_cast<const float4*>(a.in + (std::size_t(pp) * a.batch + b) * rows + ri));
