@@ -171,19 +171,48 @@ __global__ void __launch_bounds__(256) rht_pass2_reg(RhtArgs a) {
       for (int r = 0; r < P1; ++r)
         v[r] = ll_load1(win + rank_major(b, r * stride + col, a.mid_rows, a.batch, a.n), tag, a.push.rank);
     }
-  } else {
+  } else if (a.mid_rows) {  // gathered rank-major rows (sharded)
 #pragma unroll
     for (int r = 0; r < P1; ++r)
       v[r] = live ? __ldcg(a.mid + rank_major(b, r * stride + col, a.mid_rows, a.batch, a.n)) : 0.f;
-  }
-  // K3's output signs, fetched alongside the data (bit r = row r's sign)
-  unsigned long long neg = 0;
-  if (!a.fwd && live)
+  } else {
+    const float* const src = a.mid + std::size_t(b) * a.n + col;
 #pragma unroll
-    for (int r = 0; r < P1; ++r) {
-      const std::uint32_t i = r * stride + col;
-      neg |= static_cast<unsigned long long>((a.signs[i >> 3] >> (i & 7)) & 1) << r;
+    for (int r = 0; r < P1; ++r) v[r] = live ? __ldcg(src + r * stride) : 0.f;
+  }
+  // K3's output signs (bit r = row r's sign of this lane's column)
+  unsigned long long neg = 0;
+  if (!a.fwd) {
+    if (stride % 32 == 0 && (reinterpret_cast<std::uintptr_t>(a.signs) & 3) == 0 && warp_live) {
+      // lane l loads the 32 sign bits of the warp's columns in rows l and l + 32, and a
+      // 32 x 32 bit transpose across the lanes hands lane c its column's bits
+      const std::uint32_t c0 = col - (threadIdx.x & 31u), lane = threadIdx.x & 31u;
+      auto row_word = [&](std::uint32_t r) {
+        return r < std::uint32_t(P1)
+                   ? *reinterpret_cast<const std::uint32_t*>(a.signs + (std::size_t(r) * stride + c0) / 8)
+                   : 0u;
+      };
+      auto transpose32 = [&](std::uint32_t x) {
+#pragma unroll
+        for (int sft = 16; sft > 0; sft >>= 1) {
+          const std::uint32_t m = sft == 16 ? 0x0000FFFFu : sft == 8 ? 0x00FF00FFu : sft == 4 ? 0x0F0F0F0Fu
+                                : sft == 2 ? 0x33333333u : 0x55555555u;
+          const std::uint32_t y = __shfl_xor_sync(0xffffffffu, x, sft);
+          x = (lane & sft) ? (x & ~m) | ((y >> sft) & m) : (x & m) | ((y << sft) & ~m);
+        }
+        return x;
+      };
+      const std::uint32_t lo = transpose32(row_word(lane));
+      const std::uint32_t hi = P1 > 32 ? transpose32(row_word(lane + 32)) : 0u;
+      neg = (static_cast<unsigned long long>(hi) << 32) | lo;
+    } else if (live) {
+#pragma unroll
+      for (int r = 0; r < P1; ++r) {
+        const std::uint32_t i = r * stride + col;
+        neg |= static_cast<unsigned long long>((a.signs[i >> 3] >> (i & 7)) & 1) << r;
+      }
     }
+  }
 #pragma unroll
   for (int len = 1; len < P1; len <<= 1)
 #pragma unroll
