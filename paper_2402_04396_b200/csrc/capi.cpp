@@ -171,14 +171,6 @@ void setup_side_rfft(q8p_layer* L, DevSide& side, std::uint32_t n, const float* 
   side.tw = static_cast<const float2*>(upload(L, tw.data(), tw.size() * 4));
 }
 
-bool mma_k2_selected() {
-  static const bool on = [] {
-    const char* e = std::getenv("Q8P_K2");
-    return e && std::string(e) == "mma";
-  }();
-  return on;
-}
-
 // Builds a device layer from host fields for rows [r0, r1).
 q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t r1, int device) {
   if (!d.stages || d.num_stages < 1) throw ValidationError("artifact has no quantization stages");
@@ -226,8 +218,8 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
     {
       const std::vector<std::uint8_t> img = tc_lut_image();
       L->lut_img = static_cast<const std::uint8_t*>(upload(L.get(), img.data(), img.size()));
-      const std::vector<std::uint32_t> tw = mma_table_words();
-      L->mma_tables = static_cast<const std::uint32_t*>(upload(L.get(), tw.data(), tw.size() * 4));
+      const std::vector<std::uint32_t> tw = decode_table_words();
+      L->dec_tables = static_cast<const std::uint32_t*>(upload(L.get(), tw.data(), tw.size() * 4));
     }
     const std::size_t nb = d.n / 8, words = std::size_t(r1 - r0) * nb;
     const std::uint8_t* odd_dev = nullptr;  // E8P odd-parity table for the device transcode
@@ -269,12 +261,6 @@ q8p_layer* build_layer(const q8p_layer_desc& d, std::uint32_t r0, std::uint32_t 
         tc_transcode_device(L->codes[s], r1 - r0, d.n, kind, static_cast<std::uint8_t*>(slabs), odd_dev,
                             t_build_stream);
         L->tc[s].codes = slabs;
-        if (mma_k2_selected()) {  // warp-MMA records only when that kernel is selected (A/B)
-          void* recs = dev_alloc(L.get(), mma_code_bytes(r1 - r0, d.n, kind));
-          mma_transcode_device(L->codes[s], r1 - r0, d.n, kind, static_cast<std::uint8_t*>(recs), odd_dev,
-                               t_build_stream);
-          L->mma[s] = recs;
-        }
       }
     }
     cuda_check(cudaStreamSynchronize(t_build_stream), "layer upload");
@@ -434,11 +420,6 @@ std::size_t workspace_parts(const q8p_layer* L, int batch, Workspace* w, void* b
 }
 std::size_t workspace_size(const q8p_layer* L, int batch) { return workspace_parts(L, batch, nullptr, nullptr); }
 
-// K2 kernel for decode batches: Q8P_K2=mma selects the warp-level MMA kernel
-// (gemv_mma.cu; measured slower in the pipeline), otherwise the
-// tcgen05 kernel -- an A/B knob, same accumulators bit for bit.
-bool use_mma(const q8p_layer* L, int batch) { return mma_k2_selected() && mma_supported(*L, batch); }
-
 // K1 -> K2 on the layer's local rows: leaves int32 accumulators in w.zacc (tensor-core
 // path) or fp32 z rows in w.z (portable path).
 void forward_local(const q8p_layer* L, const float* x, int batch, const Workspace& w, cudaStream_t s,
@@ -453,10 +434,7 @@ void forward_local(const q8p_layer* L, const float* x, int batch, const Workspac
                         std::size_t(L->num_stages) * N * w.rows_pad, batch, s);
 #endif
     if (opts) record_event(opts->gemv_start_event, s);
-    if (use_mma(L, batch))
-      launch_gemv_mma(*L, w.bimg, w.zacc, w.rows_pad, batch, s);
-    else
-      launch_gemv_tc(*L, w.bimg, w.zacc, w.rows_pad, batch, s);
+    launch_gemv_tc(*L, w.bimg, w.zacc, w.rows_pad, batch, s);
     if (opts) record_event(opts->gemv_end_event, s);
   } else if (L->side_v.kind == 1) {  // rfft (kernels_rfft.cu): t = T_v x through the scratch
     launch_rht_in(L->side_v, x, w.t, w.u, nullptr, nullptr, nullptr, 0, batch, s);
@@ -1383,12 +1361,7 @@ q8p_status q8p_bench_gemv(const q8p_layer* L, int batch, void* ws, size_t ws_byt
     Workspace w;
     workspace_parts(L, batch, &w, ws);
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
-    for (int r = 0; r < reps; ++r) {
-      if (use_mma(L, batch))
-        launch_gemv_mma(*L, w.bimg, w.zacc, w.rows_pad, batch, s);
-      else
-        launch_gemv_tc(*L, w.bimg, w.zacc, w.rows_pad, batch, s);
-    }
+    for (int r = 0; r < reps; ++r) launch_gemv_tc(*L, w.bimg, w.zacc, w.rows_pad, batch, s);
     return Q8P_OK;
   } catch (...) {
     return status_of_current_exception();

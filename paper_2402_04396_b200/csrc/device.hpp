@@ -91,9 +91,8 @@ struct q8p_layer {
   // layers the tensor-core path cannot run (first stage not E8P; portable GEMV)
   void* codes[2] = {nullptr, nullptr};
   q8p::detail::SlabCodes tc[2];
-  void* mma[2] = {nullptr, nullptr};       // warp-MMA records (gemv_mma.cu), per stage
-  const std::uint32_t* mma_tables = nullptr;  // device [256] E8P nibble words + [256][2] e8-1bit rows
   const std::uint8_t* lut_img = nullptr;   // device 64 KiB lane-replicated decode LUT (gemv_tc.cu)
+  const std::uint32_t* dec_tables = nullptr;  // device [256] E8P nibble words + [256][2] e8-1bit rows (K4)
   std::size_t device_bytes = 0;
   std::size_t code_bytes = 0;
   std::vector<void*> allocations;
@@ -212,17 +211,7 @@ void launch_stream(const void* src, std::size_t bytes, unsigned* sink, cudaStrea
 void launch_k2_decode(const q8p_layer& L, int stage, std::int8_t* a_out, std::uint8_t* side, cudaStream_t s);
 void launch_gemv_tc(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* zacc, std::uint32_t rows_pad,
                     int batch, cudaStream_t s);
-// Warp-level tensor-core GEMV for decode batches (gemv_mma.cu): same K1 B images,
-// accumulators and K3 as the tcgen05 path.
-constexpr int kMmaMaxBatch = 8;
-std::uint32_t mma_row_blocks(std::uint32_t m_local);
-std::size_t mma_code_bytes(std::uint32_t m_local, std::uint32_t n, int kind);
-void mma_transcode_device(const void* codes, std::uint32_t m_local, std::uint32_t n, int kind, std::uint8_t* out,
-                          const std::uint8_t* odd_parity_dev, cudaStream_t s);
-bool mma_supported(const q8p_layer& L, int batch);
-void launch_gemv_mma(const q8p_layer& L, const std::uint8_t* bimg, std::int32_t* zacc, std::uint32_t rows_pad,
-                     int batch, cudaStream_t s);
-std::vector<std::uint32_t> mma_table_words();  // host image of q8p_layer::mma_tables
+std::vector<std::uint32_t> decode_table_words();  // host image of q8p_layer::dec_tables
 // K1 (fp32 flavour, q8p_rht): t = T_v x (+ amax, tsum when non-null).
 void launch_rht_in(const DevSide& side, const float* x, float* t, float* u_scratch, float* amax, float* tsum,
                    std::int32_t* zero_ptr, std::size_t zero_words, int batch, cudaStream_t s);

@@ -446,7 +446,7 @@ bool prefill_supported(const q8p_layer& L, int batch) {
   // output side (K3 sums the stream-K pieces; the rfft K3 reads one z array)
   return batch >= kPrefillMinBatch && L.side_u.kind == 0 && L.tc[0].codes != nullptr &&
          (L.num_stages == 1 || L.tc[1].codes != nullptr) &&
-         L.n % (8 * kKC) == 0 && L.mma_tables != nullptr;
+         L.n % (8 * kKC) == 0 && L.dec_tables != nullptr;
 }
 
 K4Sched prefill_sched(const q8p_layer& L, int batch) {
@@ -500,8 +500,8 @@ void launch_prefill(const q8p_layer& L, const float* t, std::uint8_t* btiles, fl
   a.sched = prefill_sched(L, batch);
   a.m = L.m_local();
   a.batch = std::uint32_t(batch);
-  a.nib = L.mma_tables;
-  a.e81 = reinterpret_cast<const uint2*>(L.mma_tables + 256);
+  a.nib = L.dec_tables;
+  a.e81 = reinterpret_cast<const uint2*>(L.dec_tables + 256);
 #ifdef Q8P_K4_TRACE
   static const char* trace_env = std::getenv("Q8P_TRACE");
   if (trace_env) {

@@ -616,6 +616,20 @@ std::vector<std::uint8_t> tc_lut_image() {
   return img;
 }
 
+// Compact decode tables (q8p_layer::dec_tables, read by K4's decoders through the
+// read-only path): [256] E8P magnitude-nibble words (d = 1,3,5 -> 0,1,2 at bits 4c),
+// then [256][2] e8-1bit doubled rows (8 x s8).
+std::vector<std::uint32_t> decode_table_words() {
+  const E8PTable& t = e8p_table();
+  const auto& d = e8_1bit_doubled();
+  std::vector<std::uint32_t> w(256 * 3, 0);
+  for (int i = 0; i < 256; ++i) {
+    for (int c = 0; c < 8; ++c) w[i] |= std::uint32_t((t.doubled[i][c] - 1) / 2) << (4 * c);
+    for (int c = 0; c < 8; ++c) w[256 + 2 * i + c / 4] |= std::uint32_t(std::uint8_t(d[i][c])) << (8 * (c % 4));
+  }
+  return w;
+}
+
 std::uint32_t tc_slab_bytes(int kind) { return kind == 0 ? kE8pSlab : kE81Slab; }
 std::uint32_t tc_row_blocks(std::uint32_t m_local) { return (m_local + 127) / 128; }
 std::uint32_t tc_k_slabs(std::uint32_t n) { return (n / 8 + kSlabCw - 1) / kSlabCw; }
