@@ -25,7 +25,7 @@ for sh in os.environ.get("SHAPES", "28672x8192").split(","):
             torch.cuda.synchronize()
     f = [g for g in glob.glob(out + ".*") if ".fused." not in g]
     t = np.fromfile(f[0], dtype=np.uint64).astype(np.int64)
-    tr = t[: 11 * K * 4].reshape(11, K, 4)
+    tr = t[: 16 * K * 4].reshape(16, K, 4)  # roles 0-10, 11-12 = per-CTA globaltimer, 13-14 = issuers g1, g2
     base = tr[tr > 0].min()
     print(f"== {sh}")
     for g in range(3):
