@@ -602,14 +602,15 @@ def run_ours(args):
         per = []
         for li, (m, n) in enumerate(layers):
             t = statistics.mean(gemv_ms[li]) * 1e-3
-            fl = 2.0 * m * n * B  # one effective matrix; the MMAs issued are 2x (bf16 hi/lo)
+            fl = 2.0 * m * n * B  # one effective matrix; the s8 MMAs issued are 2x per stage (2 limbs)
             per.append({"layer": f"{m}x{n}", "flops": fl, "us": t * 1e6, "tflops": fl / t / 1e12,
                         "tflops_issued": 2 * fl * sum(1 for _ in SCHEMES[args.bits]) / t / 1e12})
         dom = max(per, key=lambda p: p["flops"])
         roof = {"bound": "tensor", "achieved": dom["tflops"], "peak": tf_peak, "unit": "TFLOP/s",
                 "frac": dom["tflops"] / tf_peak, "traffic": None,
                 "kernel": f"q8p prefill decode-GEMM (pack + K4) on {dom['layer']} at batch {B}: 2 m n B flops / "
-                          f"mean CUDA-event duration (tflops_issued counts the bf16 hi/lo MMAs actually run)",
+                          f"mean CUDA-event duration vs the measured bf16 peak (K4 runs kind::i8 MMAs: tflops_issued counts "
+                          f"the s8 ops actually run, 2 activation limbs per stage, against an s8 peak of 2x bf16)",
                 "per_layer": per}
 
     cpu = None

@@ -1,7 +1,7 @@
 // K4: prefill (large batch) decode-GEMM on the 5th-gen tensor cores,
 // weight-stationary per tile: every weight tile is decoded ONCE into shared
-// memory and multiplied against 256 vectors (tcgen05.mma kind::f16, bf16 x bf16
-// -> fp32 accumulators in tensor memory).
+// memory and multiplied against 256 vectors (tcgen05.mma kind::i8, s8 x s8 ->
+// exact s32 accumulators in tensor memory).
 //
 // Semantics: z[b][r] = sum_s scale_s * sum_k <decode_s(codes[s][r][k]), t_b[8k:8k+8]>
 // (core/src/pipeline.cpp:172-191; the reference CLI loops infer per vector,
@@ -9,32 +9,31 @@
 //
 // Operands.  A = 4 v exactly: E8P 4 v = 2 sigma d + 2 b - 1 (odd integers in
 // [-11, 11], e8p.cpp:81-100), e8-1bit 4 v = 2 * doubled (codebook.cpp:65-72) --
-// exact in bf16.  B = scale_s * t split into two bf16 terms (hi = bf16(x),
-// lo = bf16(x - hi): 16 significant bits) accumulated into the same fp32
-// accumulator, so z = D / 4 with no epilogue scaling; RVQ stages are further
-// K items against their own scaled B.  Relative error ~1e-5 (fp32 accumulation,
-// 16-bit activations), inside the north-star 1e-3.
+// exact in s8.  B: per vector b one fixed-point scale alpha_b = max_s scale_s *
+// max|t_b| / 32000 (pack kernel), L = rint(scale_s t / alpha_b) (|L| <= 32000,
+// 16-bit activations, the precision of the former bf16 hi/lo split) as two balanced
+// s8 limbs L = 256 h + l; D_h, D_l = A . h, A . l in two s32 accumulators (exact:
+// |D| < 2^27), z = alpha_b (256 D_h + D_l) / 4 in the epilogue; RVQ stages are
+// further K items against their own L (same alpha_b).  kind::i8 runs K = 32 per
+// MMA at the f16 rate of K = 16, so the two limbs cost what ONE bf16 term did.
 //
 // Layout.  Codes: the tensor-core slabs of gemv_tc.cu (128 rows x 32 codewords
 // per stage, [row block][k slab]).  B tiles (written by the pack kernel): per
-// (N tile of 256 vectors, K chunk of 32, stage) one contiguous 32 KiB region
-// [term hi/lo][K-block of 16][32 vector groups][2 K halves][8 vectors][16 B]
-// = the canonical K-major no-swizzle UMMA layout (LBO 128 B, SBO 256 B); the A
-// tile of a K chunk is the same layout over 128 rows.
+// (N tile of 256 vectors, K chunk of 32, stage) one contiguous 16 KiB region
+// [limb h/l][32 vector groups][2 K halves][8 vectors][16 B] = the canonical
+// K-major no-swizzle UMMA layout (LBO 128 B, SBO 256 B), then alpha per vector;
+// the A tile of a K chunk is the same layout over 128 rows (4 KiB).
 //
 // CTA (persistent, stream-K: equal shares of the tiles' k-slab steps; a tile = (N
-// tile, pair of M tiles) of 256 rows x 256 vectors, split at CTA boundaries into
-// pieces that K3 sums --
-// every B byte brought from L2 feeds two M tiles):
-//   warp 0   producer: code slabs (1-D bulk copies, one per k slab, stage and M
-//            tile) and B regions (one 32 KiB bulk copy per item) into rings
-//   warp 1   MMA issuer: per item (K chunk, stage) 2 M tiles x 2 K-blocks x 2 terms
-//            of tcgen05.mma M=128 N=256 K=16 into the tiles' accumulators (2 x 256
-//            TMEM columns)
-//   warps 2-17 decoders, two teams of 8 (warp = team x M tile x lane quadrant,
-//            thread = row; team = K chunk parity): slab -> bf16 A tile per item;
-//            then the unit's epilogue (tcgen05.ld -> z rows, a team per 128 columns)
-#include <cuda_bf16.h>
+// tile, M tile) of 128 rows x 256 vectors, split at CTA boundaries into pieces
+// that K3 sums):
+//   warp 0   producer: code slabs (1-D bulk copies, one per k slab and stage) and
+//            B regions (one 16 KiB bulk copy per item) into rings
+//   warp 1   MMA issuer: per item (K chunk, stage) 2 limbs x tcgen05.mma M=128
+//            N=256 K=32 into the limbs' accumulators (2 x 256 TMEM columns)
+//   warps 2-17 decoders, four teams of 4 (warp = team x lane quadrant, thread =
+//            row; team = K chunk mod 4): slab -> s8 A tile per item; then the
+//            unit's epilogue (tcgen05.ld -> z rows, a team per 64 columns)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -51,17 +50,22 @@ namespace {
 using namespace tc05;
 
 constexpr int kNT = 256;                              // vectors per N tile (MMA N)
-constexpr int kKC = 32;                               // K per pipeline item (2 K-blocks of 16)
-constexpr int kMT = 2;                                // M tiles (128 rows each) per CTA: B reused twice
-constexpr std::uint32_t kATile = 128u * kKC * 2u;     // 8 KiB per M tile
+constexpr int kKC = 32;                               // K per pipeline item (one s8 MMA K)
+constexpr int kMT = 1;                                // M tiles (128 rows) per CTA (TMEM: 2 limbs x 256 columns)
+constexpr std::uint32_t kATile = 128u * kKC;          // 4 KiB per M tile (s8)
 constexpr std::uint32_t kABytes = kMT * kATile;
-constexpr std::uint32_t kBTerm = kNT * kKC * 2u;      // 16 KiB per bf16 term
-constexpr std::uint32_t kBBytes = 2u * kBTerm;        // hi + lo
-constexpr std::uint32_t kSlots = 3;                   // A / B pipeline depth
-constexpr std::uint32_t kCodeSlots = 8;               // code slab ring (M tiles x stages x 2 k slabs)
+constexpr std::uint32_t kBLimb = kNT * kKC;           // 8 KiB per s8 limb
+constexpr std::uint32_t kBBytes = 2u * kBLimb;        // h + l
+// A / B pipeline depth.  A team's consecutive items are up to (kTeams - 1) * nst + 1
+// apart (nst <= 2: 7); its parity wait on an A slot is only unambiguous when that
+// gap is <= kSlots (the slot's previous phase is then known complete).
+constexpr std::uint32_t kSlots = 7;
+constexpr std::uint32_t kCodeSlots = 8;               // code slab ring (stages x k slabs)
 constexpr std::uint32_t kCodeSlot = 4 * 2048 + 512;   // E8P slab bytes (e8-1bit slabs are smaller)
-constexpr int kTeams = 2;                             // decoder teams: K chunks alternate between them
-constexpr int kDecTeam = 8;                           // decoder warps per team: 2 M tiles x 4 lane quadrants
+constexpr int kTeams = 4;                             // decoder teams: K chunk kc goes to team kc % 4
+constexpr int kDecTeam = 4 * kMT;                     // decoder warps per team: M tiles x 4 lane quadrants
+constexpr float kLMax = 32000.f;                      // |L| bound: balanced limbs h, l in [-128, 127]
+static_assert((kTeams - 1) * 2 + 1 <= int(kSlots), "A/B ring too shallow for the decoder teams");
 constexpr int kDec = kTeams * kDecTeam;
 constexpr int kThreads = (2 + kDec) * 32;
 constexpr std::uint32_t kCtl = 1024, kTab = 4096;     // barriers; decode tables
@@ -69,9 +73,6 @@ constexpr std::uint32_t kOffA = kCtl + kTab, kOffB = kOffA + kSlots * kABytes, k
 constexpr std::size_t kSmem = kOffC + kCodeSlots * kCodeSlot;
 static_assert(kSmem <= 227 * 1024, "prefill smem");
 
-constexpr std::uint32_t idesc_bf16(int M, int N) {  // bf16 x bf16 -> f32, both K-major
-  return (1u << 4) | (1u << 7) | (1u << 10) | (std::uint32_t(N >> 3) << 17) | (std::uint32_t(M >> 4) << 24);
-}
 
 struct PrefillArgs {
   const std::uint8_t* codes[2];  // tensor-core slabs per stage
@@ -86,6 +87,7 @@ struct PrefillArgs {
   std::uint32_t m, batch;
   const std::uint32_t* nib;      // [256] E8P magnitude nibbles
   const uint2* e81;              // [256] e8-1bit doubled rows
+  const float* alpha;            // [NTL * 256] per-vector fixed-point scale (pack kernel)
   unsigned long long* trace;     // debug timeline (Q8P_K4_TRACE builds + Q8P_TRACE): CTA 0, nullptr = off
 };
 
@@ -113,10 +115,6 @@ __device__ __forceinline__ std::uint32_t prmt(std::uint32_t a, std::uint32_t b, 
   asm("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
   return r;
 }
-__device__ __forceinline__ std::uint32_t bf2(float a, float b) {
-  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<const std::uint32_t*>(&h);
-}
 // 32 lanes x 32 columns of fp32 from tensor memory.
 __device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, float (&v)[32]) {
   std::uint32_t r[32];
@@ -134,38 +132,48 @@ __device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// bf16 bytes of 4 v = 2 sigma d + 2 b - 1 (odd integers in [-11, 11]), looked up by
+// s8 bytes of 4 v = 2 sigma d + 2 b - 1 (odd integers in [-11, 11]), looked up by
 // PRMT with the nibble sel = m | sigma << 2 (m = 0, 1, 2 for d = 1, 3, 5; the LUT
 // nibble XOR the negate flag, as in K2):
-//   high bytes, b = 0:  [3F 40 41 _ | C0 C0 C1 _]  (1, 5, 9 | -3, -7, -11)
-//               b = 1:  [40 40 41 _ | BF C0 C1 _]  (3, 7, 11 | -1, -5, -9)
-//     = the b = 0 table with byte 0 + b and byte 4 - b (no carries);
-//   low bytes,  b = 0:  [80 A0 10 _ | 40 E0 30 _]; b = 1 is the b = 0 table with the
-//     sigma slot flipped (3, 7, 11 have the low bytes of -3, -7, -11, and so on).
-constexpr std::uint32_t kHiLo = 0x0041403Fu, kHiHi = 0x00C1C0C0u;
-constexpr std::uint32_t kLoLo = 0x0010A080u, kLoHi = 0x0030E040u;
+//   b = 0:  [01 05 09 _ | FD F9 F5 _]  (1, 5, 9 | -3, -7, -11)
+//   b = 1:  [03 07 0B _ | FF FB F7 _]  (3, 7, 11 | -1, -5, -9) = the b = 0 table + 2
+//   per byte (no carries).
+constexpr std::uint32_t kI8Pos = 0x00090501u, kI8Neg = 0x00F5F9FDu;
 
 // 4 v of one E8P codeword (slot jj of the 4-codeword idx / flag words, shift bit b)
-// as 8 bf16 (16 B, coordinates 0..7).
-__device__ __forceinline__ uint4 e8p_bf16(std::uint32_t idx, std::uint32_t fw, int jj, std::uint32_t b,
-                                          std::uint32_t tab) {
+// as 8 s8 (coordinates 0..7).
+__device__ __forceinline__ uint2 e8p_s8(std::uint32_t idx, std::uint32_t fw, int jj, std::uint32_t b,
+                                        std::uint32_t tab) {
   const std::uint32_t nib = lds32(tab + idx * 4u);
   const std::uint32_t rs = jj == 0 ? fw << 2 : jj == 1 ? fw << 1 : jj == 2 ? fw : fw >> 1;
-  const std::uint32_t sel = nib ^ (rs & 0x44444444u);       // high-byte selectors
-  const std::uint32_t sel_l = sel ^ (b * 0x44444444u);      // low-byte selectors (b flips the sigma slot)
-  const std::uint32_t h_lo = kHiLo + b, h_hi = kHiHi - b;   // the b table of high bytes
-  const std::uint32_t h03 = prmt(h_lo, h_hi, sel), h47 = prmt(h_lo, h_hi, sel >> 16);
-  const std::uint32_t l03 = prmt(kLoLo, kLoHi, sel_l), l47 = prmt(kLoLo, kLoHi, sel_l >> 16);
-  // interleave (low, high) byte pairs: element c = bytes 2c, 2c + 1
-  return make_uint4(prmt(l03, h03, 0x5140u), prmt(l03, h03, 0x7362u), prmt(l47, h47, 0x5140u),
-                    prmt(l47, h47, 0x7362u));
+  const std::uint32_t sel = nib ^ (rs & 0x44444444u);
+  const std::uint32_t bb = b * 0x00020202u;
+  return make_uint2(prmt(kI8Pos + bb, kI8Neg + bb, sel), prmt(kI8Pos + bb, kI8Neg + bb, sel >> 16));
 }
-// 4 v = 2 * doubled of an e8-1bit code.
-__device__ __forceinline__ uint4 e81_bf16(std::uint32_t code, std::uint32_t tab) {
+// 4 v = 2 * doubled of an e8-1bit code (bytewise doubling; |doubled| <= 63).
+__device__ __forceinline__ uint2 e81_s8(std::uint32_t code, std::uint32_t tab) {
   const std::uint32_t lo = lds32(tab + 1024u + code * 8u), hi = lds32(tab + 1024u + code * 8u + 4u);
-  auto v = [&](std::uint32_t w, int c) { return 2.f * float(int(std::int8_t(w >> (8 * c)))); };
-  return make_uint4(bf2(v(lo, 0), v(lo, 1)), bf2(v(lo, 2), v(lo, 3)), bf2(v(hi, 0), v(hi, 1)),
-                    bf2(v(hi, 2), v(hi, 3)));
+  return make_uint2((lo << 1) & 0xFEFEFEFEu, (hi << 1) & 0xFEFEFEFEu);
+}
+
+// One item's MMAs: limb h into D (columns d ..), limb l into D + kNT, both with the
+// item's A tile; commits free the A and B slots.  Issued by one elected lane of a
+// converged warp (one asm block: no per-MMA R2UR waterfall).
+__device__ __forceinline__ void mma_s8_item_e(std::uint32_t d, std::uint64_t a_desc, std::uint64_t b_desc,
+                                              std::uint32_t idesc, std::uint32_t acc, std::uint32_t bar0,
+                                              std::uint32_t bar1) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b64 b;\n\t.reg .b32 x;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+      "add.s64 b, %2, %7;\n\tadd.s32 x, %0, %8;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [x], %1, b, %3, p;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t"
+      "}\n" ::"r"(d),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc), "r"(bar0), "r"(bar1), "n"(kBLimb / 16), "n"(kNT)
+      : "memory");
 }
 
 __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
@@ -264,11 +272,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer: per item 2 M tiles x 2 K-blocks x 2 terms =====
+    // ===== MMA issuer: per item 2 limbs =====
     // The whole warp runs the loop (converged, uniform operands); one elected lane
     // issues each item's 8 MMAs + 2 commits in a single asm block.  (Issued from a
     // divergent `lane == 0` branch they cost ~100 cycles each: R2UR waterfalls.)
-    constexpr std::uint32_t idesc = idesc_bf16(128, kNT);
+    constexpr std::uint32_t idesc = idesc_i8(128, kNT);
     std::uint32_t g = 0, ul = 0;
     for (std::uint32_t st = s_begin; st < s_end; st = next_step(st), ++ul) {
       if (ul >= 1) mbar_wait(bar_de, (ul - 1) & 1);  // the previous unit's epilogue read the accumulators
@@ -284,8 +292,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
         k4_stamp(a, 0, g, 2);
         tc_fence_after();
         const std::uint32_t sa = sb + kOffA + sl * kABytes, sbb = sb + kOffB + sl * kBBytes;
-        mma_f16_item_e<kNT, kATile / 16, 4096 / 16, 8192 / 16, kBTerm / 16>(
-            tbase, sdesc(sa, 128, 256), sdesc(sbb, 128, 256), idesc, it != 0, bar_ae + 8 * sl, bar_be + 8 * sl);
+        mma_s8_item_e(tbase, sdesc(sa, 128, 256), sdesc(sbb, 128, 256), idesc, it != 0, bar_ae + 8 * sl,
+                      bar_be + 8 * sl);
         k4_stamp(a, 0, g, 3);
       }
       mma_commit_e(bar_df);
@@ -293,8 +301,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
   } else {
     // ===== decoders: warp = (M tile t, lane quadrant q), thread = row; then the epilogue =====
     const std::uint32_t q = std::uint32_t(warp & 3), row_in = q * 32 + std::uint32_t(lane);
-    const std::uint32_t t = (std::uint32_t(warp - 2) >> 2) & 1;  // M tile
-    const std::uint32_t team = std::uint32_t(warp - 2) >> 3;     // K chunks kc with kc % 2 == team
+    const std::uint32_t t = (std::uint32_t(warp - 2) >> 2) % kMT;  // M tile
+    const std::uint32_t team = std::uint32_t(warp - 2) / kDecTeam;  // K chunks kc with kc % kTeams == team
     std::uint32_t g = 0, cg = 0, ul = 0;
     const int kind0 = a.kind[0], kind1 = a.kind[1];  // (no runtime indexing of the parameter block)
     // One item = (K chunk kc, stage s): 4 codewords per thread into the item's A slot.
@@ -321,8 +329,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
         mbar_wait(bar_cf + 8 * it.cs, it.cph);
         if (it.g >= kSlots) mbar_wait(bar_ae + 8 * it.sl, ((it.g / kSlots) - 1) & 1);
       };
-      // decode one item's 4 codewords of this row into bf16 A bytes
-      auto decode = [&](const Item& it, uint4 (&v)[4]) {
+      // decode one item's 4 codewords of this row into s8 A bytes
+      auto decode = [&](const Item& it, uint2 (&v)[4]) {
         const std::uint32_t sc = sb + kOffC + it.cs * kCodeSlot, cq = it.kc % 8;
         const std::uint32_t wofs = (cq / 4) * 2048u + row_in * 16u + (cq % 4) * 4u;
         const std::uint32_t iw = lds32(sc + wofs);
@@ -330,34 +338,32 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
           const std::uint32_t fw = lds32(sc + 4096u + wofs), sw = lds32(sc + 8192u + row_in * 4u);
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj)
-            v[jj] = e8p_bf16((iw >> (8 * jj)) & 0xFFu, fw, jj, (sw >> (cq + 8 * jj)) & 1u, tab);
+            v[jj] = e8p_s8((iw >> (8 * jj)) & 0xFFu, fw, jj, (sw >> (cq + 8 * jj)) & 1u, tab);
         } else {
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) v[jj] = e81_bf16((iw >> (8 * jj)) & 0xFFu, tab);
+          for (int jj = 0; jj < 4; ++jj) v[jj] = e81_s8((iw >> (8 * jj)) & 0xFFu, tab);
         }
       };
-      // codeword jj = K columns 8 jj .. 8 jj + 7 of the chunk: K-block jj / 2, half jj % 2
-      auto store = [&](const Item& it, const uint4 (&v)[4]) {
-        const std::uint32_t sa = sb + kOffA + it.sl * kABytes + t * kATile;
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj)
-          sts128(sa + (jj >> 1) * 4096u + (row_in >> 3) * 256u + (jj & 1) * 128u + (row_in & 7) * 16u, v[jj]);
+      // codeword jj = K bytes 8 jj .. 8 jj + 7 of the chunk: K half jj / 2 (16-byte core-matrix rows)
+      auto store = [&](const Item& it, const uint2 (&v)[4]) {
+        const std::uint32_t sa = sb + kOffA + it.sl * kABytes + t * kATile + (row_in >> 3) * 256u + (row_in & 7) * 16u;
+        sts128(sa, make_uint4(v[0].x, v[0].y, v[1].x, v[1].y));
+        sts128(sa + 128u, make_uint4(v[2].x, v[2].y, v[3].x, v[3].y));
       };
       auto release = [&](const Item& it) {  // lane 0, after the warp's stores are fenced
         mbar_arrive(bar_af + 8 * it.sl);
-        if (it.kc % 8 >= 6) mbar_arrive(bar_ce + 8 * it.cs);  // this team's last chunk of the slab
+        if (it.kc % 8 >= 8 - kTeams) mbar_arrive(bar_ce + 8 * it.cs);  // this team's last chunk of the slab
       };
-      // One item at a time per warp, the two teams on alternate K chunks: a single
+      // One item at a time per warp, the teams on K chunks kc % kTeams: a single
       // item's chain (slab load -> LUT load -> PRMTs -> stores -> proxy fence) is
-      // latency-bound, so two teams keep two items in flight per (M tile, quadrant).
-      // (Pairing items within one warp starved the 3-slot A ring: 387 -> 410 us.)
-      for (std::uint32_t i = team * nst; i < uitems; i += (i % nst == nst - 1) ? 1 + nst : 1) {
+      // latency-bound, so the teams keep kTeams items in flight per lane quadrant.
+      for (std::uint32_t i = team * nst; i < uitems; i += (i % nst == nst - 1) ? 1 + (kTeams - 1) * nst : 1) {
         const Item it = item(i);
         k4_stamp(a, 2 + warp - 2, it.g, 0);
         wait_item(it);
         k4_stamp(a, 2 + warp - 2, it.g, 2);
         if (live) {
-          uint4 v[4];
+          uint2 v[4];
           decode(it, v);
           store(it, v);
           k4_stamp(a, 2 + warp - 2, it.g, 4);
@@ -369,18 +375,23 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
       }
       g += uitems;
       cg += ((kc1 - kc0 + 7) / 8) * nst * kMT;
-      // epilogue: z[b][r] = D_t[r][b] / 4 for this M tile's 128 rows x 256 vectors
+      // epilogue: z[b][r] = alpha_b (256 D_h[r][b] + D_l[r][b]) / 4 for the M tile's
+      // 128 rows x 256 vectors
       mbar_wait(bar_df, ul & 1);
       tc_fence_after();
       const std::uint32_t row = mt * 128 + row_in;
       for (std::uint32_t c0 = team * (kNT / kTeams); c0 < (team + 1) * (kNT / kTeams); c0 += 32) {  // team's columns
-        float d[32];
-        tmem_ld32(tbase + ((q * 32) << 16) + t * kNT + c0, d);
+        float dh[32], dl[32];
+        tmem_ld32(tbase + ((q * 32) << 16) + c0, dh);
+        tmem_ld32(tbase + ((q * 32) << 16) + kNT + c0, dl);
         if (live && row < a.m) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const std::uint32_t b = nt * kNT + c0 + j;
-            if (b < a.batch) a.z[(std::size_t(p) * a.batch + b) * a.m + row] = 0.25f * d[j];
+            if (b < a.batch)
+              a.z[(std::size_t(p) * a.batch + b) * a.m + row] =
+                  0.25f * __ldg(a.alpha + b) *
+                  fmaf(256.f, float(__float_as_int(dh[j])), float(__float_as_int(dl[j])));
           }
         }
       }
@@ -397,44 +408,59 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
   }
 }
 
-// B tiles from t [batch][n] fp32: per (N tile, K chunk, stage) the hi / lo bf16
-// terms of scale_s * t in the K-major core-matrix layout.  Thread = (vector v,
-// 8-column group kg); vectors beyond batch (last N tile) are zeros.
+// B tiles from t [batch][n] fp32.  CTA = one vector v of the N tiles (vectors
+// beyond batch: zeros, alpha 0): alpha_v = max_s scale_s * max|t_v| / kLMax, then
+// per (K chunk, stage) the balanced s8 limbs h, l of L = rint(scale_s t / alpha_v)
+// (L = 256 h + l) in the K-major core-matrix layout, 8 bytes per (limb, 8-column
+// group).  alpha goes to alpha_out[v] for the epilogue.
 __global__ void __launch_bounds__(256) pack_b_kernel(const float* __restrict__ t, std::uint32_t n,
-                                                     std::uint32_t batch, std::uint32_t NTL, int nst, float s0,
-                                                     float s1, std::uint8_t* __restrict__ out) {
-  const std::uint32_t KC = n / kKC, groups = n / 8;
-  const std::size_t total = std::size_t(NTL) * kNT * groups;
-  for (std::size_t x = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x; x < total;
-       x += std::size_t(gridDim.x) * blockDim.x) {
-    const std::uint32_t kg = std::uint32_t(x % groups), v = std::uint32_t(x / groups);
-    const std::uint32_t nt = v / kNT, vi = v % kNT, kc = kg / 4, j = (kg % 4) / 2, kh = kg % 2;
+                                                     std::uint32_t batch, int nst, float s0, float s1,
+                                                     std::uint8_t* __restrict__ out, float* __restrict__ alpha_out) {
+  __shared__ float red[8];
+  const std::uint32_t v = blockIdx.x, nt = v / kNT, vi = v % kNT, KC = n / kKC, groups = n / 8;
+  const bool live = v < batch;
+  const float* tv = t + std::size_t(v) * n;
+  float mx = 0.f;
+  if (live)
+    for (std::uint32_t i = threadIdx.x; i < n / 4; i += blockDim.x) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(tv) + i);
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(q.x), fabsf(q.y)), fmaxf(fabsf(q.z), fabsf(q.w))));
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = red[0];
+  for (int w = 1; w < int(blockDim.x >> 5); ++w) mx = fmaxf(mx, red[w]);
+  const float smax = nst > 1 ? fmaxf(s0, s1) : s0;
+  const float al = smax * mx / kLMax, inv = al > 0.f ? 1.f / al : 0.f;
+  if (threadIdx.x == 0) alpha_out[v] = al;
+  for (std::uint32_t kg = threadIdx.x; kg < groups; kg += blockDim.x) {
+    const std::uint32_t kc = kg / 4, j = kg % 4;
     float xv[8];
-    if (v < batch) {
-      const float4 lo4 = *reinterpret_cast<const float4*>(t + std::size_t(v) * n + 8 * kg);
-      const float4 hi4 = *reinterpret_cast<const float4*>(t + std::size_t(v) * n + 8 * kg + 4);
+    if (live) {
+      const float4 lo4 = __ldg(reinterpret_cast<const float4*>(tv + 8 * kg));
+      const float4 hi4 = __ldg(reinterpret_cast<const float4*>(tv + 8 * kg + 4));
       xv[0] = lo4.x, xv[1] = lo4.y, xv[2] = lo4.z, xv[3] = lo4.w, xv[4] = hi4.x, xv[5] = hi4.y, xv[6] = hi4.z,
       xv[7] = hi4.w;
     } else {
 #pragma unroll
       for (int c = 0; c < 8; ++c) xv[c] = 0.f;
     }
+    const std::size_t o = (vi >> 3) * 256 + (j >> 1) * 128 + (vi & 7) * 16 + (j & 1) * 8;
     for (int s = 0; s < nst; ++s) {
       const float sc = s ? s1 : s0;
-      std::uint32_t hi[4], lo[4];
+      std::uint32_t h[2] = {0, 0}, l[2] = {0, 0};
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float a0 = sc * xv[2 * c], a1 = sc * xv[2 * c + 1];
-        const __nv_bfloat162 h = __floats2bfloat162_rn(a0, a1);
-        const float2 hf = __bfloat1622float2(h);
-        const __nv_bfloat162 l = __floats2bfloat162_rn(a0 - hf.x, a1 - hf.y);
-        hi[c] = *reinterpret_cast<const std::uint32_t*>(&h);
-        lo[c] = *reinterpret_cast<const std::uint32_t*>(&l);
+      for (int c = 0; c < 8; ++c) {
+        const int L = __float2int_rn(sc * xv[c] * inv);  // |L| <= kLMax
+        const int lo = ((L + 128) & 255) - 128, hi = (L - lo) >> 8;
+        h[c >> 2] |= std::uint32_t(hi & 255) << (8 * (c & 3));
+        l[c >> 2] |= std::uint32_t(lo & 255) << (8 * (c & 3));
       }
       std::uint8_t* reg = out + ((std::size_t(nt) * KC + kc) * nst + s) * kBBytes;
-      const std::size_t o = std::size_t(j) * 8192 + (vi >> 3) * 256 + kh * 128 + (vi & 7) * 16;
-      *reinterpret_cast<uint4*>(reg + o) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      *reinterpret_cast<uint4*>(reg + kBTerm + o) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      *reinterpret_cast<uint2*>(reg + o) = make_uint2(h[0], h[1]);
+      *reinterpret_cast<uint2*>(reg + kBLimb + o) = make_uint2(l[0], l[1]);
     }
   }
 }
@@ -468,21 +494,18 @@ K4Sched prefill_sched(const q8p_layer& L, int batch) {
 
 std::uint32_t prefill_parts(const q8p_layer& L, int batch) { return prefill_sched(L, batch).slices; }
 
-std::size_t prefill_btile_bytes(const q8p_layer& L, int batch) {
+std::size_t prefill_btile_bytes(const q8p_layer& L, int batch) {  // B tiles, then alpha per vector
   const std::size_t ntl = (std::size_t(batch) + kNT - 1) / kNT;
-  return ntl * (L.n / kKC) * std::size_t(L.num_stages) * kBBytes;
+  return ntl * (L.n / kKC) * std::size_t(L.num_stages) * kBBytes + ntl * kNT * 4;
 }
 
 void launch_prefill(const q8p_layer& L, const float* t, std::uint8_t* btiles, float* z, int batch, cudaStream_t s) {
   const std::uint32_t NTL = std::uint32_t((batch + kNT - 1) / kNT);
-  {
-    const std::size_t total = std::size_t(NTL) * kNT * (L.n / 8);
-    const unsigned grid = unsigned(std::min<std::size_t>((total + 255) / 256, 148 * 16));
-    pack_b_kernel<<<grid, 256, 0, s>>>(t, L.n, std::uint32_t(batch), NTL, L.num_stages, L.scale[0], L.scale[1],
-                                       btiles);
-    cuda_check(cudaGetLastError(), "prefill pack launch");
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-  }
+  float* const alpha = reinterpret_cast<float*>(btiles + std::size_t(NTL) * (L.n / kKC) * L.num_stages * kBBytes);
+  pack_b_kernel<<<NTL * kNT, 256, 0, s>>>(t, L.n, std::uint32_t(batch), L.num_stages, L.scale[0], L.scale[1], btiles,
+                                          alpha);
+  cuda_check(cudaGetLastError(), "prefill pack launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   PrefillArgs a{};
   a.nst = L.num_stages;
   for (int st = 0; st < L.num_stages; ++st) {
@@ -502,6 +525,7 @@ void launch_prefill(const q8p_layer& L, const float* t, std::uint8_t* btiles, fl
   a.batch = std::uint32_t(batch);
   a.nib = L.dec_tables;
   a.e81 = reinterpret_cast<const uint2*>(L.dec_tables + 256);
+  a.alpha = alpha;
 #ifdef Q8P_K4_TRACE
   static const char* trace_env = std::getenv("Q8P_TRACE");
   if (trace_env) {

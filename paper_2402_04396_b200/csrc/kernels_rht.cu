@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kP1Threads) rht_pass1(RhtArgs a) {
     return;
   }
   __shared__ float red1[32];
-  __shared__ int s_pieces[4];
+  __shared__ int s_pieces[kP1Tiles];
   float* const Bs = sm1;
   if (a.in_sched) p1_tile_pieces(a, a.ch0 + blockIdx.x, a.P2 * Q, int(blockIdx.y) * (a.vpb > 1 ? a.vpb : 1), s_pieces);
   if constexpr (kWarp) {  // shared by the CTA's warp teams: once, up front (else the body loads it)
@@ -390,8 +390,8 @@ void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, flo
   a.in = zin;
   a.in_parts = in_parts;
   if (sched) {
-    if (a.P2 * a.q > 512 || sched->mrows < 256 || sched->nt % 8 != 0)
-      throw UnsupportedError("rht: K4 pieces need chunks <= 2 M pairs and 8 | the N tile");
+    if (a.P2 * a.q > 512 || sched->mrows < 128 || sched->nt % 8 != 0)
+      throw UnsupportedError("rht: K4 pieces need chunks <= 512 rows, M tiles >= 128 rows and 8 | the N tile");
     a.sched = *sched, a.in_sched = 1;
   }
   a.mid = u_scratch;
@@ -517,8 +517,8 @@ void launch_rht_out_local_f32(const DevSide& side, const float* zparts, int part
   a.in_parts = parts;
   a.in_local = 1;
   if (sched) {
-    if (a.P2 * a.q > 512 || sched->mrows < 256 || sched->nt % 8 != 0)
-      throw UnsupportedError("rht: K4 pieces need chunks <= 2 M pairs and 8 | the N tile");
+    if (a.P2 * a.q > 512 || sched->mrows < 128 || sched->nt % 8 != 0)
+      throw UnsupportedError("rht: K4 pieces need chunks <= 512 rows, M tiles >= 128 rows and 8 | the N tile");
     a.sched = *sched, a.in_sched = 1;
   }
   a.mid = z_send;

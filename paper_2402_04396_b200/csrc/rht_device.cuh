@@ -292,12 +292,13 @@ __device__ __forceinline__ float2 combine2(const RhtArgs& a, int b, std::uint32_
 }
 
 
-// K4 stream-K piece counts for pass 1's CTA (in_sched): the (<= 4) M-pair tiles of
+// K4 stream-K piece counts for pass 1's CTA (in_sched): the (<= kP1Tiles) M tiles of
 // chunk `ch` for the N tile of vector b0 (a CTA's vectors share it: vpb divides the
-// N tile).  Threads 0..3 write s_pieces[0..3]; the caller syncs.
+// N tile).  Threads 0..kP1Tiles-1 write s_pieces[]; the caller syncs.
+constexpr int kP1Tiles = 8;  // a <= 512-row chunk touches <= 5 tiles of >= 128 rows
 __device__ __forceinline__ void p1_tile_pieces(const RhtArgs& a, std::uint32_t ch, std::uint32_t chunk, int b0,
                                                int* s_pieces) {
-  if (threadIdx.x < 4) {
+  if (threadIdx.x < kP1Tiles) {
     const std::uint32_t e0 = ch * chunk, r0 = a.in_local ? e0 - a.row0 : e0;
     const std::uint32_t mp = r0 / a.sched.mrows + threadIdx.x, mp_last = (r0 + chunk - 1) / a.sched.mrows;
     s_pieces[threadIdx.x] =
@@ -331,7 +332,7 @@ __device__ void p1_load_base(const RhtArgs& a, float* Bs) {
 // Pass 1 on chunk `ch` of vector b.  xs: the team's [2][chunk] floats; Bs: the
 // base (p1_load_base); red: >= 32 floats of team-shared smem.
 // ll_tag: the push all-gather's call tag (a.push.ctl set), else unused.
-// pieces (in_sched): K4 stream-K piece counts of the (<= 4) M-pair tiles the chunk's rows
+// pieces (in_sched): K4 stream-K piece counts of the (<= kP1Tiles) M tiles the chunk's rows
 // touch, for this vector's N tile, from M pair p1_mp_first on (p1_tile_pieces).
 template <int Q>
 __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* xs, const float* Bs, float* red,

@@ -13,7 +13,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 TC = 1e-5    # tensor-core path: 25-bit integer activations (see test_gpu_parity.py)
-PREFILL = 1e-4  # K4 prefill (batch >= 64): bf16 hi/lo activations (16 bits), fp32 tensor-core accumulation
+PREFILL = 1e-4  # K4 prefill (batch >= 64): 16-bit fixed-point activations per vector (two s8 limbs), exact s32 accumulation
 TOL = 1e-3   # portable fp32 path / north-star bar
 
 STAGES = {2: [("e8p-2bit", 1.11)], 3: [("e8p-2bit", 1.02), ("e8-1bit", 0.49)],
