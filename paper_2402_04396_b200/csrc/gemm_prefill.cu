@@ -59,8 +59,8 @@ constexpr std::uint32_t kBBytes = 2u * kBLimb;        // h + l
 // A / B pipeline depth.  A team's consecutive items are up to (kTeams - 1) * nst + 1
 // apart (nst <= 2: 7); its parity wait on an A slot is only unambiguous when that
 // gap is <= kSlots (the slot's previous phase is then known complete).
-constexpr std::uint32_t kSlots = 7;
-constexpr std::uint32_t kCodeSlots = 8;               // code slab ring (stages x k slabs)
+constexpr std::uint32_t kSlots = 8;  // (a power of two: slot / phase by shifts)
+constexpr std::uint32_t kCodeSlots = 6;               // code slab ring (stages x k slabs: 2 x 2 in use + prefetch)
 constexpr std::uint32_t kCodeSlot = 4 * 2048 + 512;   // E8P slab bytes (e8-1bit slabs are smaller)
 constexpr int kTeams = 4;                             // decoder teams: K chunk kc goes to team kc % 4
 constexpr int kDecTeam = 4 * kMT;                     // decoder warps per team: M tiles x 4 lane quadrants
@@ -316,8 +316,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
       const std::uint32_t uitems = (kc1 - kc0) * nst;
       auto item = [&](std::uint32_t i) {
         Item it;
-        it.kc = kc0 + i / nst;
-        it.s = i % nst;
+        it.kc = kc0 + (nst == 1 ? i : i >> 1);  // nst in {1, 2}
+        it.s = nst == 1 ? 0u : i & 1u;
         const std::uint32_t cidx = cg + ((it.kc - kc0) / 8) * nst * kMT + it.s * kMT + t;
         it.cs = cidx % kCodeSlots;
         it.cph = (cidx / kCodeSlots) & 1;
