@@ -390,7 +390,7 @@ void launch_rht_out(const DevSide& side, const float* zin, float* u_scratch, flo
   a.in = zin;
   a.in_parts = in_parts;
   if (sched) {
-    if (a.P2 * a.q > 512 || sched->mrows < 128 || sched->nt % 8 != 0)
+    if (a.P2 * a.q > 512 || sched->mrows < 128 || (sched->mrows & (sched->mrows - 1)) || sched->nt % 8 != 0)
       throw UnsupportedError("rht: K4 pieces need chunks <= 512 rows, M tiles >= 128 rows and 8 | the N tile");
     a.sched = *sched, a.in_sched = 1;
   }
@@ -517,7 +517,7 @@ void launch_rht_out_local_f32(const DevSide& side, const float* zparts, int part
   a.in_parts = parts;
   a.in_local = 1;
   if (sched) {
-    if (a.P2 * a.q > 512 || sched->mrows < 128 || sched->nt % 8 != 0)
+    if (a.P2 * a.q > 512 || sched->mrows < 128 || (sched->mrows & (sched->mrows - 1)) || sched->nt % 8 != 0)
       throw UnsupportedError("rht: K4 pieces need chunks <= 512 rows, M tiles >= 128 rows and 8 | the N tile");
     a.sched = *sched, a.in_sched = 1;
   }

@@ -358,6 +358,7 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* xs
     }
   } else {
     const std::uint32_t mp_first = a.in_sched ? (a.in_local ? e0 - a.row0 : e0) / a.sched.mrows : 0;
+    const int msh = a.in_sched ? __ffs(int(a.sched.mrows)) - 1 : 0;  // K4 M tiles are 128 or 256 rows
     for (std::uint32_t v = tm.tid; v < chunk / 4; v += tm.n) {
       const std::uint32_t i = e0 + 4 * v;
       // element (part pp, vector b, row i) of the input
@@ -366,7 +367,7 @@ __device__ void rht_p1_body(const RhtArgs& a, std::uint32_t ch, int b, float* xs
           a.in + (a.in_local ? std::size_t(b) * rows + ri : rank_major(b, i, a.in_rows, a.batch, a.n))));
       // K-split partials (prefill), summed in piece order: all in_parts slices, or the
       // pieces of this (vector, row) tile under K4's stream-K schedule
-      const int parts = a.in_sched ? pieces[ri / a.sched.mrows - mp_first] : a.in_parts;
+      const int parts = a.in_sched ? pieces[(ri >> msh) - mp_first] : a.in_parts;
       for (int pp = 1; pp < parts; ++pp) {
         const float4 w4 =
             __ldcg(reinterpret_cast<const float4*>(a.in + (std::size_t(pp) * a.batch + b) * rows + ri));
