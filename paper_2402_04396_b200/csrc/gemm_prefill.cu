@@ -59,13 +59,17 @@ constexpr std::uint32_t kBBytes = 2u * kBLimb;        // h + l
 // A / B pipeline depth.  A team's consecutive items are up to (kTeams - 1) * nst + 1
 // apart (nst <= 2: 7); its parity wait on an A slot is only unambiguous when that
 // gap is <= kSlots (the slot's previous phase is then known complete).
-constexpr std::uint32_t kSlots = 8;  // (a power of two: slot / phase by shifts)
-constexpr std::uint32_t kCodeSlots = 6;               // code slab ring (stages x k slabs: 2 x 2 in use + prefetch)
+constexpr std::uint32_t kSlots = 9;
+// Code slab ring: a decoder's A-slot wait keeps it within kSlots items of the MMA;
+// with kSlots <= 8 nst + 1 (a k slab holds 8 nst items) a decoder entering k slab
+// k + 2 implies all of k slab k is done, so at most 2 k slabs x nst stages are in flight.
+constexpr std::uint32_t kCodeSlots = 4;
 constexpr std::uint32_t kCodeSlot = 4 * 2048 + 512;   // E8P slab bytes (e8-1bit slabs are smaller)
 constexpr int kTeams = 4;                             // decoder teams: K chunk kc goes to team kc % 4
 constexpr int kDecTeam = 4 * kMT;                     // decoder warps per team: M tiles x 4 lane quadrants
 constexpr float kLMax = 32000.f;                      // |L| bound: balanced limbs h, l in [-128, 127]
 static_assert((kTeams - 1) * 2 + 1 <= int(kSlots), "A/B ring too shallow for the decoder teams");
+static_assert(kSlots <= 8 * 1 + 1 && kCodeSlots >= 2 * 2, "code ring sized for decoders within one k slab of the MMA");
 constexpr int kDec = kTeams * kDecTeam;
 constexpr int kThreads = (2 + kDec) * 32;
 constexpr std::uint32_t kCtl = 1024, kTab = 4096;     // barriers; decode tables
