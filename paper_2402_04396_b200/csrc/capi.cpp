@@ -890,12 +890,13 @@ void forward_set_host_enqueue(const q8p_layer* const* layers, int count, const f
   const int dev = layers[0]->device;
   std::scoped_lock lock(g_set_aux_mu);
   SetAux& aux = set_aux(dev, 0, 2 * count + 3);
-  // Outputs on their own stream only when the copies are large: for a decode step
-  // (70B set, batch 1: 180 KB each way) the second stream's extra edges cost more
-  // than the overlap buys (e2e 102.4 vs 100.4 us per step, A/B on one box).
+  // Outputs on their own stream only when the copies are large.  70B set, e2e A/Bs
+  // on one box: batch 1 (0.36 MB of I/O) 102.4 vs 100.4 us per step and batch 16
+  // (5.8 MB) 42.6 k vs 45-60 k tokens/s favour one stream, batch 64 (23 MB) ties,
+  // batch 128 (46 MB) 164 k vs 134 k and batch 512 200 k vs 149 k favour two.
   std::size_t io_bytes = 0;
   for (int i = 0; i < count; ++i) io_bytes += std::size_t(batch) * (layers[i]->n + layers[i]->m) * 4;
-  const bool duplex = io_bytes > (std::size_t(4) << 20);
+  const bool duplex = io_bytes > (std::size_t(32) << 20);
   cudaEvent_t fork = aux.ev[0], join = aux.ev[1], join2 = aux.ev[2 * count + 2];
   cuda_check(cudaEventRecord(fork, s), "fork");
   cuda_check(cudaStreamWaitEvent(aux.side, fork, 0), "fork wait");
