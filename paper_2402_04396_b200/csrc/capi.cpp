@@ -494,7 +494,7 @@ void forward_sharded_impl(const q8p_layer* L, const float* x, float* y, int batc
   if (local_p1 && use_prefill_rows(L, batch)) {
     // prefill: K1 (replicated) -> K4 on this rank's rows -> K3 pass 1 on them (summing
     // the K-split partials) -> one all-gather -> K3 pass 2
-    launch_rht_in(L->side_v, x, w.pt, w.u, nullptr, nullptr, nullptr, 0, batch, s);
+    launch_rht_in(L->side_v, x, w.pt, w.u, prefill_amax(*L, batch, w.pbt), nullptr, nullptr, 0, batch, s);
     launch_prefill(*L, w.pt, w.pbt, w.pz, batch, s);
     const K4Sched ks = prefill_sched(*L, batch);
     launch_rht_out_local_f32(L->side_u, w.pz, int(ks.slices), L->row_begin, ml, w.u, nullptr, batch, s, &ks);
@@ -612,7 +612,7 @@ void forward_push_impl(const q8p_layer* L, q8p_peers* p, const float* x, float* 
   workspace_parts(L, batch, &w, ws);
   const PushArgs pa = p->args();
   if (use_prefill_rows(L, batch)) {  // prefill: K1 -> K4 on this rank's rows -> pushing K3 pass 1 -> pass 2
-    launch_rht_in(L->side_v, x, w.pt, w.u, nullptr, nullptr, nullptr, 0, batch, s);
+    launch_rht_in(L->side_v, x, w.pt, w.u, prefill_amax(*L, batch, w.pbt), nullptr, nullptr, 0, batch, s);
     launch_prefill(*L, w.pt, w.pbt, w.pz, batch, s);
     const K4Sched ks = prefill_sched(*L, batch);
     launch_rht_out_local_f32(L->side_u, w.pz, int(ks.slices), L->row_begin, L->m_local(), nullptr, &pa, batch, s,
@@ -642,7 +642,7 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
   Workspace w;
   workspace_parts(L, batch, &w, ws);
   if (use_prefill(L, batch)) {  // K1 (fp32 t) -> K4 (pack + decode-GEMM) -> K3
-    launch_rht_in(L->side_v, x, w.pt, w.u, nullptr, nullptr, nullptr, 0, batch, s);
+    launch_rht_in(L->side_v, x, w.pt, w.u, prefill_amax(*L, batch, w.pbt), nullptr, nullptr, 0, batch, s);
     if (opts) record_event(opts->gemv_start_event, s);  // the events bracket pack + K4
     launch_prefill(*L, w.pt, w.pbt, w.pz, batch, s);
     if (opts) record_event(opts->gemv_end_event, s);
@@ -1808,7 +1808,7 @@ q8p_status q8p_forward_sharded_push_sim(const q8p_layer* const* shards, q8p_peer
         const q8p_layer* L = shards[r];
         workspace_parts(L, batch, &w, ws);
         const PushArgs pa = peers[r]->args();
-        launch_rht_in(L->side_v, x, w.pt, w.u, nullptr, nullptr, nullptr, 0, batch, s);
+        launch_rht_in(L->side_v, x, w.pt, w.u, prefill_amax(*L, batch, w.pbt), nullptr, nullptr, 0, batch, s);
         launch_prefill(*L, w.pt, w.pbt, w.pz, batch, s);
         const K4Sched ks = prefill_sched(*L, batch);
         launch_rht_out_local_f32(L->side_u, w.pz, int(ks.slices), L->row_begin, L->m_local(), nullptr, &pa, batch,

@@ -170,6 +170,8 @@ std::uint32_t tc_bimg_bytes(std::uint32_t n, int batch);  // B images for all k 
 constexpr int kPrefillMinBatch = 64;
 bool prefill_supported(const q8p_layer& L, int batch);
 std::size_t prefill_btile_bytes(const q8p_layer& L, int batch);
+// Per-vector max |t| slot in the B-tile region: K1 (prefill) writes it, pack_b turns it into alpha.
+float* prefill_amax(const q8p_layer& L, int batch, std::uint8_t* btiles);
 // K4's stream-K schedule.  Tiles (N tile of `nt` vectors x M pair of `mrows` rows,
 // tile = nt_index * MP + mp) each have KS8 k-slab steps; the `grid` CTAs own equal
 // contiguous ranges of the tiles x KS8 steps in that order, so a tile is split

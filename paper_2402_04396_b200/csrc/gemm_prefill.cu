@@ -413,32 +413,22 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PrefillArgs a) {
 }
 
 // B tiles from t [batch][n] fp32.  CTA = one vector v of the N tiles (vectors
-// beyond batch: zeros, alpha 0): alpha_v = max_s scale_s * max|t_v| / kLMax, then
-// per (K chunk, stage) the balanced s8 limbs h, l of L = rint(scale_s t / alpha_v)
-// (L = 256 h + l) in the K-major core-matrix layout, 8 bytes per (limb, 8-column
-// group).  alpha goes to alpha_out[v] for the epilogue.
+// beyond batch: zeros, alpha 0): alpha_v = max_s scale_s * max|t_v| / kLMax (max|t_v|
+// from K1's pass 2, in amax_alpha[v]), then per (K chunk, stage) the balanced s8
+// limbs h, l of L = rint(scale_s t / alpha_v) (L = 256 h + l) in the K-major
+// core-matrix layout, 8 bytes per (limb, 8-column group).  alpha replaces the max
+// in amax_alpha[v] for the epilogue.
 __global__ void __launch_bounds__(256) pack_b_kernel(const float* __restrict__ t, std::uint32_t n,
                                                      std::uint32_t batch, int nst, float s0, float s1,
-                                                     std::uint8_t* __restrict__ out, float* __restrict__ alpha_out) {
-  __shared__ float red[8];
+                                                     std::uint8_t* __restrict__ out, float* __restrict__ amax_alpha) {
   const std::uint32_t v = blockIdx.x, nt = v / kNT, vi = v % kNT, KC = n / kKC, groups = n / 8;
   const bool live = v < batch;
   const float* tv = t + std::size_t(v) * n;
-  float mx = 0.f;
-  if (live)
-    for (std::uint32_t i = threadIdx.x; i < n / 4; i += blockDim.x) {
-      const float4 q = __ldg(reinterpret_cast<const float4*>(tv) + i);
-      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(q.x), fabsf(q.y)), fmaxf(fabsf(q.z), fabsf(q.w))));
-    }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-  __syncthreads();
-  mx = red[0];
-  for (int w = 1; w < int(blockDim.x >> 5); ++w) mx = fmaxf(mx, red[w]);
+  const float mx = live ? amax_alpha[v] : 0.f;
   const float smax = nst > 1 ? fmaxf(s0, s1) : s0;
   const float al = smax * mx / kLMax, inv = al > 0.f ? 1.f / al : 0.f;
-  if (threadIdx.x == 0) alpha_out[v] = al;
+  __syncthreads();  // every thread has read the max before thread 0 overwrites it
+  if (threadIdx.x == 0) amax_alpha[v] = al;
   for (std::uint32_t kg = threadIdx.x; kg < groups; kg += blockDim.x) {
     const std::uint32_t kc = kg / 4, j = kg % 4;
     float xv[8];
@@ -498,6 +488,11 @@ K4Sched prefill_sched(const q8p_layer& L, int batch) {
 
 std::uint32_t prefill_parts(const q8p_layer& L, int batch) { return prefill_sched(L, batch).slices; }
 
+float* prefill_amax(const q8p_layer& L, int batch, std::uint8_t* btiles) {  // after the B tiles
+  const std::size_t ntl = (std::size_t(batch) + kNT - 1) / kNT;
+  return reinterpret_cast<float*>(btiles + ntl * (L.n / kKC) * std::size_t(L.num_stages) * kBBytes);
+}
+
 std::size_t prefill_btile_bytes(const q8p_layer& L, int batch) {  // B tiles, then alpha per vector
   const std::size_t ntl = (std::size_t(batch) + kNT - 1) / kNT;
   return ntl * (L.n / kKC) * std::size_t(L.num_stages) * kBBytes + ntl * kNT * 4;
@@ -505,7 +500,7 @@ std::size_t prefill_btile_bytes(const q8p_layer& L, int batch) {  // B tiles, th
 
 void launch_prefill(const q8p_layer& L, const float* t, std::uint8_t* btiles, float* z, int batch, cudaStream_t s) {
   const std::uint32_t NTL = std::uint32_t((batch + kNT - 1) / kNT);
-  float* const alpha = reinterpret_cast<float*>(btiles + std::size_t(NTL) * (L.n / kKC) * L.num_stages * kBBytes);
+  float* const alpha = prefill_amax(L, batch, btiles);  // holds K1's max |t| per vector; pack_b makes it alpha
   pack_b_kernel<<<NTL * kNT, 256, 0, s>>>(t, L.n, std::uint32_t(batch), L.num_stages, L.scale[0], L.scale[1], btiles,
                                           alpha);
   cuda_check(cudaGetLastError(), "prefill pack launch");
