@@ -629,6 +629,16 @@ void forward_push_impl(const q8p_layer* L, q8p_peers* p, const float* x, float* 
   }
 }
 
+// Prefill chunk: the whole batch, or the most 256-vector N tiles whose B tiles fit
+// kPrefillBTileL2 (the chunks' K1 -> K4 -> K3 chains run back to back).
+constexpr std::size_t kPrefillBTileL2 = std::size_t(64) << 20;
+int prefill_chunk(const q8p_layer& L, int batch) {
+  const std::size_t per_tile = std::size_t(L.n) * L.num_stages * 512;  // B bytes per 256-vector N tile
+  const std::size_t tiles = std::max<std::size_t>(1, kPrefillBTileL2 / per_tile);
+  const std::size_t chunk = tiles * 256;
+  return chunk >= std::size_t(batch) ? batch : int(chunk);
+}
+
 void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void* ws, std::size_t ws_bytes,
                   cudaStream_t s, const q8p_forward_opts* opts = nullptr) {
   if (!L) throw ValidationError("null layer");
@@ -642,6 +652,18 @@ void forward_impl(const q8p_layer* L, const float* x, float* y, int batch, void*
   Workspace w;
   workspace_parts(L, batch, &w, ws);
   if (use_prefill(L, batch)) {  // K1 (fp32 t) -> K4 (pack + decode-GEMM) -> K3
+    // Large batches on long-K layers run in chunks whose B tiles (ceil(B / 256) x
+    // n x stages x 512 bytes) stay L2-resident: 8192x28672 at batch 2048 would
+    // stream 117 MB of B tiles through the 126 MB L2 next to the codes.
+    const int chunk = prefill_chunk(*L, batch);
+    if (chunk < batch) {
+      if (opts) record_event(opts->gemv_start_event, s);  // (brackets the chunks' whole chains)
+      for (int b0 = 0; b0 < batch; b0 += chunk)
+        forward_impl(L, x + std::size_t(b0) * L->n, y + std::size_t(b0) * L->m, std::min(chunk, batch - b0), ws,
+                     ws_bytes, s);
+      if (opts) record_event(opts->gemv_end_event, s);
+      return;
+    }
     launch_rht_in(L->side_v, x, w.pt, w.u, prefill_amax(*L, batch, w.pbt), nullptr, nullptr, 0, batch, s);
     if (opts) record_event(opts->gemv_start_event, s);  // the events bracket pack + K4
     launch_prefill(*L, w.pt, w.pbt, w.pz, batch, s);
